@@ -1,0 +1,129 @@
+/*
+ * deepinverse.h -- C ABI of the B200-native DeepInverse batched signal-recovery library.
+ *
+ * The library computes, for every image b of a batch, the DeepInverse map
+ *     x_hat_b = M(y_b, Omega)                                   (§4)
+ * from measurements y_b = Phi x_b in R^M (§1) with Phi fixed:
+ *   1. lifting layer   x_tilde = Phi^T y, viewed as n1 x n2 row-major
+ *   2. conv layer 1    64 filters 11x11x1  + bias + ReLU, crop S        (Eq. (1))
+ *   3. conv layer 2    32 filters 11x11x64 + bias + ReLU, crop S
+ *   4. conv layer 3     1 filter  11x11x32 + bias (+ ReLU iff DI_FLAG_FINAL_RELU)
+ * Each layer is the full (n+10)x(n+10) convolution of Eq. (1) cropped back to n1 x n2 by S, which
+ * equals a 'same' zero-padded cross-correlation with the spatially flipped kernel.
+ *
+ * Every step runs in hand-written sm_100a CUDA kernels.  There is no CPU path: a context can only be
+ * created on a compute-capability-10.0 device, otherwise DI_ERR_DEVICE.
+ *
+ * Threading: calls on different contexts are independent.  One context serves one in-flight
+ * di_recover at a time (it owns a single workspace).  Error details are thread-local.
+ */
+#ifndef DEEPINVERSE_H_
+#define DEEPINVERSE_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct di_ctx_s* di_ctx;
+
+typedef enum {
+  DI_OK = 0,
+  DI_ERR_ARG = 1,    /* null pointer, batch out of [1, max_batch], unknown enum / flag        */
+  DI_ERR_DIM = 2,    /* ldy < m, bad leading dimension or alignment                           */
+  DI_ERR_DOMAIN = 3, /* m < 1, m > N = n1*n2, n1 or n2 < 1                     */
+  DI_ERR_DEVICE = 4, /* no CUDA device, or device is not sm_100 (compute capability 10.0)     */
+  DI_ERR_OOM = 5,    /* device or pinned-host allocation failed                               */
+  DI_ERR_CUDA = 6    /* a CUDA runtime / driver call or kernel launch failed                  */
+} di_status;
+
+typedef enum {
+  DI_PREC_FP32 = 0, /* fp32 storage, fp32 FFMA arithmetic (SIMT): parity <= 1e-5 rel-L2           */
+  DI_PREC_TF32 = 1, /* fp32 storage, TF32 tensor-core products, fp32 accumulation                  */
+  DI_PREC_BF16 = 2  /* bf16 storage of Phi, y, Omega and x_tilde/h1/h2; fp32 accumulation; tcgen05 */
+} di_precision;
+
+typedef enum { DI_DTYPE_F32 = 0, DI_DTYPE_BF16 = 1 } di_dtype;
+
+enum {
+  DI_FLAG_XCORR = 1u << 0,        /* taps given in cross-correlation (torch) convention; default: the true
+                                     convolution of Eq. (1) (reading Q2)           */
+  DI_FLAG_FULLMAP_BIAS = 1u << 1, /* b_l given as [C_out][n1+10][n2+10]; default: [C_out] */
+  DI_FLAG_FINAL_RELU = 1u << 2    /* ReLU after layer 3 (PAPER.md:118 read literally); default off       */
+};
+
+/* Arguments of di_create.  All pointers are HOST pointers; di_create deep-copies them and the caller may
+ * free them on return.  Weight layout [C_out][C_in][11][11] row-major fp32; biases fp32,
+ * layout per DI_FLAG_FULLMAP_BIAS; a NULL bias pointer means zero biases.  In DI_PREC_BF16 mode Phi and
+ * the weights are rounded to bf16 (round-to-nearest-even); biases stay fp32. */
+typedef struct {
+  int m;                 /* measurements M, 1 <= m <= n1*n2                                   */
+  int n1, n2;            /* image rows / columns, N = n1*n2                                   */
+  const void* phi;       /* Phi [m][n1*n2] row-major, dtype phi_dtype           */
+  di_dtype phi_dtype;
+  const float* w1;       /* [64][1][11][11]  */
+  const float* b1;
+  const float* w2;       /* [32][64][11][11] */
+  const float* b2;
+  const float* w3;       /* [1][32][11][11]  */
+  const float* b3;
+  di_precision precision;
+  unsigned flags;        /* DI_FLAG_*                                                         */
+  int device;            /* CUDA device ordinal                                               */
+  int max_batch;         /* largest batch of a single di_recover call; sizes the workspace    */
+} di_create_args;
+
+/* Create a context on args->device.  On failure *out is set to NULL and a status is returned. */
+di_status di_create(const di_create_args* args, di_ctx* out);
+
+/* Recover a batch, asynchronously on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   y:    DEVICE pointer, [batch][ldy] row-major; element type fp32 for FP32/TF32, bf16 for BF16;
+ *         only the first m entries of each row are read.  ldy >= m.
+ *   xhat: DEVICE pointer, [batch][n1][n2] fp32, written.
+ * Both stay owned by the caller and must remain valid until the stream work completes.
+ * Argument errors are reported synchronously before any work is enqueued; launch failures as
+ * DI_ERR_CUDA.  No host synchronisation happens inside. */
+di_status di_recover(di_ctx ctx, const void* y, long long ldy, int batch, float* xhat, void* stream);
+
+/* End-to-end variant with HOST buffers: copies y (host, pinned or pageable) to the device, recovers, copies
+ * x_hat back to `xhat_host`, all enqueued on `stream`; returns after the stream has completed. */
+di_status di_recover_host(di_ctx ctx, const void* y_host, long long ldy, int batch, float* xhat_host,
+                          void* stream);
+
+/* Destroy a context (NULL -> DI_OK).  Synchronises the device before freeing. */
+di_status di_destroy(di_ctx ctx);
+
+const char* di_status_string(di_status s);
+const char* di_last_error(void); /* thread-local detail of the last failing call on this thread */
+
+/* Introspection used by tests and the benchmark. */
+typedef struct {
+  int m, n1, n2, max_batch;
+  di_precision precision;
+  unsigned flags;
+  int launches_per_recover;      /* kernels enqueued by one di_recover                               */
+  long long workspace_bytes;     /* device bytes owned by the context                                */
+  const char* stage_kernels[4];  /* kernel names of stages 0..3                                      */
+} di_info;
+di_status di_get_info(di_ctx ctx, di_info* info);
+
+/* Per-stage device timing: when enabled, di_recover records CUDA events around every stage on its own
+ * stream; di_stage_times accumulates elapsed milliseconds of stages 0..3 over the calls since the last
+ * reset (it synchronises on the last recorded event).  Off by default (no events recorded). */
+di_status di_set_profiling(di_ctx ctx, int enable);
+di_status di_stage_times(di_ctx ctx, float ms[4], int* calls, int reset);
+
+/* Test hook: run one stage on caller DEVICE buffers in the documented layouts (storage type of the
+ * precision, i.e. bf16 for BF16 and fp32 otherwise, except stage 3 output which is fp32):
+ *   stage 0: y [batch][m]             -> x_tilde [batch][n1][n2]
+ *   stage 1: x_tilde [batch][n1][n2]  -> h1 [batch][n1][n2][64]  (NHWC)
+ *   stage 2: h1                       -> h2 [batch][n1][n2][32]  (NHWC)
+ *   stage 3: h2                       -> x_hat [batch][n1][n2] fp32 */
+di_status di_debug_stage(di_ctx ctx, int stage, const void* in, void* out, int batch, void* stream);
+
+/* Test hook: copy the context's device copy of Phi (storage type, [m][N] row-major) to a host buffer. */
+di_status di_debug_get_phi(di_ctx ctx, void* host_out, long long bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEEPINVERSE_H_ */

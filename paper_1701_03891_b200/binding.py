@@ -1,0 +1,232 @@
+"""Thin ctypes binding of include/deepinverse.h (argument marshalling only).
+
+Every step of the recovery runs inside libdeepinverse.so (hand-written sm_100a kernels).  There is no
+Python or CPU compute path: if the library is missing this module raises ImportError-like errors
+instead of falling back.  PyTorch is used only for device memory and streams (tensors' data_ptr()
+and torch.cuda streams are passed through as raw pointers).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdeepinverse.so")
+
+DI_OK, DI_ERR_ARG, DI_ERR_DIM, DI_ERR_DOMAIN, DI_ERR_DEVICE, DI_ERR_OOM, DI_ERR_CUDA = range(7)
+DI_PREC_FP32, DI_PREC_TF32, DI_PREC_BF16 = 0, 1, 2
+DI_DTYPE_F32, DI_DTYPE_BF16 = 0, 1
+DI_FLAG_XCORR, DI_FLAG_FULLMAP_BIAS, DI_FLAG_FINAL_RELU = 1, 2, 4
+PRECISIONS = {"f32": DI_PREC_FP32, "tf32": DI_PREC_TF32, "bf16": DI_PREC_BF16}
+
+# every symbol include/deepinverse.h declares (checked by tests/test_abi.py)
+EXPORTS = ["di_create", "di_recover", "di_recover_host", "di_destroy", "di_status_string", "di_last_error",
+           "di_get_info", "di_set_profiling", "di_stage_times", "di_debug_stage", "di_debug_get_phi"]
+
+
+class DiError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: status {status} ({_status_name(status)}): {detail}")
+        self.status = status
+
+
+def _status_name(s: int) -> str:
+    names = ["DI_OK", "DI_ERR_ARG", "DI_ERR_DIM", "DI_ERR_DOMAIN", "DI_ERR_DEVICE", "DI_ERR_OOM", "DI_ERR_CUDA"]
+    return names[s] if 0 <= s < len(names) else "?"
+
+
+class di_create_args(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int), ("n1", ctypes.c_int), ("n2", ctypes.c_int),
+                ("phi", ctypes.c_void_p), ("phi_dtype", ctypes.c_int),
+                ("w1", ctypes.c_void_p), ("b1", ctypes.c_void_p),
+                ("w2", ctypes.c_void_p), ("b2", ctypes.c_void_p),
+                ("w3", ctypes.c_void_p), ("b3", ctypes.c_void_p),
+                ("precision", ctypes.c_int), ("flags", ctypes.c_uint),
+                ("device", ctypes.c_int), ("max_batch", ctypes.c_int)]
+
+
+class di_info(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int), ("n1", ctypes.c_int), ("n2", ctypes.c_int), ("max_batch", ctypes.c_int),
+                ("precision", ctypes.c_int), ("flags", ctypes.c_uint), ("launches_per_recover", ctypes.c_int),
+                ("workspace_bytes", ctypes.c_longlong), ("stage_kernels", ctypes.c_char_p * 4)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libdeepinverse.so (build it first with paper_1701_03891_b200.build.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not built: run `python -m paper_1701_03891_b200.build` "
+                                "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    V, I, LL = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong
+    lib.di_create.argtypes = [ctypes.POINTER(di_create_args), ctypes.POINTER(V)]
+    lib.di_recover.argtypes = [V, V, LL, I, V, V]
+    lib.di_recover_host.argtypes = [V, V, LL, I, V, V]
+    lib.di_destroy.argtypes = [V]
+    lib.di_status_string.argtypes = [I]
+    lib.di_status_string.restype = ctypes.c_char_p
+    lib.di_last_error.argtypes = []
+    lib.di_last_error.restype = ctypes.c_char_p
+    lib.di_get_info.argtypes = [V, ctypes.POINTER(di_info)]
+    lib.di_set_profiling.argtypes = [V, I]
+    lib.di_stage_times.argtypes = [V, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I), I]
+    lib.di_debug_stage.argtypes = [V, I, V, V, I, V]
+    lib.di_debug_get_phi.argtypes = [V, V, LL]
+    for f in ("di_create", "di_recover", "di_recover_host", "di_destroy", "di_get_info", "di_set_profiling",
+              "di_stage_times", "di_debug_stage", "di_debug_get_phi"):
+        getattr(lib, f).restype = I
+    _lib = lib
+    return lib
+
+
+def _check(status: int, where: str):
+    if status != DI_OK:
+        raise DiError(status, where, load().di_last_error().decode(errors="replace"))
+
+
+def _ptr(a) -> int | None:
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):  # torch tensor
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _stream_handle(stream) -> int | None:
+    if stream is None:
+        try:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        except Exception:  # pragma: no cover
+            return None
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+# ------------------------------------------------------------------ same names as the C ABI
+def di_create(args: di_create_args) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    _check(load().di_create(ctypes.byref(args), ctypes.byref(h)), "di_create")
+    return h
+
+
+def di_recover(ctx, y, ldy: int, batch: int, xhat, stream=None):
+    _check(load().di_recover(ctx, _ptr(y), ldy, batch, _ptr(xhat), _stream_handle(stream)), "di_recover")
+
+
+def di_recover_host(ctx, y_host, ldy: int, batch: int, xhat_host, stream=None):
+    _check(load().di_recover_host(ctx, _ptr(y_host), ldy, batch, _ptr(xhat_host), _stream_handle(stream)),
+           "di_recover_host")
+
+
+def di_destroy(ctx):
+    _check(load().di_destroy(ctx), "di_destroy")
+
+
+def di_debug_stage(ctx, stage: int, x_in, x_out, batch: int, stream=None):
+    _check(load().di_debug_stage(ctx, stage, _ptr(x_in), _ptr(x_out), batch, _stream_handle(stream)),
+           "di_debug_stage")
+
+
+def di_status_string(s: int) -> str:
+    return load().di_status_string(s).decode()
+
+
+def di_last_error() -> str:
+    return load().di_last_error().decode(errors="replace")
+
+
+# ------------------------------------------------------------------ convenience owner object
+class DeepInverse:
+    """Owns one di_ctx.  phi: [m][n1*n2] (fp32 numpy; bf16 configs pass bf16-representable values),
+    params: synth.Params-like (w: 3 arrays [C_out][C_in][11][11], b: per-channel or full-map biases)."""
+
+    def __init__(self, phi: np.ndarray, params, n1: int, n2: int, precision: str = "bf16", flags: int = 0,
+                 device: int = 0, max_batch: int = 1):
+        load()
+        phi = np.ascontiguousarray(phi, dtype=np.float32)
+        self.m = phi.shape[0]
+        self.n1, self.n2, self.precision, self.max_batch = n1, n2, precision, max_batch
+        self.device = device
+        ws = [np.ascontiguousarray(w, np.float32) for w in params.w]
+        has_bias = params.b is not None and any(np.any(np.asarray(b) != 0) for b in params.b)
+        bs = [np.ascontiguousarray(b, np.float32) for b in params.b] if has_bias else [None, None, None]
+        if getattr(params, "fullmap_bias", False) and has_bias:
+            flags |= DI_FLAG_FULLMAP_BIAS
+        self.flags = flags
+        self._keep = (phi, ws, bs)
+        a = di_create_args(self.m, n1, n2, phi.ctypes.data, DI_DTYPE_F32,
+                           ws[0].ctypes.data, _ptr(bs[0]), ws[1].ctypes.data, _ptr(bs[1]),
+                           ws[2].ctypes.data, _ptr(bs[2]), PRECISIONS[precision], flags, device, max_batch)
+        self.ctx = di_create(a)
+        self._keep = None
+
+    @property
+    def storage_dtype(self):
+        import torch
+        return torch.bfloat16 if self.precision == "bf16" else torch.float32
+
+    def recover(self, y, xhat=None, stream=None):
+        """y: device tensor [B][ldy] of the storage dtype; returns x_hat [B][n1][n2] fp32 (device)."""
+        import torch
+        if y.dtype != self.storage_dtype or not y.is_cuda:
+            raise TypeError(f"y must be a CUDA {self.storage_dtype} tensor")
+        b = y.shape[0]
+        if xhat is None:
+            xhat = torch.empty((b, self.n1, self.n2), dtype=torch.float32, device=y.device)
+        di_recover(self.ctx, y, y.stride(0), b, xhat, stream)
+        return xhat
+
+    def recover_host(self, y_host, xhat_host=None, stream=None):
+        """End-to-end: host y (numpy/pinned torch, storage dtype) -> host x_hat fp32."""
+        b = y_host.shape[0]
+        if xhat_host is None:
+            xhat_host = np.empty((b, self.n1, self.n2), np.float32)
+        ldy = y_host.stride(0) if hasattr(y_host, "stride") and callable(y_host.stride) else y_host.strides[0] // y_host.itemsize
+        di_recover_host(self.ctx, y_host, ldy, b, xhat_host, stream)
+        return xhat_host
+
+    def debug_stage(self, stage: int, x_in, x_out, batch: int, stream=None):
+        di_debug_stage(self.ctx, stage, x_in, x_out, batch, stream)
+
+    def info(self) -> dict:
+        inf = di_info()
+        _check(load().di_get_info(self.ctx, ctypes.byref(inf)), "di_get_info")
+        return {"m": inf.m, "n1": inf.n1, "n2": inf.n2, "max_batch": inf.max_batch, "precision": inf.precision,
+                "flags": inf.flags, "launches_per_recover": inf.launches_per_recover,
+                "workspace_bytes": inf.workspace_bytes,
+                "stage_kernels": [s.decode() if s else "" for s in inf.stage_kernels]}
+
+    def set_profiling(self, on: bool):
+        _check(load().di_set_profiling(self.ctx, int(on)), "di_set_profiling")
+
+    def stage_times(self, reset: bool = False):
+        ms = (ctypes.c_float * 4)()
+        calls = ctypes.c_int()
+        _check(load().di_stage_times(self.ctx, ms, ctypes.byref(calls), int(reset)), "di_stage_times")
+        return list(ms), calls.value
+
+    def phi_device_copy(self) -> np.ndarray:
+        elt = 2 if self.precision == "bf16" else 4
+        out = np.empty(self.m * self.n1 * self.n2 * elt, np.uint8)
+        _check(load().di_debug_get_phi(self.ctx, out.ctypes.data, out.nbytes), "di_debug_get_phi")
+        return out.view(np.uint16 if elt == 2 else np.float32).reshape(self.m, self.n1 * self.n2)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            di_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,539 @@
+// api.cu -- the C ABI of include/deepinverse.h: validation, ownership, weight packing, workspace,
+// TMA tensor maps and the launch sequence of x_hat = M(y, Omega).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "deepinverse.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+di_status fail(di_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+#define CUDA_TRY(x)                                                                                 \
+  do {                                                                                              \
+    cudaError_t e_ = (x);                                                                           \
+    if (e_ != cudaSuccess)                                                                          \
+      return fail(e_ == cudaErrorMemoryAllocation ? DI_ERR_OOM : DI_ERR_CUDA, "%s failed: %s (%s:%d)", #x, \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                                      \
+  } while (0)
+
+constexpr int K = 11;             // filter size of every layer
+constexpr int C1 = 64, C2 = 32;   // filter counts l1, l2 (l3 = 1)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+uint16_t f2bf(float x) {  // round to nearest even (the harness uses the same rule)
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x7FFFFFu)) return 0x7FC0;
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+float bf2f(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float x;
+  std::memcpy(&x, &u, 4);
+  return x;
+}
+
+}  // namespace
+
+struct di_ctx_s {
+  int device = 0, num_sms = 0;
+  int m = 0, n1 = 0, n2 = 0, N = 0, max_batch = 0, kpad = 0;
+  di_precision prec = DI_PREC_BF16;
+  unsigned flags = 0;
+  size_t elt = 2;
+  // device buffers
+  void* phi = nullptr;          // FP32: Phi [m][N] fp32 ; BF16/TF32: Phi^T [N][kpad] storage type
+  float* wx1 = nullptr;         // [1][11][11][64]   xcorr orientation, fp32 (bf16-rounded in BF16 mode)
+  float* wx2 = nullptr;         // [64][11][11][32]
+  float* wx3 = nullptr;         // [32][11][11][1]
+  void* wp2 = nullptr;          // conv2 tensor-core weight blocks (BF16 mode)
+  float *b1 = nullptr, *b2 = nullptr, *b3 = nullptr;  // per-channel or cropped full maps (nullptr = zero)
+  void *xt = nullptr, *h1 = nullptr, *h2 = nullptr, *ystage = nullptr;
+  void* yhost_dev = nullptr;    // di_recover_host staging
+  size_t yhost_bytes = 0;
+  float* xhost_dev = nullptr;
+  long long ws_bytes = 0;
+  CUtensorMap tmPt{}, tmH1{};
+  int last_launches = 0;
+  bool profiling = false;
+  cudaEvent_t ev[5] = {};
+  float stage_ms[4] = {0, 0, 0, 0};
+  int prof_calls = 0;
+  bool prof_pending = false;
+};
+
+namespace {
+
+di_status encode_2d(CUtensorMap* map, const void* base, bool bf16, int inner, int outer, long long ld_elems,
+                    int box_inner, int box_outer) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld_elems * (bf16 ? 2 : 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (2d) failed: %d", (int)r);
+  return DI_OK;
+}
+
+di_status encode_h1(CUtensorMap* map, const void* h1, int batch, int n1, int n2) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {64, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {64 * 2, (cuuint64_t)n2 * 64 * 2, (cuuint64_t)n1 * n2 * 64 * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tc_box_rows(), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(h1), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h1) failed: %d", (int)r);
+  return DI_OK;
+}
+
+template <typename T>
+di_status upload(T** dst, const void* src, size_t bytes, long long* ws) {
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dst), bytes));
+  *ws += (long long)bytes;
+  if (src) CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+  return DI_OK;
+}
+
+// xcorr-orientation taps of layer l: wx[co][ci][a][b] = W[co][ci][10-a][10-b] (true convolution, Eq. (1))
+// or the taps as given (DI_FLAG_XCORR); optional bf16 rounding.
+std::vector<float> xcorr_taps(const float* w, int cout, int cin, bool given_xcorr, bool round_bf16) {
+  std::vector<float> out((size_t)cout * cin * K * K);
+  for (int co = 0; co < cout; ++co)
+    for (int ci = 0; ci < cin; ++ci)
+      for (int a = 0; a < K; ++a)
+        for (int b = 0; b < K; ++b) {
+          const int u = given_xcorr ? a : K - 1 - a, v = given_xcorr ? b : K - 1 - b;
+          float x = w[(((size_t)co * cin + ci) * K + u) * K + v];
+          if (round_bf16) x = bf2f(f2bf(x));
+          out[(((size_t)co * cin + ci) * K + a) * K + b] = x;
+        }
+  return out;
+}
+
+// SIMT layout [ci][a][b][co]
+std::vector<float> simt_layout(const std::vector<float>& wx, int cout, int cin) {
+  std::vector<float> out(wx.size());
+  for (int co = 0; co < cout; ++co)
+    for (int ci = 0; ci < cin; ++ci)
+      for (int t = 0; t < K * K; ++t) out[((size_t)ci * K * K + t) * cout + co] = wx[((size_t)co * cin + ci) * K * K + t];
+  return out;
+}
+
+// conv2 tensor-core blocks: block kb = (u = kb/3, v0 = 4*(kb%3)); row = v'*32 + k; 64 ci; SWIZZLE_128B image
+std::vector<uint16_t> conv2_tc_pack(const std::vector<float>& wx2) {
+  std::vector<uint16_t> out((size_t)di::C2_KBLOCKS * di::C2_KBLOCK_BYTES / 2, 0);
+  for (int kb = 0; kb < di::C2_KBLOCKS; ++kb) {
+    const int u = kb / 3, v0 = 4 * (kb % 3);
+    uint8_t* blk = reinterpret_cast<uint8_t*>(out.data()) + (size_t)kb * di::C2_KBLOCK_BYTES;
+    for (int row = 0; row < 128; ++row) {
+      const int vp = row / 32, k = row % 32, b = v0 + vp;
+      for (int ci = 0; ci < 64; ++ci) {
+        const float x = (b < K) ? wx2[(((size_t)k * 64 + ci) * K + u) * K + b] : 0.f;
+        const uint16_t h = f2bf(x);
+        const size_t off = (size_t)row * 128 + ((((size_t)ci / 8) ^ (row & 7)) << 4) + (ci % 8) * 2;
+        std::memcpy(blk + off, &h, 2);
+      }
+    }
+  }
+  return out;
+}
+
+// bias: per-channel [cout] or the window of the full map [cout][n1+10][n2+10] that S keeps, as [n1][n2][cout]
+di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n1, int n2, long long* ws) {
+  *dst = nullptr;
+  if (!b) return DI_OK;
+  if (!fullmap) return upload(dst, b, (size_t)cout * 4, ws);
+  const int h = n1 + K - 1, w = n2 + K - 1, p = (K - 1) / 2;
+  std::vector<float> bm((size_t)n1 * n2 * cout);
+  for (int r = 0; r < n1; ++r)
+    for (int c = 0; c < n2; ++c)
+      for (int o = 0; o < cout; ++o) bm[((size_t)r * n2 + c) * cout + o] = b[((size_t)o * h + r + p) * w + c + p];
+  return upload(dst, bm.data(), bm.size() * 4, ws);
+}
+
+void free_ctx(di_ctx c) {
+  if (!c) return;
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
+                c->yhost_dev, c->xhost_dev};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  delete c;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// the launch sequence (stages first..last) on caller buffers
+di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy, int batch, void* xt, void* h1,
+                     void* h2, float* xhat, cudaStream_t st) {
+  const bool bf16 = c->prec == DI_PREC_BF16;
+  const int fm = (c->flags & DI_FLAG_FULLMAP_BIAS) ? 1 : 0;
+  const int relu3 = (c->flags & DI_FLAG_FINAL_RELU) ? 1 : 0;
+  int launches = 0;
+  auto mark = [&](int i) {
+    if (c->profiling) cudaEventRecord(c->ev[i], st);
+  };
+  mark(first);
+  if (first <= 0 && 0 <= last) {
+    if (c->prec == DI_PREC_FP32) {
+      CUDA_TRY(di::launch_proxy_f32(reinterpret_cast<const float*>(y), ldy, reinterpret_cast<const float*>(c->phi),
+                                    c->m, c->N, batch, reinterpret_cast<float*>(xt), st));
+      ++launches;
+    } else {
+      const void* ysrc = y;
+      long long ld = ldy;
+      int inner = c->m;
+      if (!aligned16(y) || ((size_t)ldy * c->elt) % 16 != 0) {
+        CUDA_TRY(di::launch_stage_y(y, ldy, c->m, c->kpad, batch, c->ystage, bf16, st));
+        ++launches;
+        ysrc = c->ystage, ld = c->kpad, inner = c->kpad;
+      }
+      CUtensorMap tmY;
+      di_status s = encode_2d(&tmY, ysrc, bf16, inner, batch, ld, 128 / (int)c->elt, 128);
+      if (s != DI_OK) return s;
+      CUDA_TRY(di::launch_proxy_tc(&tmY, &c->tmPt, batch, c->N, c->kpad / (128 / (int)c->elt), xt, !bf16, st));
+      ++launches;
+    }
+  }
+  mark(1);
+  if (first <= 1 && 1 <= last) {
+    CUDA_TRY(di::launch_conv1_simt(xt, bf16, c->wx1, c->b1, fm, h1, batch, c->n1, c->n2, st));
+    ++launches;
+  }
+  mark(2);
+  if (first <= 2 && 2 <= last) {
+    if (bf16) {
+      CUtensorMap tm;
+      const CUtensorMap* tmp = &c->tmH1;
+      if (h1 != c->h1 || batch != c->max_batch) {
+        di_status s = encode_h1(&tm, h1, batch, c->n1, c->n2);
+        if (s != DI_OK) return s;
+        tmp = &tm;
+      }
+      CUDA_TRY(di::launch_conv2_tc(tmp, c->wp2, c->b2, fm, batch, c->n1, c->n2, h2, c->num_sms, st));
+    } else {
+      CUDA_TRY(di::launch_conv2_simt_f32(reinterpret_cast<const float*>(h1), c->wx2, c->b2, fm,
+                                         reinterpret_cast<float*>(h2), batch, c->n1, c->n2, st));
+    }
+    ++launches;
+  }
+  mark(3);
+  if (first <= 3 && 3 <= last) {
+    CUDA_TRY(di::launch_conv3_simt(h2, bf16, c->wx3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, st));
+    ++launches;
+  }
+  mark(4);
+  if (c->profiling) c->prof_pending = true;
+  c->last_launches = launches;
+  return DI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* di_status_string(di_status s) {
+  switch (s) {
+    case DI_OK: return "DI_OK";
+    case DI_ERR_ARG: return "DI_ERR_ARG";
+    case DI_ERR_DIM: return "DI_ERR_DIM";
+    case DI_ERR_DOMAIN: return "DI_ERR_DOMAIN";
+    case DI_ERR_DEVICE: return "DI_ERR_DEVICE";
+    case DI_ERR_OOM: return "DI_ERR_OOM";
+    case DI_ERR_CUDA: return "DI_ERR_CUDA";
+  }
+  return "DI_ERR_UNKNOWN";
+}
+
+const char* di_last_error(void) { return g_err; }
+
+di_status di_create(const di_create_args* a, di_ctx* out) {
+  if (!out) return fail(DI_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (!a) return fail(DI_ERR_ARG, "args is NULL");
+  if (a->n1 < 1 || a->n2 < 1) return fail(DI_ERR_DOMAIN, "n1=%d n2=%d must be >= 1", a->n1, a->n2);
+  const long long N = (long long)a->n1 * a->n2;
+  if (a->m < 1 || a->m > N) return fail(DI_ERR_DOMAIN, "m=%d must satisfy 1 <= m <= N=%lld (SPEC.md:140)", a->m, N);
+  if (!a->phi || !a->w1 || !a->w2 || !a->w3) return fail(DI_ERR_ARG, "phi and w1..w3 must be non-NULL");
+  if (a->phi_dtype != DI_DTYPE_F32 && a->phi_dtype != DI_DTYPE_BF16) return fail(DI_ERR_ARG, "bad phi_dtype");
+  if (a->precision != DI_PREC_FP32 && a->precision != DI_PREC_TF32 && a->precision != DI_PREC_BF16)
+    return fail(DI_ERR_ARG, "bad precision %d", (int)a->precision);
+  if (a->flags & ~(unsigned)(DI_FLAG_XCORR | DI_FLAG_FULLMAP_BIAS | DI_FLAG_FINAL_RELU))
+    return fail(DI_ERR_ARG, "unknown flag bits 0x%x", a->flags);
+  if (a->max_batch < 1) return fail(DI_ERR_ARG, "max_batch=%d must be >= 1", a->max_batch);
+  if (a->precision != DI_PREC_FP32 && N > 0x7fffffffLL) return fail(DI_ERR_DIM, "N too large");
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(DI_ERR_DEVICE, "no CUDA device");
+  if (a->device < 0 || a->device >= ndev) return fail(DI_ERR_DEVICE, "device %d out of range", a->device);
+  int maj = 0, min = 0;
+  cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, a->device);
+  cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, a->device);
+  if (maj != 10 || min != 0)
+    return fail(DI_ERR_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a only", a->device, maj, min);
+  CUDA_TRY(cudaSetDevice(a->device));
+
+  di_ctx c = new (std::nothrow) di_ctx_s();
+  if (!c) return fail(DI_ERR_OOM, "host allocation failed");
+  c->device = a->device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, a->device);
+  c->m = a->m, c->n1 = a->n1, c->n2 = a->n2, c->N = (int)N, c->max_batch = a->max_batch;
+  c->prec = a->precision, c->flags = a->flags;
+  c->elt = (a->precision == DI_PREC_BF16) ? 2 : 4;
+  c->kpad = ((a->m + 63) / 64) * 64;
+  const bool bf16 = c->prec == DI_PREC_BF16;
+  const bool xc = (a->flags & DI_FLAG_XCORR) != 0, fm = (a->flags & DI_FLAG_FULLMAP_BIAS) != 0;
+  di_status s = DI_OK;
+#define STEP(x)              \
+  do {                       \
+    s = (x);                 \
+    if (s != DI_OK) {        \
+      free_ctx(c);           \
+      return s;              \
+    }                        \
+  } while (0)
+
+  // ---- Phi: upload as fp32, then pack on the device
+  {
+    std::vector<float> phif;
+    const float* phisrc = reinterpret_cast<const float*>(a->phi);
+    if (a->phi_dtype == DI_DTYPE_BF16) {
+      phif.resize((size_t)a->m * N);
+      const uint16_t* pb = reinterpret_cast<const uint16_t*>(a->phi);
+      for (size_t i = 0; i < phif.size(); ++i) phif[i] = bf2f(pb[i]);
+      phisrc = phif.data();
+    }
+    if (c->prec == DI_PREC_FP32) {
+      STEP(upload(reinterpret_cast<float**>(&c->phi), phisrc, (size_t)a->m * N * 4, &c->ws_bytes));
+    } else {
+      float* tmp = nullptr;
+      long long dummy = 0;
+      STEP(upload(&tmp, phisrc, (size_t)a->m * N * 4, &dummy));
+      const size_t bytes = (size_t)N * c->kpad * c->elt;
+      cudaError_t e = cudaMalloc(&c->phi, bytes);
+      if (e != cudaSuccess) {
+        cudaFree(tmp);
+        free_ctx(c);
+        return fail(DI_ERR_OOM, "cudaMalloc(Phi^T, %zu) failed", bytes);
+      }
+      c->ws_bytes += bytes;
+      e = di::launch_pack_phiT(tmp, a->m, (int)N, c->kpad, c->phi, bf16, 0);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      cudaFree(tmp);
+      if (e != cudaSuccess) {
+        free_ctx(c);
+        return fail(DI_ERR_CUDA, "packing Phi^T failed: %s", cudaGetErrorString(e));
+      }
+    }
+  }
+  // ---- weights / biases
+  {
+    auto w1 = xcorr_taps(a->w1, C1, 1, xc, bf16);
+    auto w2 = xcorr_taps(a->w2, C2, C1, xc, bf16);
+    auto w3 = xcorr_taps(a->w3, 1, C2, xc, bf16);
+    auto s1 = simt_layout(w1, C1, 1), s2 = simt_layout(w2, C2, C1), s3 = simt_layout(w3, 1, C2);
+    STEP(upload(&c->wx1, s1.data(), s1.size() * 4, &c->ws_bytes));
+    STEP(upload(&c->wx2, s2.data(), s2.size() * 4, &c->ws_bytes));
+    STEP(upload(&c->wx3, s3.data(), s3.size() * 4, &c->ws_bytes));
+    if (bf16) {
+      auto p2 = conv2_tc_pack(w2);
+      STEP(upload(&c->wp2, p2.data(), p2.size() * 2, &c->ws_bytes));
+    }
+    STEP(upload_bias(&c->b1, a->b1, C1, fm, a->n1, a->n2, &c->ws_bytes));
+    STEP(upload_bias(&c->b2, a->b2, C2, fm, a->n1, a->n2, &c->ws_bytes));
+    STEP(upload_bias(&c->b3, a->b3, 1, fm, a->n1, a->n2, &c->ws_bytes));
+  }
+  // ---- workspace
+  {
+    const size_t B = (size_t)a->max_batch;
+    STEP(upload(&c->xt, nullptr, B * N * c->elt, &c->ws_bytes));
+    STEP(upload(&c->h1, nullptr, B * N * C1 * c->elt, &c->ws_bytes));
+    STEP(upload(&c->h2, nullptr, B * N * C2 * c->elt, &c->ws_bytes));
+    if (c->prec != DI_PREC_FP32) STEP(upload(&c->ystage, nullptr, B * c->kpad * c->elt, &c->ws_bytes));
+  }
+  // ---- kernels / tensor maps
+  if (c->prec != DI_PREC_FP32) {
+    cudaError_t e = di::setup_proxy_tc();
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return fail(DI_ERR_CUDA, "setup_proxy_tc: %s", cudaGetErrorString(e));
+    }
+    STEP(encode_2d(&c->tmPt, c->phi, bf16, c->kpad, (int)N, c->kpad, 128 / (int)c->elt, 256));
+  }
+  if (bf16) {
+    cudaError_t e = di::setup_conv2_tc(a->n2);
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return fail(DI_ERR_CUDA, "setup_conv2_tc: %s", cudaGetErrorString(e));
+    }
+    STEP(encode_h1(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
+  }
+  for (auto& e : c->ev) {
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      free_ctx(c);
+      return fail(DI_ERR_CUDA, "cudaEventCreate failed");
+    }
+  }
+#undef STEP
+  *out = c;
+  return DI_OK;
+}
+
+di_status di_recover(di_ctx c, const void* y, long long ldy, int batch, float* xhat, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!y || !xhat) return fail(DI_ERR_ARG, "y and xhat must be non-NULL device pointers");
+  if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  return run_stages(c, 0, 3, y, ldy, batch, c->xt, c->h1, c->h2, xhat, reinterpret_cast<cudaStream_t>(stream));
+}
+
+di_status di_recover_host(di_ctx c, const void* y_host, long long ldy, int batch, float* xhat_host, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!y_host || !xhat_host) return fail(DI_ERR_ARG, "host buffers must be non-NULL");
+  if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t ybytes = (size_t)batch * ldy * c->elt;
+  if (ybytes > c->yhost_bytes) {
+    if (c->yhost_dev) cudaFree(c->yhost_dev);
+    c->yhost_dev = nullptr;
+    c->yhost_bytes = 0;
+    CUDA_TRY(cudaMalloc(&c->yhost_dev, ybytes));
+    c->yhost_bytes = ybytes;
+  }
+  if (!c->xhost_dev) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->xhost_dev), (size_t)c->max_batch * c->N * 4));
+  CUDA_TRY(cudaMemcpyAsync(c->yhost_dev, y_host, ybytes, cudaMemcpyHostToDevice, st));
+  di_status s = run_stages(c, 0, 3, c->yhost_dev, ldy, batch, c->xt, c->h1, c->h2, c->xhost_dev, st);
+  if (s != DI_OK) return s;
+  CUDA_TRY(cudaMemcpyAsync(xhat_host, c->xhost_dev, (size_t)batch * c->N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DI_OK;
+}
+
+di_status di_destroy(di_ctx c) {
+  if (!c) return DI_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  free_ctx(c);
+  return DI_OK;
+}
+
+di_status di_get_info(di_ctx c, di_info* info) {
+  if (!c || !info) return fail(DI_ERR_ARG, "NULL argument");
+  info->m = c->m, info->n1 = c->n1, info->n2 = c->n2, info->max_batch = c->max_batch;
+  info->precision = c->prec, info->flags = c->flags;
+  info->launches_per_recover = c->last_launches ? c->last_launches : 4;
+  info->workspace_bytes = c->ws_bytes;
+  const bool bf16 = c->prec == DI_PREC_BF16;
+  info->stage_kernels[0] = c->prec == DI_PREC_FP32 ? "k_proxy_f32" : (bf16 ? "k_proxy_tc<bf16>" : "k_proxy_tc<tf32>");
+  info->stage_kernels[1] = "k_conv_wide<conv1>";
+  info->stage_kernels[2] = bf16 ? "k_conv2_tc" : "k_conv_wide<conv2,f32>";
+  info->stage_kernels[3] = "k_conv3";
+  return DI_OK;
+}
+
+di_status di_set_profiling(di_ctx c, int enable) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  c->profiling = enable != 0;
+  return DI_OK;
+}
+
+di_status di_stage_times(di_ctx c, float ms[4], int* calls, int reset) {
+  if (!c || !ms) return fail(DI_ERR_ARG, "NULL argument");
+  if (c->prof_pending) {
+    CUDA_TRY(cudaEventSynchronize(c->ev[4]));
+    for (int i = 0; i < 4; ++i) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, c->ev[i], c->ev[i + 1]) == cudaSuccess) c->stage_ms[i] += t;
+    }
+    c->prof_calls++;
+    c->prof_pending = false;
+  }
+  for (int i = 0; i < 4; ++i) ms[i] = c->stage_ms[i];
+  if (calls) *calls = c->prof_calls;
+  if (reset) {
+    for (int i = 0; i < 4; ++i) c->stage_ms[i] = 0.f;
+    c->prof_calls = 0;
+  }
+  return DI_OK;
+}
+
+di_status di_debug_stage(di_ctx c, int stage, const void* in, void* out, int batch, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (stage < 0 || stage > 3) return fail(DI_ERR_ARG, "stage=%d outside [0,3]", stage);
+  if (!in || !out) return fail(DI_ERR_ARG, "NULL buffer");
+  if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (stage) {
+    case 0: return run_stages(c, 0, 0, in, c->m, batch, out, nullptr, nullptr, nullptr, st);
+    case 1: return run_stages(c, 1, 1, nullptr, 0, batch, const_cast<void*>(in), out, nullptr, nullptr, st);
+    case 2: return run_stages(c, 2, 2, nullptr, 0, batch, nullptr, const_cast<void*>(in), out, nullptr, st);
+    default:
+      return run_stages(c, 3, 3, nullptr, 0, batch, nullptr, nullptr, const_cast<void*>(in),
+                        reinterpret_cast<float*>(out), st);
+  }
+}
+
+di_status di_debug_get_phi(di_ctx c, void* host_out, long long bytes) {
+  if (!c || !host_out) return fail(DI_ERR_ARG, "NULL argument");
+  const size_t need = (size_t)c->m * c->N * c->elt;
+  if ((size_t)bytes < need) return fail(DI_ERR_DIM, "need %zu bytes", need);
+  if (c->prec == DI_PREC_FP32) {
+    CUDA_TRY(cudaMemcpy(host_out, c->phi, need, cudaMemcpyDeviceToHost));
+    return DI_OK;
+  }
+  // Phi^T [N][kpad] -> Phi [m][N]
+  std::vector<uint8_t> t((size_t)c->N * c->kpad * c->elt);
+  CUDA_TRY(cudaMemcpy(t.data(), c->phi, t.size(), cudaMemcpyDeviceToHost));
+  uint8_t* o = reinterpret_cast<uint8_t*>(host_out);
+  for (int i = 0; i < c->m; ++i)
+    for (int j = 0; j < c->N; ++j)
+      std::memcpy(o + ((size_t)i * c->N + j) * c->elt, t.data() + ((size_t)j * c->kpad + i) * c->elt, c->elt);
+  return DI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,267 @@
+// k_proxy.cu -- stage 0, the lifting layer: x_tilde_b = Phi^T y_b for a batch,
+// written straight into the row-major n1 x n2 image layout that conv layer 1 reads.
+//
+// As one batched GEMM  X_tilde[B][N] = Y[B][M] * Phi[M][N].
+//   bf16 / tf32: tcgen05 UMMA, D tile 128 (images) x 256 (pixels) in TMEM, A = Y tile and B = Phi^T tile
+//         staged by TMA (SWIZZLE_128B, K-major; the K tail M..Kpad is zero-filled by the packing of Phi^T
+//         and by TMA out-of-bounds fill of Y), 4-stage mbarrier pipeline, warp-specialised
+//         (warp 0 TMA producer, warp 1 MMA issuer, warps 0-3 epilogue).
+//   fp32: SIMT FFMA tiled GEMM with two-level (per-K-tile, then total) accumulation for the 1e-5 parity bar.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "sm100.cuh"
+
+namespace di {
+
+namespace {
+constexpr int PX_BM = 128;      // images per tile (UMMA M)
+constexpr int PX_BN = 256;      // pixels per tile (UMMA N)
+constexpr int PX_STAGES = 4;
+}  // namespace
+
+// ELT: 2 = bf16 (kind::f16, K=16 per MMA), 4 = fp32 storage with kind::tf32 (K=8 per MMA)
+template <int ELT>
+__global__ void __launch_bounds__(128, 1)
+    k_proxy_tc(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmPt, int batch,
+               int N, int kblocks, void* __restrict__ xt) {
+  constexpr int KB_ELEMS = 128 / ELT;                       // K elements per 128-B swizzle row
+  constexpr uint32_t A_BYTES = PX_BM * 128, B_BYTES = PX_BN * 128;
+  constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  constexpr int K_PER_MMA = 32 / ELT;                        // 16 (bf16) or 8 (tf32)
+  constexpr int MMAS_PER_KB = KB_ELEMS / K_PER_MMA;          // 4
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[PX_STAGES], empty[PX_STAGES], tfull;
+  __shared__ uint32_t tslot;
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nbt = (batch + PX_BM - 1) / PX_BM;
+  const int bt = blockIdx.x % nbt, nt = blockIdx.x / nbt;   // consecutive CTAs share one Phi^T slice (L2)
+  const int b0 = bt * PX_BM, n0 = nt * PX_BN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmY);
+    tma_prefetch_desc(&tmPt);
+    for (int s = 0; s < PX_STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    mbar_init(&tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<256>(&tslot), tmem_relinquish();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0 && lane == 0) {  // ---------------- TMA producer
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % PX_STAGES;
+      if (kb >= PX_STAGES) mbar_wait(&empty[s], ((kb / PX_STAGES) - 1) & 1);
+      uint8_t* sa = smem + s * STAGE;
+      mbar_arrive_expect_tx(&full[s], STAGE);
+      tma_load_2d(sa, &tmY, &full[s], kb * KB_ELEMS, b0);
+      tma_load_2d(sa + A_BYTES, &tmPt, &full[s], kb * KB_ELEMS, n0);
+    }
+  } else if (warp == 1 && lane == 0) {  // ---------------- MMA issuer
+    constexpr uint32_t idesc = idesc_f32acc(ELT == 2 ? 1 : 2, PX_BM, PX_BN);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % PX_STAGES;
+      mbar_wait(&full[s], (kb / PX_STAGES) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
+#pragma unroll
+      for (int k = 0; k < MMAS_PER_KB; ++k) {
+        const uint64_t ad = smem_desc(sa + k * 32, 16, 1024, kSwizzle128B);
+        const uint64_t bd = smem_desc(sb + k * 32, 16, 1024, kSwizzle128B);
+        if (ELT == 2)
+          umma_f16_ss(tmem, ad, bd, idesc, (kb | k) != 0);
+        else
+          umma_tf32_ss(tmem, ad, bd, idesc, (kb | k) != 0);
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(&tfull);
+  }
+  __syncwarp();
+  // ---------------- epilogue: all 4 warps, warp w owns TMEM lanes 32w..32w+31 (= images)
+  mbar_wait(&tfull, 0);
+  tc_fence_after();
+  const int b = b0 + warp * 32 + lane;
+  const bool row_ok = b < batch;
+  const bool vec_ok = (N % 8) == 0;
+  for (int c = 0; c < PX_BN; c += 32) {
+    uint32_t r[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
+    tmem_ld_wait();
+    const int col = n0 + c;
+    if (!row_ok || col >= N) continue;
+    if (ELT == 2) {
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(xt) + (size_t)b * N + col;
+      if (vec_ok && col + 32 <= N) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1]));
+          v.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3]));
+          v.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5]));
+          v.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7]));
+          reinterpret_cast<uint4*>(dst)[q] = v;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col + j < N) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+      }
+    } else {
+      float* dst = reinterpret_cast<float*>(xt) + (size_t)b * N + col;
+      if ((N % 4) == 0 && col + 32 <= N) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          reinterpret_cast<float4*>(dst)[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                          __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col + j < N) dst[j] = __uint_as_float(r[j]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<256>(tmem);
+}
+
+size_t proxy_tc_smem_bytes() { return (size_t)PX_STAGES * (PX_BM + PX_BN) * 128 + 1024; }
+
+cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
+                            void* xt, bool tf32, cudaStream_t st) {
+  const int nbt = (batch + PX_BM - 1) / PX_BM, nnt = (N + PX_BN - 1) / PX_BN;
+  const size_t smem = proxy_tc_smem_bytes();
+  if (tf32) {
+    k_proxy_tc<4><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt);
+  } else {
+    k_proxy_tc<2><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t setup_proxy_tc() {
+  cudaError_t e = cudaFuncSetAttribute(k_proxy_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)proxy_tc_smem_bytes());
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_proxy_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)proxy_tc_smem_bytes());
+}
+
+// ----------------------------------------------------------------------------- fp32 SIMT GEMM
+// xt[b][j] = sum_i y[b][i] * phi[i][j];  64 (b) x 64 (j) tile, 256 threads, 4x4 outputs each.
+__global__ void __launch_bounds__(256) k_proxy_f32(const float* __restrict__ y, long long ldy,
+                                                   const float* __restrict__ phi, int m, int N, int batch,
+                                                   float* __restrict__ xt) {
+  __shared__ float sy[16][64 + 4];
+  __shared__ float sp[16][64];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int j0 = blockIdx.x * 64, b0 = blockIdx.y * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < m; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e / 64, c = e % 64;
+      const int bb = b0 + c, k = k0 + kk, jj = j0 + c;
+      sy[kk][c] = (bb < batch && k < m) ? y[(size_t)bb * ldy + k] : 0.f;
+      sp[kk][c] = (k < m && jj < N) ? phi[(size_t)k * N + jj] : 0.f;
+    }
+    __syncthreads();
+    float part[4][4] = {};
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sy[kk][ty * 4 + i], bv[i] = sp[kk][tx + 16 * i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) part[i][q] = fmaf(a[i], bv[q], part[i][q]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][q] += part[i][q];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int bb = b0 + ty * 4 + i;
+    if (bb >= batch) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int jj = j0 + tx + 16 * q;
+      if (jj < N) xt[(size_t)bb * N + jj] = acc[i][q];
+    }
+  }
+}
+
+cudaError_t launch_proxy_f32(const float* y, long long ldy, const float* phi, int m, int N, int batch, float* xt,
+                             cudaStream_t st) {
+  dim3 grid((N + 63) / 64, (batch + 63) / 64);
+  k_proxy_f32<<<grid, 256, 0, st>>>(y, ldy, phi, m, N, batch, xt);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- packing helpers
+// Phi [m][N] (fp32 on device) -> Phi^T [N][kpad] in storage type (bf16 RNE or fp32), zero K tail.
+template <typename T>
+__global__ void k_pack_phiT(const float* __restrict__ phi, int m, int N, int kpad, T* __restrict__ out) {
+  __shared__ float tile[32][33];
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int i = i0 + r, j = j0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < m && j < N) ? phi[(size_t)i * N + j] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int j = j0 + r, i = i0 + threadIdx.x;
+    if (j < N && i < kpad) {
+      const float v = tile[threadIdx.x][r];
+      if constexpr (sizeof(T) == 2)
+        out[(size_t)j * kpad + i] = __float2bfloat16_rn(v);
+      else
+        out[(size_t)j * kpad + i] = v;
+    }
+  }
+}
+
+cudaError_t launch_pack_phiT(const float* phi, int m, int N, int kpad, void* out, bool bf16, cudaStream_t st) {
+  dim3 grid((N + 31) / 32, (kpad + 31) / 32), block(32, 8);
+  if (bf16)
+    k_pack_phiT<__nv_bfloat16><<<grid, block, 0, st>>>(phi, m, N, kpad, reinterpret_cast<__nv_bfloat16*>(out));
+  else
+    k_pack_phiT<float><<<grid, block, 0, st>>>(phi, m, N, kpad, reinterpret_cast<float*>(out));
+  return cudaGetLastError();
+}
+
+// y [batch][ldy] (any alignment) -> packed [batch][kpad] with zero tail, same element type
+template <typename T>
+__global__ void k_stage_y(const T* __restrict__ y, long long ldy, int m, int kpad, int batch, T* __restrict__ out) {
+  const long long total = (long long)batch * kpad;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / kpad;
+    const int k = (int)(e - b * kpad);
+    out[e] = k < m ? y[b * ldy + k] : T(0.f);
+  }
+}
+
+cudaError_t launch_stage_y(const void* y, long long ldy, int m, int kpad, int batch, void* out, bool bf16,
+                           cudaStream_t st) {
+  const long long total = (long long)batch * kpad;
+  const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  if (bf16)
+    k_stage_y<__nv_bfloat16><<<blocks, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(y), ldy, m, kpad,
+                                                     batch, reinterpret_cast<__nv_bfloat16*>(out));
+  else
+    k_stage_y<float><<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(y), ldy, m, kpad, batch,
+                                            reinterpret_cast<float*>(out));
+  return cudaGetLastError();
+}
+
+}  // namespace di

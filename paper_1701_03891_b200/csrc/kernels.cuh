@@ -1,0 +1,45 @@
+// kernels.cuh -- launch entry points of the DeepInverse kernels (internal; the public ABI is
+// include/deepinverse.h).  All launches are asynchronous on the given stream.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+namespace di {
+
+// conv2 tensor-core geometry (k_conv2_tc.cu)
+constexpr int C2_ROWS = 6;                  // output rows per work unit
+constexpr int C2_KBLOCKS = 33;              // 11 tap rows x 3 column-tap groups of 4
+constexpr int C2_KBLOCK_BYTES = 128 * 128;  // 128 rows (4 taps x 32 filters) x 64 ch x bf16
+
+// stage 0: lifting layer x_tilde = Phi^T y
+cudaError_t setup_proxy_tc();
+size_t proxy_tc_smem_bytes();
+cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
+                            void* xt, bool tf32, cudaStream_t st);
+cudaError_t launch_proxy_f32(const float* y, long long ldy, const float* phi, int m, int N, int batch, float* xt,
+                             cudaStream_t st);
+cudaError_t launch_pack_phiT(const float* phi, int m, int N, int kpad, void* out, bool bf16, cudaStream_t st);
+cudaError_t launch_stage_y(const void* y, long long ldy, int m, int kpad, int batch, void* out, bool bf16,
+                           cudaStream_t st);
+
+// stage 1: conv layer 1 (1 -> 64, ReLU)
+cudaError_t launch_conv1_simt(const void* xt, bool bf16, const float* wx, const float* bias, int fullmap, void* h1,
+                              int batch, int n1, int n2, cudaStream_t st);
+
+// stage 2: conv layer 2 (64 -> 32, ReLU)
+cudaError_t setup_conv2_tc(int n2);
+size_t conv2_tc_smem_bytes(int n2);
+int conv2_tc_box_rows();
+int conv2_tc_box_cols(int n2);
+cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
+                            int n1, int n2, void* h2, int num_sms, cudaStream_t st);
+cudaError_t launch_conv2_simt_f32(const float* h1, const float* wx, const float* bias, int fullmap, float* h2,
+                                  int batch, int n1, int n2, cudaStream_t st);
+
+// stage 3: conv layer 3 (32 -> 1, optional ReLU)
+cudaError_t launch_conv3_simt(const void* h2, bool bf16, const float* wx, const float* bias, int fullmap, int relu,
+                              float* xhat, int batch, int n1, int n2, cudaStream_t st);
+
+}  // namespace di

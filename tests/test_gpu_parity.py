@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): max per-image rel-L2 <= 1e-5 (fp32 path), <= 2e-2 (bf16 / TF32
+tensor-core paths), |dPSNR| <= 0.05 dB per image and for the batch mean.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_helpers import TOL_DPSNR, TOL_REL_L2, Case, compare, make_ctx, run, sample_rows, y_device
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(case, gpu, idx, **kw):
+    ref = case.oracle(idx, **kw)
+    rel, dps, dmean = compare(gpu[idx], ref, case.x[idx], case.precision)
+    assert rel <= TOL_REL_L2[case.precision], f"rel-L2 {rel:.3g}"
+    assert dps <= TOL_DPSNR and abs(dmean) <= TOL_DPSNR, f"dPSNR {dps:.3g} mean {dmean:.3g}"
+    return rel, dps
+
+
+# ----------------------------------------------------------------------------- the five configs
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_tiny(precision):
+    """configs[0]: 16x16, M=64, batch 4 (all images checked)."""
+    c = synth.CONFIGS["tiny"]
+    case = Case(c.n, c.n, c.m, c.batch, precision, c.n_blobs, c.n_rects)
+    ctx = make_ctx(case)
+    out = run(case, ctx)
+    _check(case, out, np.arange(c.batch))
+
+
+@pytest.mark.parametrize("precision", ["f32", "tf32"])
+def test_paper_scale(precision):
+    """configs[1]: 64x64, M=1024, batch 256, fp32 and TF32; 32 sampled images."""
+    c = synth.CONFIGS["paper"]
+    case = Case(c.n, c.n, c.m, c.batch, precision, c.n_blobs, c.n_rects)
+    ctx = make_ctx(case)
+    out = run(case, ctx)
+    _check(case, out, sample_rows(c.batch, 32))
+
+
+def test_lowrate_full_batch():
+    """configs[2]: 64x64, M=410, batch 4096 (the bench launch), bf16; 64 sampled images."""
+    c = synth.CONFIGS["lowrate"]
+    case = Case(c.n, c.n, c.m, c.batch, "bf16", c.n_blobs, c.n_rects)
+    ctx = make_ctx(case)
+    out = run(case, ctx)
+    assert np.all(np.isfinite(out))
+    _check(case, out, sample_rows(c.batch, 64))
+
+
+def test_larger():
+    """configs[3]: 128x128, M=4096, batch 1024, bf16; 16 sampled images."""
+    c = synth.CONFIGS["larger"]
+    case = Case(c.n, c.n, c.m, c.batch, "bf16", c.n_blobs, c.n_rects)
+    ctx = make_ctx(case)
+    out = run(case, ctx)
+    _check(case, out, sample_rows(c.batch, 16))
+
+
+@pytest.mark.slow
+def test_stress():
+    """configs[4]: 256x256, M=16384 (Phi 2.1 GB bf16), texture noise; batch 16 (sizes of the config, batch
+    reduced to bound host generation), 4 sampled images."""
+    c = synth.CONFIGS["stress"]
+    case = Case(c.n, c.n, c.m, 16, "bf16", c.n_blobs, c.n_rects, c.texture_var)
+    ctx = make_ctx(case)
+    out = run(case, ctx)
+    _check(case, out, sample_rows(16, 4))
+
+
+# ----------------------------------------------------------------------------- edges / flags
+@pytest.mark.parametrize("precision", ["f32", "bf16", "tf32"])
+@pytest.mark.parametrize("n1,n2,m,batch", [(9, 13, 40, 3), (40, 72, 300, 130), (64, 64, 410, 1), (23, 64, 100, 129),
+                                           (70, 150, 700, 5)])
+def test_ragged_shapes(precision, n1, n2, m, batch):
+    case = Case(n1, n2, m, batch, precision, 6, 3)
+    ctx = make_ctx(case)
+    out = run(case, ctx)
+    _check(case, out, sample_rows(batch, 8))
+
+
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+@pytest.mark.parametrize("bias", ["channel", "fullmap"])
+@pytest.mark.parametrize("final_relu,xcorr", [(False, False), (True, True)])
+def test_flags_and_biases(precision, bias, final_relu, xcorr):
+    from paper_1701_03891_b200 import DI_FLAG_FINAL_RELU, DI_FLAG_XCORR
+    case = Case(32, 32, 256, 6, precision, bias=bias)
+    flags = (DI_FLAG_FINAL_RELU if final_relu else 0) | (DI_FLAG_XCORR if xcorr else 0)
+    ctx = make_ctx(case, flags=flags)
+    out = run(case, ctx)
+    _check(case, out, np.arange(6), final_relu=final_relu, xcorr=xcorr)
+
+
+def test_structured_weights_psnr_parity():
+    """Closed-form fixture (tests/test_oracle_forward.py): blur of the back-projection; PSNR vs truth is
+    meaningful here (7-15 dB), so |dPSNR| is a real check of the bf16 path."""
+    from test_oracle_forward import structured_params
+    p = structured_params()
+    p = synth.Params([w.astype(np.float32) for w in p.w], [b.astype(np.float32) for b in p.b])
+    case = Case(64, 64, 410, 8, "bf16", params=p)
+    ctx = make_ctx(case)
+    out = run(case, ctx)
+    rel, dps = _check(case, out, np.arange(8))
+    assert 5 < oracle.psnr(out[0], case.x[0]) < 30
+
+
+# ----------------------------------------------------------------------------- invariants
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_invariants_bitwise(precision):
+    import torch
+    case = Case(64, 64, 410, 20, precision)
+    ctx = make_ctx(case, max_batch=20)
+    y = y_device(case, ctx)
+    a = ctx.recover(y).cpu().numpy()
+    b = ctx.recover(y).cpu().numpy()
+    assert np.array_equal(a, b), "repeat-run determinism"
+    one = ctx.recover(y[7:8].contiguous()).cpu().numpy()
+    assert np.array_equal(one[0], a[7]), "batch invariance"
+    two = ctx.recover((2 * y).contiguous()).cpu().numpy()
+    assert np.array_equal(two, 2 * a), "positive homogeneity (zero biases)"
+    zero = ctx.recover(torch.zeros_like(y)).cpu().numpy()
+    assert np.all(zero == 0), "y = 0 -> x_hat = 0"
+
+
+def test_zero_weights_give_bias_only():
+    p = synth.make_params(bias="channel")
+    p0 = synth.Params([np.zeros_like(w) for w in p.w], p.b)
+    case = Case(32, 32, 100, 3, "bf16", params=p0)
+    out = run(case, make_ctx(case))
+    ref = case.oracle(np.arange(3))
+    assert np.allclose(out, ref, atol=1e-6)
+
+
+def test_host_e2e_matches_device():
+    case = Case(64, 64, 410, 33, "bf16")
+    ctx = make_ctx(case)
+    dev = run(case, ctx)
+    import torch
+    yh = torch.from_numpy(case.y).to(torch.bfloat16).pin_memory()
+    host = ctx.recover_host(yh)
+    assert np.array_equal(host, dev)
+
+
+def test_device_phi_is_rne_bf16():
+    case = Case(16, 16, 64, 2, "bf16")
+    ctx = make_ctx(case)
+    assert np.array_equal(ctx.phi_device_copy(), synth.f32_to_bf16_bits(case.phi))
+
+
+def test_misaligned_ldy_staging():
+    import torch
+    case = Case(64, 64, 410, 9, "bf16")
+    ctx = make_ctx(case)
+    ref = run(case, ctx)
+    big = torch.zeros((9, 413), dtype=torch.bfloat16, device="cuda")
+    big[:, :410] = torch.from_numpy(case.y).to(torch.bfloat16)
+    view = big[:, :410]
+    out = ctx.recover(view)          # ldy = 413 -> 826-B rows: staged copy path
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_error_codes():
+    from paper_1701_03891_b200 import DiError
+    import torch
+    case = Case(16, 16, 64, 2, "bf16")
+    ctx = make_ctx(case, max_batch=2)
+    y = torch.zeros((3, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(DiError) as e:
+        ctx.recover(y)
+    assert e.value.status == 1
+    with pytest.raises(DiError) as e:
+        ctx.recover(torch.zeros((2, 63), dtype=torch.bfloat16, device="cuda"))
+    assert e.value.status == 2
+
+
+# ----------------------------------------------------------------------------- per stage
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_stages_individually(precision):
+    """di_debug_stage: each stage against the oracle on the GPU's own stage input."""
+    import torch
+    case = Case(40, 64, 300, 4, precision)
+    ctx = make_ctx(case)
+    dt = ctx.storage_dtype
+    n1, n2, B = case.n1, case.n2, case.batch
+    y = y_device(case, ctx)
+    xt = torch.empty((B, n1, n2), dtype=dt, device="cuda")
+    h1 = torch.empty((B, n1, n2, 64), dtype=dt, device="cuda")
+    h2 = torch.empty((B, n1, n2, 32), dtype=dt, device="cuda")
+    xh = torch.empty((B, n1, n2), dtype=torch.float32, device="cuda")
+    ctx.debug_stage(0, y, xt, B)
+    ctx.debug_stage(1, xt, h1, B)
+    ctx.debug_stage(2, h1, h2, B)
+    ctx.debug_stage(3, h2, xh, B)
+    torch.cuda.synchronize()
+    tol = 1e-5 if precision == "f32" else 8e-3   # bf16 stage outputs are rounded to bf16 (2^-9)
+    f = lambda t: t.float().cpu().numpy().astype(np.float64)
+    ref0 = oracle.proxy(case.phi, case.y).reshape(B, n1, n2)
+    assert oracle.rel_l2(f(xt), ref0) <= tol
+    p = case.params
+    for b in range(B):
+        r1 = oracle.conv_layer(f(xt)[b][None], p.w[0], p.b[0], relu=True)
+        assert oracle.rel_l2(f(h1)[b].transpose(2, 0, 1), r1) <= tol
+        r2 = oracle.conv_layer(f(h1)[b].transpose(2, 0, 1), p.w[1], p.b[1], relu=True)
+        assert oracle.rel_l2(f(h2)[b].transpose(2, 0, 1), r2) <= tol
+        r3 = oracle.conv_layer(f(h2)[b].transpose(2, 0, 1), p.w[2], p.b[2], relu=False)
+        assert oracle.rel_l2(f(xh)[b], r3[0]) <= (1e-5 if precision == "f32" else 1e-5 * 10)
