@@ -81,6 +81,12 @@ __global__ void __launch_bounds__(256, 1)
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
+  // Guard rows after the strip: the zero tap slot (v = 11) of the last output position and the padded
+  // columns of the last tile read up to GUARD_ROWS rows past the TMA box.  Their weights / outputs are
+  // zero / discarded, but 0 * (NaN garbage) would not be, so the guard must hold finite values.
+  for (int i = threadIdx.x; i < GUARD_ROWS * 128 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(strip + strip_bytes)[i] = make_uint4(0, 0, 0, 0);
+  fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
