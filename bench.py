@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""bench.py -- batched DeepInverse recovery throughput on B200 (BASELINE.json `metric`).
+
+One *step* = one di_recover of a whole per-GPU batch: y -> x_tilde = Phi^T y -> conv 1->64+ReLU ->
+conv 64->32+ReLU -> conv 32->1 -> x_hat (every row of SURVEY.md §8(a)), inputs resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config lowrate] [--impl ours|reference]
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...   (one rank per GPU)
+
+Multi-GPU: the images are independent, so rank r recovers global images
+[r*B, (r+1)*B) with Phi and Omega replicated and NO collective on the data path ("scaling": "weak").
+torch.distributed (NCCL) only aligns the start (barrier) and takes the max of the per-rank device times.
+
+Rank 0 prints ONE JSON line.  `value` = images recovered by all ranks / max-over-ranks device time;
+`e2e` = the same through di_recover_host (pinned host y in, host x_hat out, copies inside the timed
+region); `roofline` = the dominant kernel (conv layer 2) measured live with CUDA events recorded by the
+library on the launching stream; `cpu_baseline` = the fp64 oracle (oracle/, test infrastructure) timed
+as it stands on this host's cores over a bounded sample of the same workload.
+
+`--impl reference`: this tier has no reference implementation; the reference arm is the oracle, run on
+the host cores over a bounded sample per step (rank 0 only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "recovered images/sec per GPU and 8-GPU; achieved tensor-core TFLOP/s vs peak"
+UNIT = "images/s"
+KSZ = 11
+CONV2_FLOP_PER_PX = 2 * 32 * 64 * KSZ * KSZ          # 495 616
+PATH_FLOP_PER_PX = 2 * (64 * 1 + 32 * 64 + 1 * 32) * KSZ * KSZ   # 2 * 259 424 conv taps
+
+
+# ----------------------------------------------------------------------------- distributed plumbing
+def dist_env() -> tuple[int, int, int]:
+    """(rank, world, local_rank) from the torchrun environment (1 process when absent)."""
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def shard(rank: int, per_rank: int) -> tuple[int, int]:
+    """Global image indices [start, stop) recovered by `rank` (contiguous blocks, weak scaling)."""
+    return rank * per_rank, (rank + 1) * per_rank
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank scalar over the process group (identity without one)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(device=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        if device is not None and dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[device.index])
+        else:
+            dist.barrier()
+
+
+def aggregate(per_rank_units: int, world: int, max_seconds: float) -> float:
+    """Whole-job throughput: units of all ranks / slowest rank's time."""
+    return per_rank_units * world / max_seconds
+
+
+# ----------------------------------------------------------------------------- clocks (nvidia-smi)
+_CLK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+_REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+class ClockSampler:
+    """Samples nvidia-smi every 200 ms while the timed region runs (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={_CLK_FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self) -> dict:
+        rows = []
+        if self.path and os.path.exists(self.path):
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    rows.append((float(f[1]), float(f[2]), float(f[3]) if f[3] not in ("", "[N/A]") else 0.0,
+                                 f[5:9]))
+                except ValueError:
+                    continue
+            os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        load = [r for r in rows if r[2] > 300.0] or rows
+        reasons = sorted({_REASONS[i] for r in load for i, v in enumerate(r[3]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load),
+                "power_w_max": max(r[2] for r in rows)}
+
+
+# ----------------------------------------------------------------------------- workload
+def workload(name: str):
+    import synth
+    c = synth.CONFIGS[name]
+    prec = c.precisions[-1] if name != "paper" else "tf32"
+    return c, prec
+
+
+def make_inputs(c, prec: str, start: int, count: int):
+    """Seeded synthetic inputs of the config; global image indices start..start+count-1."""
+    import synth
+    st = "bf16" if prec == "bf16" else "f32"
+    phi = synth.make_phi(c.m, c.N, st)
+    x = synth.make_images(c.n, start, count, c.n_blobs, c.n_rects, c.texture_var)
+    y = synth.measure(phi, x, st)
+    params = synth.make_params().rounded(st)
+    return phi, x, y, params
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"bf16_tflops": d["bf16_tflops"], "bf16_tflops_sustained": d.get("bf16_tflops_sustained"),
+                "hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def traffic_for(kernel: str, config: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from a committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    e = d.get(f"{kernel}@{config}")
+    return e.get("bytes_per_launch") if e else None
+
+
+# ----------------------------------------------------------------------------- CPU oracle timing
+def oracle_sample(c, prec: str, budget_s: float, threads: int, max_images: int | None = None) -> dict:
+    """Time the fp64 oracle (as it stands) on the first images of the workload, in chunks of `threads`
+    images (OpenMP over images), until `budget_s` of wall time is used.  Returns images/s."""
+    import oracle
+    phi, x, y, params = make_inputs(c, prec, 0, threads)
+    done, t_total = 0, 0.0
+    while True:
+        t0 = time.perf_counter()
+        oracle.forward(y, phi, params, c.n, c.n, threads=threads)
+        t_total += time.perf_counter() - t0
+        done += y.shape[0]
+        if t_total >= budget_s or (max_images is not None and done >= max_images):
+            break
+    return {"value": done / t_total, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{done} images of workload {c.name} ({c.n}x{c.n}, M={c.m}) in chunks of {threads} "
+                      f"(one per OpenMP thread), fp64, {t_total:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    c, prec = workload(args.config)
+    threads = os.cpu_count() or 1
+    import oracle
+    phi, x, y, params = make_inputs(c, prec, 0, threads)
+    for _ in range(args.warmup):
+        oracle.forward(y[:1], phi, params, c.n, c.n, threads=1)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.forward(y, phi, params, c.n, c.n, threads=threads)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = args.steps * y.shape[0] / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(c, prec, 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{y.shape[0]} images of {c.name} per step (one per OpenMP thread), "
+                                       f"fp64 C oracle, {args.steps} steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(c, prec, world):
+    return {"workload": f"{c.name}: {c.n}x{c.n} images (N={c.N}), M={c.m} (M/N={c.m / c.N:.3g}), "
+                        f"batch {c.batch}/GPU, {prec}",
+            "n": c.n, "m": c.m, "batch_per_gpu": c.batch, "global_batch": c.batch * world,
+            "precision": prec, "layers": "Phi^T | 64@11x11x1+ReLU | 32@11x11x64+ReLU | 1@11x11x32",
+            "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
+            "l2": "inputs larger than L2: per-step working set h1+h2 = "
+                  f"{c.batch * c.N * 96 * (2 if prec == 'bf16' else 4) / 1e9:.2f} GB >> 126 MB L2"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU path)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1701_03891_b200 import DeepInverse, build as _b  # noqa: F401
+    import paper_1701_03891_b200.build as pb
+    pb.build()
+
+    c, prec = workload(args.config)
+    B = args.batch or c.batch
+    lo, hi = shard(rank, B)
+    phi, x, y, params = make_inputs(c, prec, lo, B)
+    ctx = DeepInverse(phi, params, c.n, c.n, prec, device=local, max_batch=B)
+    sdt = ctx.storage_dtype
+    y_dev = torch.from_numpy(y).to(device=dev, dtype=sdt)
+    xhat = torch.empty((B, c.n, c.n), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(max(args.warmup, 0)):
+        ctx.recover(y_dev, xhat)
+    torch.cuda.synchronize(dev)
+
+    # ---------------- device-resident timed region
+    ctx.set_profiling(True)
+    ctx.stage_times(reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(dev)
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ctx.recover(y_dev, xhat)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier(dev)
+    ms = ev0.elapsed_time(ev1)
+    stage_ms, calls = ctx.stage_times(reset=True)
+    ctx.set_profiling(False)
+    clocks = clk.summary()
+    launches = ctx.info()["launches_per_recover"] * args.steps
+    t_max = max_over_ranks(ms / 1e3, dev)
+    value = aggregate(B * args.steps, world, t_max)
+
+    # ---------------- end to end through the public host API (pinned y in, host x_hat out)
+    y_host = torch.from_numpy(y).to(dtype=sdt).pin_memory()
+    x_host = torch.empty((B, c.n, c.n), dtype=torch.float32).pin_memory()
+    for _ in range(max(args.warmup, 1)):
+        ctx.recover_host(y_host, x_host.numpy())
+    barrier(dev)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ctx.recover_host(y_host, x_host.numpy())
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_t = max_over_ranks(e0.elapsed_time(e1) / 1e3, dev)
+    e2e = {"value": aggregate(B * args.steps, world, e2e_t), "unit": UNIT,
+           "h2d_bytes_per_step": int(y_host.numel() * y_host.element_size()),
+           "d2h_bytes_per_step": int(x_host.numel() * x_host.element_size())}
+
+    # ---------------- dominant kernel roofline (conv layer 2), live CUDA events on the launching stream
+    pk = peaks()
+    conv2_ms = stage_ms[2] / max(calls, 1)
+    conv2_flop = CONV2_FLOP_PER_PX * B * c.N
+    achieved = conv2_flop / (conv2_ms / 1e3) / 1e12
+    if prec == "bf16":
+        peak = pk["bf16_tflops"]
+        peak_note = f"bf16 dense, burst, {pk['source']}"
+    elif prec == "tf32":
+        peak = pk["bf16_tflops"] / 2
+        peak_note = f"tf32 = measured bf16 burst x 1/2 (nominal 1.1 / 2.25 PF), {pk['source']}"
+    else:
+        peak = None
+        peak_note = "fp32 SIMT path"
+    kname = ctx.info()["stage_kernels"][2]
+    roof = {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if peak else None,
+            "frac_of_sustained": (achieved / pk["bf16_tflops_sustained"]) if (peak and prec == "bf16") else None,
+            "peak_note": peak_note, "traffic": traffic_for(kname, c.name),
+            "algorithmic": f"2*32*64*121 = {CONV2_FLOP_PER_PX} FLOP/pixel x {B * c.N} pixels per launch",
+            "launch_ms": conv2_ms}
+
+    per_step = ms / args.steps
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_over_ranks(per_step, dev), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "config": config_dict(c, prec, world), "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "clocks": clocks,
+            "stages_ms": {"proxy": stage_ms[0] / max(calls, 1), "conv1": stage_ms[1] / max(calls, 1),
+                          "conv2": stage_ms[2] / max(calls, 1), "conv3": stage_ms[3] / max(calls, 1)},
+            "path_tflops": (PATH_FLOP_PER_PX + 2 * c.m) * c.N * B / (per_step / 1e3) / 1e12,
+            "per_gpu_images_s": B / (per_step / 1e3)}
+
+    # ---------------- CPU baseline (oracle as it stands), rank 0 at N=1 only
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        line["cpu_baseline"] = oracle_sample(c, prec, args.cpu_budget, threads)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="lowrate", choices=["tiny", "paper", "lowrate", "larger", "stress"])
+    ap.add_argument("--batch", type=int, default=0, help="override the per-GPU batch (default: the config's)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle time for cpu_baseline")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

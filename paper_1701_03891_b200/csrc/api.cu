@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <array>
 #include <new>
 #include <vector>
 
@@ -90,10 +91,10 @@ struct di_ctx_s {
   CUtensorMap tmPt{}, tmH1{};
   int last_launches = 0;
   bool profiling = false;
-  cudaEvent_t ev[5] = {};
+  std::vector<std::array<cudaEvent_t, 5>> evpool;  // one set of stage-boundary events per profiled call
+  int ev_used = 0;                                  // sets recorded since the last di_stage_times
   float stage_ms[4] = {0, 0, 0, 0};
   int prof_calls = 0;
-  bool prof_pending = false;
 };
 
 namespace {
@@ -198,8 +199,9 @@ void free_ctx(di_ctx c) {
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
     if (p) cudaFree(p);
-  for (auto& e : c->ev)
-    if (e) cudaEventDestroy(e);
+  for (auto& set : c->evpool)
+    for (auto e : set)
+      if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -212,8 +214,17 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
   const int fm = (c->flags & DI_FLAG_FULLMAP_BIAS) ? 1 : 0;
   const int relu3 = (c->flags & DI_FLAG_FINAL_RELU) ? 1 : 0;
   int launches = 0;
+  cudaEvent_t* ev = nullptr;
+  if (c->profiling) {
+    if (c->ev_used == (int)c->evpool.size()) {
+      std::array<cudaEvent_t, 5> set{};
+      for (auto& e : set) CUDA_TRY(cudaEventCreate(&e));
+      c->evpool.push_back(set);
+    }
+    ev = c->evpool[c->ev_used++].data();
+  }
   auto mark = [&](int i) {
-    if (c->profiling) cudaEventRecord(c->ev[i], st);
+    if (ev) cudaEventRecord(ev[i], st);
   };
   mark(first);
   if (first <= 0 && 0 <= last) {
@@ -265,7 +276,6 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
     ++launches;
   }
   mark(4);
-  if (c->profiling) c->prof_pending = true;
   c->last_launches = launches;
   return DI_OK;
 }
@@ -410,12 +420,6 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     }
     STEP(encode_h1(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
   }
-  for (auto& e : c->ev) {
-    if (cudaEventCreate(&e) != cudaSuccess) {
-      free_ctx(c);
-      return fail(DI_ERR_CUDA, "cudaEventCreate failed");
-    }
-  }
 #undef STEP
   *out = c;
   return DI_OK;
@@ -484,14 +488,16 @@ di_status di_set_profiling(di_ctx c, int enable) {
 
 di_status di_stage_times(di_ctx c, float ms[4], int* calls, int reset) {
   if (!c || !ms) return fail(DI_ERR_ARG, "NULL argument");
-  if (c->prof_pending) {
-    CUDA_TRY(cudaEventSynchronize(c->ev[4]));
-    for (int i = 0; i < 4; ++i) {
-      float t = 0.f;
-      if (cudaEventElapsedTime(&t, c->ev[i], c->ev[i + 1]) == cudaSuccess) c->stage_ms[i] += t;
+  if (c->ev_used > 0) {
+    CUDA_TRY(cudaEventSynchronize(c->evpool[c->ev_used - 1][4]));
+    for (int k = 0; k < c->ev_used; ++k) {
+      for (int i = 0; i < 4; ++i) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, c->evpool[k][i], c->evpool[k][i + 1]) == cudaSuccess) c->stage_ms[i] += t;
+      }
+      c->prof_calls++;
     }
-    c->prof_calls++;
-    c->prof_pending = false;
+    c->ev_used = 0;
   }
   for (int i = 0; i < 4; ++i) ms[i] = c->stage_ms[i];
   if (calls) *calls = c->prof_calls;
