@@ -1,0 +1,75 @@
+"""Multi-process host logic of the batch-sharded path (bench.py), world_size 2 over gloo on CPU.
+
+The GPU path shards images across ranks with no data-path collective; what the ranks
+share is the sharding rule, the max-over-ranks timing and the seeded inputs, which must be identical
+however the batch is split.
+"""
+import os
+import socket
+
+import numpy as np
+import torch.multiprocessing as mp
+
+import bench
+import synth
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r, w, _ = bench.dist_env()
+        per = 3
+        lo, hi = bench.shard(r, per)
+        c = synth.CONFIGS["tiny"]
+        x = synth.make_images(c.n, lo, hi - lo, c.n_blobs, c.n_rects)
+        # max over ranks of a per-rank "device time"
+        t = bench.max_over_ranks(1.0 + r)
+        bench.barrier()
+        # gather the shards to rank 0 (checking only, as in the GPU harness)
+        xt = torch.from_numpy(x)
+        parts = [torch.empty_like(xt) for _ in range(w)]
+        dist.all_gather(parts, xt)
+        if r == 0:
+            q.put((lo, hi, t, bench.aggregate(per, w, t), torch.cat(parts).numpy()))
+        else:
+            q.put((lo, hi, t, None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharding_timing_and_gather():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ranges = sorted((a, b) for a, b, *_ in res)
+    assert ranges == [(0, 3), (3, 6)], "contiguous blocks of global image indices"
+    assert all(t == 2.0 for _, _, t, _, _ in res), "max over ranks"
+    agg, gathered = next((a, g) for *_, a, g in res if a is not None)
+    assert agg == 6 / 2.0, "whole-job throughput = all ranks' units / slowest rank"
+    c = synth.CONFIGS["tiny"]
+    whole = synth.make_images(c.n, 0, 6, c.n_blobs, c.n_rects)
+    assert np.array_equal(gathered, whole), "sharded inputs identical to the unsharded batch"
+
+
+def test_single_process_defaults():
+    assert bench.dist_env()[1] >= 1
+    assert bench.shard(0, 4096) == (0, 4096)
+    assert bench.max_over_ranks(3.5) == 3.5
