@@ -846,6 +846,150 @@ static void t10() {
   cudaFree(dA), cudaFree(dB), cudaFree(dD);
 }
 
+
+// ------------------------------------------------------------------------ t11 / t12: narrow swizzles
+// Rows of RB bytes (RB = 32 -> SWIZZLE_32B, 64 -> SWIZZLE_64B, 128 -> SWIZZLE_128B), K = RB/2 bf16 per row.
+// Swizzle is applied on absolute smem address bits: 16-B chunk bits [4, 4+log2(RB/16)) ^= bits [7, ...).
+__device__ __forceinline__ uint32_t swz_off(uint32_t off, int RB) {
+  const uint32_t mask = (RB == 128) ? 7u : (RB == 64 ? 3u : 1u);
+  return off ^ (((off >> 7) & mask) << 4);
+}
+__device__ void st_swz(uint8_t* base, const __nv_bfloat16* g, int rows, int RB) {
+  const int cpr = RB / 16;
+  for (int idx = threadIdx.x; idx < rows * cpr; idx += blockDim.x) {
+    int r = idx / cpr, c = idx % cpr;
+    uint4 v = reinterpret_cast<const uint4*>(g)[idx];
+    *reinterpret_cast<uint4*>(base + swz_off(r * RB + c * 16, RB)) = v;
+  }
+}
+__host__ __device__ inline uint32_t layout_of(int RB) { return RB == 128 ? 2u : (RB == 64 ? 4u : 6u); }
+
+// D[128][N] = A[a0 : a0+128][K] * B[N][K]^T, A and B in the RB-swizzled layout
+__global__ void k_mma_swz(const __nv_bfloat16* A, int arows, const __nv_bfloat16* B, int N, int a0, int RB,
+                          float* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;             // up to 256 rows x 128 B = 32 KB
+  uint8_t* sB = smem + 32768;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  int w = threadIdx.x >> 5;
+  st_swz(sA, A, arows, RB);
+  st_swz(sB, B, N, RB);
+  fence_async_smem();
+  if (w == 0) tmem_alloc<512>(&tslot), tmem_relinquish();
+  if (threadIdx.x == 32) mbar_init(&bar, 1), fence_mbar_init();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tb = tslot;
+  if (threadIdx.x == 0) {
+    uint32_t idesc = idesc_f32acc(1, 128, N);
+    const int nk = RB / 32;
+    const uint32_t sbo = 8 * RB;
+    for (int k = 0; k < nk; ++k) {
+      uint32_t sa = smem_u32(sA) + a0 * RB + k * 32;
+      uint32_t sb = smem_u32(sB) + k * 32;
+      umma_f16_ss(tb, smem_desc(sa, 16, sbo, layout_of(RB)), smem_desc(sb, 16, sbo, layout_of(RB)), idesc, k > 0);
+    }
+    umma_commit(&bar);
+  }
+  wait_bounded(&bar, 0);
+  tc_fence_after();
+  dump_tmem(tb, out, N);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (w == 0) tmem_dealloc<512>(tb);
+}
+
+static void t11() {
+  for (int RB : {32, 64}) {
+    const int K = RB / 2;
+    std::vector<float> Af, Bf;
+    auto A = randbf(256 * K, 11 + RB, Af);
+    auto B = randbf(256 * K, 12 + RB, Bf);
+    __nv_bfloat16 *dA = dup(A), *dB = dup(B);
+    float* dD;
+    CK(cudaMalloc(&dD, 128 * 256 * 4));
+    CK(cudaFuncSetAttribute(k_mma_swz, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024));
+    std::vector<float> D(128 * 256);
+    for (int N : {16, 32, 64, 256})
+      for (int a0 : {0, 1, 3, 5, 7, 8, 13, 74, 111}) {
+        if (a0 + 128 > 256) continue;
+        k_mma_swz<<<1, 128, 65536 + 1024>>>(dA, 256, dB, N, a0, RB, dD);
+        if (check_err("t11")) return;
+        CK(cudaMemcpy(D.data(), dD, 128 * N * 4, cudaMemcpyDeviceToHost));
+        double e = 0;
+        for (int m = 0; m < 128; ++m)
+          for (int n = 0; n < N; ++n) {
+            double s = 0;
+            for (int k = 0; k < K; ++k) s += (double)Af[(a0 + m) * K + k] * Bf[n * K + k];
+            e = fmax(e, fabs(s - D[m * N + n]));
+          }
+        printf("{\"test\":\"t11_swizzle_window\",\"RB\":%d,\"N\":%d,\"a0\":%d,\"maxerr\":%.3g,\"pass\":%s}\n", RB, N,
+               a0, e, e < 1e-3 ? "true" : "false");
+      }
+    cudaFree(dA), cudaFree(dB), cudaFree(dD);
+  }
+}
+
+// SS throughput with RB-swizzled operands: M=128, N, K = RB/2 per "block" (RB/32 MMAs of K=16)
+__global__ void __launch_bounds__(128, 1) k_thr_swz(int N, int RB, int iters, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  int w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  fence_async_smem();
+  if (w == 0) tmem_alloc<512>(&tslot), tmem_relinquish();
+  if (threadIdx.x == 32) mbar_init(&bar, 1), fence_mbar_init();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tb = tslot;
+  if (threadIdx.x == 0) {
+    uint32_t idesc = idesc_f32acc(1, 128, N);
+    const int nk = RB / 32;
+    const uint32_t sbo = 8 * RB;
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it)
+      for (int k = 0; k < nk; ++k) {
+        uint32_t sa = smem_u32(smem) + (it & 7) * RB * 3 + k * 32;     // shifting A windows, as in the convs
+        uint32_t sb = smem_u32(smem) + 32768 + k * 32;
+        umma_f16_ss(tb, smem_desc(sa, 16, sbo, layout_of(RB)), smem_desc(sb, 16, sbo, layout_of(RB)), idesc, 1);
+      }
+    umma_commit(&bar);
+    wait_bounded(&bar, 0);
+    cyc[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (w == 0) tmem_dealloc<512>(tb);
+}
+
+static void t12(int nsm) {
+  unsigned long long* dc;
+  CK(cudaMalloc(&dc, nsm * 8));
+  CK(cudaFuncSetAttribute(k_thr_swz, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024));
+  for (int RB : {32, 64, 128})
+    for (int N : {16, 32, 64, 128, 256}) {
+      const int nk = RB / 32;
+      int iters = 2048 * 256 / N / nk;
+      k_thr_swz<<<nsm, 128, 65536 + 1024>>>(N, RB, 16, dc);
+      k_thr_swz<<<nsm, 128, 65536 + 1024>>>(N, RB, iters, dc);
+      if (check_err("t12")) return;
+      std::vector<unsigned long long> hc(nsm);
+      CK(cudaMemcpy(hc.data(), dc, nsm * 8, cudaMemcpyDeviceToHost));
+      double cmax = 0;
+      for (int i = 0; i < nsm; ++i) cmax = fmax(cmax, (double)hc[i]);
+      double mmas = (double)iters * nk;
+      printf("{\"test\":\"t12_ss_throughput\",\"RB\":%d,\"N\":%d,\"cyc_per_mma\":%.2f,\"floor_cyc\":%.1f,"
+             "\"smem_B_per_clk\":%.1f}\n", RB, N, cmax / mmas, 128.0 * N / 256.0, (128.0 * 32 + N * 32.0) / (cmax / mmas));
+    }
+  cudaFree(dc);
+}
+
 int main(int argc, char** argv) {
   int dev = 0, nsm = 0;
   CK(cudaSetDevice(dev));
@@ -862,5 +1006,7 @@ int main(int argc, char** argv) {
   if (on("t7")) t7(nsm);
   if (on("t9")) t9(nsm);
   if (on("t10")) t10();
+  if (on("t11")) t11();
+  if (on("t12")) t12(nsm);
   return 0;
 }
