@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <array>
 #include <new>
@@ -82,13 +83,15 @@ struct di_ctx_s {
   float* wx2 = nullptr;         // [64][11][11][32]
   float* wx3 = nullptr;         // [32][11][11][1]
   void* wp2 = nullptr;          // conv2 tensor-core weight blocks (BF16 mode)
+  void* wp1 = nullptr;          // conv1 tensor-core weight blocks (BF16 mode, SWIZZLE_32B image)
+  void* wp3 = nullptr;          // conv3 tensor-core weight blocks (BF16 mode, SWIZZLE_64B image)
   float *b1 = nullptr, *b2 = nullptr, *b3 = nullptr;  // per-channel or cropped full maps (nullptr = zero)
   void *xt = nullptr, *h1 = nullptr, *h2 = nullptr, *ystage = nullptr;
   void* yhost_dev = nullptr;    // di_recover_host staging
   size_t yhost_bytes = 0;
   float* xhost_dev = nullptr;
   long long ws_bytes = 0;
-  CUtensorMap tmPt{}, tmH1{};
+  CUtensorMap tmPt{}, tmH1{}, tmH2{};
   int last_launches = 0;
   bool profiling = false;
   std::vector<std::array<cudaEvent_t, 5>> evpool;  // one set of stage-boundary events per profiled call
@@ -125,6 +128,20 @@ di_status encode_h1(CUtensorMap* map, const void* h1, int batch, int n1, int n2)
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h1) failed: %d", (int)r);
+  return DI_OK;
+}
+
+di_status encode_h2(CUtensorMap* map, const void* h2, int batch, int n1, int n2) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {32, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {32 * 2, (cuuint64_t)n2 * 32 * 2, (cuuint64_t)n1 * n2 * 32 * 2};
+  cuuint32_t box[4] = {32, (cuuint32_t)di::conv3_tc_box_cols(n2), (cuuint32_t)di::conv3_tc_box_rows(), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(h2), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h2) failed: %d", (int)r);
   return DI_OK;
 }
 
@@ -180,6 +197,36 @@ std::vector<uint16_t> conv2_tc_pack(const std::vector<float>& wx2) {
   return out;
 }
 
+// conv1 tensor-core blocks: block u (2 KB) = 64 filter rows x 16 column taps (v >= 11 zero), bf16, SWIZZLE_32B
+// image (16-B chunk h of row f at f*32 + ((h ^ ((f >> 2) & 1)) << 4)).
+std::vector<uint16_t> conv1_tc_pack(const std::vector<float>& wx1) {
+  std::vector<uint16_t> out(11 * 2048 / 2, 0);
+  uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
+  for (int u = 0; u < K; ++u)
+    for (int f = 0; f < 64; ++f)
+      for (int v = 0; v < 16; ++v) {
+        const uint16_t h = v < K ? f2bf(wx1[((size_t)f * K + u) * K + v]) : 0;
+        const size_t off = (size_t)u * 2048 + f * 32 + ((((size_t)v / 8) ^ ((f >> 2) & 1)) << 4) + (v % 8) * 2;
+        std::memcpy(base + off, &h, 2);
+      }
+  return out;
+}
+
+// conv3 tensor-core blocks: block u (2 KB) = 32 rows (row v < 11: tap v; else zero) x 32 input channels, bf16,
+// SWIZZLE_64B image (16-B chunk h of row r at r*64 + ((h ^ ((r >> 1) & 3)) << 4)).
+std::vector<uint16_t> conv3_tc_pack(const std::vector<float>& wx3) {
+  std::vector<uint16_t> out(11 * 2048 / 2, 0);
+  uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
+  for (int u = 0; u < K; ++u)
+    for (int r = 0; r < 32; ++r)
+      for (int c = 0; c < 32; ++c) {
+        const uint16_t h = r < K ? f2bf(wx3[((size_t)c * K + u) * K + r]) : 0;
+        const size_t off = (size_t)u * 2048 + r * 64 + ((((size_t)c / 8) ^ ((r >> 1) & 3)) << 4) + (c % 8) * 2;
+        std::memcpy(base + off, &h, 2);
+      }
+  return out;
+}
+
 // bias: per-channel [cout] or the window of the full map [cout][n1+10][n2+10] that S keeps, as [n1][n2][cout]
 di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n1, int n2, long long* ws) {
   *dst = nullptr;
@@ -195,7 +242,7 @@ di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n
 
 void free_ctx(di_ctx c) {
   if (!c) return;
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -250,7 +297,10 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
   }
   mark(1);
   if (first <= 1 && 1 <= last) {
-    CUDA_TRY(di::launch_conv1_simt(xt, bf16, c->wx1, c->b1, fm, h1, batch, c->n1, c->n2, st));
+    if (bf16)
+      CUDA_TRY(di::launch_conv1_tc(xt, c->wp1, c->b1, fm, h1, batch, c->n1, c->n2, c->num_sms, st));
+    else
+      CUDA_TRY(di::launch_conv1_simt(xt, bf16, c->wx1, c->b1, fm, h1, batch, c->n1, c->n2, st));
     ++launches;
   }
   mark(2);
@@ -272,7 +322,18 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
   }
   mark(3);
   if (first <= 3 && 3 <= last) {
-    CUDA_TRY(di::launch_conv3_simt(h2, bf16, c->wx3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, st));
+    if (bf16) {
+      CUtensorMap tm;
+      const CUtensorMap* tmp = &c->tmH2;
+      if (h2 != c->h2 || batch != c->max_batch) {
+        di_status s = encode_h2(&tm, h2, batch, c->n1, c->n2);
+        if (s != DI_OK) return s;
+        tmp = &tm;
+      }
+      CUDA_TRY(di::launch_conv3_tc(tmp, c->wp3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, c->num_sms, st));
+    } else {
+      CUDA_TRY(di::launch_conv3_simt(h2, bf16, c->wx3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, st));
+    }
     ++launches;
   }
   mark(4);
@@ -390,6 +451,10 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     if (bf16) {
       auto p2 = conv2_tc_pack(w2);
       STEP(upload(&c->wp2, p2.data(), p2.size() * 2, &c->ws_bytes));
+      auto p1 = conv1_tc_pack(w1);
+      STEP(upload(&c->wp1, p1.data(), p1.size() * 2, &c->ws_bytes));
+      auto p3 = conv3_tc_pack(w3);
+      STEP(upload(&c->wp3, p3.data(), p3.size() * 2, &c->ws_bytes));
     }
     STEP(upload_bias(&c->b1, a->b1, C1, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b2, a->b2, C2, fm, a->n1, a->n2, &c->ws_bytes));
@@ -419,6 +484,12 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       return fail(DI_ERR_CUDA, "setup_conv2_tc: %s", cudaGetErrorString(e));
     }
     STEP(encode_h1(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
+    e = di::setup_conv13_tc(a->n2);
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return fail(DI_ERR_CUDA, "setup_conv13_tc: %s", cudaGetErrorString(e));
+    }
+    STEP(encode_h2(&c->tmH2, c->h2, a->max_batch, a->n1, a->n2));
   }
 #undef STEP
   *out = c;
@@ -474,9 +545,9 @@ di_status di_get_info(di_ctx c, di_info* info) {
   info->workspace_bytes = c->ws_bytes;
   const bool bf16 = c->prec == DI_PREC_BF16;
   info->stage_kernels[0] = c->prec == DI_PREC_FP32 ? "k_proxy_f32" : (bf16 ? "k_proxy_tc<bf16>" : "k_proxy_tc<tf32>");
-  info->stage_kernels[1] = "k_conv_wide<conv1>";
+  info->stage_kernels[1] = bf16 ? "k_conv1_tc" : "k_conv_wide<conv1>";
   info->stage_kernels[2] = bf16 ? "k_conv2_tc" : "k_conv_wide<conv2,f32>";
-  info->stage_kernels[3] = "k_conv3";
+  info->stage_kernels[3] = bf16 ? "k_conv3_tc" : "k_conv3";
   return DI_OK;
 }
 

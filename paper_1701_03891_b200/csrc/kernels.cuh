@@ -13,6 +13,10 @@ constexpr int C2_ROWS = 6;                  // output rows per work unit
 constexpr int C2_KBLOCKS = 33;              // 11 tap rows x 3 column-tap groups of 4
 constexpr int C2_KBLOCK_BYTES = 128 * 128;  // 128 rows (4 taps x 32 filters) x 64 ch x bf16
 
+// conv1 / conv3 tensor-core geometry (k_conv13_tc.cu)
+constexpr int C1TC_ROWS = 8;                // conv1 output rows per work unit
+constexpr int C3TC_ROWS = 6;                // conv3 output rows per work unit
+
 // stage 0: lifting layer x_tilde = Phi^T y
 cudaError_t setup_proxy_tc();
 size_t proxy_tc_smem_bytes();
@@ -28,6 +32,10 @@ cudaError_t launch_stage_y(const void* y, long long ldy, int m, int kpad, int ba
 cudaError_t launch_conv1_simt(const void* xt, bool bf16, const float* wx, const float* bias, int fullmap, void* h1,
                               int batch, int n1, int n2, cudaStream_t st);
 
+cudaError_t setup_conv13_tc(int n2);
+cudaError_t launch_conv1_tc(const void* xt, const void* w1pack, const float* bias, int fullmap, void* h1, int batch,
+                            int n1, int n2, int num_sms, cudaStream_t st);
+
 // stage 2: conv layer 2 (64 -> 32, ReLU)
 cudaError_t setup_conv2_tc(int n2);
 size_t conv2_tc_smem_bytes(int n2);
@@ -41,5 +49,10 @@ cudaError_t launch_conv2_simt_f32(const float* h1, const float* wx, const float*
 // stage 3: conv layer 3 (32 -> 1, optional ReLU)
 cudaError_t launch_conv3_simt(const void* h2, bool bf16, const float* wx, const float* bias, int fullmap, int relu,
                               float* xhat, int batch, int n1, int n2, cudaStream_t st);
+
+int conv3_tc_box_rows();
+int conv3_tc_box_cols(int n2);
+cudaError_t launch_conv3_tc(const CUtensorMap* tmH2, const void* w3pack, const float* bias, int fullmap, int relu,
+                            float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st);
 
 }  // namespace di

@@ -49,6 +49,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// wait with back-off: for producer-side waits that are not on the critical path; keeps the spinning warp
+// from stealing issue slots from the epilogue warp that shares its SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
+
 // ----------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -142,6 +148,21 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+
+// weight-stationary MMA (.ws): M in {32, 64, 128}, N in {64, 128, 256}; no collector reuse.
+// D layout in TMEM (verified by tools/ladder.cu t7): M=32 -> quadrant q holds columns [q*N/4, (q+1)*N/4) of D
+// in N/4 TMEM columns (lane 32q+m = row m); M=64 -> quadrants {0,1} hold rows 0..63 for D columns [0, N/2),
+// quadrants {2,3} rows 0..63 for columns [N/2, N), in N/2 TMEM columns.
+__device__ __forceinline__ void umma_ws_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.ws.cta_group::1.kind::f16.collector::b0::discard [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // all prior tcgen05.mma of this thread -> arrive (once) on an mbarrier when complete
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -15,6 +15,6 @@ if [ "${SKIP_NCU:-0}" != 1 ]; then
   $CMD > $OUT/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
   $CMD > $OUT/plain2.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_conv2_tc} -s ${NCU_SKIP:-3} -c 1 \
-      -o $OUT/prof_conv2 $CMD > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -3 $OUT/ncu_full.log
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_conv2_tc} -s ${NCU_SKIP:-3} -c ${NCU_COUNT:-1} \
+      -o $OUT/prof_${NCU_NAME:-conv2} $CMD > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -3 $OUT/ncu_full.log
 fi

@@ -990,6 +990,124 @@ static void t12(int nsm) {
   cudaFree(dc);
 }
 
+// t13: A = aligned SW128 weights (M=128), B = RB-swizzled activations at shifted windows (the conv mapping)
+__global__ void __launch_bounds__(128, 1) k_thr_b(int N, int RB, int iters, int shift, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  int w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 98304 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  fence_async_smem();
+  if (w == 0) tmem_alloc<512>(&tslot), tmem_relinquish();
+  if (threadIdx.x == 32) mbar_init(&bar, 1), fence_mbar_init();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tb = tslot;
+  if (threadIdx.x == 0) {
+    uint32_t idesc = idesc_f32acc(1, 128, N);
+    const uint32_t sbo = 8 * RB;
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int k = it & 3;
+      uint32_t sa = smem_u32(smem) + k * 32;
+      uint32_t sb = smem_u32(smem) + 16384 + (shift ? (it % 11) * 74 * RB : 0) + (k % (RB / 32)) * 32;
+      umma_f16_ss(tb, smem_desc(sa, 16, 1024, 2), smem_desc(sb, 16, sbo, layout_of(RB)), idesc, 1);
+    }
+    umma_commit(&bar);
+    wait_bounded(&bar, 0);
+    cyc[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (w == 0) tmem_dealloc<512>(tb);
+}
+static void t13(int nsm) {
+  unsigned long long* dc;
+  CK(cudaMalloc(&dc, nsm * 8));
+  CK(cudaFuncSetAttribute(k_thr_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 98304 + 1024));
+  for (int RB : {32, 64, 128})
+    for (int N : {64, 128, 256})
+      for (int shift : {0, 1}) {
+        if (16384 + 10 * 74 * RB + N * RB > 98304) continue;
+        int iters = 4096 * 256 / N;
+        k_thr_b<<<nsm, 128, 98304 + 1024>>>(N, RB, 16, shift, dc);
+        k_thr_b<<<nsm, 128, 98304 + 1024>>>(N, RB, iters, shift, dc);
+        if (check_err("t13")) return;
+        std::vector<unsigned long long> hc(nsm);
+        CK(cudaMemcpy(hc.data(), dc, nsm * 8, cudaMemcpyDeviceToHost));
+        double cmax = 0;
+        for (int i = 0; i < nsm; ++i) cmax = fmax(cmax, (double)hc[i]);
+        printf("{\"test\":\"t13_B_swizzle_throughput\",\"RB\":%d,\"N\":%d,\"shift\":%d,\"cyc_per_mma\":%.2f,"
+               "\"floor_cyc\":%.1f}\n", RB, N, shift, cmax / iters, 128.0 * N / 256.0);
+      }
+  cudaFree(dc);
+}
+
+// t14: like t13 with `nacc` accumulators interleaved (is the per-MMA floor a D-dependency latency?)
+__global__ void __launch_bounds__(128, 1) k_thr_acc(int N, int RB, int iters, int nacc, int mode,
+                                                     unsigned long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  int w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 200704 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  fence_async_smem();
+  if (w == 0) tmem_alloc<512>(&tslot), tmem_relinquish();
+  if (threadIdx.x == 32) mbar_init(&bar, 1), fence_mbar_init();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tb = tslot;
+  if (threadIdx.x == 0) {
+    uint32_t idesc = idesc_f32acc(1, 128, N);
+    const uint32_t sbo = 8 * RB;
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem) + 16384;
+    unsigned long long t0 = clock64();
+    int sh = 0;
+    for (int it = 0; it < iters; ++it) {
+      const int k = it & 3;
+      const uint32_t sa = a0 + k * 32;
+      const uint32_t sb = b0 + (mode ? sh * RB : 0) + (k & (RB / 32 - 1)) * 32;
+      if (++sh == 11 * 74) sh = 0;
+      const uint32_t d = tb + (uint32_t)((it % nacc) * N);
+      umma_f16_ss(d, smem_desc(sa, 16, 1024, 2), smem_desc(sb, 16, sbo, layout_of(RB)), idesc, 1);
+    }
+    umma_commit(&bar);
+    wait_bounded(&bar, 0);
+    cyc[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (w == 0) tmem_dealloc<512>(tb);
+}
+static void t14(int nsm) {
+  unsigned long long* dc;
+  CK(cudaMalloc(&dc, nsm * 8));
+  const int SM = 200704;
+  CK(cudaFuncSetAttribute(k_thr_acc, cudaFuncAttributeMaxDynamicSharedMemorySize, SM + 1024));
+  for (int RB : {32, 64, 128})
+    for (int N : {32, 64, 128, 256})
+      for (int nacc : {1, 2, 4})
+        for (int mode : {0, 1}) {
+          if (nacc * N > 512) continue;
+          if (16384 + 11 * 74 * RB + 256 * RB > SM) continue;
+          int iters = 4096 * 256 / N;
+          k_thr_acc<<<nsm, 128, SM + 1024>>>(N, RB, 16, nacc, mode, dc);
+          k_thr_acc<<<nsm, 128, SM + 1024>>>(N, RB, iters, nacc, mode, dc);
+          if (check_err("t14")) return;
+          std::vector<unsigned long long> hc(nsm);
+          CK(cudaMemcpy(hc.data(), dc, nsm * 8, cudaMemcpyDeviceToHost));
+          double cmax = 0;
+          for (int i = 0; i < nsm; ++i) cmax = fmax(cmax, (double)hc[i]);
+          printf("{\"test\":\"t14\",\"RB\":%d,\"N\":%d,\"nacc\":%d,\"shift\":%d,\"cyc_per_mma\":%.2f,\"floor\":%.0f}\n",
+                 RB, N, nacc, mode, cmax / iters, 128.0 * N / 256.0);
+        }
+  cudaFree(dc);
+}
+
 int main(int argc, char** argv) {
   int dev = 0, nsm = 0;
   CK(cudaSetDevice(dev));
@@ -1008,5 +1126,7 @@ int main(int argc, char** argv) {
   if (on("t10")) t10();
   if (on("t11")) t11();
   if (on("t12")) t12(nsm);
+  if (on("t13")) t13(nsm);
+  if (on("t14")) t14(nsm);
   return 0;
 }
