@@ -18,6 +18,8 @@ HEADERS = ["sm100.cuh", "kernels.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", "-diag-suppress", "177"]
+# extra flags for experiments only (e.g. DI_NVCC_EXTRA=-DDI_PROF_CONV2 for the conv2 issuer cycle breakdown)
+FLAGS += os.environ.get("DI_NVCC_EXTRA", "").split()
 
 
 def _stale(target: str, deps: list[str]) -> bool:

@@ -15,8 +15,8 @@
 // (one tcgen05.ld per warp), sums the 4 quadrants through shared memory, adds the bias, applies
 // ReLU, rounds to bf16 and stores NHWC h2 with 16-B coalesced stores.
 //
-// Work unit = (image b, 6 output rows from r0, <=64 output columns from c0).  The strip of the unit
-// ((6+10) rows x (W+10) columns x 64 ch, bf16) is loaded by ONE 4-D TMA box whose out-of-bounds
+// Work unit = (image b, R = 5 output rows from r0, <=64 output columns from c0).  The strip of the unit
+// ((R+10) rows x (W+10) columns x 64 ch, bf16) is loaded by ONE 4-D TMA box whose out-of-bounds
 // elements are zero: that is the zero padding of Eq. (1) at the image border.
 // Positions are linear in the padded strip (pitch P = W+10); tiles of 256 positions overlap by 3.
 //
@@ -25,6 +25,9 @@
 // TMEM: two 256-column fp32 accumulators (double buffer: MMA of tile i+1 overlaps the epilogue of tile i).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "sm100.cuh"
@@ -36,10 +39,13 @@ constexpr int R = C2_ROWS;             // output rows per unit (6)
 constexpr int WSEG = 64;               // output columns per unit (max)
 constexpr int NT = 256;                // UMMA N per tile
 constexpr int OUT_PER_TILE = NT - 3;   // 253 complete output positions per tile
-constexpr int WSTAGES = 3;
+constexpr int WSTAGES = 4;             // weight ring depth (L2 latency of a 16-KB bulk copy ~ 2 K-blocks)
 constexpr int KBLOCKS = C2_KBLOCKS;    // 33
 constexpr uint32_t WBYTES = C2_KBLOCK_BYTES;  // 16 KB
 constexpr int GUARD_ROWS = 24;
+constexpr int HALF_ROWS = (R + 10 + 1) / 2;  // strip rows of half A (half B: R + 10 - HALF_ROWS)
+constexpr int SPS = 36;                  // epilogue transpose row stride (floats): conflict-free float4 reads
+constexpr int ECH = 16;                  // epilogue chunk: output positions per TMEM load
 
 struct Geo {
   int n1, n2, wseg, P, nrb, ncs, units;
@@ -50,13 +56,18 @@ __host__ __device__ inline int strip_rows_bytes(int P) { return (R + 10) * P * 1
 
 // last chunk of a full tile (c0 = 224, at most 29 outputs): columns c0+q .. c0+q+28 <= 255, loaded as
 // 16 + 8 + 4 + 1 columns at fixed register offsets (no dynamic register indexing)
-__device__ __forceinline__ void ld_tail29(uint32_t taddr, uint32_t* r) {
-  tmem_ld16(taddr, r);
-  tmem_ld8(taddr + 16, r + 16);
-  tmem_ld4(taddr + 24, r + 24);
-  tmem_ld1(taddr + 28, r + 28);
+// last 16-column chunk of a full tile (c0 = 240, at most 13 outputs): columns c0+q .. c0+q+12 <= 255
+__device__ __forceinline__ void ld_tail13(uint32_t taddr, uint32_t* r) {
+  tmem_ld8(taddr, r);
+  tmem_ld4(taddr + 8, r + 8);
+  tmem_ld1(taddr + 12, r + 12);
 }
 
+
+// SPLIT = true: the strip is loaded as two halves (rows 0..7 / 8..15) by a dedicated producer thread, with
+// one full/empty barrier pair per half, so the next unit's half A streams in while the last tile of this unit
+// only reads half B (and half B while the first K-blocks of the next unit only read half A).
+template <bool SPLIT>
 __global__ void __launch_bounds__(256, 1)
     k_conv2_tc(const __grid_constant__ CUtensorMap tmH1, const __nv_bfloat16* __restrict__ wpack,
                const float* __restrict__ bias, int fullmap, Geo g, __nv_bfloat16* __restrict__ h2) {
@@ -66,16 +77,15 @@ __global__ void __launch_bounds__(256, 1)
   const int strip_alloc = (strip_bytes + GUARD_ROWS * 128 + 1023) & ~1023;
   uint8_t* strip = smem;
   uint8_t* wst = smem + strip_alloc;
-  float* sP = reinterpret_cast<float*>(wst + WSTAGES * WBYTES);  // [4][32][32]
+  float* sP = reinterpret_cast<float*>(wst + WSTAGES * WBYTES);  // [4][32 positions][SPS]
 
-  __shared__ uint64_t strip_full, strip_empty, wfull[WSTAGES], wempty[WSTAGES], tfull[2], tempty[2];
+  __shared__ uint64_t hfull[2], hempty[2], wfull[WSTAGES], wempty[WSTAGES], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
   const int warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmH1);
-    mbar_init(&strip_full, 1);
-    mbar_init(&strip_empty, 1);
+    for (int h = 0; h < 2; ++h) mbar_init(&hfull[h], 1), mbar_init(&hempty[h], 1);
     for (int s = 0; s < WSTAGES; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], 1);
     for (int s = 0; s < 2; ++s) mbar_init(&tfull[s], 1), mbar_init(&tempty[s], 4);
     fence_mbar_init();
@@ -93,41 +103,79 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = tslot;
 
   const int per_img = g.nrb * g.ncs;
+  const int half_bytes = HALF_ROWS * g.P * 128;
+  const int halfpos = HALF_ROWS * g.P;    // first strip position of half B
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------ producer
-      int wk = 0, it = 0;
+    if (lane == 0) {  // ------------------------------------------------ weight (+ unsplit strip) producer
+      uint32_t wk = 0;                    // weight K-blocks issued (stage wk % WSTAGES)
+      int it = 0;
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
         const int b = u / per_img, rem = u - b * per_img;
         const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
         const int rows = min(R, g.n1 - r0);
         const int L = (rows - 1) * g.P + g.wseg;
         const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
-        if (it > 0) mbar_wait(&strip_empty, (it - 1) & 1);
-        mbar_arrive_expect_tx(&strip_full, strip_bytes);
-        tma_load_4d(strip, &tmH1, &strip_full, 0, c0 - 5, r0 - 5, b);
+        if (!SPLIT) {
+          if (it > 0) mbar_wait(&hempty[0], (it - 1) & 1);
+          mbar_arrive_expect_tx(&hfull[0], strip_bytes);
+          tma_load_4d(strip, &tmH1, &hfull[0], 0, c0 - 5, r0 - 5, b);
+        }
         for (int t = 0; t < ntiles; ++t) {
-          for (int kb = 0; kb < KBLOCKS; ++kb, ++wk) {
-            const int s = wk % WSTAGES;
-            if (wk >= WSTAGES) mbar_wait(&wempty[s], ((wk / WSTAGES) - 1) & 1);
-            mbar_arrive_expect_tx(&wfull[s], WBYTES);
-            bulk_load(wst + s * WBYTES, reinterpret_cast<const uint8_t*>(wpack) + (size_t)kb * WBYTES, WBYTES,
-                      &wfull[s]);
+          const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack);
+          for (int kb = 0; kb < KBLOCKS; ++kb, ++wk, wsrc += WBYTES) {
+            const uint32_t st = wk % WSTAGES;
+            if (wk >= WSTAGES) mbar_wait(&wempty[st], ((wk / WSTAGES) - 1) & 1);
+#ifdef DI_EXP_HALFW
+            mbar_arrive_expect_tx(&wfull[st], WBYTES / 2);   // experiment: half the weight bytes (wrong results)
+            bulk_load(wst + st * WBYTES, wsrc, WBYTES / 2, &wfull[st]);
+#else
+            mbar_arrive_expect_tx(&wfull[st], WBYTES);
+            bulk_load(wst + st * WBYTES, wsrc, WBYTES, &wfull[st]);
+#endif
           }
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      int wk = 0, it = 0, ti = 0;
-      const uint32_t strip_s = smem_u32(strip), wst_s = smem_u32(wst);
+  } else if (warp == 3) {
+    if (SPLIT && lane == 0) {  // ---------------------------------------- strip producer (two halves)
+      int it = 0;
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
         const int b = u / per_img, rem = u - b * per_img;
+        const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
+        if (it > 0) mbar_wait(&hempty[0], (it - 1) & 1);
+        mbar_arrive_expect_tx(&hfull[0], half_bytes);
+        tma_load_4d(strip, &tmH1, &hfull[0], 0, c0 - 5, r0 - 5, b);
+        if (it > 0) mbar_wait(&hempty[1], (it - 1) & 1);
+        mbar_arrive_expect_tx(&hfull[1], half_bytes);
+        tma_load_4d(strip + half_bytes, &tmH1, &hfull[1], 0, c0 - 5, r0 - 5 + HALF_ROWS, b);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      // Lean loop: descriptors built once, per-MMA addresses are immediate 64-bit adds of (bytes >> 4); the
+      // stage index of K-block (uu, j) is j (33 K-blocks per tile, 3 stages).  A single issuing thread is
+      // latency-bound, so every instruction here costs tensor-pipe time.
+      const uint64_t bdesc0 = smem_desc(smem_u32(strip), 16, 1024, kSwizzle128B);
+      const uint64_t adesc0 = smem_desc(smem_u32(wst), 16, 1024, kSwizzle128B);
+      const uint64_t pstep = (uint64_t)g.P * 8;    // one tap row = P positions x 128 B, >> 4
+      uint32_t wk = 0;
+      int it = 0, ti = 0;
+#ifdef DI_PROF_CONV2
+      long long c_h = 0, c_t = 0, c_w = 0, c_w0 = 0, c_w1 = 0, c0_ = clock64();
+#define PT0 long long _t0 = clock64();
+#define PT1(acc) acc += clock64() - _t0;
+#else
+#define PT0
+#define PT1(acc)
+#endif
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+        const int rem = u % per_img;
         const int r0 = (rem / g.ncs) * R;
-        (void)b;
         const int rows = min(R, g.n1 - r0);
         const int L = (rows - 1) * g.P + g.wseg;
         const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
-        mbar_wait(&strip_full, it & 1);
+        { PT0 mbar_wait(&hfull[0], it & 1); PT1(c_h) }
+        bool bready = !SPLIT, afree = false;
         tc_fence_after();
         for (int t = 0; t < ntiles; ++t, ++ti) {
           const int n0 = t * OUT_PER_TILE;
@@ -135,35 +183,62 @@ __global__ void __launch_bounds__(256, 1)
           const int nmma = min(NT, (cnt + 3 + 15) & ~15);
           const uint32_t idesc = idesc_f32acc(1, 128, nmma);
           const int buf = ti & 1;
-          if (ti >= 2) mbar_wait(&tempty[buf], ((ti >> 1) - 1) & 1);
+          { PT0 if (ti >= 2) mbar_wait(&tempty[buf], ((ti >> 1) - 1) & 1); PT1(c_t) }
           tc_fence_after();
           const uint32_t d = tmem + buf * 256;
-          for (int kb = 0; kb < KBLOCKS; ++kb, ++wk) {
-            const int s = wk % WSTAGES;
-            mbar_wait(&wfull[s], (wk / WSTAGES) & 1);
-            tc_fence_after();
-            const int uu = kb / 3, v0 = (kb - uu * 3) * 4;
-            const uint32_t bpos = strip_s + (uint32_t)(n0 + uu * g.P + v0) * 128;
-            const uint32_t apos = wst_s + s * WBYTES;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              umma_f16_ss(d, smem_desc(apos + k * 32, 16, 1024, kSwizzle128B),
-                          smem_desc(bpos + k * 32, 16, 1024, kSwizzle128B), idesc, (kb | k) != 0);
+          const bool last = t == ntiles - 1;
+          uint64_t bd = bdesc0 + (uint64_t)(n0 * 8);
+          int pos = n0;                     // first strip position read by tap row uu (v0 = 0)
+          for (int uu = 0; uu < 11; ++uu, bd += pstep, pos += g.P) {
+            if (SPLIT && !bready && pos + 8 + nmma - 1 >= halfpos) {
+              mbar_wait(&hfull[1], it & 1);
+              bready = true;
+              tc_fence_after();
             }
-            umma_commit(&wempty[s]);
+#pragma unroll
+            for (int j = 0; j < 3; ++j, ++wk) {   // column-tap groups v0 = 0, 4, 8
+              const uint32_t st = wk % WSTAGES;
+#ifdef DI_PROF_CONV2
+              { PT0 mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
+                if (t == 0 && uu < 3) { PT1(c_w0) } else if (t == 0) { PT1(c_w) } else { PT1(c_w1) } }
+#else
+              mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
+#endif
+              tc_fence_after();
+              const uint64_t ad = adesc0 + (uint64_t)(st * (WBYTES >> 4));
+              const uint64_t b = bd + (uint64_t)(32 * j);   // v0 = 4j positions x 128 B >> 4
+              umma_f16_ss(d, ad, b, idesc, (uu | j) != 0);
+              umma_f16_ss(d, ad + 2, b + 2, idesc, 1);
+              umma_f16_ss(d, ad + 4, b + 4, idesc, 1);
+              umma_f16_ss(d, ad + 6, b + 6, idesc, 1);
+              umma_commit(&wempty[st]);
+            }
+            // half A is free once the last tile has passed the last tap row whose window starts in it
+            if (SPLIT && last && pos < halfpos && pos + g.P >= halfpos) umma_commit(&hempty[0]), afree = true;
           }
           umma_commit(&tfull[buf]);
         }
-        umma_commit(&strip_empty);
+        if (SPLIT) {
+          if (!afree) umma_commit(&hempty[0]);    // (the last tile's tap rows never crossed into half B)
+          if (!bready) mbar_wait(&hfull[1], it & 1);
+          umma_commit(&hempty[1]);
+        } else {
+          umma_commit(&hempty[0]);
+        }
       }
+#ifdef DI_PROF_CONV2
+      if (blockIdx.x % 37 == 0)
+        printf("conv2 cta %d: cycles %lld strip-wait %lld tmem-wait %lld weight-wait first9 %lld tile0-rest %lld "
+               "later-tiles %lld units %d kblocks %u\n", blockIdx.x, clock64() - c0_, c_h, c_t, c_w0, c_w, c_w1, it, wk);
+#endif
     }
   } else if (warp >= 4) {  // ---------------------------------------------- epilogue
     const int q = warp - 4;              // TMEM lane quadrant = column-tap group v'
     const int e = threadIdx.x - 128;     // 0..127
-    const int jj = e >> 2, kg = e & 3;   // reduce role: output position jj of the chunk, channels 8kg..8kg+7
-    float bch[8];
+    const int jj = e >> 3, kg = e & 7;   // reduce role: output position jj of the chunk, channels 4kg..4kg+3
+    float bch[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) bch[i] = (!fullmap && bias) ? bias[8 * kg + i] : 0.f;
+    for (int i = 0; i < 4; ++i) bch[i] = (!fullmap && bias) ? bias[4 * kg + i] : 0.f;
     int ti = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
       const int b = u / per_img, rem = u - b * per_img;
@@ -178,49 +253,40 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&tfull[buf], (ti >> 1) & 1);
         tc_fence_after();
         const uint32_t tq = tmem + buf * 256 + ((uint32_t)(q * 32) << 16);
-        for (int c = 0; c < cnt; c += 32) {
-          const int nout = min(32, cnt - c);
-          uint32_t r[32];
-          if (c + q + 32 <= NT)
-            tmem_ld32(tq + c + q, r);
+        for (int c = 0; c < cnt; c += ECH) {
+          const int nout = min(ECH, cnt - c);
+          uint32_t r[ECH];
+          if (c + q + ECH <= NT)
+            tmem_ld16(tq + c + q, r);
           else
-            ld_tail29(tq + c + q, r);
+            ld_tail13(tq + c + q, r);
           tmem_ld_wait();
-          float* dst = sP + q * 1024 + lane;   // sP[q][j][k], k = lane
+          float* dst = sP + q * (ECH * SPS) + lane;   // sP[q][j][k], k = lane
 #pragma unroll
-          for (int j = 0; j < 32; ++j) dst[j * 32] = __uint_as_float(r[j]);
+          for (int j = 0; j < ECH; ++j) dst[j * SPS] = __uint_as_float(r[j]);
           named_bar(1, 128);
           if (jj < nout) {
             const int o = n0 + c + jj;
             const int rr = o / g.P, cc = o - rr * g.P;
             const int orow = r0 + rr, ocol = c0 + cc;
-            if (cc < g.wseg && ocol < g.n2 && orow < g.n1) {
-              float s[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) s[i] = 0.f;
+            if (cc < g.wseg && ocol < g.n2 && rr < rows) {
+              float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
               for (int qq = 0; qq < 4; ++qq) {
-                const float4* p = reinterpret_cast<const float4*>(sP + qq * 1024 + jj * 32 + 8 * kg);
-                const float4 a = p[0], bq = p[1];
-                s[0] += a.x, s[1] += a.y, s[2] += a.z, s[3] += a.w;
-                s[4] += bq.x, s[5] += bq.y, s[6] += bq.z, s[7] += bq.w;
+                const float4 a = *reinterpret_cast<const float4*>(sP + qq * (ECH * SPS) + jj * SPS + 4 * kg);
+                sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
               }
               const size_t pix = ((size_t)b * g.n1 + orow) * g.n2 + ocol;
               if (fullmap && bias) {
-                const float4* bp = reinterpret_cast<const float4*>(bias + pix % ((size_t)g.n1 * g.n2) * 32 + 8 * kg);
-                const float4 a = bp[0], bq = bp[1];
-                s[0] += a.x, s[1] += a.y, s[2] += a.z, s[3] += a.w;
-                s[4] += bq.x, s[5] += bq.y, s[6] += bq.z, s[7] += bq.w;
+                const float4 a = *reinterpret_cast<const float4*>(bias + pix % ((size_t)g.n1 * g.n2) * 32 + 4 * kg);
+                sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
               } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) s[i] += bch[i];
+                sum.x += bch[0], sum.y += bch[1], sum.z += bch[2], sum.w += bch[3];
               }
-              uint4 v;
-              v.x = pack_bf16x2(fmaxf(s[0], 0.f), fmaxf(s[1], 0.f));
-              v.y = pack_bf16x2(fmaxf(s[2], 0.f), fmaxf(s[3], 0.f));
-              v.z = pack_bf16x2(fmaxf(s[4], 0.f), fmaxf(s[5], 0.f));
-              v.w = pack_bf16x2(fmaxf(s[6], 0.f), fmaxf(s[7], 0.f));
-              *reinterpret_cast<uint4*>(h2 + pix * 32 + 8 * kg) = v;
+              uint2 v;
+              v.x = pack_bf16x2(fmaxf(sum.x, 0.f), fmaxf(sum.y, 0.f));
+              v.y = pack_bf16x2(fmaxf(sum.z, 0.f), fmaxf(sum.w, 0.f));
+              *reinterpret_cast<uint2*>(h2 + pix * 32 + 4 * kg) = v;
             }
           }
           named_bar(1, 128);
@@ -249,21 +315,34 @@ static Geo make_geo(int batch, int n1, int n2) {
 size_t conv2_tc_smem_bytes(int n2) {
   const int wseg = n2 < WSEG ? n2 : WSEG, P = wseg + 10;
   const size_t strip_alloc = ((size_t)strip_rows_bytes(P) + GUARD_ROWS * 128 + 1023) & ~(size_t)1023;
-  return strip_alloc + WSTAGES * WBYTES + 4 * 32 * 32 * 4 + 1024;
+  return strip_alloc + WSTAGES * WBYTES + 4 * ECH * SPS * 4 + 1024;
 }
 
-int conv2_tc_box_rows() { return R + 10; }
+// Split strip loading (SPLIT = true) needs equal halves (R + 10 even) and a second tensor map otherwise; with
+// R = 5 and a 4-deep weight ring it measured no gain, so the unsplit schedule is used.
+// The strip is loaded in one box per unit.  Loading it as two halves with a separate producer so that the load
+// overlaps the MMAs of the previous unit (k_conv2_tc<true>) removes the strip wait but measured slower on B200
+// (the TMA writes compete with the UMMA operand reads for shared-memory bandwidth, which this kernel saturates:
+// DESIGN.md §6), so it is kept for reference and not launched.
+static bool conv2_split() { return false; }
+
+int conv2_tc_box_rows() { return conv2_split() ? HALF_ROWS : R + 10; }
 int conv2_tc_box_cols(int n2) { return (n2 < WSEG ? n2 : WSEG) + 10; }
 
 cudaError_t setup_conv2_tc(int n2) {
-  return cudaFuncSetAttribute(k_conv2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)conv2_tc_smem_bytes(n2));
+  cudaError_t e = cudaFuncSetAttribute(k_conv2_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)conv2_tc_smem_bytes(n2));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_conv2_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)conv2_tc_smem_bytes(n2));
 }
 
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st) {
   Geo g = make_geo(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv2_tc<<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(*tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias,
+  auto k = conv2_split() ? k_conv2_tc<true> : k_conv2_tc<false>;
+  k<<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(*tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias,
                                                          fullmap, g, reinterpret_cast<__nv_bfloat16*>(h2));
   return cudaGetLastError();
 }
