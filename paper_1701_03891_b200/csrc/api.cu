@@ -91,7 +91,8 @@ struct di_ctx_s {
   size_t yhost_bytes = 0;
   float* xhost_dev = nullptr;
   long long ws_bytes = 0;
-  CUtensorMap tmPt{}, tmH1{}, tmH2{};
+  CUtensorMap tmPt{}, tmH1{}, tmH2{}, tmX{};
+  bool has_tmX = false;
   int last_launches = 0;
   bool profiling = false;
   std::vector<std::array<cudaEvent_t, 5>> evpool;  // one set of stage-boundary events per profiled call
@@ -128,6 +129,21 @@ di_status encode_h1(CUtensorMap* map, const void* h1, int batch, int n1, int n2)
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h1) failed: %d", (int)r);
+  return DI_OK;
+}
+
+// x_tilde [batch][n1][n2] bf16 for the conv1 strip TMA (needs n2 % 8 == 0: 16-B row stride)
+di_status encode_xt(CUtensorMap* map, const void* xt, int batch, int n1, int n2) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)n2 * 2, (cuuint64_t)n1 * n2 * 2};
+  cuuint32_t box[3] = {(cuuint32_t)di::conv1_tc_box_cols(n2), (cuuint32_t)di::conv1_tc_box_rows(), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(xt), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (x_tilde) failed: %d", (int)r);
   return DI_OK;
 }
 
@@ -198,17 +214,22 @@ std::vector<uint16_t> conv2_tc_pack(const std::vector<float>& wx2) {
 }
 
 // conv1 tensor-core blocks: block u (2 KB) = 64 filter rows x 16 column taps (v >= 11 zero), bf16, SWIZZLE_32B
-// image (16-B chunk h of row f at f*32 + ((h ^ ((f >> 2) & 1)) << 4)).
+// image (16-B chunk h of row m at m*32 + ((h ^ ((m >> 2) & 1)) << 4)).  Row m = 16G + j holds filter
+// 16G + 2j (j < 8) or 16G + 2(j - 8) + 1 (j >= 8): the epilogue's 16x256b TMEM load then hands each thread the two
+// adjacent channels of a bf16x2 store (k_conv13_tc.cu).
 std::vector<uint16_t> conv1_tc_pack(const std::vector<float>& wx1) {
   std::vector<uint16_t> out(11 * 2048 / 2, 0);
   uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
   for (int u = 0; u < K; ++u)
-    for (int f = 0; f < 64; ++f)
+    for (int m = 0; m < 64; ++m) {
+      const int grp = m / 16, j = m % 16;
+      const int f = 16 * grp + (j < 8 ? 2 * j : 2 * (j - 8) + 1);
       for (int v = 0; v < 16; ++v) {
         const uint16_t h = v < K ? f2bf(wx1[((size_t)f * K + u) * K + v]) : 0;
-        const size_t off = (size_t)u * 2048 + f * 32 + ((((size_t)v / 8) ^ ((f >> 2) & 1)) << 4) + (v % 8) * 2;
+        const size_t off = (size_t)u * 2048 + m * 32 + ((((size_t)v / 8) ^ ((m >> 2) & 1)) << 4) + (v % 8) * 2;
         std::memcpy(base + off, &h, 2);
       }
+    }
   return out;
 }
 
@@ -297,8 +318,19 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
   }
   mark(1);
   if (first <= 1 && 1 <= last) {
-    if (bf16)
-      CUDA_TRY(di::launch_conv1_tc(xt, c->wp1, c->b1, fm, h1, batch, c->n1, c->n2, c->num_sms, st));
+    if (bf16) {
+      CUtensorMap tm;
+      const CUtensorMap* tmp = nullptr;
+      if (c->has_tmX) {
+        tmp = &c->tmX;
+        if (xt != c->xt || batch != c->max_batch) {
+          di_status s = encode_xt(&tm, xt, batch, c->n1, c->n2);
+          if (s != DI_OK) return s;
+          tmp = &tm;
+        }
+      }
+      CUDA_TRY(di::launch_conv1_tc(tmp, xt, c->wp1, c->b1, fm, h1, batch, c->n1, c->n2, c->num_sms, st));
+    }
     else
       CUDA_TRY(di::launch_conv1_simt(xt, bf16, c->wx1, c->b1, fm, h1, batch, c->n1, c->n2, st));
     ++launches;
@@ -490,6 +522,10 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       return fail(DI_ERR_CUDA, "setup_conv13_tc: %s", cudaGetErrorString(e));
     }
     STEP(encode_h2(&c->tmH2, c->h2, a->max_batch, a->n1, a->n2));
+    if (a->n2 % 8 == 0) {
+      STEP(encode_xt(&c->tmX, c->xt, a->max_batch, a->n1, a->n2));
+      c->has_tmX = true;
+    }
   }
 #undef STEP
   *out = c;

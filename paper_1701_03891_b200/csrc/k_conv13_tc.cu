@@ -22,11 +22,13 @@
 // the last sum (11 lanes at column offsets v) done by the epilogue through shared memory.  A tile of 256
 // positions yields 246 complete outputs.
 //
-// Roles (256 threads): warp 0 producer (weights once; conv3: TMA strips), warp 1 single-thread MMA issuer,
-// warps 2-3 conv1 im2row builders (warp 2 also allocates TMEM), warps 4-7 epilogue (TMEM lane quadrants).
+// Roles: warp 0 producer (weights once; conv3: TMA strips), warp 1 single-thread MMA issuer, warps 2-3 conv1
+// im2row builders (warp 2 also allocates TMEM), epilogue warps 4-7 (conv3) / 4-11 (conv1) on the TMEM quadrants.
 // Strips / im2row buffers are double-buffered across units; accumulators rotate over 4 TMEM slots.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <cstdio>
 
 #include "kernels.cuh"
 #include "sm100.cuh"
@@ -45,11 +47,12 @@ __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; 
 // ---------------------------------------------------------------- conv1 geometry
 constexpr int R1 = C1TC_ROWS;           // output rows per unit
 constexpr int P1MAX = 80;
-constexpr int IM_ROWS = R1 * P1MAX + 256 + 10 * P1MAX;   // im2row rows per buffer (>= ntiles*256 + 10P)
+constexpr int IM_ROWS = (R1 + 10) * 64;                  // im2row rows per buffer: (R + 10) rows x W <= 64
 constexpr int IM_BYTES = IM_ROWS * 32;
-constexpr int STRIP_WORDS = (IM_ROWS + 32) / 2;          // strip_lin as words (zero past the real strip)
+constexpr int STRIP_WORDS = ((R1 + 10) * P1MAX + 32) / 2; // strip_lin as words (zero past the real strip)
 constexpr int SW1_OFF = ((STRIP_WORDS + 31) & ~31) + 16;  // word offset of the one-element-shifted copy
 constexpr int FILL_PER_THREAD = ((R1 + 10) * P1MAX + 63) / 64;   // strip elements per builder thread
+constexpr int XC_STRIDE = ((R1 + 10) * (P1MAX + 8) * 2 + 64 + 127) & ~127;   // TMA strip buffer stride (bytes)
 constexpr int W1_BYTES = 11 * 64 * 32;                   // 11 tap rows x 64 filters x 16 taps bf16
 
 // ---------------------------------------------------------------- conv3 geometry
@@ -61,33 +64,53 @@ constexpr int SROW = 267;                                // S row stride (floats
 }  // namespace
 
 // =============================================================================================== conv1
-__global__ void __launch_bounds__(256, 1)
-    k_conv1_tc(const __nv_bfloat16* __restrict__ xt, const uint8_t* __restrict__ w1pack,
-               const float* __restrict__ bias, int fullmap, Geo13 g, __nv_bfloat16* __restrict__ h1) {
+// im2row rows are indexed by OUTPUT position p = r * W + c (W = wseg, no padding positions): row p holds the 16
+// values x~[r + u - 5][c - 5 .. c + 10] for the tap row u of the current K-block, i.e. strip[r + u][c .. c + 15] of the
+// zero-padded strip (pitch P); K-block u reads the window starting at row p0 + u * W.  A tile is 256 consecutive
+// output positions, so its outputs are contiguous in NHWC h1 whenever the unit spans the full image width.
+// Epilogue: tcgen05.ld.16x256b gives thread t the TMEM lanes t/4 and t/4 + 8 of a 16-lane group at columns
+// 2(t%4), 2(t%4)+1 (tools/ladder.cu t15); the filters are permuted in the packed weights so that those two lanes are
+// the adjacent channels 2i, 2i+1 -- a bf16x2 word stores straight to h1 with no shared-memory transpose.
+// TMAX = true (n2 % 8 == 0): the strip arrives by TMA (out-of-bounds zero fill), double-buffered across units and
+// issued one unit ahead; TMAX = false: builders gather it with plain loads (any n2).  (A TMA box whose innermost
+// start coordinate is not 16-B aligned faults on B200 -- tools/scratch/tma3d.cu -- hence the 8-column left margin.)
+template <bool TMAX>
+__global__ void __launch_bounds__(384, 1)
+    k_conv1_tc(const __grid_constant__ CUtensorMap tmX, const __nv_bfloat16* __restrict__ xt,
+               const uint8_t* __restrict__ w1pack, const float* __restrict__ bias, int fullmap, Geo13 g,
+               __nv_bfloat16* __restrict__ h1) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* wbuf = smem;                                           // 22 KB
-  uint8_t* const im0 = smem + W1_BYTES;   // 2 x 54 KB im2row buffers (1024-aligned: W1_BYTES = 22528)
+  uint8_t* const im0 = smem + W1_BYTES;   // 2 im2row buffers (1024-aligned: W1_BYTES = 22528)
   uint32_t* const sw0 = reinterpret_cast<uint32_t*>(smem + W1_BYTES + 2 * IM_BYTES);
   uint32_t* const sw1 = sw0 + SW1_OFF;
+  uint8_t* const xc0 = smem + W1_BYTES + 2 * IM_BYTES;   // TMAX: 2 buffers x 8 shifted copies (aliases sw0/sw1)
 
-  __shared__ uint64_t wbar, im_full[2], im_empty[2], acc_full[NACC], acc_empty[NACC];
+  __shared__ uint64_t wbar, im_full[2], im_empty[2], acc_full[NACC], acc_empty[NACC], xfull[2];
   __shared__ uint32_t tslot;
   const int warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     mbar_init(&wbar, 1);
     for (int s = 0; s < 2; ++s) mbar_init(&im_full[s], 64), mbar_init(&im_empty[s], 1);
-    for (int a = 0; a < NACC; ++a) mbar_init(&acc_full[a], 1), mbar_init(&acc_empty[a], 4);
+    for (int a = 0; a < NACC; ++a) mbar_init(&acc_full[a], 1), mbar_init(&acc_empty[a], 8);
+    for (int s = 0; s < 2; ++s) mbar_init(&xfull[s], 1);
+    if (TMAX) tma_prefetch_desc(&tmX);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
-  for (int i = threadIdx.x; i < 2 * SW1_OFF; i += blockDim.x) sw0[i] = 0u;   // zero tails of both copies
+  if (TMAX) {   // zero the tails past each copy (TMA never writes them; windows of the last rows read them)
+    for (int i = threadIdx.x; i < 2 * XC_STRIDE / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(xc0)[i] = 0u;
+    fence_async_smem();
+  } else {
+    for (int i = threadIdx.x; i < 2 * SW1_OFF; i += blockDim.x) sw0[i] = 0u;   // zero tails of both copies
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
   const int per_img = g.nrb * g.ncs;
-  const int P = g.P;
+  const int P = g.P, W = g.wseg;
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ weights, once
@@ -100,25 +123,39 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const uint64_t adesc0 = smem_desc(smem_u32(wbuf), 16, 256, kSwizzle32B);
       const uint64_t bdesc_base = smem_desc(smem_u32(im0), 16, 256, kSwizzle32B);
+      const uint64_t bstep = (uint64_t)((W * 32) >> 4);
       int it = 0, ti = 0;
+#ifdef DI_PROF_CONV1
+      long long c_im = 0, c_acc = 0, c0_ = clock64();
+#endif
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
         const int rem = u % per_img;
         const int r0 = (rem / g.ncs) * g.R;
-        const int rows = min(g.R, g.n1 - r0);
-        const int L = (rows - 1) * P + g.wseg;
+        const int npos = min(g.R, g.n1 - r0) * W;
         const int s = it & 1;
+#ifdef DI_PROF_CONV1
+        long long t0 = clock64();
+#endif
         mbar_wait(&im_full[s], (it >> 1) & 1);
+#ifdef DI_PROF_CONV1
+        c_im += clock64() - t0;
+#endif
         tc_fence_after();
-        for (int n0 = 0; n0 < L; n0 += 256, ++ti) {
-          const int cnt = min(256, L - n0);
+        for (int n0 = 0; n0 < npos; n0 += 256, ++ti) {
+          const int cnt = min(256, npos - n0);
           const int N = cnt > 128 ? 256 : (cnt > 64 ? 128 : 64);
           const uint32_t idesc = idesc_f32acc(1, 64, N);
           const int a = ti % NACC;
+#ifdef DI_PROF_CONV1
+          long long t1 = clock64();
+#endif
           if (ti >= NACC) mbar_wait(&acc_empty[a], ((ti / NACC) - 1) & 1);
+#ifdef DI_PROF_CONV1
+          c_acc += clock64() - t1;
+#endif
           tc_fence_after();
           const uint32_t d = tmem + a * 128;
           uint64_t bd = bdesc_base + (uint64_t)(((s * IM_BYTES) + n0 * 32) >> 4);
-          const uint64_t bstep = (uint64_t)((P * 32) >> 4);
 #pragma unroll
           for (int tu = 0; tu < 11; ++tu) {
             umma_ws_f16(d, adesc0 + (uint64_t)((tu * 2048) >> 4), bd, idesc, tu != 0);
@@ -128,108 +165,198 @@ __global__ void __launch_bounds__(256, 1)
         }
         umma_commit(&im_empty[s]);
       }
+#ifdef DI_PROF_CONV1
+      if (blockIdx.x % 37 == 0)
+        printf("conv1 cta %d issuer: cycles %lld im-wait %lld acc-wait %lld units %d tiles %d\n", blockIdx.x,
+               clock64() - c0_, c_im, c_acc, it, ti);
+#endif
     }
   } else if (warp < 4) {  // ------------------------------------------- im2row builders (64 threads)
     // strip_lin[idx] = x_tilde[b][r0-5+rr][c0-5+cc] (zero outside the image and past the 5-px halo), kept twice
     // as 32-bit words: sw0 = strip_lin, sw1 = strip_lin shifted by one element, so that the 16-element window
-    // of ANY row m is 8 aligned words (from sw0 if m is even, sw1 if odd).  sw1 sits 16 words (mod 32) after
-    // sw0: a warp's 32 consecutive rows read 32 distinct banks.
+    // starting at ANY strip position m is 8 aligned words (from sw0 if m is even, sw1 if odd).  sw1 sits 16 words
+    // (mod 32) after sw0: a warp's 32 consecutive rows read 32 distinct banks.
     const int bt = threadIdx.x - 64;
     uint16_t* s0 = reinterpret_cast<uint16_t*>(sw0);
     uint16_t* s1 = reinterpret_cast<uint16_t*>(sw1);
+    const uint32_t wmagic = (1u << 20) / (uint32_t)W + 1;   // p / W for p < 2^13 (W <= 64)
     int it = 0;
+#ifdef DI_PROF_CONV1
+    long long b_wait = 0, b_load = 0, b_build = 0, b0_ = clock64();
+#endif
     for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
       const int b = u / per_img, rem = u - b * per_img;
       const int r0 = (rem / g.ncs) * g.R, c0 = (rem % g.ncs) * g.wseg;
       const int s = it & 1;
+#ifdef DI_PROF_CONV1
+      long long bt0 = clock64();
+#endif
       if (it >= 2) mbar_wait(&im_empty[s], ((it >> 1) - 1) & 1);
-      const uint16_t* src = reinterpret_cast<const uint16_t*>(xt) + (size_t)b * g.n1 * g.n2;
-      // all loads of this thread first (memory-level parallelism), then the shared-memory stores
-      const int strip_real = (g.R + 10) * P;
-      uint16_t v[FILL_PER_THREAD];
-#pragma unroll
-      for (int i = 0; i < FILL_PER_THREAD; ++i) {
-        const int idx = bt + 64 * i;
-        const int rr = idx / P, cc = idx - rr * P;
-        const int gy = r0 - 5 + rr, gx = c0 - 5 + cc;
-        v[i] = 0;
-        if (idx < strip_real && cc < g.wseg + 10 && gy >= 0 && gy < g.n1 && gx >= 0 && gx < g.n2)
-          v[i] = src[(size_t)gy * g.n2 + gx];
-      }
-#pragma unroll
-      for (int i = 0; i < FILL_PER_THREAD; ++i) {
-        const int idx = bt + 64 * i;
-        if (idx < strip_real) {
-          s0[idx] = v[i];
-          if (idx > 0) s1[idx - 1] = v[i];
-        }
-      }
-      named_bar(2, 64);
-      // im2row: row m = strip_lin[m .. m+15], SWIZZLE_32B (16-B chunk h of row m at m*32 + ((h ^ (m>>2 & 1)) << 4))
+#ifdef DI_PROF_CONV1
+      long long bt1 = clock64();
+      b_wait += bt1 - bt0;
+#endif
       uint8_t* dst = im0 + s * IM_BYTES;
-      for (int m = bt; m < IM_ROWS; m += 64) {
-        const uint32_t* w = ((m & 1) ? sw1 : sw0) + (m >> 1);
-        const int sw = (m >> 2) & 1;
-        *reinterpret_cast<uint4*>(dst + m * 32 + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint4*>(dst + m * 32 + ((1 ^ sw) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
+      const int nrows = (g.R + 10) * W;
+      if (TMAX) {
+        if (bt == 0) {
+          // the strip of unit `un` into buffer `buf` (unit it+1 is issued one unit ahead).  TMA needs a 16-B
+          // aligned innermost start, so the box starts 8 columns left of the unit (not 5): strip[r][cc] sits at
+          // copy[r * Q + cc + 3] with Q = P + 8.
+          for (int k = (it == 0 ? 0 : 1); k < 2; ++k) {
+            const int un = u + k * gridDim.x, buf = (it + k) & 1;
+            if (un >= g.units) break;
+            const int bb = un / per_img, rm = un - bb * per_img;
+            const int rr0 = (rm / g.ncs) * g.R, cc0 = (rm % g.ncs) * g.wseg;
+            mbar_arrive_expect_tx(&xfull[buf], (g.R + 10) * (P + 8) * 2);
+            tma_load_3d(xc0 + buf * XC_STRIDE, &tmX, &xfull[buf], cc0 - 8, rr0 - 5, bb);
+          }
+        }
+        mbar_wait(&xfull[s], (it >> 1) & 1);
+#ifdef DI_PROF_CONV1
+        long long bt2 = clock64();
+        b_load += bt2 - bt1;
+#endif
+        // row p -> copy position m = r*Q + c + 3; its 16-element window = 8 words funnel-shifted by (m & 1) * 16
+        const uint32_t* xw = reinterpret_cast<const uint32_t*>(xc0 + s * XC_STRIDE);
+        const int Q = P + 8;
+        for (int p = bt; p < nrows; p += 64) {
+          const int r = (int)(((uint32_t)p * wmagic) >> 20), c = p - r * W;
+          const int m = r * Q + c + 3;
+          const uint32_t* w = xw + (m >> 1);
+          const uint32_t sh = (m & 1) * 16;
+          uint32_t o[8];
+          uint32_t prev = w[0];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t nxt = w[i + 1];
+            o[i] = __funnelshift_r(prev, nxt, sh);
+            prev = nxt;
+          }
+          const int sw = (p >> 2) & 1;
+          *reinterpret_cast<uint4*>(dst + p * 32 + (sw << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<uint4*>(dst + p * 32 + ((1 ^ sw) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+#ifdef DI_PROF_CONV1
+        b_build += clock64() - bt2;
+#endif
+      } else {
+#ifdef DI_PROF_CONV1
+        long long bt2 = clock64();
+#endif
+        const uint16_t* src = reinterpret_cast<const uint16_t*>(xt) + (size_t)b * g.n1 * g.n2;
+        // all loads of this thread first (memory-level parallelism), then the shared-memory stores
+        const int strip_real = (g.R + 10) * P;
+        uint16_t v[FILL_PER_THREAD];
+  #pragma unroll
+        for (int i = 0; i < FILL_PER_THREAD; ++i) {
+          const int idx = bt + 64 * i;
+          const int rr = idx / P, cc = idx - rr * P;
+          const int gy = r0 - 5 + rr, gx = c0 - 5 + cc;
+          v[i] = 0;
+          if (idx < strip_real && cc < g.wseg + 10 && gy >= 0 && gy < g.n1 && gx >= 0 && gx < g.n2)
+            v[i] = src[(size_t)gy * g.n2 + gx];
+        }
+  #pragma unroll
+        for (int i = 0; i < FILL_PER_THREAD; ++i) {
+          const int idx = bt + 64 * i;
+          if (idx < strip_real) {
+            s0[idx] = v[i];
+            if (idx > 0) s1[idx - 1] = v[i];
+          }
+        }
+        named_bar(2, 64);
+  #ifdef DI_PROF_CONV1
+        long long bt2 = clock64();
+        b_load += bt2 - bt1;
+  #endif
+        // im2row row p (output position r*W + c) = strip_lin[r*P + c .. +15], SWIZZLE_32B
+        // (16-B chunk h of row p at p*32 + ((h ^ (p>>2 & 1)) << 4))
+        for (int p = bt; p < nrows; p += 64) {
+          const int r = (int)(((uint32_t)p * wmagic) >> 20), c = p - r * W;
+          const int m = r * P + c;
+          const uint32_t* w = ((m & 1) ? sw1 : sw0) + (m >> 1);
+          const int sw = (p >> 2) & 1;
+          *reinterpret_cast<uint4*>(dst + p * 32 + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(dst + p * 32 + ((1 ^ sw) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
+        }
       }
       fence_async_smem();
       mbar_arrive(&im_full[s]);
       named_bar(2, 64);  // the strip is refilled for the next unit only after every builder is done reading it
+#ifdef DI_PROF_CONV1
+      b_build += clock64() - bt2;
+#endif
     }
-  } else {  // -------------------------------------------------------- epilogue, warps 4..7
-    const int q = warp - 4;
-    const int f = 32 * (q & 1) + lane;  // filter (TMEM lane within the quadrant)
-    __nv_bfloat16* tw = reinterpret_cast<__nv_bfloat16*>(sw0 + 2 * SW1_OFF) + q * 32 * 32;   // 2 KB per warp
-    const float bch = (!fullmap && bias) ? bias[f] : 0.f;
+#ifdef DI_PROF_CONV1
+    if (blockIdx.x % 37 == 0 && bt == 0)
+      printf("conv1 cta %d builder: cycles %lld wait %lld strip-load %lld im2row %lld\n", blockIdx.x,
+             clock64() - b0_, b_wait, b_load, b_build);
+#endif
+  } else {  // -------------------------------------------------------- epilogue, warps 4..11
+    // .ws M=64 D layout: quadrants {0,1} = filter rows 0..63 for tile columns [0, N/2), {2,3} for [N/2, N).
+    // Warp w reads quadrant q = w % 4, 16-lane group hh = (w - 4) / 4; in group G = 2*(q&1) + hh, thread t holds
+    // channels 16G + 2i, 16G + 2i + 1 (i = t/4; permuted weight rows) at columns 2(t%4), 2(t%4)+1 of each
+    // 8-column block.
+    const int q = warp & 3, hh = (warp - 4) >> 2;
+    const int i4 = lane >> 2, cpair = 2 * (lane & 3);
+    const int ch = 16 * (2 * (q & 1) + hh) + 2 * i4;          // this thread's channels ch, ch + 1
+    const float b0 = (!fullmap && bias) ? bias[ch] : 0.f, b1 = (!fullmap && bias) ? bias[ch + 1] : 0.f;
+    const uint32_t wmagic = (1u << 20) / (uint32_t)W + 1;
     int ti = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
       const int b = u / per_img, rem = u - b * per_img;
       const int r0 = (rem / g.ncs) * g.R, c0 = (rem % g.ncs) * g.wseg;
-      const int rows = min(g.R, g.n1 - r0);
-      const int L = (rows - 1) * P + g.wseg;
-      for (int n0 = 0; n0 < L; n0 += 256, ++ti) {
-        const int cnt = min(256, L - n0);
+      const int npos = min(g.R, g.n1 - r0) * W;
+      const bool linear = g.ncs == 1;    // the unit spans the full width: outputs are contiguous in h1
+      const size_t pix0 = ((size_t)b * g.n1 + r0) * g.n2 + c0;
+      for (int n0 = 0; n0 < npos; n0 += 256, ++ti) {
+        const int cnt = min(256, npos - n0);
         const int N = cnt > 128 ? 256 : (cnt > 64 ? 128 : 64);
         const int half = N / 2;
         const int a = ti % NACC;
         mbar_wait(&acc_full[a], (ti / NACC) & 1);
         tc_fence_after();
-        const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32) << 16);
         const int pbase = n0 + (q >> 1) * half;
+        const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32 + 16 * hh) << 16);
+        const bool fast = linear && cnt == N && !fullmap;
         for (int c = 0; c < half; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
+          uint32_t r[16];
+          tmem_ld_16x256b_x4(taddr + c, r);
           tmem_ld_wait();
-          // position o0 + j of the strip -> (row rr, column cc); j < 32 < P wraps at most once
-          const int o0 = pbase + c;
-          const int rr0 = o0 / P, cc0 = o0 - rr0 * P;
-          // (1) bias + ReLU + bf16, transposed through this warp's smem tile T[j][channel] (64-B rows)
+          if (fast) {   // full tile of a full-width unit: contiguous outputs, no per-element checks
+            uint32_t* dst = reinterpret_cast<uint32_t*>(h1 + (pix0 + pbase + c + cpair) * 64 + ch);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            float bv = bch;
-            if (fullmap && bias) {
-              int cc = cc0 + j, rr = rr0;
-              if (cc >= P) cc -= P, ++rr;
-              const int gy = min(r0 + rr, g.n1 - 1), gx = min(c0 + cc, g.n2 - 1);
-              bv = bias[((size_t)gy * g.n2 + gx) * 64 + f];
-            }
-            tw[j * 32 + lane] = __float2bfloat16_rn(fmaxf(__uint_as_float(r[j]) + bv, 0.f));
-          }
-          __syncwarp();
-          // (2) 16-B coalesced NHWC stores: thread -> (position j = lane/4 + 8i, 8-channel chunk k = lane%4)
-          const uint4* t4 = reinterpret_cast<const uint4*>(tw);
+            for (int k = 0; k < 4; ++k)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int j = (lane >> 2) + 8 * i, k = lane & 3;
-            int cc = cc0 + j, rr = rr0;
-            if (cc >= P) cc -= P, ++rr;
-            if (o0 + j < n0 + cnt && cc < g.wseg && c0 + cc < g.n2 && rr < rows) {
-              const size_t pix = ((size_t)b * g.n1 + r0 + rr) * g.n2 + c0 + cc;
-              *reinterpret_cast<uint4*>(h1 + pix * 64 + 32 * (q & 1) + 8 * k) = t4[j * 4 + k];
-            }
+              for (int e = 0; e < 2; ++e)
+                dst[(8 * k + e) * 32] = pack_bf16x2(fmaxf(__uint_as_float(r[4 * k + e]) + b0, 0.f),
+                                                    fmaxf(__uint_as_float(r[4 * k + 2 + e]) + b1, 0.f));
+            continue;
           }
-          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int p = pbase + c + 8 * k + cpair + e;        // output position within the unit
+              if (p >= n0 + cnt) continue;
+              size_t pix;
+              if (linear) {
+                pix = pix0 + p;
+              } else {
+                const int rr = (int)(((uint32_t)p * wmagic) >> 20), cc = p - rr * W;
+                if (c0 + cc >= g.n2) continue;
+                pix = pix0 + (size_t)rr * g.n2 + cc;
+              }
+              float v0 = __uint_as_float(r[4 * k + e]), v1 = __uint_as_float(r[4 * k + 2 + e]);
+              if (fullmap && bias) {
+                const size_t pm = pix % ((size_t)g.n1 * g.n2);
+                v0 += bias[pm * 64 + ch], v1 += bias[pm * 64 + ch + 1];
+              } else {
+                v0 += b0, v1 += b1;
+              }
+              *reinterpret_cast<uint32_t*>(h1 + pix * 64 + ch) = pack_bf16x2(fmaxf(v0, 0.f), fmaxf(v1, 0.f));
+            }
         }
         tc_fence_before();
         __syncwarp();
@@ -392,7 +519,10 @@ static Geo13 make_geo13(int batch, int n1, int n2, int R, bool conv1) {
   return g;
 }
 
-size_t conv1_tc_smem_bytes() { return (size_t)W1_BYTES + 2 * IM_BYTES + 2 * SW1_OFF * 4 + 4 * 2048 + 1024; }
+size_t conv1_tc_smem_bytes() {
+  const size_t strips = (size_t)2 * XC_STRIDE > (size_t)2 * SW1_OFF * 4 ? (size_t)2 * XC_STRIDE : (size_t)2 * SW1_OFF * 4;
+  return (size_t)W1_BYTES + 2 * IM_BYTES + strips + 1024;
+}
 
 size_t conv3_tc_smem_bytes(int n2) {
   const int wseg = n2 < 64 ? n2 : 64, P = wseg + 10;
@@ -403,19 +533,26 @@ int conv3_tc_box_rows() { return R3 + 10; }
 int conv3_tc_box_cols(int n2) { return (n2 < 64 ? n2 : 64) + 10; }
 
 cudaError_t setup_conv13_tc(int n2) {
-  cudaError_t e = cudaFuncSetAttribute(k_conv1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_conv1_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)conv1_tc_smem_bytes());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_conv1_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)conv1_tc_smem_bytes());
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_conv3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)conv3_tc_smem_bytes(n2));
 }
 
-cudaError_t launch_conv1_tc(const void* xt, const void* w1pack, const float* bias, int fullmap, void* h1, int batch,
-                            int n1, int n2, int num_sms, cudaStream_t st) {
+int conv1_tc_box_rows() { return R1 + 10; }
+int conv1_tc_box_cols(int n2) { return (((n2 < 64 ? n2 : 64) + 10 + 7) & ~7) + 8; }
+
+cudaError_t launch_conv1_tc(const CUtensorMap* tmX, const void* xt, const void* w1pack, const float* bias,
+                            int fullmap, void* h1, int batch, int n1, int n2, int num_sms, cudaStream_t st) {
   Geo13 g = make_geo13(batch, n1, n2, R1, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv1_tc<<<grid, 256, conv1_tc_smem_bytes(), st>>>(reinterpret_cast<const __nv_bfloat16*>(xt),
-                                                       reinterpret_cast<const uint8_t*>(w1pack), bias, fullmap, g,
-                                                       reinterpret_cast<__nv_bfloat16*>(h1));
+  auto k = tmX ? k_conv1_tc<true> : k_conv1_tc<false>;
+  CUtensorMap dummy{};
+  k<<<grid, 384, conv1_tc_smem_bytes(), st>>>(tmX ? *tmX : dummy, reinterpret_cast<const __nv_bfloat16*>(xt),
+                                              reinterpret_cast<const uint8_t*>(w1pack), bias, fullmap, g,
+                                              reinterpret_cast<__nv_bfloat16*>(h1));
   return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@ constexpr int C2_KBLOCKS = 33;              // 11 tap rows x 3 column-tap groups
 constexpr int C2_KBLOCK_BYTES = 128 * 128;  // 128 rows (4 taps x 32 filters) x 64 ch x bf16
 
 // conv1 / conv3 tensor-core geometry (k_conv13_tc.cu)
-constexpr int C1TC_ROWS = 8;                // conv1 output rows per work unit
+constexpr int C1TC_ROWS = 16;               // conv1 output rows per work unit
 constexpr int C3TC_ROWS = 6;                // conv3 output rows per work unit
 
 // stage 0: lifting layer x_tilde = Phi^T y
@@ -33,8 +33,11 @@ cudaError_t launch_conv1_simt(const void* xt, bool bf16, const float* wx, const 
                               int batch, int n1, int n2, cudaStream_t st);
 
 cudaError_t setup_conv13_tc(int n2);
-cudaError_t launch_conv1_tc(const void* xt, const void* w1pack, const float* bias, int fullmap, void* h1, int batch,
-                            int n1, int n2, int num_sms, cudaStream_t st);
+int conv1_tc_box_rows();
+int conv1_tc_box_cols(int n2);
+// tmX: 3-D tensor map of x_tilde (n2 % 8 == 0) for the TMA strip path, or nullptr for the gather path
+cudaError_t launch_conv1_tc(const CUtensorMap* tmX, const void* xt, const void* w1pack, const float* bias,
+                            int fullmap, void* h1, int batch, int n1, int n2, int num_sms, cudaStream_t st);
 
 // stage 2: conv layer 2 (64 -> 32, ReLU)
 cudaError_t setup_conv2_tc(int n2);

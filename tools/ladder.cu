@@ -1108,6 +1108,58 @@ static void t14(int nsm) {
   cudaFree(dc);
 }
 
+// t15: register layout of tcgen05.ld.16x256b (x1 and x2) and 16x64b: TMEM cell (lane, col) = lane*1000 + col
+__global__ void k_t15(float* out) {
+  __shared__ uint32_t tslot;
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (w == 0) tmem_alloc<512>(&tslot), tmem_relinquish();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tb = tslot;
+  for (int c = 0; c < 64; c += 16) {
+    uint32_t r[16];
+    for (int j = 0; j < 16; ++j) r[j] = __float_as_uint((float)((w * 32 + l) * 1000 + c + j));
+    tmem_st16(tb + ((uint32_t)(w * 32) << 16) + c, r);
+  }
+  tmem_st_wait();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (w == 0) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(tb));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int j = 0; j < 4; ++j) out[l * 16 + j] = __uint_as_float(r[j]);
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(tb + (16u << 16)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int j = 0; j < 8; ++j) out[l * 16 + 4 + j] = __uint_as_float(r[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (w == 0) tmem_dealloc<512>(tb);
+}
+static void t15() {
+  float* d;
+  CK(cudaMalloc(&d, 32 * 16 * 4));
+  k_t15<<<1, 128>>>(d);
+  if (check_err("t15")) return;
+  std::vector<float> h(32 * 16);
+  CK(cudaMemcpy(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost));
+  for (int t = 0; t < 32; ++t) {
+    printf("{\"test\":\"t15\",\"thread\":%d,\"x1_lane0\":[", t);
+    for (int j = 0; j < 4; ++j) printf("%s%.0f", j ? "," : "", h[t * 16 + j]);
+    printf("],\"x2_lane16\":[");
+    for (int j = 0; j < 8; ++j) printf("%s%.0f", j ? "," : "", h[t * 16 + 4 + j]);
+    printf("]}\n");
+  }
+  cudaFree(d);
+}
+
 int main(int argc, char** argv) {
   int dev = 0, nsm = 0;
   CK(cudaSetDevice(dev));
@@ -1128,5 +1180,6 @@ int main(int argc, char** argv) {
   if (on("t12")) t12(nsm);
   if (on("t13")) t13(nsm);
   if (on("t14")) t14(nsm);
+  if (on("t15")) t15();
   return 0;
 }
