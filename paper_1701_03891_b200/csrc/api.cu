@@ -90,6 +90,8 @@ struct di_ctx_s {
   void* yhost_dev = nullptr;    // di_recover_host staging
   size_t yhost_bytes = 0;
   float* xhost_dev = nullptr;
+  cudaStream_t cstream = nullptr;               // di_recover_host: device->host copy stream
+  cudaEvent_t cev[4] = {};                       // di_recover_host: chunk-done events
   long long ws_bytes = 0;
   CUtensorMap tmPt{}, tmH1{}, tmH2{}, tmX{};
   bool has_tmX = false;
@@ -270,6 +272,9 @@ void free_ctx(di_ctx c) {
   for (auto& set : c->evpool)
     for (auto e : set)
       if (e) cudaEventDestroy(e);
+  for (auto e : c->cev)
+    if (e) cudaEventDestroy(e);
+  if (c->cstream) cudaStreamDestroy(c->cstream);
   delete c;
 }
 
@@ -557,10 +562,28 @@ di_status di_recover_host(di_ctx c, const void* y_host, long long ldy, int batch
     c->yhost_bytes = ybytes;
   }
   if (!c->xhost_dev) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->xhost_dev), (size_t)c->max_batch * c->N * 4));
+  if (!c->cstream) CUDA_TRY(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+  for (auto& e : c->cev)
+    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CUDA_TRY(cudaMemcpyAsync(c->yhost_dev, y_host, ybytes, cudaMemcpyHostToDevice, st));
-  di_status s = run_stages(c, 0, 3, c->yhost_dev, ldy, batch, c->xt, c->h1, c->h2, c->xhost_dev, st);
-  if (s != DI_OK) return s;
-  CUDA_TRY(cudaMemcpyAsync(xhat_host, c->xhost_dev, (size_t)batch * c->N * 4, cudaMemcpyDeviceToHost, st));
+  // Large batches run as up to 4 chunks so that the device->host copy of x_hat for chunk k (copy stream)
+  // overlaps the kernels of chunk k+1 (caller's stream).  Chunks share the workspace: chunk k+1 only overwrites
+  // x_tilde/h1/h2, never the x_hat rows chunk k is still copying out.
+  const int nchunk = batch >= 2048 ? 4 : (batch >= 512 ? 2 : 1);
+  int b0 = 0;
+  for (int k = 0; k < nchunk; ++k) {
+    const int b1 = (k == nchunk - 1) ? batch : ((long long)batch * (k + 1) / nchunk) & ~3;
+    const int nb = b1 - b0;
+    di_status s = run_stages(c, 0, 3, reinterpret_cast<const uint8_t*>(c->yhost_dev) + (size_t)b0 * ldy * c->elt, ldy,
+                             nb, c->xt, c->h1, c->h2, c->xhost_dev + (size_t)b0 * c->N, st);
+    if (s != DI_OK) return s;
+    CUDA_TRY(cudaEventRecord(c->cev[k], st));
+    CUDA_TRY(cudaStreamWaitEvent(c->cstream, c->cev[k], 0));
+    CUDA_TRY(cudaMemcpyAsync(xhat_host + (size_t)b0 * c->N, c->xhost_dev + (size_t)b0 * c->N, (size_t)nb * c->N * 4,
+                             cudaMemcpyDeviceToHost, c->cstream));
+    b0 = b1;
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->cstream));
   CUDA_TRY(cudaStreamSynchronize(st));
   return DI_OK;
 }

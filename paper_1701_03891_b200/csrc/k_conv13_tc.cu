@@ -428,17 +428,32 @@ __global__ void __launch_bounds__(256, 1)
       const uint64_t bdesc_base = smem_desc(smem_u32(strip0), 16, 512, kSwizzle64B);
       const uint64_t bstep = (uint64_t)((P * 64) >> 4);
       int it = 0, ti = 0;
+#ifdef DI_PROF_CONV3
+      long long c_s = 0, c_a = 0, c0_ = clock64();
+#endif
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
         const int rem = u % per_img;
         const int r0 = (rem / g.ncs) * g.R;
         const int rows = min(g.R, g.n1 - r0);
         const int L = (rows - 1) * P + g.wseg;
         const int s = it & 1;
+#ifdef DI_PROF_CONV3
+        long long t0 = clock64();
+#endif
         mbar_wait(&sfull[s], (it >> 1) & 1);
+#ifdef DI_PROF_CONV3
+        c_s += clock64() - t0;
+#endif
         tc_fence_after();
         for (int n0 = 0; n0 < L; n0 += OUT3, ++ti) {
           const int a = ti % NACC;
+#ifdef DI_PROF_CONV3
+          long long t1 = clock64();
+#endif
           if (ti >= NACC) mbar_wait(&acc_empty[a], ((ti / NACC) - 1) & 1);
+#ifdef DI_PROF_CONV3
+          c_a += clock64() - t1;
+#endif
           tc_fence_after();
           const uint32_t d = tmem + a * 64;
           uint64_t bd = bdesc_base + (uint64_t)((s * strip_alloc + n0 * 64) >> 4);
@@ -453,6 +468,11 @@ __global__ void __launch_bounds__(256, 1)
         }
         umma_commit(&sempty[s]);
       }
+#ifdef DI_PROF_CONV3
+      if (blockIdx.x % 37 == 0)
+        printf("conv3 cta %d issuer: cycles %lld strip-wait %lld acc-wait %lld units %d tiles %d\n", blockIdx.x,
+               clock64() - c0_, c_s, c_a, it, ti);
+#endif
     }
   } else if (warp >= 4) {  // ---------------------------------------------- epilogue
     const int q = warp - 4;
