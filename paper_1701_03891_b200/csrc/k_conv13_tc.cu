@@ -319,13 +319,17 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const int pbase = n0 + (q >> 1) * half;
         const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32 + 16 * hh) << 16);
-        const bool fast = linear && cnt == N && !fullmap;
+        // fast path: full tile, and each 32-position chunk is contiguous in h1 (full-width unit, or a full 64-wide
+        // segment: 32 | W keeps a chunk inside one image row)
+        const bool fast = cnt == N && !fullmap && (linear || (W == 64 && c0 + 64 <= g.n2));
         for (int c = 0; c < half; c += 32) {
           uint32_t r[16];
           tmem_ld_16x256b_x4(taddr + c, r);
           tmem_ld_wait();
-          if (fast) {   // full tile of a full-width unit: contiguous outputs, no per-element checks
-            uint32_t* dst = reinterpret_cast<uint32_t*>(h1 + (pix0 + pbase + c + cpair) * 64 + ch);
+          if (fast) {   // no per-element checks
+            const int p0 = pbase + c;
+            const size_t cpix = linear ? pix0 + p0 : pix0 + (size_t)(p0 >> 6) * g.n2 + (p0 & 63);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(h1 + (cpix + cpair) * 64 + ch);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
 #pragma unroll

@@ -39,7 +39,10 @@ constexpr int R = C2_ROWS;             // output rows per unit (6)
 constexpr int WSEG = 64;               // output columns per unit (max)
 constexpr int NT = 256;                // UMMA N per tile
 constexpr int OUT_PER_TILE = NT - 3;   // 253 complete output positions per tile
-constexpr int WSTAGES = 4;             // weight ring depth (L2 latency of a 16-KB bulk copy ~ 2 K-blocks)
+#ifndef DI_C2_WSTAGES
+#define DI_C2_WSTAGES 4
+#endif
+constexpr int WSTAGES = DI_C2_WSTAGES;             // weight ring depth (L2 latency of a 16-KB bulk copy ~ 2 K-blocks)
 constexpr int KBLOCKS = C2_KBLOCKS;    // 33
 constexpr uint32_t WBYTES = C2_KBLOCK_BYTES;  // 16 KB
 constexpr int GUARD_ROWS = 24;
@@ -261,6 +264,15 @@ __global__ void __launch_bounds__(256, 1)
           else
             ld_tail13(tq + c + q, r);
           tmem_ld_wait();
+#ifdef DI_EXP_NOEPI_SMEM
+          {   // experiment: no shared-memory transpose (wrong results): raw registers straight to h2
+            uint32_t x = 0;
+#pragma unroll
+            for (int j = 0; j < ECH; ++j) x ^= r[j];
+            if (x == 0x12345678u) h2[(size_t)blockIdx.x * 64 + lane] = __float2bfloat16_rn(0.f);
+            continue;
+          }
+#endif
           float* dst = sP + q * (ECH * SPS) + lane;   // sP[q][j][k], k = lane
 #pragma unroll
           for (int j = 0; j < ECH; ++j) dst[j * SPS] = __uint_as_float(r[j]);

@@ -9,7 +9,10 @@
 namespace di {
 
 // conv2 tensor-core geometry (k_conv2_tc.cu)
-constexpr int C2_ROWS = 6;                  // output rows per work unit
+#ifndef DI_C2_ROWS
+#define DI_C2_ROWS 6
+#endif
+constexpr int C2_ROWS = DI_C2_ROWS;         // output rows per work unit
 constexpr int C2_KBLOCKS = 33;              // 11 tap rows x 3 column-tap groups of 4
 constexpr int C2_KBLOCK_BYTES = 128 * 128;  // 128 rows (4 taps x 32 filters) x 64 ch x bf16
 
