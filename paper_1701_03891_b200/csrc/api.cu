@@ -85,6 +85,7 @@ struct di_ctx_s {
   void* wp2 = nullptr;          // conv2 tensor-core weight blocks (BF16 mode)
   void* wp1 = nullptr;          // conv1 tensor-core weight blocks (BF16 mode, SWIZZLE_32B image)
   void* wp3 = nullptr;          // conv3 tensor-core weight blocks (BF16 mode, SWIZZLE_64B image)
+  void* wp2t = nullptr;         // conv2 TF32 weight blocks (TF32 mode)
   float *b1 = nullptr, *b2 = nullptr, *b3 = nullptr;  // per-channel or cropped full maps (nullptr = zero)
   void *xt = nullptr, *h1 = nullptr, *h2 = nullptr, *ystage = nullptr;
   void* yhost_dev = nullptr;    // di_recover_host staging
@@ -131,6 +132,21 @@ di_status encode_h1(CUtensorMap* map, const void* h1, int batch, int n1, int n2)
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h1) failed: %d", (int)r);
+  return DI_OK;
+}
+
+// h1 [batch][n1][n2][64] fp32 for the TF32 conv2: box = 32 channels (one 128-B swizzle row) x P x 16 rows
+di_status encode_h1_f32(CUtensorMap* map, const void* h1, int batch, int n1, int n2) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {64, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {64 * 4, (cuuint64_t)n2 * 64 * 4, (cuuint64_t)n1 * n2 * 64 * 4};
+  cuuint32_t box[4] = {32, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tf32_box_rows(), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(h1), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h1 f32) failed: %d", (int)r);
   return DI_OK;
 }
 
@@ -215,6 +231,28 @@ std::vector<uint16_t> conv2_tc_pack(const std::vector<float>& wx2) {
   return out;
 }
 
+// TF32 conv2 blocks: K-block kb = h*33 + u*3 + j (channel half h, tap row u, column-tap group v0 = 4j); row
+// v'*32 + k, 32 fp32 channels 32h..32h+31 (128 B), SWIZZLE_128B image (16-B chunk = 4 channels).  Values stay fp32:
+// the tensor core reads them as TF32.
+std::vector<float> conv2_tf32_pack(const std::vector<float>& wx2) {
+  std::vector<float> out((size_t)2 * di::C2_KBLOCKS * di::C2_KBLOCK_BYTES / 4, 0.f);
+  for (int h = 0; h < 2; ++h)
+    for (int kb = 0; kb < di::C2_KBLOCKS; ++kb) {
+      const int u = kb / 3, v0 = 4 * (kb % 3);
+      uint8_t* blk = reinterpret_cast<uint8_t*>(out.data()) + ((size_t)h * di::C2_KBLOCKS + kb) * di::C2_KBLOCK_BYTES;
+      for (int row = 0; row < 128; ++row) {
+        const int vp = row / 32, k = row % 32, b = v0 + vp;
+        for (int c = 0; c < 32; ++c) {
+          const int ci = 32 * h + c;
+          const float x = (b < K) ? wx2[(((size_t)k * 64 + ci) * K + u) * K + b] : 0.f;
+          const size_t off = (size_t)row * 128 + ((((size_t)c / 4) ^ (row & 7)) << 4) + (c % 4) * 4;
+          std::memcpy(blk + off, &x, 4);
+        }
+      }
+    }
+  return out;
+}
+
 // conv1 tensor-core blocks: block u (2 KB) = 64 filter rows x 16 column taps (v >= 11 zero), bf16, SWIZZLE_32B
 // image (16-B chunk h of row m at m*32 + ((h ^ ((m >> 2) & 1)) << 4)).  Row m = 16G + j holds filter
 // 16G + 2j (j < 8) or 16G + 2(j - 8) + 1 (j >= 8): the epilogue's 16x256b TMEM load then hands each thread the two
@@ -265,7 +303,7 @@ di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n
 
 void free_ctx(di_ctx c) {
   if (!c) return;
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -351,6 +389,16 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
         tmp = &tm;
       }
       CUDA_TRY(di::launch_conv2_tc(tmp, c->wp2, c->b2, fm, batch, c->n1, c->n2, h2, c->num_sms, st));
+    } else if (c->prec == DI_PREC_TF32) {
+      CUtensorMap tm;
+      const CUtensorMap* tmp = &c->tmH1;
+      if (h1 != c->h1 || batch != c->max_batch) {
+        di_status s = encode_h1_f32(&tm, h1, batch, c->n1, c->n2);
+        if (s != DI_OK) return s;
+        tmp = &tm;
+      }
+      CUDA_TRY(di::launch_conv2_tf32(tmp, c->wp2t, c->b2, fm, batch, c->n1, c->n2, reinterpret_cast<float*>(h2),
+                                     c->num_sms, st));
     } else {
       CUDA_TRY(di::launch_conv2_simt_f32(reinterpret_cast<const float*>(h1), c->wx2, c->b2, fm,
                                          reinterpret_cast<float*>(h2), batch, c->n1, c->n2, st));
@@ -493,6 +541,10 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       auto p3 = conv3_tc_pack(w3);
       STEP(upload(&c->wp3, p3.data(), p3.size() * 2, &c->ws_bytes));
     }
+    if (c->prec == DI_PREC_TF32) {
+      auto pt = conv2_tf32_pack(w2);
+      STEP(upload(&c->wp2t, pt.data(), pt.size() * 4, &c->ws_bytes));
+    }
     STEP(upload_bias(&c->b1, a->b1, C1, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b2, a->b2, C2, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b3, a->b3, 1, fm, a->n1, a->n2, &c->ws_bytes));
@@ -506,6 +558,14 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     if (c->prec != DI_PREC_FP32) STEP(upload(&c->ystage, nullptr, B * c->kpad * c->elt, &c->ws_bytes));
   }
   // ---- kernels / tensor maps
+  if (c->prec == DI_PREC_TF32) {
+    cudaError_t e = di::setup_conv2_tf32(a->n2);
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return fail(DI_ERR_CUDA, "setup_conv2_tf32: %s", cudaGetErrorString(e));
+    }
+    STEP(encode_h1_f32(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
+  }
   if (c->prec != DI_PREC_FP32) {
     cudaError_t e = di::setup_proxy_tc();
     if (e != cudaSuccess) {
@@ -605,7 +665,7 @@ di_status di_get_info(di_ctx c, di_info* info) {
   const bool bf16 = c->prec == DI_PREC_BF16;
   info->stage_kernels[0] = c->prec == DI_PREC_FP32 ? "k_proxy_f32" : (bf16 ? "k_proxy_tc<bf16>" : "k_proxy_tc<tf32>");
   info->stage_kernels[1] = bf16 ? "k_conv1_tc" : "k_conv_wide<conv1>";
-  info->stage_kernels[2] = bf16 ? "k_conv2_tc" : "k_conv_wide<conv2,f32>";
+  info->stage_kernels[2] = bf16 ? "k_conv2_tc" : (c->prec == DI_PREC_TF32 ? "k_conv2_tf32" : "k_conv_wide<conv2,f32>");
   info->stage_kernels[3] = bf16 ? "k_conv3_tc" : "k_conv3";
   return DI_OK;
 }

@@ -1,0 +1,239 @@
+// k_conv2_tf32.cu -- stage 2 (conv layer 2: 32 filters 11x11x64 + bias + ReLU, crop S)
+// for the TF32 mode: fp32 activations, TF32 tensor-core products (tcgen05.mma kind::tf32), fp32 accumulation.
+//
+// Same implicit-GEMM mapping as the bf16 kernel (k_conv2_tc.cu): pixels are the UMMA N dimension, four column
+// taps v' x 32 filters stack into M = 128, the B operand is a window of a zero-padded shared-memory strip and
+// output o receives sum_v' D[v'*32 + k][o - n0 + v'].  What differs:
+//   * an fp32 position row of 64 channels is 256 B = two 128-B swizzle rows, so the K dimension is split into two
+//     channel halves h (32 channels each); K-block = (h, u, v0): 66 per tile, 4 MMAs of K = 8 each;
+//   * the strip holds ONE channel half (16 rows x 74 positions x 128 B, one 4-D TMA box at channel 32h) and is
+//     reloaded for h = 1;
+//   * both tiles of a unit (<= 2 for R = 6) accumulate at once (TMEM columns [0, 256) and [256, 512)) so each
+//     16-KB weight block serves both tiles and the strip is loaded once per channel half per unit; the epilogue
+//     therefore runs between units (no TMEM double buffering).
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "sm100.cuh"
+
+namespace di {
+
+namespace {
+constexpr int R = C2_ROWS;             // output rows per unit (6)
+constexpr int WSEG = 64;
+constexpr int NT = 256;
+constexpr int OUT_PER_TILE = NT - 3;   // 253
+constexpr int WSTAGES = 4;
+constexpr int KB_HALF = C2_KBLOCKS;    // 33 K-blocks per channel half
+constexpr uint32_t WBYTES = C2_KBLOCK_BYTES;  // 16 KB: 128 rows x 32 fp32 channels
+constexpr int GUARD_ROWS = 24;
+constexpr int SPS = 36;
+constexpr int ECH = 16;
+
+struct GeoT {
+  int n1, n2, wseg, P, nrb, ncs, units;
+};
+}  // namespace
+
+__device__ __forceinline__ void ld_tail13_t(uint32_t taddr, uint32_t* r) {
+  tmem_ld8(taddr, r);
+  tmem_ld4(taddr + 8, r + 8);
+  tmem_ld1(taddr + 12, r + 12);
+}
+
+__global__ void __launch_bounds__(256, 1)
+    k_conv2_tf32(const __grid_constant__ CUtensorMap tmH1, const float* __restrict__ wpack,
+                 const float* __restrict__ bias, int fullmap, GeoT g, float* __restrict__ h2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int strip_bytes = (R + 10) * g.P * 128;
+  const int strip_alloc = (strip_bytes + GUARD_ROWS * 128 + 1023) & ~1023;
+  uint8_t* strip = smem;
+  uint8_t* wst = smem + strip_alloc;
+  float* sP = reinterpret_cast<float*>(wst + WSTAGES * WBYTES);
+
+  __shared__ uint64_t sfull, sempty, wfull[WSTAGES], wempty[WSTAGES], tfull, tempty;
+  __shared__ uint32_t tslot;
+  const int warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmH1);
+    mbar_init(&sfull, 1), mbar_init(&sempty, 1);
+    for (int s = 0; s < WSTAGES; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], 1);
+    mbar_init(&tfull, 1), mbar_init(&tempty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
+  for (int i = threadIdx.x; i < GUARD_ROWS * 128 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(strip + strip_bytes)[i] = make_uint4(0, 0, 0, 0);
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const int per_img = g.nrb * g.ncs;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ producer: strips + weights, in order
+      uint32_t wk = 0, sk = 0;
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
+        const int b = u / per_img, rem = u - b * per_img;
+        const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
+        for (int h = 0; h < 2; ++h, ++sk) {
+          if (sk > 0) mbar_wait(&sempty, (sk - 1) & 1);
+          mbar_arrive_expect_tx(&sfull, strip_bytes);
+          tma_load_4d(strip, &tmH1, &sfull, 32 * h, c0 - 5, r0 - 5, b);
+          const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack) + (size_t)h * KB_HALF * WBYTES;
+          for (int kb = 0; kb < KB_HALF; ++kb, ++wk, wsrc += WBYTES) {
+            const uint32_t st = wk % WSTAGES;
+            if (wk >= WSTAGES) mbar_wait(&wempty[st], ((wk / WSTAGES) - 1) & 1);
+            mbar_arrive_expect_tx(&wfull[st], WBYTES);
+            bulk_load(wst + st * WBYTES, wsrc, WBYTES, &wfull[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      const uint64_t bdesc0 = smem_desc(smem_u32(strip), 16, 1024, kSwizzle128B);
+      const uint64_t adesc0 = smem_desc(smem_u32(wst), 16, 1024, kSwizzle128B);
+      const uint64_t pstep = (uint64_t)g.P * 8;
+      uint32_t wk = 0, sk = 0;
+      int it = 0;
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+        const int rem = u % per_img;
+        const int r0 = (rem / g.ncs) * R;
+        const int rows = min(R, g.n1 - r0);
+        const int L = (rows - 1) * g.P + g.wseg;
+        const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;   // 1 or 2
+        const int nB = ntiles > 1 ? min(NT, (min(OUT_PER_TILE, L - OUT_PER_TILE) + 3 + 15) & ~15) : 0;
+        const int nA = min(NT, (min(OUT_PER_TILE, L) + 3 + 15) & ~15);
+        const uint32_t idA = idesc_f32acc(2, 128, nA), idB = idesc_f32acc(2, 128, nB > 0 ? nB : 16);
+        if (it > 0) mbar_wait(&tempty, (it - 1) & 1);   // the epilogue drained the previous unit
+        tc_fence_after();
+        for (int h = 0; h < 2; ++h, ++sk) {
+          mbar_wait(&sfull, sk & 1);
+          tc_fence_after();
+          uint64_t bd = bdesc0;
+          for (int uu = 0; uu < 11; ++uu, bd += pstep) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j, ++wk) {
+              const uint32_t st = wk % WSTAGES;
+              mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
+              tc_fence_after();
+              const uint64_t ad = adesc0 + (uint64_t)(st * (WBYTES >> 4));
+              const uint64_t b = bd + (uint64_t)(32 * j);
+              const uint32_t acc0 = (h | uu | j) != 0;
+              umma_tf32_ss(tmem, ad, b, idA, acc0);
+              umma_tf32_ss(tmem, ad + 2, b + 2, idA, 1);
+              umma_tf32_ss(tmem, ad + 4, b + 4, idA, 1);
+              umma_tf32_ss(tmem, ad + 6, b + 6, idA, 1);
+              if (nB > 0) {
+                const uint64_t bb = b + (uint64_t)(OUT_PER_TILE * 8);
+                umma_tf32_ss(tmem + 256, ad, bb, idB, acc0);
+                umma_tf32_ss(tmem + 256, ad + 2, bb + 2, idB, 1);
+                umma_tf32_ss(tmem + 256, ad + 4, bb + 4, idB, 1);
+                umma_tf32_ss(tmem + 256, ad + 6, bb + 6, idB, 1);
+              }
+              umma_commit(&wempty[st]);
+            }
+          }
+          umma_commit(&sempty);
+        }
+        umma_commit(&tfull);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------------------------------------- epilogue
+    const int q = warp - 4;
+    const int e = threadIdx.x - 128;
+    const int jj = e >> 3, kg = e & 7;   // output position jj of the chunk, channels 4kg..4kg+3
+    float4 bch = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!fullmap && bias) bch = *reinterpret_cast<const float4*>(bias + 4 * kg);
+    int it = 0;
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+      const int b = u / per_img, rem = u - b * per_img;
+      const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
+      const int rows = min(R, g.n1 - r0);
+      const int L = (rows - 1) * g.P + g.wseg;
+      const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
+      mbar_wait(&tfull, it & 1);
+      tc_fence_after();
+      for (int t = 0; t < ntiles; ++t) {
+        const int n0 = t * OUT_PER_TILE;
+        const int cnt = min(OUT_PER_TILE, L - n0);
+        const uint32_t tq = tmem + t * 256 + ((uint32_t)(q * 32) << 16);
+        for (int c = 0; c < cnt; c += ECH) {
+          const int nout = min(ECH, cnt - c);
+          uint32_t r[ECH];
+          if (c + q + ECH <= NT)
+            tmem_ld16(tq + c + q, r);
+          else
+            ld_tail13_t(tq + c + q, r);
+          tmem_ld_wait();
+          float* dst = sP + q * (ECH * SPS) + lane;
+#pragma unroll
+          for (int j = 0; j < ECH; ++j) dst[j * SPS] = __uint_as_float(r[j]);
+          named_bar(1, 128);
+          if (jj < nout) {
+            const int o = n0 + c + jj;
+            const int rr = o / g.P, cc = o - rr * g.P;
+            if (cc < g.wseg && c0 + cc < g.n2 && rr < rows) {
+              float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) {
+                const float4 a = *reinterpret_cast<const float4*>(sP + qq * (ECH * SPS) + jj * SPS + 4 * kg);
+                sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
+              }
+              const size_t pix = ((size_t)b * g.n1 + r0 + rr) * g.n2 + c0 + cc;
+              float4 bv = bch;
+              if (fullmap && bias) bv = *reinterpret_cast<const float4*>(bias + pix % ((size_t)g.n1 * g.n2) * 32 + 4 * kg);
+              sum.x = fmaxf(sum.x + bv.x, 0.f), sum.y = fmaxf(sum.y + bv.y, 0.f);
+              sum.z = fmaxf(sum.z + bv.z, 0.f), sum.w = fmaxf(sum.w + bv.w, 0.f);
+              *reinterpret_cast<float4*>(h2 + pix * 32 + 4 * kg) = sum;
+            }
+          }
+          named_bar(1, 128);
+        }
+      }
+      tc_fence_before();
+      if (lane == 0) mbar_arrive(&tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+static GeoT make_geo_t(int batch, int n1, int n2) {
+  GeoT g;
+  g.n1 = n1, g.n2 = n2;
+  g.wseg = n2 < WSEG ? n2 : WSEG;
+  g.P = g.wseg + 10;
+  g.nrb = (n1 + R - 1) / R;
+  g.ncs = (n2 + g.wseg - 1) / g.wseg;
+  g.units = batch * g.nrb * g.ncs;
+  return g;
+}
+
+size_t conv2_tf32_smem_bytes(int n2) {
+  const int wseg = n2 < WSEG ? n2 : WSEG, P = wseg + 10;
+  const size_t strip_alloc = ((size_t)(R + 10) * P * 128 + GUARD_ROWS * 128 + 1023) & ~(size_t)1023;
+  return strip_alloc + WSTAGES * WBYTES + 4 * ECH * SPS * 4 + 1024;
+}
+
+int conv2_tf32_box_rows() { return R + 10; }
+
+cudaError_t setup_conv2_tf32(int n2) {
+  return cudaFuncSetAttribute(k_conv2_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)conv2_tf32_smem_bytes(n2));
+}
+
+cudaError_t launch_conv2_tf32(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
+                              int n1, int n2, float* h2, int num_sms, cudaStream_t st) {
+  GeoT g = make_geo_t(batch, n1, n2);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  k_conv2_tf32<<<grid, 256, conv2_tf32_smem_bytes(n2), st>>>(*tmH1, reinterpret_cast<const float*>(wpack), bias,
+                                                             fullmap, g, h2);
+  return cudaGetLastError();
+}
+
+}  // namespace di

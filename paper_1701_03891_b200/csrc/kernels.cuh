@@ -49,6 +49,11 @@ int conv2_tc_box_rows();
 int conv2_tc_box_cols(int n2);
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st);
+size_t conv2_tf32_smem_bytes(int n2);
+int conv2_tf32_box_rows();
+cudaError_t setup_conv2_tf32(int n2);
+cudaError_t launch_conv2_tf32(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
+                              int n1, int n2, float* h2, int num_sms, cudaStream_t st);
 cudaError_t launch_conv2_simt_f32(const float* h1, const float* wx, const float* bias, int fullmap, float* h2,
                                   int batch, int n1, int n2, cudaStream_t st);
 

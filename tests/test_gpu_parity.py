@@ -83,7 +83,7 @@ def test_ragged_shapes(precision, n1, n2, m, batch):
     _check(case, out, sample_rows(batch, 8))
 
 
-@pytest.mark.parametrize("precision", ["f32", "bf16"])
+@pytest.mark.parametrize("precision", ["f32", "bf16", "tf32"])
 @pytest.mark.parametrize("bias", ["channel", "fullmap"])
 @pytest.mark.parametrize("final_relu,xcorr", [(False, False), (True, True)])
 def test_flags_and_biases(precision, bias, final_relu, xcorr):
@@ -178,7 +178,7 @@ def test_error_codes():
 
 
 # ----------------------------------------------------------------------------- per stage
-@pytest.mark.parametrize("precision", ["f32", "bf16"])
+@pytest.mark.parametrize("precision", ["f32", "bf16", "tf32"])
 def test_stages_individually(precision):
     """di_debug_stage: each stage against the oracle on the GPU's own stage input."""
     import torch
@@ -196,7 +196,7 @@ def test_stages_individually(precision):
     ctx.debug_stage(2, h1, h2, B)
     ctx.debug_stage(3, h2, xh, B)
     torch.cuda.synchronize()
-    tol = 1e-5 if precision == "f32" else 8e-3   # bf16 stage outputs are rounded to bf16 (2^-9)
+    tol = 1e-5 if precision == "f32" else 8e-3   # bf16 stage outputs are rounded to bf16 (2^-9); tf32 products
     f = lambda t: t.float().cpu().numpy().astype(np.float64)
     ref0 = oracle.proxy(case.phi, case.y).reshape(B, n1, n2)
     assert oracle.rel_l2(f(xt), ref0) <= tol
