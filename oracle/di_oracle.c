@@ -8,6 +8,7 @@
  * (paper_1701_03891_b200/csrc) and the CUDA path never calls it.
  *
  * Every function is the paper's definition written out, in the paper's order:
+ *   dio_measure     y = Phi x (the measurement model)        PAPER.md:27 (§1)
  *   dio_proxy       x_tilde = Phi^T y                        PAPER.md:121 (§4)
  *                   viewed as n1 x n2, row-major j = r*n2+c  PAPER.md:122 (§4); SURVEY.md §8(c) Q8
  *   dio_conv_layer  Eq. (1): (x_c)^k_ij = S(ReLU((W^k * x)_ij + (b^k)_ij))
@@ -32,6 +33,23 @@
 #define DIO_ERR_ARG 1
 #define DIO_ERR_DIM 2
 #define DIO_ERR_OOM 5
+
+/* y[b][i] = sum_j Phi[i][j] * x[b][j]   (y = Phi x, x vectorised row-major j = r*n2 + c).
+ * phi: [m][n] row-major; x: [batch][n]; y: [batch][m]. */
+int dio_measure(int m, int n, int batch, const double *phi, const double *x, double *y)
+{
+    if (m < 1 || n < 1 || batch < 0 || !phi || !x || !y) return DIO_ERR_ARG;
+    for (int b = 0; b < batch; ++b) {
+        const double *xb = x + (size_t)b * n;
+        double *yb = y + (size_t)b * m;
+        for (int i = 0; i < m; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < n; ++j) s += phi[(size_t)i * n + j] * xb[j];
+            yb[i] = s;
+        }
+    }
+    return DIO_OK;
+}
 
 /* x_tilde[b][j] = sum_i Phi[i][j] * y[b][i]   (x_tilde = Phi^T y).
  * phi: [m][n] row-major; y: [batch][m]; xt: [batch][n]. */

@@ -39,9 +39,10 @@ def _load():
         P = ctypes.POINTER(ctypes.c_double)
         I = ctypes.c_int
         lib.dio_proxy.argtypes = [I, I, I, P, P, P]
+        lib.dio_measure.argtypes = [I, I, I, P, P, P]
         lib.dio_conv_layer.argtypes = [I, I, I, I, I, P, P, P, I, I, I, P]
         lib.dio_forward.argtypes = [I, I, I, I, I, ctypes.POINTER(I), I, P, P, P, P, I, I, I, P, I]
-        for f in (lib.dio_proxy, lib.dio_conv_layer, lib.dio_forward):
+        for f in (lib.dio_proxy, lib.dio_measure, lib.dio_conv_layer, lib.dio_forward):
             f.restype = I
         _lib = lib
     return _lib
@@ -53,6 +54,18 @@ def _d(a):
 
 def _p(a):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if a is not None else None
+
+
+def measure(phi, x) -> np.ndarray:
+    """y = Phi x for x [B][n1][n2] (or [B][N]) -> [B][M]."""
+    phi = _d(phi)
+    m, n = phi.shape
+    x = _d(np.asarray(x).reshape(-1, n))
+    out = np.empty((x.shape[0], m), np.float64)
+    rc = _load().dio_measure(m, n, x.shape[0], _p(phi), _p(x), _p(out))
+    if rc:
+        raise ValueError(f"dio_measure status {rc}")
+    return out
 
 
 def proxy(phi, y) -> np.ndarray:

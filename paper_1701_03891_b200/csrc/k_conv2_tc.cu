@@ -83,6 +83,9 @@ __global__ void __launch_bounds__(256, 1)
   float* sP = reinterpret_cast<float*>(wst + WSTAGES * WBYTES);  // [4][32 positions][SPS]
 
   __shared__ uint64_t hfull[2], hempty[2], wfull[WSTAGES], wempty[WSTAGES], tfull[2], tempty[2];
+#ifdef DI_PROF_CONV2
+  __shared__ long long t_issue[WSTAGES];   // producer: clock64 when the copy of the stage's K-block was issued
+#endif
   __shared__ uint32_t tslot;
   const int warp = warp_id(), lane = lane_id();
 
@@ -132,6 +135,9 @@ __global__ void __launch_bounds__(256, 1)
             mbar_arrive_expect_tx(&wfull[st], WBYTES / 2);   // experiment: half the weight bytes (wrong results)
             bulk_load(wst + st * WBYTES, wsrc, WBYTES / 2, &wfull[st]);
 #else
+#ifdef DI_PROF_CONV2
+            t_issue[st] = clock64();
+#endif
             mbar_arrive_expect_tx(&wfull[st], WBYTES);
             bulk_load(wst + st * WBYTES, wsrc, WBYTES, &wfull[st]);
 #endif
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t wk = 0;
       int it = 0, ti = 0;
 #ifdef DI_PROF_CONV2
-      long long c_h = 0, c_t = 0, c_w = 0, c_w0 = 0, c_w1 = 0, c0_ = clock64();
+      long long c_h = 0, c_t = 0, c_w = 0, c_w0 = 0, c_w1 = 0, c0_ = clock64(), c_lat = 0, c_latmax = 0;
 #define PT0 long long _t0 = clock64();
 #define PT1(acc) acc += clock64() - _t0;
 #else
@@ -203,7 +209,9 @@ __global__ void __launch_bounds__(256, 1)
               const uint32_t st = wk % WSTAGES;
 #ifdef DI_PROF_CONV2
               { PT0 mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
-                if (t == 0 && uu < 3) { PT1(c_w0) } else if (t == 0) { PT1(c_w) } else { PT1(c_w1) } }
+                if (t == 0 && uu < 3) { PT1(c_w0) } else if (t == 0) { PT1(c_w) } else { PT1(c_w1) }
+                const long long lat = clock64() - *(volatile long long*)&t_issue[st];
+                c_lat += lat; c_latmax = max(c_latmax, lat); }
 #else
               mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
 #endif
@@ -232,7 +240,8 @@ __global__ void __launch_bounds__(256, 1)
 #ifdef DI_PROF_CONV2
       if (blockIdx.x % 37 == 0)
         printf("conv2 cta %d: cycles %lld strip-wait %lld tmem-wait %lld weight-wait first9 %lld tile0-rest %lld "
-               "later-tiles %lld units %d kblocks %u\n", blockIdx.x, clock64() - c0_, c_h, c_t, c_w0, c_w, c_w1, it, wk);
+               "later-tiles %lld units %d kblocks %u | issue->ready mean %lld max %lld\n", blockIdx.x, clock64() - c0_,
+               c_h, c_t, c_w0, c_w, c_w1, it, wk, c_lat / (long long)wk, c_latmax);
 #endif
     }
   } else if (warp >= 4) {  // ---------------------------------------------- epilogue

@@ -1,4 +1,6 @@
 """Pins for oracle.proxy, x_tilde = Phi^T y -- CPU only."""
+import math
+
 import numpy as np
 import pytest
 
@@ -71,3 +73,42 @@ def test_proxy_psd_and_linear():
 def test_bad_shapes_raise():
     with pytest.raises(ValueError):
         oracle.proxy(np.zeros((0, 4)), np.zeros((1, 0)))
+
+
+# ----------------------------------------------------------------------------- sensing model (NEXT-1)
+def test_measure_vs_numpy_loop_and_adjoint():
+    """y = Phi x: numpy matmul, an explicit loop on a tiny case, and the adjoint identity
+    <Phi x, y> = <x, Phi^T y> against the (independently pinned) proxy."""
+    r = np.random.default_rng(3)
+    phi = r.standard_normal((7, 12))
+    x = r.standard_normal((3, 3, 4))
+    y = oracle.measure(phi, x)
+    assert np.allclose(y, x.reshape(3, 12) @ phi.T, rtol=1e-13, atol=1e-13)
+    loop = [[sum(phi[i][j] * x.reshape(3, 12)[b][j] for j in range(12)) for i in range(7)] for b in range(3)]
+    assert np.allclose(y, np.array(loop), rtol=1e-13, atol=1e-13)
+    w = r.standard_normal((3, 7))
+    lhs = np.sum(y * w, axis=1)
+    rhs = np.sum(x.reshape(3, 12) * oracle.proxy(phi, w), axis=1)
+    assert np.allclose(lhs, rhs, rtol=1e-12)
+
+
+def test_measure_identity_and_zero():
+    x = np.arange(16, dtype=np.float64).reshape(1, 4, 4)
+    assert np.array_equal(oracle.measure(np.eye(16), x), x.reshape(1, 16))
+    assert np.all(oracle.measure(np.ones((3, 16)), np.zeros((2, 16))) == 0)
+
+
+def test_noise_snr_rule_determinism_and_noiseless():
+    """SPEC.md:168-170: +inf -> unchanged; 20 dB -> mean ||w||^2/||y||^2 within [0.005, 0.02] over 100 draws;
+    same seed -> identical vector."""
+    r = np.random.default_rng(5)
+    y = r.standard_normal((100, 410))
+    assert np.array_equal(oracle.add_noise(y, math.inf, 1), y)
+    ratios = [np.sum((oracle.add_noise(y[i:i + 1], 20.0, 7 + i) - y[i:i + 1]) ** 2) / np.sum(y[i] ** 2)
+              for i in range(100)]
+    assert 0.005 <= float(np.mean(ratios)) <= 0.02
+    assert abs(float(np.mean(ratios)) - 0.01) < 0.001    # 100 x 410 samples: tight around the target
+    assert np.array_equal(oracle.add_noise(y[:3], 20.0, 11), oracle.add_noise(y[:3], 20.0, 11))
+    assert not np.array_equal(oracle.add_noise(y[:3], 20.0, 11), oracle.add_noise(y[:3], 20.0, 12))
+    with pytest.raises(ValueError):
+        oracle.add_noise(np.zeros((1, 4)), 20.0, 1)
