@@ -92,6 +92,25 @@ di_status di_recover(di_ctx ctx, const void* y, long long ldy, int batch, float*
 di_status di_recover_host(di_ctx ctx, const void* y_host, long long ldy, int batch, float* xhat_host,
                           void* stream);
 
+/* ---- Sensing model and metrics around the recovery path --------------------------------
+ * di_measure:   y = Phi x (§1) for a batch of images with the context's Phi.
+ *               x: DEVICE [batch][n1][n2] fp32 (row-major vectorisation j = r*n2 + c, Q8);
+ *               y: DEVICE [batch][ldy], storage type of the precision (bf16 for BF16: x and Phi as bf16, fp32
+ *               accumulation, one RNE rounding; fp32 for FP32/TF32).  ldy >= m.  Asynchronous on `stream`.
+ * di_add_noise: y_b += w_b with w_b ~ N(0, sigma_b^2 I), sigma_b^2 = ||y_b||^2 / (m * 10^(snr_db/10)), i.e.
+ *               10 log10(||y||^2 / E||w||^2) = snr_db (Table 3's 20 dB noise; measurement-domain
+ *               reading DESIGN.md Q14).  Standard normal i of image b is counter b*m + i of the splitmix64/Box-Muller
+ *               stream keyed by (seed, stream 5) -- the generator of synth/rng.py.  snr_db = +inf: no-op.
+ *               y: DEVICE, storage type, in place.
+ * di_metrics:   per image, fp64: out[b] = PSNR = 10 log10(max(x_b)^2 / MSE) (+inf if MSE = 0),
+ *               out[batch + b] = NMSE = ||xhat_b - x_b||^2 / ||x_b||^2, out[2*batch + b] = success
+ *               1(NMSE <= 0.1).  xhat, x: DEVICE [batch][n1][n2] fp32; out: DEVICE [3][batch] double.
+ * batch must lie in [1, max_batch] (di_measure / di_add_noise) or >= 1 (di_metrics). */
+di_status di_measure(di_ctx ctx, const float* x, int batch, void* y, long long ldy, void* stream);
+di_status di_add_noise(di_ctx ctx, void* y, long long ldy, int batch, double snr_db, unsigned long long seed,
+                       void* stream);
+di_status di_metrics(di_ctx ctx, const float* xhat, const float* x, int batch, double* out, void* stream);
+
 /* Destroy a context (NULL -> DI_OK).  Synchronises the device before freeing. */
 di_status di_destroy(di_ctx ctx);
 

@@ -5,5 +5,6 @@ x_hat = M(y, Omega): lifting layer x_tilde = Phi^T y, then three 11x11 convoluti
 C ABI include/deepinverse.h.  This package is the ctypes binding plus the in-tree build.
 """
 from .binding import (DI_FLAG_FINAL_RELU, DI_FLAG_FULLMAP_BIAS, DI_FLAG_XCORR, EXPORTS, LIB_PATH,  # noqa: F401
-                      DeepInverse, DiError, di_create, di_create_args, di_debug_stage, di_destroy,
-                      di_last_error, di_recover, di_recover_host, di_status_string, load)
+                      DeepInverse, DiError, di_add_noise, di_create, di_create_args, di_debug_stage, di_destroy,
+                      di_last_error, di_measure, di_metrics, di_recover, di_recover_host, di_status_string,
+                      load)

@@ -23,7 +23,8 @@ PRECISIONS = {"f32": DI_PREC_FP32, "tf32": DI_PREC_TF32, "bf16": DI_PREC_BF16}
 
 # every symbol include/deepinverse.h declares (checked by tests/test_abi.py)
 EXPORTS = ["di_create", "di_recover", "di_recover_host", "di_destroy", "di_status_string", "di_last_error",
-           "di_get_info", "di_set_profiling", "di_stage_times", "di_debug_stage", "di_debug_get_phi"]
+           "di_get_info", "di_set_profiling", "di_stage_times", "di_debug_stage", "di_debug_get_phi",
+           "di_measure", "di_add_noise", "di_metrics"]
 
 
 class DiError(RuntimeError):
@@ -79,8 +80,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.di_stage_times.argtypes = [V, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I), I]
     lib.di_debug_stage.argtypes = [V, I, V, V, I, V]
     lib.di_debug_get_phi.argtypes = [V, V, LL]
+    lib.di_measure.argtypes = [V, V, I, V, LL, V]
+    lib.di_add_noise.argtypes = [V, V, LL, I, ctypes.c_double, ctypes.c_ulonglong, V]
+    lib.di_metrics.argtypes = [V, V, V, I, V, V]
     for f in ("di_create", "di_recover", "di_recover_host", "di_destroy", "di_get_info", "di_set_profiling",
-              "di_stage_times", "di_debug_stage", "di_debug_get_phi"):
+              "di_stage_times", "di_debug_stage", "di_debug_get_phi", "di_measure", "di_add_noise", "di_metrics"):
         getattr(lib, f).restype = I
     _lib = lib
     return lib
@@ -136,6 +140,19 @@ def di_debug_stage(ctx, stage: int, x_in, x_out, batch: int, stream=None):
            "di_debug_stage")
 
 
+def di_measure(ctx, x, batch: int, y, ldy: int, stream=None):
+    _check(load().di_measure(ctx, _ptr(x), batch, _ptr(y), ldy, _stream_handle(stream)), "di_measure")
+
+
+def di_add_noise(ctx, y, ldy: int, batch: int, snr_db: float, seed: int, stream=None):
+    _check(load().di_add_noise(ctx, _ptr(y), ldy, batch, float(snr_db), int(seed), _stream_handle(stream)),
+           "di_add_noise")
+
+
+def di_metrics(ctx, xhat, x, batch: int, out, stream=None):
+    _check(load().di_metrics(ctx, _ptr(xhat), _ptr(x), batch, _ptr(out), _stream_handle(stream)), "di_metrics")
+
+
 def di_status_string(s: int) -> str:
     return load().di_status_string(s).decode()
 
@@ -154,6 +171,7 @@ class DeepInverse:
         load()
         phi = np.ascontiguousarray(phi, dtype=np.float32)
         self.m = phi.shape[0]
+        self.N = phi.shape[1]
         self.n1, self.n2, self.precision, self.max_batch = n1, n2, precision, max_batch
         self.device = device
         ws = [np.ascontiguousarray(w, np.float32) for w in params.w]
@@ -193,6 +211,30 @@ class DeepInverse:
         ldy = y_host.stride(0) if hasattr(y_host, "stride") and callable(y_host.stride) else y_host.strides[0] // y_host.itemsize
         di_recover_host(self.ctx, y_host, ldy, b, xhat_host, stream)
         return xhat_host
+
+    def measure(self, x, y=None, stream=None):
+        """y = Phi x: x device fp32 [B][n1][n2] -> y device [B][m] in the storage dtype."""
+        import torch
+        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+            raise TypeError("x must be a contiguous CUDA float32 tensor [B][n1][n2]")
+        b = x.shape[0]
+        if y is None:
+            y = torch.empty((b, self.m), dtype=self.storage_dtype, device=x.device)
+        di_measure(self.ctx, x, b, y, y.stride(0), stream)
+        return y
+
+    def add_noise(self, y, snr_db: float, seed: int, stream=None):
+        """In place: y_b += N(0, ||y_b||^2 / (m 10^(snr/10))) noise (Table 3 reading, Q14)."""
+        di_add_noise(self.ctx, y, y.stride(0), y.shape[0], snr_db, seed, stream)
+        return y
+
+    def metrics(self, xhat, x, stream=None):
+        """Per-image PSNR, NMSE and success on the device, fp64: [3][B] numpy."""
+        import torch
+        b = x.shape[0]
+        out = torch.empty((3, b), dtype=torch.float64, device=x.device)
+        di_metrics(self.ctx, xhat, x, b, out, stream)
+        return out.cpu().numpy()
 
     def debug_stage(self, stage: int, x_in, x_out, batch: int, stream=None):
         di_debug_stage(self.ctx, stage, x_in, x_out, batch, stream)

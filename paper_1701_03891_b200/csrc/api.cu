@@ -86,6 +86,9 @@ struct di_ctx_s {
   void* wp1 = nullptr;          // conv1 tensor-core weight blocks (BF16 mode, SWIZZLE_32B image)
   void* wp3 = nullptr;          // conv3 tensor-core weight blocks (BF16 mode, SWIZZLE_64B image)
   void* wp2t = nullptr;         // conv2 TF32 weight blocks (TF32 mode)
+  void* phi_rm = nullptr;       // di_measure: Phi [m][npad] in the storage type (BF16/TF32; built on first use)
+  void* xs = nullptr;           // di_measure: staged x [max_batch][npad] in the storage type
+  int npad = 0;
   float *b1 = nullptr, *b2 = nullptr, *b3 = nullptr;  // per-channel or cropped full maps (nullptr = zero)
   void *xt = nullptr, *h1 = nullptr, *h2 = nullptr, *ystage = nullptr;
   void* yhost_dev = nullptr;    // di_recover_host staging
@@ -303,7 +306,7 @@ di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n
 
 void free_ctx(di_ctx c) {
   if (!c) return;
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->phi_rm, c->xs, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -645,6 +648,80 @@ di_status di_recover_host(di_ctx c, const void* y_host, long long ldy, int batch
   }
   CUDA_TRY(cudaStreamSynchronize(c->cstream));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return DI_OK;
+}
+
+// stream key of synth/rng.py: stream_key(stream, sub = 0, seed)
+static uint64_t sm64_mix_h(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+static uint64_t stream_key(uint64_t stream, uint64_t seed) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull;
+  z = sm64_mix_h(z + stream);
+  return sm64_mix_h(z ^ (0ull * 0xBF58476D1CE4E5B9ull + 0x632BE59BD9B4E019ull));
+}
+
+di_status di_measure(di_ctx c, const float* x, int batch, void* y, long long ldy, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!x || !y) return fail(DI_ERR_ARG, "x and y must be non-NULL device pointers");
+  if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (c->prec == DI_PREC_FP32) {
+    CUDA_TRY(di::launch_measure_f32(x, reinterpret_cast<const float*>(c->phi), c->m, c->N, batch,
+                                    reinterpret_cast<float*>(y), ldy, st));
+    return DI_OK;
+  }
+  const bool bf16 = c->prec == DI_PREC_BF16;
+  const int kel = 128 / (int)c->elt;                // K elements per 128-B swizzle row
+  if (!c->phi_rm) {                                 // Phi [m][npad] from the packed Phi^T, once
+    c->npad = ((c->N + kel - 1) / kel) * kel;
+    CUDA_TRY(cudaMalloc(&c->phi_rm, (size_t)c->m * c->npad * c->elt));
+    CUDA_TRY(cudaMalloc(&c->xs, (size_t)c->max_batch * c->npad * c->elt));
+    c->ws_bytes += (long long)((size_t)c->m * c->npad + (size_t)c->max_batch * c->npad) * c->elt;
+    CUDA_TRY(di::launch_untranspose(c->phi, c->m, c->N, c->kpad, c->npad, c->phi_rm, bf16, st));
+  }
+  CUDA_TRY(di::launch_stage_x(x, c->N, c->npad, batch, c->xs, bf16, st));
+  // Y[B][m] = Xs[B][npad] . Phi_rm[m][npad]^T on the tcgen05 GEMM of the lifting layer (operand roles swapped)
+  CUtensorMap tmA, tmB;
+  di_status s = encode_2d(&tmA, c->xs, bf16, c->npad, batch, c->npad, kel, 128);
+  if (s != DI_OK) return s;
+  s = encode_2d(&tmB, c->phi_rm, bf16, c->npad, c->m, c->npad, kel, 256);
+  if (s != DI_OK) return s;
+  void* out = (ldy == c->m && (reinterpret_cast<uintptr_t>(y) & 15) == 0) ? y : c->ystage;
+  CUDA_TRY(di::launch_proxy_tc(&tmA, &tmB, batch, c->m, c->npad / kel, out, !bf16, st));
+  if (out != y)
+    CUDA_TRY(cudaMemcpy2DAsync(y, (size_t)ldy * c->elt, out, (size_t)c->m * c->elt, (size_t)c->m * c->elt, batch,
+                               cudaMemcpyDeviceToDevice, st));
+  return DI_OK;
+}
+
+di_status di_add_noise(di_ctx c, void* y, long long ldy, int batch, double snr_db, unsigned long long seed,
+                       void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!y) return fail(DI_ERR_ARG, "y must be a non-NULL device pointer");
+  if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
+  if (std::isnan(snr_db)) return fail(DI_ERR_DOMAIN, "snr_db is NaN");
+  if (std::isinf(snr_db) && snr_db > 0) return DI_OK;   // noiseless
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  CUDA_TRY(di::launch_add_noise(y, ldy, c->m, batch, snr_db, stream_key(5, seed), c->prec == DI_PREC_BF16,
+                                reinterpret_cast<cudaStream_t>(stream)));
+  return DI_OK;
+}
+
+di_status di_metrics(di_ctx c, const float* xhat, const float* x, int batch, double* out, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!xhat || !x || !out) return fail(DI_ERR_ARG, "NULL device pointer");
+  if (batch < 1) return fail(DI_ERR_ARG, "batch=%d must be >= 1", batch);
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  CUDA_TRY(di::launch_metrics(xhat, x, c->N, batch, out, reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }
 

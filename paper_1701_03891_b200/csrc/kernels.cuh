@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <cstdint>
 
 namespace di {
 
@@ -65,5 +66,15 @@ int conv3_tc_box_rows();
 int conv3_tc_box_cols(int n2);
 cudaError_t launch_conv3_tc(const CUtensorMap* tmH2, const void* w3pack, const float* bias, int fullmap, int relu,
                             float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st);
+
+// sensing model and metrics (k_sense.cu)
+cudaError_t launch_stage_x(const float* x, int N, int ldo, int batch, void* out, bool bf16, cudaStream_t st);
+cudaError_t launch_untranspose(const void* phiT, int m, int N, int kpad, int ldp, void* phi, bool bf16,
+                               cudaStream_t st);
+cudaError_t launch_measure_f32(const float* x, const float* phi, int m, int N, int batch, float* y, long long ldy,
+                               cudaStream_t st);
+cudaError_t launch_add_noise(void* y, long long ldy, int m, int batch, double snr_db, uint64_t key, bool bf16,
+                             cudaStream_t st);
+cudaError_t launch_metrics(const float* xhat, const float* x, int N, int batch, double* out, cudaStream_t st);
 
 }  // namespace di
