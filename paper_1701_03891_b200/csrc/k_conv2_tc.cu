@@ -15,14 +15,16 @@
 // (one tcgen05.ld per warp), sums the 4 quadrants through shared memory, adds the bias, applies
 // ReLU, rounds to bf16 and stores NHWC h2 with 16-B coalesced stores.
 //
-// Work unit = (image b, R = 5 output rows from r0, <=64 output columns from c0).  The strip of the unit
+// Work unit = (image b, R = 6 output rows from r0, <=64 output columns from c0).  The strip of the unit
 // ((R+10) rows x (W+10) columns x 64 ch, bf16) is loaded by ONE 4-D TMA box whose out-of-bounds
 // elements are zero: that is the zero padding of Eq. (1) at the image border.
 // Positions are linear in the padded strip (pitch P = W+10); tiles of 256 positions overlap by 3.
 //
-// Roles (256 threads): warp 0 TMA producer (strip + 16-KB weight K-blocks via bulk copies, 3 stages),
-// warp 1 single-thread MMA issuer, warp 2 TMEM allocator, warps 4..7 epilogue (one TMEM lane quadrant each).
+// Roles (256 threads): warp 0 producer (strip by TMA at unit start, 16-KB weight K-blocks by bulk copies into a
+// 4-deep ring), warp 1 single-thread MMA issuer (lean loop: prebuilt descriptors), warp 2 TMEM allocator,
+// warps 4..7 epilogue (one TMEM lane quadrant each, conflict-free 16-position shared-memory transpose).
 // TMEM: two 256-column fp32 accumulators (double buffer: MMA of tile i+1 overlaps the epilogue of tile i).
+// Bound: the shared-memory port (A + B operand reads + weight fills ~ 121 B/clk of ~128), DESIGN.md §6.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -42,7 +44,7 @@ constexpr int OUT_PER_TILE = NT - 3;   // 253 complete output positions per tile
 #ifndef DI_C2_WSTAGES
 #define DI_C2_WSTAGES 4
 #endif
-constexpr int WSTAGES = DI_C2_WSTAGES;             // weight ring depth (L2 latency of a 16-KB bulk copy ~ 2 K-blocks)
+constexpr int WSTAGES = DI_C2_WSTAGES;  // weight ring depth (a 16-KB bulk copy takes ~1.4k cycles to land)
 constexpr int KBLOCKS = C2_KBLOCKS;    // 33
 constexpr uint32_t WBYTES = C2_KBLOCK_BYTES;  // 16 KB
 constexpr int GUARD_ROWS = 24;
