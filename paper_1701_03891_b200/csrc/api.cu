@@ -168,14 +168,18 @@ di_status encode_xt(CUtensorMap* map, const void* xt, int batch, int n1, int n2)
   return DI_OK;
 }
 
-di_status encode_h2(CUtensorMap* map, const void* h2, int batch, int n1, int n2) {
+// h2 [batch][n1][n2][32] for conv3: bf16 (box = all 32 channels = 64 B) or fp32 for TF32 (box = 16 channels = 64 B)
+di_status encode_h2(CUtensorMap* map, const void* h2, int batch, int n1, int n2, bool f32 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const cuuint64_t e = f32 ? 4 : 2;
   cuuint64_t dims[4] = {32, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
-  cuuint64_t strides[3] = {32 * 2, (cuuint64_t)n2 * 32 * 2, (cuuint64_t)n1 * n2 * 32 * 2};
-  cuuint32_t box[4] = {32, (cuuint32_t)di::conv3_tc_box_cols(n2), (cuuint32_t)di::conv3_tc_box_rows(), 1};
+  cuuint64_t strides[3] = {32 * e, (cuuint64_t)n2 * 32 * e, (cuuint64_t)n1 * n2 * 32 * e};
+  cuuint32_t box[4] = {(cuuint32_t)di::conv3_tc_box_ch(f32), (cuuint32_t)di::conv3_tc_box_cols(n2),
+                       (cuuint32_t)di::conv3_tc_box_rows(), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(h2), dims, strides, box, es,
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                   const_cast<void*>(h2), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h2) failed: %d", (int)r);
@@ -288,6 +292,22 @@ std::vector<uint16_t> conv3_tc_pack(const std::vector<float>& wx3) {
         const size_t off = (size_t)u * 2048 + r * 64 + ((((size_t)c / 8) ^ ((r >> 1) & 3)) << 4) + (c % 8) * 2;
         std::memcpy(base + off, &h, 2);
       }
+  return out;
+}
+
+// TF32 conv3 blocks: block (h, u) (2 KB, index h*11 + u) = 32 rows (row v < 11: tap v of tap row u) x 16 fp32
+// channels 16h..16h+15, SWIZZLE_64B image (16-B chunk = 4 channels; chunk j of row r at r*64 + ((j ^ ((r>>1)&3)) << 4)).
+std::vector<float> conv3_tf32_pack(const std::vector<float>& wx3) {
+  std::vector<float> out((size_t)2 * 11 * 2048 / 4, 0.f);
+  uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
+  for (int h = 0; h < 2; ++h)
+    for (int u = 0; u < K; ++u)
+      for (int r = 0; r < 32; ++r)
+        for (int c = 0; c < 16; ++c) {
+          const float x = r < K ? wx3[((size_t)(16 * h + c) * K + u) * K + r] : 0.f;
+          const size_t off = (size_t)(h * 11 + u) * 2048 + r * 64 + ((((size_t)c / 4) ^ ((r >> 1) & 3)) << 4) + (c % 4) * 4;
+          std::memcpy(base + off, &x, 4);
+        }
   return out;
 }
 
@@ -410,15 +430,15 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
   }
   mark(3);
   if (first <= 3 && 3 <= last) {
-    if (bf16) {
+    if (c->prec != DI_PREC_FP32) {
       CUtensorMap tm;
       const CUtensorMap* tmp = &c->tmH2;
       if (h2 != c->h2 || batch != c->max_batch) {
-        di_status s = encode_h2(&tm, h2, batch, c->n1, c->n2);
+        di_status s = encode_h2(&tm, h2, batch, c->n1, c->n2, !bf16);
         if (s != DI_OK) return s;
         tmp = &tm;
       }
-      CUDA_TRY(di::launch_conv3_tc(tmp, c->wp3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, c->num_sms, st));
+      CUDA_TRY(di::launch_conv3_tc(tmp, c->wp3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, c->num_sms, !bf16, st));
     } else {
       CUDA_TRY(di::launch_conv3_simt(h2, bf16, c->wx3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, st));
     }
@@ -547,6 +567,8 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     if (c->prec == DI_PREC_TF32) {
       auto pt = conv2_tf32_pack(w2);
       STEP(upload(&c->wp2t, pt.data(), pt.size() * 4, &c->ws_bytes));
+      auto p3 = conv3_tf32_pack(w3);
+      STEP(upload(&c->wp3, p3.data(), p3.size() * 4, &c->ws_bytes));
     }
     STEP(upload_bias(&c->b1, a->b1, C1, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b2, a->b2, C2, fm, a->n1, a->n2, &c->ws_bytes));
@@ -568,6 +590,12 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       return fail(DI_ERR_CUDA, "setup_conv2_tf32: %s", cudaGetErrorString(e));
     }
     STEP(encode_h1_f32(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
+    e = di::setup_conv13_tc(a->n2);
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return fail(DI_ERR_CUDA, "setup_conv13_tc: %s", cudaGetErrorString(e));
+    }
+    STEP(encode_h2(&c->tmH2, c->h2, a->max_batch, a->n1, a->n2, true));
   }
   if (c->prec != DI_PREC_FP32) {
     cudaError_t e = di::setup_proxy_tc();
@@ -743,7 +771,7 @@ di_status di_get_info(di_ctx c, di_info* info) {
   info->stage_kernels[0] = c->prec == DI_PREC_FP32 ? "k_proxy_f32" : (bf16 ? "k_proxy_tc<bf16>" : "k_proxy_tc<tf32>");
   info->stage_kernels[1] = bf16 ? "k_conv1_tc" : "k_conv_wide<conv1>";
   info->stage_kernels[2] = bf16 ? "k_conv2_tc" : (c->prec == DI_PREC_TF32 ? "k_conv2_tf32" : "k_conv_wide<conv2,f32>");
-  info->stage_kernels[3] = bf16 ? "k_conv3_tc" : "k_conv3";
+  info->stage_kernels[3] = c->prec != DI_PREC_FP32 ? "k_conv3_tc" : "k_conv3";
   return DI_OK;
 }
 

@@ -39,7 +39,7 @@ namespace {
 constexpr int NACC = 4;
 
 struct Geo13 {
-  int n1, n2, wseg, P, R, nrb, ncs, units;
+  int n1, n2, wseg, P, R, nrb, ncs, units, guard;   // guard: finite rows kept past each conv3 strip
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -58,7 +58,6 @@ constexpr int W1_BYTES = 11 * 64 * 32;                   // 11 tap rows x 64 fil
 // ---------------------------------------------------------------- conv3 geometry
 constexpr int R3 = C3TC_ROWS;
 constexpr int OUT3 = 256 - 10;
-constexpr int GUARD3 = 256;                              // finite rows past the strip (see below)
 constexpr int W3_BYTES = 11 * 32 * 64;                   // 11 tap rows x 32 (v) rows x 32 ch bf16
 constexpr int SROW = 267;                                // S row stride (floats), odd -> conflict-free
 }  // namespace
@@ -374,17 +373,24 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // =============================================================================================== conv3
+// TF32 = true: fp32 h2 with TF32 products.  An fp32 position row of 32 channels is 128 B, so the channels split into
+// two halves of 16 (64-B rows, the bf16 layout); the strip is loaded once per half (strip sequence sk = unit*2 + h,
+// double-buffered) and the K-loop runs half-major over the unit's (<= 2) tiles, whose accumulators stay live across
+// both halves.  BF16: one "half" of 32 channels.
+template <bool TF32>
 __global__ void __launch_bounds__(256, 1)
     k_conv3_tc(const __grid_constant__ CUtensorMap tmH2, const uint8_t* __restrict__ w3pack,
                const float* __restrict__ bias, int fullmap, int relu, Geo13 g, float* __restrict__ xhat) {
+  constexpr int NH = TF32 ? 2 : 1;
+  constexpr int WB = NH * W3_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int P = g.P;
   const int strip_bytes = (g.R + 10) * P * 64;
-  const int strip_alloc = (strip_bytes + GUARD3 * 64 + 1023) & ~1023;
-  uint8_t* wbuf = smem;                                       // 22 KB (1024-aligned size: 22528)
-  uint8_t* const strip0 = smem + W3_BYTES;  // 2 strip buffers, strip_alloc apart
-  float* S = reinterpret_cast<float*>(smem + W3_BYTES + 2 * strip_alloc);   // [11][SROW]
+  const int strip_alloc = (strip_bytes + g.guard * 64 + 1023) & ~1023;
+  uint8_t* wbuf = smem;                                       // NH x 22 KB (1024-aligned)
+  uint8_t* const strip0 = smem + WB;  // 2 strip buffers, strip_alloc apart
+  float* S = reinterpret_cast<float*>(smem + WB + 2 * strip_alloc);   // [11][SROW]
 
   __shared__ uint64_t wbar, sfull[2], sempty[2], acc_full[NACC], acc_empty[NACC];
   __shared__ uint32_t tslot;
@@ -397,10 +403,10 @@ __global__ void __launch_bounds__(256, 1)
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<256>(&tslot), tmem_relinquish();
-  // Guard rows after each strip: the B windows of the last tile of a unit read up to 245 rows past the
+  // Guard rows after each strip: the B windows of the last tile of a unit read up to g.guard rows past the
   // TMA box (their outputs are discarded), but 0 * NaN would not be: keep them finite.
   for (int s = 0; s < 2; ++s)
-    for (int i = threadIdx.x; i < GUARD3 * 64 / 16; i += blockDim.x)
+    for (int i = threadIdx.x; i < g.guard * 64 / 16; i += blockDim.x)
       reinterpret_cast<uint4*>(strip0 + s * strip_alloc + strip_bytes)[i] = make_uint4(0, 0, 0, 0);
   fence_async_smem();
   tc_fence_before();
@@ -411,66 +417,84 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ producer
-      mbar_arrive_expect_tx(&wbar, W3_BYTES);
-      bulk_load(wbuf, w3pack, W3_BYTES, &wbar);
-      int it = 0;
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+      mbar_arrive_expect_tx(&wbar, WB);
+      bulk_load(wbuf, w3pack, WB, &wbar);
+      int sk = 0;
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
         const int b = u / per_img, rem = u - b * per_img;
         const int r0 = (rem / g.ncs) * g.R, c0 = (rem % g.ncs) * g.wseg;
-        const int s = it & 1;
-        if (it >= 2) mbar_wait(&sempty[s], ((it >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&sfull[s], strip_bytes);
-        tma_load_4d(strip0 + s * strip_alloc, &tmH2, &sfull[s], 0, c0 - 5, r0 - 5, b);
+        for (int h = 0; h < NH; ++h, ++sk) {
+          const int s = sk & 1;
+          if (sk >= 2) mbar_wait(&sempty[s], ((sk >> 1) - 1) & 1);
+          mbar_arrive_expect_tx(&sfull[s], strip_bytes);
+          tma_load_4d(strip0 + s * strip_alloc, &tmH2, &sfull[s], 16 * h, c0 - 5, r0 - 5, b);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       mbar_wait(&wbar, 0);
       tc_fence_after();
-      constexpr uint32_t idesc = idesc_f32acc(1, 32, 256);
+      constexpr uint32_t idesc = idesc_f32acc(TF32 ? 2 : 1, 32, 256);
       const uint64_t adesc0 = smem_desc(smem_u32(wbuf), 16, 512, kSwizzle64B);
       const uint64_t bdesc_base = smem_desc(smem_u32(strip0), 16, 512, kSwizzle64B);
       const uint64_t bstep = (uint64_t)((P * 64) >> 4);
-      int it = 0, ti = 0;
+      int sk = 0, ti = 0;
 #ifdef DI_PROF_CONV3
       long long c_s = 0, c_a = 0, c0_ = clock64();
+      int it = 0;
 #endif
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
         const int rem = u % per_img;
         const int r0 = (rem / g.ncs) * g.R;
         const int rows = min(g.R, g.n1 - r0);
         const int L = (rows - 1) * P + g.wseg;
-        const int s = it & 1;
+        const int ntiles = (L + OUT3 - 1) / OUT3;
+        for (int h = 0; h < NH; ++h, ++sk) {
+          const int s = sk & 1;
 #ifdef DI_PROF_CONV3
-        long long t0 = clock64();
+          long long t0 = clock64();
 #endif
-        mbar_wait(&sfull[s], (it >> 1) & 1);
+          mbar_wait(&sfull[s], (sk >> 1) & 1);
 #ifdef DI_PROF_CONV3
-        c_s += clock64() - t0;
-#endif
-        tc_fence_after();
-        for (int n0 = 0; n0 < L; n0 += OUT3, ++ti) {
-          const int a = ti % NACC;
-#ifdef DI_PROF_CONV3
-          long long t1 = clock64();
-#endif
-          if (ti >= NACC) mbar_wait(&acc_empty[a], ((ti / NACC) - 1) & 1);
-#ifdef DI_PROF_CONV3
-          c_a += clock64() - t1;
+          c_s += clock64() - t0;
 #endif
           tc_fence_after();
-          const uint32_t d = tmem + a * 64;
-          uint64_t bd = bdesc_base + (uint64_t)((s * strip_alloc + n0 * 64) >> 4);
+          for (int t = 0; t < ntiles; ++t) {
+            const int tt = ti + t, a = tt % NACC;
+            if (h == 0 && tt >= NACC) {
+#ifdef DI_PROF_CONV3
+              long long t1 = clock64();
+#endif
+              mbar_wait(&acc_empty[a], ((tt / NACC) - 1) & 1);
+#ifdef DI_PROF_CONV3
+              c_a += clock64() - t1;
+#endif
+              tc_fence_after();
+            }
+            const uint32_t d = tmem + a * 64;
+            uint64_t bd = bdesc_base + (uint64_t)((s * strip_alloc + t * OUT3 * 64) >> 4);
+            const uint64_t a0 = adesc0 + (uint64_t)((h * W3_BYTES) >> 4);
 #pragma unroll
-          for (int tu = 0; tu < 11; ++tu) {
-            const uint64_t ad = adesc0 + (uint64_t)((tu * 2048) >> 4);
-            umma_ws_f16(d, ad, bd, idesc, tu != 0);
-            umma_ws_f16(d, ad + 2, bd + 2, idesc, 1);   // second K=16 half: +32 B
-            bd += bstep;
+            for (int tu = 0; tu < 11; ++tu) {
+              const uint64_t ad = a0 + (uint64_t)((tu * 2048) >> 4);
+              if (TF32) {
+                umma_ws_tf32(d, ad, bd, idesc, (h | tu) != 0);
+                umma_ws_tf32(d, ad + 2, bd + 2, idesc, 1);   // second K=8 chunk: +32 B
+              } else {
+                umma_ws_f16(d, ad, bd, idesc, tu != 0);
+                umma_ws_f16(d, ad + 2, bd + 2, idesc, 1);    // second K=16 half: +32 B
+              }
+              bd += bstep;
+            }
+            if (h == NH - 1) umma_commit(&acc_full[a]);
           }
-          umma_commit(&acc_full[a]);
+          umma_commit(&sempty[s]);
         }
-        umma_commit(&sempty[s]);
+        ti += ntiles;
+#ifdef DI_PROF_CONV3
+        ++it;
+#endif
       }
 #ifdef DI_PROF_CONV3
       if (blockIdx.x % 37 == 0)
@@ -540,6 +564,7 @@ static Geo13 make_geo13(int batch, int n1, int n2, int R, bool conv1) {
   g.nrb = ceil_div(n1, R);
   g.ncs = ceil_div(n2, g.wseg);
   g.units = batch * g.nrb * g.ncs;
+  g.guard = 0;
   return g;
 }
 
@@ -548,12 +573,21 @@ size_t conv1_tc_smem_bytes() {
   return (size_t)W1_BYTES + 2 * IM_BYTES + strips + 1024;
 }
 
-size_t conv3_tc_smem_bytes(int n2) {
+// finite guard rows past a conv3 strip: the last tile's last K-block reads positions up to
+// (ntiles - 1) * OUT3 + 10 P + 255 of a (R + 10) P-position strip
+static int conv3_guard(int wseg) {
+  const int P = wseg + 10, L = (R3 - 1) * P + wseg, nt = ceil_div(L, OUT3);
+  const int need = (nt - 1) * OUT3 + 10 * P + 256 - (R3 + 10) * P;
+  return (need > 0 ? need : 0) + 8;
+}
+
+size_t conv3_tc_smem_bytes(int n2, bool tf32) {
   const int wseg = n2 < 64 ? n2 : 64, P = wseg + 10;
-  const size_t strip_alloc = ((size_t)(R3 + 10) * P * 64 + GUARD3 * 64 + 1023) & ~(size_t)1023;
-  return (size_t)W3_BYTES + 2 * strip_alloc + 11 * SROW * 4 + 1024;
+  const size_t strip_alloc = ((size_t)(R3 + 10) * P * 64 + (size_t)conv3_guard(wseg) * 64 + 1023) & ~(size_t)1023;
+  return (size_t)(tf32 ? 2 : 1) * W3_BYTES + 2 * strip_alloc + 11 * SROW * 4 + 1024;
 }
 int conv3_tc_box_rows() { return R3 + 10; }
+int conv3_tc_box_ch(bool tf32) { return tf32 ? 16 : 32; }
 int conv3_tc_box_cols(int n2) { return (n2 < 64 ? n2 : 64) + 10; }
 
 cudaError_t setup_conv13_tc(int n2) {
@@ -562,7 +596,11 @@ cudaError_t setup_conv13_tc(int n2) {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_conv1_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)conv1_tc_smem_bytes());
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_conv3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)conv3_tc_smem_bytes(n2));
+  e = cudaFuncSetAttribute(k_conv3_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)conv3_tc_smem_bytes(n2, false));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_conv3_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)conv3_tc_smem_bytes(n2, true));
 }
 
 int conv1_tc_box_rows() { return R1 + 10; }
@@ -581,11 +619,13 @@ cudaError_t launch_conv1_tc(const CUtensorMap* tmX, const void* xt, const void* 
 }
 
 cudaError_t launch_conv3_tc(const CUtensorMap* tmH2, const void* w3pack, const float* bias, int fullmap, int relu,
-                            float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st) {
+                            float* xhat, int batch, int n1, int n2, int num_sms, bool tf32, cudaStream_t st) {
   Geo13 g = make_geo13(batch, n1, n2, R3, false);
+  g.guard = conv3_guard(g.wseg);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv3_tc<<<grid, 256, conv3_tc_smem_bytes(n2), st>>>(*tmH2, reinterpret_cast<const uint8_t*>(w3pack), bias,
-                                                         fullmap, relu, g, xhat);
+  auto k = tf32 ? k_conv3_tc<true> : k_conv3_tc<false>;
+  k<<<grid, 256, conv3_tc_smem_bytes(n2, tf32), st>>>(*tmH2, reinterpret_cast<const uint8_t*>(w3pack), bias,
+                                                      fullmap, relu, g, xhat);
   return cudaGetLastError();
 }
 

@@ -64,8 +64,9 @@ cudaError_t launch_conv3_simt(const void* h2, bool bf16, const float* wx, const 
 
 int conv3_tc_box_rows();
 int conv3_tc_box_cols(int n2);
+int conv3_tc_box_ch(bool tf32);
 cudaError_t launch_conv3_tc(const CUtensorMap* tmH2, const void* w3pack, const float* bias, int fullmap, int relu,
-                            float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st);
+                            float* xhat, int batch, int n1, int n2, int num_sms, bool tf32, cudaStream_t st);
 
 // sensing model and metrics (k_sense.cu)
 cudaError_t launch_stage_x(const float* x, int N, int ldo, int batch, void* out, bool bf16, cudaStream_t st);

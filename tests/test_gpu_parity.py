@@ -208,4 +208,7 @@ def test_stages_individually(precision):
         r2 = oracle.conv_layer(f(h1)[b].transpose(2, 0, 1), p.w[1], p.b[1], relu=True)
         assert oracle.rel_l2(f(h2)[b].transpose(2, 0, 1), r2) <= tol
         r3 = oracle.conv_layer(f(h2)[b].transpose(2, 0, 1), p.w[2], p.b[2], relu=False)
-        assert oracle.rel_l2(f(xh)[b], r3[0]) <= (1e-5 if precision == "f32" else 1e-5 * 10)
+        # stage 3 reads exact stage-2 values: fp32 FFMA ~1e-6; bf16 operands are exact, fp32 accumulation ~1e-6;
+        # TF32 truncates the fp32 h2 and weights to 10-bit mantissas (2^-11 per product)
+        tol3 = {"f32": 1e-5, "bf16": 1e-4, "tf32": 2e-3}[precision]
+        assert oracle.rel_l2(f(xh)[b], r3[0]) <= tol3
