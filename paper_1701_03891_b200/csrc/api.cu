@@ -153,15 +153,19 @@ di_status encode_h1_f32(CUtensorMap* map, const void* h1, int batch, int n1, int
   return DI_OK;
 }
 
-// x_tilde [batch][n1][n2] bf16 for the conv1 strip TMA (needs n2 % 8 == 0: 16-B row stride)
-di_status encode_xt(CUtensorMap* map, const void* xt, int batch, int n1, int n2) {
+// x_tilde [batch][n1][n2] for the conv1 strip TMA: bf16 (needs n2 % 8 == 0: 16-B row stride) or fp32 for TF32
+// (n2 % 4 == 0)
+di_status encode_xt(CUtensorMap* map, const void* xt, int batch, int n1, int n2, bool f32 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const cuuint64_t e = f32 ? 4 : 2;
   cuuint64_t dims[3] = {(cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)n2 * 2, (cuuint64_t)n1 * n2 * 2};
-  cuuint32_t box[3] = {(cuuint32_t)di::conv1_tc_box_cols(n2), (cuuint32_t)di::conv1_tc_box_rows(), 1};
+  cuuint64_t strides[2] = {(cuuint64_t)n2 * e, (cuuint64_t)n1 * n2 * e};
+  cuuint32_t box[3] = {(cuuint32_t)di::conv1_tc_box_cols(n2),
+                       (cuuint32_t)(f32 ? di::conv1_tf32_box_rows() : di::conv1_tc_box_rows()), 1};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(xt), dims, strides, box, es,
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                   const_cast<void*>(xt), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (x_tilde) failed: %d", (int)r);
@@ -295,6 +299,24 @@ std::vector<uint16_t> conv3_tc_pack(const std::vector<float>& wx3) {
   return out;
 }
 
+// TF32 conv1 blocks: block u (4 KB) = 64 filter rows (permuted as in conv1_tc_pack) x 16 fp32 column taps (v >= 11
+// zero), SWIZZLE_64B image (16-B chunk j of row m at m*64 + ((j ^ ((m >> 1) & 3)) << 4)).
+std::vector<float> conv1_tf32_pack(const std::vector<float>& wx1) {
+  std::vector<float> out(11 * 4096 / 4, 0.f);
+  uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
+  for (int u = 0; u < K; ++u)
+    for (int m = 0; m < 64; ++m) {
+      const int grp = m / 16, j = m % 16;
+      const int f = 16 * grp + (j < 8 ? 2 * j : 2 * (j - 8) + 1);
+      for (int v = 0; v < 16; ++v) {
+        const float x = v < K ? wx1[((size_t)f * K + u) * K + v] : 0.f;
+        const size_t off = (size_t)u * 4096 + m * 64 + ((((size_t)v / 4) ^ ((m >> 1) & 3)) << 4) + (v % 4) * 4;
+        std::memcpy(base + off, &x, 4);
+      }
+    }
+  return out;
+}
+
 // TF32 conv3 blocks: block (h, u) (2 KB, index h*11 + u) = 32 rows (row v < 11: tap v of tap row u) x 16 fp32
 // channels 16h..16h+15, SWIZZLE_64B image (16-B chunk = 4 channels; chunk j of row r at r*64 + ((j ^ ((r>>1)&3)) << 4)).
 std::vector<float> conv3_tf32_pack(const std::vector<float>& wx3) {
@@ -384,7 +406,17 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
   }
   mark(1);
   if (first <= 1 && 1 <= last) {
-    if (bf16) {
+    if (c->prec == DI_PREC_TF32 && c->has_tmX) {
+      CUtensorMap tm;
+      const CUtensorMap* tmp = &c->tmX;
+      if (xt != c->xt || batch != c->max_batch) {
+        di_status s = encode_xt(&tm, xt, batch, c->n1, c->n2, true);
+        if (s != DI_OK) return s;
+        tmp = &tm;
+      }
+      CUDA_TRY(di::launch_conv1_tf32(tmp, c->wp1, c->b1, fm, reinterpret_cast<float*>(h1), batch, c->n1, c->n2,
+                                     c->num_sms, st));
+    } else if (bf16) {
       CUtensorMap tm;
       const CUtensorMap* tmp = nullptr;
       if (c->has_tmX) {
@@ -569,6 +601,8 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       STEP(upload(&c->wp2t, pt.data(), pt.size() * 4, &c->ws_bytes));
       auto p3 = conv3_tf32_pack(w3);
       STEP(upload(&c->wp3, p3.data(), p3.size() * 4, &c->ws_bytes));
+      auto p1 = conv1_tf32_pack(w1);
+      STEP(upload(&c->wp1, p1.data(), p1.size() * 4, &c->ws_bytes));
     }
     STEP(upload_bias(&c->b1, a->b1, C1, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b2, a->b2, C2, fm, a->n1, a->n2, &c->ws_bytes));
@@ -596,6 +630,10 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       return fail(DI_ERR_CUDA, "setup_conv13_tc: %s", cudaGetErrorString(e));
     }
     STEP(encode_h2(&c->tmH2, c->h2, a->max_batch, a->n1, a->n2, true));
+    if (a->n2 % 4 == 0) {
+      STEP(encode_xt(&c->tmX, c->xt, a->max_batch, a->n1, a->n2, true));
+      c->has_tmX = true;
+    }
   }
   if (c->prec != DI_PREC_FP32) {
     cudaError_t e = di::setup_proxy_tc();
@@ -769,7 +807,7 @@ di_status di_get_info(di_ctx c, di_info* info) {
   info->workspace_bytes = c->ws_bytes;
   const bool bf16 = c->prec == DI_PREC_BF16;
   info->stage_kernels[0] = c->prec == DI_PREC_FP32 ? "k_proxy_f32" : (bf16 ? "k_proxy_tc<bf16>" : "k_proxy_tc<tf32>");
-  info->stage_kernels[1] = bf16 ? "k_conv1_tc" : "k_conv_wide<conv1>";
+  info->stage_kernels[1] = bf16 ? "k_conv1_tc" : (c->prec == DI_PREC_TF32 && c->has_tmX ? "k_conv1_tf32" : "k_conv_wide<conv1>");
   info->stage_kernels[2] = bf16 ? "k_conv2_tc" : (c->prec == DI_PREC_TF32 ? "k_conv2_tf32" : "k_conv_wide<conv2,f32>");
   info->stage_kernels[3] = c->prec != DI_PREC_FP32 ? "k_conv3_tc" : "k_conv3";
   return DI_OK;

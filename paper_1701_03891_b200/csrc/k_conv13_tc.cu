@@ -372,6 +372,184 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+
+// =============================================================================================== conv1, TF32
+// TF32 mode (fp32 x_tilde, TF32 products): the same mapping as k_conv1_tc with 64-B im2row rows (16 fp32 taps,
+// SWIZZLE_64B, two kind::tf32 K = 8 MMAs per tap row), R = 8 rows per unit, the strip always by TMA (needs
+// n2 % 4 == 0; otherwise the SIMT conv1 runs), fp32 h1 stores of channel pairs.
+constexpr int R1T = 8;
+constexpr int IM_ROWS_T = (R1T + 10) * 64;
+constexpr int IM_BYTES_T = IM_ROWS_T * 64;
+constexpr int W1T_BYTES = 11 * 64 * 64;                      // 11 tap rows x 64 filters x 16 fp32 taps
+constexpr int XT_STRIDE = ((R1T + 10) * (P1MAX + 8) * 4 + 128 + 127) & ~127;
+
+__global__ void __launch_bounds__(384, 1)
+    k_conv1_tf32(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ w1pack,
+                 const float* __restrict__ bias, int fullmap, Geo13 g, float* __restrict__ h1) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* wbuf = smem;                                 // 44 KB
+  uint8_t* const im0 = smem + W1T_BYTES;                // 2 im2row buffers
+  uint8_t* const xc0 = smem + W1T_BYTES + 2 * IM_BYTES_T;   // 2 strip buffers
+
+  __shared__ uint64_t wbar, im_full[2], im_empty[2], acc_full[NACC], acc_empty[NACC], xfull[2];
+  __shared__ uint32_t tslot;
+  const int warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    mbar_init(&wbar, 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&im_full[s], 64), mbar_init(&im_empty[s], 1), mbar_init(&xfull[s], 1);
+    for (int a = 0; a < NACC; ++a) mbar_init(&acc_full[a], 1), mbar_init(&acc_empty[a], 8);
+    tma_prefetch_desc(&tmX);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
+  for (int i = threadIdx.x; i < 2 * XT_STRIDE / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(xc0)[i] = 0u;
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const int per_img = g.nrb * g.ncs;
+  const int P = g.P, W = g.wseg, Q = P + 8;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ weights, once
+      mbar_arrive_expect_tx(&wbar, W1T_BYTES);
+      bulk_load(wbuf, w1pack, W1T_BYTES, &wbar);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      mbar_wait(&wbar, 0);
+      tc_fence_after();
+      const uint64_t adesc0 = smem_desc(smem_u32(wbuf), 16, 512, kSwizzle64B);
+      const uint64_t bdesc_base = smem_desc(smem_u32(im0), 16, 512, kSwizzle64B);
+      const uint64_t bstep = (uint64_t)((W * 64) >> 4);
+      int it = 0, ti = 0;
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+        const int rem = u % per_img;
+        const int r0 = (rem / g.ncs) * g.R;
+        const int npos = min(g.R, g.n1 - r0) * W;
+        const int s = it & 1;
+        mbar_wait(&im_full[s], (it >> 1) & 1);
+        tc_fence_after();
+        for (int n0 = 0; n0 < npos; n0 += 256, ++ti) {
+          const int cnt = min(256, npos - n0);
+          const int N = cnt > 128 ? 256 : (cnt > 64 ? 128 : 64);
+          const uint32_t idesc = idesc_f32acc(2, 64, N);
+          const int a = ti % NACC;
+          if (ti >= NACC) mbar_wait(&acc_empty[a], ((ti / NACC) - 1) & 1);
+          tc_fence_after();
+          const uint32_t d = tmem + a * 128;
+          uint64_t bd = bdesc_base + (uint64_t)(((s * IM_BYTES_T) + n0 * 64) >> 4);
+#pragma unroll
+          for (int tu = 0; tu < 11; ++tu) {
+            const uint64_t ad = adesc0 + (uint64_t)((tu * 4096) >> 4);
+            umma_ws_tf32(d, ad, bd, idesc, tu != 0);
+            umma_ws_tf32(d, ad + 2, bd + 2, idesc, 1);        // taps 8..15: +32 B
+            bd += bstep;
+          }
+          umma_commit(&acc_full[a]);
+        }
+        umma_commit(&im_empty[s]);
+      }
+    }
+  } else if (warp < 4) {  // ------------------------------------------- im2row builders (64 threads)
+    const int bt = threadIdx.x - 64;
+    const uint32_t wmagic = (1u << 20) / (uint32_t)W + 1;
+    int it = 0;
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+      const int s = it & 1;
+      if (it >= 2) mbar_wait(&im_empty[s], ((it >> 1) - 1) & 1);
+      if (bt == 0) {   // strip of unit `un` into buffer `buf`, one unit ahead; box starts 8 columns left (16-B rule)
+        for (int k = (it == 0 ? 0 : 1); k < 2; ++k) {
+          const int un = u + k * gridDim.x, buf = (it + k) & 1;
+          if (un >= g.units) break;
+          const int bb = un / per_img, rm = un - bb * per_img;
+          const int rr0 = (rm / g.ncs) * g.R, cc0 = (rm % g.ncs) * g.wseg;
+          mbar_arrive_expect_tx(&xfull[buf], (g.R + 10) * Q * 4);
+          tma_load_3d(xc0 + buf * XT_STRIDE, &tmX, &xfull[buf], cc0 - 8, rr0 - 5, bb);
+        }
+      }
+      mbar_wait(&xfull[s], (it >> 1) & 1);
+      // im2row row p (output position r*W + c) = strip[r][c .. c+15] = copy[r*Q + c + 3 ..]; SWIZZLE_64B:
+      // 16-B chunk j of row p at p*64 + ((j ^ ((p >> 1) & 3)) << 4)
+      const uint32_t* xw = reinterpret_cast<const uint32_t*>(xc0 + s * XT_STRIDE);
+      uint8_t* dst = im0 + s * IM_BYTES_T;
+      const int nrows = (g.R + 10) * W;
+      for (int p = bt; p < nrows; p += 64) {
+        const int r = (int)(((uint32_t)p * wmagic) >> 20), c = p - r * W;
+        const uint32_t* w = xw + r * Q + c + 3;
+        const int sw = (p >> 1) & 3;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint4*>(dst + p * 64 + ((j ^ sw) << 4)) =
+              make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+      }
+      fence_async_smem();
+      mbar_arrive(&im_full[s]);
+      named_bar(2, 64);
+    }
+  } else {  // -------------------------------------------------------- epilogue, warps 4..11 (as k_conv1_tc)
+    const int q = warp & 3, hh = (warp - 4) >> 2;
+    const int i4 = lane >> 2, cpair = 2 * (lane & 3);
+    const int ch = 16 * (2 * (q & 1) + hh) + 2 * i4;
+    const float b0 = (!fullmap && bias) ? bias[ch] : 0.f, b1 = (!fullmap && bias) ? bias[ch + 1] : 0.f;
+    const uint32_t wmagic = (1u << 20) / (uint32_t)W + 1;
+    int ti = 0;
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
+      const int b = u / per_img, rem = u - b * per_img;
+      const int r0 = (rem / g.ncs) * g.R, c0 = (rem % g.ncs) * g.wseg;
+      const int npos = min(g.R, g.n1 - r0) * W;
+      const bool linear = g.ncs == 1;
+      const size_t pix0 = ((size_t)b * g.n1 + r0) * g.n2 + c0;
+      for (int n0 = 0; n0 < npos; n0 += 256, ++ti) {
+        const int cnt = min(256, npos - n0);
+        const int N = cnt > 128 ? 256 : (cnt > 64 ? 128 : 64);
+        const int half = N / 2;
+        const int a = ti % NACC;
+        mbar_wait(&acc_full[a], (ti / NACC) & 1);
+        tc_fence_after();
+        const int pbase = n0 + (q >> 1) * half;
+        const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32 + 16 * hh) << 16);
+        for (int c = 0; c < half; c += 32) {
+          uint32_t r[16];
+          tmem_ld_16x256b_x4(taddr + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int p = pbase + c + 8 * k + cpair + e;
+              if (p >= n0 + cnt) continue;
+              size_t pix;
+              if (linear) {
+                pix = pix0 + p;
+              } else {
+                const int rr = (int)(((uint32_t)p * wmagic) >> 20), cc = p - rr * W;
+                if (c0 + cc >= g.n2) continue;
+                pix = pix0 + (size_t)rr * g.n2 + cc;
+              }
+              float v0 = __uint_as_float(r[4 * k + e]), v1 = __uint_as_float(r[4 * k + 2 + e]);
+              if (fullmap && bias) {
+                const size_t pm = pix % ((size_t)g.n1 * g.n2);
+                v0 += bias[pm * 64 + ch], v1 += bias[pm * 64 + ch + 1];
+              } else {
+                v0 += b0, v1 += b1;
+              }
+              *reinterpret_cast<float2*>(h1 + pix * 64 + ch) = make_float2(fmaxf(v0, 0.f), fmaxf(v1, 0.f));
+            }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[a]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // =============================================================================================== conv3
 // TF32 = true: fp32 h2 with TF32 products.  An fp32 position row of 32 channels is 128 B, so the channels split into
 // two halves of 16 (64-B rows, the bf16 layout); the strip is loaded once per half (strip sequence sk = unit*2 + h,
@@ -590,7 +768,22 @@ int conv3_tc_box_rows() { return R3 + 10; }
 int conv3_tc_box_ch(bool tf32) { return tf32 ? 16 : 32; }
 int conv3_tc_box_cols(int n2) { return (n2 < 64 ? n2 : 64) + 10; }
 
+size_t conv1_tf32_smem_bytes() { return (size_t)W1T_BYTES + 2 * IM_BYTES_T + 2 * XT_STRIDE + 1024; }
+int conv1_tf32_box_rows() { return R1T + 10; }
+
+cudaError_t launch_conv1_tf32(const CUtensorMap* tmX, const void* w1pack, const float* bias, int fullmap, float* h1,
+                              int batch, int n1, int n2, int num_sms, cudaStream_t st) {
+  Geo13 g = make_geo13(batch, n1, n2, R1T, true);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  k_conv1_tf32<<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack), bias,
+                                                           fullmap, g, h1);
+  return cudaGetLastError();
+}
+
 cudaError_t setup_conv13_tc(int n2) {
+  cudaError_t e0 = cudaFuncSetAttribute(k_conv1_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)conv1_tf32_smem_bytes());
+  if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaFuncSetAttribute(k_conv1_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)conv1_tc_smem_bytes());
   if (e != cudaSuccess) return e;

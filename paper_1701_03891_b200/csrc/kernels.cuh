@@ -43,6 +43,11 @@ int conv1_tc_box_cols(int n2);
 cudaError_t launch_conv1_tc(const CUtensorMap* tmX, const void* xt, const void* w1pack, const float* bias,
                             int fullmap, void* h1, int batch, int n1, int n2, int num_sms, cudaStream_t st);
 
+int conv1_tf32_box_rows();
+// TF32 mode: tmX = 3-D map of the fp32 x_tilde (n2 % 4 == 0), box (P + 8) x (8 + 10) x 1
+cudaError_t launch_conv1_tf32(const CUtensorMap* tmX, const void* w1pack, const float* bias, int fullmap, float* h1,
+                              int batch, int n1, int n2, int num_sms, cudaStream_t st);
+
 // stage 2: conv layer 2 (64 -> 32, ReLU)
 cudaError_t setup_conv2_tc(int n2);
 size_t conv2_tc_smem_bytes(int n2);
