@@ -339,6 +339,24 @@ def run_ours(args):
             "path_tflops": (PATH_FLOP_PER_PX + 2 * c.m) * c.N * B / (per_step / 1e3) / 1e12,
             "per_gpu_images_s": B / (per_step / 1e3)}
 
+    # ---------------- sensing model and metrics around the path, device-timed
+    xt_dev = torch.from_numpy(x).to(dev)
+    yb = torch.empty_like(y_dev)
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ctx.measure(xt_dev, yb)
+    torch.cuda.synchronize(dev)
+    sev[0].record(stream)
+    ctx.measure(xt_dev, yb)
+    sev[1].record(stream)
+    ctx.add_noise(yb, 20.0, 1701)
+    sev[2].record(stream)
+    mt = ctx.metrics(xhat, xt_dev)
+    sev[3].record(stream)
+    torch.cuda.synchronize(dev)
+    line["sensing"] = {"measure_ms": sev[0].elapsed_time(sev[1]), "noise_20db_ms": sev[1].elapsed_time(sev[2]),
+                       "metrics_ms_incl_d2h": sev[2].elapsed_time(sev[3]),
+                       "mean_psnr_db_random_init": float(np.mean(mt[0]))}
+
     # ---------------- CPU baseline (oracle as it stands), rank 0 at N=1 only
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
