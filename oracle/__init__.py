@@ -9,6 +9,6 @@ Parity status: every function here is pinned by tests/test_oracle_*.py
 (brute force, library routines, closed forms and invariants) -- see
 DESIGN.md §Oracle pins.
 """
-from .oracle import conv_layer, forward, lib_path, measure, proxy  # noqa: F401
+from .oracle import conv_layer, forward, lib_path, measure, proxy, train_grad  # noqa: F401
 from .sensing import add_noise, noise_key  # noqa: F401
 from .metrics import nmse, psnr, rel_l2, success  # noqa: F401

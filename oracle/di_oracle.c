@@ -16,6 +16,8 @@
  *                   similar manner" with a sum over input channels
  *
  *   dio_forward     x_tilde -> layer 1 -> layer 2 -> layer 3
+ *   dio_train_grad  MSE loss L(Omega) and dL/dOmega by reverse-mode differentiation of the literal forward
+ *                   PAPER.md:136 (§4); pinned by central finite differences (tests/test_oracle_train.py)
  *
  * Readings: '*' is the true (flipped-kernel) 2-D
  * convolution with full output size (n1+k1-1) x (n2+k2-1), zero outside the
@@ -160,5 +162,151 @@ int dio_forward(int batch, int m, int n1, int n2, int nl, const int *widths, int
         }
         free(a); free(t);
     }
+    return err;
+}
+
+/* ---------------------------------------------------------------------------------------------------------
+ * Training gradients: the MSE loss of PAPER.md:136,
+ *     L(Omega) = scale * sum_b ||M(y_b, Omega) - x_b||^2        (scale = 1/l for the paper's mean over l images)
+ * and its gradient with respect to every W_l[o][c][u][v] (true-convolution orientation of Eq. (1)) and per-channel
+ * bias b_l[o], by reverse-mode differentiation of the literal forward map:
+ *     G = F + b on the full (n1+k-1) x (n2+k-1) map, F = W * X (true convolution), Y = S(act(G)):
+ *     dG = S^T(dY) (zero outside the centred window) masked by act'(G) (ReLU: G > 0, i.e. Y > 0),
+ *     db[o] = sum dG[o],  dW[o][c][u][v] = sum_{i,j} dG[o][i][j] X[c][i-u][j-v],
+ *     dX[c][i'][j'] = sum_o sum_{u,v} W[o][c][u][v] dG[o][i'+u][j'+v].
+ * The lifting layer Phi^T is fixed, so no gradient flows into Phi.
+ * grad_w: [sum_l cout*cin*k*k], grad_b: [sum_l cout] (same concatenation as dio_forward's w_all / b_all with
+ * per-channel biases).  Per-image gradients are accumulated per thread (static schedule) and summed in thread
+ * order: deterministic for a fixed thread count. */
+static void conv_backward(int cin, int cout, int n1, int n2, int k, const double *X, const double *W,
+                          const double *Y, int relu, const double *dY, double *dW, double *db, double *dX)
+{
+    const int p = (k - 1) / 2;
+    const size_t nn = (size_t)n1 * n2;
+    double *dG = (double *)malloc(cout * nn * sizeof(double));
+    for (int o = 0; o < cout; ++o)
+        for (size_t q = 0; q < nn; ++q) {
+            double g = dY[o * nn + q];
+            if (relu && !(Y[o * nn + q] > 0.0)) g = 0.0;
+            dG[o * nn + q] = g;
+            db[o] += g;
+        }
+    /* in window coordinates (r, s) = (i - p, j - p): X[c][i-u][j-v] = X[c][r+p-u][s+p-v] */
+    for (int o = 0; o < cout; ++o)
+        for (int c = 0; c < cin; ++c)
+            for (int u = 0; u < k; ++u)
+                for (int v = 0; v < k; ++v) {
+                    double acc = 0.0;
+                    for (int r = 0; r < n1; ++r) {
+                        const int xr = r + p - u;
+                        if (xr < 0 || xr >= n1) continue;
+                        for (int s = 0; s < n2; ++s) {
+                            const int xs = s + p - v;
+                            if (xs < 0 || xs >= n2) continue;
+                            acc += dG[o * nn + (size_t)r * n2 + s] * X[c * nn + (size_t)xr * n2 + xs];
+                        }
+                    }
+                    dW[(((size_t)o * cin + c) * k + u) * k + v] += acc;
+                }
+    if (dX) {
+        memset(dX, 0, cin * nn * sizeof(double));
+        for (int o = 0; o < cout; ++o)
+            for (int c = 0; c < cin; ++c)
+                for (int u = 0; u < k; ++u)
+                    for (int v = 0; v < k; ++v) {
+                        const double wt = W[(((size_t)o * cin + c) * k + u) * k + v];
+                        for (int i = 0; i < n1; ++i) {            /* dX[c][i][j] += W dG[o][i+u-p][j+v-p] */
+                            const int gr = i + u - p;
+                            if (gr < 0 || gr >= n1) continue;
+                            for (int j = 0; j < n2; ++j) {
+                                const int gs = j + v - p;
+                                if (gs < 0 || gs >= n2) continue;
+                                dX[c * nn + (size_t)i * n2 + j] += wt * dG[o * nn + (size_t)gr * n2 + gs];
+                            }
+                        }
+                    }
+    }
+    free(dG);
+}
+
+int dio_train_grad(int batch, int m, int n1, int n2, int nl, const int *widths, int k, const double *phi,
+                   const double *y, const double *x_true, const double *w_all, const double *b_all, int final_relu,
+                   double scale, double *grad_w, double *grad_b, double *loss, int threads)
+{
+    if (batch < 1 || m < 1 || n1 < 1 || n2 < 1 || nl < 1 || nl > 63 || !widths || !phi || !y || !x_true || !w_all ||
+        !grad_w || !grad_b || !loss)
+        return DIO_ERR_ARG;
+    if (widths[0] != 1 || widths[nl] != 1 || (k % 2) == 0) return DIO_ERR_DIM;
+    const size_t nn = (size_t)n1 * n2;
+    size_t woff[64], boff[64];
+    woff[0] = boff[0] = 0;
+    int cmax = 1;
+    for (int l = 0; l < nl; ++l) {
+        woff[l + 1] = woff[l] + (size_t)widths[l + 1] * widths[l] * k * k;
+        boff[l + 1] = boff[l] + (size_t)widths[l + 1];
+        if (widths[l + 1] > cmax) cmax = widths[l + 1];
+    }
+    const size_t nw = woff[nl], nb = boff[nl];
+    const int nt = threads > 0 ? threads : 1;
+    double *acc = (double *)calloc((size_t)nt * (nw + nb + 1), sizeof(double));
+    if (!acc) return DIO_ERR_OOM;
+    int err = DIO_OK;
+#pragma omp parallel num_threads(nt)
+    {
+#ifdef _OPENMP
+        extern int omp_get_thread_num(void);
+        const int tid = omp_get_thread_num();
+#else
+        const int tid = 0;
+#endif
+        double *gw = acc + (size_t)tid * (nw + nb + 1), *gb = gw + nw, *gl = gb + nb;
+        double **act = (double **)calloc(nl + 1, sizeof(double *));
+        double *dA = (double *)malloc(cmax * nn * sizeof(double)), *dB = (double *)malloc(cmax * nn * sizeof(double));
+        int e = (act && dA && dB) ? DIO_OK : DIO_ERR_OOM;
+        for (int l = 0; l <= nl && e == DIO_OK; ++l) {
+            act[l] = (double *)malloc((size_t)widths[l] * nn * sizeof(double));
+            if (!act[l]) e = DIO_ERR_OOM;
+        }
+#pragma omp for schedule(static)
+        for (int b = 0; b < batch; ++b) {
+            if (e != DIO_OK) continue;
+            /* forward, keeping every layer's output */
+            e = dio_proxy(m, (int)nn, 1, phi, y + (size_t)b * m, act[0]);
+            for (int l = 0; l < nl && e == DIO_OK; ++l)
+                e = dio_conv_layer(widths[l], widths[l + 1], n1, n2, k, act[l], w_all + woff[l],
+                                   b_all ? b_all + boff[l] : NULL, 0, (l < nl - 1) || final_relu, 0, act[l + 1]);
+            if (e != DIO_OK) continue;
+            /* loss and dL/dx_hat = 2 scale (x_hat - x) */
+            for (size_t q = 0; q < nn; ++q) {
+                const double d = act[nl][q] - x_true[(size_t)b * nn + q];
+                *gl += scale * d * d;
+                dA[q] = 2.0 * scale * d;
+            }
+            /* backward through the conv layers; the fixed lifting layer gets no gradient */
+            for (int l = nl - 1; l >= 0; --l) {
+                conv_backward(widths[l], widths[l + 1], n1, n2, k, act[l], w_all + woff[l], act[l + 1],
+                              (l < nl - 1) || final_relu, dA, gw + woff[l], gb + boff[l], l > 0 ? dB : NULL);
+                double *t = dA; dA = dB; dB = t;
+            }
+        }
+        if (e != DIO_OK) {
+#pragma omp critical
+            err = e;
+        }
+        for (int l = 0; l <= nl; ++l) free(act ? act[l] : NULL);
+        free(act); free(dA); free(dB);
+    }
+    if (err == DIO_OK) {
+        memset(grad_w, 0, nw * sizeof(double));
+        memset(grad_b, 0, nb * sizeof(double));
+        *loss = 0.0;
+        for (int t = 0; t < nt; ++t) {                 /* fixed summation order */
+            const double *gw = acc + (size_t)t * (nw + nb + 1);
+            for (size_t i = 0; i < nw; ++i) grad_w[i] += gw[i];
+            for (size_t i = 0; i < nb; ++i) grad_b[i] += gw[nw + i];
+            *loss += gw[nw + nb];
+        }
+    }
+    free(acc);
     return err;
 }

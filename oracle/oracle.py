@@ -40,9 +40,11 @@ def _load():
         I = ctypes.c_int
         lib.dio_proxy.argtypes = [I, I, I, P, P, P]
         lib.dio_measure.argtypes = [I, I, I, P, P, P]
+        lib.dio_train_grad.argtypes = [I, I, I, I, I, ctypes.POINTER(I), I, P, P, P, P, P, I, ctypes.c_double, P, P,
+                                       P, I]
         lib.dio_conv_layer.argtypes = [I, I, I, I, I, P, P, P, I, I, I, P]
         lib.dio_forward.argtypes = [I, I, I, I, I, ctypes.POINTER(I), I, P, P, P, P, I, I, I, P, I]
-        for f in (lib.dio_proxy, lib.dio_measure, lib.dio_conv_layer, lib.dio_forward):
+        for f in (lib.dio_proxy, lib.dio_measure, lib.dio_conv_layer, lib.dio_forward, lib.dio_train_grad):
             f.restype = I
         _lib = lib
     return _lib
@@ -118,3 +120,38 @@ def forward(y, phi, params, n1, n2, final_relu=False, xcorr=False, threads=None)
     if rc:
         raise ValueError(f"dio_forward status {rc}")
     return out
+
+
+def train_grad(y, x, phi, params, n1, n2, scale=None, final_relu=False, threads=None):
+    """Loss scale * sum_b ||M(y_b) - x_b||^2 (scale defaults to 1/batch) and its gradient with respect
+    to the weights ([C_out][C_in][k][k] per layer, true-convolution orientation) and per-channel biases.
+    Returns (loss, [dW1, dW2, dW3], [db1, db2, db3])."""
+    y = _d(np.atleast_2d(y))
+    x = _d(np.asarray(x).reshape(y.shape[0], -1))
+    phi = _d(phi)
+    ws = [np.asarray(w) for w in params.w]
+    widths = [ws[0].shape[1]] + [w.shape[0] for w in ws]
+    k = ws[0].shape[-1]
+    w_all = _d(np.concatenate([w.ravel() for w in ws]))
+    b_all = _d(np.concatenate([np.asarray(b).ravel() for b in params.b])) if params.b is not None else None
+    if params.b is not None and b_all.size != sum(widths[1:]):
+        raise ValueError("training gradients need per-channel biases")
+    gw = np.empty_like(w_all)
+    gb = np.empty(sum(widths[1:]), np.float64)
+    loss = np.zeros(1, np.float64)
+    wid = (ctypes.c_int * len(widths))(*widths)
+    if scale is None:
+        scale = 1.0 / y.shape[0]
+    if threads is None:
+        threads = os.cpu_count() or 1
+    rc = _load().dio_train_grad(y.shape[0], phi.shape[0], n1, n2, len(ws), wid, k, _p(phi), _p(y), _p(x), _p(w_all),
+                                _p(b_all), int(final_relu), float(scale), _p(gw), _p(gb), _p(loss), int(threads))
+    if rc:
+        raise ValueError(f"dio_train_grad status {rc}")
+    dws, dbs, o, ob = [], [], 0, 0
+    for w in ws:
+        dws.append(gw[o:o + w.size].reshape(w.shape))
+        dbs.append(gb[ob:ob + w.shape[0]])
+        o += w.size
+        ob += w.shape[0]
+    return float(loss[0]), dws, dbs
