@@ -111,6 +111,23 @@ di_status di_add_noise(di_ctx ctx, void* y, long long ldy, int batch, double snr
                        void* stream);
 di_status di_metrics(di_ctx ctx, const float* xhat, const float* x, int batch, double* out, void* stream);
 
+/* ---- Training step (FP32 contexts with per-channel or zero biases) ------------------------
+ * Parameter vector layout (di_num_params() = 259 521 floats), the orientation given to di_create (true convolution,
+ * or cross-correlation with DI_FLAG_XCORR):  [W1 64x1x11x11 | W2 32x64x11x11 | W3 1x32x11x11 | b1 64 | b2 32 | b3 1].
+ * di_train_grad: forward on the context's current parameters, loss L = scale * sum_b ||x_hat_b - x_b||^2 (
+ *                scale = 1/l for the paper's mean over l images) into DEVICE loss[0] (double), and dL/dparams into
+ *                DEVICE grads [di_num_params()] (fp32; reductions are deterministic).  y: DEVICE [batch][ldy] fp32,
+ *                x_true: DEVICE [batch][n1][n2] fp32.  Phi (the lifting layer) is fixed and not trained.
+ *                Data-parallel training all-reduces `grads` across ranks (sum, with scale = 1/global batch) between
+ *                di_train_grad and di_sgd_step.
+ * di_sgd_step:   vel = momentum * vel + grads; params -= lr * vel; the kernels' weight layouts follow.
+ * di_get_params: DEVICE copy of the current parameters. */
+long long di_num_params(void);
+di_status di_train_grad(di_ctx ctx, const void* y, long long ldy, const float* x_true, int batch, double scale,
+                        float* grads, double* loss, void* stream);
+di_status di_sgd_step(di_ctx ctx, const float* grads, double lr, double momentum, void* stream);
+di_status di_get_params(di_ctx ctx, float* params, void* stream);
+
 /* Destroy a context (NULL -> DI_OK).  Synchronises the device before freeing. */
 di_status di_destroy(di_ctx ctx);
 

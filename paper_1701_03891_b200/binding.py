@@ -24,7 +24,8 @@ PRECISIONS = {"f32": DI_PREC_FP32, "tf32": DI_PREC_TF32, "bf16": DI_PREC_BF16}
 # every symbol include/deepinverse.h declares (checked by tests/test_abi.py)
 EXPORTS = ["di_create", "di_recover", "di_recover_host", "di_destroy", "di_status_string", "di_last_error",
            "di_get_info", "di_set_profiling", "di_stage_times", "di_debug_stage", "di_debug_get_phi",
-           "di_measure", "di_add_noise", "di_metrics"]
+           "di_measure", "di_add_noise", "di_metrics", "di_num_params", "di_train_grad", "di_sgd_step",
+           "di_get_params"]
 
 
 class DiError(RuntimeError):
@@ -83,8 +84,14 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.di_measure.argtypes = [V, V, I, V, LL, V]
     lib.di_add_noise.argtypes = [V, V, LL, I, ctypes.c_double, ctypes.c_ulonglong, V]
     lib.di_metrics.argtypes = [V, V, V, I, V, V]
+    lib.di_num_params.argtypes = []
+    lib.di_num_params.restype = LL
+    lib.di_train_grad.argtypes = [V, V, LL, V, I, ctypes.c_double, V, V, V]
+    lib.di_sgd_step.argtypes = [V, V, ctypes.c_double, ctypes.c_double, V]
+    lib.di_get_params.argtypes = [V, V, V]
     for f in ("di_create", "di_recover", "di_recover_host", "di_destroy", "di_get_info", "di_set_profiling",
-              "di_stage_times", "di_debug_stage", "di_debug_get_phi", "di_measure", "di_add_noise", "di_metrics"):
+              "di_stage_times", "di_debug_stage", "di_debug_get_phi", "di_measure", "di_add_noise", "di_metrics",
+              "di_train_grad", "di_sgd_step", "di_get_params"):
         getattr(lib, f).restype = I
     _lib = lib
     return lib
@@ -151,6 +158,23 @@ def di_add_noise(ctx, y, ldy: int, batch: int, snr_db: float, seed: int, stream=
 
 def di_metrics(ctx, xhat, x, batch: int, out, stream=None):
     _check(load().di_metrics(ctx, _ptr(xhat), _ptr(x), batch, _ptr(out), _stream_handle(stream)), "di_metrics")
+
+
+def di_num_params() -> int:
+    return int(load().di_num_params())
+
+
+def di_train_grad(ctx, y, ldy: int, x_true, batch: int, scale: float, grads, loss, stream=None):
+    _check(load().di_train_grad(ctx, _ptr(y), ldy, _ptr(x_true), batch, float(scale), _ptr(grads), _ptr(loss),
+                                _stream_handle(stream)), "di_train_grad")
+
+
+def di_sgd_step(ctx, grads, lr: float, momentum: float = 0.0, stream=None):
+    _check(load().di_sgd_step(ctx, _ptr(grads), float(lr), float(momentum), _stream_handle(stream)), "di_sgd_step")
+
+
+def di_get_params(ctx, params, stream=None):
+    _check(load().di_get_params(ctx, _ptr(params), _stream_handle(stream)), "di_get_params")
 
 
 def di_status_string(s: int) -> str:
@@ -236,6 +260,28 @@ class DeepInverse:
         di_metrics(self.ctx, xhat, x, b, out, stream)
         return out.cpu().numpy()
 
+    # ------------------------------------------------------------ training (FP32 contexts, NEXT-2)
+    def train_grad(self, y, x, scale=None, grads=None, stream=None):
+        """Loss scale * sum ||M(y) - x||^2 (scale defaults to 1/batch) and its gradient (device fp32
+        [di_num_params()]).  Returns (loss tensor (device, float64 [1]), grads)."""
+        import torch
+        b = y.shape[0]
+        if grads is None:
+            grads = torch.empty(di_num_params(), dtype=torch.float32, device=y.device)
+        loss = torch.empty(1, dtype=torch.float64, device=y.device)
+        di_train_grad(self.ctx, y, y.stride(0), x, b, 1.0 / b if scale is None else scale, grads, loss, stream)
+        return loss, grads
+
+    def sgd_step(self, grads, lr: float, momentum: float = 0.0, stream=None):
+        di_sgd_step(self.ctx, grads, lr, momentum, stream)
+
+    def params(self, stream=None):
+        """Current parameters as numpy arrays ([W1, W2, W3], [b1, b2, b3]) in the orientation given at creation."""
+        import torch
+        p = torch.empty(di_num_params(), dtype=torch.float32, device=f"cuda:{self.device}")
+        di_get_params(self.ctx, p, stream)
+        return split_params(p.cpu().numpy())
+
     def debug_stage(self, stage: int, x_in, x_out, batch: int, stream=None):
         di_debug_stage(self.ctx, stage, x_in, x_out, batch, stream)
 
@@ -272,3 +318,17 @@ class DeepInverse:
             self.close()
         except Exception:
             pass
+
+
+PARAM_SHAPES = [(64, 1, 11, 11), (32, 64, 11, 11), (1, 32, 11, 11)]
+
+
+def split_params(flat):
+    """[W1 | W2 | W3 | b1 | b2 | b3] -> ([W1, W2, W3], [b1, b2, b3]) (views of `flat`)."""
+    ws, o = [], 0
+    for sh in PARAM_SHAPES:
+        n = int(np.prod(sh))
+        ws.append(flat[o:o + n].reshape(sh))
+        o += n
+    bs = [flat[o:o + 64], flat[o + 64:o + 96], flat[o + 96:o + 97]]
+    return ws, bs

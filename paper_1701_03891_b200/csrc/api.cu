@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <array>
 #include <new>
 #include <vector>
@@ -86,6 +87,13 @@ struct di_ctx_s {
   void* wp1 = nullptr;          // conv1 tensor-core weight blocks (BF16 mode, SWIZZLE_32B image)
   void* wp3 = nullptr;          // conv3 tensor-core weight blocks (BF16 mode, SWIZZLE_64B image)
   void* wp2t = nullptr;         // conv2 TF32 weight blocks (TF32 mode)
+  // training (FP32 contexts with per-channel biases): parameters in the API orientation, momentum, backward
+  // weight layouts and the backward workspace (allocated on the first di_train_grad)
+  float* params = nullptr;      // [W1 | W2 | W3 | b1 | b2 | b3], di::N_PARAMS
+  float* vel = nullptr;
+  float *wt2 = nullptr, *wt3 = nullptr;
+  float *xh_ws = nullptr, *dxh = nullptr, *dh1 = nullptr, *dh2 = nullptr, *part_w = nullptr, *part_b = nullptr;
+  double* loss_img = nullptr;
   void* phi_rm = nullptr;       // di_measure: Phi [m][npad] in the storage type (BF16/TF32; built on first use)
   void* xs = nullptr;           // di_measure: staged x [max_batch][npad] in the storage type
   int npad = 0;
@@ -348,7 +356,8 @@ di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n
 
 void free_ctx(di_ctx c) {
   if (!c) return;
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->phi_rm, c->xs, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->phi_rm, c->xs, c->params, c->vel,
+                c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -607,6 +616,20 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     STEP(upload_bias(&c->b1, a->b1, C1, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b2, a->b2, C2, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b3, a->b3, 1, fm, a->n1, a->n2, &c->ws_bytes));
+    if (c->prec == DI_PREC_FP32 && !fm) {   // trainable context: parameters in the API orientation
+      std::vector<float> prm(di::N_PARAMS, 0.f);
+      const size_t n1w = (size_t)C1 * K * K, n2w = (size_t)C2 * C1 * K * K, n3w = (size_t)C2 * K * K;
+      std::memcpy(prm.data(), a->w1, n1w * 4);
+      std::memcpy(prm.data() + n1w, a->w2, n2w * 4);
+      std::memcpy(prm.data() + n1w + n2w, a->w3, n3w * 4);
+      float* pb = prm.data() + n1w + n2w + n3w;
+      if (a->b1) std::memcpy(pb, a->b1, C1 * 4);
+      if (a->b2) std::memcpy(pb + C1, a->b2, C2 * 4);
+      if (a->b3) std::memcpy(pb + C1 + C2, a->b3, 4);
+      STEP(upload(&c->params, prm.data(), prm.size() * 4, &c->ws_bytes));
+      STEP(upload(&c->vel, nullptr, prm.size() * 4, &c->ws_bytes));
+      CUDA_TRY(cudaMemset(c->vel, 0, prm.size() * 4));
+    }
   }
   // ---- workspace
   {
@@ -790,6 +813,99 @@ di_status di_metrics(di_ctx c, const float* xhat, const float* x, int batch, dou
   CUDA_TRY(di::launch_metrics(xhat, x, c->N, batch, out, reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }
+
+// ---------------------------------------------------------------------------------------------- training
+static di_status train_alloc(di_ctx c) {
+  if (c->dxh) return DI_OK;
+  const size_t B = (size_t)c->max_batch, N = (size_t)c->N;
+  auto al = [&](auto** p, size_t bytes) -> di_status {
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+    c->ws_bytes += (long long)bytes;
+    return DI_OK;
+  };
+  di_status s;
+  if ((s = al(&c->wt2, (size_t)C2 * K * K * C1 * 4)) != DI_OK) return s;
+  if ((s = al(&c->wt3, (size_t)K * K * C2 * 4)) != DI_OK) return s;
+  if ((s = al(&c->xh_ws, B * N * 4)) != DI_OK) return s;
+  if ((s = al(&c->dxh, B * N * 4)) != DI_OK) return s;
+  if ((s = al(&c->dh2, B * N * C2 * 4)) != DI_OK) return s;
+  if ((s = al(&c->dh1, B * N * C1 * 4)) != DI_OK) return s;
+  const size_t pw = std::max({(size_t)(di::WGRAD_CHUNKS / 4) * C2 * K * K, (size_t)(di::WGRAD_CHUNKS / 32) * C2 * C1 * K * K,
+                              (size_t)(di::WGRAD_CHUNKS / 4) * C1 * K * K});
+  if ((s = al(&c->part_w, pw * 4)) != DI_OK) return s;
+  if ((s = al(&c->part_b, (size_t)di::WGRAD_CHUNKS * C1 * 4)) != DI_OK) return s;
+  if ((s = al(&c->loss_img, B * 8)) != DI_OK) return s;
+  // backward layouts (and the forward ones, identical to di_create's) from the parameters
+  CUDA_TRY(di::launch_sgd_repack(c->params, nullptr, c->vel, di::N_PARAMS, 0.f, 0.f, !(c->flags & DI_FLAG_XCORR),
+                                 c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2, c->b3, 0));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return DI_OK;
+}
+
+static di_status train_check(di_ctx c) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (c->prec != DI_PREC_FP32 || !c->params)
+    return fail(DI_ERR_ARG, "training needs a DI_PREC_FP32 context with per-channel (or zero) biases");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  if (!c->b1 || !c->b2 || !c->b3) {   // trainable biases need storage even when created zero
+    if (!c->b1) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->b1), C1 * 4));
+    if (!c->b2) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->b2), C2 * 4));
+    if (!c->b3) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->b3), 4));
+  }
+  return train_alloc(c);
+}
+
+di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_true, int batch, double scale,
+                        float* grads, double* loss, void* stream) {
+  di_status s = train_check(c);
+  if (s != DI_OK) return s;
+  if (!y || !x_true || !grads || !loss) return fail(DI_ERR_ARG, "NULL device pointer");
+  if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int flip = !(c->flags & DI_FLAG_XCORR);
+  const int relu3 = (c->flags & DI_FLAG_FINAL_RELU) ? 1 : 0;
+  // forward, keeping x_tilde, h1, h2 (post-ReLU) in the workspace
+  s = run_stages(c, 0, 3, y, ldy, batch, c->xt, c->h1, c->h2, c->xh_ws, st);
+  if (s != DI_OK) return s;
+  const size_t n1w = (size_t)C1 * K * K, n2w = (size_t)C2 * C1 * K * K, n3w = (size_t)C2 * K * K;
+  float* gb = grads + n1w + n2w + n3w;
+  CUDA_TRY(di::launch_loss_grad(c->xh_ws, x_true, c->N, batch, scale, c->dxh, c->loss_img, loss, st));
+  if (relu3)   // dG3 = dx_hat * ReLU'(x_hat): the mask is applied by the layer-3 dgrad input convention below
+    CUDA_TRY(di::launch_dgrad_mask(c->dxh, c->xh_ws, (size_t)batch * c->N, st));
+  const float* xt = reinterpret_cast<const float*>(c->xt);
+  const float* h1 = reinterpret_cast<const float*>(c->h1);
+  const float* h2 = reinterpret_cast<const float*>(c->h2);
+  CUDA_TRY(di::launch_wgrad(3, h2, c->dxh, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w + n2w,
+                            gb + C1 + C2, st));
+  CUDA_TRY(di::launch_dgrad3_f32(c->dxh, c->wt3, h2, c->dh2, batch, c->n1, c->n2, st));
+  CUDA_TRY(di::launch_wgrad(2, h1, c->dh2, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w, gb + C1,
+                            st));
+  CUDA_TRY(di::launch_dgrad2_f32(c->dh2, c->wt2, h1, c->dh1, batch, c->n1, c->n2, st));
+  CUDA_TRY(di::launch_wgrad(1, xt, c->dh1, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads, gb, st));
+  return DI_OK;
+}
+
+di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, void* stream) {
+  di_status s = train_check(c);
+  if (s != DI_OK) return s;
+  if (!grads) return fail(DI_ERR_ARG, "grads is NULL");
+  if (!(lr >= 0.0) || !(momentum >= 0.0 && momentum < 1.0)) return fail(DI_ERR_DOMAIN, "lr >= 0, 0 <= momentum < 1");
+  CUDA_TRY(di::launch_sgd_repack(c->params, grads, c->vel, di::N_PARAMS, (float)lr, (float)momentum,
+                                 !(c->flags & DI_FLAG_XCORR), c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2,
+                                 c->b3, reinterpret_cast<cudaStream_t>(stream)));
+  return DI_OK;
+}
+
+di_status di_get_params(di_ctx c, float* params, void* stream) {
+  if (!c || !params) return fail(DI_ERR_ARG, "NULL argument");
+  if (!c->params) return fail(DI_ERR_ARG, "not a trainable (FP32, per-channel bias) context");
+  CUDA_TRY(cudaMemcpyAsync(params, c->params, (size_t)di::N_PARAMS * 4, cudaMemcpyDeviceToDevice,
+                           reinterpret_cast<cudaStream_t>(stream)));
+  return DI_OK;
+}
+
+long long di_num_params(void) { return di::N_PARAMS; }
 
 di_status di_destroy(di_ctx c) {
   if (!c) return DI_OK;

@@ -29,6 +29,7 @@ __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return _
 template <typename Tin, typename Tout, int CIN, int COUT, int CO_T, int CI_CHUNK>
 __global__ void __launch_bounds__(256)
     k_conv_wide(const Tin* __restrict__ in, const float* __restrict__ wx, const float* __restrict__ bias, int fullmap,
+                const Tout* __restrict__ mask,
                 int relu, Tout* __restrict__ out, int n1, int n2) {
   constexpr int TH = 8, TW = 32, PX = 4;
   constexpr int HT = TH + 10, WT = TW + 10;
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(256)
       if (bias) bv = fullmap ? bias[((size_t)oy * n2 + ox) * COUT + co] : bias[co];
       v[c] = acc[p][c] + bv;
       if (relu) v[c] = fmaxf(v[c], 0.f);
+      if (mask && !(static_cast<float>(mask[pix * COUT + co]) > 0.f)) v[c] = 0.f;   // backward: ReLU'(forward)
     }
     Tout* dst = out + pix * COUT + cg * CO_T;
     if constexpr (sizeof(Tout) == 2) {
@@ -137,15 +139,15 @@ __global__ void __launch_bounds__(256)
 
 template <typename Tin, typename Tout, int CIN, int COUT, int CO_T, int CI_CHUNK>
 static cudaError_t launch_wide(const void* in, const float* wx, const float* bias, int fullmap, int relu, void* out,
-                               int batch, int n1, int n2, cudaStream_t st) {
+                               int batch, int n1, int n2, cudaStream_t st, const void* mask = nullptr) {
   constexpr int TH = 8, TW = 32;
   const size_t smem = (size_t)(CI_CHUNK * (TH + 10) * (TW + 10) + CI_CHUNK * 121 * COUT) * sizeof(float);
   auto k = k_conv_wide<Tin, Tout, CIN, COUT, CO_T, CI_CHUNK>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((n2 + TW - 1) / TW, (n1 + TH - 1) / TH, batch);
-  k<<<grid, 256, smem, st>>>(reinterpret_cast<const Tin*>(in), wx, bias, fullmap, relu, reinterpret_cast<Tout*>(out),
-                             n1, n2);
+  k<<<grid, 256, smem, st>>>(reinterpret_cast<const Tin*>(in), wx, bias, fullmap, reinterpret_cast<const Tout*>(mask),
+                             relu, reinterpret_cast<Tout*>(out), n1, n2);
   return cudaGetLastError();
 }
 
@@ -154,6 +156,17 @@ cudaError_t launch_conv1_simt(const void* xt, bool bf16, const float* wx, const 
   if (bf16)
     return launch_wide<__nv_bfloat16, __nv_bfloat16, 1, 64, 16, 1>(xt, wx, bias, fullmap, 1, h1, batch, n1, n2, st);
   return launch_wide<float, float, 1, 64, 16, 1>(xt, wx, bias, fullmap, 1, h1, batch, n1, n2, st);
+}
+
+// training (k_train.cu): 'same' cross-correlations that transport gradients back through conv layers 3 and 2,
+// masked by ReLU'(forward activation): d_out[p][co] = 1(mask > 0) * sum wt[ci][a][b][co] d_in[p + (a-5, b-5)][ci]
+cudaError_t launch_dgrad3_f32(const float* dxhat, const float* wt3, const float* h2, float* dh2, int batch, int n1,
+                              int n2, cudaStream_t st) {
+  return launch_wide<float, float, 1, 32, 8, 1>(dxhat, wt3, nullptr, 0, 0, dh2, batch, n1, n2, st, h2);
+}
+cudaError_t launch_dgrad2_f32(const float* dh2, const float* wt2, const float* h1, float* dh1, int batch, int n1,
+                              int n2, cudaStream_t st) {
+  return launch_wide<float, float, 32, 64, 16, 2>(dh2, wt2, nullptr, 0, 0, dh1, batch, n1, n2, st, h1);
 }
 
 cudaError_t launch_conv2_simt_f32(const float* h1, const float* wx, const float* bias, int fullmap, float* h2,

@@ -1,0 +1,247 @@
+// k_train.cu -- the training step of DeepInverse for fp32 contexts:
+//   loss      L = scale * sum_b ||x_hat_b - x_b||^2                       (scale = 1/l)
+//   gradient  reverse-mode through the three conv layers of Eq. (1); the lifting layer
+//             Phi^T is fixed and receives none
+//   update    plain SGD with optional momentum ("backpropagation"; the optimiser is unstated)
+// In the kernels' cross-correlation orientation (wx[co][ci][a][b], 'same' zero padding), with dG = dY * ReLU'(Y):
+//   db[co]             = sum_{b,p} dG[p][co]
+//   dwx[co][ci][a][b]  = sum_{b,p} dG[p][co] * X[p + (a-5, b-5)][ci]        (k_wgrad, this file)
+//   dX[p][ci]          = sum_{co,a,b} wx[co][ci][10-a][10-b] dG[p + (a-5, b-5)][co]   (k_conv_wide with transposed,
+//                        flipped weights and the previous activation as mask: k_conv_simt.cu)
+// Reductions over pixels are two-level and deterministic: fp32 per block over its pixel tiles, then fp64 over
+// blocks in a fixed order (k_wgrad_reduce).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace di {
+
+namespace {
+constexpr int TH = 8, TW = 32;       // pixel tile
+constexpr int KS = 11;
+}  // namespace
+
+// ----------------------------------------------------------------------------- loss and dL/dx_hat
+// one block per image: dxhat = 2 scale (xhat - x); per-image loss partial (fp64) to loss_img[b]
+__global__ void __launch_bounds__(256) k_loss_grad(const float* __restrict__ xhat, const float* __restrict__ x, int N,
+                                                   double scale, float* __restrict__ dxhat,
+                                                   double* __restrict__ loss_img) {
+  __shared__ double red[8];
+  const size_t off = (size_t)blockIdx.x * N;
+  double acc = 0.0;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    const float d = xhat[off + j] - x[off + j];
+    acc += (double)d * d;
+    dxhat[off + j] = (float)(2.0 * scale) * d;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    loss_img[blockIdx.x] = scale * t;
+  }
+}
+
+// dG3 = dx_hat * 1(x_hat > 0) when the last layer applies ReLU (DI_FLAG_FINAL_RELU)
+__global__ void k_mask(float* __restrict__ d, const float* __restrict__ y, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    if (!(y[i] > 0.f)) d[i] = 0.f;
+}
+cudaError_t launch_dgrad_mask(float* d, const float* y, size_t n, cudaStream_t st) {
+  k_mask<<<1184, 256, 0, st>>>(d, y, n);
+  return cudaGetLastError();
+}
+
+// sum of per-image losses in image order (deterministic) -> loss[0]
+__global__ void k_sum_f64(const double* __restrict__ v, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += v[i];
+    *out = t;
+  }
+}
+
+cudaError_t launch_loss_grad(const float* xhat, const float* x, int N, int batch, double scale, float* dxhat,
+                             double* loss_img, double* loss, cudaStream_t st) {
+  k_loss_grad<<<batch, 256, 0, st>>>(xhat, x, N, scale, dxhat, loss_img);
+  k_sum_f64<<<1, 32, 0, st>>>(loss_img, batch, loss);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- weight gradients
+// Block (ci-chunk, co-chunk) x pixel-tile chunk; thread (co_l, ci_l, ag) accumulates the taps (a, b) with
+// a = ag, ag + 4, ag + 8 (< 11) and all 11 b for its (co, ci) over the block's pixel tiles: per tap row a and pixel
+// row r, one 42-wide X row in registers slides under the 32 dG values of that row (352 FMAs per 74 loads).
+// Threads with ci_l = 0, ag = 0 of the ci-chunk-0 blocks also sum dG for the bias gradient.
+template <int CIN, int COUT, int CI_T, int CO_T>
+__global__ void __launch_bounds__(CI_T * CO_T * 4)
+    k_wgrad(const float* __restrict__ X, const float* __restrict__ dG, int batch, int n1, int n2, int nchunk,
+            float* __restrict__ part_w, float* __restrict__ part_b) {
+  constexpr int NT = CI_T * CO_T * 4;
+  constexpr int HT = TH + 10, WT = TW + 10;
+  __shared__ float sx[CI_T][HT][WT];
+  __shared__ float sg[CO_T][TH][TW];
+  const int ci0 = (blockIdx.x % (CIN / CI_T)) * CI_T, co0 = (blockIdx.x / (CIN / CI_T)) * CO_T;
+  const int chunk = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int ag = tid / (CI_T * CO_T), rem = tid % (CI_T * CO_T);
+  const int co_l = rem / CI_T, ci_l = rem % CI_T;
+  const bool do_bias = ci0 == 0 && ci_l == 0 && ag == 0;
+  float acc[3][KS];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < KS; ++j) acc[i][j] = 0.f;
+  float bacc = 0.f;
+  const int tx = (n2 + TW - 1) / TW, ty = (n1 + TH - 1) / TH;
+  const long long ntiles = (long long)batch * tx * ty;
+  for (long long t = chunk; t < ntiles; t += nchunk) {
+    const int b = (int)(t / (tx * ty)), tr = (int)(t % (tx * ty));
+    const int y0 = (tr / tx) * TH, x0 = (tr % tx) * TW;
+    __syncthreads();
+    for (int e = tid; e < CI_T * HT * WT; e += NT) {
+      const int c = e / (HT * WT), r2 = e % (HT * WT), yy = r2 / WT, xx = r2 % WT;
+      const int gy = y0 + yy - 5, gx = x0 + xx - 5;
+      sx[c][yy][xx] = (gy >= 0 && gy < n1 && gx >= 0 && gx < n2)
+                          ? X[(((size_t)b * n1 + gy) * n2 + gx) * CIN + ci0 + c] : 0.f;
+    }
+    for (int e = tid; e < CO_T * TH * TW; e += NT) {
+      const int c = e / (TH * TW), r2 = e % (TH * TW), yy = r2 / TW, xx = r2 % TW;
+      const int gy = y0 + yy, gx = x0 + xx;
+      sg[c][yy][xx] = (gy < n1 && gx < n2) ? dG[(((size_t)b * n1 + gy) * n2 + gx) * COUT + co0 + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ai = 0; ai < 3; ++ai) {
+      const int a = ag + 4 * ai;
+      if (a >= KS) continue;
+#pragma unroll 1
+      for (int r = 0; r < TH; ++r) {
+        float xr[WT];
+#pragma unroll
+        for (int j = 0; j < WT; ++j) xr[j] = sx[ci_l][r + a][j];
+#pragma unroll
+        for (int px = 0; px < TW; ++px) {
+          const float g = sg[co_l][r][px];
+#pragma unroll
+          for (int bb = 0; bb < KS; ++bb) acc[ai][bb] = fmaf(g, xr[px + bb], acc[ai][bb]);
+        }
+      }
+    }
+    if (do_bias)
+      for (int i = 0; i < TH * TW; ++i) bacc += sg[co_l][i / TW][i % TW];
+  }
+  // partial[chunk][co][ci][a][b]
+  float* pw = part_w + (size_t)chunk * COUT * CIN * KS * KS;
+#pragma unroll
+  for (int ai = 0; ai < 3; ++ai) {
+    const int a = ag + 4 * ai;
+    if (a >= KS) continue;
+#pragma unroll
+    for (int bb = 0; bb < KS; ++bb)
+      pw[(((size_t)(co0 + co_l) * CIN + ci0 + ci_l) * KS + a) * KS + bb] = acc[ai][bb];
+  }
+  if (do_bias) part_b[(size_t)chunk * COUT + co0 + co_l] = bacc;
+}
+
+// dW (API orientation) = sum over chunks (fp64, chunk order); xcorr-orientation tap (a, b) is the user's (u, v) =
+// (10 - a, 10 - b) unless the context was created with DI_FLAG_XCORR
+__global__ void k_wgrad_reduce(const float* __restrict__ part_w, const float* __restrict__ part_b, int nchunk,
+                               int nw, int nb, int flip, float* __restrict__ gw, float* __restrict__ gb) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw + nb; i += gridDim.x * blockDim.x) {
+    double t = 0.0;
+    if (i < nw) {
+      for (int c = 0; c < nchunk; ++c) t += part_w[(size_t)c * nw + i];
+      const int tap = i % (KS * KS), base = i - tap, a = tap / KS, b = tap % KS;
+      gw[base + (flip ? (KS - 1 - a) * KS + (KS - 1 - b) : tap)] = (float)t;
+    } else {
+      const int j = i - nw;
+      for (int c = 0; c < nchunk; ++c) t += part_b[(size_t)c * nb + j];
+      gb[j] = (float)t;
+    }
+  }
+}
+
+template <int CIN, int COUT, int CI_T, int CO_T>
+static cudaError_t wgrad(const float* X, const float* dG, int batch, int n1, int n2, int nchunk, float* part_w,
+                         float* part_b, int flip, float* gw, float* gb, cudaStream_t st) {
+  dim3 grid((CIN / CI_T) * (COUT / CO_T), nchunk);
+  k_wgrad<CIN, COUT, CI_T, CO_T><<<grid, CI_T * CO_T * 4, 0, st>>>(X, dG, batch, n1, n2, nchunk, part_w, part_b);
+  const int nw = COUT * CIN * KS * KS;
+  k_wgrad_reduce<<<(nw + COUT + 255) / 256, 256, 0, st>>>(part_w, part_b, nchunk, nw, COUT, flip, gw, gb);
+  return cudaGetLastError();
+}
+
+// layer 3: X = h2 (32 ch), dG = dx_hat (1 ch); layer 2: X = h1 (64), dG = dh2 (32); layer 1: X = x_tilde (1),
+// dG = dh1 (64).  part_w / part_b: scratch of WGRAD_CHUNKS x (weights / biases of the layer).
+cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, int n1, int n2, float* part_w,
+                         float* part_b, int flip, float* gw, float* gb, cudaStream_t st) {
+  // (CI_T, CO_T) keep the static tiles under 48 KB; grid.x * nchunk ~ WGRAD_CHUNKS blocks
+  switch (layer) {
+    case 3: return wgrad<32, 1, 8, 1>(X, dG, batch, n1, n2, WGRAD_CHUNKS / 4, part_w, part_b, flip, gw, gb, st);
+    case 2: return wgrad<64, 32, 8, 8>(X, dG, batch, n1, n2, WGRAD_CHUNKS / 32, part_w, part_b, flip, gw, gb, st);
+    default: return wgrad<1, 64, 1, 16>(X, dG, batch, n1, n2, WGRAD_CHUNKS / 4, part_w, part_b, flip, gw, gb, st);
+  }
+}
+
+// ----------------------------------------------------------------------------- SGD and weight repacking
+// params / grads / vel: [W1 (64*121) | W2 (32*64*121) | W3 (32*121) | b1 (64) | b2 (32) | b3 (1)] in the API
+// orientation.  vel = momentum * vel + grad; param -= lr * vel.
+__global__ void k_sgd(float* __restrict__ params, const float* __restrict__ grads, float* __restrict__ vel, int n,
+                      float lr, float momentum) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float v = momentum * vel[i] + grads[i];
+    vel[i] = v;
+    params[i] -= lr * v;
+  }
+}
+
+// from the API-orientation parameters: the forward SIMT layouts wx_l[ci][a][b][co] (cross-correlation taps), the
+// backward layouts wt3[0][a][b][c] = wx3[0][c][10-a][10-b] and wt2[k][a][b][c] = wx2[k][c][10-a][10-b] (co <-> ci
+// swapped), and the per-channel bias arrays
+__global__ void k_repack(const float* __restrict__ params, int flip, float* __restrict__ wx1, float* __restrict__ wx2,
+                         float* __restrict__ wx3, float* __restrict__ wt2, float* __restrict__ wt3,
+                         float* __restrict__ b1, float* __restrict__ b2, float* __restrict__ b3) {
+  constexpr int T = KS * KS, N1 = 64 * T, N2 = 32 * 64 * T, N3 = 32 * T;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N1 + N2 + N3 + 97; i += gridDim.x * blockDim.x) {
+    if (i >= N1 + N2 + N3) {
+      const int j = i - (N1 + N2 + N3);
+      const float v = params[i];
+      if (j < 64) b1[j] = v; else if (j < 96) b2[j - 64] = v; else b3[0] = v;
+      continue;
+    }
+    int li, co, ci, cin, cout;
+    if (i < N1) li = i, cin = 1, cout = 64;
+    else if (i < N1 + N2) li = i - N1, cin = 64, cout = 32;
+    else li = i - N1 - N2, cin = 32, cout = 1;
+    const int tap = li % T;
+    co = li / T / cin, ci = (li / T) % cin;
+    const int u = tap / KS, v = tap % KS;
+    const int a = flip ? KS - 1 - u : u, b = flip ? KS - 1 - v : v;     // cross-correlation tap (a, b)
+    const float w = params[i];
+    const size_t fwd = (((size_t)ci * KS + a) * KS + b) * cout + co;    // [ci][a][b][co]
+    if (i < N1) {
+      wx1[fwd] = w;
+    } else if (i < N1 + N2) {
+      wx2[fwd] = w;
+      wt2[(((size_t)co * KS + (KS - 1 - a)) * KS + (KS - 1 - b)) * 64 + ci] = w;   // [k=co][a'][b'][c=ci]
+    } else {
+      wx3[fwd] = w;
+      wt3[(((size_t)0 * KS + (KS - 1 - a)) * KS + (KS - 1 - b)) * 32 + ci] = w;    // [0][a'][b'][c=ci]
+    }
+  }
+}
+
+cudaError_t launch_sgd_repack(float* params, const float* grads, float* vel, int n, float lr, float momentum, int flip,
+                              float* wx1, float* wx2, float* wx3, float* wt2, float* wt3, float* b1, float* b2,
+                              float* b3, cudaStream_t st) {
+  if (grads) k_sgd<<<296, 256, 0, st>>>(params, grads, vel, n, lr, momentum);
+  k_repack<<<296, 256, 0, st>>>(params, flip, wx1, wx2, wx3, wt2, wt3, b1, b2, b3);
+  return cudaGetLastError();
+}
+
+}  // namespace di

@@ -83,4 +83,20 @@ cudaError_t launch_add_noise(void* y, long long ldy, int m, int batch, double sn
                              cudaStream_t st);
 cudaError_t launch_metrics(const float* xhat, const float* x, int N, int batch, double* out, cudaStream_t st);
 
+// training step, fp32 contexts (k_train.cu, k_conv_simt.cu)
+constexpr int WGRAD_CHUNKS = 592;           // pixel-tile chunks of the weight-gradient reductions (4 x 148)
+constexpr int N_PARAMS = 64 * 121 + 32 * 64 * 121 + 32 * 121 + 64 + 32 + 1;   // 259 521
+cudaError_t launch_loss_grad(const float* xhat, const float* x, int N, int batch, double scale, float* dxhat,
+                             double* loss_img, double* loss, cudaStream_t st);
+cudaError_t launch_dgrad_mask(float* d, const float* y, size_t n, cudaStream_t st);
+cudaError_t launch_dgrad3_f32(const float* dxhat, const float* wt3, const float* h2, float* dh2, int batch, int n1,
+                              int n2, cudaStream_t st);
+cudaError_t launch_dgrad2_f32(const float* dh2, const float* wt2, const float* h1, float* dh1, int batch, int n1,
+                              int n2, cudaStream_t st);
+cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, int n1, int n2, float* part_w,
+                         float* part_b, int flip, float* gw, float* gb, cudaStream_t st);
+cudaError_t launch_sgd_repack(float* params, const float* grads, float* vel, int n, float lr, float momentum, int flip,
+                              float* wx1, float* wx2, float* wx3, float* wt2, float* wt3, float* b1, float* b2,
+                              float* b3, cudaStream_t st);
+
 }  // namespace di

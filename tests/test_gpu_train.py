@@ -1,0 +1,85 @@
+"""GPU parity of the training step: loss and gradients of di_train_grad against the fp64
+oracle (oracle.train_grad, pinned by finite differences), SGD consistency and a decreasing loss."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_helpers import Case, make_ctx
+
+pytestmark = pytest.mark.gpu
+
+# fp32 forward (<= 1e-5) and fp32 gradient sums (per 256-pixel tile in fp32, then fp64 across tiles)
+TOL_GRAD = 1e-4
+
+
+def _grads_ok(ctx, case, scale=None, final_relu=False, xcorr=False):
+    import torch
+    from paper_1701_03891_b200 import split_params
+    y = torch.from_numpy(case.y).cuda()
+    x = torch.from_numpy(case.x).cuda()
+    loss, g = ctx.train_grad(y, x, scale)
+    torch.cuda.synchronize()
+    ws, bs = split_params(g.cpu().numpy().astype(np.float64))
+    p = case.params
+    if xcorr:   # the oracle works in the true-convolution orientation
+        p = synth.Params([w[:, :, ::-1, ::-1].copy() for w in p.w], p.b)
+    rl, rw, rb = oracle.train_grad(case.y, case.x, case.phi, p, case.n1, case.n2, scale=scale, final_relu=final_relu)
+    if xcorr:
+        rw = [w[:, :, ::-1, ::-1] for w in rw]
+    assert abs(float(loss.item()) - rl) <= 1e-5 * abs(rl)
+    for l in range(3):
+        assert oracle.rel_l2(ws[l], rw[l]) <= TOL_GRAD, ("W", l, oracle.rel_l2(ws[l], rw[l]))
+        assert oracle.rel_l2(bs[l], rb[l]) <= TOL_GRAD, ("b", l, oracle.rel_l2(bs[l], rb[l]))
+
+
+@pytest.mark.parametrize("n1,n2,m,batch", [(16, 16, 64, 4), (40, 72, 300, 3), (9, 13, 40, 2)])
+def test_gradients_match_oracle(n1, n2, m, batch):
+    case = Case(n1, n2, m, batch, "f32", 6, 3, bias="channel")
+    _grads_ok(make_ctx(case), case)
+
+
+@pytest.mark.parametrize("final_relu,xcorr", [(True, False), (False, True)])
+def test_gradients_flags(final_relu, xcorr):
+    from paper_1701_03891_b200 import DI_FLAG_FINAL_RELU, DI_FLAG_XCORR
+    case = Case(24, 24, 128, 3, "f32", 6, 3, bias="channel")
+    flags = (DI_FLAG_FINAL_RELU if final_relu else 0) | (DI_FLAG_XCORR if xcorr else 0)
+    _grads_ok(make_ctx(case, flags=flags), case, final_relu=final_relu, xcorr=xcorr)
+
+
+def test_sgd_updates_the_forward_and_lowers_the_loss():
+    import torch
+    case = Case(32, 32, 256, 8, "f32", 6, 3, bias="channel")
+    ctx = make_ctx(case)
+    y = torch.from_numpy(case.y).cuda()
+    x = torch.from_numpy(case.x).cuda()
+    losses, lr = [], None
+    for _ in range(6):
+        loss, g = ctx.train_grad(y, x)
+        losses.append(float(loss.item()))
+        if lr is None:   # a step small against the curvature: first-order decrease 5 % of the loss
+            lr = 0.05 * losses[0] / float((g.double() ** 2).sum())
+        ctx.sgd_step(g, lr=lr, momentum=0.5)
+    assert all(np.isfinite(losses)) and losses[-1] < 0.9 * losses[0], losses
+    # the updated parameters drive the forward: GPU recovery == oracle forward with the read-back parameters
+    ws, bs = ctx.params()
+    p = synth.Params([w.astype(np.float64) for w in ws], [b.astype(np.float64) for b in bs])
+    out = ctx.recover(y).cpu().numpy()
+    ref = oracle.forward(case.y, case.phi, p, case.n1, case.n2)
+    assert max(oracle.rel_l2(a, r) for a, r in zip(out, ref)) <= 1e-5
+    # one SGD step without momentum is exactly params - lr * grads
+    _, g = ctx.train_grad(y, x)
+    before = np.concatenate([w.ravel() for w in ctx.params()[0]] + [b for b in ctx.params()[1]])
+    ctx.sgd_step(g, lr=1e-3, momentum=0.0)
+    after = np.concatenate([w.ravel() for w in ctx.params()[0]] + [b for b in ctx.params()[1]])
+    # (the momentum buffer from the loop above persists: vel = 0 * vel + g)
+    assert np.allclose(after, before - np.float32(1e-3) * g.cpu().numpy(), rtol=0, atol=1e-7)
+
+
+def test_training_rejects_non_fp32_contexts():
+    import torch
+    from paper_1701_03891_b200 import DiError
+    case = Case(16, 16, 64, 2, "bf16")
+    ctx = make_ctx(case)
+    with pytest.raises(DiError):
+        ctx.train_grad(torch.from_numpy(case.y).cuda().to(torch.bfloat16), torch.from_numpy(case.x).cuda())
