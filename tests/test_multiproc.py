@@ -73,3 +73,52 @@ def test_single_process_defaults():
     assert bench.dist_env()[1] >= 1
     assert bench.shard(0, 4096) == (0, 4096)
     assert bench.max_over_ranks(3.5) == 3.5
+
+
+def _train_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        phi, p, y, x, n1, n2 = _train_case()
+        per = y.shape[0] // world
+        sl = slice(rank * per, (rank + 1) * per)
+        loss, dws, dbs = oracle.train_grad(y[sl], x[sl], phi, p, n1, n2, scale=1.0 / y.shape[0], threads=1)
+        flat = torch.from_numpy(np.concatenate([g.ravel() for g in dws + dbs] + [np.array([loss])]))
+        dist.all_reduce(flat)          # the one collective of data-parallel training (tools/train_dp.py)
+        if rank == 0:
+            q.put(flat.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _train_case():
+    r = np.random.default_rng(7)
+    n1, n2, m, b = 6, 6, 20, 4
+    phi = r.standard_normal((m, n1 * n2)) / np.sqrt(m)
+    widths = (1, 3, 2, 1)
+    ws = [r.standard_normal((widths[l + 1], widths[l], 3, 3)) * 0.5 for l in range(3)]
+    bs = [r.uniform(-0.1, 0.1, widths[l + 1]) for l in range(3)]
+    return phi, synth.Params(ws, bs), r.standard_normal((b, m)), r.uniform(0, 1, (b, n1, n2)), n1, n2
+
+
+def test_two_rank_gradient_allreduce_equals_full_batch_gradient():
+    """Data-parallel training: shard gradients with scale 1/global batch, summed by all_reduce, equal the
+    full-batch gradient (the decomposition tools/train_dp.py relies on)."""
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_train_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    got = q.get(timeout=120)
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    phi, p, y, x, n1, n2 = _train_case()
+    loss, dws, dbs = oracle.train_grad(y, x, phi, p, n1, n2, scale=1.0 / y.shape[0], threads=1)
+    ref = np.concatenate([g.ravel() for g in dws + dbs] + [np.array([loss])])
+    assert np.allclose(got, ref, rtol=1e-12, atol=1e-15)
