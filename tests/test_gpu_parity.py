@@ -212,3 +212,37 @@ def test_stages_individually(precision):
         # TF32 truncates the fp32 h2 and weights to 10-bit mantissas (2^-11 per product)
         tol3 = {"f32": 1e-5, "bf16": 1e-4, "tf32": 2e-3}[precision]
         assert oracle.rel_l2(f(xh)[b], r3[0]) <= tol3
+
+
+# ----------------------------------------------------------------------------- degenerate shapes
+@pytest.mark.parametrize("precision", ["f32", "bf16", "tf32"])
+@pytest.mark.parametrize("n1,n2,m,batch", [
+    (1, 1, 1, 2),        # N = 1, M = 1: every tap but the centre reads the zero padding
+    (1, 64, 16, 3),      # one-row images (strip mostly padding)
+    (64, 1, 16, 3),      # one-column images
+    (8, 8, 64, 5),       # M = N (square Phi)
+    (5, 8, 1, 4),        # a single measurement
+    (16, 4, 30, 3),      # n2 = 4: smallest width with an fp32 TMA row (TF32 conv1 strip)
+    (3, 200, 50, 2),     # n2 > 64 with a ragged last column segment, fewer rows than a unit
+])
+def test_degenerate_shapes(precision, n1, n2, m, batch):
+    case = Case(n1, n2, m, batch, precision, 3, 2)
+    ctx = make_ctx(case)
+    out = run(case, ctx)
+    assert np.all(np.isfinite(out))
+    ref = case.oracle(np.arange(batch))
+    rel = max(oracle.rel_l2(g, r) for g, r in zip(out, ref))
+    assert rel <= TOL_REL_L2[precision], rel
+
+
+def test_batch_zero_and_oversize_are_argument_errors():
+    import torch
+    from paper_1701_03891_b200 import DiError, di_recover
+    case = Case(16, 16, 64, 2, "bf16")
+    ctx = make_ctx(case, max_batch=2)
+    y = torch.zeros((2, 64), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty((2, 16, 16), device="cuda")
+    for b in (0, -1, 3):
+        with pytest.raises(DiError) as e:
+            di_recover(ctx.ctx, y, 64, b, out)
+        assert e.value.status == 1
