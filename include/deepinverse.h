@@ -70,6 +70,9 @@ typedef struct {
   unsigned flags;        /* DI_FLAG_*                                                         */
   int device;            /* CUDA device ordinal                                               */
   int max_batch;         /* largest batch of a single di_recover call; sizes the workspace    */
+  const float* lift;     /* optional learned lifting matrix L [n1*n2][m] row-major fp32: x_tilde = L y
+                            ("one could learn the weights").  NULL: the
+                            paper's fixed adjoint L = Phi^T.  Phi still defines di_measure.   */
 } di_create_args;
 
 /* Create a context on args->device.  On failure *out is set to NULL and a status is returned. */
@@ -159,7 +162,8 @@ di_status di_stage_times(di_ctx ctx, float ms[4], int* calls, int reset);
  *   stage 3: h2                       -> x_hat [batch][n1][n2] fp32 */
 di_status di_debug_stage(di_ctx ctx, int stage, const void* in, void* out, int batch, void* stream);
 
-/* Test hook: copy the context's device copy of Phi (storage type, [m][N] row-major) to a host buffer. */
+/* Test hook: copy the context's device copy of the lifting matrix's transpose (Phi, or L^T for a learned lifting;
+ * storage type, [m][N] row-major) to a host buffer. */
 di_status di_debug_get_phi(di_ctx ctx, void* host_out, long long bytes);
 
 #ifdef __cplusplus

@@ -46,7 +46,7 @@ class di_create_args(ctypes.Structure):
                 ("w2", ctypes.c_void_p), ("b2", ctypes.c_void_p),
                 ("w3", ctypes.c_void_p), ("b3", ctypes.c_void_p),
                 ("precision", ctypes.c_int), ("flags", ctypes.c_uint),
-                ("device", ctypes.c_int), ("max_batch", ctypes.c_int)]
+                ("device", ctypes.c_int), ("max_batch", ctypes.c_int), ("lift", ctypes.c_void_p)]
 
 
 class di_info(ctypes.Structure):
@@ -191,7 +191,7 @@ class DeepInverse:
     params: synth.Params-like (w: 3 arrays [C_out][C_in][11][11], b: per-channel or full-map biases)."""
 
     def __init__(self, phi: np.ndarray, params, n1: int, n2: int, precision: str = "bf16", flags: int = 0,
-                 device: int = 0, max_batch: int = 1):
+                 device: int = 0, max_batch: int = 1, lift: np.ndarray | None = None):
         load()
         phi = np.ascontiguousarray(phi, dtype=np.float32)
         self.m = phi.shape[0]
@@ -204,10 +204,14 @@ class DeepInverse:
         if getattr(params, "fullmap_bias", False) and has_bias:
             flags |= DI_FLAG_FULLMAP_BIAS
         self.flags = flags
-        self._keep = (phi, ws, bs)
+        lift = None if lift is None else np.ascontiguousarray(lift, dtype=np.float32)
+        if lift is not None and lift.shape != (phi.shape[1], phi.shape[0]):
+            raise ValueError(f"lift must be [N][m] = {(phi.shape[1], phi.shape[0])}")
+        self._keep = (phi, ws, bs, lift)
         a = di_create_args(self.m, n1, n2, phi.ctypes.data, DI_DTYPE_F32,
                            ws[0].ctypes.data, _ptr(bs[0]), ws[1].ctypes.data, _ptr(bs[1]),
-                           ws[2].ctypes.data, _ptr(bs[2]), PRECISIONS[precision], flags, device, max_batch)
+                           ws[2].ctypes.data, _ptr(bs[2]), PRECISIONS[precision], flags, device, max_batch,
+                           _ptr(lift))
         self.ctx = di_create(a)
         self._keep = None
 

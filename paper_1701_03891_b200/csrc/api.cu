@@ -95,6 +95,7 @@ struct di_ctx_s {
   float *xh_ws = nullptr, *dxh = nullptr, *dh1 = nullptr, *dh2 = nullptr, *part_w = nullptr, *part_b = nullptr;
   double* loss_img = nullptr;
   void* phi_rm = nullptr;       // di_measure: Phi [m][npad] in the storage type (BF16/TF32; built on first use)
+  float* phi_sense = nullptr;   // di_measure in FP32 mode when a learned lifting replaced Phi: Phi [m][N]
   void* xs = nullptr;           // di_measure: staged x [max_batch][npad] in the storage type
   int npad = 0;
   float *b1 = nullptr, *b2 = nullptr, *b3 = nullptr;  // per-channel or cropped full maps (nullptr = zero)
@@ -357,7 +358,7 @@ di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n
 void free_ctx(di_ctx c) {
   if (!c) return;
   void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->phi_rm, c->xs, c->params, c->vel,
-                c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
+                c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->phi_sense, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -555,15 +556,23 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     }                        \
   } while (0)
 
-  // ---- Phi: upload as fp32, then pack on the device
+  // ---- the lifting matrix (Phi^T, or a learned L) as its transpose [m][N]: upload as fp32, then pack on the device
+  std::vector<float> phif;   // Phi as fp32 (kept for di_measure when a learned lifting replaces Phi^T)
+  const float* phi32 = reinterpret_cast<const float*>(a->phi);
+  if (a->phi_dtype == DI_DTYPE_BF16) {
+    phif.resize((size_t)a->m * N);
+    const uint16_t* pb = reinterpret_cast<const uint16_t*>(a->phi);
+    for (size_t i = 0; i < phif.size(); ++i) phif[i] = bf2f(pb[i]);
+    phi32 = phif.data();
+  }
   {
-    std::vector<float> phif;
-    const float* phisrc = reinterpret_cast<const float*>(a->phi);
-    if (a->phi_dtype == DI_DTYPE_BF16) {
-      phif.resize((size_t)a->m * N);
-      const uint16_t* pb = reinterpret_cast<const uint16_t*>(a->phi);
-      for (size_t i = 0; i < phif.size(); ++i) phif[i] = bf2f(pb[i]);
-      phisrc = phif.data();
+    std::vector<float> liftT;
+    const float* phisrc = phi32;
+    if (a->lift) {                                  // L [N][m] -> L^T [m][N]
+      liftT.resize((size_t)a->m * N);
+      for (long long j = 0; j < N; ++j)
+        for (int i = 0; i < a->m; ++i) liftT[(size_t)i * N + j] = a->lift[(size_t)j * a->m + i];
+      phisrc = liftT.data();
     }
     if (c->prec == DI_PREC_FP32) {
       STEP(upload(reinterpret_cast<float**>(&c->phi), phisrc, (size_t)a->m * N * 4, &c->ws_bytes));
@@ -586,6 +595,29 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
         free_ctx(c);
         return fail(DI_ERR_CUDA, "packing Phi^T failed: %s", cudaGetErrorString(e));
       }
+    }
+  }
+  // ---- a learned lifting replaces Phi^T in the proxy only; di_measure keeps sensing with Phi
+  if (a->lift) {
+    if (c->prec == DI_PREC_FP32) {
+      STEP(upload(&c->phi_sense, phi32, (size_t)a->m * N * 4, &c->ws_bytes));
+    } else {
+      const int kel = 128 / (int)c->elt;
+      c->npad = (int)(((N + kel - 1) / kel) * kel);
+      std::vector<uint8_t> prm((size_t)a->m * c->npad * c->elt, 0);
+      for (int i = 0; i < a->m; ++i)
+        for (long long j = 0; j < N; ++j) {
+          const float v = phi32[(size_t)i * N + j];
+          uint8_t* d = prm.data() + ((size_t)i * c->npad + j) * c->elt;
+          if (bf16) {
+            const uint16_t h = f2bf(v);
+            std::memcpy(d, &h, 2);
+          } else {
+            std::memcpy(d, &v, 4);
+          }
+        }
+      STEP(upload(reinterpret_cast<uint8_t**>(&c->phi_rm), prm.data(), prm.size(), &c->ws_bytes));
+      STEP(upload(reinterpret_cast<uint8_t**>(&c->xs), nullptr, (size_t)a->max_batch * c->npad * c->elt, &c->ws_bytes));
     }
   }
   // ---- weights / biases
@@ -763,7 +795,7 @@ di_status di_measure(di_ctx c, const float* x, int batch, void* y, long long ldy
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (c->prec == DI_PREC_FP32) {
-    CUDA_TRY(di::launch_measure_f32(x, reinterpret_cast<const float*>(c->phi), c->m, c->N, batch,
+    CUDA_TRY(di::launch_measure_f32(x, c->phi_sense ? c->phi_sense : reinterpret_cast<const float*>(c->phi), c->m, c->N, batch,
                                     reinterpret_cast<float*>(y), ldy, st));
     return DI_OK;
   }

@@ -246,3 +246,24 @@ def test_batch_zero_and_oversize_are_argument_errors():
         with pytest.raises(DiError) as e:
             di_recover(ctx.ctx, y, 64, b, out)
         assert e.value.status == 1
+
+
+# ----------------------------------------------------------------------------- learned lifting (NEXT-3)
+@pytest.mark.parametrize("precision", ["f32", "bf16", "tf32"])
+def test_learned_lifting_matrix(precision):
+    """A learned lifting L [N][M] replaces Phi^T in the first layer; Phi still senses (di_measure)."""
+    import torch
+    from paper_1701_03891_b200 import DeepInverse
+    case = Case(24, 40, 200, 5, precision, 4, 2)
+    r = np.random.default_rng(99)
+    lift = (r.standard_normal((case.n1 * case.n2, case.m)) / np.sqrt(case.m)).astype(np.float32)
+    if precision == "bf16":
+        lift = synth.round_bf16(lift)
+    ctx = DeepInverse(case.phi, case.params, case.n1, case.n2, precision, max_batch=case.batch, lift=lift)
+    out = run(case, ctx)
+    ref = oracle.forward(case.y, lift.T, case.params, case.n1, case.n2)   # x_tilde = (L^T)^T y = L y
+    assert max(oracle.rel_l2(g, r_) for g, r_ in zip(out, ref)) <= TOL_REL_L2[precision]
+    xs = synth.round_bf16(case.x) if precision == "bf16" else case.x
+    y = ctx.measure(torch.from_numpy(case.x).cuda()).float().cpu().numpy()
+    ym = oracle.measure(case.phi, xs)
+    assert max(oracle.rel_l2(a, b) for a, b in zip(y, ym)) <= (1e-5 if precision == "f32" else 1e-2)
