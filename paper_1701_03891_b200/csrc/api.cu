@@ -648,7 +648,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     STEP(upload_bias(&c->b1, a->b1, C1, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b2, a->b2, C2, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b3, a->b3, 1, fm, a->n1, a->n2, &c->ws_bytes));
-    if (c->prec == DI_PREC_FP32 && !fm) {   // trainable context: parameters in the API orientation
+    if ((c->prec == DI_PREC_FP32 || c->prec == DI_PREC_TF32) && !fm) {   // trainable: parameters, API orientation
       std::vector<float> prm(di::N_PARAMS, 0.f);
       const size_t n1w = (size_t)C1 * K * K, n2w = (size_t)C2 * C1 * K * K, n3w = (size_t)C2 * K * K;
       std::memcpy(prm.data(), a->w1, n1w * 4);
@@ -870,14 +870,17 @@ static di_status train_alloc(di_ctx c) {
   // backward layouts (and the forward ones, identical to di_create's) from the parameters
   CUDA_TRY(di::launch_sgd_repack(c->params, nullptr, c->vel, di::N_PARAMS, 0.f, 0.f, !(c->flags & DI_FLAG_XCORR),
                                  c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2, c->b3, 0));
+  if (c->prec == DI_PREC_TF32)
+    CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
+                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), 0));
   CUDA_TRY(cudaDeviceSynchronize());
   return DI_OK;
 }
 
 static di_status train_check(di_ctx c) {
   if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
-  if (c->prec != DI_PREC_FP32 || !c->params)
-    return fail(DI_ERR_ARG, "training needs a DI_PREC_FP32 context with per-channel (or zero) biases");
+  if ((c->prec != DI_PREC_FP32 && c->prec != DI_PREC_TF32) || !c->params)
+    return fail(DI_ERR_ARG, "training needs a DI_PREC_FP32 or DI_PREC_TF32 context with per-channel (or zero) biases");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
   if (!c->b1 || !c->b2 || !c->b3) {   // trainable biases need storage even when created zero
     if (!c->b1) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->b1), C1 * 4));
@@ -926,6 +929,10 @@ di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, 
   CUDA_TRY(di::launch_sgd_repack(c->params, grads, c->vel, di::N_PARAMS, (float)lr, (float)momentum,
                                  !(c->flags & DI_FLAG_XCORR), c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2,
                                  c->b3, reinterpret_cast<cudaStream_t>(stream)));
+  if (c->prec == DI_PREC_TF32)
+    CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
+                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3),
+                                    reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }
 

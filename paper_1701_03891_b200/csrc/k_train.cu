@@ -236,6 +236,45 @@ __global__ void k_repack(const float* __restrict__ params, int flip, float* __re
   }
 }
 
+// TF32 contexts: the tensor-core weight images (k_conv13_tc.cu / k_conv2_tf32.cu layouts, same as api.cu's host
+// packers) re-derived on the device from the parameters after every SGD step
+__device__ __forceinline__ float wx_at(const float* __restrict__ W, int cin, int co, int ci, int a, int b, int flip) {
+  const int u = flip ? KS - 1 - a : a, v = flip ? KS - 1 - b : b;
+  return W[(((size_t)co * cin + ci) * KS + u) * KS + v];
+}
+
+__global__ void k_repack_tf32(const float* __restrict__ params, int flip, float* __restrict__ wp1,
+                              float* __restrict__ wp2t, float* __restrict__ wp3) {
+  constexpr int T = KS * KS, N1 = 64 * T, N2 = 32 * 64 * T;
+  const float* W1 = params;
+  const float* W2 = params + N1;
+  const float* W3 = params + N1 + N2;
+  constexpr int E2 = 2 * 33 * 4096, E1 = 11 * 1024, E3 = 22 * 512;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E2 + E1 + E3; e += gridDim.x * blockDim.x) {
+    if (e < E2) {                     // conv2: [h][kb] blocks of 128 rows x 32 ch, SWIZZLE_128B
+      const int blk = e / 4096, o = (e % 4096) * 4, row = o / 128, r = o % 128;
+      const int c = (((r / 16) ^ (row & 7)) * 4) + (r % 16) / 4;
+      const int h = blk / 33, kb = blk % 33, u = kb / 3, b = 4 * (kb % 3) + row / 32, k = row % 32;
+      wp2t[e] = b < KS ? wx_at(W2, 64, k, 32 * h + c, u, b, flip) : 0.f;
+    } else if (e < E2 + E1) {         // conv1: [u] blocks of 64 permuted filters x 16 taps, SWIZZLE_64B
+      const int i = e - E2, u = i / 1024, o = (i % 1024) * 4, m = o / 64, r = o % 64;
+      const int v = (((r / 16) ^ ((m >> 1) & 3)) * 4) + (r % 16) / 4;
+      const int grp = m / 16, j = m % 16, f = 16 * grp + (j < 8 ? 2 * j : 2 * (j - 8) + 1);
+      wp1[i] = v < KS ? wx_at(W1, 1, f, 0, u, v, flip) : 0.f;
+    } else {                          // conv3: [h*11 + u] blocks of 32 rows (taps v) x 16 ch, SWIZZLE_64B
+      const int i = e - E2 - E1, blk = i / 512, h = blk / 11, u = blk % 11, o = (i % 512) * 4, row = o / 64,
+                r = o % 64;
+      const int c = (((r / 16) ^ ((row >> 1) & 3)) * 4) + (r % 16) / 4;
+      wp3[i] = row < KS ? wx_at(W3, 32, 0, 16 * h + c, u, row, flip) : 0.f;
+    }
+  }
+}
+
+cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, cudaStream_t st) {
+  k_repack_tf32<<<296, 256, 0, st>>>(params, flip, wp1, wp2t, wp3);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sgd_repack(float* params, const float* grads, float* vel, int n, float lr, float momentum, int flip,
                               float* wx1, float* wx2, float* wx3, float* wt2, float* wt3, float* b1, float* b2,
                               float* b3, cudaStream_t st) {

@@ -95,6 +95,7 @@ cudaError_t launch_dgrad2_f32(const float* dh2, const float* wt2, const float* h
                               int n2, cudaStream_t st);
 cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, int n1, int n2, float* part_w,
                          float* part_b, int flip, float* gw, float* gb, cudaStream_t st);
+cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, cudaStream_t st);
 cudaError_t launch_sgd_repack(float* params, const float* grads, float* vel, int n, float lr, float momentum, int flip,
                               float* wx1, float* wx2, float* wx3, float* wt2, float* wt3, float* b1, float* b2,
                               float* b3, cudaStream_t st);

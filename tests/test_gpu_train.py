@@ -9,11 +9,13 @@ from gpu_helpers import Case, make_ctx
 
 pytestmark = pytest.mark.gpu
 
-# fp32 forward (<= 1e-5) and fp32 gradient sums (per 256-pixel tile in fp32, then fp64 across tiles)
-TOL_GRAD = 1e-4
+# fp32 forward (<= 1e-5) and fp32 gradient sums (per 256-pixel tile in fp32, then fp64 across tiles); TF32: the
+# forward's 10-bit-mantissa products (the 2e-2 bar of the TF32 path)
+TOL_GRAD = {"f32": 1e-4, "tf32": 2e-2}
 
 
 def _grads_ok(ctx, case, scale=None, final_relu=False, xcorr=False):
+    tol = TOL_GRAD[case.precision]
     import torch
     from paper_1701_03891_b200 import split_params
     y = torch.from_numpy(case.y).cuda()
@@ -27,15 +29,16 @@ def _grads_ok(ctx, case, scale=None, final_relu=False, xcorr=False):
     rl, rw, rb = oracle.train_grad(case.y, case.x, case.phi, p, case.n1, case.n2, scale=scale, final_relu=final_relu)
     if xcorr:
         rw = [w[:, :, ::-1, ::-1] for w in rw]
-    assert abs(float(loss.item()) - rl) <= 1e-5 * abs(rl)
+    assert abs(float(loss.item()) - rl) <= (1e-5 if case.precision == "f32" else 1e-2) * abs(rl)
     for l in range(3):
-        assert oracle.rel_l2(ws[l], rw[l]) <= TOL_GRAD, ("W", l, oracle.rel_l2(ws[l], rw[l]))
-        assert oracle.rel_l2(bs[l], rb[l]) <= TOL_GRAD, ("b", l, oracle.rel_l2(bs[l], rb[l]))
+        assert oracle.rel_l2(ws[l], rw[l]) <= tol, ("W", l, oracle.rel_l2(ws[l], rw[l]))
+        assert oracle.rel_l2(bs[l], rb[l]) <= tol, ("b", l, oracle.rel_l2(bs[l], rb[l]))
 
 
+@pytest.mark.parametrize("precision", ["f32", "tf32"])
 @pytest.mark.parametrize("n1,n2,m,batch", [(16, 16, 64, 4), (40, 72, 300, 3), (9, 13, 40, 2)])
-def test_gradients_match_oracle(n1, n2, m, batch):
-    case = Case(n1, n2, m, batch, "f32", 6, 3, bias="channel")
+def test_gradients_match_oracle(precision, n1, n2, m, batch):
+    case = Case(n1, n2, m, batch, precision, 6, 3, bias="channel")
     _grads_ok(make_ctx(case), case)
 
 
@@ -47,9 +50,10 @@ def test_gradients_flags(final_relu, xcorr):
     _grads_ok(make_ctx(case, flags=flags), case, final_relu=final_relu, xcorr=xcorr)
 
 
-def test_sgd_updates_the_forward_and_lowers_the_loss():
+@pytest.mark.parametrize("precision", ["f32", "tf32"])
+def test_sgd_updates_the_forward_and_lowers_the_loss(precision):
     import torch
-    case = Case(32, 32, 256, 8, "f32", 6, 3, bias="channel")
+    case = Case(32, 32, 256, 8, precision, 6, 3, bias="channel")
     ctx = make_ctx(case)
     y = torch.from_numpy(case.y).cuda()
     x = torch.from_numpy(case.x).cuda()
@@ -66,7 +70,7 @@ def test_sgd_updates_the_forward_and_lowers_the_loss():
     p = synth.Params([w.astype(np.float64) for w in ws], [b.astype(np.float64) for b in bs])
     out = ctx.recover(y).cpu().numpy()
     ref = oracle.forward(case.y, case.phi, p, case.n1, case.n2)
-    assert max(oracle.rel_l2(a, r) for a, r in zip(out, ref)) <= 1e-5
+    assert max(oracle.rel_l2(a, r) for a, r in zip(out, ref)) <= (1e-5 if precision == "f32" else 2e-2)
     # one SGD step without momentum is exactly params - lr * grads
     _, g = ctx.train_grad(y, x)
     before = np.concatenate([w.ravel() for w in ctx.params()[0]] + [b for b in ctx.params()[1]])
