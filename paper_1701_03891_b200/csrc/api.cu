@@ -87,6 +87,8 @@ struct di_ctx_s {
   void* wp1 = nullptr;          // conv1 tensor-core weight blocks (BF16 mode, SWIZZLE_32B image)
   void* wp3 = nullptr;          // conv3 tensor-core weight blocks (BF16 mode, SWIZZLE_64B image)
   void* wp2t = nullptr;         // conv2 TF32 weight blocks (TF32 mode)
+  float* wp2d = nullptr;        // training, TF32 mode: layer-2 dgrad weight blocks (k_dgrad2_tf32)
+  CUtensorMap tmDG2;            // training, TF32 mode: dG2 strips (fp32, 32 channels)
   // training (FP32 contexts with per-channel biases): parameters in the API orientation, momentum, backward
   // weight layouts and the backward workspace (allocated on the first di_train_grad)
   float* params = nullptr;      // [W1 | W2 | W3 | b1 | b2 | b3], di::N_PARAMS
@@ -182,6 +184,21 @@ di_status encode_xt(CUtensorMap* map, const void* xt, int batch, int n1, int n2,
 }
 
 // h2 [batch][n1][n2][32] for conv3: bf16 (box = all 32 channels = 64 B) or fp32 for TF32 (box = 16 channels = 64 B)
+// dG2 [batch][n1][n2][32] fp32 for the layer-2 dgrad strips (same box as the TF32 conv2 strip)
+di_status encode_dg2(CUtensorMap* map, const void* dg2, int batch, int n1, int n2) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {32, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {32 * 4, (cuuint64_t)n2 * 32 * 4, (cuuint64_t)n1 * n2 * 32 * 4};
+  cuuint32_t box[4] = {32, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tf32_box_rows(), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(dg2), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (dG2) failed: %d", (int)r);
+  return DI_OK;
+}
+
 di_status encode_h2(CUtensorMap* map, const void* h2, int batch, int n1, int n2, bool f32 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
@@ -357,7 +374,7 @@ di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n
 
 void free_ctx(di_ctx c) {
   if (!c) return;
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->phi_rm, c->xs, c->params, c->vel,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->phi_rm, c->xs, c->params, c->vel,
                 c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->phi_sense, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
@@ -870,9 +887,13 @@ static di_status train_alloc(di_ctx c) {
   // backward layouts (and the forward ones, identical to di_create's) from the parameters
   CUDA_TRY(di::launch_sgd_repack(c->params, nullptr, c->vel, di::N_PARAMS, 0.f, 0.f, !(c->flags & DI_FLAG_XCORR),
                                  c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2, c->b3, 0));
-  if (c->prec == DI_PREC_TF32)
+  if (c->prec == DI_PREC_TF32) {
+    if ((s = al(&c->wp2d, (size_t)di::DG2_KBLOCKS * di::C2_KBLOCK_BYTES)) != DI_OK) return s;
+    if ((s = encode_dg2(&c->tmDG2, c->dh2, c->max_batch, c->n1, c->n2)) != DI_OK) return s;
+    CUDA_TRY(di::setup_dgrad2_tf32(c->n2));
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
-                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), 0));
+                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d, 0));
+  }
   CUDA_TRY(cudaDeviceSynchronize());
   return DI_OK;
 }
@@ -916,7 +937,10 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   CUDA_TRY(di::launch_dgrad3_f32(c->dxh, c->wt3, h2, c->dh2, batch, c->n1, c->n2, st));
   CUDA_TRY(di::launch_wgrad(2, h1, c->dh2, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w, gb + C1,
                             st));
-  CUDA_TRY(di::launch_dgrad2_f32(c->dh2, c->wt2, h1, c->dh1, batch, c->n1, c->n2, st));
+  if (c->prec == DI_PREC_TF32)
+    CUDA_TRY(di::launch_dgrad2_tf32(&c->tmDG2, c->wp2d, h1, batch, c->n1, c->n2, c->dh1, c->num_sms, st));
+  else
+    CUDA_TRY(di::launch_dgrad2_f32(c->dh2, c->wt2, h1, c->dh1, batch, c->n1, c->n2, st));
   CUDA_TRY(di::launch_wgrad(1, xt, c->dh1, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads, gb, st));
   return DI_OK;
 }
@@ -931,7 +955,7 @@ di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, 
                                  c->b3, reinterpret_cast<cudaStream_t>(stream)));
   if (c->prec == DI_PREC_TF32)
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
-                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3),
+                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d,
                                     reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }

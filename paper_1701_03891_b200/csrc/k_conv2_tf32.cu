@@ -203,6 +203,174 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------------------------------------------
+// Training: the layer-2 data gradient on the same tensor cores.
+//   dH1[p][ci] = [h1[p][ci] > 0] * sum_{co,a,b} wx2[co][ci][10-a][10-b] * dG2[p + (a-5, b-5)][co]
+// is a centred 11x11 correlation 32 -> 64 channels with the transposed, rotated filter bank, so it takes the
+// forward's mapping with the roles of the channel counts swapped: two column taps v' x 64 input channels ci stack
+// into M = 128, K = the 32 channels co of dG2 (one 128-B swizzle row per position: a single strip per unit), and
+// K-block (u, v0 = 2j), j < 6: 66 per unit (tap 11 is a zero slot).  Output o receives D[ci][o-n0] +
+// D[64+ci][o-n0+1]; the epilogue applies the layer-1 ReLU mask and writes dH1 fp32 NHWC.
+constexpr int KB_DG = 66;
+
+__global__ void __launch_bounds__(256, 1)
+    k_dgrad2_tf32(const __grid_constant__ CUtensorMap tmDG, const float* __restrict__ wpack,
+                  const float* __restrict__ h1, GeoT g, float* __restrict__ dh1) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int strip_bytes = (R + 10) * g.P * 128;
+  const int strip_alloc = (strip_bytes + GUARD_ROWS * 128 + 1023) & ~1023;
+  uint8_t* strip = smem;
+  uint8_t* wst = smem + strip_alloc;
+  float* sP = reinterpret_cast<float*>(wst + WSTAGES * WBYTES);
+
+  __shared__ uint64_t sfull, sempty, wfull[WSTAGES], wempty[WSTAGES], tfull, tempty;
+  __shared__ uint32_t tslot;
+  const int warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmDG);
+    mbar_init(&sfull, 1), mbar_init(&sempty, 1);
+    for (int s = 0; s < WSTAGES; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], 1);
+    mbar_init(&tfull, 1), mbar_init(&tempty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
+  for (int i = threadIdx.x; i < GUARD_ROWS * 128 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(strip + strip_bytes)[i] = make_uint4(0, 0, 0, 0);
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const int per_img = g.nrb * g.ncs;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ producer: strips + weights, in order
+      uint32_t wk = 0, sk = 0;
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++sk) {
+        const int b = u / per_img, rem = u - b * per_img;
+        const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
+        if (sk > 0) mbar_wait(&sempty, (sk - 1) & 1);
+        mbar_arrive_expect_tx(&sfull, strip_bytes);
+        tma_load_4d(strip, &tmDG, &sfull, 0, c0 - 5, r0 - 5, b);
+        const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack);
+        for (int kb = 0; kb < KB_DG; ++kb, ++wk, wsrc += WBYTES) {
+          const uint32_t st = wk % WSTAGES;
+          if (wk >= WSTAGES) mbar_wait(&wempty[st], ((wk / WSTAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&wfull[st], WBYTES);
+          bulk_load(wst + st * WBYTES, wsrc, WBYTES, &wfull[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      const uint64_t bdesc0 = smem_desc(smem_u32(strip), 16, 1024, kSwizzle128B);
+      const uint64_t adesc0 = smem_desc(smem_u32(wst), 16, 1024, kSwizzle128B);
+      const uint64_t pstep = (uint64_t)g.P * 8;
+      uint32_t wk = 0;
+      int it = 0;
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+        const int rem = u % per_img;
+        const int r0 = (rem / g.ncs) * R;
+        const int rows = min(R, g.n1 - r0);
+        const int L = (rows - 1) * g.P + g.wseg;
+        const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;   // 1 or 2
+        const int nB = ntiles > 1 ? min(NT, (min(OUT_PER_TILE, L - OUT_PER_TILE) + 1 + 15) & ~15) : 0;
+        const int nA = min(NT, (min(OUT_PER_TILE, L) + 1 + 15) & ~15);
+        const uint32_t idA = idesc_f32acc(2, 128, nA), idB = idesc_f32acc(2, 128, nB > 0 ? nB : 16);
+        if (it > 0) mbar_wait(&tempty, (it - 1) & 1);   // the epilogue drained the previous unit
+        tc_fence_after();
+        mbar_wait(&sfull, it & 1);
+        tc_fence_after();
+        uint64_t bd = bdesc0;
+        for (int uu = 0; uu < 11; ++uu, bd += pstep) {
+#pragma unroll
+          for (int j = 0; j < 6; ++j, ++wk) {
+            const uint32_t st = wk % WSTAGES;
+            mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
+            tc_fence_after();
+            const uint64_t ad = adesc0 + (uint64_t)(st * (WBYTES >> 4));
+            const uint64_t b = bd + (uint64_t)(16 * j);
+            const uint32_t acc0 = (uu | j) != 0;
+            umma_tf32_ss(tmem, ad, b, idA, acc0);
+            umma_tf32_ss(tmem, ad + 2, b + 2, idA, 1);
+            umma_tf32_ss(tmem, ad + 4, b + 4, idA, 1);
+            umma_tf32_ss(tmem, ad + 6, b + 6, idA, 1);
+            if (nB > 0) {
+              const uint64_t bb = b + (uint64_t)(OUT_PER_TILE * 8);
+              umma_tf32_ss(tmem + 256, ad, bb, idB, acc0);
+              umma_tf32_ss(tmem + 256, ad + 2, bb + 2, idB, 1);
+              umma_tf32_ss(tmem + 256, ad + 4, bb + 4, idB, 1);
+              umma_tf32_ss(tmem + 256, ad + 6, bb + 6, idB, 1);
+            }
+            umma_commit(&wempty[st]);
+          }
+        }
+        umma_commit(&sempty);
+        umma_commit(&tfull);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------------------------------------- epilogue
+    const int q = warp - 4, shift = q >> 1;   // TMEM quadrant q: tap v' = q / 2, channels 32 (q % 2) + lane
+    const int e = threadIdx.x - 128;
+    const int jj = e >> 3, kg = e & 7;        // output position jj of the chunk, channels 8kg..8kg+7
+    const int hq = kg >> 2, cl = (kg & 3) * 8;
+    int it = 0;
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+      const int b = u / per_img, rem = u - b * per_img;
+      const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
+      const int rows = min(R, g.n1 - r0);
+      const int L = (rows - 1) * g.P + g.wseg;
+      const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
+      mbar_wait(&tfull, it & 1);
+      tc_fence_after();
+      for (int t = 0; t < ntiles; ++t) {
+        const int n0 = t * OUT_PER_TILE;
+        const int cnt = min(OUT_PER_TILE, L - n0);
+        const uint32_t tq = tmem + t * 256 + ((uint32_t)(q * 32) << 16);
+        for (int c = 0; c < cnt; c += ECH) {
+          const int nout = min(ECH, cnt - c);
+          uint32_t r[ECH];
+          if (c + shift + ECH <= NT)
+            tmem_ld16(tq + c + shift, r);
+          else
+            ld_tail13_t(tq + c + shift, r);
+          tmem_ld_wait();
+          float* dst = sP + q * (ECH * SPS) + lane;
+#pragma unroll
+          for (int j = 0; j < ECH; ++j) dst[j * SPS] = __uint_as_float(r[j]);
+          named_bar(1, 128);
+          if (jj < nout) {
+            const int o = n0 + c + jj;
+            const int rr = o / g.P, cc = o - rr * g.P;
+            if (cc < g.wseg && c0 + cc < g.n2 && rr < rows) {
+              const float* s0 = sP + hq * (ECH * SPS) + jj * SPS + cl;
+              const float* s1 = s0 + 2 * (ECH * SPS);
+              const size_t pix = ((size_t)b * g.n1 + r0 + rr) * g.n2 + c0 + cc;
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const float4 a0 = *reinterpret_cast<const float4*>(s0 + 4 * hh);
+                const float4 a1 = *reinterpret_cast<const float4*>(s1 + 4 * hh);
+                const float4 m = __ldg(reinterpret_cast<const float4*>(h1 + pix * 64 + 8 * kg + 4 * hh));
+                float4 v;
+                v.x = m.x > 0.f ? a0.x + a1.x : 0.f, v.y = m.y > 0.f ? a0.y + a1.y : 0.f;
+                v.z = m.z > 0.f ? a0.z + a1.z : 0.f, v.w = m.w > 0.f ? a0.w + a1.w : 0.f;
+                *reinterpret_cast<float4*>(dh1 + pix * 64 + 8 * kg + 4 * hh) = v;
+              }
+            }
+          }
+          named_bar(1, 128);
+        }
+      }
+      tc_fence_before();
+      if (lane == 0) mbar_arrive(&tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 static GeoT make_geo_t(int batch, int n1, int n2) {
   GeoT g;
   g.n1 = n1, g.n2 = n2;
@@ -233,6 +401,20 @@ cudaError_t launch_conv2_tf32(const CUtensorMap* tmH1, const void* wpack, const 
   const int grid = g.units < num_sms ? g.units : num_sms;
   k_conv2_tf32<<<grid, 256, conv2_tf32_smem_bytes(n2), st>>>(*tmH1, reinterpret_cast<const float*>(wpack), bias,
                                                              fullmap, g, h2);
+  return cudaGetLastError();
+}
+
+cudaError_t setup_dgrad2_tf32(int n2) {
+  return cudaFuncSetAttribute(k_dgrad2_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)conv2_tf32_smem_bytes(n2));
+}
+
+cudaError_t launch_dgrad2_tf32(const CUtensorMap* tmDG, const void* wpack, const float* h1, int batch, int n1, int n2,
+                               float* dh1, int num_sms, cudaStream_t st) {
+  GeoT g = make_geo_t(batch, n1, n2);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  k_dgrad2_tf32<<<grid, 256, conv2_tf32_smem_bytes(n2), st>>>(*tmDG, reinterpret_cast<const float*>(wpack), h1, g,
+                                                              dh1);
   return cudaGetLastError();
 }
 
