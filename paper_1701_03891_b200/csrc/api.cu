@@ -89,6 +89,9 @@ struct di_ctx_s {
   void* wp2t = nullptr;         // conv2 TF32 weight blocks (TF32 mode)
   float* wp2d = nullptr;        // training, TF32 mode: layer-2 dgrad weight blocks (k_dgrad2_tf32)
   CUtensorMap tmDG2;            // training, TF32 mode: dG2 strips (fp32, 32 channels)
+  void *h1b = nullptr, *dg2b = nullptr;   // training, TF32 mode: bf16 copies of h1 / dG2 (layer-2 wgrad operands)
+  float* part_w2 = nullptr;     // training, TF32 mode: per-CTA layer-2 wgrad partials
+  CUtensorMap tmH1b, tmDG2b;
   // training (FP32 contexts with per-channel biases): parameters in the API orientation, momentum, backward
   // weight layouts and the backward workspace (allocated on the first di_train_grad)
   float* params = nullptr;      // [W1 | W2 | W3 | b1 | b2 | b3], di::N_PARAMS
@@ -196,6 +199,21 @@ di_status encode_dg2(CUtensorMap* map, const void* dg2, int batch, int n1, int n
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (dG2) failed: %d", (int)r);
+  return DI_OK;
+}
+
+// bf16 NHWC activations with `ch` channels (64: SWIZZLE_128B, 32: SWIZZLE_64B) for the layer-2 wgrad strips
+di_status encode_wg2(CUtensorMap* map, const void* p, int batch, int n1, int n2, int ch, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {(cuuint64_t)ch, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)ch * 2, (cuuint64_t)n2 * ch * 2, (cuuint64_t)n1 * n2 * ch * 2};
+  cuuint32_t box[4] = {(cuuint32_t)ch, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)box_rows, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(p), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, ch == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (wgrad2 operand) failed: %d", (int)r);
   return DI_OK;
 }
 
@@ -374,7 +392,7 @@ di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n
 
 void free_ctx(di_ctx c) {
   if (!c) return;
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->phi_rm, c->xs, c->params, c->vel,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->h1b, c->dg2b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
                 c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->phi_sense, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
@@ -891,6 +909,14 @@ static di_status train_alloc(di_ctx c) {
     if ((s = al(&c->wp2d, (size_t)di::DG2_KBLOCKS * di::C2_KBLOCK_BYTES)) != DI_OK) return s;
     if ((s = encode_dg2(&c->tmDG2, c->dh2, c->max_batch, c->n1, c->n2)) != DI_OK) return s;
     CUDA_TRY(di::setup_dgrad2_tf32(c->n2));
+    if ((s = al(&c->h1b, B * N * C1 * 2)) != DI_OK) return s;
+    if ((s = al(&c->dg2b, B * N * C2 * 2)) != DI_OK) return s;
+    if ((s = al(&c->part_w2, di::wgrad2_tc_part_floats(c->num_sms) * 4)) != DI_OK) return s;
+    if ((s = encode_wg2(&c->tmH1b, c->h1b, c->max_batch, c->n1, c->n2, 64, di::wgrad2_tc_h_box_rows())) != DI_OK)
+      return s;
+    if ((s = encode_wg2(&c->tmDG2b, c->dg2b, c->max_batch, c->n1, c->n2, 32, di::wgrad2_tc_g_box_rows())) != DI_OK)
+      return s;
+    CUDA_TRY(di::setup_wgrad2_tc(c->n2));
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
                                     reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d, 0));
   }
@@ -935,8 +961,17 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   CUDA_TRY(di::launch_wgrad(3, h2, c->dxh, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w + n2w,
                             gb + C1 + C2, st));
   CUDA_TRY(di::launch_dgrad3_f32(c->dxh, c->wt3, h2, c->dh2, batch, c->n1, c->n2, st));
-  CUDA_TRY(di::launch_wgrad(2, h1, c->dh2, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w, gb + C1,
-                            st));
+  if (c->prec == DI_PREC_TF32) {   // bf16 operands, tcgen05 MN-major contraction over pixels (k_wgrad2_tc.cu)
+    const size_t npix = (size_t)batch * c->N;
+    CUDA_TRY(di::launch_dg2_bf16(c->dh2, npix, c->dg2b, c->part_b, st));
+    CUDA_TRY(di::launch_bias_reduce(c->part_b, di::WGRAD_CHUNKS, C2, gb + C1, st));
+    CUDA_TRY(di::launch_to_bf16(h1, c->h1b, npix * C1, st));
+    CUDA_TRY(di::launch_wgrad2_tc(&c->tmH1b, &c->tmDG2b, batch, c->n1, c->n2, c->part_w2, flip, grads + n1w,
+                                  c->num_sms, st));
+  } else {
+    CUDA_TRY(di::launch_wgrad(2, h1, c->dh2, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w, gb + C1,
+                              st));
+  }
   if (c->prec == DI_PREC_TF32)
     CUDA_TRY(di::launch_dgrad2_tf32(&c->tmDG2, c->wp2d, h1, batch, c->n1, c->n2, c->dh1, c->num_sms, st));
   else

@@ -176,6 +176,11 @@ static cudaError_t wgrad(const float* X, const float* dG, int batch, int n1, int
   return cudaGetLastError();
 }
 
+cudaError_t launch_bias_reduce(const float* part_b, int nchunk, int nb, float* gb, cudaStream_t st) {
+  k_wgrad_reduce<<<1, 256, 0, st>>>(nullptr, part_b, nchunk, 0, nb, 0, nullptr, gb);
+  return cudaGetLastError();
+}
+
 // layer 3: X = h2 (32 ch), dG = dx_hat (1 ch); layer 2: X = h1 (64), dG = dh2 (32); layer 1: X = x_tilde (1),
 // dG = dh1 (64).  part_w / part_b: scratch of WGRAD_CHUNKS x (weights / biases of the layer).
 cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, int n1, int n2, float* part_w,

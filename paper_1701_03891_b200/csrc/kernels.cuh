@@ -102,6 +102,18 @@ cudaError_t setup_dgrad2_tf32(int n2);
 cudaError_t launch_dgrad2_tf32(const CUtensorMap* tmDG, const void* wpack, const float* h1, int batch, int n1, int n2,
                                float* dh1, int num_sms, cudaStream_t st);
 constexpr int DG2_KBLOCKS = 66;
+// training, TF32 contexts: layer-2 weight gradient on tcgen05 from bf16 copies of h1 / dG2 (k_wgrad2_tc.cu)
+constexpr int WG2_ROWS = 6;
+size_t wgrad2_tc_smem_bytes(int n2);
+int wgrad2_tc_h_box_rows();
+int wgrad2_tc_g_box_rows();
+size_t wgrad2_tc_part_floats(int num_sms);
+cudaError_t setup_wgrad2_tc(int n2);
+cudaError_t launch_wgrad2_tc(const CUtensorMap* tmH, const CUtensorMap* tmG, int batch, int n1, int n2, float* part,
+                             int flip, float* gw, int num_sms, cudaStream_t st);
+cudaError_t launch_to_bf16(const float* src, void* dst, size_t n, cudaStream_t st);
+cudaError_t launch_dg2_bf16(const float* dg, size_t npix, void* dst, float* part_b, cudaStream_t st);
+cudaError_t launch_bias_reduce(const float* part_b, int nchunk, int nb, float* gb, cudaStream_t st);
 cudaError_t launch_sgd_repack(float* params, const float* grads, float* vel, int n, float lr, float momentum, int flip,
                               float* wx1, float* wx2, float* wx3, float* wt2, float* wt3, float* b1, float* b2,
                               float* b3, cudaStream_t st);
