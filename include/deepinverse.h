@@ -87,6 +87,21 @@ di_status di_create(const di_create_args* args, di_ctx* out);
  * DI_ERR_CUDA.  No host synchronisation happens inside. */
 di_status di_recover(di_ctx ctx, const void* y, long long ldy, int batch, float* xhat, void* stream);
 
+/* ---- Row-sharded Phi (PAPER.md:148, 181 -- images beyond one GPU's Phi) -------------
+ * With Phi split over its M rows across G ranks (rank g holds Phi_g = rows [lo_g, hi_g) and the matching entries
+ * y_g of every measurement), the lifting layer is a sum of per-rank partials:
+ *     x_tilde_b = Phi^T y_b = sum_g Phi_g^T y_{g,b}.
+ * A context created with Phi_g (m = hi_g - lo_g rows; any 1 <= m <= N) computes its partial with
+ * di_proxy_partial; the caller sums the partials across ranks (one NCCL reduce-scatter over the batch, or an
+ * all-reduce) and runs the convolutions on the summed proxy with di_recover_from_proxy.
+ *   di_proxy_partial:      y DEVICE [batch][ldy] (di_recover's element type), xt_part DEVICE [batch][n1*n2] fp32,
+ *                          written (fp32 even in BF16 contexts: partials are summed before any rounding).
+ *   di_recover_from_proxy: xt DEVICE [batch][n1*n2] fp32 (read; BF16 contexts round it once, RNE, to the bf16
+ *                          x_tilde), xhat DEVICE [batch][n1][n2] fp32 (written).  Uses the context's workspace.
+ * Errors as di_recover.  Learned-lifting contexts (args->lift) apply L's rows in place of Phi_g^T. */
+di_status di_proxy_partial(di_ctx ctx, const void* y, long long ldy, int batch, float* xt_part, void* stream);
+di_status di_recover_from_proxy(di_ctx ctx, const float* xt, int batch, float* xhat, void* stream);
+
 /* End-to-end variant with HOST buffers: copies y (host, pinned or pageable) to the device, recovers, copies
  * x_hat back to `xhat_host` (pinned host memory makes the copies asynchronous).  Kernels run on `stream`; batches
  * >= 512 are split into 2-4 chunks whose x_hat copies run on an internal stream, overlapping the next chunk's

@@ -25,7 +25,7 @@ PRECISIONS = {"f32": DI_PREC_FP32, "tf32": DI_PREC_TF32, "bf16": DI_PREC_BF16}
 EXPORTS = ["di_create", "di_recover", "di_recover_host", "di_destroy", "di_status_string", "di_last_error",
            "di_get_info", "di_set_profiling", "di_stage_times", "di_debug_stage", "di_debug_get_phi",
            "di_measure", "di_add_noise", "di_metrics", "di_num_params", "di_train_grad", "di_sgd_step",
-           "di_get_params"]
+           "di_get_params", "di_proxy_partial", "di_recover_from_proxy"]
 
 
 class DiError(RuntimeError):
@@ -89,9 +89,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.di_train_grad.argtypes = [V, V, LL, V, I, ctypes.c_double, V, V, V]
     lib.di_sgd_step.argtypes = [V, V, ctypes.c_double, ctypes.c_double, V]
     lib.di_get_params.argtypes = [V, V, V]
+    lib.di_proxy_partial.argtypes = [V, V, LL, I, V, V]
+    lib.di_recover_from_proxy.argtypes = [V, V, I, V, V]
     for f in ("di_create", "di_recover", "di_recover_host", "di_destroy", "di_get_info", "di_set_profiling",
               "di_stage_times", "di_debug_stage", "di_debug_get_phi", "di_measure", "di_add_noise", "di_metrics",
-              "di_train_grad", "di_sgd_step", "di_get_params"):
+              "di_train_grad", "di_sgd_step", "di_get_params", "di_proxy_partial", "di_recover_from_proxy"):
         getattr(lib, f).restype = I
     _lib = lib
     return lib
@@ -136,6 +138,16 @@ def di_recover(ctx, y, ldy: int, batch: int, xhat, stream=None):
 def di_recover_host(ctx, y_host, ldy: int, batch: int, xhat_host, stream=None):
     _check(load().di_recover_host(ctx, _ptr(y_host), ldy, batch, _ptr(xhat_host), _stream_handle(stream)),
            "di_recover_host")
+
+
+def di_proxy_partial(ctx, y, ldy: int, batch: int, xt_part, stream=None):
+    _check(load().di_proxy_partial(ctx, _ptr(y), ldy, batch, _ptr(xt_part), _stream_handle(stream)),
+           "di_proxy_partial")
+
+
+def di_recover_from_proxy(ctx, xt, batch: int, xhat, stream=None):
+    _check(load().di_recover_from_proxy(ctx, _ptr(xt), batch, _ptr(xhat), _stream_handle(stream)),
+           "di_recover_from_proxy")
 
 
 def di_destroy(ctx):
@@ -229,6 +241,29 @@ class DeepInverse:
         if xhat is None:
             xhat = torch.empty((b, self.n1, self.n2), dtype=torch.float32, device=y.device)
         di_recover(self.ctx, y, y.stride(0), b, xhat, stream)
+        return xhat
+
+    def proxy_partial(self, y, out=None, stream=None):
+        """Row-sharded lifting (NEXT-4): y device [B][ldy] over this context's rows of Phi -> fp32 partial
+        x_tilde [B][n1*n2] (device), to be summed across ranks."""
+        import torch
+        if y.dtype != self.storage_dtype or not y.is_cuda:
+            raise TypeError(f"y must be a CUDA {self.storage_dtype} tensor")
+        b = y.shape[0]
+        if out is None:
+            out = torch.empty((b, self.n1 * self.n2), dtype=torch.float32, device=y.device)
+        di_proxy_partial(self.ctx, y, y.stride(0), b, out, stream)
+        return out
+
+    def recover_from_proxy(self, xt, xhat=None, stream=None):
+        """Convolutions on a (summed) fp32 proxy x_tilde [B][n1*n2] (device) -> x_hat [B][n1][n2] fp32."""
+        import torch
+        if xt.dtype != torch.float32 or not xt.is_cuda or not xt.is_contiguous():
+            raise TypeError("xt must be a contiguous CUDA float32 tensor [B][n1*n2]")
+        b = xt.shape[0]
+        if xhat is None:
+            xhat = torch.empty((b, self.n1, self.n2), dtype=torch.float32, device=xt.device)
+        di_recover_from_proxy(self.ctx, xt, b, xhat, stream)
         return xhat
 
     def recover_host(self, y_host, xhat_host=None, stream=None):

@@ -408,6 +408,32 @@ void free_ctx(di_ctx c) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// stage 0 (lifting) into xt: the path dtype, or fp32 when out_f32 (row-sharded partial proxies)
+di_status run_proxy(di_ctx c, const void* y, long long ldy, int batch, void* xt, bool out_f32, cudaStream_t st,
+                    int& launches) {
+  const bool bf16 = c->prec == DI_PREC_BF16;
+  if (c->prec == DI_PREC_FP32) {
+    CUDA_TRY(di::launch_proxy_f32(reinterpret_cast<const float*>(y), ldy, reinterpret_cast<const float*>(c->phi),
+                                  c->m, c->N, batch, reinterpret_cast<float*>(xt), st));
+    ++launches;
+  } else {
+    const void* ysrc = y;
+    long long ld = ldy;
+    int inner = c->m;
+    if (!aligned16(y) || ((size_t)ldy * c->elt) % 16 != 0) {
+      CUDA_TRY(di::launch_stage_y(y, ldy, c->m, c->kpad, batch, c->ystage, bf16, st));
+      ++launches;
+      ysrc = c->ystage, ld = c->kpad, inner = c->kpad;
+    }
+    CUtensorMap tmY;
+    di_status s = encode_2d(&tmY, ysrc, bf16, inner, batch, ld, 128 / (int)c->elt, 128);
+    if (s != DI_OK) return s;
+    CUDA_TRY(di::launch_proxy_tc(&tmY, &c->tmPt, batch, c->N, c->kpad / (128 / (int)c->elt), xt, !bf16, st, out_f32));
+    ++launches;
+  }
+  return DI_OK;
+}
+
 // the launch sequence (stages first..last) on caller buffers
 di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy, int batch, void* xt, void* h1,
                      void* h2, float* xhat, cudaStream_t st) {
@@ -429,25 +455,8 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
   };
   mark(first);
   if (first <= 0 && 0 <= last) {
-    if (c->prec == DI_PREC_FP32) {
-      CUDA_TRY(di::launch_proxy_f32(reinterpret_cast<const float*>(y), ldy, reinterpret_cast<const float*>(c->phi),
-                                    c->m, c->N, batch, reinterpret_cast<float*>(xt), st));
-      ++launches;
-    } else {
-      const void* ysrc = y;
-      long long ld = ldy;
-      int inner = c->m;
-      if (!aligned16(y) || ((size_t)ldy * c->elt) % 16 != 0) {
-        CUDA_TRY(di::launch_stage_y(y, ldy, c->m, c->kpad, batch, c->ystage, bf16, st));
-        ++launches;
-        ysrc = c->ystage, ld = c->kpad, inner = c->kpad;
-      }
-      CUtensorMap tmY;
-      di_status s = encode_2d(&tmY, ysrc, bf16, inner, batch, ld, 128 / (int)c->elt, 128);
-      if (s != DI_OK) return s;
-      CUDA_TRY(di::launch_proxy_tc(&tmY, &c->tmPt, batch, c->N, c->kpad / (128 / (int)c->elt), xt, !bf16, st));
-      ++launches;
-    }
+    di_status s0 = run_proxy(c, y, ldy, batch, xt, false, st, launches);
+    if (s0 != DI_OK) return s0;
   }
   mark(1);
   if (first <= 1 && 1 <= last) {
@@ -763,6 +772,30 @@ di_status di_recover(di_ctx c, const void* y, long long ldy, int batch, float* x
   if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
   return run_stages(c, 0, 3, y, ldy, batch, c->xt, c->h1, c->h2, xhat, reinterpret_cast<cudaStream_t>(stream));
+}
+
+di_status di_proxy_partial(di_ctx c, const void* y, long long ldy, int batch, float* xt_part, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!y || !xt_part) return fail(DI_ERR_ARG, "y and xt_part must be non-NULL device pointers");
+  if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  int launches = 0;
+  return run_proxy(c, y, ldy, batch, xt_part, true, reinterpret_cast<cudaStream_t>(stream), launches);
+}
+
+di_status di_recover_from_proxy(di_ctx c, const float* xt, int batch, float* xhat, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!xt || !xhat) return fail(DI_ERR_ARG, "xt and xhat must be non-NULL device pointers");
+  if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  void* x1 = const_cast<float*>(xt);
+  if (c->prec == DI_PREC_BF16) {   // the bf16 path's x_tilde: the summed proxy rounded once (RNE)
+    CUDA_TRY(di::launch_round_bf16(xt, c->xt, (size_t)batch * c->N, st));
+    x1 = c->xt;
+  }
+  return run_stages(c, 1, 3, nullptr, 0, batch, x1, c->h1, c->h2, xhat, st);
 }
 
 di_status di_recover_host(di_ctx c, const void* y_host, long long ldy, int batch, float* xhat_host, void* stream) {

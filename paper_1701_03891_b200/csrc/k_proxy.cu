@@ -21,8 +21,9 @@ constexpr int PX_BN = 256;      // pixels per tile (UMMA N)
 constexpr int PX_STAGES = 4;
 }  // namespace
 
-// ELT: 2 = bf16 (kind::f16, K=16 per MMA), 4 = fp32 storage with kind::tf32 (K=8 per MMA)
-template <int ELT>
+// ELT: 2 = bf16 (kind::f16, K=16 per MMA), 4 = fp32 storage with kind::tf32 (K=8 per MMA).
+// OF32: fp32 output even for bf16 operands (row-sharded partial proxies, summed across ranks before rounding)
+template <int ELT, bool OF32 = (ELT == 4)>
 __global__ void __launch_bounds__(128, 1)
     k_proxy_tc(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmPt, int batch,
                int N, int kblocks, void* __restrict__ xt) {
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(128, 1)
     tmem_ld_wait();
     const int col = n0 + c;
     if (!row_ok || col >= N) continue;
-    if (ELT == 2) {
+    if (ELT == 2 && !OF32) {
       __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(xt) + (size_t)b * N + col;
       if (vec_ok && col + 32 <= N) {
 #pragma unroll
@@ -135,11 +136,13 @@ __global__ void __launch_bounds__(128, 1)
 size_t proxy_tc_smem_bytes() { return (size_t)PX_STAGES * (PX_BM + PX_BN) * 128 + 1024; }
 
 cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
-                            void* xt, bool tf32, cudaStream_t st) {
+                            void* xt, bool tf32, cudaStream_t st, bool out_f32) {
   const int nbt = (batch + PX_BM - 1) / PX_BM, nnt = (N + PX_BN - 1) / PX_BN;
   const size_t smem = proxy_tc_smem_bytes();
   if (tf32) {
     k_proxy_tc<4><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt);
+  } else if (out_f32) {
+    k_proxy_tc<2, true><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt);
   } else {
     k_proxy_tc<2><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt);
   }
@@ -150,8 +153,22 @@ cudaError_t setup_proxy_tc() {
   cudaError_t e = cudaFuncSetAttribute(k_proxy_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)proxy_tc_smem_bytes());
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_proxy_tc<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)proxy_tc_smem_bytes());
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_proxy_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)proxy_tc_smem_bytes());
+}
+
+// fp32 -> bf16 (RNE), any n: a summed row-sharded proxy rounded once to the bf16 path's x_tilde
+__global__ void k_round_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+cudaError_t launch_round_bf16(const float* src, void* dst, size_t n, cudaStream_t st) {
+  k_round_bf16<<<4 * 148, 256, 0, st>>>(src, reinterpret_cast<__nv_bfloat16*>(dst), n);
+  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------------------- fp32 SIMT GEMM

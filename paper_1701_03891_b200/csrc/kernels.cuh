@@ -25,7 +25,8 @@ constexpr int C3TC_ROWS = 6;                // conv3 output rows per work unit
 cudaError_t setup_proxy_tc();
 size_t proxy_tc_smem_bytes();
 cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
-                            void* xt, bool tf32, cudaStream_t st);
+                            void* xt, bool tf32, cudaStream_t st, bool out_f32 = false);
+cudaError_t launch_round_bf16(const float* src, void* dst, size_t n, cudaStream_t st);
 cudaError_t launch_proxy_f32(const float* y, long long ldy, const float* phi, int m, int N, int batch, float* xt,
                              cudaStream_t st);
 cudaError_t launch_pack_phiT(const float* phi, int m, int N, int kpad, void* out, bool bf16, cudaStream_t st);

@@ -122,3 +122,65 @@ def test_two_rank_gradient_allreduce_equals_full_batch_gradient():
     loss, dws, dbs = oracle.train_grad(y, x, phi, p, n1, n2, scale=1.0 / y.shape[0], threads=1)
     ref = np.concatenate([g.ravel() for g in dws + dbs] + [np.array([loss])])
     assert np.allclose(got, ref, rtol=1e-12, atol=1e-15)
+
+
+def _rowshard_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    import oracle
+    from paper_1701_03891_b200.rowshard import batch_range, row_range, sum_scatter
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        phi, y = _rowshard_case()
+        lo, hi = row_range(phi.shape[0], world, rank)
+        part = torch.from_numpy(oracle.proxy(phi[lo:hi], y[:, lo:hi]).reshape(y.shape[0], -1))
+        mine = sum_scatter(part)                       # the one collective of the row-sharded path
+        q.put((rank, (lo, hi), batch_range(y.shape[0], world, rank), mine.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _rowshard_case():
+    r = np.random.default_rng(11)
+    m, n, b = 37, 8, 4
+    return r.standard_normal((m, n * n)) / np.sqrt(m), r.standard_normal((b, m))
+
+
+def test_two_rank_row_sharded_proxy_reduce_scatter():
+    """NEXT-4 host logic: the row blocks tile Phi's rows, and the reduce-scatter of the per-rank partial proxies
+    leaves each rank the full-Phi proxy of its batch block (x_tilde = sum_g Phi_g^T y_g)."""
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rowshard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    res = sorted([q.get(timeout=120) for _ in range(2)], key=lambda t: t[0])
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    phi, y = _rowshard_case()
+    assert [r[1] for r in res] == [(0, 19), (19, 37)]
+    full = oracle.proxy(phi, y).reshape(y.shape[0], -1)
+    for _, _, (lo, hi), mine in res:
+        assert np.allclose(mine, full[lo:hi], rtol=1e-12, atol=1e-12)
+
+
+def test_row_and_batch_ranges():
+    from paper_1701_03891_b200.rowshard import batch_range, row_range
+    for m in (1, 7, 410, 16384):
+        for w in (1, 2, 3, 8):
+            if w > m:
+                continue
+            spans = [row_range(m, w, r) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == m
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+    assert batch_range(8, 4, 3) == (6, 8)
+    import pytest
+    with pytest.raises(ValueError):
+        batch_range(6, 4, 0)
+    with pytest.raises(ValueError):
+        row_range(2, 3, 0)
