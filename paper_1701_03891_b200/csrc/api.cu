@@ -944,12 +944,14 @@ static di_status train_alloc(di_ctx c) {
     CUDA_TRY(di::setup_dgrad2_tf32(c->n2));
     if ((s = al(&c->h1b, B * N * C1 * 2)) != DI_OK) return s;
     if ((s = al(&c->dg2b, B * N * C2 * 2)) != DI_OK) return s;
-    if ((s = al(&c->part_w2, di::wgrad2_tc_part_floats(c->num_sms) * 4)) != DI_OK) return s;
+    if ((s = al(&c->part_w2, std::max(di::wgrad2_tc_part_floats(c->num_sms), di::wgrad13_tc_part_floats(c->num_sms)) * 4)) != DI_OK)
+      return s;
     if ((s = encode_wg2(&c->tmH1b, c->h1b, c->max_batch, c->n1, c->n2, 64, di::wgrad2_tc_h_box_rows())) != DI_OK)
       return s;
     if ((s = encode_wg2(&c->tmDG2b, c->dg2b, c->max_batch, c->n1, c->n2, 32, di::wgrad2_tc_g_box_rows())) != DI_OK)
       return s;
     CUDA_TRY(di::setup_wgrad2_tc(c->n2));
+    CUDA_TRY(di::setup_wgrad13_tc(c->n2));
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
                                     reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d, 0));
   }
@@ -991,10 +993,15 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   const float* xt = reinterpret_cast<const float*>(c->xt);
   const float* h1 = reinterpret_cast<const float*>(c->h1);
   const float* h2 = reinterpret_cast<const float*>(c->h2);
-  CUDA_TRY(di::launch_wgrad(3, h2, c->dxh, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w + n2w,
-                            gb + C1 + C2, st));
+  const bool tc = c->prec == DI_PREC_TF32;   // tensor-core backward (k_dgrad2_tf32, k_wgrad*_tc)
+  if (tc)
+    CUDA_TRY(di::launch_wgrad3_tc(h2, c->dxh, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads + n1w + n2w,
+                                  gb + C1 + C2, c->num_sms, st));
+  else
+    CUDA_TRY(di::launch_wgrad(3, h2, c->dxh, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w + n2w,
+                              gb + C1 + C2, st));
   CUDA_TRY(di::launch_dgrad3_f32(c->dxh, c->wt3, h2, c->dh2, batch, c->n1, c->n2, st));
-  if (c->prec == DI_PREC_TF32) {   // bf16 operands, tcgen05 MN-major contraction over pixels (k_wgrad2_tc.cu)
+  if (tc) {   // bf16 operands, tcgen05 MN-major contraction over pixels (k_wgrad2_tc.cu)
     const size_t npix = (size_t)batch * c->N;
     CUDA_TRY(di::launch_dg2_bf16(c->dh2, npix, c->dg2b, c->part_b, st));
     CUDA_TRY(di::launch_bias_reduce(c->part_b, di::WGRAD_CHUNKS, C2, gb + C1, st));
@@ -1009,7 +1016,11 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
     CUDA_TRY(di::launch_dgrad2_tf32(&c->tmDG2, c->wp2d, h1, batch, c->n1, c->n2, c->dh1, c->num_sms, st));
   else
     CUDA_TRY(di::launch_dgrad2_f32(c->dh2, c->wt2, h1, c->dh1, batch, c->n1, c->n2, st));
-  CUDA_TRY(di::launch_wgrad(1, xt, c->dh1, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads, gb, st));
+  if (tc)
+    CUDA_TRY(di::launch_wgrad1_tc(xt, c->dh1, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads, gb,
+                                  c->num_sms, st));
+  else
+    CUDA_TRY(di::launch_wgrad(1, xt, c->dh1, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads, gb, st));
   return DI_OK;
 }
 

@@ -1,0 +1,373 @@
+// k_wgrad13_tc.cu -- training: the weight gradients of the THIN layers on tcgen05.
+//
+//   layer 1 (C_in = 1):  dwx1[co][a][b] = sum_p dG1[p][co] * x~[p + (a-5, b-5)]           (k_train.cu header)
+//   layer 3 (C_out = 1): dwx3[ci][a][b] = sum_p dG3[p]     * h2[p + (a-5, b-5)][ci]
+//
+// Both contract over pixel positions with one single-channel operand.  As in k_wgrad2_tc.cu the operands are
+// MN-major bf16 tiles (kind::f16; tf32 cannot read MN-major), fp32 accumulation in TMEM over all the CTA's work
+// units, and the taps are descriptor strides -- plus, for the single-channel map, a shared-memory TOEPLITZ
+// EXPANSION: row q of E holds the 16 values map[q + j] (j = 0..15, a 32-B row, SWIZZLE_32B), so that E viewed
+// as an MN-major operand with atoms P rows apart is the (row tap, column tap) x position matrix of the map:
+//   layer 1: A = E(x~) (M = 8 row taps x 16 column taps, atom i = row tap a0 + i at LBO = P rows of E),
+//            B = dG1 strip (SWIZZLE_128B, N = 64 channels), two MMAs per 16 positions (a0 = 0 and a0 = 3; the
+//            rows a = 3..7 of the second are duplicates and discarded);
+//   layer 3: A = h2 strip (SWIZZLE_64B, M = 4 row taps x 32 channels, atoms P positions apart),
+//            B = E'(dG3) with E'[k][j] = dG3[k - j] (N = 16 column taps), three MMAs per 16 positions
+//            (a0 = 0, 4, 7; a = 7 of the third is discarded).
+// The gradient operand (dG1 / dG3) covers only the unit's own output pixels (origin (r0, c0), zero in the 10
+// trailing columns of each P-position row), the activation operand (x~ / h2) carries the 5-pixel halo (origin
+// (r0 - 5, c0 - 5)), so position p + a P + b is pixel p shifted by (a - 5, b - 5) without wrapping into the next
+// row, and every (pixel, tap) product is counted once.  Work units are
+// double-buffered: the 128 threads convert unit i+1 (fp32 -> bf16, swizzled) while the MMAs of unit i run.
+// Bias gradients (sum of the fp32 dG over pixels) are summed by the loading threads in a fixed assignment.
+// Per-CTA partials are reduced in fp64 in a fixed order (deterministic).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "sm100.cuh"
+
+namespace di {
+
+namespace {
+constexpr int R = WG13_ROWS;      // output rows per unit
+constexpr int WSEG = 64;
+constexpr int KS = 11;
+
+struct GeoT13 {
+  int n1, n2, wseg, P, nrb, ncs, units;
+  int off2, stage;                // second region offset, stage bytes
+};
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+
+// layer 1 stage: [dG1: 16 lead + R*P + 32 guard positions x 128 B] [E: 32 lead + NE + 32 guard rows x 32 B]
+__host__ __device__ inline int l1_ne(int P) { return (R + 11) * P + 16; }
+__host__ __device__ inline int l1_nx(int P) { return l1_ne(P) + 16; }
+// layer 3 stage: [h2: 16 lead + NH + 32 guard positions x 64 B] [E': 32 lead + NB + 32 guard rows x 32 B]
+__host__ __device__ inline int l3_nh(int P) { return (R + 11) * P + 32; }
+__host__ __device__ inline int l3_nb(int P) { return R * P + 32; }
+}  // namespace
+
+// =============================================================================================== layer 1
+__global__ void __launch_bounds__(128, 1)
+    k_wgrad1_tc(const float* __restrict__ xt, const float* __restrict__ dg1, GeoT13 g, float* __restrict__ part,
+                float* __restrict__ part_b) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* xs = reinterpret_cast<float*>(smem + 2 * g.stage);
+  __shared__ uint64_t done[2], fin;
+  __shared__ uint32_t tslot;
+  __shared__ float red[128][9];
+  const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
+  const int P = g.P, NE = l1_ne(P), NX = l1_nx(P);
+  if (tid == 0) {
+    mbar_init(&done[0], 1), mbar_init(&done[1], 1), mbar_init(&fin, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<128>(&tslot), tmem_relinquish();
+  for (int s = 0; s < 2; ++s) {   // zero every stage once: leads / guards are never rewritten
+    uint4* p = reinterpret_cast<uint4*>(smem + s * g.stage);
+    for (int i = tid; i < g.stage / 16; i += 128) p[i] = make_uint4(0, 0, 0, 0);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const int per_img = g.nrb * g.ncs;
+  const int cg = tid & 7;   // fixed 8-channel group of this thread's dG1 chunks (bias partials)
+  float bs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const uint32_t id = idesc_f32acc(1, 128, 64, 1, 1);
+  int it = 0;
+  uint32_t acc = 0;
+  for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+    const int s = it & 1;
+    const int b = u / per_img, rem = u - b * per_img;
+    const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
+    const int rows = min(R, g.n1 - r0);
+    uint8_t* d1 = smem + s * g.stage;          // position q at d1 + (16 + q) * 128
+    uint8_t* ex = smem + s * g.stage + g.off2;  // row q at ex + (32 + q) * 32
+    if (it >= 2) mbar_wait(&done[s], ((it >> 1) - 1) & 1);
+    // dG1 of the unit's pixels: position q -> (r0 + q / P, c0 + q % P), columns >= wseg zero; bf16 SW128
+    for (int i = tid; i < R * P * 8; i += 128) {
+      const int q = i >> 3, row = q / P, col = q - row * P;
+      const int gr = r0 + row, gc = c0 + col;
+      uint4 o = make_uint4(0, 0, 0, 0);
+      if (row < rows && col < g.wseg && gc < g.n2) {
+        const float4* src = reinterpret_cast<const float4*>(dg1 + (((size_t)b * g.n1 + gr) * g.n2 + gc) * 64 + 8 * cg);
+        const float4 v0 = __ldg(src), v1 = __ldg(src + 1);
+        bs[0] += v0.x, bs[1] += v0.y, bs[2] += v0.z, bs[3] += v0.w, bs[4] += v1.x, bs[5] += v1.y, bs[6] += v1.z,
+            bs[7] += v1.w;
+        o = make_uint4(pack2(v0.x, v0.y), pack2(v0.z, v0.w), pack2(v1.x, v1.y), pack2(v1.z, v1.w));
+      }
+      *reinterpret_cast<uint4*>(d1 + (16 + q) * 128 + ((cg ^ (q & 7)) << 4)) = o;
+    }
+    // x~ strip with halo: xs[q] = x~(r0 - 5 + q / P, c0 - 5 + q % P)
+    for (int q = tid; q < NX; q += 128) {
+      const int row = q / P, col = q - row * P;
+      const int gr = r0 - 5 + row, gc = c0 - 5 + col;
+      xs[q] = (gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2) ? __ldg(xt + ((size_t)b * g.n1 + gr) * g.n2 + gc) : 0.f;
+    }
+    __syncthreads();
+    // Toeplitz expansion E[q][j] = xs[q + j], SW32 (16-B chunk c at c ^ ((q >> 2) & 1))
+    for (int i = tid; i < 2 * NE; i += 128) {
+      const int q = i >> 1, c = i & 1;
+      const float* x = xs + q + 8 * c;
+      *reinterpret_cast<uint4*>(ex + (32 + q) * 32 + ((c ^ ((q >> 2) & 1)) << 4)) =
+          make_uint4(pack2(x[0], x[1]), pack2(x[2], x[3]), pack2(x[4], x[5]), pack2(x[6], x[7]));
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const int nk = (rows * P + 15) >> 4;
+      uint64_t bd = smem_desc(smem_u32(d1 + 16 * 128), 128, 1024, kSwizzle128B);
+      uint64_t a1 = smem_desc(smem_u32(ex + 32 * 32), P * 32, 256, kSwizzle32B);
+      uint64_t a2 = smem_desc(smem_u32(ex + (32 + 3 * P) * 32), P * 32, 256, kSwizzle32B);
+      for (int k = 0; k < nk; ++k, bd += 128, a1 += 32, a2 += 32) {   // +16 positions
+        umma_f16_ss(tmem, a1, bd, id, acc);
+        umma_f16_ss(tmem + 64, a2, bd, id, acc);
+        acc = 1;
+      }
+      umma_commit(&done[s]);
+    }
+    __syncthreads();   // xs is rewritten by the next unit's loaders
+  }
+  if (tid == 0) umma_commit(&fin);
+  mbar_wait(&fin, 0);
+  tc_fence_after();
+  float* dst = part + ((size_t)blockIdx.x * 128 + warp * 32 + lane) * 128;
+  for (int c = 0; c < 128; c += 16) {
+    uint32_t r[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(dst + c + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[tid][j] = bs[j];
+  __syncthreads();
+  if (tid < 64) {   // channel 8 cg' + j: threads with tid % 8 == cg', in order
+    const int c8 = tid >> 3, j = tid & 7;
+    float t = 0.f;
+    for (int r = c8; r < 128; r += 8) t += red[r][j];
+    part_b[(size_t)blockIdx.x * 64 + tid] = t;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<128>(tmem);
+}
+
+// gw1 [64][11][11] (API orientation), gb1 [64]
+__global__ void k_wgrad1_reduce(const float* __restrict__ part, const float* __restrict__ part_b, int nct, int flip,
+                                float* __restrict__ gw, float* __restrict__ gb) {
+  constexpr int NW = 64 * KS * KS;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NW + 64; i += gridDim.x * blockDim.x) {
+    double t = 0.0;
+    if (i < NW) {
+      const int bb = i % KS, a = (i / KS) % KS, co = i / (KS * KS);
+      const int m = a <= 7 ? a * 16 + bb : (a - 3) * 16 + bb, n = a <= 7 ? co : 64 + co;
+      for (int c = 0; c < nct; ++c) t += part[((size_t)c * 128 + m) * 128 + n];
+      gw[(size_t)co * KS * KS + (flip ? (KS - 1 - a) * KS + (KS - 1 - bb) : a * KS + bb)] = (float)t;
+    } else {
+      for (int c = 0; c < nct; ++c) t += part_b[(size_t)c * 64 + (i - NW)];
+      gb[i - NW] = (float)t;
+    }
+  }
+}
+
+// =============================================================================================== layer 3
+__global__ void __launch_bounds__(128, 1)
+    k_wgrad3_tc(const float* __restrict__ h2, const float* __restrict__ dg3, GeoT13 g, float* __restrict__ part,
+                float* __restrict__ part_b) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* ds = reinterpret_cast<float*>(smem + 2 * g.stage) + 16;   // ds[-16 .. NB + 16)
+  __shared__ uint64_t done[2], fin;
+  __shared__ uint32_t tslot;
+  __shared__ float red[128];
+  const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
+  const int P = g.P, NH = l3_nh(P), NB = l3_nb(P);
+  if (tid == 0) {
+    mbar_init(&done[0], 1), mbar_init(&done[1], 1), mbar_init(&fin, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<64>(&tslot), tmem_relinquish();
+  for (int s = 0; s < 2; ++s) {
+    uint4* p = reinterpret_cast<uint4*>(smem + s * g.stage);
+    for (int i = tid; i < g.stage / 16; i += 128) p[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (int i = tid; i < NB + 32; i += 128) ds[i - 16] = 0.f;
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const int per_img = g.nrb * g.ncs;
+  float bsum = 0.f;
+  const uint32_t id = idesc_f32acc(1, 128, 16, 1, 1);
+  int it = 0;
+  uint32_t acc = 0;
+  for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+    const int s = it & 1;
+    const int b = u / per_img, rem = u - b * per_img;
+    const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
+    const int rows = min(R, g.n1 - r0);
+    uint8_t* hs = smem + s * g.stage;          // position q at hs + (16 + q) * 64
+    uint8_t* ex = smem + s * g.stage + g.off2;  // row k at ex + (32 + k) * 32
+    if (it >= 2) mbar_wait(&done[s], ((it >> 1) - 1) & 1);
+    // h2 strip with halo: q -> h2(r0 - 5 + q / P, c0 - 5 + q % P), bf16 SW64 (chunk c at c ^ ((q >> 1) & 3))
+    for (int i = tid; i < NH * 4; i += 128) {
+      const int q = i >> 2, c = i & 3, row = q / P, col = q - row * P;
+      const int gr = r0 - 5 + row, gc = c0 - 5 + col;
+      uint4 o = make_uint4(0, 0, 0, 0);
+      if (gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2) {
+        const float4* src = reinterpret_cast<const float4*>(h2 + (((size_t)b * g.n1 + gr) * g.n2 + gc) * 32 + 8 * c);
+        const float4 v0 = __ldg(src), v1 = __ldg(src + 1);
+        o = make_uint4(pack2(v0.x, v0.y), pack2(v0.z, v0.w), pack2(v1.x, v1.y), pack2(v1.z, v1.w));
+      }
+      *reinterpret_cast<uint4*>(hs + (16 + q) * 64 + ((c ^ ((q >> 1) & 3)) << 4)) = o;
+    }
+    // dG3 of the unit's own pixels (zero elsewhere): ds[p], p -> (r0 + p / P, c0 + p % P)
+    for (int p = tid; p < R * P; p += 128) {
+      const int row = p / P, col = p - row * P;
+      const int gc = c0 + col;
+      float v = 0.f;
+      if (row < rows && col < g.wseg && gc < g.n2)
+        v = __ldg(dg3 + ((size_t)b * g.n1 + r0 + row) * g.n2 + gc);
+      bsum += v;
+      ds[p] = v;
+    }
+    __syncthreads();
+    // E'[k][j] = ds[k - j], SW32
+    for (int i = tid; i < 2 * NB; i += 128) {
+      const int k = i >> 1, c = i & 1;
+      const float* x = ds + k - 8 * c;   // j = 8c .. 8c + 7 -> ds[k - j]
+      *reinterpret_cast<uint4*>(ex + (32 + k) * 32 + ((c ^ ((k >> 2) & 1)) << 4)) =
+          make_uint4(pack2(x[0], x[-1]), pack2(x[-2], x[-3]), pack2(x[-4], x[-5]), pack2(x[-6], x[-7]));
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const int nk = (rows * P + 11 + 15) >> 4;
+      uint64_t bd = smem_desc(smem_u32(ex + 32 * 32), 32, 256, kSwizzle32B);
+      uint64_t a0 = smem_desc(smem_u32(hs + 16 * 64), P * 64, 512, kSwizzle64B);
+      uint64_t a1 = smem_desc(smem_u32(hs + (16 + 4 * P) * 64), P * 64, 512, kSwizzle64B);
+      uint64_t a2 = smem_desc(smem_u32(hs + (16 + 7 * P) * 64), P * 64, 512, kSwizzle64B);
+      for (int k = 0; k < nk; ++k, bd += 32, a0 += 64, a1 += 64, a2 += 64) {   // +16 positions
+        umma_f16_ss(tmem, a0, bd, id, acc);
+        umma_f16_ss(tmem + 16, a1, bd, id, acc);
+        umma_f16_ss(tmem + 32, a2, bd, id, acc);
+        acc = 1;
+      }
+      umma_commit(&done[s]);
+    }
+    __syncthreads();   // ds is rewritten by the next unit
+  }
+  if (tid == 0) umma_commit(&fin);
+  mbar_wait(&fin, 0);
+  tc_fence_after();
+  float* dst = part + ((size_t)blockIdx.x * 128 + warp * 32 + lane) * 48;
+  for (int c = 0; c < 48; c += 16) {
+    uint32_t r[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(dst + c + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+  }
+  red[tid] = bsum;
+  __syncthreads();
+  if (tid == 0) {
+    float t = 0.f;
+    for (int r = 0; r < 128; ++r) t += red[r];
+    part_b[blockIdx.x] = t;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<64>(tmem);
+}
+
+// gw3 [32][11][11] (API orientation of W3 [1][32][11][11]), gb3 [1]
+__global__ void k_wgrad3_reduce(const float* __restrict__ part, const float* __restrict__ part_b, int nct, int flip,
+                                float* __restrict__ gw, float* __restrict__ gb) {
+  constexpr int NW = 32 * KS * KS;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NW + 1; i += gridDim.x * blockDim.x) {
+    double t = 0.0;
+    if (i < NW) {
+      const int bb = i % KS, a = (i / KS) % KS, ci = i / (KS * KS);
+      const int grp = a < 4 ? 0 : a < 8 ? 1 : 2, ii = a - (grp == 0 ? 0 : grp == 1 ? 4 : 7);
+      const int m = ii * 32 + ci, n = grp * 16 + bb;
+      for (int c = 0; c < nct; ++c) t += part[((size_t)c * 128 + m) * 48 + n];
+      gw[(size_t)ci * KS * KS + (flip ? (KS - 1 - a) * KS + (KS - 1 - bb) : a * KS + bb)] = (float)t;
+    } else {
+      for (int c = 0; c < nct; ++c) t += part_b[c];
+      gb[0] = (float)t;
+    }
+  }
+}
+
+// =============================================================================================== host
+static GeoT13 make_geo(int batch, int n1, int n2, bool l1) {
+  GeoT13 g;
+  g.n1 = n1, g.n2 = n2;
+  g.wseg = n2 < WSEG ? n2 : WSEG;
+  g.P = g.wseg + 10;
+  g.nrb = (n1 + R - 1) / R;
+  g.ncs = (n2 + g.wseg - 1) / g.wseg;
+  g.units = batch * g.nrb * g.ncs;
+  int r1, r2;
+  if (l1) {
+    r1 = (16 + R * g.P + 32) * 128;
+    r2 = (32 + l1_ne(g.P) + 32) * 32;
+  } else {
+    r1 = (16 + l3_nh(g.P) + 32) * 64;
+    r2 = (32 + l3_nb(g.P) + 32) * 32;
+  }
+  g.off2 = (r1 + 1023) & ~1023;
+  g.stage = (g.off2 + r2 + 1023) & ~1023;
+  return g;
+}
+
+static size_t smem_bytes(int n2, bool l1) {
+  GeoT13 g = make_geo(1, 1, n2, l1);
+  const size_t extra = l1 ? (size_t)(l1_nx(g.P) + 16) * 4 : (size_t)(l3_nb(g.P) + 48) * 4;
+  return 2 * (size_t)g.stage + extra + 1024;
+}
+
+size_t wgrad13_tc_part_floats(int num_sms) { return (size_t)num_sms * 128 * 128; }
+
+cudaError_t setup_wgrad13_tc(int n2) {
+  cudaError_t e = cudaFuncSetAttribute(k_wgrad1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_bytes(n2, true));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_wgrad3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(n2, false));
+}
+
+cudaError_t launch_wgrad1_tc(const float* xt, const float* dg1, int batch, int n1, int n2, float* part, float* part_b,
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st) {
+  GeoT13 g = make_geo(batch, n1, n2, true);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  k_wgrad1_tc<<<grid, 128, smem_bytes(n2, true), st>>>(xt, dg1, g, part, part_b);
+  k_wgrad1_reduce<<<(64 * KS * KS + 64 + 255) / 256, 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wgrad3_tc(const float* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st) {
+  GeoT13 g = make_geo(batch, n1, n2, false);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  k_wgrad3_tc<<<grid, 128, smem_bytes(n2, false), st>>>(h2, dg3, g, part, part_b);
+  k_wgrad3_reduce<<<(32 * KS * KS + 1 + 255) / 256, 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
+  return cudaGetLastError();
+}
+
+}  // namespace di

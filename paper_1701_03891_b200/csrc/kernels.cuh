@@ -114,6 +114,14 @@ cudaError_t launch_wgrad2_tc(const CUtensorMap* tmH, const CUtensorMap* tmG, int
                              int flip, float* gw, int num_sms, cudaStream_t st);
 cudaError_t launch_to_bf16(const float* src, void* dst, size_t n, cudaStream_t st);
 cudaError_t launch_dg2_bf16(const float* dg, size_t npix, void* dst, float* part_b, cudaStream_t st);
+// training, TF32 contexts: layer-1 / layer-3 weight gradients on tcgen05 (k_wgrad13_tc.cu)
+constexpr int WG13_ROWS = 6;
+size_t wgrad13_tc_part_floats(int num_sms);
+cudaError_t setup_wgrad13_tc(int n2);
+cudaError_t launch_wgrad1_tc(const float* xt, const float* dg1, int batch, int n1, int n2, float* part, float* part_b,
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st);
+cudaError_t launch_wgrad3_tc(const float* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st);
 cudaError_t launch_bias_reduce(const float* part_b, int nchunk, int nb, float* gb, cudaStream_t st);
 cudaError_t launch_sgd_repack(float* params, const float* grads, float* vel, int n, float lr, float momentum, int flip,
                               float* wx1, float* wx2, float* wx3, float* wt2, float* wt3, float* b1, float* b2,

@@ -159,6 +159,62 @@ __global__ void kb2(const float* S, const float* S2, int a0, int PA, int b0, int
   __syncthreads();
   if (threadIdx.x < 32) tmem_dealloc<256>(tmem);
 }
+// generic MN-major probe: A rows of RA bytes (SWA swizzle), M = 128 as NA_M atoms of RA/2 elements at stride PA
+// rows; B rows of RB bytes, N = RB/2 (one atom).  A[g*EA + i][k] = SA[a0 + g*PA + k][i], B[k][j] = SB[b0 + k][j]
+__device__ __forceinline__ uint32_t swz(uint32_t lin, int R) {   // address-based swizzle of byte offset lin
+  if (R == 128) return lin ^ (((lin >> 7) & 7) << 4);
+  if (R == 64) return lin ^ (((lin >> 7) & 3) << 4);
+  return lin ^ (((lin >> 7) & 1) << 4);
+}
+__global__ void kg(const float* S, const float* S2, int RA, int RB, int a0, int PA, int b0, int KS, float* D) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = sm;
+  uint8_t* sB = sm + ROWS * 128;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int EA = RA / 2, EB = RB / 2;
+  for (int e = threadIdx.x; e < ROWS * EA; e += blockDim.x) {
+    const int r = e / EA, c = e % EA;
+    const uint32_t lin = r * RA + (c / 8) * 16;
+    *reinterpret_cast<__nv_bfloat16*>(sA + swz(lin, RA) + (c % 8) * 2) = __float2bfloat16(S[e]);
+  }
+  for (int e = threadIdx.x; e < ROWS * EB; e += blockDim.x) {
+    const int r = e / EB, c = e % EB;
+    const uint32_t lin = r * RB + (c / 8) * 16;
+    *reinterpret_cast<__nv_bfloat16*>(sB + swz(lin, RB) + (c % 8) * 2) = __float2bfloat16(S2[e]);
+  }
+  fence_async_smem();
+  if (threadIdx.x == 0) mbar_init(&bar, 1), fence_mbar_init();
+  if (threadIdx.x < 32) tmem_alloc<256>(&tslot), tmem_relinquish();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t lay = [](int R) { return R == 128 ? kSwizzle128B : R == 64 ? kSwizzle64B : kSwizzle32B; }(RA);
+  const uint32_t layb = RB == 128 ? kSwizzle128B : RB == 64 ? kSwizzle64B : kSwizzle32B;
+  if (threadIdx.x == 0) {
+    const uint32_t id = idesc_f32acc(1, 128, EB, 1, 1);
+    for (int ks = 0; ks < KS; ++ks) {
+      const uint64_t ad = smem_desc(smem_u32(sA + (a0 + 16 * ks) * RA), PA * RA, 8 * RA, lay);
+      const uint64_t bd = smem_desc(smem_u32(sB + (b0 + 16 * ks) * RB), RB, 8 * RB, layb);
+      umma_f16_ss(tmem, ad, bd, id, ks > 0);
+    }
+    umma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  for (int c = 0; c < EB; c += 16) {
+    uint32_t r[16];
+    tmem_ld16(tmem + ((uint32_t)(w * 32) << 16) + c, r);
+    tmem_ld_wait();
+    for (int j = 0; j < 16; ++j) D[(w * 32 + l) * 256 + c + j] = __uint_as_float(r[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<256>(tmem);
+}
 static float bfr(float x) { return __bfloat162float(__float2bfloat16(x)); }
 
 static float tf(float x) {
@@ -317,6 +373,38 @@ int main() {
         }
       printf("kb2 %s a0=%d PA=%d b0=%d NA=%d KS=%d maxerr=%.3g max|D|=%.3g\n", cudaGetErrorString(e), cs.a0, cs.PA,
              cs.b0, cs.NA, cs.KS, maxerr, mx);
+    }
+  }
+  cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * ROWS * 128 + 1024);
+  {
+    std::vector<float> A(ROWS * 64), B(ROWS * 64);
+    for (auto& v : A) v = rnd();
+    for (auto& v : B) v = rnd();
+    float *dA, *dB;
+    cudaMalloc(&dA, A.size() * 4), cudaMalloc(&dB, B.size() * 4);
+    cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
+    struct C { int RA, RB, a0, PA, b0, KS; } cb[] = {{32, 128, 0, 16, 0, 1}, {32, 128, 3, 21, 5, 3}, {32, 128, 1, 74, 9, 4},
+                                                     {64, 32, 0, 16, 0, 1}, {64, 32, 3, 21, 5, 3}, {64, 32, 2, 40, 7, 4},
+                                                     {128, 32, 5, 33, 2, 3}};
+    for (auto cs : cb) {
+      cudaMemset(dD, 0, 128 * 256 * 4);
+      kg<<<1, 128, 2 * ROWS * 128 + 1024>>>(dA, dB, cs.RA, cs.RB, cs.a0, cs.PA, cs.b0, cs.KS, dD);
+      cudaError_t e = cudaDeviceSynchronize();
+      std::vector<float> D(128 * 256);
+      cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+      const int EA = cs.RA / 2, EB = cs.RB / 2;
+      double maxerr = 0, mx = 0;
+      for (int m = 0; m < 128; ++m)
+        for (int n = 0; n < EB; ++n) {
+          const int g = m / EA, i = m % EA;
+          double ref = 0;
+          for (int kk = 0; kk < 16 * cs.KS; ++kk)
+            ref += (double)bfr(A[(cs.a0 + g * cs.PA + kk) * EA + i]) * bfr(B[(cs.b0 + kk) * EB + n]);
+          maxerr = fmax(maxerr, fabs(ref - D[m * 256 + n])), mx = fmax(mx, fabs(D[m * 256 + n]));
+        }
+      printf("kg %s RA=%d RB=%d a0=%d PA=%d b0=%d KS=%d maxerr=%.3g max|D|=%.3g\n", cudaGetErrorString(e), cs.RA, cs.RB,
+             cs.a0, cs.PA, cs.b0, cs.KS, maxerr, mx);
     }
   }
   return 0;
