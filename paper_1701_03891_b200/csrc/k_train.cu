@@ -176,8 +176,24 @@ static cudaError_t wgrad(const float* X, const float* dG, int batch, int n1, int
   return cudaGetLastError();
 }
 
+// gb[j] = sum over chunks of part_b[chunk][j]: one block per output, fixed strided fp64 partials + fixed tree
+__global__ void __launch_bounds__(256) k_bias_reduce(const float* __restrict__ part_b, int nchunk, int nb,
+                                                     float* __restrict__ gb) {
+  __shared__ double sh[256];
+  const int j = blockIdx.x;
+  double t = 0.0;
+  for (int c = threadIdx.x; c < nchunk; c += 256) t += part_b[(size_t)c * nb + j];
+  sh[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) gb[j] = (float)sh[0];
+}
+
 cudaError_t launch_bias_reduce(const float* part_b, int nchunk, int nb, float* gb, cudaStream_t st) {
-  k_wgrad_reduce<<<1, 256, 0, st>>>(nullptr, part_b, nchunk, 0, nb, 0, nullptr, gb);
+  k_bias_reduce<<<nb, 256, 0, st>>>(part_b, nchunk, nb, gb);
   return cudaGetLastError();
 }
 

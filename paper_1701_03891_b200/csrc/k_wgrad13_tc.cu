@@ -93,24 +93,44 @@ __global__ void __launch_bounds__(128, 1)
     uint8_t* ex = smem + s * g.stage + g.off2;  // row q at ex + (32 + q) * 32
     if (it >= 2) mbar_wait(&done[s], ((it >> 1) - 1) & 1);
     // dG1 of the unit's pixels: position q -> (r0 + q / P, c0 + q % P), columns >= wseg zero; bf16 SW128
-    for (int i = tid; i < R * P * 8; i += 128) {
-      const int q = i >> 3, row = q / P, col = q - row * P;
-      const int gr = r0 + row, gc = c0 + col;
-      uint4 o = make_uint4(0, 0, 0, 0);
-      if (row < rows && col < g.wseg && gc < g.n2) {
-        const float4* src = reinterpret_cast<const float4*>(dg1 + (((size_t)b * g.n1 + gr) * g.n2 + gc) * 64 + 8 * cg);
-        const float4 v0 = __ldg(src), v1 = __ldg(src + 1);
+    constexpr int U = 4;   // chunks per thread in flight (memory-level parallelism)
+    for (int i0 = tid; i0 < R * P * 8; i0 += 128 * U) {
+      float4 v[U][2];
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int i = i0 + uu * 128, q = i >> 3, row = q / P, col = q - row * P;
+        const int gr = r0 + row, gc = c0 + col;
+        v[uu][0] = v[uu][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < R * P * 8 && row < rows && col < g.wseg && gc < g.n2) {
+          const float4* src =
+              reinterpret_cast<const float4*>(dg1 + (((size_t)b * g.n1 + gr) * g.n2 + gc) * 64 + 8 * cg);
+          v[uu][0] = __ldg(src), v[uu][1] = __ldg(src + 1);
+        }
+      }
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int i = i0 + uu * 128, q = i >> 3;
+        if (i >= R * P * 8) break;
+        const float4 v0 = v[uu][0], v1 = v[uu][1];
         bs[0] += v0.x, bs[1] += v0.y, bs[2] += v0.z, bs[3] += v0.w, bs[4] += v1.x, bs[5] += v1.y, bs[6] += v1.z,
             bs[7] += v1.w;
-        o = make_uint4(pack2(v0.x, v0.y), pack2(v0.z, v0.w), pack2(v1.x, v1.y), pack2(v1.z, v1.w));
+        *reinterpret_cast<uint4*>(d1 + (16 + q) * 128 + ((cg ^ (q & 7)) << 4)) =
+            make_uint4(pack2(v0.x, v0.y), pack2(v0.z, v0.w), pack2(v1.x, v1.y), pack2(v1.z, v1.w));
       }
-      *reinterpret_cast<uint4*>(d1 + (16 + q) * 128 + ((cg ^ (q & 7)) << 4)) = o;
     }
     // x~ strip with halo: xs[q] = x~(r0 - 5 + q / P, c0 - 5 + q % P)
-    for (int q = tid; q < NX; q += 128) {
-      const int row = q / P, col = q - row * P;
-      const int gr = r0 - 5 + row, gc = c0 - 5 + col;
-      xs[q] = (gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2) ? __ldg(xt + ((size_t)b * g.n1 + gr) * g.n2 + gc) : 0.f;
+    for (int q0 = tid; q0 < NX; q0 += 128 * 8) {
+      float v[8];
+#pragma unroll
+      for (int uu = 0; uu < 8; ++uu) {
+        const int q = q0 + uu * 128, row = q / P, col = q - row * P;
+        const int gr = r0 - 5 + row, gc = c0 - 5 + col;
+        v[uu] = (q < NX && gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2)
+                    ? __ldg(xt + ((size_t)b * g.n1 + gr) * g.n2 + gc) : 0.f;
+      }
+#pragma unroll
+      for (int uu = 0; uu < 8; ++uu)
+        if (q0 + uu * 128 < NX) xs[q0 + uu * 128] = v[uu];
     }
     __syncthreads();
     // Toeplitz expansion E[q][j] = xs[q + j], SW32 (16-B chunk c at c ^ ((q >> 2) & 1))
@@ -223,26 +243,41 @@ __global__ void __launch_bounds__(128, 1)
     uint8_t* ex = smem + s * g.stage + g.off2;  // row k at ex + (32 + k) * 32
     if (it >= 2) mbar_wait(&done[s], ((it >> 1) - 1) & 1);
     // h2 strip with halo: q -> h2(r0 - 5 + q / P, c0 - 5 + q % P), bf16 SW64 (chunk c at c ^ ((q >> 1) & 3))
-    for (int i = tid; i < NH * 4; i += 128) {
-      const int q = i >> 2, c = i & 3, row = q / P, col = q - row * P;
-      const int gr = r0 - 5 + row, gc = c0 - 5 + col;
-      uint4 o = make_uint4(0, 0, 0, 0);
-      if (gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2) {
-        const float4* src = reinterpret_cast<const float4*>(h2 + (((size_t)b * g.n1 + gr) * g.n2 + gc) * 32 + 8 * c);
-        const float4 v0 = __ldg(src), v1 = __ldg(src + 1);
-        o = make_uint4(pack2(v0.x, v0.y), pack2(v0.z, v0.w), pack2(v1.x, v1.y), pack2(v1.z, v1.w));
+    constexpr int U = 4;
+    for (int i0 = tid; i0 < NH * 4; i0 += 128 * U) {
+      float4 v[U][2];
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int i = i0 + uu * 128, q = i >> 2, c = i & 3, row = q / P, col = q - row * P;
+        const int gr = r0 - 5 + row, gc = c0 - 5 + col;
+        v[uu][0] = v[uu][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < NH * 4 && gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2) {
+          const float4* src = reinterpret_cast<const float4*>(h2 + (((size_t)b * g.n1 + gr) * g.n2 + gc) * 32 + 8 * c);
+          v[uu][0] = __ldg(src), v[uu][1] = __ldg(src + 1);
+        }
       }
-      *reinterpret_cast<uint4*>(hs + (16 + q) * 64 + ((c ^ ((q >> 1) & 3)) << 4)) = o;
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int i = i0 + uu * 128, q = i >> 2, c = i & 3;
+        if (i >= NH * 4) break;
+        const float4 v0 = v[uu][0], v1 = v[uu][1];
+        *reinterpret_cast<uint4*>(hs + (16 + q) * 64 + ((c ^ ((q >> 1) & 3)) << 4)) =
+            make_uint4(pack2(v0.x, v0.y), pack2(v0.z, v0.w), pack2(v1.x, v1.y), pack2(v1.z, v1.w));
+      }
     }
     // dG3 of the unit's own pixels (zero elsewhere): ds[p], p -> (r0 + p / P, c0 + p % P)
-    for (int p = tid; p < R * P; p += 128) {
-      const int row = p / P, col = p - row * P;
-      const int gc = c0 + col;
-      float v = 0.f;
-      if (row < rows && col < g.wseg && gc < g.n2)
-        v = __ldg(dg3 + ((size_t)b * g.n1 + r0 + row) * g.n2 + gc);
-      bsum += v;
-      ds[p] = v;
+    for (int p0 = tid; p0 < R * P; p0 += 128 * 4) {
+      float v[4];
+#pragma unroll
+      for (int uu = 0; uu < 4; ++uu) {
+        const int p = p0 + uu * 128, row = p / P, col = p - row * P;
+        const int gc = c0 + col;
+        v[uu] = (p < R * P && row < rows && col < g.wseg && gc < g.n2)
+                    ? __ldg(dg3 + ((size_t)b * g.n1 + r0 + row) * g.n2 + gc) : 0.f;
+      }
+#pragma unroll
+      for (int uu = 0; uu < 4; ++uu)
+        if (p0 + uu * 128 < R * P) bsum += v[uu], ds[p0 + uu * 128] = v[uu];
     }
     __syncthreads();
     // E'[k][j] = ds[k - j], SW32
