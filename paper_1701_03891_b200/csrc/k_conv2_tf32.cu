@@ -23,7 +23,7 @@ constexpr int R = C2_ROWS;             // output rows per unit (6)
 constexpr int WSEG = 64;
 constexpr int NT = 256;
 constexpr int OUT_PER_TILE = NT - 3;   // 253
-constexpr int WSTAGES = 4;
+constexpr int WSTAGES = 3;   // 3 x 16 KB: room for two epilogue groups' staging
 constexpr int KB_HALF = C2_KBLOCKS;    // 33 K-blocks per channel half
 constexpr uint32_t WBYTES = C2_KBLOCK_BYTES;  // 16 KB: 128 rows x 32 fp32 channels
 constexpr int GUARD_ROWS = 24;
@@ -41,7 +41,7 @@ __device__ __forceinline__ void ld_tail13_t(uint32_t taddr, uint32_t* r) {
   tmem_ld1(taddr + 12, r + 12);
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     k_conv2_tf32(const __grid_constant__ CUtensorMap tmH1, const float* __restrict__ wpack,
                  const float* __restrict__ bias, int fullmap, GeoT g, float* __restrict__ h2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmH1);
     mbar_init(&sfull, 1), mbar_init(&sempty, 1);
     for (int s = 0; s < WSTAGES; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], 1);
-    mbar_init(&tfull, 1), mbar_init(&tempty, 4);
+    mbar_init(&tfull, 1), mbar_init(&tempty, 8);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
@@ -142,10 +142,11 @@ __global__ void __launch_bounds__(256, 1)
         umma_commit(&tfull);
       }
     }
-  } else if (warp >= 4) {  // ---------------------------------------------- epilogue
-    const int q = warp - 4;
-    const int e = threadIdx.x - 128;
+  } else if (warp >= 4) {  // ---------------------------------------------- epilogue: group grp = tile grp
+    const int q = warp & 3, grp = (warp - 4) >> 2;   // TMEM lane quadrant = warp % 4
+    const int e = (threadIdx.x - 128) & 127;
     const int jj = e >> 3, kg = e & 7;   // output position jj of the chunk, channels 4kg..4kg+3
+    float* const sPg = sP + grp * (4 * ECH * SPS);
     float4 bch = make_float4(0.f, 0.f, 0.f, 0.f);
     if (!fullmap && bias) bch = *reinterpret_cast<const float4*>(bias + 4 * kg);
     int it = 0;
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(256, 1)
       const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
       mbar_wait(&tfull, it & 1);
       tc_fence_after();
-      for (int t = 0; t < ntiles; ++t) {
+      for (int t = grp; t < ntiles; t += 2) {
         const int n0 = t * OUT_PER_TILE;
         const int cnt = min(OUT_PER_TILE, L - n0);
         const uint32_t tq = tmem + t * 256 + ((uint32_t)(q * 32) << 16);
@@ -169,10 +170,10 @@ __global__ void __launch_bounds__(256, 1)
           else
             ld_tail13_t(tq + c + q, r);
           tmem_ld_wait();
-          float* dst = sP + q * (ECH * SPS) + lane;
+          float* dst = sPg + q * (ECH * SPS) + lane;
 #pragma unroll
           for (int j = 0; j < ECH; ++j) dst[j * SPS] = __uint_as_float(r[j]);
-          named_bar(1, 128);
+          named_bar(1 + grp, 128);
           if (jj < nout) {
             const int o = n0 + c + jj;
             const int rr = o / g.P, cc = o - rr * g.P;
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(256, 1)
               float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
               for (int qq = 0; qq < 4; ++qq) {
-                const float4 a = *reinterpret_cast<const float4*>(sP + qq * (ECH * SPS) + jj * SPS + 4 * kg);
+                const float4 a = *reinterpret_cast<const float4*>(sPg + qq * (ECH * SPS) + jj * SPS + 4 * kg);
                 sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
               }
               const size_t pix = ((size_t)b * g.n1 + r0 + rr) * g.n2 + c0 + cc;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(256, 1)
               *reinterpret_cast<float4*>(h2 + pix * 32 + 4 * kg) = sum;
             }
           }
-          named_bar(1, 128);
+          named_bar(1 + grp, 128);
         }
       }
       tc_fence_before();
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(256, 1)
 // D[64+ci][o-n0+1]; the epilogue applies the layer-1 ReLU mask and writes dH1 fp32 NHWC.
 constexpr int KB_DG = 66;
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     k_dgrad2_tf32(const __grid_constant__ CUtensorMap tmDG, const float* __restrict__ wpack,
                   const float* __restrict__ h1, GeoT g, float* __restrict__ dh1) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmDG);
     mbar_init(&sfull, 1), mbar_init(&sempty, 1);
     for (int s = 0; s < WSTAGES; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], 1);
-    mbar_init(&tfull, 1), mbar_init(&tempty, 4);
+    mbar_init(&tfull, 1), mbar_init(&tempty, 8);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
@@ -310,9 +311,11 @@ __global__ void __launch_bounds__(256, 1)
         umma_commit(&tfull);
       }
     }
-  } else if (warp >= 4) {  // ---------------------------------------------- epilogue
-    const int q = warp - 4, shift = q >> 1;   // TMEM quadrant q: tap v' = q / 2, channels 32 (q % 2) + lane
-    const int e = threadIdx.x - 128;
+  } else if (warp >= 4) {  // ---------------------------------------------- epilogue: group grp = tile grp
+    const int q = warp & 3, shift = q >> 1;   // TMEM quadrant q: tap v' = q / 2, channels 32 (q % 2) + lane
+    const int grp = (warp - 4) >> 2;
+    const int e = (threadIdx.x - 128) & 127;
+    float* const sPg = sP + grp * (4 * ECH * SPS);
     const int jj = e >> 3, kg = e & 7;        // output position jj of the chunk, channels 8kg..8kg+7
     const int hq = kg >> 2, cl = (kg & 3) * 8;
     int it = 0;
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(256, 1)
       const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
       mbar_wait(&tfull, it & 1);
       tc_fence_after();
-      for (int t = 0; t < ntiles; ++t) {
+      for (int t = grp; t < ntiles; t += 2) {
         const int n0 = t * OUT_PER_TILE;
         const int cnt = min(OUT_PER_TILE, L - n0);
         const uint32_t tq = tmem + t * 256 + ((uint32_t)(q * 32) << 16);
@@ -336,15 +339,15 @@ __global__ void __launch_bounds__(256, 1)
           else
             ld_tail13_t(tq + c + shift, r);
           tmem_ld_wait();
-          float* dst = sP + q * (ECH * SPS) + lane;
+          float* dst = sPg + q * (ECH * SPS) + lane;
 #pragma unroll
           for (int j = 0; j < ECH; ++j) dst[j * SPS] = __uint_as_float(r[j]);
-          named_bar(1, 128);
+          named_bar(1 + grp, 128);
           if (jj < nout) {
             const int o = n0 + c + jj;
             const int rr = o / g.P, cc = o - rr * g.P;
             if (cc < g.wseg && c0 + cc < g.n2 && rr < rows) {
-              const float* s0 = sP + hq * (ECH * SPS) + jj * SPS + cl;
+              const float* s0 = sPg + hq * (ECH * SPS) + jj * SPS + cl;
               const float* s1 = s0 + 2 * (ECH * SPS);
               const size_t pix = ((size_t)b * g.n1 + r0 + rr) * g.n2 + c0 + cc;
 #pragma unroll
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
           }
-          named_bar(1, 128);
+          named_bar(1 + grp, 128);
         }
       }
       tc_fence_before();
@@ -385,7 +388,7 @@ static GeoT make_geo_t(int batch, int n1, int n2) {
 size_t conv2_tf32_smem_bytes(int n2) {
   const int wseg = n2 < WSEG ? n2 : WSEG, P = wseg + 10;
   const size_t strip_alloc = ((size_t)(R + 10) * P * 128 + GUARD_ROWS * 128 + 1023) & ~(size_t)1023;
-  return strip_alloc + WSTAGES * WBYTES + 4 * ECH * SPS * 4 + 1024;
+  return strip_alloc + WSTAGES * WBYTES + 2 * 4 * ECH * SPS * 4 + 1024;
 }
 
 int conv2_tf32_box_rows() { return R + 10; }
@@ -399,7 +402,7 @@ cudaError_t launch_conv2_tf32(const CUtensorMap* tmH1, const void* wpack, const 
                               int n1, int n2, float* h2, int num_sms, cudaStream_t st) {
   GeoT g = make_geo_t(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv2_tf32<<<grid, 256, conv2_tf32_smem_bytes(n2), st>>>(*tmH1, reinterpret_cast<const float*>(wpack), bias,
+  k_conv2_tf32<<<grid, 384, conv2_tf32_smem_bytes(n2), st>>>(*tmH1, reinterpret_cast<const float*>(wpack), bias,
                                                              fullmap, g, h2);
   return cudaGetLastError();
 }
@@ -413,7 +416,7 @@ cudaError_t launch_dgrad2_tf32(const CUtensorMap* tmDG, const void* wpack, const
                                float* dh1, int num_sms, cudaStream_t st) {
   GeoT g = make_geo_t(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_dgrad2_tf32<<<grid, 256, conv2_tf32_smem_bytes(n2), st>>>(*tmDG, reinterpret_cast<const float*>(wpack), h1, g,
+  k_dgrad2_tf32<<<grid, 384, conv2_tf32_smem_bytes(n2), st>>>(*tmDG, reinterpret_cast<const float*>(wpack), h1, g,
                                                               dh1);
   return cudaGetLastError();
 }
