@@ -88,6 +88,9 @@ struct di_ctx_s {
   void* wp3 = nullptr;          // conv3 tensor-core weight blocks (BF16 mode, SWIZZLE_64B image)
   void* wp2t = nullptr;         // conv2 TF32 weight blocks (TF32 mode)
   float* wp2d = nullptr;        // training, TF32 mode: layer-2 dgrad weight blocks (k_dgrad2_tf32)
+  float* wpd3 = nullptr;        // training, TF32 mode: layer-3 dgrad bank in the conv1 TF32 layout
+  bool has_tmDX = false;
+  CUtensorMap tmDX;             // training, TF32 mode: dG3 strips (the conv1 x_tilde map over dxh)
   CUtensorMap tmDG2;            // training, TF32 mode: dG2 strips (fp32, 32 channels)
   void *h1b = nullptr, *dg2b = nullptr;   // training, TF32 mode: bf16 copies of h1 / dG2 (layer-2 wgrad operands)
   float* part_w2 = nullptr;     // training, TF32 mode: per-CTA layer-2 wgrad partials
@@ -392,7 +395,7 @@ di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n
 
 void free_ctx(di_ctx c) {
   if (!c) return;
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->h1b, c->dg2b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->wpd3, c->h1b, c->dg2b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
                 c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->phi_sense, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
@@ -952,8 +955,13 @@ static di_status train_alloc(di_ctx c) {
       return s;
     CUDA_TRY(di::setup_wgrad2_tc(c->n2));
     CUDA_TRY(di::setup_wgrad13_tc(c->n2));
+    if (c->n2 % 4 == 0) {   // the conv1 TF32 strip map over dG3 (16-B row stride)
+      if ((s = al(&c->wpd3, (size_t)11 * 4096)) != DI_OK) return s;
+      if ((s = encode_xt(&c->tmDX, c->dxh, c->max_batch, c->n1, c->n2, true)) != DI_OK) return s;
+      c->has_tmDX = true;
+    }
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
-                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d, 0));
+                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d, c->wpd3, 0));
   }
   CUDA_TRY(cudaDeviceSynchronize());
   return DI_OK;
@@ -1000,7 +1008,10 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   else
     CUDA_TRY(di::launch_wgrad(3, h2, c->dxh, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w + n2w,
                               gb + C1 + C2, st));
-  CUDA_TRY(di::launch_dgrad3_f32(c->dxh, c->wt3, h2, c->dh2, batch, c->n1, c->n2, st));
+  if (tc && c->has_tmDX)
+    CUDA_TRY(di::launch_dgrad3_tf32(&c->tmDX, c->wpd3, h2, c->dh2, batch, c->n1, c->n2, c->num_sms, st));
+  else
+    CUDA_TRY(di::launch_dgrad3_f32(c->dxh, c->wt3, h2, c->dh2, batch, c->n1, c->n2, st));
   if (tc) {   // bf16 operands, tcgen05 MN-major contraction over pixels (k_wgrad2_tc.cu)
     const size_t npix = (size_t)batch * c->N;
     CUDA_TRY(di::launch_dg2_bf16(c->dh2, npix, c->dg2b, c->part_b, st));
@@ -1035,7 +1046,7 @@ di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, 
   if (c->prec == DI_PREC_TF32)
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
                                     reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d,
-                                    reinterpret_cast<cudaStream_t>(stream)));
+                                    c->wpd3, reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }
 

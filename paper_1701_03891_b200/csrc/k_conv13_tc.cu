@@ -383,9 +383,15 @@ constexpr int IM_BYTES_T = IM_ROWS_T * 64;
 constexpr int W1T_BYTES = 11 * 64 * 64;                      // 11 tap rows x 64 filters x 16 fp32 taps
 constexpr int XT_STRIDE = ((R1T + 10) * (P1MAX + 8) * 4 + 128 + 127) & ~127;
 
+// DG3 = true: the training step's layer-3 data gradient on the same machinery:
+//   dH2[p][ci] = [h2[p][ci] > 0] * sum_{u,v} wx3[0][ci][10-u][10-v] * dG3[p + (u-5, v-5)]
+// is a 1 -> 32 'same' correlation: the strip is dG3 (tmX over dG3), the packed filters are the rotated layer-3
+// taps in rows 0..31 (rows 32..63 zero), and the epilogue writes 32 channels masked by h2 instead of bias+ReLU.
+template <bool DG3>
 __global__ void __launch_bounds__(384, 1)
     k_conv1_tf32(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ w1pack,
-                 const float* __restrict__ bias, int fullmap, Geo13 g, float* __restrict__ h1) {
+                 const float* __restrict__ bias, int fullmap, Geo13 g, float* __restrict__ h1,
+                 const float* __restrict__ mask) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* wbuf = smem;                                 // 44 KB
@@ -511,10 +517,37 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const int pbase = n0 + (q >> 1) * half;
         const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32 + 16 * hh) << 16);
-        for (int c = 0; c < half; c += 32) {
+        for (int c = 0; c < half && !(DG3 && ch >= 32); c += 32) {   // DG3: warps of rows >= 32 idle
           uint32_t r[16];
           tmem_ld_16x256b_x4(taddr + c, r);
           tmem_ld_wait();
+          if (DG3) {   // all 8 mask loads in flight before the stores
+            size_t pixv[8];
+            bool ok[8];
+            float2 m[8];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const int p = pbase + c + 8 * (kk >> 1) + cpair + (kk & 1);
+              ok[kk] = p < n0 + cnt;
+              if (linear) {
+                pixv[kk] = pix0 + p;
+              } else {
+                const int rr = (int)(((uint32_t)p * wmagic) >> 20), cc = p - rr * W;
+                ok[kk] = ok[kk] && c0 + cc < g.n2;
+                pixv[kk] = pix0 + (size_t)rr * g.n2 + cc;
+              }
+              m[kk] = ok[kk] ? __ldg(reinterpret_cast<const float2*>(mask + pixv[kk] * 32 + ch)) : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const float v0 = __uint_as_float(r[4 * (kk >> 1) + (kk & 1)]);
+              const float v1 = __uint_as_float(r[4 * (kk >> 1) + 2 + (kk & 1)]);
+              if (ok[kk])
+                *reinterpret_cast<float2*>(h1 + pixv[kk] * 32 + ch) =
+                    make_float2(m[kk].x > 0.f ? v0 : 0.f, m[kk].y > 0.f ? v1 : 0.f);
+            }
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -775,14 +808,26 @@ cudaError_t launch_conv1_tf32(const CUtensorMap* tmX, const void* w1pack, const 
                               int batch, int n1, int n2, int num_sms, cudaStream_t st) {
   Geo13 g = make_geo13(batch, n1, n2, R1T, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv1_tf32<<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack), bias,
-                                                           fullmap, g, h1);
+  k_conv1_tf32<false><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack),
+                                                                  bias, fullmap, g, h1, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const float* h2, float* dh2, int batch,
+                               int n1, int n2, int num_sms, cudaStream_t st) {
+  Geo13 g = make_geo13(batch, n1, n2, R1T, true);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  k_conv1_tf32<true><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmDX, reinterpret_cast<const uint8_t*>(wpack),
+                                                                 nullptr, 0, g, dh2, h2);
   return cudaGetLastError();
 }
 
 cudaError_t setup_conv13_tc(int n2) {
-  cudaError_t e0 = cudaFuncSetAttribute(k_conv1_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e0 = cudaFuncSetAttribute(k_conv1_tf32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)conv1_tf32_smem_bytes());
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(k_conv1_tf32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)conv1_tf32_smem_bytes());
   if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaFuncSetAttribute(k_conv1_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)conv1_tc_smem_bytes());
