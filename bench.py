@@ -90,14 +90,43 @@ _REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_pow
 
 
 class ClockSampler:
-    """Samples nvidia-smi every 200 ms while the timed region runs (B200_PROFILING.md clocks line)."""
+    """Samples SM clock, power and throttle reasons every ~5 ms while the timed region runs (NVML from a thread;
+    nvidia-smi -lms 200 as the fallback) -- the B200_PROFILING.md clocks line."""
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
+        self.rows = []          # (sm_mhz, max_mhz, power_w, [hw_slowdown, hw_thermal, sw_thermal, sw_power_cap])
         self.proc = None
         self.path = None
+        self.thread = None
+        self.stop = False
+
+    def _nvml_loop(self, nv, h):
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), pw, [bool(rs & bt) for bt in bits]))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            import threading
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            time.sleep(0.05)
+            return self
+        except Exception:
+            self.thread = None
         try:
             fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
             os.close(fd)
@@ -111,6 +140,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        if self.thread is not None:
+            self.stop = True
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -120,7 +152,7 @@ class ClockSampler:
             self.fh.close()
 
     def summary(self) -> dict:
-        rows = []
+        rows = list(self.rows)
         if self.path and os.path.exists(self.path):
             for line in open(self.path):
                 f = [x.strip() for x in line.split(",")]
@@ -128,17 +160,17 @@ class ClockSampler:
                     continue
                 try:
                     rows.append((float(f[1]), float(f[2]), float(f[3]) if f[3] not in ("", "[N/A]") else 0.0,
-                                 f[5:9]))
+                                 [v.lower().startswith("active") for v in f[5:9]]))
                 except ValueError:
                     continue
             os.unlink(self.path)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         load = [r for r in rows if r[2] > 300.0] or rows
-        reasons = sorted({_REASONS[i] for r in load for i, v in enumerate(r[3]) if v.lower().startswith("active")})
+        reasons = sorted({_REASONS[i] for r in load for i, v in enumerate(r[3]) if v})
         return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
                 "reasons": reasons, "samples": len(rows), "samples_under_load": len(load),
-                "power_w_max": max(r[2] for r in rows)}
+                "power_w_max": max(r[2] for r in rows), "sampler": "nvml" if self.rows else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------- workload
