@@ -87,3 +87,46 @@ def test_training_rejects_non_fp32_contexts():
     ctx = make_ctx(case)
     with pytest.raises(DiError):
         ctx.train_grad(torch.from_numpy(case.y).cuda().to(torch.bfloat16), torch.from_numpy(case.x).cuda())
+
+
+@pytest.mark.parametrize("final_relu,xcorr", [(True, False), (False, True)])
+def test_gradients_flags_tf32(final_relu, xcorr):
+    """The tensor-core backward honours the flags: FINAL_RELU masks dG3, XCORR changes the tap orientation of
+    every repacked bank (forward, dgrad2, dgrad3) and of the weight-gradient reduction."""
+    from paper_1701_03891_b200 import DI_FLAG_FINAL_RELU, DI_FLAG_XCORR
+    case = Case(24, 24, 128, 3, "tf32", 6, 3, bias="channel")
+    flags = (DI_FLAG_FINAL_RELU if final_relu else 0) | (DI_FLAG_XCORR if xcorr else 0)
+    _grads_ok(make_ctx(case, flags=flags), case, final_relu=final_relu, xcorr=xcorr)
+
+
+def test_gradients_paper_geometry_tf32():
+    """64x64 images (the paper config's geometry: 11 row blocks of 6 with a partial last block, full-width units)
+    on the tensor-core backward, 6 images."""
+    case = Case(64, 64, 1024, 6, "tf32", 8, 4, bias="channel")
+    _grads_ok(make_ctx(case), case)
+
+
+def test_gradients_column_segments_tf32():
+    """96-wide images: two column segments per row block, so the wgrad strips zero their halo columns in shared
+    memory (k_wgrad2_tc) and the thin-layer operands are cut at the segment edge (k_wgrad13_tc)."""
+    case = Case(20, 96, 400, 2, "tf32", 6, 3, bias="channel")
+    _grads_ok(make_ctx(case), case)
+
+
+@pytest.mark.parametrize("precision", ["f32", "tf32"])
+def test_gradients_are_deterministic(precision):
+    """Every reduction is two-level in a fixed order (no atomics): repeated calls give identical bits, and the
+    gradient of a batch is independent of the batch capacity of the context."""
+    import torch
+    case = Case(32, 32, 200, 5, precision, 6, 3, bias="channel")
+    y = torch.from_numpy(case.y).cuda()
+    x = torch.from_numpy(case.x).cuda()
+    a = make_ctx(case)
+    b = make_ctx(case, max_batch=16)
+    l1, g1 = a.train_grad(y, x, 0.2)
+    g1 = g1.clone()
+    l2, g2 = a.train_grad(y, x, 0.2)
+    l3, g3 = b.train_grad(y, x, 0.2)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2) and float(l1.item()) == float(l2.item())
+    assert torch.equal(g1, g3) and float(l1.item()) == float(l3.item())
