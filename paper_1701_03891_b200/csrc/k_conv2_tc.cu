@@ -133,7 +133,9 @@ __global__ void __launch_bounds__(256, 1)
           for (int kb = 0; kb < KBLOCKS; ++kb, ++wk, wsrc += WBYTES) {
             const uint32_t st = wk % WSTAGES;
             if (wk >= WSTAGES) mbar_wait(&wempty[st], ((wk / WSTAGES) - 1) & 1);
-#ifdef DI_EXP_HALFW
+#if defined(DI_EXP_NOW)
+            mbar_arrive(&wfull[st]);                          // experiment: no weight copies (wrong results)
+#elif defined(DI_EXP_HALFW)
             mbar_arrive_expect_tx(&wfull[st], WBYTES / 2);   // experiment: half the weight bytes (wrong results)
             bulk_load(wst + st * WBYTES, wsrc, WBYTES / 2, &wfull[st]);
 #else
