@@ -59,6 +59,11 @@ cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const fl
 size_t conv2_tf32_smem_bytes(int n2);
 int conv2_tf32_box_rows();
 cudaError_t setup_conv2_tf32(int n2);
+// generic TF32 layer C_in -> C_out, (C_in, C_out) in {32, 64}^2, bias + ReLU (deeper / wider stacks, NEXT-3);
+// wpack: convg_tf32_kblocks(cin, cout) blocks of 16 KB (api.cu conv_tf32_pack)
+int convg_tf32_kblocks(int cin, int cout);
+cudaError_t launch_convg_tf32(int cin, int cout, const CUtensorMap* tmIn, const void* wpack, const float* bias,
+                              int batch, int n1, int n2, float* out, int num_sms, cudaStream_t st);
 cudaError_t launch_conv2_tf32(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
                               int n1, int n2, float* h2, int num_sms, cudaStream_t st);
 cudaError_t launch_conv2_simt_f32(const float* h1, const float* wx, const float* bias, int fullmap, float* h2,
