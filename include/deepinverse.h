@@ -51,6 +51,15 @@ enum {
   DI_FLAG_FINAL_RELU = 1u << 2    /* ReLU after layer 3 (PAPER.md:118 read literally); default off       */
 };
 
+/* One layer of a custom stack ("DeepInverses with larger capacities"):
+ * an Eq. (1) layer with 11x11 taps, W [cout][cin][11][11] (orientation per DI_FLAG_XCORR), b [cout] per channel
+ * (NULL = zero).  ReLU after every layer but the last (the last one iff DI_FLAG_FINAL_RELU), as in Eq. (1). */
+typedef struct {
+  int cin, cout;
+  const float* w;
+  const float* b;
+} di_layer;
+
 /* Arguments of di_create.  All pointers are HOST pointers; di_create deep-copies them and the caller may
  * free them on return.  Weight layout [C_out][C_in][11][11] row-major fp32; biases fp32,
  * layout per DI_FLAG_FULLMAP_BIAS; a NULL bias pointer means zero biases.  In DI_PREC_BF16 mode Phi and
@@ -73,6 +82,14 @@ typedef struct {
   const float* lift;     /* optional learned lifting matrix L [n1*n2][m] row-major fp32: x_tilde = L y
                             ("one could learn the weights").  NULL: the
                             paper's fixed adjoint L = Phi^T.  Phi still defines di_measure.   */
+  int n_layers;          /* 0: the paper's three layers w1..b3.  >= 2: the custom stack `layers` (w1..b3 unused):
+                            layers[0].cin = 1, layers[n-1].cout = 1, layers[i].cin = layers[i-1].cout.  Supported
+                            (FP32 and TF32 contexts, per-channel biases): first layer 1 -> {32, 64}, interior
+                            layers {32, 64} -> {32, 64}, last layer 32 -> 1; TF32 also needs n2 % 4 == 0.
+                            Other shapes, BF16 or DI_FLAG_FULLMAP_BIAS: DI_ERR_ARG.  Custom stacks support
+                            di_recover / di_recover_host / di_recover_from_proxy / sensing / metrics; training and
+                            di_debug_stage stages >= 1 are for the paper's stack only (DI_ERR_ARG).            */
+  const di_layer* layers;
 } di_create_args;
 
 /* Create a context on args->device.  On failure *out is set to NULL and a status is returned. */

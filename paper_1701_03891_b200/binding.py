@@ -39,6 +39,10 @@ def _status_name(s: int) -> str:
     return names[s] if 0 <= s < len(names) else "?"
 
 
+class di_layer(ctypes.Structure):
+    _fields_ = [("cin", ctypes.c_int), ("cout", ctypes.c_int), ("w", ctypes.c_void_p), ("b", ctypes.c_void_p)]
+
+
 class di_create_args(ctypes.Structure):
     _fields_ = [("m", ctypes.c_int), ("n1", ctypes.c_int), ("n2", ctypes.c_int),
                 ("phi", ctypes.c_void_p), ("phi_dtype", ctypes.c_int),
@@ -46,7 +50,8 @@ class di_create_args(ctypes.Structure):
                 ("w2", ctypes.c_void_p), ("b2", ctypes.c_void_p),
                 ("w3", ctypes.c_void_p), ("b3", ctypes.c_void_p),
                 ("precision", ctypes.c_int), ("flags", ctypes.c_uint),
-                ("device", ctypes.c_int), ("max_batch", ctypes.c_int), ("lift", ctypes.c_void_p)]
+                ("device", ctypes.c_int), ("max_batch", ctypes.c_int), ("lift", ctypes.c_void_p),
+                ("n_layers", ctypes.c_int), ("layers", ctypes.c_void_p)]
 
 
 class di_info(ctypes.Structure):
@@ -200,7 +205,9 @@ def di_last_error() -> str:
 # ------------------------------------------------------------------ convenience owner object
 class DeepInverse:
     """Owns one di_ctx.  phi: [m][n1*n2] (fp32 numpy; bf16 configs pass bf16-representable values),
-    params: synth.Params-like (w: 3 arrays [C_out][C_in][11][11], b: per-channel or full-map biases)."""
+    params: synth.Params-like (w: arrays [C_out][C_in][11][11], b: per-channel or full-map biases).  The paper's
+    three layers (64, 32, 1) use w1..b3; any other stack (widths per include/deepinverse.h)
+    is passed as di_create_args.layers."""
 
     def __init__(self, phi: np.ndarray, params, n1: int, n2: int, precision: str = "bf16", flags: int = 0,
                  device: int = 0, max_batch: int = 1, lift: np.ndarray | None = None):
@@ -219,11 +226,23 @@ class DeepInverse:
         lift = None if lift is None else np.ascontiguousarray(lift, dtype=np.float32)
         if lift is not None and lift.shape != (phi.shape[1], phi.shape[0]):
             raise ValueError(f"lift must be [N][m] = {(phi.shape[1], phi.shape[0])}")
-        self._keep = (phi, ws, bs, lift)
-        a = di_create_args(self.m, n1, n2, phi.ctypes.data, DI_DTYPE_F32,
-                           ws[0].ctypes.data, _ptr(bs[0]), ws[1].ctypes.data, _ptr(bs[1]),
-                           ws[2].ctypes.data, _ptr(bs[2]), PRECISIONS[precision], flags, device, max_batch,
-                           _ptr(lift))
+        widths = tuple(w.shape[0] for w in ws)
+        self.custom = len(ws) != 3 or widths != (64, 32, 1)
+        if self.custom:
+            if len(bs) < len(ws):
+                bs = [None] * len(ws)
+            arr = (di_layer * len(ws))(*[di_layer(w.shape[1], w.shape[0], w.ctypes.data, _ptr(b))
+                                         for w, b in zip(ws, bs)])
+            self._keep = (phi, ws, bs, lift, arr)
+            a = di_create_args(self.m, n1, n2, phi.ctypes.data, DI_DTYPE_F32, None, None, None, None, None, None,
+                               PRECISIONS[precision], flags, device, max_batch, _ptr(lift), len(ws),
+                               ctypes.cast(arr, ctypes.c_void_p))
+        else:
+            self._keep = (phi, ws, bs, lift)
+            a = di_create_args(self.m, n1, n2, phi.ctypes.data, DI_DTYPE_F32,
+                               ws[0].ctypes.data, _ptr(bs[0]), ws[1].ctypes.data, _ptr(bs[1]),
+                               ws[2].ctypes.data, _ptr(bs[2]), PRECISIONS[precision], flags, device, max_batch,
+                               _ptr(lift), 0, None)
         self.ctx = di_create(a)
         self._keep = None
 

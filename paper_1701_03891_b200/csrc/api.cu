@@ -87,6 +87,15 @@ struct di_ctx_s {
   void* wp1 = nullptr;          // conv1 tensor-core weight blocks (BF16 mode, SWIZZLE_32B image)
   void* wp3 = nullptr;          // conv3 tensor-core weight blocks (BF16 mode, SWIZZLE_64B image)
   void* wp2t = nullptr;         // conv2 TF32 weight blocks (TF32 mode)
+  struct Layer {                // one layer of a custom stack
+    int cin = 0, cout = 0;
+    float* wx = nullptr;        // FP32: SIMT layout [ci][a][b][co]
+    void* wp = nullptr;         // TF32: tensor-core image (conv1 / generic / conv3 layout by position)
+    float* b = nullptr;
+    CUtensorMap tm;             // TF32: strip map over this layer's input activation
+  };
+  std::vector<Layer> stack;     // empty: the paper's three layers (w1..b3)
+  float* act[2] = {nullptr, nullptr};   // custom stack: ping-pong activations [max_batch][N][<= 64] fp32
   float* wp2d = nullptr;        // training, TF32 mode: layer-2 dgrad weight blocks (k_dgrad2_tf32)
   float* wpd3 = nullptr;        // training, TF32 mode: layer-3 dgrad bank in the conv1 TF32 layout
   bool has_tmDX = false;
@@ -190,12 +199,13 @@ di_status encode_xt(CUtensorMap* map, const void* xt, int batch, int n1, int n2,
 }
 
 // h2 [batch][n1][n2][32] for conv3: bf16 (box = all 32 channels = 64 B) or fp32 for TF32 (box = 16 channels = 64 B)
-// dG2 [batch][n1][n2][32] fp32 for the layer-2 dgrad strips (same box as the TF32 conv2 strip)
-di_status encode_dg2(CUtensorMap* map, const void* dg2, int batch, int n1, int n2) {
+// fp32 NHWC activations with `ch` channels (a multiple of 32) for the TF32 strips of k_conv_tf32 (32-channel box):
+// the layer-2 dgrad's dG2 and the interior layers of custom stacks
+di_status encode_act_f32(CUtensorMap* map, const void* dg2, int batch, int n1, int n2, int ch) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  cuuint64_t dims[4] = {32, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
-  cuuint64_t strides[3] = {32 * 4, (cuuint64_t)n2 * 32 * 4, (cuuint64_t)n1 * n2 * 32 * 4};
+  cuuint64_t dims[4] = {(cuuint64_t)ch, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)ch * 4, (cuuint64_t)n2 * ch * 4, (cuuint64_t)n1 * n2 * ch * 4};
   cuuint32_t box[4] = {32, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tf32_box_rows(), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(dg2), dims, strides, box, es,
@@ -380,6 +390,29 @@ std::vector<float> conv3_tf32_pack(const std::vector<float>& wx3) {
   return out;
 }
 
+// TF32 blocks of a generic C_in -> C_out layer (k_conv_tf32): block (h, u, j), index (h*11 + u)*J + j, J =
+// ceil(11 / TAPS), TAPS = 128 / C_out: row v'*C_out + k (tap TAPS j + v', zero past 10), 32 fp32 channels 32h + c,
+// SWIZZLE_128B (16-B chunk of 4 channels at row*128 + ((c/4 ^ (row & 7)) << 4)).  conv2_tf32_pack is the
+// (64, 32) case.
+std::vector<float> conv_tf32_pack(const std::vector<float>& wx, int cin, int cout) {
+  const int taps = 128 / cout, J = (K + taps - 1) / taps, nh = cin / 32;
+  std::vector<float> out((size_t)nh * K * J * 4096, 0.f);
+  uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
+  for (int h = 0; h < nh; ++h)
+    for (int u = 0; u < K; ++u)
+      for (int j = 0; j < J; ++j)
+        for (int row = 0; row < 128; ++row) {
+          const int v = taps * j + row / cout, k = row % cout;
+          for (int c = 0; c < 32; ++c) {
+            const float x = v < K ? wx[(((size_t)k * cin + 32 * h + c) * K + u) * K + v] : 0.f;
+            const size_t off = (size_t)((h * K + u) * J + j) * 16384 + row * 128 + ((((size_t)c / 4) ^ (row & 7)) << 4) +
+                               (c % 4) * 4;
+            std::memcpy(base + off, &x, 4);
+          }
+        }
+  return out;
+}
+
 // bias: per-channel [cout] or the window of the full map [cout][n1+10][n2+10] that S keeps, as [n1][n2][cout]
 di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n1, int n2, long long* ws) {
   *dst = nullptr;
@@ -395,6 +428,13 @@ di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n
 
 void free_ctx(di_ctx c) {
   if (!c) return;
+  for (auto& l : c->stack) {
+    if (l.wx) cudaFree(l.wx);
+    if (l.wp) cudaFree(l.wp);
+    if (l.b) cudaFree(l.b);
+  }
+  for (auto p : c->act)
+    if (p) cudaFree(p);
   void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->wpd3, c->h1b, c->dg2b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
                 c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->phi_sense, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
@@ -437,6 +477,42 @@ di_status run_proxy(di_ctx c, const void* y, long long ldy, int batch, void* xt,
   return DI_OK;
 }
 
+// custom stack: x_tilde -> layer 0 -> ... -> x_hat, interior activations ping-pong in act[]
+di_status run_stack(di_ctx c, int batch, void* xt, float* xhat, cudaStream_t st, int& launches) {
+  const int L = (int)c->stack.size();
+  const int relu_last = (c->flags & DI_FLAG_FINAL_RELU) ? 1 : 0;
+  const void* in = xt;
+  for (int i = 0; i < L; ++i) {
+    const di_ctx_s::Layer& l = c->stack[i];
+    float* out = i == L - 1 ? xhat : c->act[i & 1];
+    if (c->prec == DI_PREC_TF32) {
+      if (i == 0) {
+        CUtensorMap tm;
+        const CUtensorMap* tmp = &c->tmX;
+        if (xt != c->xt || batch != c->max_batch) {
+          di_status s = encode_xt(&tm, xt, batch, c->n1, c->n2, true);
+          if (s != DI_OK) return s;
+          tmp = &tm;
+        }
+        CUDA_TRY(di::launch_conv1g_tf32(l.cout, tmp, l.wp, l.b, out, batch, c->n1, c->n2, c->num_sms, st));
+      } else if (i == L - 1) {
+        CUDA_TRY(di::launch_conv3_tc(&l.tm, l.wp, l.b, 0, relu_last, xhat, batch, c->n1, c->n2, c->num_sms, true, st));
+      } else {
+        CUDA_TRY(di::launch_convg_tf32(l.cin, l.cout, &l.tm, l.wp, l.b, batch, c->n1, c->n2, out, c->num_sms, st));
+      }
+    } else {
+      if (i == L - 1)
+        CUDA_TRY(di::launch_conv3_simt(in, false, l.wx, l.b, 0, relu_last, xhat, batch, c->n1, c->n2, st));
+      else
+        CUDA_TRY(di::launch_convg_simt(l.cin, l.cout, reinterpret_cast<const float*>(in), l.wx, l.b, out, batch,
+                                       c->n1, c->n2, st));
+    }
+    ++launches;
+    in = out;
+  }
+  return DI_OK;
+}
+
 // the launch sequence (stages first..last) on caller buffers
 di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy, int batch, void* xt, void* h1,
                      void* h2, float* xhat, cudaStream_t st) {
@@ -462,6 +538,17 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
     if (s0 != DI_OK) return s0;
   }
   mark(1);
+  if (!c->stack.empty()) {   // custom stack: its layers are one block (stage 1), stages 2 and 3 empty
+    if (first <= 1 && 3 <= last) {
+      di_status s1 = run_stack(c, batch, xt, xhat, st, launches);
+      if (s1 != DI_OK) return s1;
+    } else if (last >= 1) {
+      return fail(DI_ERR_ARG, "custom stacks run stages 1..3 as one block");
+    }
+    mark(2), mark(3), mark(4);
+    c->last_launches = launches;
+    return DI_OK;
+  }
   if (first <= 1 && 1 <= last) {
     if (c->prec == DI_PREC_TF32 && c->has_tmX) {
       CUtensorMap tm;
@@ -564,7 +651,28 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   if (a->n1 < 1 || a->n2 < 1) return fail(DI_ERR_DOMAIN, "n1=%d n2=%d must be >= 1", a->n1, a->n2);
   const long long N = (long long)a->n1 * a->n2;
   if (a->m < 1 || a->m > N) return fail(DI_ERR_DOMAIN, "m=%d must satisfy 1 <= m <= N=%lld (SPEC.md:140)", a->m, N);
-  if (!a->phi || !a->w1 || !a->w2 || !a->w3) return fail(DI_ERR_ARG, "phi and w1..w3 must be non-NULL");
+  const bool custom = a->n_layers != 0;
+  if (!a->phi) return fail(DI_ERR_ARG, "phi must be non-NULL");
+  if (!custom && (!a->w1 || !a->w2 || !a->w3)) return fail(DI_ERR_ARG, "w1..w3 must be non-NULL");
+  if (custom) {   // SURVEY.md §8(f) NEXT-3 custom stacks: shapes the kernels implement
+    const int L = a->n_layers;
+    if (L < 2 || !a->layers) return fail(DI_ERR_ARG, "n_layers=%d: a custom stack needs >= 2 layers", L);
+    if (a->precision == DI_PREC_BF16) return fail(DI_ERR_ARG, "custom stacks run in FP32 or TF32 contexts");
+    if (a->flags & DI_FLAG_FULLMAP_BIAS) return fail(DI_ERR_ARG, "custom stacks take per-channel biases");
+    if (a->precision == DI_PREC_TF32 && a->n2 % 4 != 0) return fail(DI_ERR_ARG, "TF32 custom stacks need n2 %% 4 == 0");
+    for (int i = 0; i < L; ++i) {
+      const di_layer& l = a->layers[i];
+      if (!l.w) return fail(DI_ERR_ARG, "layers[%d].w is NULL", i);
+      if (i > 0 && l.cin != a->layers[i - 1].cout)
+        return fail(DI_ERR_DIM, "layers[%d].cin=%d != layers[%d].cout=%d", i, l.cin, i - 1, a->layers[i - 1].cout);
+      const bool w32_64 = (l.cout == 32 || l.cout == 64);
+      const bool ok = i == 0 ? (l.cin == 1 && w32_64) : i == L - 1 ? (l.cin == 32 && l.cout == 1)
+                                                                   : ((l.cin == 32 || l.cin == 64) && w32_64);
+      if (!ok)
+        return fail(DI_ERR_ARG, "layers[%d] %d -> %d unsupported (first 1 -> {32,64}, interior {32,64} -> {32,64}, "
+                    "last 32 -> 1)", i, l.cin, l.cout);
+    }
+  }
   if (a->phi_dtype != DI_DTYPE_F32 && a->phi_dtype != DI_DTYPE_BF16) return fail(DI_ERR_ARG, "bad phi_dtype");
   if (a->precision != DI_PREC_FP32 && a->precision != DI_PREC_TF32 && a->precision != DI_PREC_BF16)
     return fail(DI_ERR_ARG, "bad precision %d", (int)a->precision);
@@ -668,7 +776,32 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     }
   }
   // ---- weights / biases
-  {
+  if (custom) {   // the custom stack's banks in the layout of the kernel that runs each layer
+    const int L = a->n_layers;
+    c->stack.resize(L);
+    for (int i = 0; i < L; ++i) {
+      const di_layer& al = a->layers[i];
+      di_ctx_s::Layer& l = c->stack[i];
+      l.cin = al.cin, l.cout = al.cout;
+      auto wx = xcorr_taps(al.w, al.cout, al.cin, xc, false);
+      if (c->prec == DI_PREC_FP32) {
+        auto sl = simt_layout(wx, al.cout, al.cin);
+        STEP(upload(&l.wx, sl.data(), sl.size() * 4, &c->ws_bytes));
+      } else if (i == 0) {   // conv1 machinery: 64 bank rows, rows >= cout zero
+        std::vector<float> w64((size_t)64 * K * K, 0.f);
+        std::copy(wx.begin(), wx.end(), w64.begin());
+        auto pk = conv1_tf32_pack(w64);
+        STEP(upload(reinterpret_cast<float**>(&l.wp), pk.data(), pk.size() * 4, &c->ws_bytes));
+      } else if (i == L - 1) {
+        auto pk = conv3_tf32_pack(wx);
+        STEP(upload(reinterpret_cast<float**>(&l.wp), pk.data(), pk.size() * 4, &c->ws_bytes));
+      } else {
+        auto pk = conv_tf32_pack(wx, al.cin, al.cout);
+        STEP(upload(reinterpret_cast<float**>(&l.wp), pk.data(), pk.size() * 4, &c->ws_bytes));
+      }
+      STEP(upload_bias(&l.b, al.b, al.cout, false, a->n1, a->n2, &c->ws_bytes));
+    }
+  } else {
     auto w1 = xcorr_taps(a->w1, C1, 1, xc, bf16);
     auto w2 = xcorr_taps(a->w2, C2, C1, xc, bf16);
     auto w3 = xcorr_taps(a->w3, 1, C2, xc, bf16);
@@ -714,8 +847,14 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   {
     const size_t B = (size_t)a->max_batch;
     STEP(upload(&c->xt, nullptr, B * N * c->elt, &c->ws_bytes));
-    STEP(upload(&c->h1, nullptr, B * N * C1 * c->elt, &c->ws_bytes));
-    STEP(upload(&c->h2, nullptr, B * N * C2 * c->elt, &c->ws_bytes));
+    if (custom) {
+      int wmax = 0;
+      for (const auto& l : c->stack) wmax = std::max(wmax, l.cout);
+      for (auto& p : c->act) STEP(upload(&p, nullptr, B * N * wmax * 4, &c->ws_bytes));
+    } else {
+      STEP(upload(&c->h1, nullptr, B * N * C1 * c->elt, &c->ws_bytes));
+      STEP(upload(&c->h2, nullptr, B * N * C2 * c->elt, &c->ws_bytes));
+    }
     if (c->prec != DI_PREC_FP32) STEP(upload(&c->ystage, nullptr, B * c->kpad * c->elt, &c->ws_bytes));
   }
   // ---- kernels / tensor maps
@@ -725,13 +864,23 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       free_ctx(c);
       return fail(DI_ERR_CUDA, "setup_conv2_tf32: %s", cudaGetErrorString(e));
     }
-    STEP(encode_h1_f32(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
     e = di::setup_conv13_tc(a->n2);
     if (e != cudaSuccess) {
       free_ctx(c);
       return fail(DI_ERR_CUDA, "setup_conv13_tc: %s", cudaGetErrorString(e));
     }
-    STEP(encode_h2(&c->tmH2, c->h2, a->max_batch, a->n1, a->n2, true));
+    if (custom) {   // each layer's input strip map over the ping-pong buffer it reads
+      for (int i = 1; i < (int)c->stack.size(); ++i) {
+        di_ctx_s::Layer& l = c->stack[i];
+        if (i == (int)c->stack.size() - 1)
+          STEP(encode_h2(&l.tm, c->act[(i - 1) & 1], a->max_batch, a->n1, a->n2, true));
+        else
+          STEP(encode_act_f32(&l.tm, c->act[(i - 1) & 1], a->max_batch, a->n1, a->n2, l.cin));
+      }
+    } else {
+      STEP(encode_h1_f32(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
+      STEP(encode_h2(&c->tmH2, c->h2, a->max_batch, a->n1, a->n2, true));
+    }
     if (a->n2 % 4 == 0) {
       STEP(encode_xt(&c->tmX, c->xt, a->max_batch, a->n1, a->n2, true));
       c->has_tmX = true;
@@ -943,7 +1092,7 @@ static di_status train_alloc(di_ctx c) {
                                  c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2, c->b3, 0));
   if (c->prec == DI_PREC_TF32) {
     if ((s = al(&c->wp2d, (size_t)di::DG2_KBLOCKS * di::C2_KBLOCK_BYTES)) != DI_OK) return s;
-    if ((s = encode_dg2(&c->tmDG2, c->dh2, c->max_batch, c->n1, c->n2)) != DI_OK) return s;
+    if ((s = encode_act_f32(&c->tmDG2, c->dh2, c->max_batch, c->n1, c->n2, 32)) != DI_OK) return s;
     CUDA_TRY(di::setup_dgrad2_tf32(c->n2));
     if ((s = al(&c->h1b, B * N * C1 * 2)) != DI_OK) return s;
     if ((s = al(&c->dg2b, B * N * C2 * 2)) != DI_OK) return s;
@@ -969,6 +1118,7 @@ static di_status train_alloc(di_ctx c) {
 
 static di_status train_check(di_ctx c) {
   if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!c->stack.empty()) return fail(DI_ERR_ARG, "training is implemented for the paper's three-layer stack");
   if ((c->prec != DI_PREC_FP32 && c->prec != DI_PREC_TF32) || !c->params)
     return fail(DI_ERR_ARG, "training needs a DI_PREC_FP32 or DI_PREC_TF32 context with per-channel (or zero) biases");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
@@ -1115,6 +1265,7 @@ di_status di_debug_stage(di_ctx c, int stage, const void* in, void* out, int bat
   if (stage < 0 || stage > 3) return fail(DI_ERR_ARG, "stage=%d outside [0,3]", stage);
   if (!in || !out) return fail(DI_ERR_ARG, "NULL buffer");
   if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  if (stage > 0 && !c->stack.empty()) return fail(DI_ERR_ARG, "per-stage hooks are for the paper's stack");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (stage) {
     case 0: return run_stages(c, 0, 0, in, c->m, batch, out, nullptr, nullptr, nullptr, st);

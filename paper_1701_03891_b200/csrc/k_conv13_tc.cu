@@ -387,7 +387,8 @@ constexpr int XT_STRIDE = ((R1T + 10) * (P1MAX + 8) * 4 + 128 + 127) & ~127;
 //   dH2[p][ci] = [h2[p][ci] > 0] * sum_{u,v} wx3[0][ci][10-u][10-v] * dG3[p + (u-5, v-5)]
 // is a 1 -> 32 'same' correlation: the strip is dG3 (tmX over dG3), the packed filters are the rotated layer-3
 // taps in rows 0..31 (rows 32..63 zero), and the epilogue writes 32 channels masked by h2 instead of bias+ReLU.
-template <bool DG3>
+// COUT = 32 (bank rows 32..63 zero) or 64 output channels; DG3 = masked epilogue (no bias / ReLU).
+template <int COUT, bool DG3>
 __global__ void __launch_bounds__(384, 1)
     k_conv1_tf32(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ w1pack,
                  const float* __restrict__ bias, int fullmap, Geo13 g, float* __restrict__ h1,
@@ -499,7 +500,8 @@ __global__ void __launch_bounds__(384, 1)
     const int q = warp & 3, hh = (warp - 4) >> 2;
     const int i4 = lane >> 2, cpair = 2 * (lane & 3);
     const int ch = 16 * (2 * (q & 1) + hh) + 2 * i4;
-    const float b0 = (!fullmap && bias) ? bias[ch] : 0.f, b1 = (!fullmap && bias) ? bias[ch + 1] : 0.f;
+    const float b0 = (!fullmap && bias && ch < COUT) ? bias[ch] : 0.f;
+    const float b1 = (!fullmap && bias && ch < COUT) ? bias[ch + 1] : 0.f;
     const uint32_t wmagic = (1u << 20) / (uint32_t)W + 1;
     int ti = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const int pbase = n0 + (q >> 1) * half;
         const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32 + 16 * hh) << 16);
-        for (int c = 0; c < half && !(DG3 && ch >= 32); c += 32) {   // DG3: warps of rows >= 32 idle
+        for (int c = 0; c < half && ch < COUT; c += 32) {   // warps of bank rows >= COUT idle
           uint32_t r[16];
           tmem_ld_16x256b_x4(taddr + c, r);
           tmem_ld_wait();
@@ -565,11 +567,11 @@ __global__ void __launch_bounds__(384, 1)
               float v0 = __uint_as_float(r[4 * k + e]), v1 = __uint_as_float(r[4 * k + 2 + e]);
               if (fullmap && bias) {
                 const size_t pm = pix % ((size_t)g.n1 * g.n2);
-                v0 += bias[pm * 64 + ch], v1 += bias[pm * 64 + ch + 1];
+                v0 += bias[pm * COUT + ch], v1 += bias[pm * COUT + ch + 1];
               } else {
                 v0 += b0, v1 += b1;
               }
-              *reinterpret_cast<float2*>(h1 + pix * 64 + ch) = make_float2(fmaxf(v0, 0.f), fmaxf(v1, 0.f));
+              *reinterpret_cast<float2*>(h1 + pix * COUT + ch) = make_float2(fmaxf(v0, 0.f), fmaxf(v1, 0.f));
             }
         }
         tc_fence_before();
@@ -808,8 +810,19 @@ cudaError_t launch_conv1_tf32(const CUtensorMap* tmX, const void* w1pack, const 
                               int batch, int n1, int n2, int num_sms, cudaStream_t st) {
   Geo13 g = make_geo13(batch, n1, n2, R1T, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv1_tf32<false><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack),
-                                                                  bias, fullmap, g, h1, nullptr);
+  k_conv1_tf32<64, false><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack),
+                                                                      bias, fullmap, g, h1, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv1g_tf32(int cout, const CUtensorMap* tmX, const void* w1pack, const float* bias, float* out,
+                               int batch, int n1, int n2, int num_sms, cudaStream_t st) {
+  if (cout == 64) return launch_conv1_tf32(tmX, w1pack, bias, 0, out, batch, n1, n2, num_sms, st);
+  if (cout != 32) return cudaErrorInvalidValue;
+  Geo13 g = make_geo13(batch, n1, n2, R1T, true);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  k_conv1_tf32<32, false><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack),
+                                                                      bias, 0, g, out, nullptr);
   return cudaGetLastError();
 }
 
@@ -817,16 +830,19 @@ cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const
                                int n1, int n2, int num_sms, cudaStream_t st) {
   Geo13 g = make_geo13(batch, n1, n2, R1T, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv1_tf32<true><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmDX, reinterpret_cast<const uint8_t*>(wpack),
-                                                                 nullptr, 0, g, dh2, h2);
+  k_conv1_tf32<32, true><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmDX, reinterpret_cast<const uint8_t*>(wpack),
+                                                                     nullptr, 0, g, dh2, h2);
   return cudaGetLastError();
 }
 
 cudaError_t setup_conv13_tc(int n2) {
-  cudaError_t e0 = cudaFuncSetAttribute(k_conv1_tf32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e0 = cudaFuncSetAttribute(k_conv1_tf32<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)conv1_tf32_smem_bytes());
   if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(k_conv1_tf32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e0 = cudaFuncSetAttribute(k_conv1_tf32<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)conv1_tf32_smem_bytes());
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(k_conv1_tf32<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)conv1_tf32_smem_bytes());
   if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaFuncSetAttribute(k_conv1_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

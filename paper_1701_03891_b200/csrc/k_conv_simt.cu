@@ -169,6 +169,18 @@ cudaError_t launch_dgrad2_f32(const float* dh2, const float* wt2, const float* h
   return launch_wide<float, float, 32, 64, 16, 2>(dh2, wt2, nullptr, 0, 0, dh1, batch, n1, n2, st, h1);
 }
 
+// custom stacks: the same kernel for the other supported widths, bias + ReLU
+cudaError_t launch_convg_simt(int cin, int cout, const float* in, const float* wx, const float* bias, float* out,
+                              int batch, int n1, int n2, cudaStream_t st) {
+  if (cin == 1 && cout == 32) return launch_wide<float, float, 1, 32, 8, 1>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  if (cin == 1 && cout == 64) return launch_wide<float, float, 1, 64, 16, 1>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  if (cin == 32 && cout == 32) return launch_wide<float, float, 32, 32, 8, 2>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  if (cin == 32 && cout == 64) return launch_wide<float, float, 32, 64, 16, 2>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  if (cin == 64 && cout == 32) return launch_wide<float, float, 64, 32, 8, 2>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  if (cin == 64 && cout == 64) return launch_wide<float, float, 64, 64, 16, 2>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_conv2_simt_f32(const float* h1, const float* wx, const float* bias, int fullmap, float* h2,
                                   int batch, int n1, int n2, cudaStream_t st) {
   return launch_wide<float, float, 64, 32, 8, 2>(h1, wx, bias, fullmap, 1, h2, batch, n1, n2, st);

@@ -110,6 +110,12 @@ cudaError_t launch_dgrad2_tf32(const CUtensorMap* tmDG, const void* wpack, const
 constexpr int DG2_KBLOCKS = 66;
 // training, TF32 contexts: layer-3 data gradient as a 1 -> 32 TF32 conv on the conv1 machinery (k_conv13_tc.cu);
 // tmDX: the conv1 x_tilde tensor map over dG3; wpack: 11 x 4096 B (conv1 TF32 layout)
+// custom stacks (NEXT-3): first layer 1 -> cout (32 or 64) in TF32 on the conv1 machinery (bank rows >= cout zero)
+cudaError_t launch_conv1g_tf32(int cout, const CUtensorMap* tmX, const void* w1pack, const float* bias, float* out,
+                               int batch, int n1, int n2, int num_sms, cudaStream_t st);
+// custom stacks, FP32 SIMT: (cin, cout) in {(1,32), (1,64), (32,32), (32,64), (64,32), (64,64)}, bias + ReLU
+cudaError_t launch_convg_simt(int cin, int cout, const float* in, const float* wx, const float* bias, float* out,
+                              int batch, int n1, int n2, cudaStream_t st);
 cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const float* h2, float* dh2, int batch,
                                int n1, int n2, int num_sms, cudaStream_t st);
 // training, TF32 contexts: layer-2 weight gradient on tcgen05 from bf16 copies of h1 / dG2 (k_wgrad2_tc.cu)

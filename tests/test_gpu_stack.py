@@ -1,0 +1,85 @@
+"""Custom layer stacks ("DeepInverses with larger capacities"): deeper and
+wider stacks of Eq. (1) layers through di_create_args.layers, against the fp64 oracle's forward pass over the same
+layer list (oracle.forward takes any stack).  FP32 runs the SIMT kernels, TF32 the tensor-core kernels (first layer
+on the conv1 machinery, interior layers on k_conv_tf32<C_in, C_out>, last layer on the conv3 kernel)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_helpers import TOL_REL_L2, Case, compare
+
+pytestmark = pytest.mark.gpu
+
+
+def stack_params(widths, seed=5, bias=True):
+    """He-normal taps (reading Q9) and U[-0.1, 0.1] per-channel biases for the layer widths."""
+    r = np.random.default_rng(seed)
+    ws, bs = [], []
+    for cin, cout in zip(widths[:-1], widths[1:]):
+        ws.append((r.standard_normal((cout, cin, 11, 11)) * np.sqrt(2.0 / (cin * 121))).astype(np.float32))
+        bs.append(r.uniform(-0.1, 0.1, cout).astype(np.float32) if bias else np.zeros(cout, np.float32))
+    return synth.Params(ws, bs)
+
+
+def run_stack(widths, precision, n1, n2, m, batch, flags=0, final_relu=False):
+    import torch
+    from paper_1701_03891_b200 import DeepInverse
+    case = Case(n1, n2, m, batch, precision, 6, 3, params=stack_params(widths))
+    ctx = DeepInverse(case.phi, case.params, n1, n2, precision, flags=flags, max_batch=batch)
+    assert ctx.custom
+    out = ctx.recover(torch.from_numpy(case.y).cuda()).cpu().numpy()
+    ref = oracle.forward(case.y, case.phi, case.params, n1, n2, final_relu=final_relu)
+    ctx.close()
+    return compare(out, ref, case.x, precision)
+
+
+@pytest.mark.parametrize("precision", ["f32", "tf32"])
+@pytest.mark.parametrize("widths", [(1, 64, 64, 32, 1), (1, 32, 32, 32, 32, 1), (1, 32, 64, 32, 1), (1, 32, 1)])
+def test_stack_matches_oracle(precision, widths):
+    rel, dps, _ = run_stack(widths, precision, 32, 32, 200, 3)
+    assert rel <= TOL_REL_L2[precision], (widths, rel)
+
+
+def test_stack_column_segments_and_ragged_rows_tf32():
+    """72-wide, 40-row images: two column segments per row block and a partial last row block in every layer."""
+    rel, _, _ = run_stack((1, 64, 64, 32, 1), "tf32", 40, 72, 300, 2)
+    assert rel <= TOL_REL_L2["tf32"], rel
+
+
+def test_stack_final_relu_f32():
+    from paper_1701_03891_b200 import DI_FLAG_FINAL_RELU
+    rel, _, _ = run_stack((1, 32, 32, 1), "f32", 24, 24, 100, 2, flags=DI_FLAG_FINAL_RELU, final_relu=True)
+    assert rel <= TOL_REL_L2["f32"], rel
+
+
+def test_stack_batch_invariance_tf32():
+    """Image i of a batch equals the same image recovered alone (every kernel is per-image independent)."""
+    import torch
+    from paper_1701_03891_b200 import DeepInverse
+    case = Case(32, 32, 200, 4, "tf32", 6, 3, params=stack_params((1, 64, 64, 32, 1)))
+    ctx = DeepInverse(case.phi, case.params, 32, 32, "tf32", max_batch=4)
+    y = torch.from_numpy(case.y).cuda()
+    full = ctx.recover(y).cpu().numpy()
+    one = ctx.recover(y[2:3].contiguous()).cpu().numpy()
+    assert np.array_equal(full[2], one[0])
+    ctx.close()
+
+
+@pytest.mark.parametrize("widths,precision", [((1, 16, 1), "tf32"), ((1, 64, 128, 1), "f32"), ((1, 64, 1), "tf32"),
+                                               ((1, 32, 32, 1), "bf16")])
+def test_stack_unsupported_shapes_are_rejected(widths, precision):
+    from paper_1701_03891_b200 import DeepInverse, DiError
+    case = Case(16, 16, 64, 1, "f32", params=stack_params(widths))
+    with pytest.raises(DiError):
+        DeepInverse(case.phi, case.params, 16, 16, precision, max_batch=1)
+
+
+def test_stack_training_is_rejected():
+    import torch
+    from paper_1701_03891_b200 import DeepInverse, DiError
+    case = Case(16, 16, 64, 2, "f32", params=stack_params((1, 32, 32, 1)))
+    ctx = DeepInverse(case.phi, case.params, 16, 16, "f32", max_batch=2)
+    with pytest.raises(DiError):
+        ctx.train_grad(torch.from_numpy(case.y).cuda(), torch.from_numpy(case.x).cuda())
+    ctx.close()
