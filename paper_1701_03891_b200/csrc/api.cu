@@ -98,6 +98,8 @@ struct di_ctx_s {
   float* act[2] = {nullptr, nullptr};   // custom stack: ping-pong activations [max_batch][N][<= 64] fp32
   float* wp2d = nullptr;        // training, TF32 mode: layer-2 dgrad weight blocks (k_dgrad2_tf32)
   float* wpd3 = nullptr;        // training, TF32 mode: layer-3 dgrad bank in the conv1 TF32 layout
+  void* wp2db = nullptr;        // training, TF32 mode: layer-2 dgrad bf16 weight blocks (66 x 8 KB)
+  CUtensorMap tmDG2s;           // training, TF32 mode: bf16 dG2 strips for the bf16 dgrad2 (box rows R + 10)
   bool has_tmDX = false;
   CUtensorMap tmDX;             // training, TF32 mode: dG3 strips (the conv1 x_tilde map over dxh)
   CUtensorMap tmDG2;            // training, TF32 mode: dG2 strips (fp32, 32 channels)
@@ -227,6 +229,21 @@ di_status encode_wg2(CUtensorMap* map, const void* p, int batch, int n1, int n2,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, ch == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (wgrad2 operand) failed: %d", (int)r);
+  return DI_OK;
+}
+
+// dG2 [batch][n1][n2][32] bf16 as the strip of the bf16 layer-2 dgrad: box 32 ch x P x (R + 10) rows, SWIZZLE_64B
+di_status encode_dg2b_strip(CUtensorMap* map, const void* p, int batch, int n1, int n2) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {32, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {32 * 2, (cuuint64_t)n2 * 32 * 2, (cuuint64_t)n1 * n2 * 32 * 2};
+  cuuint32_t box[4] = {32, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tf32_box_rows(), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(p), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (dG2 bf16 strip) failed: %d", (int)r);
   return DI_OK;
 }
 
@@ -435,7 +452,7 @@ void free_ctx(di_ctx c) {
   }
   for (auto p : c->act)
     if (p) cudaFree(p);
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->wpd3, c->h1b, c->dg2b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->wpd3, c->wp2db, c->h1b, c->dg2b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
                 c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->phi_sense, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
@@ -1112,8 +1129,6 @@ static di_status train_alloc(di_ctx c) {
   CUDA_TRY(di::launch_sgd_repack(c->params, nullptr, c->vel, di::N_PARAMS, 0.f, 0.f, !(c->flags & DI_FLAG_XCORR),
                                  c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2, c->b3, 0));
   if (c->prec == DI_PREC_TF32) {
-    if ((s = al(&c->wp2d, (size_t)di::DG2_KBLOCKS * di::C2_KBLOCK_BYTES)) != DI_OK) return s;
-    if ((s = encode_act_f32(&c->tmDG2, c->dh2, c->max_batch, c->n1, c->n2, 32)) != DI_OK) return s;
     CUDA_TRY(di::setup_dgrad2_tf32(c->n2));
     if ((s = al(&c->h1b, B * N * C1 * 2)) != DI_OK) return s;
     if ((s = al(&c->dg2b, B * N * C2 * 2)) != DI_OK) return s;
@@ -1125,13 +1140,15 @@ static di_status train_alloc(di_ctx c) {
       return s;
     CUDA_TRY(di::setup_wgrad2_tc(c->n2));
     CUDA_TRY(di::setup_wgrad13_tc(c->n2));
+    if ((s = al(reinterpret_cast<uint8_t**>(&c->wp2db), (size_t)di::DG2_KBLOCKS * 8192)) != DI_OK) return s;
+    if ((s = encode_dg2b_strip(&c->tmDG2s, c->dg2b, c->max_batch, c->n1, c->n2)) != DI_OK) return s;
     if (c->n2 % 4 == 0) {   // the conv1 TF32 strip map over dG3 (16-B row stride)
       if ((s = al(&c->wpd3, (size_t)11 * 4096)) != DI_OK) return s;
       if ((s = encode_xt(&c->tmDX, c->dxh, c->max_batch, c->n1, c->n2, true)) != DI_OK) return s;
       c->has_tmDX = true;
     }
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
-                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d, c->wpd3, 0));
+                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d, c->wpd3, c->wp2db, 0));
   }
   CUDA_TRY(cudaDeviceSynchronize());
   return DI_OK;
@@ -1194,8 +1211,8 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
     CUDA_TRY(di::launch_wgrad(2, h1, c->dh2, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w, gb + C1,
                               st));
   }
-  if (c->prec == DI_PREC_TF32)
-    CUDA_TRY(di::launch_dgrad2_tf32(&c->tmDG2, c->wp2d, h1, batch, c->n1, c->n2, c->dh1, c->num_sms, st));
+  if (c->prec == DI_PREC_TF32)   // bf16 operands from the dG2 copy made for wgrad2: twice the TF32 MMA rate
+    CUDA_TRY(di::launch_dgrad2_bf16(&c->tmDG2s, c->wp2db, h1, batch, c->n1, c->n2, c->dh1, c->num_sms, st));
   else
     CUDA_TRY(di::launch_dgrad2_f32(c->dh2, c->wt2, h1, c->dh1, batch, c->n1, c->n2, st));
   if (tc)
@@ -1217,7 +1234,7 @@ di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, 
   if (c->prec == DI_PREC_TF32)
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
                                     reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d,
-                                    c->wpd3, reinterpret_cast<cudaStream_t>(stream)));
+                                    c->wpd3, c->wp2db, reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }
 

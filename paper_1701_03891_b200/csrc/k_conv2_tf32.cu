@@ -47,7 +47,9 @@ enum { EPI_BIAS_RELU = 0, EPI_MASK = 1 };
 
 // MODE EPI_BIAS_RELU: out = ReLU(conv + bias) (per-channel bias, or full-map bias [n1*n2][C_out] when fullmap);
 // MODE EPI_MASK:      out = [mask > 0] * conv (the ReLU' of the layer whose gradient this is)
-template <int CIN, int COUT, int MODE>
+// BF = true: bf16 operands (kind::f16, K = 16 per MMA) -- the training step's layer-2 data gradient: a strip row is
+// the C_in bf16 channels (64 B for C_in = 32, SWIZZLE_64B), one K-block = the whole row (2 MMAs), 8-KB weight blocks.
+template <int CIN, int COUT, int MODE, bool BF = false>
 __global__ void __launch_bounds__(384, 1)
     k_conv_tf32(const __grid_constant__ CUtensorMap tmIn, const float* __restrict__ wpack,
                 const float* __restrict__ bias, int fullmap, const float* __restrict__ mask, GeoT g,
@@ -55,16 +57,21 @@ __global__ void __launch_bounds__(384, 1)
   constexpr int TAPS = 128 / COUT;            // column taps stacked in M
   constexpr int J = (11 + TAPS - 1) / TAPS;   // column-tap groups per tap row
   constexpr int KBH = 11 * J;                 // K-blocks per channel half
-  constexpr int NH = CIN / 32;                // channel halves
+  constexpr int BOXC = BF ? (CIN < 64 ? CIN : 64) : 32;   // channels per strip row (one 64/128-B swizzle row)
+  constexpr int RB = BOXC * (BF ? 2 : 4);     // strip / weight row bytes
+  constexpr int NH = CIN / BOXC;              // channel halves
+  constexpr int KMMA = RB / 32;               // MMAs per K-block (32 B of K each)
+  constexpr uint32_t WB = 128 * RB;           // weight block bytes
+  constexpr uint32_t SWZ = RB == 128 ? kSwizzle128B : kSwizzle64B;
   constexpr int QPT = COUT / 32;              // TMEM lane quadrants per tap
   constexpr int CPT = COUT / 8;               // channels per epilogue thread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int strip_bytes = (R + 10) * g.P * 128;
-  const int strip_alloc = (strip_bytes + GUARD_ROWS * 128 + 1023) & ~1023;
+  const int strip_bytes = (R + 10) * g.P * RB;
+  const int strip_alloc = (strip_bytes + GUARD_ROWS * RB + 1023) & ~1023;
   uint8_t* strip = smem;
   uint8_t* wst = smem + strip_alloc;
-  float* sP = reinterpret_cast<float*>(wst + WSTAGES * WBYTES);
+  float* sP = reinterpret_cast<float*>(wst + WSTAGES * WB);
 
   __shared__ uint64_t sfull, sempty, wfull[WSTAGES], wempty[WSTAGES], tfull, tempty;
   __shared__ uint32_t tslot;
@@ -77,7 +84,7 @@ __global__ void __launch_bounds__(384, 1)
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
-  for (int i = threadIdx.x; i < GUARD_ROWS * 128 / 16; i += blockDim.x)
+  for (int i = threadIdx.x; i < GUARD_ROWS * RB / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(strip + strip_bytes)[i] = make_uint4(0, 0, 0, 0);
   fence_async_smem();
   tc_fence_before();
@@ -95,22 +102,22 @@ __global__ void __launch_bounds__(384, 1)
         for (int h = 0; h < NH; ++h, ++sk) {
           if (sk > 0) mbar_wait(&sempty, (sk - 1) & 1);
           mbar_arrive_expect_tx(&sfull, strip_bytes);
-          tma_load_4d(strip, &tmIn, &sfull, 32 * h, c0 - 5, r0 - 5, b);
-          const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack) + (size_t)h * KBH * WBYTES;
-          for (int kb = 0; kb < KBH; ++kb, ++wk, wsrc += WBYTES) {
+          tma_load_4d(strip, &tmIn, &sfull, BOXC * h, c0 - 5, r0 - 5, b);
+          const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack) + (size_t)h * KBH * WB;
+          for (int kb = 0; kb < KBH; ++kb, ++wk, wsrc += WB) {
             const uint32_t st = wk % WSTAGES;
             if (wk >= WSTAGES) mbar_wait(&wempty[st], ((wk / WSTAGES) - 1) & 1);
-            mbar_arrive_expect_tx(&wfull[st], WBYTES);
-            bulk_load(wst + st * WBYTES, wsrc, WBYTES, &wfull[st]);
+            mbar_arrive_expect_tx(&wfull[st], WB);
+            bulk_load(wst + st * WB, wsrc, WB, &wfull[st]);
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      const uint64_t bdesc0 = smem_desc(smem_u32(strip), 16, 1024, kSwizzle128B);
-      const uint64_t adesc0 = smem_desc(smem_u32(wst), 16, 1024, kSwizzle128B);
-      const uint64_t pstep = (uint64_t)g.P * 8;
+      const uint64_t bdesc0 = smem_desc(smem_u32(strip), 16, 8 * RB, SWZ);
+      const uint64_t adesc0 = smem_desc(smem_u32(wst), 16, 8 * RB, SWZ);
+      const uint64_t pstep = (uint64_t)g.P * (RB >> 4);
       uint32_t wk = 0, sk = 0;
       int it = 0;
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
@@ -121,7 +128,7 @@ __global__ void __launch_bounds__(384, 1)
         const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;   // 1 or 2
         const int nB = ntiles > 1 ? min(NT, (min(OUT_PER_TILE, L - OUT_PER_TILE) + TAPS - 1 + 15) & ~15) : 0;
         const int nA = min(NT, (min(OUT_PER_TILE, L) + TAPS - 1 + 15) & ~15);
-        const uint32_t idA = idesc_f32acc(2, 128, nA), idB = idesc_f32acc(2, 128, nB > 0 ? nB : 16);
+        const uint32_t idA = idesc_f32acc(BF ? 1 : 2, 128, nA), idB = idesc_f32acc(BF ? 1 : 2, 128, nB > 0 ? nB : 16);
         if (it > 0) mbar_wait(&tempty, (it - 1) & 1);   // the epilogue drained the previous unit
         tc_fence_after();
         for (int h = 0; h < NH; ++h, ++sk) {
@@ -134,19 +141,25 @@ __global__ void __launch_bounds__(384, 1)
               const uint32_t st = wk % WSTAGES;
               mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
               tc_fence_after();
-              const uint64_t ad = adesc0 + (uint64_t)(st * (WBYTES >> 4));
-              const uint64_t b = bd + (uint64_t)(8 * TAPS * j);   // v0 = TAPS j positions x 128 B >> 4
+              const uint64_t ad = adesc0 + (uint64_t)(st * (WB >> 4));
+              const uint64_t b = bd + (uint64_t)(TAPS * j * (RB >> 4));   // v0 = TAPS j positions
               const uint32_t acc0 = (h | uu | j) != 0;
-              umma_tf32_ss(tmem, ad, b, idA, acc0);
-              umma_tf32_ss(tmem, ad + 2, b + 2, idA, 1);
-              umma_tf32_ss(tmem, ad + 4, b + 4, idA, 1);
-              umma_tf32_ss(tmem, ad + 6, b + 6, idA, 1);
+#pragma unroll
+              for (int kk = 0; kk < KMMA; ++kk) {
+                if (BF)
+                  umma_f16_ss(tmem, ad + 2 * kk, b + 2 * kk, idA, kk ? 1u : acc0);
+                else
+                  umma_tf32_ss(tmem, ad + 2 * kk, b + 2 * kk, idA, kk ? 1u : acc0);
+              }
               if (nB > 0) {
-                const uint64_t bb = b + (uint64_t)(OUT_PER_TILE * 8);
-                umma_tf32_ss(tmem + 256, ad, bb, idB, acc0);
-                umma_tf32_ss(tmem + 256, ad + 2, bb + 2, idB, 1);
-                umma_tf32_ss(tmem + 256, ad + 4, bb + 4, idB, 1);
-                umma_tf32_ss(tmem + 256, ad + 6, bb + 6, idB, 1);
+                const uint64_t bb = b + (uint64_t)(OUT_PER_TILE * (RB >> 4));
+#pragma unroll
+                for (int kk = 0; kk < KMMA; ++kk) {
+                  if (BF)
+                    umma_f16_ss(tmem + 256, ad + 2 * kk, bb + 2 * kk, idB, kk ? 1u : acc0);
+                  else
+                    umma_tf32_ss(tmem + 256, ad + 2 * kk, bb + 2 * kk, idB, kk ? 1u : acc0);
+                }
               }
               umma_commit(&wempty[st]);
             }
@@ -268,7 +281,23 @@ cudaError_t setup_conv2_tf32(int n2) {
   return set_smem<64, 64, EPI_BIAS_RELU>(n2);
 }
 
-cudaError_t setup_dgrad2_tf32(int n2) { return set_smem<32, 64, EPI_MASK>(n2); }
+cudaError_t setup_dgrad2_tf32(int n2) {
+  cudaError_t e = set_smem<32, 64, EPI_MASK>(n2);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_conv_tf32<32, 64, EPI_MASK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)conv2_tf32_smem_bytes(n2));
+}
+
+// training: layer-2 data gradient from the bf16 copy of dG2 (tmDGb: [B][n1][n2][32] bf16, box 32 ch x P x (R + 10)
+// rows, SWIZZLE_64B) with bf16 weight blocks (66 x 8 KB) -- twice the MMA rate of the TF32 form
+cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const float* h1, int batch, int n1, int n2,
+                               float* dh1, int num_sms, cudaStream_t st) {
+  GeoT g = make_geo_t(batch, n1, n2);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  k_conv_tf32<32, 64, EPI_MASK, true><<<grid, 384, conv2_tf32_smem_bytes(n2), st>>>(
+      *tmDGb, reinterpret_cast<const float*>(wpack), nullptr, 0, h1, g, dh1);
+  return cudaGetLastError();
+}
 
 template <int CIN, int COUT, int MODE>
 static cudaError_t launch(const CUtensorMap* tm, const void* wpack, const float* bias, int fullmap, const float* mask,

@@ -10,6 +10,7 @@
 //                        flipped weights and the previous activation as mask: k_conv_simt.cu)
 // Reductions over pixels are two-level and deterministic: fp32 per block over its pixel tiles, then fp64 over
 // blocks in a fixed order (k_wgrad_reduce).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -266,13 +267,24 @@ __device__ __forceinline__ float wx_at(const float* __restrict__ W, int cin, int
 
 __global__ void k_repack_tf32(const float* __restrict__ params, int flip, float* __restrict__ wp1,
                               float* __restrict__ wp2t, float* __restrict__ wp3, float* __restrict__ wp2d,
-                              float* __restrict__ wpd3) {
+                              float* __restrict__ wpd3, uint16_t* __restrict__ wp2db) {
   constexpr int T = KS * KS, N1 = 64 * T, N2 = 32 * 64 * T;
   const float* W1 = params;
   const float* W2 = params + N1;
   const float* W3 = params + N1 + N2;
   constexpr int E2 = 2 * 33 * 4096, E1 = 11 * 1024, E3 = 22 * 512, E4 = DG2_KBLOCKS * 4096, E5 = 11 * 1024;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E2 + E1 + E3 + E4 + E5; e += gridDim.x * blockDim.x) {
+  constexpr int E6 = DG2_KBLOCKS * 4096;   // bf16 layer-2 dgrad blocks: 66 x (128 rows x 32 co x 2 B), SWIZZLE_64B
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E2 + E1 + E3 + E4 + E5 + E6; e += gridDim.x * blockDim.x) {
+    if (e >= E2 + E1 + E3 + E4 + E5) {
+      if (!wp2db) continue;
+      const int i = e - E2 - E1 - E3 - E4 - E5;
+      const int blk = i / 4096, u = blk / 6, j = blk % 6, o = (i % 4096) * 2, row = o / 64, r = o % 64;
+      const int co = (((r / 16) ^ ((row >> 1) & 3)) * 8) + (r % 16) / 2;
+      const int bb = 2 * j + row / 64, ci = row % 64;
+      const float v = bb < KS ? wx_at(W2, 64, co, ci, KS - 1 - u, KS - 1 - bb, flip) : 0.f;
+      wp2db[i] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+      continue;
+    }
     if (e < E2) {                     // conv2: [h][kb] blocks of 128 rows x 32 ch, SWIZZLE_128B
       const int blk = e / 4096, o = (e % 4096) * 4, row = o / 128, r = o % 128;
       const int c = (((r / 16) ^ (row & 7)) * 4) + (r % 16) / 4;
@@ -305,8 +317,8 @@ __global__ void k_repack_tf32(const float* __restrict__ params, int flip, float*
 }
 
 cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wp2d,
-                               float* wpd3, cudaStream_t st) {
-  k_repack_tf32<<<592, 256, 0, st>>>(params, flip, wp1, wp2t, wp3, wp2d, wpd3);
+                               float* wpd3, void* wp2db, cudaStream_t st) {
+  k_repack_tf32<<<592, 256, 0, st>>>(params, flip, wp1, wp2t, wp3, wp2d, wpd3, reinterpret_cast<uint16_t*>(wp2db));
   return cudaGetLastError();
 }
 

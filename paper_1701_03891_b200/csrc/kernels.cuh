@@ -102,7 +102,9 @@ cudaError_t launch_dgrad2_f32(const float* dh2, const float* wt2, const float* h
 cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, int n1, int n2, float* part_w,
                          float* part_b, int flip, float* gw, float* gb, cudaStream_t st);
 cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wp2d,
-                               float* wpd3, cudaStream_t st);
+                               float* wpd3, void* wp2db, cudaStream_t st);
+cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const float* h1, int batch, int n1, int n2,
+                               float* dh1, int num_sms, cudaStream_t st);
 // training, TF32 contexts: layer-2 data gradient on tcgen05 (k_conv2_tf32.cu); wpack = 66 blocks of 16 KB
 cudaError_t setup_dgrad2_tf32(int n2);
 cudaError_t launch_dgrad2_tf32(const CUtensorMap* tmDG, const void* wpack, const float* h1, int batch, int n1, int n2,
