@@ -104,6 +104,7 @@ struct di_ctx_s {
   CUtensorMap tmDX;             // training, TF32 mode: dG3 strips (the conv1 x_tilde map over dxh)
   CUtensorMap tmDG2;            // training, TF32 mode: dG2 strips (fp32, 32 channels)
   void *h1b = nullptr, *dg2b = nullptr;   // training, TF32 mode: bf16 copies of h1 / dG2 (layer-2 wgrad operands)
+  void* dh1b = nullptr;                   // training, TF32 mode: dH1 in bf16 (bf16 dgrad2 -> wgrad1)
   float* part_w2 = nullptr;     // training, TF32 mode: per-CTA layer-2 wgrad partials
   CUtensorMap tmH1b, tmDG2b;
   // training (FP32 contexts with per-channel biases): parameters in the API orientation, momentum, backward
@@ -452,7 +453,7 @@ void free_ctx(di_ctx c) {
   }
   for (auto p : c->act)
     if (p) cudaFree(p);
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->wpd3, c->wp2db, c->h1b, c->dg2b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->wpd3, c->wp2db, c->h1b, c->dg2b, c->dh1b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
                 c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->phi_sense, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
@@ -1132,6 +1133,7 @@ static di_status train_alloc(di_ctx c) {
     CUDA_TRY(di::setup_dgrad2_tf32(c->n2));
     if ((s = al(&c->h1b, B * N * C1 * 2)) != DI_OK) return s;
     if ((s = al(&c->dg2b, B * N * C2 * 2)) != DI_OK) return s;
+    if ((s = al(&c->dh1b, B * N * C1 * 2)) != DI_OK) return s;
     if ((s = al(&c->part_w2, std::max(di::wgrad2_tc_part_floats(c->num_sms), di::wgrad13_tc_part_floats(c->num_sms)) * 4)) != DI_OK)
       return s;
     if ((s = encode_wg2(&c->tmH1b, c->h1b, c->max_batch, c->n1, c->n2, 64, di::wgrad2_tc_h_box_rows())) != DI_OK)
@@ -1212,11 +1214,11 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
                               st));
   }
   if (c->prec == DI_PREC_TF32)   // bf16 operands from the dG2 copy made for wgrad2: twice the TF32 MMA rate
-    CUDA_TRY(di::launch_dgrad2_bf16(&c->tmDG2s, c->wp2db, h1, batch, c->n1, c->n2, c->dh1, c->num_sms, st));
+    CUDA_TRY(di::launch_dgrad2_bf16(&c->tmDG2s, c->wp2db, c->h1b, batch, c->n1, c->n2, c->dh1b, c->num_sms, st));
   else
     CUDA_TRY(di::launch_dgrad2_f32(c->dh2, c->wt2, h1, c->dh1, batch, c->n1, c->n2, st));
   if (tc)
-    CUDA_TRY(di::launch_wgrad1_tc(xt, c->dh1, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads, gb,
+    CUDA_TRY(di::launch_wgrad1_tc(xt, c->dh1b, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads, gb,
                                   c->num_sms, st));
   else
     CUDA_TRY(di::launch_wgrad(1, xt, c->dh1, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads, gb, st));

@@ -218,6 +218,16 @@ __global__ void __launch_bounds__(384, 1)
                       *reinterpret_cast<const float4*>(sPg + (tp * QPT + cblk) * (ECH * SPS) + jj * SPS + cl + 4 * v4);
                   sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
                 }
+                if (MODE == EPI_MASK && BF) {   // bf16 in / out: the ReLU' mask from bf16 h1, bf16 dh1 for wgrad1
+                  const size_t off = pix * COUT + c0ch + 4 * v4;
+                  const uint2 mm = __ldg(reinterpret_cast<const uint2*>(mask) + off / 4);
+                  sum.x = __uint_as_float(mm.x << 16) > 0.f ? sum.x : 0.f;
+                  sum.y = __uint_as_float(mm.x & 0xffff0000u) > 0.f ? sum.y : 0.f;
+                  sum.z = __uint_as_float(mm.y << 16) > 0.f ? sum.z : 0.f;
+                  sum.w = __uint_as_float(mm.y & 0xffff0000u) > 0.f ? sum.w : 0.f;
+                  reinterpret_cast<uint2*>(out)[off / 4] = make_uint2(pack_bf16x2(sum.x, sum.y), pack_bf16x2(sum.z, sum.w));
+                  continue;
+                }
                 float* op = out + pix * COUT + c0ch + 4 * v4;
                 if (MODE == EPI_MASK) {
                   const float4 m = __ldg(reinterpret_cast<const float4*>(mask + pix * COUT + c0ch + 4 * v4));
@@ -289,13 +299,15 @@ cudaError_t setup_dgrad2_tf32(int n2) {
 }
 
 // training: layer-2 data gradient from the bf16 copy of dG2 (tmDGb: [B][n1][n2][32] bf16, box 32 ch x P x (R + 10)
-// rows, SWIZZLE_64B) with bf16 weight blocks (66 x 8 KB) -- twice the MMA rate of the TF32 form
-cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const float* h1, int batch, int n1, int n2,
-                               float* dh1, int num_sms, cudaStream_t st) {
+// rows, SWIZZLE_64B) with bf16 weight blocks (66 x 8 KB) -- twice the MMA rate of the TF32 form; the ReLU' mask is
+// read from bf16 h1 (h1b) and dH1 is written in bf16 (the operand wgrad1 contracts)
+cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const void* h1b, int batch, int n1, int n2,
+                               void* dh1b, int num_sms, cudaStream_t st) {
   GeoT g = make_geo_t(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
   k_conv_tf32<32, 64, EPI_MASK, true><<<grid, 384, conv2_tf32_smem_bytes(n2), st>>>(
-      *tmDGb, reinterpret_cast<const float*>(wpack), nullptr, 0, h1, g, dh1);
+      *tmDGb, reinterpret_cast<const float*>(wpack), nullptr, 0, reinterpret_cast<const float*>(h1b), g,
+      reinterpret_cast<float*>(dh1b));
   return cudaGetLastError();
 }
 

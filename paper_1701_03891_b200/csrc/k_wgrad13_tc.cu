@@ -1,6 +1,7 @@
 // k_wgrad13_tc.cu -- training: the weight gradients of the THIN layers on tcgen05.
 //
 //   layer 1 (C_in = 1):  dwx1[co][a][b] = sum_p dG1[p][co] * x~[p + (a-5, b-5)]           (k_train.cu header)
+//                        (dG1 arrives in bf16 from the bf16 layer-2 dgrad; its bias sum is taken over those values)
 //   layer 3 (C_out = 1): dwx3[ci][a][b] = sum_p dG3[p]     * h2[p + (a-5, b-5)][ci]
 //
 // Both contract over pixel positions with one single-channel operand.  As in k_wgrad2_tc.cu the operands are
@@ -54,8 +55,8 @@ __host__ __device__ inline int l3_nb(int P) { return R * P + 32; }
 
 // =============================================================================================== layer 1
 __global__ void __launch_bounds__(128, 1)
-    k_wgrad1_tc(const float* __restrict__ xt, const float* __restrict__ dg1, GeoT13 g, float* __restrict__ part,
-                float* __restrict__ part_b) {
+    k_wgrad1_tc(const float* __restrict__ xt, const __nv_bfloat16* __restrict__ dg1, GeoT13 g,
+                float* __restrict__ part, float* __restrict__ part_b) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xs = reinterpret_cast<float*>(smem + 2 * g.stage);
@@ -95,27 +96,25 @@ __global__ void __launch_bounds__(128, 1)
     // dG1 of the unit's pixels: position q -> (r0 + q / P, c0 + q % P), columns >= wseg zero; bf16 SW128
     constexpr int U = 4;   // chunks per thread in flight (memory-level parallelism)
     for (int i0 = tid; i0 < R * P * 8; i0 += 128 * U) {
-      float4 v[U][2];
+      uint4 v[U];
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int i = i0 + uu * 128, q = i >> 3, row = q / P, col = q - row * P;
         const int gr = r0 + row, gc = c0 + col;
-        v[uu][0] = v[uu][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (i < R * P * 8 && row < rows && col < g.wseg && gc < g.n2) {
-          const float4* src =
-              reinterpret_cast<const float4*>(dg1 + (((size_t)b * g.n1 + gr) * g.n2 + gc) * 64 + 8 * cg);
-          v[uu][0] = __ldg(src), v[uu][1] = __ldg(src + 1);
-        }
+        v[uu] = make_uint4(0, 0, 0, 0);
+        if (i < R * P * 8 && row < rows && col < g.wseg && gc < g.n2)
+          v[uu] = __ldg(reinterpret_cast<const uint4*>(dg1 + (((size_t)b * g.n1 + gr) * g.n2 + gc) * 64 + 8 * cg));
       }
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int i = i0 + uu * 128, q = i >> 3;
         if (i >= R * P * 8) break;
-        const float4 v0 = v[uu][0], v1 = v[uu][1];
-        bs[0] += v0.x, bs[1] += v0.y, bs[2] += v0.z, bs[3] += v0.w, bs[4] += v1.x, bs[5] += v1.y, bs[6] += v1.z,
-            bs[7] += v1.w;
-        *reinterpret_cast<uint4*>(d1 + (16 + q) * 128 + ((cg ^ (q & 7)) << 4)) =
-            make_uint4(pack2(v0.x, v0.y), pack2(v0.z, v0.w), pack2(v1.x, v1.y), pack2(v1.z, v1.w));
+        const uint4 w = v[uu];
+        bs[0] += __uint_as_float(w.x << 16), bs[1] += __uint_as_float(w.x & 0xffff0000u);
+        bs[2] += __uint_as_float(w.y << 16), bs[3] += __uint_as_float(w.y & 0xffff0000u);
+        bs[4] += __uint_as_float(w.z << 16), bs[5] += __uint_as_float(w.z & 0xffff0000u);
+        bs[6] += __uint_as_float(w.w << 16), bs[7] += __uint_as_float(w.w & 0xffff0000u);
+        *reinterpret_cast<uint4*>(d1 + (16 + q) * 128 + ((cg ^ (q & 7)) << 4)) = w;
       }
     }
     // x~ strip with halo: xs[q] = x~(r0 - 5 + q / P, c0 - 5 + q % P)
@@ -387,11 +386,12 @@ cudaError_t setup_wgrad13_tc(int n2) {
   return cudaFuncSetAttribute(k_wgrad3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(n2, false));
 }
 
-cudaError_t launch_wgrad1_tc(const float* xt, const float* dg1, int batch, int n1, int n2, float* part, float* part_b,
+cudaError_t launch_wgrad1_tc(const float* xt, const void* dg1, int batch, int n1, int n2, float* part, float* part_b,
                              int flip, float* gw, float* gb, int num_sms, cudaStream_t st) {
   GeoT13 g = make_geo(batch, n1, n2, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_wgrad1_tc<<<grid, 128, smem_bytes(n2, true), st>>>(xt, dg1, g, part, part_b);
+  k_wgrad1_tc<<<grid, 128, smem_bytes(n2, true), st>>>(xt, reinterpret_cast<const __nv_bfloat16*>(dg1), g, part,
+                                                       part_b);
   k_wgrad1_reduce<<<(64 * KS * KS + 64 + 255) / 256, 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
   return cudaGetLastError();
 }

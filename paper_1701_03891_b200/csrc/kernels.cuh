@@ -103,8 +103,8 @@ cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, 
                          float* part_b, int flip, float* gw, float* gb, cudaStream_t st);
 cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wp2d,
                                float* wpd3, void* wp2db, cudaStream_t st);
-cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const float* h1, int batch, int n1, int n2,
-                               float* dh1, int num_sms, cudaStream_t st);
+cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const void* h1b, int batch, int n1, int n2,
+                               void* dh1b, int num_sms, cudaStream_t st);
 // training, TF32 contexts: layer-2 data gradient on tcgen05 (k_conv2_tf32.cu); wpack = 66 blocks of 16 KB
 cudaError_t setup_dgrad2_tf32(int n2);
 cudaError_t launch_dgrad2_tf32(const CUtensorMap* tmDG, const void* wpack, const float* h1, int batch, int n1, int n2,
@@ -135,7 +135,8 @@ cudaError_t launch_dg2_bf16(const float* dg, size_t npix, void* dst, float* part
 constexpr int WG13_ROWS = 6;
 size_t wgrad13_tc_part_floats(int num_sms);
 cudaError_t setup_wgrad13_tc(int n2);
-cudaError_t launch_wgrad1_tc(const float* xt, const float* dg1, int batch, int n1, int n2, float* part, float* part_b,
+// dg1: [B][N][64] bf16 (the bf16 dgrad2 output)
+cudaError_t launch_wgrad1_tc(const float* xt, const void* dg1, int batch, int n1, int n2, float* part, float* part_b,
                              int flip, float* gw, float* gb, int num_sms, cudaStream_t st);
 cudaError_t launch_wgrad3_tc(const float* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
                              int flip, float* gw, float* gb, int num_sms, cudaStream_t st);
