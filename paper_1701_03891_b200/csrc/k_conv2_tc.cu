@@ -48,7 +48,6 @@ constexpr int WSTAGES = DI_C2_WSTAGES;  // weight ring depth (a 16-KB bulk copy 
 constexpr int KBLOCKS = C2_KBLOCKS;    // 33
 constexpr uint32_t WBYTES = C2_KBLOCK_BYTES;  // 16 KB
 constexpr int GUARD_ROWS = 24;
-constexpr int HALF_ROWS = (R + 10 + 1) / 2;  // strip rows of half A (half B: R + 10 - HALF_ROWS)
 constexpr int SPS = 36;                  // epilogue transpose row stride (floats): conflict-free float4 reads
 constexpr int ECH = 16;                  // epilogue chunk: output positions per TMEM load
 
@@ -69,10 +68,6 @@ __device__ __forceinline__ void ld_tail13(uint32_t taddr, uint32_t* r) {
 }
 
 
-// SPLIT = true: the strip is loaded as two halves (rows 0..7 / 8..15) by a dedicated producer thread, with
-// one full/empty barrier pair per half, so the next unit's half A streams in while the last tile of this unit
-// only reads half B (and half B while the first K-blocks of the next unit only read half A).
-template <bool SPLIT>
 __global__ void __launch_bounds__(256, 1)
     k_conv2_tc(const __grid_constant__ CUtensorMap tmH1, const __nv_bfloat16* __restrict__ wpack,
                const float* __restrict__ bias, int fullmap, Geo g, __nv_bfloat16* __restrict__ h2) {
@@ -111,10 +106,8 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = tslot;
 
   const int per_img = g.nrb * g.ncs;
-  const int half_bytes = HALF_ROWS * g.P * 128;
-  const int halfpos = HALF_ROWS * g.P;    // first strip position of half B
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------ weight (+ unsplit strip) producer
+    if (lane == 0) {  // ------------------------------------------------ strip + weight producer
       uint32_t wk = 0;                    // weight K-blocks issued (stage wk % WSTAGES)
       int it = 0;
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
@@ -123,11 +116,9 @@ __global__ void __launch_bounds__(256, 1)
         const int rows = min(R, g.n1 - r0);
         const int L = (rows - 1) * g.P + g.wseg;
         const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
-        if (!SPLIT) {
-          if (it > 0) mbar_wait(&hempty[0], (it - 1) & 1);
-          mbar_arrive_expect_tx(&hfull[0], strip_bytes);
-          tma_load_4d(strip, &tmH1, &hfull[0], 0, c0 - 5, r0 - 5, b);
-        }
+        if (it > 0) mbar_wait(&hempty[0], (it - 1) & 1);
+        mbar_arrive_expect_tx(&hfull[0], strip_bytes);
+        tma_load_4d(strip, &tmH1, &hfull[0], 0, c0 - 5, r0 - 5, b);
         for (int t = 0; t < ntiles; ++t) {
           const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack);
           for (int kb = 0; kb < KBLOCKS; ++kb, ++wk, wsrc += WBYTES) {
@@ -147,20 +138,6 @@ __global__ void __launch_bounds__(256, 1)
 #endif
           }
         }
-      }
-    }
-  } else if (warp == 3) {
-    if (SPLIT && lane == 0) {  // ---------------------------------------- strip producer (two halves)
-      int it = 0;
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
-        const int b = u / per_img, rem = u - b * per_img;
-        const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
-        if (it > 0) mbar_wait(&hempty[0], (it - 1) & 1);
-        mbar_arrive_expect_tx(&hfull[0], half_bytes);
-        tma_load_4d(strip, &tmH1, &hfull[0], 0, c0 - 5, r0 - 5, b);
-        if (it > 0) mbar_wait(&hempty[1], (it - 1) & 1);
-        mbar_arrive_expect_tx(&hfull[1], half_bytes);
-        tma_load_4d(strip + half_bytes, &tmH1, &hfull[1], 0, c0 - 5, r0 - 5 + HALF_ROWS, b);
       }
     }
   } else if (warp == 1) {
@@ -188,7 +165,6 @@ __global__ void __launch_bounds__(256, 1)
         const int L = (rows - 1) * g.P + g.wseg;
         const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
         { PT0 mbar_wait(&hfull[0], it & 1); PT1(c_h) }
-        bool bready = !SPLIT, afree = false;
         tc_fence_after();
         for (int t = 0; t < ntiles; ++t, ++ti) {
           const int n0 = t * OUT_PER_TILE;
@@ -199,15 +175,8 @@ __global__ void __launch_bounds__(256, 1)
           { PT0 if (ti >= 2) mbar_wait(&tempty[buf], ((ti >> 1) - 1) & 1); PT1(c_t) }
           tc_fence_after();
           const uint32_t d = tmem + buf * 256;
-          const bool last = t == ntiles - 1;
           uint64_t bd = bdesc0 + (uint64_t)(n0 * 8);
-          int pos = n0;                     // first strip position read by tap row uu (v0 = 0)
-          for (int uu = 0; uu < 11; ++uu, bd += pstep, pos += g.P) {
-            if (SPLIT && !bready && pos + 8 + nmma - 1 >= halfpos) {
-              mbar_wait(&hfull[1], it & 1);
-              bready = true;
-              tc_fence_after();
-            }
+          for (int uu = 0; uu < 11; ++uu, bd += pstep) {
 #pragma unroll
             for (int j = 0; j < 3; ++j, ++wk) {   // column-tap groups v0 = 0, 4, 8
               const uint32_t st = wk % WSTAGES;
@@ -228,18 +197,10 @@ __global__ void __launch_bounds__(256, 1)
               umma_f16_ss(d, ad + 6, b + 6, idesc, 1);
               umma_commit(&wempty[st]);
             }
-            // half A is free once the last tile has passed the last tap row whose window starts in it
-            if (SPLIT && last && pos < halfpos && pos + g.P >= halfpos) umma_commit(&hempty[0]), afree = true;
           }
           umma_commit(&tfull[buf]);
         }
-        if (SPLIT) {
-          if (!afree) umma_commit(&hempty[0]);    // (the last tile's tap rows never crossed into half B)
-          if (!bready) mbar_wait(&hfull[1], it & 1);
-          umma_commit(&hempty[1]);
-        } else {
-          umma_commit(&hempty[0]);
-        }
+        umma_commit(&hempty[0]);
       }
 #ifdef DI_PROF_CONV2
       if (blockIdx.x % 37 == 0)
@@ -343,31 +304,21 @@ size_t conv2_tc_smem_bytes(int n2) {
   return strip_alloc + WSTAGES * WBYTES + 4 * ECH * SPS * 4 + 1024;
 }
 
-// Split strip loading (SPLIT = true) needs equal halves (R + 10 even) and a second tensor map otherwise; with
-// R = 5 and a 4-deep weight ring it measured no gain, so the unsplit schedule is used.
 // The strip is loaded in one box per unit.  Loading it as two halves with a separate producer so that the load
-// overlaps the MMAs of the previous unit (k_conv2_tc<true>) removes the strip wait but measured slower on B200
-// (the TMA writes compete with the UMMA operand reads for shared-memory bandwidth, which this kernel saturates:
-// DESIGN.md §6), so it is kept for reference and not launched.
-static bool conv2_split() { return false; }
-
-int conv2_tc_box_rows() { return conv2_split() ? HALF_ROWS : R + 10; }
+// overlaps the MMAs of the previous unit removes the strip wait but measured slower on B200 (the TMA writes
+// compete with the UMMA operand reads for shared-memory bandwidth, which this kernel saturates: DESIGN.md §11).
+int conv2_tc_box_rows() { return R + 10; }
 int conv2_tc_box_cols(int n2) { return (n2 < WSEG ? n2 : WSEG) + 10; }
 
 cudaError_t setup_conv2_tc(int n2) {
-  cudaError_t e = cudaFuncSetAttribute(k_conv2_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)conv2_tc_smem_bytes(n2));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_conv2_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)conv2_tc_smem_bytes(n2));
+  return cudaFuncSetAttribute(k_conv2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)conv2_tc_smem_bytes(n2));
 }
 
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st) {
   Geo g = make_geo(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  auto k = conv2_split() ? k_conv2_tc<true> : k_conv2_tc<false>;
-  k<<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(*tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias,
+  k_conv2_tc<<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(*tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias,
                                                          fullmap, g, reinterpret_cast<__nv_bfloat16*>(h2));
   return cudaGetLastError();
 }
