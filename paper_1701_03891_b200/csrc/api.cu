@@ -1131,6 +1131,7 @@ static di_status train_alloc(di_ctx c) {
                                  c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2, c->b3, 0));
   if (c->prec == DI_PREC_TF32) {
     CUDA_TRY(di::setup_dgrad2_tf32(c->n2));
+    CUDA_TRY(di::setup_conv2_tc(c->n2));   // the bf16 layer-2 kernel also runs the layer-2 data gradient
     if ((s = al(&c->h1b, B * N * C1 * 2)) != DI_OK) return s;
     if ((s = al(&c->dg2b, B * N * C2 * 2)) != DI_OK) return s;
     if ((s = al(&c->dh1b, B * N * C1 * 2)) != DI_OK) return s;

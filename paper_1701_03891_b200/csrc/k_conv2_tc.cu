@@ -55,7 +55,7 @@ struct Geo {
   int n1, n2, wseg, P, nrb, ncs, units;
 };
 
-__host__ __device__ inline int strip_rows_bytes(int P) { return (R + 10) * P * 128; }
+__host__ __device__ inline int strip_rows_bytes(int P) { return (R + 10) * P * 128; }   // the largest (C_in = 64)
 }  // namespace
 
 // last chunk of a full tile (c0 = 224, at most 29 outputs): columns c0+q .. c0+q+28 <= 255, loaded as
@@ -68,16 +68,29 @@ __device__ __forceinline__ void ld_tail13(uint32_t taddr, uint32_t* r) {
 }
 
 
+enum { C2_BIAS_RELU = 0, C2_MASK = 1 };
+
+// Template over the channel counts (the paper's layer 2 is <64, 32, C2_BIAS_RELU>): TAPS = 128 / C_out column taps
+// x C_out filters in M, strip rows of C_in bf16 channels (128 B: SWIZZLE_128B; 64 B: SWIZZLE_64B), K-block = one
+// strip row (C_in / 16 MMAs of K = 16), 11 ceil(11 / TAPS) K-blocks per tile.  <32, 64, C2_MASK> is the training
+// step's layer-2 data gradient: dG2 (bf16) in, the rotated bank, out = [h1 > 0] * conv in bf16 (mask = bf16 h1).
+template <int CIN, int COUT, int MODE>
 __global__ void __launch_bounds__(256, 1)
     k_conv2_tc(const __grid_constant__ CUtensorMap tmH1, const __nv_bfloat16* __restrict__ wpack,
-               const float* __restrict__ bias, int fullmap, Geo g, __nv_bfloat16* __restrict__ h2) {
+               const float* __restrict__ bias, int fullmap, Geo g, __nv_bfloat16* __restrict__ h2,
+               const __nv_bfloat16* __restrict__ mask) {
+  constexpr int TAPS = 128 / COUT, J = (11 + TAPS - 1) / TAPS, KB = 11 * J;
+  constexpr int RB = CIN * 2, KMMA = RB / 32;
+  constexpr uint32_t WB = 128 * RB;
+  constexpr uint32_t SWZ = RB == 128 ? kSwizzle128B : kSwizzle64B;
+  constexpr int QPT = COUT / 32, CPT = COUT / 8;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int strip_bytes = strip_rows_bytes(g.P);
-  const int strip_alloc = (strip_bytes + GUARD_ROWS * 128 + 1023) & ~1023;
+  const int strip_bytes = (R + 10) * g.P * RB;
+  const int strip_alloc = (strip_bytes + GUARD_ROWS * RB + 1023) & ~1023;
   uint8_t* strip = smem;
   uint8_t* wst = smem + strip_alloc;
-  float* sP = reinterpret_cast<float*>(wst + WSTAGES * WBYTES);  // [4][32 positions][SPS]
+  float* sP = reinterpret_cast<float*>(wst + WSTAGES * WB);  // [4][ECH positions][SPS]
 
   __shared__ uint64_t hfull[2], hempty[2], wfull[WSTAGES], wempty[WSTAGES], tfull[2], tempty[2];
 #ifdef DI_PROF_CONV2
@@ -97,7 +110,7 @@ __global__ void __launch_bounds__(256, 1)
   // Guard rows after the strip: the zero tap slot (v = 11) of the last output position and the padded
   // columns of the last tile read up to GUARD_ROWS rows past the TMA box.  Their weights / outputs are
   // zero / discarded, but 0 * (NaN garbage) would not be, so the guard must hold finite values.
-  for (int i = threadIdx.x; i < GUARD_ROWS * 128 / 16; i += blockDim.x)
+  for (int i = threadIdx.x; i < GUARD_ROWS * RB / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(strip + strip_bytes)[i] = make_uint4(0, 0, 0, 0);
   fence_async_smem();
   tc_fence_before();
@@ -121,20 +134,20 @@ __global__ void __launch_bounds__(256, 1)
         tma_load_4d(strip, &tmH1, &hfull[0], 0, c0 - 5, r0 - 5, b);
         for (int t = 0; t < ntiles; ++t) {
           const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack);
-          for (int kb = 0; kb < KBLOCKS; ++kb, ++wk, wsrc += WBYTES) {
+          for (int kb = 0; kb < KB; ++kb, ++wk, wsrc += WB) {
             const uint32_t st = wk % WSTAGES;
             if (wk >= WSTAGES) mbar_wait(&wempty[st], ((wk / WSTAGES) - 1) & 1);
 #if defined(DI_EXP_NOW)
             mbar_arrive(&wfull[st]);                          // experiment: no weight copies (wrong results)
 #elif defined(DI_EXP_HALFW)
-            mbar_arrive_expect_tx(&wfull[st], WBYTES / 2);   // experiment: half the weight bytes (wrong results)
-            bulk_load(wst + st * WBYTES, wsrc, WBYTES / 2, &wfull[st]);
+            mbar_arrive_expect_tx(&wfull[st], WB / 2);   // experiment: half the weight bytes (wrong results)
+            bulk_load(wst + st * WB, wsrc, WB / 2, &wfull[st]);
 #else
 #ifdef DI_PROF_CONV2
             t_issue[st] = clock64();
 #endif
-            mbar_arrive_expect_tx(&wfull[st], WBYTES);
-            bulk_load(wst + st * WBYTES, wsrc, WBYTES, &wfull[st]);
+            mbar_arrive_expect_tx(&wfull[st], WB);
+            bulk_load(wst + st * WB, wsrc, WB, &wfull[st]);
 #endif
           }
         }
@@ -145,9 +158,9 @@ __global__ void __launch_bounds__(256, 1)
       // Lean loop: descriptors built once, per-MMA addresses are immediate 64-bit adds of (bytes >> 4); the
       // stage index of K-block (uu, j) is j (33 K-blocks per tile, 3 stages).  A single issuing thread is
       // latency-bound, so every instruction here costs tensor-pipe time.
-      const uint64_t bdesc0 = smem_desc(smem_u32(strip), 16, 1024, kSwizzle128B);
-      const uint64_t adesc0 = smem_desc(smem_u32(wst), 16, 1024, kSwizzle128B);
-      const uint64_t pstep = (uint64_t)g.P * 8;    // one tap row = P positions x 128 B, >> 4
+      const uint64_t bdesc0 = smem_desc(smem_u32(strip), 16, 8 * RB, SWZ);
+      const uint64_t adesc0 = smem_desc(smem_u32(wst), 16, 8 * RB, SWZ);
+      const uint64_t pstep = (uint64_t)g.P * (RB >> 4);    // one tap row = P positions x RB bytes, >> 4
       uint32_t wk = 0;
       int it = 0, ti = 0;
 #ifdef DI_PROF_CONV2
@@ -169,16 +182,16 @@ __global__ void __launch_bounds__(256, 1)
         for (int t = 0; t < ntiles; ++t, ++ti) {
           const int n0 = t * OUT_PER_TILE;
           const int cnt = min(OUT_PER_TILE, L - n0);
-          const int nmma = min(NT, (cnt + 3 + 15) & ~15);
+          const int nmma = min(NT, (cnt + TAPS - 1 + 15) & ~15);
           const uint32_t idesc = idesc_f32acc(1, 128, nmma);
           const int buf = ti & 1;
           { PT0 if (ti >= 2) mbar_wait(&tempty[buf], ((ti >> 1) - 1) & 1); PT1(c_t) }
           tc_fence_after();
           const uint32_t d = tmem + buf * 256;
-          uint64_t bd = bdesc0 + (uint64_t)(n0 * 8);
+          uint64_t bd = bdesc0 + (uint64_t)(n0 * (RB >> 4));
           for (int uu = 0; uu < 11; ++uu, bd += pstep) {
 #pragma unroll
-            for (int j = 0; j < 3; ++j, ++wk) {   // column-tap groups v0 = 0, 4, 8
+            for (int j = 0; j < J; ++j, ++wk) {   // column-tap groups v0 = TAPS j (0, 4, 8 for C_out = 32)
               const uint32_t st = wk % WSTAGES;
 #ifdef DI_PROF_CONV2
               { PT0 mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
@@ -189,12 +202,11 @@ __global__ void __launch_bounds__(256, 1)
               mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
 #endif
               tc_fence_after();
-              const uint64_t ad = adesc0 + (uint64_t)(st * (WBYTES >> 4));
-              const uint64_t b = bd + (uint64_t)(32 * j);   // v0 = 4j positions x 128 B >> 4
+              const uint64_t ad = adesc0 + (uint64_t)(st * (WB >> 4));
+              const uint64_t b = bd + (uint64_t)(TAPS * j * (RB >> 4));   // v0 = TAPS j positions
               umma_f16_ss(d, ad, b, idesc, (uu | j) != 0);
-              umma_f16_ss(d, ad + 2, b + 2, idesc, 1);
-              umma_f16_ss(d, ad + 4, b + 4, idesc, 1);
-              umma_f16_ss(d, ad + 6, b + 6, idesc, 1);
+#pragma unroll
+              for (int kk = 1; kk < KMMA; ++kk) umma_f16_ss(d, ad + 2 * kk, b + 2 * kk, idesc, 1);
               umma_commit(&wempty[st]);
             }
           }
@@ -210,12 +222,14 @@ __global__ void __launch_bounds__(256, 1)
 #endif
     }
   } else if (warp >= 4) {  // ---------------------------------------------- epilogue
-    const int q = warp - 4;              // TMEM lane quadrant = column-tap group v'
+    const int q = warp - 4;              // TMEM lane quadrant: column tap q / QPT, channel block q % QPT
+    const int shift = q / QPT;
     const int e = threadIdx.x - 128;     // 0..127
-    const int jj = e >> 3, kg = e & 7;   // reduce role: output position jj of the chunk, channels 4kg..4kg+3
-    float bch[4];
+    const int jj = e >> 3, kg = e & 7;   // reduce role: output position jj of the chunk, channels CPT kg ..
+    const int c0ch = CPT * kg, cblk = c0ch / 32, cl = c0ch % 32;
+    float bch[CPT];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) bch[i] = (!fullmap && bias) ? bias[4 * kg + i] : 0.f;
+    for (int i = 0; i < CPT; ++i) bch[i] = (MODE == C2_BIAS_RELU && !fullmap && bias) ? bias[c0ch + i] : 0.f;
     int ti = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
       const int b = u / per_img, rem = u - b * per_img;
@@ -233,10 +247,10 @@ __global__ void __launch_bounds__(256, 1)
         for (int c = 0; c < cnt; c += ECH) {
           const int nout = min(ECH, cnt - c);
           uint32_t r[ECH];
-          if (c + q + ECH <= NT)
-            tmem_ld16(tq + c + q, r);
+          if (c + shift + ECH <= NT)
+            tmem_ld16(tq + c + shift, r);
           else
-            ld_tail13(tq + c + q, r);
+            ld_tail13(tq + c + shift, r);
           tmem_ld_wait();
 #ifdef DI_EXP_NOEPI_SMEM
           {   // experiment: no shared-memory transpose (wrong results): raw registers straight to h2
@@ -256,23 +270,36 @@ __global__ void __launch_bounds__(256, 1)
             const int rr = o / g.P, cc = o - rr * g.P;
             const int orow = r0 + rr, ocol = c0 + cc;
             if (cc < g.wseg && ocol < g.n2 && rr < rows) {
-              float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) {
-                const float4 a = *reinterpret_cast<const float4*>(sP + qq * (ECH * SPS) + jj * SPS + 4 * kg);
-                sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
-              }
               const size_t pix = ((size_t)b * g.n1 + orow) * g.n2 + ocol;
-              if (fullmap && bias) {
-                const float4 a = *reinterpret_cast<const float4*>(bias + pix % ((size_t)g.n1 * g.n2) * 32 + 4 * kg);
-                sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
-              } else {
-                sum.x += bch[0], sum.y += bch[1], sum.z += bch[2], sum.w += bch[3];
+#pragma unroll
+              for (int v4 = 0; v4 < CPT / 4; ++v4) {
+                float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int tp = 0; tp < TAPS; ++tp) {
+                  const float4 a = *reinterpret_cast<const float4*>(sP + (tp * QPT + cblk) * (ECH * SPS) + jj * SPS +
+                                                                    cl + 4 * v4);
+                  sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
+                }
+                const size_t off = pix * COUT + c0ch + 4 * v4;
+                uint2 v;
+                if (MODE == C2_MASK) {
+                  const uint2 mm = __ldg(reinterpret_cast<const uint2*>(mask + off));
+                  v.x = pack_bf16x2(__uint_as_float(mm.x << 16) > 0.f ? sum.x : 0.f,
+                                    __uint_as_float(mm.x & 0xffff0000u) > 0.f ? sum.y : 0.f);
+                  v.y = pack_bf16x2(__uint_as_float(mm.y << 16) > 0.f ? sum.z : 0.f,
+                                    __uint_as_float(mm.y & 0xffff0000u) > 0.f ? sum.w : 0.f);
+                } else {
+                  if (fullmap && bias) {
+                    const float4 a = *reinterpret_cast<const float4*>(bias + pix % ((size_t)g.n1 * g.n2) * COUT + c0ch + 4 * v4);
+                    sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
+                  } else {
+                    sum.x += bch[4 * v4], sum.y += bch[4 * v4 + 1], sum.z += bch[4 * v4 + 2], sum.w += bch[4 * v4 + 3];
+                  }
+                  v.x = pack_bf16x2(fmaxf(sum.x, 0.f), fmaxf(sum.y, 0.f));
+                  v.y = pack_bf16x2(fmaxf(sum.z, 0.f), fmaxf(sum.w, 0.f));
+                }
+                *reinterpret_cast<uint2*>(h2 + off) = v;
               }
-              uint2 v;
-              v.x = pack_bf16x2(fmaxf(sum.x, 0.f), fmaxf(sum.y, 0.f));
-              v.y = pack_bf16x2(fmaxf(sum.z, 0.f), fmaxf(sum.w, 0.f));
-              *reinterpret_cast<uint2*>(h2 + pix * 32 + 4 * kg) = v;
             }
           }
           named_bar(1, 128);
@@ -311,15 +338,33 @@ int conv2_tc_box_rows() { return R + 10; }
 int conv2_tc_box_cols(int n2) { return (n2 < WSEG ? n2 : WSEG) + 10; }
 
 cudaError_t setup_conv2_tc(int n2) {
-  return cudaFuncSetAttribute(k_conv2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)conv2_tc_smem_bytes(n2));
+  cudaError_t e = cudaFuncSetAttribute(k_conv2_tc<64, 32, C2_BIAS_RELU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)conv2_tc_smem_bytes(n2));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_conv2_tc<32, 64, C2_MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)conv2_tc_smem_bytes(n2));
 }
 
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st) {
   Geo g = make_geo(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv2_tc<<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(*tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias,
-                                                         fullmap, g, reinterpret_cast<__nv_bfloat16*>(h2));
+  k_conv2_tc<64, 32, C2_BIAS_RELU><<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(
+      *tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias, fullmap, g, reinterpret_cast<__nv_bfloat16*>(h2),
+      nullptr);
+  return cudaGetLastError();
+}
+
+// training: the layer-2 data gradient on the bf16 layer-2 machinery (TMEM double buffering, weights per tile):
+// tmDGb = dG2 [B][n1][n2][32] bf16 strips (box 32 ch x P x (R + 10) rows, SWIZZLE_64B), wpack = 66 x 8-KB blocks
+// (rows v' * 64 + ci, 32 co, SWIZZLE_64B), h1b = bf16 h1 (the ReLU' mask), dh1b = bf16 output
+cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const void* h1b, int batch, int n1, int n2,
+                               void* dh1b, int num_sms, cudaStream_t st) {
+  Geo g = make_geo(batch, n1, n2);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  k_conv2_tc<32, 64, C2_MASK><<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(
+      *tmDGb, reinterpret_cast<const __nv_bfloat16*>(wpack), nullptr, 0, g, reinterpret_cast<__nv_bfloat16*>(dh1b),
+      reinterpret_cast<const __nv_bfloat16*>(h1b));
   return cudaGetLastError();
 }
 

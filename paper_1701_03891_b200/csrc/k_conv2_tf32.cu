@@ -47,9 +47,7 @@ enum { EPI_BIAS_RELU = 0, EPI_MASK = 1 };
 
 // MODE EPI_BIAS_RELU: out = ReLU(conv + bias) (per-channel bias, or full-map bias [n1*n2][C_out] when fullmap);
 // MODE EPI_MASK:      out = [mask > 0] * conv (the ReLU' of the layer whose gradient this is)
-// BF = true: bf16 operands (kind::f16, K = 16 per MMA) -- the training step's layer-2 data gradient: a strip row is
-// the C_in bf16 channels (64 B for C_in = 32, SWIZZLE_64B), one K-block = the whole row (2 MMAs), 8-KB weight blocks.
-template <int CIN, int COUT, int MODE, bool BF = false>
+template <int CIN, int COUT, int MODE>
 __global__ void __launch_bounds__(384, 1)
     k_conv_tf32(const __grid_constant__ CUtensorMap tmIn, const float* __restrict__ wpack,
                 const float* __restrict__ bias, int fullmap, const float* __restrict__ mask, GeoT g,
@@ -57,8 +55,8 @@ __global__ void __launch_bounds__(384, 1)
   constexpr int TAPS = 128 / COUT;            // column taps stacked in M
   constexpr int J = (11 + TAPS - 1) / TAPS;   // column-tap groups per tap row
   constexpr int KBH = 11 * J;                 // K-blocks per channel half
-  constexpr int BOXC = BF ? (CIN < 64 ? CIN : 64) : 32;   // channels per strip row (one 64/128-B swizzle row)
-  constexpr int RB = BOXC * (BF ? 2 : 4);     // strip / weight row bytes
+  constexpr int BOXC = 32;                    // fp32 channels per strip row (one 128-B swizzle row)
+  constexpr int RB = BOXC * 4;                // strip / weight row bytes
   constexpr int NH = CIN / BOXC;              // channel halves
   constexpr int KMMA = RB / 32;               // MMAs per K-block (32 B of K each)
   constexpr uint32_t WB = 128 * RB;           // weight block bytes
@@ -128,7 +126,7 @@ __global__ void __launch_bounds__(384, 1)
         const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;   // 1 or 2
         const int nB = ntiles > 1 ? min(NT, (min(OUT_PER_TILE, L - OUT_PER_TILE) + TAPS - 1 + 15) & ~15) : 0;
         const int nA = min(NT, (min(OUT_PER_TILE, L) + TAPS - 1 + 15) & ~15);
-        const uint32_t idA = idesc_f32acc(BF ? 1 : 2, 128, nA), idB = idesc_f32acc(BF ? 1 : 2, 128, nB > 0 ? nB : 16);
+        const uint32_t idA = idesc_f32acc(2, 128, nA), idB = idesc_f32acc(2, 128, nB > 0 ? nB : 16);
         if (it > 0) mbar_wait(&tempty, (it - 1) & 1);   // the epilogue drained the previous unit
         tc_fence_after();
         for (int h = 0; h < NH; ++h, ++sk) {
@@ -145,21 +143,11 @@ __global__ void __launch_bounds__(384, 1)
               const uint64_t b = bd + (uint64_t)(TAPS * j * (RB >> 4));   // v0 = TAPS j positions
               const uint32_t acc0 = (h | uu | j) != 0;
 #pragma unroll
-              for (int kk = 0; kk < KMMA; ++kk) {
-                if (BF)
-                  umma_f16_ss(tmem, ad + 2 * kk, b + 2 * kk, idA, kk ? 1u : acc0);
-                else
-                  umma_tf32_ss(tmem, ad + 2 * kk, b + 2 * kk, idA, kk ? 1u : acc0);
-              }
+              for (int kk = 0; kk < KMMA; ++kk) umma_tf32_ss(tmem, ad + 2 * kk, b + 2 * kk, idA, kk ? 1u : acc0);
               if (nB > 0) {
                 const uint64_t bb = b + (uint64_t)(OUT_PER_TILE * (RB >> 4));
 #pragma unroll
-                for (int kk = 0; kk < KMMA; ++kk) {
-                  if (BF)
-                    umma_f16_ss(tmem + 256, ad + 2 * kk, bb + 2 * kk, idB, kk ? 1u : acc0);
-                  else
-                    umma_tf32_ss(tmem + 256, ad + 2 * kk, bb + 2 * kk, idB, kk ? 1u : acc0);
-                }
+                for (int kk = 0; kk < KMMA; ++kk) umma_tf32_ss(tmem + 256, ad + 2 * kk, bb + 2 * kk, idB, kk ? 1u : acc0);
               }
               umma_commit(&wempty[st]);
             }
@@ -217,16 +205,6 @@ __global__ void __launch_bounds__(384, 1)
                   const float4 a =
                       *reinterpret_cast<const float4*>(sPg + (tp * QPT + cblk) * (ECH * SPS) + jj * SPS + cl + 4 * v4);
                   sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
-                }
-                if (MODE == EPI_MASK && BF) {   // bf16 in / out: the ReLU' mask from bf16 h1, bf16 dh1 for wgrad1
-                  const size_t off = pix * COUT + c0ch + 4 * v4;
-                  const uint2 mm = __ldg(reinterpret_cast<const uint2*>(mask) + off / 4);
-                  sum.x = __uint_as_float(mm.x << 16) > 0.f ? sum.x : 0.f;
-                  sum.y = __uint_as_float(mm.x & 0xffff0000u) > 0.f ? sum.y : 0.f;
-                  sum.z = __uint_as_float(mm.y << 16) > 0.f ? sum.z : 0.f;
-                  sum.w = __uint_as_float(mm.y & 0xffff0000u) > 0.f ? sum.w : 0.f;
-                  reinterpret_cast<uint2*>(out)[off / 4] = make_uint2(pack_bf16x2(sum.x, sum.y), pack_bf16x2(sum.z, sum.w));
-                  continue;
                 }
                 float* op = out + pix * COUT + c0ch + 4 * v4;
                 if (MODE == EPI_MASK) {
@@ -291,25 +269,7 @@ cudaError_t setup_conv2_tf32(int n2) {
   return set_smem<64, 64, EPI_BIAS_RELU>(n2);
 }
 
-cudaError_t setup_dgrad2_tf32(int n2) {
-  cudaError_t e = set_smem<32, 64, EPI_MASK>(n2);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_conv_tf32<32, 64, EPI_MASK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)conv2_tf32_smem_bytes(n2));
-}
-
-// training: layer-2 data gradient from the bf16 copy of dG2 (tmDGb: [B][n1][n2][32] bf16, box 32 ch x P x (R + 10)
-// rows, SWIZZLE_64B) with bf16 weight blocks (66 x 8 KB) -- twice the MMA rate of the TF32 form; the ReLU' mask is
-// read from bf16 h1 (h1b) and dH1 is written in bf16 (the operand wgrad1 contracts)
-cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const void* h1b, int batch, int n1, int n2,
-                               void* dh1b, int num_sms, cudaStream_t st) {
-  GeoT g = make_geo_t(batch, n1, n2);
-  const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv_tf32<32, 64, EPI_MASK, true><<<grid, 384, conv2_tf32_smem_bytes(n2), st>>>(
-      *tmDGb, reinterpret_cast<const float*>(wpack), nullptr, 0, reinterpret_cast<const float*>(h1b), g,
-      reinterpret_cast<float*>(dh1b));
-  return cudaGetLastError();
-}
+cudaError_t setup_dgrad2_tf32(int n2) { return set_smem<32, 64, EPI_MASK>(n2); }
 
 template <int CIN, int COUT, int MODE>
 static cudaError_t launch(const CUtensorMap* tm, const void* wpack, const float* bias, int fullmap, const float* mask,
