@@ -96,13 +96,11 @@ struct di_ctx_s {
   };
   std::vector<Layer> stack;     // empty: the paper's three layers (w1..b3)
   float* act[2] = {nullptr, nullptr};   // custom stack: ping-pong activations [max_batch][N][<= 64] fp32
-  float* wp2d = nullptr;        // training, TF32 mode: layer-2 dgrad weight blocks (k_dgrad2_tf32)
   float* wpd3 = nullptr;        // training, TF32 mode: layer-3 dgrad bank in the conv1 TF32 layout
   void* wp2db = nullptr;        // training, TF32 mode: layer-2 dgrad bf16 weight blocks (66 x 8 KB)
   CUtensorMap tmDG2s;           // training, TF32 mode: bf16 dG2 strips for the bf16 dgrad2 (box rows R + 10)
   bool has_tmDX = false;
   CUtensorMap tmDX;             // training, TF32 mode: dG3 strips (the conv1 x_tilde map over dxh)
-  CUtensorMap tmDG2;            // training, TF32 mode: dG2 strips (fp32, 32 channels)
   void *h1b = nullptr, *dg2b = nullptr;   // training, TF32 mode: bf16 copies of h1 / dG2 (layer-2 wgrad operands)
   void* dh1b = nullptr;                   // training, TF32 mode: dH1 in bf16 (bf16 dgrad2 -> wgrad1)
   float* part_w2 = nullptr;     // training, TF32 mode: per-CTA layer-2 wgrad partials
@@ -453,7 +451,7 @@ void free_ctx(di_ctx c) {
   }
   for (auto p : c->act)
     if (p) cudaFree(p);
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wp2d, c->wpd3, c->wp2db, c->h1b, c->dg2b, c->dh1b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
+  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wpd3, c->wp2db, c->h1b, c->dg2b, c->dh1b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
                 c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->phi_sense, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
@@ -1130,7 +1128,6 @@ static di_status train_alloc(di_ctx c) {
   CUDA_TRY(di::launch_sgd_repack(c->params, nullptr, c->vel, di::N_PARAMS, 0.f, 0.f, !(c->flags & DI_FLAG_XCORR),
                                  c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2, c->b3, 0));
   if (c->prec == DI_PREC_TF32) {
-    CUDA_TRY(di::setup_dgrad2_tf32(c->n2));
     CUDA_TRY(di::setup_conv2_tc(c->n2));   // the bf16 layer-2 kernel also runs the layer-2 data gradient
     if ((s = al(&c->h1b, B * N * C1 * 2)) != DI_OK) return s;
     if ((s = al(&c->dg2b, B * N * C2 * 2)) != DI_OK) return s;
@@ -1151,7 +1148,7 @@ static di_status train_alloc(di_ctx c) {
       c->has_tmDX = true;
     }
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
-                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d, c->wpd3, c->wp2db, 0));
+                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wpd3, c->wp2db, 0));
   }
   CUDA_TRY(cudaDeviceSynchronize());
   return DI_OK;
@@ -1192,7 +1189,7 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   const float* xt = reinterpret_cast<const float*>(c->xt);
   const float* h1 = reinterpret_cast<const float*>(c->h1);
   const float* h2 = reinterpret_cast<const float*>(c->h2);
-  const bool tc = c->prec == DI_PREC_TF32;   // tensor-core backward (k_dgrad2_tf32, k_wgrad*_tc)
+  const bool tc = c->prec == DI_PREC_TF32;   // tensor-core backward (k_conv2_tc<32, 64>, k_wgrad*_tc, dgrad3)
   if (tc)
     CUDA_TRY(di::launch_wgrad3_tc(h2, c->dxh, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads + n1w + n2w,
                                   gb + C1 + C2, c->num_sms, st));
@@ -1236,8 +1233,8 @@ di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, 
                                  c->b3, reinterpret_cast<cudaStream_t>(stream)));
   if (c->prec == DI_PREC_TF32)
     CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
-                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wp2d,
-                                    c->wpd3, c->wp2db, reinterpret_cast<cudaStream_t>(stream)));
+                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wpd3,
+                                    c->wp2db, reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }
 

@@ -1,7 +1,7 @@
 // k_conv2_tf32.cu -- the 11x11 multi-channel convolutions in TF32 mode (fp32 activations, tcgen05.mma kind::tf32,
 // fp32 accumulation), one template for every (C_in, C_out) in {32, 64} x {32, 64}:
 //   * stage 2 of the paper's stack, conv layer 2 (64 -> 32, bias + ReLU, crop S);
-//   * the training step's layer-2 data gradient (32 -> 64 with the rotated bank, ReLU'-masked; k_train.cu);
+//   * (EPI_MASK: a ReLU'-masked data gradient; the training step runs its layer-2 one on the bf16 kernel instead);
 //   * the interior layers of deeper / wider stacks.
 //
 // Same implicit-GEMM mapping as the bf16 kernel (k_conv2_tc.cu): pixels are the UMMA N dimension, TAPS = 128 / C_out
@@ -269,7 +269,6 @@ cudaError_t setup_conv2_tf32(int n2) {
   return set_smem<64, 64, EPI_BIAS_RELU>(n2);
 }
 
-cudaError_t setup_dgrad2_tf32(int n2) { return set_smem<32, 64, EPI_MASK>(n2); }
 
 template <int CIN, int COUT, int MODE>
 static cudaError_t launch(const CUtensorMap* tm, const void* wpack, const float* bias, int fullmap, const float* mask,
@@ -284,11 +283,6 @@ static cudaError_t launch(const CUtensorMap* tm, const void* wpack, const float*
 cudaError_t launch_conv2_tf32(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
                               int n1, int n2, float* h2, int num_sms, cudaStream_t st) {
   return launch<64, 32, EPI_BIAS_RELU>(tmH1, wpack, bias, fullmap, nullptr, batch, n1, n2, h2, num_sms, st);
-}
-
-cudaError_t launch_dgrad2_tf32(const CUtensorMap* tmDG, const void* wpack, const float* h1, int batch, int n1, int n2,
-                               float* dh1, int num_sms, cudaStream_t st) {
-  return launch<32, 64, EPI_MASK>(tmDG, wpack, nullptr, 0, h1, batch, n1, n2, dh1, num_sms, st);
 }
 
 cudaError_t launch_convg_tf32(int cin, int cout, const CUtensorMap* tmIn, const void* wpack, const float* bias,

@@ -266,13 +266,13 @@ __device__ __forceinline__ float wx_at(const float* __restrict__ W, int cin, int
 }
 
 __global__ void k_repack_tf32(const float* __restrict__ params, int flip, float* __restrict__ wp1,
-                              float* __restrict__ wp2t, float* __restrict__ wp3, float* __restrict__ wp2d,
-                              float* __restrict__ wpd3, uint16_t* __restrict__ wp2db) {
+                              float* __restrict__ wp2t, float* __restrict__ wp3, float* __restrict__ wpd3,
+                              uint16_t* __restrict__ wp2db) {
   constexpr int T = KS * KS, N1 = 64 * T, N2 = 32 * 64 * T;
   const float* W1 = params;
   const float* W2 = params + N1;
   const float* W3 = params + N1 + N2;
-  constexpr int E2 = 2 * 33 * 4096, E1 = 11 * 1024, E3 = 22 * 512, E4 = DG2_KBLOCKS * 4096, E5 = 11 * 1024;
+  constexpr int E2 = 2 * 33 * 4096, E1 = 11 * 1024, E3 = 22 * 512, E4 = 0, E5 = 11 * 1024;
   constexpr int E6 = DG2_KBLOCKS * 4096;   // bf16 layer-2 dgrad blocks: 66 x (128 rows x 32 co x 2 B), SWIZZLE_64B
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E2 + E1 + E3 + E4 + E5 + E6; e += gridDim.x * blockDim.x) {
     if (e >= E2 + E1 + E3 + E4 + E5) {
@@ -306,19 +306,13 @@ __global__ void k_repack_tf32(const float* __restrict__ params, int flip, float*
       const int v = (((r / 16) ^ ((m >> 1) & 3)) * 4) + (r % 16) / 4;
       const int grp = m / 16, j = m % 16, f = 16 * grp + (j < 8 ? 2 * j : 2 * (j - 8) + 1);
       wpd3[i] = (v < KS && f < 32) ? wx_at(W3, 32, 0, f, KS - 1 - u, KS - 1 - v, flip) : 0.f;
-    } else if (wp2d) {                // layer-2 dgrad: [u*6 + j] blocks of (v' x 64 ci) rows x 32 co, SWIZZLE_128B,
-      const int i = e - E2 - E1 - E3; //   A[v'*64 + ci][co] = wx2[co][ci][10-u][10-(2j+v')]
-      const int blk = i / 4096, u = blk / 6, j = blk % 6, o = (i % 4096) * 4, row = o / 128, r = o % 128;
-      const int co = (((r / 16) ^ (row & 7)) * 4) + (r % 16) / 4;
-      const int b = 2 * j + row / 64, ci = row % 64;
-      wp2d[i] = b < KS ? wx_at(W2, 64, co, ci, KS - 1 - u, KS - 1 - b, flip) : 0.f;
     }
   }
 }
 
-cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wp2d,
-                               float* wpd3, void* wp2db, cudaStream_t st) {
-  k_repack_tf32<<<592, 256, 0, st>>>(params, flip, wp1, wp2t, wp3, wp2d, wpd3, reinterpret_cast<uint16_t*>(wp2db));
+cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wpd3,
+                               void* wp2db, cudaStream_t st) {
+  k_repack_tf32<<<592, 256, 0, st>>>(params, flip, wp1, wp2t, wp3, wpd3, reinterpret_cast<uint16_t*>(wp2db));
   return cudaGetLastError();
 }
 

@@ -101,14 +101,11 @@ cudaError_t launch_dgrad2_f32(const float* dh2, const float* wt2, const float* h
                               int n2, cudaStream_t st);
 cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, int n1, int n2, float* part_w,
                          float* part_b, int flip, float* gw, float* gb, cudaStream_t st);
-cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wp2d,
-                               float* wpd3, void* wp2db, cudaStream_t st);
+cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wpd3,
+                               void* wp2db, cudaStream_t st);
 cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const void* h1b, int batch, int n1, int n2,
                                void* dh1b, int num_sms, cudaStream_t st);
-// training, TF32 contexts: layer-2 data gradient on tcgen05 (k_conv2_tf32.cu); wpack = 66 blocks of 16 KB
-cudaError_t setup_dgrad2_tf32(int n2);
-cudaError_t launch_dgrad2_tf32(const CUtensorMap* tmDG, const void* wpack, const float* h1, int batch, int n1, int n2,
-                               float* dh1, int num_sms, cudaStream_t st);
+// training: layer-2 data gradient on the bf16 layer-2 kernel (k_conv2_tc.cu); wpack = 66 blocks of 8 KB
 constexpr int DG2_KBLOCKS = 66;
 // training, TF32 contexts: layer-3 data gradient as a 1 -> 32 TF32 conv on the conv1 machinery (k_conv13_tc.cu);
 // tmDX: the conv1 x_tilde tensor map over dG3; wpack: 11 x 4096 B (conv1 TF32 layout)
