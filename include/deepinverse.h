@@ -146,8 +146,12 @@ di_status di_add_noise(di_ctx ctx, void* y, long long ldy, int batch, double snr
                        void* stream);
 di_status di_metrics(di_ctx ctx, const float* xhat, const float* x, int batch, double* out, void* stream);
 
-/* ---- Training step (FP32 or TF32 contexts with per-channel or zero biases) ----------------
- * TF32 contexts run the forward on the TF32 tensor-core kernels (backward kernels are fp32 SIMT in both).
+/* ---- Training step (contexts of the paper's stack with per-channel or zero biases) ----------
+ * FP32 contexts: SIMT forward and backward (fp32 products).  TF32 contexts: TF32 tensor-core forward; backward on the
+ * tensor cores with bf16 operands for the layer-2 data / weight gradients and the thin-layer weight gradients, TF32
+ * for the layer-3 data gradient.  BF16 contexts: the bf16 forward (weights = RNE-rounded fp32 master parameters),
+ * the same tensor-core backward; BF16 training needs n2 % 4 == 0 (DI_ERR_ARG otherwise).  Gradients and the
+ * parameters stay fp32.
  * Parameter vector layout (di_num_params() = 259 521 floats), the orientation given to di_create (true convolution,
  * or cross-correlation with DI_FLAG_XCORR):  [W1 64x1x11x11 | W2 32x64x11x11 | W3 1x32x11x11 | b1 64 | b2 32 | b3 1].
  * di_train_grad: forward on the context's current parameters, loss L = scale * sum_b ||x_hat_b - x_b||^2 (

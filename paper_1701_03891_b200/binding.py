@@ -318,11 +318,14 @@ class DeepInverse:
         di_metrics(self.ctx, xhat, x, b, out, stream)
         return out.cpu().numpy()
 
-    # ------------------------------------------------------------ training (FP32 contexts, NEXT-2)
+    # ------------------------------------------------------------ training (NEXT-2; paper stack, per-channel biases)
     def train_grad(self, y, x, scale=None, grads=None, stream=None):
         """Loss scale * sum ||M(y) - x||^2 (scale defaults to 1/batch) and its gradient (device fp32
-        [di_num_params()]).  Returns (loss tensor (device, float64 [1]), grads)."""
+        [di_num_params()]).  y: device [B][ldy] of the storage dtype; x: device fp32 [B][n1][n2].
+        Returns (loss tensor (device, float64 [1]), grads)."""
         import torch
+        if y.dtype != self.storage_dtype or not y.is_cuda:
+            raise TypeError(f"y must be a CUDA {self.storage_dtype} tensor")
         b = y.shape[0]
         if grads is None:
             grads = torch.empty(di_num_params(), dtype=torch.float32, device=y.device)

@@ -844,7 +844,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     STEP(upload_bias(&c->b1, a->b1, C1, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b2, a->b2, C2, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b3, a->b3, 1, fm, a->n1, a->n2, &c->ws_bytes));
-    if ((c->prec == DI_PREC_FP32 || c->prec == DI_PREC_TF32) && !fm) {   // trainable: parameters, API orientation
+    if (!fm) {   // trainable: fp32 master parameters in the API orientation
       std::vector<float> prm(di::N_PARAMS, 0.f);
       const size_t n1w = (size_t)C1 * K * K, n2w = (size_t)C2 * C1 * K * K, n3w = (size_t)C2 * K * K;
       std::memcpy(prm.data(), a->w1, n1w * 4);
@@ -1104,6 +1104,19 @@ di_status di_metrics(di_ctx c, const float* xhat, const float* x, int batch, dou
 }
 
 // ---------------------------------------------------------------------------------------------- training
+// the tensor-core weight images from the parameters: the forward's (TF32 fp32 images or BF16 bf16 images) and the
+// backward's (layer-3 dgrad bank, bf16 layer-2 dgrad blocks)
+static cudaError_t repack_tc(di_ctx c, cudaStream_t st) {
+  const int flip = !(c->flags & DI_FLAG_XCORR);
+  if (c->prec == DI_PREC_BF16) {
+    cudaError_t e = di::launch_repack_tf32(c->params, flip, nullptr, nullptr, nullptr, c->wpd3, c->wp2db, st);
+    if (e != cudaSuccess) return e;
+    return di::launch_repack_bf16(c->params, flip, c->wp1, c->wp2, c->wp3, st);
+  }
+  return di::launch_repack_tf32(c->params, flip, reinterpret_cast<float*>(c->wp1), reinterpret_cast<float*>(c->wp2t),
+                                reinterpret_cast<float*>(c->wp3), c->wpd3, c->wp2db, st);
+}
+
 static di_status train_alloc(di_ctx c) {
   if (c->dxh) return DI_OK;
   const size_t B = (size_t)c->max_batch, N = (size_t)c->N;
@@ -1127,14 +1140,16 @@ static di_status train_alloc(di_ctx c) {
   // backward layouts (and the forward ones, identical to di_create's) from the parameters
   CUDA_TRY(di::launch_sgd_repack(c->params, nullptr, c->vel, di::N_PARAMS, 0.f, 0.f, !(c->flags & DI_FLAG_XCORR),
                                  c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2, c->b3, 0));
-  if (c->prec == DI_PREC_TF32) {
+  if (c->prec != DI_PREC_FP32) {
+    const bool bf = c->prec == DI_PREC_BF16;
     CUDA_TRY(di::setup_conv2_tc(c->n2));   // the bf16 layer-2 kernel also runs the layer-2 data gradient
-    if ((s = al(&c->h1b, B * N * C1 * 2)) != DI_OK) return s;
+    if (!bf && (s = al(&c->h1b, B * N * C1 * 2)) != DI_OK) return s;   // (BF16: h1 itself is bf16)
     if ((s = al(&c->dg2b, B * N * C2 * 2)) != DI_OK) return s;
     if ((s = al(&c->dh1b, B * N * C1 * 2)) != DI_OK) return s;
     if ((s = al(&c->part_w2, std::max(di::wgrad2_tc_part_floats(c->num_sms), di::wgrad13_tc_part_floats(c->num_sms)) * 4)) != DI_OK)
       return s;
-    if ((s = encode_wg2(&c->tmH1b, c->h1b, c->max_batch, c->n1, c->n2, 64, di::wgrad2_tc_h_box_rows())) != DI_OK)
+    if ((s = encode_wg2(&c->tmH1b, bf ? c->h1 : c->h1b, c->max_batch, c->n1, c->n2, 64, di::wgrad2_tc_h_box_rows())) !=
+        DI_OK)
       return s;
     if ((s = encode_wg2(&c->tmDG2b, c->dg2b, c->max_batch, c->n1, c->n2, 32, di::wgrad2_tc_g_box_rows())) != DI_OK)
       return s;
@@ -1147,8 +1162,7 @@ static di_status train_alloc(di_ctx c) {
       if ((s = encode_xt(&c->tmDX, c->dxh, c->max_batch, c->n1, c->n2, true)) != DI_OK) return s;
       c->has_tmDX = true;
     }
-    CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
-                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wpd3, c->wp2db, 0));
+    CUDA_TRY(repack_tc(c, 0));
   }
   CUDA_TRY(cudaDeviceSynchronize());
   return DI_OK;
@@ -1157,8 +1171,9 @@ static di_status train_alloc(di_ctx c) {
 static di_status train_check(di_ctx c) {
   if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
   if (!c->stack.empty()) return fail(DI_ERR_ARG, "training is implemented for the paper's three-layer stack");
-  if ((c->prec != DI_PREC_FP32 && c->prec != DI_PREC_TF32) || !c->params)
-    return fail(DI_ERR_ARG, "training needs a DI_PREC_FP32 or DI_PREC_TF32 context with per-channel (or zero) biases");
+  if (!c->params) return fail(DI_ERR_ARG, "training needs a context with per-channel (or zero) biases");
+  if (c->prec == DI_PREC_BF16 && c->n2 % 4 != 0)
+    return fail(DI_ERR_ARG, "BF16 training needs n2 %% 4 == 0 (the layer-3 data gradient's strip map)");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
   if (!c->b1 || !c->b2 || !c->b3) {   // trainable biases need storage even when created zero
     if (!c->b1) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->b1), C1 * 4));
@@ -1189,35 +1204,37 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   const float* xt = reinterpret_cast<const float*>(c->xt);
   const float* h1 = reinterpret_cast<const float*>(c->h1);
   const float* h2 = reinterpret_cast<const float*>(c->h2);
-  const bool tc = c->prec == DI_PREC_TF32;   // tensor-core backward (k_conv2_tc<32, 64>, k_wgrad*_tc, dgrad3)
+  const bool tc = c->prec != DI_PREC_FP32;   // tensor-core backward (k_conv2_tc<32, 64>, k_wgrad*_tc, dgrad3)
+  const bool bf = c->prec == DI_PREC_BF16;   // BF16 contexts: x_tilde, h1, h2 are bf16
   if (tc)
-    CUDA_TRY(di::launch_wgrad3_tc(h2, c->dxh, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads + n1w + n2w,
-                                  gb + C1 + C2, c->num_sms, st));
+    CUDA_TRY(di::launch_wgrad3_tc(c->h2, c->dxh, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads + n1w + n2w,
+                                  gb + C1 + C2, c->num_sms, st, bf));
   else
     CUDA_TRY(di::launch_wgrad(3, h2, c->dxh, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w + n2w,
                               gb + C1 + C2, st));
   if (tc && c->has_tmDX)
-    CUDA_TRY(di::launch_dgrad3_tf32(&c->tmDX, c->wpd3, h2, c->dh2, batch, c->n1, c->n2, c->num_sms, st));
+    CUDA_TRY(di::launch_dgrad3_tf32(&c->tmDX, c->wpd3, c->h2, c->dh2, batch, c->n1, c->n2, c->num_sms, st, bf));
   else
     CUDA_TRY(di::launch_dgrad3_f32(c->dxh, c->wt3, h2, c->dh2, batch, c->n1, c->n2, st));
   if (tc) {   // bf16 operands, tcgen05 MN-major contraction over pixels (k_wgrad2_tc.cu)
     const size_t npix = (size_t)batch * c->N;
     CUDA_TRY(di::launch_dg2_bf16(c->dh2, npix, c->dg2b, c->part_b, st));
     CUDA_TRY(di::launch_bias_reduce(c->part_b, di::WGRAD_CHUNKS, C2, gb + C1, st));
-    CUDA_TRY(di::launch_to_bf16(h1, c->h1b, npix * C1, st));
+    if (!bf) CUDA_TRY(di::launch_to_bf16(h1, c->h1b, npix * C1, st));   // (BF16: h1 is the bf16 operand)
     CUDA_TRY(di::launch_wgrad2_tc(&c->tmH1b, &c->tmDG2b, batch, c->n1, c->n2, c->part_w2, flip, grads + n1w,
                                   c->num_sms, st));
   } else {
     CUDA_TRY(di::launch_wgrad(2, h1, c->dh2, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w, gb + C1,
                               st));
   }
-  if (c->prec == DI_PREC_TF32)   // bf16 operands from the dG2 copy made for wgrad2: twice the TF32 MMA rate
-    CUDA_TRY(di::launch_dgrad2_bf16(&c->tmDG2s, c->wp2db, c->h1b, batch, c->n1, c->n2, c->dh1b, c->num_sms, st));
+  if (tc)   // bf16 operands from the dG2 copy made for wgrad2: twice the TF32 MMA rate
+    CUDA_TRY(di::launch_dgrad2_bf16(&c->tmDG2s, c->wp2db, bf ? c->h1 : c->h1b, batch, c->n1, c->n2, c->dh1b,
+                                    c->num_sms, st));
   else
     CUDA_TRY(di::launch_dgrad2_f32(c->dh2, c->wt2, h1, c->dh1, batch, c->n1, c->n2, st));
   if (tc)
-    CUDA_TRY(di::launch_wgrad1_tc(xt, c->dh1b, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads, gb,
-                                  c->num_sms, st));
+    CUDA_TRY(di::launch_wgrad1_tc(c->xt, c->dh1b, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads, gb,
+                                  c->num_sms, st, bf));
   else
     CUDA_TRY(di::launch_wgrad(1, xt, c->dh1, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads, gb, st));
   return DI_OK;
@@ -1231,10 +1248,7 @@ di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, 
   CUDA_TRY(di::launch_sgd_repack(c->params, grads, c->vel, di::N_PARAMS, (float)lr, (float)momentum,
                                  !(c->flags & DI_FLAG_XCORR), c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2,
                                  c->b3, reinterpret_cast<cudaStream_t>(stream)));
-  if (c->prec == DI_PREC_TF32)
-    CUDA_TRY(di::launch_repack_tf32(c->params, !(c->flags & DI_FLAG_XCORR), reinterpret_cast<float*>(c->wp1),
-                                    reinterpret_cast<float*>(c->wp2t), reinterpret_cast<float*>(c->wp3), c->wpd3,
-                                    c->wp2db, reinterpret_cast<cudaStream_t>(stream)));
+  if (c->prec != DI_PREC_FP32) CUDA_TRY(repack_tc(c, reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }
 

@@ -392,7 +392,7 @@ template <int COUT, bool DG3>
 __global__ void __launch_bounds__(384, 1)
     k_conv1_tf32(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ w1pack,
                  const float* __restrict__ bias, int fullmap, Geo13 g, float* __restrict__ h1,
-                 const float* __restrict__ mask) {
+                 const void* __restrict__ mask, int mask_bf16) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* wbuf = smem;                                 // 44 KB
@@ -538,7 +538,23 @@ __global__ void __launch_bounds__(384, 1)
                 ok[kk] = ok[kk] && c0 + cc < g.n2;
                 pixv[kk] = pix0 + (size_t)rr * g.n2 + cc;
               }
-              m[kk] = ok[kk] ? __ldg(reinterpret_cast<const float2*>(mask + pixv[kk] * 32 + ch)) : make_float2(0.f, 0.f);
+            }
+            if (mask_bf16) {   // BF16 contexts: h2 is bf16 (branch hoisted so the 8 loads issue back to back)
+              uint32_t mb[8];
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                mb[kk] = ok[kk] ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const __nv_bfloat16*>(mask) +
+                                                                         pixv[kk] * 32 + ch))
+                                : 0u;
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                m[kk] = make_float2(__uint_as_float(mb[kk] << 16), __uint_as_float(mb[kk] & 0xffff0000u));
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                m[kk] = ok[kk] ? __ldg(reinterpret_cast<const float2*>(reinterpret_cast<const float*>(mask) +
+                                                                       pixv[kk] * 32 + ch))
+                               : make_float2(0.f, 0.f);
             }
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
@@ -811,7 +827,7 @@ cudaError_t launch_conv1_tf32(const CUtensorMap* tmX, const void* w1pack, const 
   Geo13 g = make_geo13(batch, n1, n2, R1T, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
   k_conv1_tf32<64, false><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack),
-                                                                      bias, fullmap, g, h1, nullptr);
+                                                                      bias, fullmap, g, h1, nullptr, 0);
   return cudaGetLastError();
 }
 
@@ -822,16 +838,16 @@ cudaError_t launch_conv1g_tf32(int cout, const CUtensorMap* tmX, const void* w1p
   Geo13 g = make_geo13(batch, n1, n2, R1T, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
   k_conv1_tf32<32, false><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack),
-                                                                      bias, 0, g, out, nullptr);
+                                                                      bias, 0, g, out, nullptr, 0);
   return cudaGetLastError();
 }
 
-cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const float* h2, float* dh2, int batch,
-                               int n1, int n2, int num_sms, cudaStream_t st) {
+cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const void* h2, float* dh2, int batch,
+                               int n1, int n2, int num_sms, cudaStream_t st, bool h2_bf16) {
   Geo13 g = make_geo13(batch, n1, n2, R1T, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
   k_conv1_tf32<32, true><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmDX, reinterpret_cast<const uint8_t*>(wpack),
-                                                                     nullptr, 0, g, dh2, h2);
+                                                                     nullptr, 0, g, dh2, h2, h2_bf16 ? 1 : 0);
   return cudaGetLastError();
 }
 

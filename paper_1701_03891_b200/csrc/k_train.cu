@@ -286,16 +286,19 @@ __global__ void k_repack_tf32(const float* __restrict__ params, int flip, float*
       continue;
     }
     if (e < E2) {                     // conv2: [h][kb] blocks of 128 rows x 32 ch, SWIZZLE_128B
+      if (!wp2t) continue;
       const int blk = e / 4096, o = (e % 4096) * 4, row = o / 128, r = o % 128;
       const int c = (((r / 16) ^ (row & 7)) * 4) + (r % 16) / 4;
       const int h = blk / 33, kb = blk % 33, u = kb / 3, b = 4 * (kb % 3) + row / 32, k = row % 32;
       wp2t[e] = b < KS ? wx_at(W2, 64, k, 32 * h + c, u, b, flip) : 0.f;
     } else if (e < E2 + E1) {         // conv1: [u] blocks of 64 permuted filters x 16 taps, SWIZZLE_64B
+      if (!wp1) continue;
       const int i = e - E2, u = i / 1024, o = (i % 1024) * 4, m = o / 64, r = o % 64;
       const int v = (((r / 16) ^ ((m >> 1) & 3)) * 4) + (r % 16) / 4;
       const int grp = m / 16, j = m % 16, f = 16 * grp + (j < 8 ? 2 * j : 2 * (j - 8) + 1);
       wp1[i] = v < KS ? wx_at(W1, 1, f, 0, u, v, flip) : 0.f;
     } else if (e < E2 + E1 + E3) {    // conv3: [h*11 + u] blocks of 32 rows (taps v) x 16 ch, SWIZZLE_64B
+      if (!wp3) continue;
       const int i = e - E2 - E1, blk = i / 512, h = blk / 11, u = blk % 11, o = (i % 512) * 4, row = o / 64,
                 r = o % 64;
       const int c = (((r / 16) ^ ((row >> 1) & 3)) * 4) + (r % 16) / 4;
@@ -308,6 +311,41 @@ __global__ void k_repack_tf32(const float* __restrict__ params, int flip, float*
       wpd3[i] = (v < KS && f < 32) ? wx_at(W3, 32, 0, f, KS - 1 - u, KS - 1 - v, flip) : 0.f;
     }
   }
+}
+
+// BF16 contexts: the bf16 forward images (api.cu conv1_tc_pack / conv2_tc_pack / conv3_tc_pack), RNE-rounded
+__device__ __forceinline__ uint16_t bfbits(float v) { return __bfloat16_as_ushort(__float2bfloat16_rn(v)); }
+
+__global__ void k_repack_bf16(const float* __restrict__ params, int flip, uint16_t* __restrict__ wp1,
+                              uint16_t* __restrict__ wp2, uint16_t* __restrict__ wp3) {
+  constexpr int T = KS * KS, N1 = 64 * T, N2 = 32 * 64 * T;
+  const float* W1 = params;
+  const float* W2 = params + N1;
+  const float* W3 = params + N1 + N2;
+  constexpr int E2 = 33 * 8192, E1 = 11 * 1024, E3 = 11 * 1024;   // bf16 elements per image
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E2 + E1 + E3; e += gridDim.x * blockDim.x) {
+    if (e < E2) {                     // conv2: block u*3 + j, row v'*32 + k, 64 ci (128 B), SWIZZLE_128B
+      const int kb = e / 8192, o = (e % 8192) * 2, row = o / 128, r = o % 128;
+      const int ci = (((r / 16) ^ (row & 7)) * 8) + (r % 16) / 2;
+      const int u = kb / 3, b = 4 * (kb % 3) + row / 32, k = row % 32;
+      wp2[e] = bfbits(b < KS ? wx_at(W2, 64, k, ci, u, b, flip) : 0.f);
+    } else if (e < E2 + E1) {         // conv1: block u, row m (permuted filter), 16 taps (32 B), SWIZZLE_32B
+      const int i = e - E2, u = i / 1024, o = (i % 1024) * 2, m = o / 32, r = o % 32;
+      const int v = (((r / 16) ^ ((m >> 2) & 1)) * 8) + (r % 16) / 2;
+      const int grp = m / 16, j = m % 16, f = 16 * grp + (j < 8 ? 2 * j : 2 * (j - 8) + 1);
+      wp1[i] = bfbits(v < KS ? wx_at(W1, 1, f, 0, u, v, flip) : 0.f);
+    } else {                          // conv3: block u, row r (tap v = r), 32 ch (64 B), SWIZZLE_64B
+      const int i = e - E2 - E1, u = i / 1024, o = (i % 1024) * 2, row = o / 64, r = o % 64;
+      const int c = (((r / 16) ^ ((row >> 1) & 3)) * 8) + (r % 16) / 2;
+      wp3[i] = bfbits(row < KS ? wx_at(W3, 32, 0, c, u, row, flip) : 0.f);
+    }
+  }
+}
+
+cudaError_t launch_repack_bf16(const float* params, int flip, void* wp1, void* wp2, void* wp3, cudaStream_t st) {
+  k_repack_bf16<<<592, 256, 0, st>>>(params, flip, reinterpret_cast<uint16_t*>(wp1), reinterpret_cast<uint16_t*>(wp2),
+                                     reinterpret_cast<uint16_t*>(wp3));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wpd3,

@@ -55,8 +55,8 @@ __host__ __device__ inline int l3_nb(int P) { return R * P + 32; }
 
 // =============================================================================================== layer 1
 __global__ void __launch_bounds__(128, 1)
-    k_wgrad1_tc(const float* __restrict__ xt, const __nv_bfloat16* __restrict__ dg1, GeoT13 g,
-                float* __restrict__ part, float* __restrict__ part_b) {
+    k_wgrad1_tc(const void* __restrict__ xt, const __nv_bfloat16* __restrict__ dg1, GeoT13 g,
+                float* __restrict__ part, float* __restrict__ part_b, int xbf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xs = reinterpret_cast<float*>(smem + 2 * g.stage);
@@ -124,8 +124,11 @@ __global__ void __launch_bounds__(128, 1)
       for (int uu = 0; uu < 8; ++uu) {
         const int q = q0 + uu * 128, row = q / P, col = q - row * P;
         const int gr = r0 - 5 + row, gc = c0 - 5 + col;
+        const size_t xi = ((size_t)b * g.n1 + gr) * g.n2 + gc;
         v[uu] = (q < NX && gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2)
-                    ? __ldg(xt + ((size_t)b * g.n1 + gr) * g.n2 + gc) : 0.f;
+                    ? (xbf ? __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(xt) + xi))
+                           : __ldg(reinterpret_cast<const float*>(xt) + xi))
+                    : 0.f;
       }
 #pragma unroll
       for (int uu = 0; uu < 8; ++uu)
@@ -203,8 +206,8 @@ __global__ void k_wgrad1_reduce(const float* __restrict__ part, const float* __r
 
 // =============================================================================================== layer 3
 __global__ void __launch_bounds__(128, 1)
-    k_wgrad3_tc(const float* __restrict__ h2, const float* __restrict__ dg3, GeoT13 g, float* __restrict__ part,
-                float* __restrict__ part_b) {
+    k_wgrad3_tc(const void* __restrict__ h2, const float* __restrict__ dg3, GeoT13 g, float* __restrict__ part,
+                float* __restrict__ part_b, int hbf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* ds = reinterpret_cast<float*>(smem + 2 * g.stage) + 16;   // ds[-16 .. NB + 16)
@@ -244,24 +247,28 @@ __global__ void __launch_bounds__(128, 1)
     // h2 strip with halo: q -> h2(r0 - 5 + q / P, c0 - 5 + q % P), bf16 SW64 (chunk c at c ^ ((q >> 1) & 3))
     constexpr int U = 4;
     for (int i0 = tid; i0 < NH * 4; i0 += 128 * U) {
-      float4 v[U][2];
+      uint4 w[U];   // 8 channels of one position as bf16
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int i = i0 + uu * 128, q = i >> 2, c = i & 3, row = q / P, col = q - row * P;
         const int gr = r0 - 5 + row, gc = c0 - 5 + col;
-        v[uu][0] = v[uu][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        w[uu] = make_uint4(0, 0, 0, 0);
         if (i < NH * 4 && gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2) {
-          const float4* src = reinterpret_cast<const float4*>(h2 + (((size_t)b * g.n1 + gr) * g.n2 + gc) * 32 + 8 * c);
-          v[uu][0] = __ldg(src), v[uu][1] = __ldg(src + 1);
+          const size_t off = (((size_t)b * g.n1 + gr) * g.n2 + gc) * 32 + 8 * c;
+          if (hbf) {
+            w[uu] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(h2) + off));
+          } else {
+            const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(h2) + off);
+            const float4 v0 = __ldg(src), v1 = __ldg(src + 1);
+            w[uu] = make_uint4(pack2(v0.x, v0.y), pack2(v0.z, v0.w), pack2(v1.x, v1.y), pack2(v1.z, v1.w));
+          }
         }
       }
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
         const int i = i0 + uu * 128, q = i >> 2, c = i & 3;
         if (i >= NH * 4) break;
-        const float4 v0 = v[uu][0], v1 = v[uu][1];
-        *reinterpret_cast<uint4*>(hs + (16 + q) * 64 + ((c ^ ((q >> 1) & 3)) << 4)) =
-            make_uint4(pack2(v0.x, v0.y), pack2(v0.z, v0.w), pack2(v1.x, v1.y), pack2(v1.z, v1.w));
+        *reinterpret_cast<uint4*>(hs + (16 + q) * 64 + ((c ^ ((q >> 1) & 3)) << 4)) = w[uu];
       }
     }
     // dG3 of the unit's own pixels (zero elsewhere): ds[p], p -> (r0 + p / P, c0 + p % P)
@@ -386,21 +393,21 @@ cudaError_t setup_wgrad13_tc(int n2) {
   return cudaFuncSetAttribute(k_wgrad3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(n2, false));
 }
 
-cudaError_t launch_wgrad1_tc(const float* xt, const void* dg1, int batch, int n1, int n2, float* part, float* part_b,
-                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st) {
+cudaError_t launch_wgrad1_tc(const void* xt, const void* dg1, int batch, int n1, int n2, float* part, float* part_b,
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool xt_bf16) {
   GeoT13 g = make_geo(batch, n1, n2, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
   k_wgrad1_tc<<<grid, 128, smem_bytes(n2, true), st>>>(xt, reinterpret_cast<const __nv_bfloat16*>(dg1), g, part,
-                                                       part_b);
+                                                       part_b, xt_bf16 ? 1 : 0);
   k_wgrad1_reduce<<<(64 * KS * KS + 64 + 255) / 256, 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
   return cudaGetLastError();
 }
 
-cudaError_t launch_wgrad3_tc(const float* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
-                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st) {
+cudaError_t launch_wgrad3_tc(const void* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool h2_bf16) {
   GeoT13 g = make_geo(batch, n1, n2, false);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_wgrad3_tc<<<grid, 128, smem_bytes(n2, false), st>>>(h2, dg3, g, part, part_b);
+  k_wgrad3_tc<<<grid, 128, smem_bytes(n2, false), st>>>(h2, dg3, g, part, part_b, h2_bf16 ? 1 : 0);
   k_wgrad3_reduce<<<(32 * KS * KS + 1 + 255) / 256, 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
   return cudaGetLastError();
 }

@@ -103,6 +103,7 @@ cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, 
                          float* part_b, int flip, float* gw, float* gb, cudaStream_t st);
 cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wpd3,
                                void* wp2db, cudaStream_t st);
+cudaError_t launch_repack_bf16(const float* params, int flip, void* wp1, void* wp2, void* wp3, cudaStream_t st);
 cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const void* h1b, int batch, int n1, int n2,
                                void* dh1b, int num_sms, cudaStream_t st);
 // training: layer-2 data gradient on the bf16 layer-2 kernel (k_conv2_tc.cu); wpack = 66 blocks of 8 KB
@@ -115,8 +116,8 @@ cudaError_t launch_conv1g_tf32(int cout, const CUtensorMap* tmX, const void* w1p
 // custom stacks, FP32 SIMT: (cin, cout) in {(1,32), (1,64), (32,32), (32,64), (64,32), (64,64)}, bias + ReLU
 cudaError_t launch_convg_simt(int cin, int cout, const float* in, const float* wx, const float* bias, float* out,
                               int batch, int n1, int n2, cudaStream_t st);
-cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const float* h2, float* dh2, int batch,
-                               int n1, int n2, int num_sms, cudaStream_t st);
+cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const void* h2, float* dh2, int batch,
+                               int n1, int n2, int num_sms, cudaStream_t st, bool h2_bf16 = false);
 // training, TF32 contexts: layer-2 weight gradient on tcgen05 from bf16 copies of h1 / dG2 (k_wgrad2_tc.cu)
 constexpr int WG2_ROWS = 6;
 size_t wgrad2_tc_smem_bytes(int n2);
@@ -133,10 +134,11 @@ constexpr int WG13_ROWS = 6;
 size_t wgrad13_tc_part_floats(int num_sms);
 cudaError_t setup_wgrad13_tc(int n2);
 // dg1: [B][N][64] bf16 (the bf16 dgrad2 output)
-cudaError_t launch_wgrad1_tc(const float* xt, const void* dg1, int batch, int n1, int n2, float* part, float* part_b,
-                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st);
-cudaError_t launch_wgrad3_tc(const float* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
-                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st);
+// xt / h2: fp32, or bf16 when xt_bf16 / h2_bf16 (BF16 contexts)
+cudaError_t launch_wgrad1_tc(const void* xt, const void* dg1, int batch, int n1, int n2, float* part, float* part_b,
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool xt_bf16 = false);
+cudaError_t launch_wgrad3_tc(const void* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool h2_bf16 = false);
 cudaError_t launch_bias_reduce(const float* part_b, int nchunk, int nb, float* gb, cudaStream_t st);
 cudaError_t launch_sgd_repack(float* params, const float* grads, float* vel, int n, float lr, float momentum, int flip,
                               float* wx1, float* wx2, float* wx3, float* wt2, float* wt3, float* b1, float* b2,

@@ -11,14 +11,14 @@ pytestmark = pytest.mark.gpu
 
 # fp32 forward (<= 1e-5) and fp32 gradient sums (per 256-pixel tile in fp32, then fp64 across tiles); TF32: the
 # forward's 10-bit-mantissa products (the 2e-2 bar of the TF32 path)
-TOL_GRAD = {"f32": 1e-4, "tf32": 2e-2}
+TOL_GRAD = {"f32": 1e-4, "tf32": 2e-2, "bf16": 2e-2}
 
 
 def _grads_ok(ctx, case, scale=None, final_relu=False, xcorr=False):
     tol = TOL_GRAD[case.precision]
     import torch
     from paper_1701_03891_b200 import split_params
-    y = torch.from_numpy(case.y).cuda()
+    y = torch.from_numpy(case.y).cuda().to(ctx.storage_dtype)
     x = torch.from_numpy(case.x).cuda()
     loss, g = ctx.train_grad(y, x, scale)
     torch.cuda.synchronize()
@@ -42,6 +42,23 @@ def test_gradients_match_oracle(precision, n1, n2, m, batch):
     _grads_ok(make_ctx(case), case)
 
 
+@pytest.mark.parametrize("n1,n2,m,batch", [(16, 16, 64, 4), (40, 72, 300, 3), (64, 64, 410, 4)])
+def test_gradients_match_oracle_bf16(n1, n2, m, batch):
+    """BF16 contexts train on the bf16 forward (x_tilde, h1, h2 stored in bf16) and the bf16 / TF32 tensor-core
+    backward; the oracle runs on the same bf16-rounded Phi, y and Omega."""
+    case = Case(n1, n2, m, batch, "bf16", 6, 3, bias="channel")
+    _grads_ok(make_ctx(case), case)
+
+
+def test_bf16_training_needs_n2_multiple_of_4():
+    import torch
+    from paper_1701_03891_b200 import DiError
+    case = Case(9, 13, 40, 2, "bf16", 6, 3, bias="channel")
+    ctx = make_ctx(case)
+    with pytest.raises(DiError):
+        ctx.train_grad(torch.from_numpy(case.y).cuda().to(torch.bfloat16), torch.from_numpy(case.x).cuda())
+
+
 @pytest.mark.parametrize("final_relu,xcorr", [(True, False), (False, True)])
 def test_gradients_flags(final_relu, xcorr):
     from paper_1701_03891_b200 import DI_FLAG_FINAL_RELU, DI_FLAG_XCORR
@@ -50,12 +67,12 @@ def test_gradients_flags(final_relu, xcorr):
     _grads_ok(make_ctx(case, flags=flags), case, final_relu=final_relu, xcorr=xcorr)
 
 
-@pytest.mark.parametrize("precision", ["f32", "tf32"])
+@pytest.mark.parametrize("precision", ["f32", "tf32", "bf16"])
 def test_sgd_updates_the_forward_and_lowers_the_loss(precision):
     import torch
     case = Case(32, 32, 256, 8, precision, 6, 3, bias="channel")
     ctx = make_ctx(case)
-    y = torch.from_numpy(case.y).cuda()
+    y = torch.from_numpy(case.y).cuda().to(ctx.storage_dtype)
     x = torch.from_numpy(case.x).cuda()
     losses, lr = [], None
     for _ in range(6):
@@ -67,6 +84,8 @@ def test_sgd_updates_the_forward_and_lowers_the_loss(precision):
     assert all(np.isfinite(losses)) and losses[-1] < 0.9 * losses[0], losses
     # the updated parameters drive the forward: GPU recovery == oracle forward with the read-back parameters
     ws, bs = ctx.params()
+    if precision == "bf16":   # BF16 contexts run the forward on the RNE-rounded fp32 master weights (deepinverse.h)
+        ws = [synth.round_bf16(w) for w in ws]
     p = synth.Params([w.astype(np.float64) for w in ws], [b.astype(np.float64) for b in bs])
     out = ctx.recover(y).cpu().numpy()
     ref = oracle.forward(case.y, case.phi, p, case.n1, case.n2)
@@ -80,13 +99,13 @@ def test_sgd_updates_the_forward_and_lowers_the_loss(precision):
     assert np.allclose(after, before - np.float32(1e-3) * g.cpu().numpy(), rtol=0, atol=1e-7)
 
 
-def test_training_rejects_non_fp32_contexts():
+def test_training_rejects_fullmap_bias_contexts():
     import torch
     from paper_1701_03891_b200 import DiError
-    case = Case(16, 16, 64, 2, "bf16")
+    case = Case(16, 16, 64, 2, "f32", bias="fullmap")
     ctx = make_ctx(case)
     with pytest.raises(DiError):
-        ctx.train_grad(torch.from_numpy(case.y).cuda().to(torch.bfloat16), torch.from_numpy(case.x).cuda())
+        ctx.train_grad(torch.from_numpy(case.y).cuda(), torch.from_numpy(case.x).cuda())
 
 
 @pytest.mark.parametrize("final_relu,xcorr", [(True, False), (False, True)])

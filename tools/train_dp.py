@@ -2,7 +2,7 @@
 scale = 1/global_batch (di_train_grad), the gradients are summed across ranks with one NCCL all-reduce (the only
 collective of the method), and every rank applies the same SGD step (di_sgd_step).  Prints per-step device times.
 
-  python tools/train_dp.py [steps] [batch_per_rank] [config] [f32|tf32]
+  python tools/train_dp.py [steps] [batch_per_rank] [config] [f32|tf32|bf16]
   torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/train_dp.py ..."""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -21,11 +21,12 @@ dev = torch.device("cuda", local)
 if world > 1:
     dist.init_process_group("nccl", device_id=dev)
 c = synth.CONFIGS[cfg]
-phi = synth.make_phi(c.m, c.N, "f32")
+st = "bf16" if prec == "bf16" else "f32"
+phi = synth.make_phi(c.m, c.N, st)
 x = synth.make_images(c.n, rank * B, B, c.n_blobs, c.n_rects, c.texture_var)
-y = synth.measure(phi, x, "f32")
-ctx = DeepInverse(phi, synth.make_params(bias="channel"), c.n, c.n, prec, device=local, max_batch=B)
-yd, xd = torch.from_numpy(y).to(dev), torch.from_numpy(x).to(dev)
+y = synth.measure(phi, x, st)
+ctx = DeepInverse(phi, synth.make_params(bias="channel").rounded(st), c.n, c.n, prec, device=local, max_batch=B)
+yd, xd = torch.from_numpy(y).to(dev).to(ctx.storage_dtype), torch.from_numpy(x).to(dev)
 scale = 1.0 / (B * world)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 times, losses, lr = [], [], None
