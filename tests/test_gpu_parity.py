@@ -267,3 +267,31 @@ def test_learned_lifting_matrix(precision):
     y = ctx.measure(torch.from_numpy(case.x).cuda()).float().cpu().numpy()
     ym = oracle.measure(case.phi, xs)
     assert max(oracle.rel_l2(a, b) for a, b in zip(y, ym)) <= (1e-5 if precision == "f32" else 1e-2)
+
+
+def test_inference_time_flat_across_measurement_rate():
+    """PAPER.md Table 1 (§5): DeepInverse's recovery time does not depend on M/N -- the lifting GEMM is a small
+    share next to the convolutions.  bf16, 64x64, batch 1024, M/N from 0.01 to 0.5: the slowest and fastest
+    median di_recover times stay within 15 %."""
+    import torch
+    from paper_1701_03891_b200 import DeepInverse
+    n, B = 64, 1024
+    times = {}
+    for m in (41, 410, 1229, 2048):
+        phi = synth.make_phi(m, n * n, "bf16")
+        ctx = DeepInverse(phi, synth.make_params().rounded("bf16"), n, n, "bf16", max_batch=B)
+        y = torch.randn((B, m), device="cuda").to(torch.bfloat16)
+        out = torch.empty((B, n, n), device="cuda")
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        for _ in range(2):
+            ctx.recover(y, out)
+        ts = []
+        for _ in range(5):
+            ev[0].record()
+            ctx.recover(y, out)
+            ev[1].record()
+            torch.cuda.synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]))
+        times[m] = float(np.median(ts))
+        ctx.close()
+    assert max(times.values()) <= 1.15 * min(times.values()), times
