@@ -75,7 +75,7 @@ enum { C2_BIAS_RELU = 0, C2_MASK = 1 };
 // strip row (C_in / 16 MMAs of K = 16), 11 ceil(11 / TAPS) K-blocks per tile.  <32, 64, C2_MASK> is the training
 // step's layer-2 data gradient: dG2 (bf16) in, the rotated bank, out = [h1 > 0] * conv in bf16 (mask = bf16 h1).
 template <int CIN, int COUT, int MODE>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
     k_conv2_tc(const __grid_constant__ CUtensorMap tmH1, const __nv_bfloat16* __restrict__ wpack,
                const float* __restrict__ bias, int fullmap, Geo g, __nv_bfloat16* __restrict__ h2,
                const __nv_bfloat16* __restrict__ mask) {
@@ -84,17 +84,22 @@ __global__ void __launch_bounds__(256, 1)
   constexpr uint32_t WB = 128 * RB;
   constexpr uint32_t SWZ = RB == 128 ? kSwizzle128B : kSwizzle64B;
   constexpr int QPT = COUT / 32, CPT = COUT / 8;
+  // epilogue groups: C_out = 64 (twice the epilogue work per tile) runs two groups of 4 warps, one per TMEM buffer
+  constexpr int EG = COUT == 64 ? 2 : 1;
+  // weight ring: the same 64 KB in blocks of WB bytes (8 stages of 8 KB for 64-B rows: the lead must cover the
+  // ~1.4k-cycle bulk-copy latency in MMA time)
+  constexpr int WST = WSTAGES * 128 / RB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int strip_bytes = (R + 10) * g.P * RB;
   const int strip_alloc = (strip_bytes + GUARD_ROWS * RB + 1023) & ~1023;
   uint8_t* strip = smem;
   uint8_t* wst = smem + strip_alloc;
-  float* sP = reinterpret_cast<float*>(wst + WSTAGES * WB);  // [4][ECH positions][SPS]
+  float* sP = reinterpret_cast<float*>(wst + WST * WB);  // [4][ECH positions][SPS]
 
-  __shared__ uint64_t hfull[2], hempty[2], wfull[WSTAGES], wempty[WSTAGES], tfull[2], tempty[2];
+  __shared__ uint64_t hfull[2], hempty[2], wfull[WST], wempty[WST], tfull[2], tempty[2];
 #ifdef DI_PROF_CONV2
-  __shared__ long long t_issue[WSTAGES];   // producer: clock64 when the copy of the stage's K-block was issued
+  __shared__ long long t_issue[WST];   // producer: clock64 when the copy of the stage's K-block was issued
 #endif
   __shared__ uint32_t tslot;
   const int warp = warp_id(), lane = lane_id();
@@ -102,7 +107,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmH1);
     for (int h = 0; h < 2; ++h) mbar_init(&hfull[h], 1), mbar_init(&hempty[h], 1);
-    for (int s = 0; s < WSTAGES; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], 1);
+    for (int s = 0; s < WST; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], 1);
     for (int s = 0; s < 2; ++s) mbar_init(&tfull[s], 1), mbar_init(&tempty[s], 4);
     fence_mbar_init();
   }
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(256, 1)
   const int per_img = g.nrb * g.ncs;
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ strip + weight producer
-      uint32_t wk = 0;                    // weight K-blocks issued (stage wk % WSTAGES)
+      uint32_t wk = 0;                    // weight K-blocks issued (stage wk % WST)
       int it = 0;
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
         const int b = u / per_img, rem = u - b * per_img;
@@ -135,8 +140,8 @@ __global__ void __launch_bounds__(256, 1)
         for (int t = 0; t < ntiles; ++t) {
           const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack);
           for (int kb = 0; kb < KB; ++kb, ++wk, wsrc += WB) {
-            const uint32_t st = wk % WSTAGES;
-            if (wk >= WSTAGES) mbar_wait(&wempty[st], ((wk / WSTAGES) - 1) & 1);
+            const uint32_t st = wk % WST;
+            if (wk >= WST) mbar_wait(&wempty[st], ((wk / WST) - 1) & 1);
 #if defined(DI_EXP_NOW)
             mbar_arrive(&wfull[st]);                          // experiment: no weight copies (wrong results)
 #elif defined(DI_EXP_HALFW)
@@ -192,14 +197,14 @@ __global__ void __launch_bounds__(256, 1)
           for (int uu = 0; uu < 11; ++uu, bd += pstep) {
 #pragma unroll
             for (int j = 0; j < J; ++j, ++wk) {   // column-tap groups v0 = TAPS j (0, 4, 8 for C_out = 32)
-              const uint32_t st = wk % WSTAGES;
+              const uint32_t st = wk % WST;
 #ifdef DI_PROF_CONV2
-              { PT0 mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
+              { PT0 mbar_wait(&wfull[st], (wk / WST) & 1);
                 if (t == 0 && uu < 3) { PT1(c_w0) } else if (t == 0) { PT1(c_w) } else { PT1(c_w1) }
                 const long long lat = clock64() - *(volatile long long*)&t_issue[st];
                 c_lat += lat; c_latmax = max(c_latmax, lat); }
 #else
-              mbar_wait(&wfull[st], (wk / WSTAGES) & 1);
+              mbar_wait(&wfull[st], (wk / WST) & 1);
 #endif
               tc_fence_after();
               const uint64_t ad = adesc0 + (uint64_t)(st * (WB >> 4));
@@ -222,9 +227,11 @@ __global__ void __launch_bounds__(256, 1)
 #endif
     }
   } else if (warp >= 4) {  // ---------------------------------------------- epilogue
-    const int q = warp - 4;              // TMEM lane quadrant: column tap q / QPT, channel block q % QPT
+    const int q = warp & 3;              // TMEM lane quadrant: column tap q / QPT, channel block q % QPT
+    const int grp = (warp - 4) >> 2;     // epilogue group: TMEM buffer grp when EG = 2
     const int shift = q / QPT;
-    const int e = threadIdx.x - 128;     // 0..127
+    const int e = (threadIdx.x - 128) & 127;
+    float* const sPg = sP + grp * (4 * ECH * SPS);
     const int jj = e >> 3, kg = e & 7;   // reduce role: output position jj of the chunk, channels CPT kg ..
     const int c0ch = CPT * kg, cblk = c0ch / 32, cl = c0ch % 32;
     float bch[CPT];
@@ -241,6 +248,7 @@ __global__ void __launch_bounds__(256, 1)
         const int n0 = t * OUT_PER_TILE;
         const int cnt = min(OUT_PER_TILE, L - n0);
         const int buf = ti & 1;
+        if (EG == 2 && buf != grp) continue;
         mbar_wait(&tfull[buf], (ti >> 1) & 1);
         tc_fence_after();
         const uint32_t tq = tmem + buf * 256 + ((uint32_t)(q * 32) << 16);
@@ -261,10 +269,10 @@ __global__ void __launch_bounds__(256, 1)
             continue;
           }
 #endif
-          float* dst = sP + q * (ECH * SPS) + lane;   // sP[q][j][k], k = lane
+          float* dst = sPg + q * (ECH * SPS) + lane;   // sP[q][j][k], k = lane
 #pragma unroll
           for (int j = 0; j < ECH; ++j) dst[j * SPS] = __uint_as_float(r[j]);
-          named_bar(1, 128);
+          named_bar(1 + grp, 128);
           if (jj < nout) {
             const int o = n0 + c + jj;
             const int rr = o / g.P, cc = o - rr * g.P;
@@ -276,7 +284,7 @@ __global__ void __launch_bounds__(256, 1)
                 float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int tp = 0; tp < TAPS; ++tp) {
-                  const float4 a = *reinterpret_cast<const float4*>(sP + (tp * QPT + cblk) * (ECH * SPS) + jj * SPS +
+                  const float4 a = *reinterpret_cast<const float4*>(sPg + (tp * QPT + cblk) * (ECH * SPS) + jj * SPS +
                                                                     cl + 4 * v4);
                   sum.x += a.x, sum.y += a.y, sum.z += a.z, sum.w += a.w;
                 }
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
           }
-          named_bar(1, 128);
+          named_bar(1 + grp, 128);
         }
         tc_fence_before();
         if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -362,7 +370,7 @@ cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, cons
                                void* dh1b, int num_sms, cudaStream_t st) {
   Geo g = make_geo(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv2_tc<32, 64, C2_MASK><<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(
+  k_conv2_tc<32, 64, C2_MASK><<<grid, 384, conv2_tc_smem_bytes(n2), st>>>(
       *tmDGb, reinterpret_cast<const __nv_bfloat16*>(wpack), nullptr, 0, g, reinterpret_cast<__nv_bfloat16*>(dh1b),
       reinterpret_cast<const __nv_bfloat16*>(h1b));
   return cudaGetLastError();
