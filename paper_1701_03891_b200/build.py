@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdeepinverse.so")
 SOURCES = ["api.cu", "k_proxy.cu", "k_conv_simt.cu", "k_conv2_tc.cu", "k_conv13_tc.cu", "k_conv2_tf32.cu", "k_sense.cu", "k_train.cu",
-           "k_wgrad2_tc.cu", "k_wgrad13_tc.cu"]
+           "k_wgrad2_tc.cu", "k_wgrad13_tc.cu", "k_conv3_r4.cu"]
 HEADERS = ["sm100.cuh", "kernels.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

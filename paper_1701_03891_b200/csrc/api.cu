@@ -253,7 +253,7 @@ di_status encode_h2(CUtensorMap* map, const void* h2, int batch, int n1, int n2,
   cuuint64_t dims[4] = {32, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
   cuuint64_t strides[3] = {32 * e, (cuuint64_t)n2 * 32 * e, (cuuint64_t)n1 * n2 * 32 * e};
   cuuint32_t box[4] = {(cuuint32_t)di::conv3_tc_box_ch(f32), (cuuint32_t)di::conv3_tc_box_cols(n2),
-                       (cuuint32_t)di::conv3_tc_box_rows(), 1};
+                       (cuuint32_t)(f32 ? di::conv3_tc_box_rows() : di::conv3_r4_box_rows()), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
                    const_cast<void*>(h2), dims, strides, box, es,
@@ -369,6 +369,23 @@ std::vector<uint16_t> conv3_tc_pack(const std::vector<float>& wx3) {
         const size_t off = (size_t)u * 2048 + r * 64 + ((((size_t)c / 8) ^ ((r >> 1) & 3)) << 4) + (c % 8) * 2;
         std::memcpy(base + off, &h, 2);
       }
+  return out;
+}
+
+// bf16 conv3, four rows stacked in M (k_conv3_r4): the stack T[i] = W[10 - i], i = -3..13 (zero outside 0..10), entry
+// i + 3 = 32 rows (row v < 11: column tap v) x 32 channels bf16, SWIZZLE_64B -- A_k is the 128-row window from T[10 - k]
+std::vector<uint16_t> conv3_r4_pack(const std::vector<float>& wx3) {
+  std::vector<uint16_t> out(17 * 2048 / 2, 0);
+  uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
+  for (int ip = 0; ip < 17; ++ip) {
+    const int u = 10 - (ip - 3);
+    for (int r = 0; r < 32; ++r)
+      for (int c = 0; c < 32; ++c) {
+        const uint16_t h = (u >= 0 && u < K && r < K) ? f2bf(wx3[((size_t)c * K + u) * K + r]) : 0;
+        const size_t off = (size_t)ip * 2048 + r * 64 + ((((size_t)c / 8) ^ ((r >> 1) & 3)) << 4) + (c % 8) * 2;
+        std::memcpy(base + off, &h, 2);
+      }
+  }
   return out;
 }
 
@@ -630,7 +647,10 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
         if (s != DI_OK) return s;
         tmp = &tm;
       }
-      CUDA_TRY(di::launch_conv3_tc(tmp, c->wp3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, c->num_sms, !bf16, st));
+      if (bf16)
+        CUDA_TRY(di::launch_conv3_r4(tmp, c->wp3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, c->num_sms, st));
+      else
+        CUDA_TRY(di::launch_conv3_tc(tmp, c->wp3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, c->num_sms, true, st));
     } else {
       CUDA_TRY(di::launch_conv3_simt(h2, bf16, c->wx3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, st));
     }
@@ -830,7 +850,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       STEP(upload(&c->wp2, p2.data(), p2.size() * 2, &c->ws_bytes));
       auto p1 = conv1_tc_pack(w1);
       STEP(upload(&c->wp1, p1.data(), p1.size() * 2, &c->ws_bytes));
-      auto p3 = conv3_tc_pack(w3);
+      auto p3 = conv3_r4_pack(w3);
       STEP(upload(&c->wp3, p3.data(), p3.size() * 2, &c->ws_bytes));
     }
     if (c->prec == DI_PREC_TF32) {
@@ -923,6 +943,13 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       return fail(DI_ERR_CUDA, "setup_conv13_tc: %s", cudaGetErrorString(e));
     }
     STEP(encode_h2(&c->tmH2, c->h2, a->max_batch, a->n1, a->n2));
+    {
+      cudaError_t e3 = di::setup_conv3_r4(a->n2);
+      if (e3 != cudaSuccess) {
+        free_ctx(c);
+        return fail(DI_ERR_CUDA, "setup_conv3_r4: %s", cudaGetErrorString(e3));
+      }
+    }
     if (a->n2 % 8 == 0) {
       STEP(encode_xt(&c->tmX, c->xt, a->max_batch, a->n1, a->n2));
       c->has_tmX = true;

@@ -74,6 +74,12 @@ cudaError_t launch_conv3_simt(const void* h2, bool bf16, const float* wx, const 
                               float* xhat, int batch, int n1, int n2, cudaStream_t st);
 
 int conv3_tc_box_rows();
+// bf16 conv layer 3 with four output rows stacked in M (k_conv3_r4.cu); tpack: the T stack (17 x 2 KB)
+int conv3_r4_box_rows();
+int conv3_r4_tpack_bytes();
+cudaError_t setup_conv3_r4(int n2);
+cudaError_t launch_conv3_r4(const CUtensorMap* tmH2, const void* tpack, const float* bias, int fullmap, int relu,
+                            float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st);
 int conv3_tc_box_cols(int n2);
 int conv3_tc_box_ch(bool tf32);
 cudaError_t launch_conv3_tc(const CUtensorMap* tmH2, const void* w3pack, const float* bias, int fullmap, int relu,
