@@ -372,17 +372,20 @@ std::vector<uint16_t> conv3_tc_pack(const std::vector<float>& wx3) {
   return out;
 }
 
-// bf16 conv3, four rows stacked in M (k_conv3_r4): the stack T[i] = W[10 - i], i = -3..13 (zero outside 0..10), entry
-// i + 3 = 32 rows (row v < 11: column tap v) x 32 channels bf16, SWIZZLE_64B -- A_k is the 128-row window from T[10 - k]
+// bf16 conv3, C3R_RP rows stacked in M (k_conv3_r4): the stack T[i] = W[10 - i], i = C3R_IMIN .., zero outside 0..10;
+// entry e = i - C3R_IMIN = C3R_ES rows (row v < 11: column tap v) x 32 channels bf16, SWIZZLE_64B -- window k's A
+// operand is the 128-row window from T[10 - k]
 std::vector<uint16_t> conv3_r4_pack(const std::vector<float>& wx3) {
-  std::vector<uint16_t> out(17 * 2048 / 2, 0);
+  const int es = di::C3R_ES;
+  std::vector<uint16_t> out((size_t)di::conv3_r4_tpack_bytes() / 2, 0);
   uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
-  for (int ip = 0; ip < 17; ++ip) {
-    const int u = 10 - (ip - 3);
-    for (int r = 0; r < 32; ++r)
+  for (int e = 0; e < di::C3R_NENT; ++e) {
+    const int u = 10 - (e + di::C3R_IMIN);
+    for (int r = 0; r < es; ++r)
       for (int c = 0; c < 32; ++c) {
         const uint16_t h = (u >= 0 && u < K && r < K) ? f2bf(wx3[((size_t)c * K + u) * K + r]) : 0;
-        const size_t off = (size_t)ip * 2048 + r * 64 + ((((size_t)c / 8) ^ ((r >> 1) & 3)) << 4) + (c % 8) * 2;
+        const size_t rho = (size_t)e * es + r;
+        const size_t off = rho * 64 + (((c / 8) ^ ((rho >> 1) & 3)) << 4) + (c % 8) * 2;
         std::memcpy(base + off, &h, 2);
       }
   }

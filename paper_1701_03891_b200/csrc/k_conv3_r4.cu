@@ -1,17 +1,20 @@
 // k_conv3_r4.cu -- stage 3 of the bf16 path, conv layer 3 (1 filter 11x11x32 + bias, ReLU iff DI_FLAG_FINAL_RELU,
-// crop S) with FOUR OUTPUT ROWS STACKED IN M.
+// crop S) with RP = 4 or 8 OUTPUT ROWS STACKED IN M (C3R_RP in kernels.cuh; 8 by default --
+// the description below is for 4: with 8, M = 8 rows x 16 (11 column taps), 18 windows, stack entries of 16 rows).
 //
 // C_out = 1 leaves the UMMA M dimension to the taps.  The first design (k_conv3_tc) stacks the 11 column taps of one
 // tap row in M = 32 (.ws) and walks the 11 tap rows as K-blocks, so every strip position is read by 11 MMAs per
-// 246 outputs and the tensor core's shared-memory reads bound it.  Here M = 128 = 4 output rows t x 32 (11 column
-// taps v): window k (k = 0..13) is the strip shifted by k rows, and quadrant t of its A operand holds the taps of
-// tap row u = k - t, so that
-//   D[(t, v)][n] = sum_k sum_c W[k - t][v][c] strip[n + k P][c]  and  x_hat[row 4p + t][j] = sum_v D[(t, v)][j + v].
-// A_k = [W[k]; W[k-1]; W[k-2]; W[k-3]] is a 128-row window of ONE stack T[i] = W[10 - i] (i = -3..13, zero outside
-// 0..10): A_k starts at T[10 - k] -- the whole bank is 17 x 2 KB resident in shared memory, and a window is a
-// descriptor start address.  N = P rounded up to 16 (<= 80) covers one strip row; per 4 x 64 outputs: 28 MMAs (K =
-// 16) reading 6.5 KB each, 24 % fewer operand bytes per output than k_conv3_tc.  Each epilogue warp owns one
-// output row (its TMEM quadrant) and sums its 11 diagonals through a private shared-memory tile.
+// 246 outputs and the tensor core's shared-memory reads bound it (0.87 ms at lowrate).  Here M = 128 = RP output rows
+// t x ES rows (11 column taps v, padded): window k (k = 0 .. RP + 9) is the strip shifted by k rows, and rows (t, .)
+// of its A operand hold the taps of tap row u = k - t, so that
+//   D[(t, v)][n] = sum_k sum_c W[k - t][v][c] strip[n + k P][c]  and  x_hat[row RP p + t][j] = sum_v D[(t, v)][j + v].
+// A_k = [W[k]; W[k-1]; ...; W[k-RP+1]] is a 128-row window of ONE stack T[i] = W[10 - i] (zero outside 0..10): A_k
+// starts at T[10 - k], the whole bank stays resident in shared memory, and a window is a descriptor start address.
+// N = P rounded up to 16 (<= 80) covers one strip row.  RP = 8 (ES = 16): per 8 x 64 outputs 18 windows x 2 MMAs
+// (K = 16) of 6.5 KB of operands -- 0.07 MMAs per output against 0.09 (k_conv3_tc) and 0.11 (RP = 4): 0.43 ms.
+// Each epilogue warp owns RPW = 32 / ES output rows (its TMEM quadrant) and sums their 11 diagonals through a
+// private shared-memory tile.  (Streaming the strip one row per window instead, with RP = 11, measured slower: the
+// per-window barrier handshake bounds the single issuing thread.)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -21,14 +24,16 @@
 namespace di {
 
 namespace {
-constexpr int R = 8;                   // output rows per unit: 2 passes of 4
-constexpr int NPASS = R / 4;
+constexpr int RP = C3R_RP, ES = C3R_ES, NWIN = C3R_NWIN, IMIN = C3R_IMIN;
+constexpr int R = 8;                   // output rows per unit
+constexpr int NPASS = R / RP;
 constexpr int NACC = 4;                // TMEM accumulator slots (128 columns each)
-constexpr int TBLK = 32 * 64;          // one T entry: 32 rows (v) x 32 channels bf16, SWIZZLE_64B
-constexpr int TBYTES = 17 * TBLK;      // T[-3..13]
+constexpr int TBLK = ES * 64;          // one T entry: ES rows (v) x 32 channels bf16, SWIZZLE_64B
+constexpr int TBYTES = (C3R_NENT * TBLK + 1023) & ~1023;
 constexpr int GUARD = 16;              // zero positions past the strip (windows read up to N - P past the box)
 constexpr int SROW = 84;               // epilogue tile row stride (floats): 16-B rows
-constexpr int SWARP = 11 * SROW;       // per epilogue warp
+constexpr int RPW = 32 / ES;           // output rows per epilogue warp (its TMEM quadrant)
+constexpr int SWARP = RPW * 11 * SROW; // per epilogue warp
 
 struct GeoR4 {
   int n1, n2, wseg, P, N, nrb, ncs, units;
@@ -102,10 +107,10 @@ __global__ void __launch_bounds__(256, 1)
             tc_fence_after();
           }
           const uint32_t d = tmem + a * 128;
-          uint64_t bd = bdesc0 + (uint64_t)((s * strip_alloc) >> 4) + (uint64_t)(4 * p) * rstep;
+          uint64_t bd = bdesc0 + (uint64_t)((s * strip_alloc) >> 4) + (uint64_t)(RP * p) * rstep;
 #pragma unroll 2
-          for (int k = 0; k < 14; ++k, bd += rstep) {
-            const uint64_t ad = adesc0 + (uint64_t)(((13 - k) * TBLK) >> 4);   // T[10 - k] .. T[13 - k]
+          for (int k = 0; k < NWIN; ++k, bd += rstep) {
+            const uint64_t ad = adesc0 + (uint64_t)(((10 - k - IMIN) * TBLK) >> 4);   // T[10 - k] ..
             umma_f16_ss(d, ad, bd, idesc, k != 0);
             umma_f16_ss(d, ad + 2, bd + 2, idesc, 1);                       // channels 16..31: +32 B
           }
@@ -114,7 +119,7 @@ __global__ void __launch_bounds__(256, 1)
         umma_commit(&sempty[s]);
       }
     }
-  } else if (warp >= 4) {  // ---------------------------------------------- epilogue: warp q = output row q
+  } else if (warp >= 4) {  // ------------------------------- epilogue: warp q = output rows RPW q .. RPW q + RPW - 1
     const int q = warp - 4;
     float* const Sq = S + q * SWARP;
     const float bsc = (!fullmap && bias) ? bias[0] : 0.f;
@@ -135,21 +140,21 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[a]);
-        if (lane < 11) {
-          float4* dst = reinterpret_cast<float4*>(Sq + lane * SROW);
+        if ((lane % ES) < 11) {   // S row (lane / ES) * 11 + v: tap v of output row RPW q + lane / ES
+          float4* dst = reinterpret_cast<float4*>(Sq + ((lane / ES) * 11 + lane % ES) * SROW);
 #pragma unroll
           for (int j = 0; j < 20; ++j)
             dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                  __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
         }
         __syncwarp();
-        const int row = r0 + 4 * p + q;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int j = lane + 32 * h;
+        for (int h = 0; h < 2 * RPW; ++h) {
+          const int j = lane + 32 * (h & 1), tr = h >> 1;
+          const int row = r0 + RP * p + RPW * q + tr;
           float acc = 0.f;
 #pragma unroll
-          for (int v = 0; v < 11; ++v) acc += Sq[v * SROW + j + v];
+          for (int v = 0; v < 11; ++v) acc += Sq[(tr * 11 + v) * SROW + j + v];
           if (j < g.wseg && c0 + j < g.n2 && row < g.n1) {
             const size_t pix = ((size_t)b * g.n1 + row) * g.n2 + c0 + j;
             acc += (fullmap && bias) ? bias[pix % ((size_t)g.n1 * g.n2)] : bsc;

@@ -322,7 +322,7 @@ __global__ void k_repack_bf16(const float* __restrict__ params, int flip, uint16
   const float* W1 = params;
   const float* W2 = params + N1;
   const float* W3 = params + N1 + N2;
-  constexpr int E2 = 33 * 8192, E1 = 11 * 1024, E3 = 17 * 1024;   // bf16 elements per image
+  constexpr int E2 = 33 * 8192, E1 = 11 * 1024, E3 = C3R_NENT * C3R_ES * 32;   // bf16 elements per image
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E2 + E1 + E3; e += gridDim.x * blockDim.x) {
     if (e < E2) {                     // conv2: block u*3 + j, row v'*32 + k, 64 ci (128 B), SWIZZLE_128B
       const int kb = e / 8192, o = (e % 8192) * 2, row = o / 128, r = o % 128;
@@ -334,11 +334,11 @@ __global__ void k_repack_bf16(const float* __restrict__ params, int flip, uint16
       const int v = (((r / 16) ^ ((m >> 2) & 1)) * 8) + (r % 16) / 2;
       const int grp = m / 16, j = m % 16, f = 16 * grp + (j < 8 ? 2 * j : 2 * (j - 8) + 1);
       wp1[i] = bfbits(v < KS ? wx_at(W1, 1, f, 0, u, v, flip) : 0.f);
-    } else {                          // conv3 (k_conv3_r4): T stack entry ip = tap row u = 13 - ip, row r = tap v,
-      const int i = e - E2 - E1, ip = i / 1024, o = (i % 1024) * 2, row = o / 64, r = o % 64;   // 32 ch, SW64
-      const int c = (((r / 16) ^ ((row >> 1) & 3)) * 8) + (r % 16) / 2;
-      const int u = 13 - ip;
-      wp3[i] = bfbits((row < KS && u >= 0 && u < KS) ? wx_at(W3, 32, 0, c, u, row, flip) : 0.f);
+    } else {                          // conv3 (k_conv3_r4): stack row rho = entry e x ES + tap v, 32 ch, SW64
+      const int i = e - E2 - E1, rho = i / 32, o = (i % 32) * 2;
+      const int c = ((((o / 16) ^ ((rho >> 1) & 3))) * 8) + (o % 16) / 2;
+      const int v = rho % C3R_ES, u = 10 - (rho / C3R_ES + C3R_IMIN);
+      wp3[i] = bfbits((v < KS && u >= 0 && u < KS) ? wx_at(W3, 32, 0, c, u, v, flip) : 0.f);
     }
   }
 }
