@@ -119,6 +119,19 @@ di_status di_recover(di_ctx ctx, const void* y, long long ldy, int batch, float*
 di_status di_proxy_partial(di_ctx ctx, const void* y, long long ldy, int batch, float* xt_part, void* stream);
 di_status di_recover_from_proxy(di_ctx ctx, const float* xt, int batch, float* xhat, void* stream);
 
+/* The same reduce-scatter done by the lifting GEMM itself over peer memory: rank `rank` of `world` (<= 8) computes its
+ * fp32 partial for all `batch` images (batch % world == 0, nb = batch / world) and its epilogue stores the rows of
+ * image b straight into slot `rank` of the staging buffer of b's owner r = b / nb:
+ *     slots[r] + (rank * nb + b % nb) * n1*n2        (slots[r]: DEVICE pointer usable on this GPU -- the owner's
+ *                                                      staging [world][nb][n1*n2] fp32, peer-mapped for r != rank)
+ * After every rank's di_proxy_scatter has completed (a cross-rank barrier, the caller's), each owner runs
+ * di_recover_from_slots on its staging: x_tilde = sum of the world slots in rank order (deterministic; rounded once
+ * to bf16 in BF16 contexts), then the convolutions, x_hat DEVICE [nb][n1][n2] fp32.  FP32 contexts compute the
+ * partial locally and copy its rows out.  Errors as di_recover (world / rank / divisibility: DI_ERR_ARG). */
+di_status di_proxy_scatter(di_ctx ctx, const void* y, long long ldy, int batch, float* const* slots, int world,
+                           int rank, void* stream);
+di_status di_recover_from_slots(di_ctx ctx, const float* staging, int world, int nb, float* xhat, void* stream);
+
 /* End-to-end variant with HOST buffers: copies y (host, pinned or pageable) to the device, recovers, copies
  * x_hat back to `xhat_host` (pinned host memory makes the copies asynchronous).  Kernels run on `stream`; batches
  * >= 512 are split into chunks of halving size (B/2, B/4, ..., >= 128) whose x_hat copies run on an internal

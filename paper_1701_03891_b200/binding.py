@@ -25,7 +25,7 @@ PRECISIONS = {"f32": DI_PREC_FP32, "tf32": DI_PREC_TF32, "bf16": DI_PREC_BF16}
 EXPORTS = ["di_create", "di_recover", "di_recover_host", "di_destroy", "di_status_string", "di_last_error",
            "di_get_info", "di_set_profiling", "di_stage_times", "di_debug_stage", "di_debug_get_phi",
            "di_measure", "di_add_noise", "di_metrics", "di_num_params", "di_train_grad", "di_sgd_step",
-           "di_get_params", "di_proxy_partial", "di_recover_from_proxy"]
+           "di_get_params", "di_proxy_partial", "di_recover_from_proxy", "di_proxy_scatter", "di_recover_from_slots"]
 
 
 class DiError(RuntimeError):
@@ -96,9 +96,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.di_get_params.argtypes = [V, V, V]
     lib.di_proxy_partial.argtypes = [V, V, LL, I, V, V]
     lib.di_recover_from_proxy.argtypes = [V, V, I, V, V]
+    lib.di_proxy_scatter.argtypes = [V, V, LL, I, V, I, I, V]
+    lib.di_recover_from_slots.argtypes = [V, V, I, I, V, V]
     for f in ("di_create", "di_recover", "di_recover_host", "di_destroy", "di_get_info", "di_set_profiling",
               "di_stage_times", "di_debug_stage", "di_debug_get_phi", "di_measure", "di_add_noise", "di_metrics",
-              "di_train_grad", "di_sgd_step", "di_get_params", "di_proxy_partial", "di_recover_from_proxy"):
+              "di_train_grad", "di_sgd_step", "di_get_params", "di_proxy_partial", "di_recover_from_proxy", "di_proxy_scatter",
+              "di_recover_from_slots"):
         getattr(lib, f).restype = I
     _lib = lib
     return lib
@@ -114,6 +117,8 @@ def _ptr(a) -> int | None:
         return None
     if hasattr(a, "data_ptr"):  # torch tensor
         return a.data_ptr()
+    if isinstance(a, int):      # raw device pointer (e.g. a cudaMalloc'd staging buffer)
+        return a
     return a.ctypes.data
 
 
@@ -153,6 +158,18 @@ def di_proxy_partial(ctx, y, ldy: int, batch: int, xt_part, stream=None):
 def di_recover_from_proxy(ctx, xt, batch: int, xhat, stream=None):
     _check(load().di_recover_from_proxy(ctx, _ptr(xt), batch, _ptr(xhat), _stream_handle(stream)),
            "di_recover_from_proxy")
+
+
+def di_proxy_scatter(ctx, y, ldy: int, batch: int, slots, world: int, rank: int, stream=None):
+    """slots: sequence of `world` device pointers (ints)."""
+    arr = (ctypes.c_void_p * world)(*[int(p) for p in slots])
+    _check(load().di_proxy_scatter(ctx, _ptr(y), ldy, batch, arr, world, rank, _stream_handle(stream)),
+           "di_proxy_scatter")
+
+
+def di_recover_from_slots(ctx, staging, world: int, nb: int, xhat, stream=None):
+    _check(load().di_recover_from_slots(ctx, _ptr(staging), world, nb, _ptr(xhat), _stream_handle(stream)),
+           "di_recover_from_slots")
 
 
 def di_destroy(ctx):
@@ -283,6 +300,22 @@ class DeepInverse:
         if xhat is None:
             xhat = torch.empty((b, self.n1, self.n2), dtype=torch.float32, device=xt.device)
         di_recover_from_proxy(self.ctx, xt, b, xhat, stream)
+        return xhat
+
+    def proxy_scatter(self, y, slots, world: int, rank: int, stream=None):
+        """Row-sharded lifting with the reduce-scatter in the GEMM epilogue (NEXT-4): the partial rows of image b go
+        to slots[b // nb] (device pointers: the owners' [world][nb][N] fp32 staging buffers, peer-mapped)."""
+        if y.dtype != self.storage_dtype or not y.is_cuda:
+            raise TypeError(f"y must be a CUDA {self.storage_dtype} tensor")
+        di_proxy_scatter(self.ctx, y, y.stride(0), y.shape[0], slots, world, rank, stream)
+
+    def recover_from_slots(self, staging, world: int, xhat=None, stream=None):
+        """Owner side: x_tilde = sum of the world slots of `staging` [world][nb][N] fp32 (rank order), then the convs."""
+        import torch
+        nb = staging.shape[1]
+        if xhat is None:
+            xhat = torch.empty((nb, self.n1, self.n2), dtype=torch.float32, device=staging.device)
+        di_recover_from_slots(self.ctx, staging, world, nb, xhat, stream)
         return xhat
 
     def recover_host(self, y_host, xhat_host=None, stream=None):

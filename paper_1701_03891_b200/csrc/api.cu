@@ -489,12 +489,16 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 // stage 0 (lifting) into xt: the path dtype, or fp32 when out_f32 (row-sharded partial proxies)
 di_status run_proxy(di_ctx c, const void* y, long long ldy, int batch, void* xt, bool out_f32, cudaStream_t st,
-                    int& launches) {
+                    int& launches, const di::ProxyScatter* sc = nullptr) {
   const bool bf16 = c->prec == DI_PREC_BF16;
   if (c->prec == DI_PREC_FP32) {
     CUDA_TRY(di::launch_proxy_f32(reinterpret_cast<const float*>(y), ldy, reinterpret_cast<const float*>(c->phi),
                                   c->m, c->N, batch, reinterpret_cast<float*>(xt), st));
     ++launches;
+    if (sc) {
+      CUDA_TRY(di::launch_scatter_rows(reinterpret_cast<const float*>(xt), batch, c->N, sc, st));
+      ++launches;
+    }
   } else {
     const void* ysrc = y;
     long long ld = ldy;
@@ -507,7 +511,8 @@ di_status run_proxy(di_ctx c, const void* y, long long ldy, int batch, void* xt,
     CUtensorMap tmY;
     di_status s = encode_2d(&tmY, ysrc, bf16, inner, batch, ld, 128 / (int)c->elt, 128);
     if (s != DI_OK) return s;
-    CUDA_TRY(di::launch_proxy_tc(&tmY, &c->tmPt, batch, c->N, c->kpad / (128 / (int)c->elt), xt, !bf16, st, out_f32));
+    CUDA_TRY(di::launch_proxy_tc(&tmY, &c->tmPt, batch, c->N, c->kpad / (128 / (int)c->elt), xt, !bf16, st, out_f32,
+                                 sc));
     ++launches;
   }
   return DI_OK;
@@ -980,6 +985,37 @@ di_status di_proxy_partial(di_ctx c, const void* y, long long ldy, int batch, fl
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
   int launches = 0;
   return run_proxy(c, y, ldy, batch, xt_part, true, reinterpret_cast<cudaStream_t>(stream), launches);
+}
+
+di_status di_proxy_scatter(di_ctx c, const void* y, long long ldy, int batch, float* const* slots, int world, int rank,
+                           void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!y || !slots) return fail(DI_ERR_ARG, "y and slots must be non-NULL");
+  if (world < 1 || world > 8 || rank < 0 || rank >= world)
+    return fail(DI_ERR_ARG, "world=%d rank=%d: need 1 <= world <= 8, 0 <= rank < world", world, rank);
+  if (batch < 1 || batch > c->max_batch || batch % world != 0)
+    return fail(DI_ERR_ARG, "batch=%d must be in [1, %d] and a multiple of world=%d", batch, c->max_batch, world);
+  if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
+  di::ProxyScatter sc{};
+  for (int r = 0; r < world; ++r) {
+    if (!slots[r]) return fail(DI_ERR_ARG, "slots[%d] is NULL", r);
+    sc.slots[r] = slots[r];
+  }
+  sc.world = world, sc.rank = rank, sc.nb = batch / world;
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  int launches = 0;
+  return run_proxy(c, y, ldy, batch, c->xt, true, reinterpret_cast<cudaStream_t>(stream), launches, &sc);
+}
+
+di_status di_recover_from_slots(di_ctx c, const float* staging, int world, int nb, float* xhat, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!staging || !xhat) return fail(DI_ERR_ARG, "staging and xhat must be non-NULL device pointers");
+  if (world < 1 || world > 8) return fail(DI_ERR_ARG, "world=%d outside [1, 8]", world);
+  if (nb < 1 || nb > c->max_batch) return fail(DI_ERR_ARG, "nb=%d outside [1, %d]", nb, c->max_batch);
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CUDA_TRY(di::launch_reduce_slots(staging, world, nb, c->N, c->xt, c->prec == DI_PREC_BF16, st));
+  return run_stages(c, 1, 3, nullptr, 0, nb, c->xt, c->h1, c->h2, xhat, st);
 }
 
 di_status di_recover_from_proxy(di_ctx c, const float* xt, int batch, float* xhat, void* stream) {

@@ -26,7 +26,7 @@ constexpr int PX_STAGES = 4;
 template <int ELT, bool OF32 = (ELT == 4)>
 __global__ void __launch_bounds__(128, 1)
     k_proxy_tc(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmPt, int batch,
-               int N, int kblocks, void* __restrict__ xt) {
+               int N, int kblocks, void* __restrict__ xt, ProxyScatter sc) {
   constexpr int KB_ELEMS = 128 / ELT;                       // K elements per 128-B swizzle row
   constexpr uint32_t A_BYTES = PX_BM * 128, B_BYTES = PX_BN * 128;
   constexpr uint32_t STAGE = A_BYTES + B_BYTES;
@@ -115,7 +115,13 @@ __global__ void __launch_bounds__(128, 1)
           if (col + j < N) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
       }
     } else {
-      float* dst = reinterpret_cast<float*>(xt) + (size_t)b * N + col;
+      float* dst;
+      if (sc.world > 0) {   // row-sharded Phi: straight into the owner's slot for this rank (peer memory)
+        const int r = b / sc.nb;
+        dst = sc.slots[r] + ((size_t)sc.rank * sc.nb + (b - r * sc.nb)) * N + col;
+      } else {
+        dst = reinterpret_cast<float*>(xt) + (size_t)b * N + col;
+      }
       if ((N % 4) == 0 && col + 32 <= N) {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
@@ -136,15 +142,17 @@ __global__ void __launch_bounds__(128, 1)
 size_t proxy_tc_smem_bytes() { return (size_t)PX_STAGES * (PX_BM + PX_BN) * 128 + 1024; }
 
 cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
-                            void* xt, bool tf32, cudaStream_t st, bool out_f32) {
+                            void* xt, bool tf32, cudaStream_t st, bool out_f32, const ProxyScatter* sc) {
   const int nbt = (batch + PX_BM - 1) / PX_BM, nnt = (N + PX_BN - 1) / PX_BN;
   const size_t smem = proxy_tc_smem_bytes();
+  ProxyScatter s0{};
+  if (sc) s0 = *sc;
   if (tf32) {
-    k_proxy_tc<4><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt);
-  } else if (out_f32) {
-    k_proxy_tc<2, true><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt);
+    k_proxy_tc<4><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0);
+  } else if (out_f32 || sc) {
+    k_proxy_tc<2, true><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0);
   } else {
-    k_proxy_tc<2><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt);
+    k_proxy_tc<2><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0);
   }
   return cudaGetLastError();
 }
@@ -158,6 +166,39 @@ cudaError_t setup_proxy_tc() {
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_proxy_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)proxy_tc_smem_bytes());
+}
+
+// FP32 contexts: rows of a local partial to the owners' slots
+__global__ void k_scatter_rows(const float* __restrict__ src, int batch, int N, ProxyScatter sc) {
+  const size_t total = (size_t)batch * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / N), j = (int)(i - (size_t)b * N), r = b / sc.nb;
+    sc.slots[r][((size_t)sc.rank * sc.nb + (b - r * sc.nb)) * N + j] = src[i];
+  }
+}
+
+cudaError_t launch_scatter_rows(const float* src, int batch, int N, const ProxyScatter* sc, cudaStream_t st) {
+  k_scatter_rows<<<4 * 148, 256, 0, st>>>(src, batch, N, *sc);
+  return cudaGetLastError();
+}
+
+// the owner's reduction: x_tilde[b][j] = sum_{r = 0..world-1} staging[r][b][j], in rank order (deterministic)
+__global__ void k_reduce_slots(const float* __restrict__ staging, int world, int nb, int N, void* __restrict__ out,
+                               int bf16) {
+  const size_t total = (size_t)nb * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int r = 0; r < world; ++r) acc += staging[(size_t)r * total + i];
+    if (bf16)
+      reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(acc);
+    else
+      reinterpret_cast<float*>(out)[i] = acc;
+  }
+}
+
+cudaError_t launch_reduce_slots(const float* staging, int world, int nb, int N, void* out, bool bf16, cudaStream_t st) {
+  k_reduce_slots<<<4 * 148, 256, 0, st>>>(staging, world, nb, N, out, bf16 ? 1 : 0);
+  return cudaGetLastError();
 }
 
 // fp32 -> bf16 (RNE), any n: a summed row-sharded proxy rounded once to the bf16 path's x_tilde

@@ -22,10 +22,22 @@ constexpr int C1TC_ROWS = 16;               // conv1 output rows per work unit
 constexpr int C3TC_ROWS = 6;                // conv3 output rows per work unit
 
 // stage 0: lifting layer x_tilde = Phi^T y
+// Row-sharded Phi (NEXT-4): the fp32 partial of image b goes straight to the staging buffer of the rank that owns
+// b's batch block: slots[b / nb] + (rank * nb + b % nb) * N (slots[r] may be a peer-mapped pointer into rank r's
+// memory); world = 0 disables the scatter
+struct ProxyScatter {
+  float* slots[8];
+  int world, rank, nb;
+};
 cudaError_t setup_proxy_tc();
 size_t proxy_tc_smem_bytes();
 cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
-                            void* xt, bool tf32, cudaStream_t st, bool out_f32 = false);
+                            void* xt, bool tf32, cudaStream_t st, bool out_f32 = false,
+                            const ProxyScatter* sc = nullptr);
+// rows of a local fp32 partial [batch][N] to the owners' slots (FP32 contexts); the owner's fixed-order slot sum
+// staging [world][nb][N] -> x_tilde [nb][N] (fp32, or RNE bf16 when bf16)
+cudaError_t launch_scatter_rows(const float* src, int batch, int N, const ProxyScatter* sc, cudaStream_t st);
+cudaError_t launch_reduce_slots(const float* staging, int world, int nb, int N, void* out, bool bf16, cudaStream_t st);
 cudaError_t launch_round_bf16(const float* src, void* dst, size_t n, cudaStream_t st);
 cudaError_t launch_proxy_f32(const float* y, long long ldy, const float* phi, int m, int N, int batch, float* xt,
                              cudaStream_t st);

@@ -48,6 +48,50 @@ def sum_scatter(part: torch.Tensor, group=None) -> torch.Tensor:
     return out
 
 
+class PeerStaging:
+    """This rank's staging buffer [world][nb][N] fp32 (cudaMalloc'd, so its CUDA IPC handle covers it exactly) and the
+    device pointers of every rank's staging buffer as seen from this GPU (IPC handles exchanged with one
+    all_gather_object; opened with lazy peer access)."""
+
+    def __init__(self, world: int, rank: int, nb: int, N: int, group=None):
+        from cuda.bindings import runtime as rt
+        self.world, self.rank, self.nb, self.N = world, rank, nb, N
+        self._rt = rt
+        err, ptr = rt.cudaMalloc(world * nb * N * 4)
+        if err != rt.cudaError_t.cudaSuccess:
+            raise RuntimeError(f"cudaMalloc(staging) failed: {err}")
+        self.ptr = int(ptr)
+        self._opened = []
+        if world == 1:
+            self.peers = [self.ptr]
+            return
+        err, h = rt.cudaIpcGetMemHandle(self.ptr)
+        if err != rt.cudaError_t.cudaSuccess:
+            raise RuntimeError(f"cudaIpcGetMemHandle failed: {err}")
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h.reserved), group=group)
+        self.peers = []
+        for r, hb in enumerate(handles):
+            if r == rank:
+                self.peers.append(self.ptr)
+                continue
+            hh = rt.cudaIpcMemHandle_t()
+            hh.reserved = hb
+            err, p = rt.cudaIpcOpenMemHandle(hh, rt.cudaIpcMemLazyEnablePeerAccess)
+            if err != rt.cudaError_t.cudaSuccess:
+                raise RuntimeError(f"cudaIpcOpenMemHandle(rank {r}) failed: {err}")
+            self.peers.append(int(p))
+            self._opened.append(int(p))
+
+    def close(self):
+        for p in self._opened:
+            self._rt.cudaIpcCloseMemHandle(p)
+        self._opened = []
+        if self.ptr:
+            self._rt.cudaFree(self.ptr)
+            self.ptr = 0
+
+
 class RowShardedDeepInverse:
     """One rank's share of a row-sharded recovery.
 
@@ -60,10 +104,34 @@ class RowShardedDeepInverse:
         self.group = group
         self.ctx = DeepInverse(phi_rows, params, n1, n2, precision, device=device, max_batch=max_batch, **kw)
 
-    def recover(self, y_rows: torch.Tensor, stream=None) -> torch.Tensor:
-        part = self.ctx.proxy_partial(y_rows, stream=stream)
-        xt = sum_scatter(part, self.group)
-        return self.ctx.recover_from_proxy(xt, stream=stream)
+    def recover(self, y_rows: torch.Tensor, stream=None, fused: bool = False) -> torch.Tensor:
+        if not fused:
+            part = self.ctx.proxy_partial(y_rows, stream=stream)
+            xt = sum_scatter(part, self.group)
+            return self.ctx.recover_from_proxy(xt, stream=stream)
+        from .binding import di_recover_from_slots
+        world = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        rank = dist.get_rank(self.group) if dist.is_initialized() else 0
+        lo, hi = batch_range(y_rows.shape[0], world, rank)
+        nb = hi - lo
+        st = getattr(self, "_staging", None)
+        if st is None or st.nb != nb:
+            if st is not None:
+                st.close()
+            st = self._staging = PeerStaging(world, rank, nb, self.ctx.n1 * self.ctx.n2, self.group)
+        if world > 1:   # the owners finished reducing the previous call's slots
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+        self.ctx.proxy_scatter(y_rows, st.peers, world, rank, stream=stream)
+        if world > 1:   # every rank's rows have landed in this rank's staging
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+        xhat = torch.empty((nb, self.ctx.n1, self.ctx.n2), dtype=torch.float32, device=y_rows.device)
+        di_recover_from_slots(self.ctx.ctx, st.ptr, world, nb, xhat, stream)
+        return xhat
 
     def close(self):
+        st = getattr(self, "_staging", None)
+        if st is not None:
+            st.close()
         self.ctx.close()

@@ -65,3 +65,70 @@ def test_recover_from_proxy_argument_errors():
     with pytest.raises(TypeError):
         ctx.recover_from_proxy(torch.zeros((2, 256), device="cuda", dtype=torch.bfloat16))
     ctx.close()
+
+
+@pytest.mark.parametrize("precision,n,m,batch,world", [("bf16", 32, 256, 4, 2), ("bf16", 64, 410, 6, 3),
+                                                        ("tf32", 16, 100, 4, 4), ("f32", 16, 100, 4, 2)])
+def test_fused_scatter_matches_full_phi_and_the_unfused_form(precision, n, m, batch, world):
+    """di_proxy_scatter (the lifting GEMM's epilogue storing each image's partial rows into the owner's slot) and
+    di_recover_from_slots (the owner's rank-order slot sum + convolutions), with `world` virtual ranks on one GPU:
+    each rank's GEMM runs to completion before the next (no kernel waits on another), writing into the owners'
+    staging buffers through plain device pointers -- on G GPUs the same pointers are CUDA-IPC peer mappings.  Equal
+    bit for bit to di_recover_from_proxy on the same rank-order sum, and to the full-Phi oracle within tolerance."""
+    import torch
+    from paper_1701_03891_b200 import DeepInverse, batch_range, row_range
+    case = Case(n, n, m, batch, precision, bias="channel")
+    N, nb = n * n, batch // world
+    staging = [torch.zeros((world, nb, N), dtype=torch.float32, device="cuda") for _ in range(world)]
+    ctxs, parts = [], []
+    for g in range(world):
+        lo, hi = row_range(m, world, g)
+        ctx = DeepInverse(np.ascontiguousarray(case.phi[lo:hi]), case.params, n, n, precision, max_batch=batch)
+        y = torch.from_numpy(np.ascontiguousarray(case.y[:, lo:hi])).to("cuda", ctx.storage_dtype)
+        ctx.proxy_scatter(y, [s.data_ptr() for s in staging], world, g)
+        parts.append(ctx.proxy_partial(y))
+        ctxs.append(ctx)
+    torch.cuda.synchronize()
+    ref = case.oracle(np.arange(batch))
+    for r in range(world):
+        lo, hi = batch_range(batch, world, r)
+        for g in range(world):   # slot g of owner r holds rank g's partial rows of r's block
+            assert torch.equal(staging[r][g], parts[g][lo:hi])
+        out = ctxs[r].recover_from_slots(staging[r], world).cpu().numpy()
+        total = parts[0][lo:hi].clone()
+        for g in range(1, world):
+            total += parts[g][lo:hi]
+        ref_unfused = ctxs[r].recover_from_proxy(total.contiguous()).cpu().numpy()
+        assert np.array_equal(out, ref_unfused)
+        rel, _, _ = compare(out, ref[lo:hi], case.x[lo:hi], precision)
+        assert rel <= TOL_REL_L2[precision], rel
+    for c in ctxs:
+        c.close()
+
+
+def test_fused_single_rank_recover():
+    """RowShardedDeepInverse.recover(fused=True) without a process group (world = 1) equals the replicated path."""
+    import torch
+    from paper_1701_03891_b200 import RowShardedDeepInverse
+    case = Case(32, 32, 256, 4, "bf16", bias="channel")
+    rs = RowShardedDeepInverse(case.phi, case.params, 32, 32, "bf16", max_batch=4)
+    y = torch.from_numpy(case.y).to("cuda", torch.bfloat16)
+    a = rs.recover(y, fused=True).cpu().numpy()
+    b = rs.ctx.recover(y).cpu().numpy()
+    rel = max(oracle.rel_l2(u, v) for u, v in zip(a, b))
+    assert rel <= 1e-6, rel   # the bf16 rounding of an fp32 proxy vs the GEMM's own bf16 epilogue
+    rs.close()
+
+
+def test_proxy_scatter_argument_errors():
+    import torch
+    from paper_1701_03891_b200 import DeepInverse, DiError
+    case = Case(16, 16, 64, 4, "bf16")
+    ctx = DeepInverse(case.phi, case.params, 16, 16, "bf16", max_batch=4)
+    y = torch.from_numpy(case.y).to("cuda", torch.bfloat16)
+    buf = torch.zeros((3, 1, 256), device="cuda")
+    with pytest.raises(DiError):
+        ctx.proxy_scatter(y, [buf.data_ptr()] * 3, 3, 0)      # batch 4 not a multiple of 3
+    with pytest.raises(DiError):
+        ctx.proxy_scatter(y, [buf.data_ptr()] * 2, 2, 2)      # rank outside [0, world)
+    ctx.close()
