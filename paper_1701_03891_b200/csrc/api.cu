@@ -357,20 +357,6 @@ std::vector<uint16_t> conv1_tc_pack(const std::vector<float>& wx1) {
   return out;
 }
 
-// conv3 tensor-core blocks: block u (2 KB) = 32 rows (row v < 11: tap v; else zero) x 32 input channels, bf16,
-// SWIZZLE_64B image (16-B chunk h of row r at r*64 + ((h ^ ((r >> 1) & 3)) << 4)).
-std::vector<uint16_t> conv3_tc_pack(const std::vector<float>& wx3) {
-  std::vector<uint16_t> out(11 * 2048 / 2, 0);
-  uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
-  for (int u = 0; u < K; ++u)
-    for (int r = 0; r < 32; ++r)
-      for (int c = 0; c < 32; ++c) {
-        const uint16_t h = r < K ? f2bf(wx3[((size_t)c * K + u) * K + r]) : 0;
-        const size_t off = (size_t)u * 2048 + r * 64 + ((((size_t)c / 8) ^ ((r >> 1) & 3)) << 4) + (c % 8) * 2;
-        std::memcpy(base + off, &h, 2);
-      }
-  return out;
-}
 
 // bf16 conv3, C3R_RP rows stacked in M (k_conv3_r4): the stack T[i] = W[10 - i], i = C3R_IMIN .., zero outside 0..10;
 // entry e = i - C3R_IMIN = C3R_ES rows (row v < 11: column tap v) x 32 channels bf16, SWIZZLE_64B -- window k's A
