@@ -105,6 +105,7 @@ struct di_ctx_s {
   void* dh1b = nullptr;                   // training, TF32 mode: dH1 in bf16 (bf16 dgrad2 -> wgrad1)
   float* part_w2 = nullptr;     // training, TF32 mode: per-CTA layer-2 wgrad partials
   CUtensorMap tmH1b, tmDG2b;
+  CUtensorMap tmH2w;            // training, BF16 mode: bf16 h2 strips for k_wgrad3_tc
   // training (FP32 contexts with per-channel biases): parameters in the API orientation, momentum, backward
   // weight layouts and the backward workspace (allocated on the first di_train_grad)
   float* params = nullptr;      // [W1 | W2 | W3 | b1 | b2 | b3], di::N_PARAMS
@@ -1207,6 +1208,8 @@ static di_status train_alloc(di_ctx c) {
       return s;
     CUDA_TRY(di::setup_wgrad2_tc(c->n2));
     CUDA_TRY(di::setup_wgrad13_tc(c->n2));
+    if (bf && (s = encode_wg2(&c->tmH2w, c->h2, c->max_batch, c->n1, c->n2, 32, di::wgrad3_tc_h_box_rows())) != DI_OK)
+      return s;
     if ((s = al(reinterpret_cast<uint8_t**>(&c->wp2db), (size_t)di::DG2_KBLOCKS * 8192)) != DI_OK) return s;
     if ((s = encode_dg2b_strip(&c->tmDG2s, c->dg2b, c->max_batch, c->n1, c->n2)) != DI_OK) return s;
     if (c->n2 % 4 == 0) {   // the conv1 TF32 strip map over dG3 (16-B row stride)
@@ -1260,7 +1263,7 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   const bool bf = c->prec == DI_PREC_BF16;   // BF16 contexts: x_tilde, h1, h2 are bf16
   if (tc)
     CUDA_TRY(di::launch_wgrad3_tc(c->h2, c->dxh, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads + n1w + n2w,
-                                  gb + C1 + C2, c->num_sms, st, bf));
+                                  gb + C1 + C2, c->num_sms, st, bf, bf ? &c->tmH2w : nullptr));
   else
     CUDA_TRY(di::launch_wgrad(3, h2, c->dxh, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w + n2w,
                               gb + C1 + C2, st));

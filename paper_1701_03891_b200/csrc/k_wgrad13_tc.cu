@@ -207,17 +207,19 @@ __global__ void k_wgrad1_reduce(const float* __restrict__ part, const float* __r
 // =============================================================================================== layer 3
 __global__ void __launch_bounds__(128, 1)
     k_wgrad3_tc(const void* __restrict__ h2, const float* __restrict__ dg3, GeoT13 g, float* __restrict__ part,
-                float* __restrict__ part_b, int hbf) {
+                float* __restrict__ part_b, int hbf, const __grid_constant__ CUtensorMap tmH2, int use_tma) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* ds = reinterpret_cast<float*>(smem + 2 * g.stage) + 16;   // ds[-16 .. NB + 16)
-  __shared__ uint64_t done[2], fin;
+  __shared__ uint64_t done[2], fin, hbar[2];
   __shared__ uint32_t tslot;
   __shared__ float red[128];
   const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
   const int P = g.P, NH = l3_nh(P), NB = l3_nb(P);
   if (tid == 0) {
     mbar_init(&done[0], 1), mbar_init(&done[1], 1), mbar_init(&fin, 1);
+    mbar_init(&hbar[0], 1), mbar_init(&hbar[1], 1);
+    if (use_tma) tma_prefetch_desc(&tmH2);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<64>(&tslot), tmem_relinquish();
@@ -244,9 +246,14 @@ __global__ void __launch_bounds__(128, 1)
     uint8_t* hs = smem + s * g.stage;          // position q at hs + (16 + q) * 64
     uint8_t* ex = smem + s * g.stage + g.off2;  // row k at ex + (32 + k) * 32
     if (it >= 2) mbar_wait(&done[s], ((it >> 1) - 1) & 1);
-    // h2 strip with halo: q -> h2(r0 - 5 + q / P, c0 - 5 + q % P), bf16 SW64 (chunk c at c ^ ((q >> 1) & 3))
+    // h2 strip with halo: q -> h2(r0 - 5 + q / P, c0 - 5 + q % P), bf16 SW64 (chunk c at c ^ ((q >> 1) & 3));
+    // bf16 h2 (BF16 contexts): one TMA box of R + 11 rows (out-of-bounds zero fill), else converting loaders
+    if (use_tma && tid == 0) {
+      mbar_arrive_expect_tx(&hbar[s], (uint32_t)((R + 11) * P * 64));
+      tma_load_4d(hs + 16 * 64, &tmH2, &hbar[s], 0, c0 - 5, r0 - 5, b);
+    }
     constexpr int U = 4;
-    for (int i0 = tid; i0 < NH * 4; i0 += 128 * U) {
+    for (int i0 = tid; !use_tma && i0 < NH * 4; i0 += 128 * U) {
       uint4 w[U];   // 8 channels of one position as bf16
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
@@ -296,6 +303,7 @@ __global__ void __launch_bounds__(128, 1)
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
+      if (use_tma) mbar_wait(&hbar[s], (it >> 1) & 1);
       tc_fence_after();
       const int nk = (rows * P + 11 + 15) >> 4;
       uint64_t bd = smem_desc(smem_u32(ex + 32 * 32), 32, 256, kSwizzle32B);
@@ -403,11 +411,17 @@ cudaError_t launch_wgrad1_tc(const void* xt, const void* dg1, int batch, int n1,
   return cudaGetLastError();
 }
 
+int wgrad3_tc_h_box_rows() { return R + 11; }
+
 cudaError_t launch_wgrad3_tc(const void* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
-                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool h2_bf16) {
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool h2_bf16,
+                             const CUtensorMap* tmH2) {
   GeoT13 g = make_geo(batch, n1, n2, false);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_wgrad3_tc<<<grid, 128, smem_bytes(n2, false), st>>>(h2, dg3, g, part, part_b, h2_bf16 ? 1 : 0);
+  CUtensorMap dummy{};
+  const int use_tma = (h2_bf16 && tmH2) ? 1 : 0;
+  k_wgrad3_tc<<<grid, 128, smem_bytes(n2, false), st>>>(h2, dg3, g, part, part_b, h2_bf16 ? 1 : 0,
+                                                        use_tma ? *tmH2 : dummy, use_tma);
   k_wgrad3_reduce<<<(32 * KS * KS + 1 + 255) / 256, 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
   return cudaGetLastError();
 }

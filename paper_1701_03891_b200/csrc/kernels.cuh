@@ -165,7 +165,9 @@ cudaError_t setup_wgrad13_tc(int n2);
 cudaError_t launch_wgrad1_tc(const void* xt, const void* dg1, int batch, int n1, int n2, float* part, float* part_b,
                              int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool xt_bf16 = false);
 cudaError_t launch_wgrad3_tc(const void* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
-                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool h2_bf16 = false);
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool h2_bf16 = false,
+                             const CUtensorMap* tmH2 = nullptr);
+int wgrad3_tc_h_box_rows();   // bf16 h2 strip box of k_wgrad3_tc (32 ch x P x rows, SWIZZLE_64B)
 cudaError_t launch_bias_reduce(const float* part_b, int nchunk, int nb, float* gb, cudaStream_t st);
 cudaError_t launch_sgd_repack(float* params, const float* grads, float* vel, int n, float lr, float momentum, int flip,
                               float* wx1, float* wx2, float* wx3, float* wt2, float* wt3, float* b1, float* b2,
