@@ -106,6 +106,7 @@ struct di_ctx_s {
   float* part_w2 = nullptr;     // training, TF32 mode: per-CTA layer-2 wgrad partials
   CUtensorMap tmH1b, tmDG2b;
   CUtensorMap tmH2w;            // training, BF16 mode: bf16 h2 strips for k_wgrad3_tc
+  CUtensorMap tmD1w;            // training, TF32/BF16: bf16 dH1 strips for k_wgrad1_tc
   // training (FP32 contexts with per-channel biases): parameters in the API orientation, momentum, backward
   // weight layouts and the backward workspace (allocated on the first di_train_grad)
   float* params = nullptr;      // [W1 | W2 | W3 | b1 | b2 | b3], di::N_PARAMS
@@ -1210,6 +1211,8 @@ static di_status train_alloc(di_ctx c) {
     CUDA_TRY(di::setup_wgrad13_tc(c->n2));
     if (bf && (s = encode_wg2(&c->tmH2w, c->h2, c->max_batch, c->n1, c->n2, 32, di::wgrad3_tc_h_box_rows())) != DI_OK)
       return s;
+    if ((s = encode_wg2(&c->tmD1w, c->dh1b, c->max_batch, c->n1, c->n2, 64, di::wgrad1_tc_d_box_rows())) != DI_OK)
+      return s;
     if ((s = al(reinterpret_cast<uint8_t**>(&c->wp2db), (size_t)di::DG2_KBLOCKS * 8192)) != DI_OK) return s;
     if ((s = encode_dg2b_strip(&c->tmDG2s, c->dg2b, c->max_batch, c->n1, c->n2)) != DI_OK) return s;
     if (c->n2 % 4 == 0) {   // the conv1 TF32 strip map over dG3 (16-B row stride)
@@ -1289,7 +1292,7 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
     CUDA_TRY(di::launch_dgrad2_f32(c->dh2, c->wt2, h1, c->dh1, batch, c->n1, c->n2, st));
   if (tc)
     CUDA_TRY(di::launch_wgrad1_tc(c->xt, c->dh1b, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads, gb,
-                                  c->num_sms, st, bf));
+                                  c->num_sms, st, bf, &c->tmD1w));
   else
     CUDA_TRY(di::launch_wgrad(1, xt, c->dh1, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads, gb, st));
   return DI_OK;

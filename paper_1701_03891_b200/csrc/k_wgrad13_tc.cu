@@ -56,17 +56,20 @@ __host__ __device__ inline int l3_nb(int P) { return R * P + 32; }
 // =============================================================================================== layer 1
 __global__ void __launch_bounds__(128, 1)
     k_wgrad1_tc(const void* __restrict__ xt, const __nv_bfloat16* __restrict__ dg1, GeoT13 g,
-                float* __restrict__ part, float* __restrict__ part_b, int xbf) {
+                float* __restrict__ part, float* __restrict__ part_b, int xbf, const __grid_constant__ CUtensorMap tmD1,
+                int use_tma) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xs = reinterpret_cast<float*>(smem + 2 * g.stage);
-  __shared__ uint64_t done[2], fin;
+  __shared__ uint64_t done[2], fin, dbar[2];
   __shared__ uint32_t tslot;
   __shared__ float red[128][9];
   const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
   const int P = g.P, NE = l1_ne(P), NX = l1_nx(P);
   if (tid == 0) {
     mbar_init(&done[0], 1), mbar_init(&done[1], 1), mbar_init(&fin, 1);
+    mbar_init(&dbar[0], 1), mbar_init(&dbar[1], 1);
+    if (use_tma) tma_prefetch_desc(&tmD1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<128>(&tslot), tmem_relinquish();
@@ -93,9 +96,15 @@ __global__ void __launch_bounds__(128, 1)
     uint8_t* d1 = smem + s * g.stage;          // position q at d1 + (16 + q) * 128
     uint8_t* ex = smem + s * g.stage + g.off2;  // row q at ex + (32 + q) * 32
     if (it >= 2) mbar_wait(&done[s], ((it >> 1) - 1) & 1);
-    // dG1 of the unit's pixels: position q -> (r0 + q / P, c0 + q % P), columns >= wseg zero; bf16 SW128
+    // dG1 of the unit's pixels: position q -> (r0 + q / P, c0 + q % P), columns >= wseg zero; bf16 SW128.
+    // use_tma: one TMA box of R rows x P columns (out-of-bounds zero fill); the columns of the next segment are
+    // zeroed and the bias sums read back from shared memory once it has landed (below)
+    if (use_tma && tid == 0) {
+      mbar_arrive_expect_tx(&dbar[s], (uint32_t)(R * P * 128));
+      tma_load_4d(d1 + 16 * 128, &tmD1, &dbar[s], 0, c0, r0, b);
+    }
     constexpr int U = 4;   // chunks per thread in flight (memory-level parallelism)
-    for (int i0 = tid; i0 < R * P * 8; i0 += 128 * U) {
+    for (int i0 = tid; !use_tma && i0 < R * P * 8; i0 += 128 * U) {
       uint4 v[U];
 #pragma unroll
       for (int uu = 0; uu < U; ++uu) {
@@ -133,6 +142,23 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
       for (int uu = 0; uu < 8; ++uu)
         if (q0 + uu * 128 < NX) xs[q0 + uu * 128] = v[uu];
+    }
+    if (use_tma) {
+      mbar_wait(&dbar[s], (it >> 1) & 1);
+      if (g.ncs > 1)   // columns wseg .. P-1 of each row belong to the next segment
+        for (int i = tid; i < R * (P - g.wseg) * 8; i += 128) {
+          const int row = i / ((P - g.wseg) * 8), rr = i % ((P - g.wseg) * 8);
+          const int q = row * P + g.wseg + rr / 8;
+          *reinterpret_cast<uint4*>(d1 + (16 + q) * 128 + ((rr % 8) << 4)) = make_uint4(0, 0, 0, 0);
+        }
+      __syncthreads();
+      for (int q = tid >> 3; q < rows * P; q += 16) {   // bias partials: channel group cg, fixed assignment
+        const uint4 w = *reinterpret_cast<const uint4*>(d1 + (16 + q) * 128 + ((cg ^ (q & 7)) << 4));
+        bs[0] += __uint_as_float(w.x << 16), bs[1] += __uint_as_float(w.x & 0xffff0000u);
+        bs[2] += __uint_as_float(w.y << 16), bs[3] += __uint_as_float(w.y & 0xffff0000u);
+        bs[4] += __uint_as_float(w.z << 16), bs[5] += __uint_as_float(w.z & 0xffff0000u);
+        bs[6] += __uint_as_float(w.w << 16), bs[7] += __uint_as_float(w.w & 0xffff0000u);
+      }
     }
     __syncthreads();
     // Toeplitz expansion E[q][j] = xs[q + j], SW32 (16-B chunk c at c ^ ((q >> 2) & 1))
@@ -401,12 +427,17 @@ cudaError_t setup_wgrad13_tc(int n2) {
   return cudaFuncSetAttribute(k_wgrad3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(n2, false));
 }
 
+int wgrad1_tc_d_box_rows() { return R; }
+
 cudaError_t launch_wgrad1_tc(const void* xt, const void* dg1, int batch, int n1, int n2, float* part, float* part_b,
-                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool xt_bf16) {
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool xt_bf16,
+                             const CUtensorMap* tmD1) {
   GeoT13 g = make_geo(batch, n1, n2, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
+  CUtensorMap dummy{};
   k_wgrad1_tc<<<grid, 128, smem_bytes(n2, true), st>>>(xt, reinterpret_cast<const __nv_bfloat16*>(dg1), g, part,
-                                                       part_b, xt_bf16 ? 1 : 0);
+                                                       part_b, xt_bf16 ? 1 : 0, tmD1 ? *tmD1 : dummy,
+                                                       tmD1 ? 1 : 0);
   k_wgrad1_reduce<<<(64 * KS * KS + 64 + 255) / 256, 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
   return cudaGetLastError();
 }

@@ -163,7 +163,9 @@ cudaError_t setup_wgrad13_tc(int n2);
 // dg1: [B][N][64] bf16 (the bf16 dgrad2 output)
 // xt / h2: fp32, or bf16 when xt_bf16 / h2_bf16 (BF16 contexts)
 cudaError_t launch_wgrad1_tc(const void* xt, const void* dg1, int batch, int n1, int n2, float* part, float* part_b,
-                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool xt_bf16 = false);
+                             int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool xt_bf16 = false,
+                             const CUtensorMap* tmD1 = nullptr);
+int wgrad1_tc_d_box_rows();   // bf16 dG1 strip box of k_wgrad1_tc (64 ch x P x rows, SWIZZLE_128B)
 cudaError_t launch_wgrad3_tc(const void* h2, const float* dg3, int batch, int n1, int n2, float* part, float* part_b,
                              int flip, float* gw, float* gb, int num_sms, cudaStream_t st, bool h2_bf16 = false,
                              const CUtensorMap* tmH2 = nullptr);
