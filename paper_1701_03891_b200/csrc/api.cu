@@ -173,7 +173,7 @@ di_status encode_h1_f32(CUtensorMap* map, const void* h1, int batch, int n1, int
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[4] = {64, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
   cuuint64_t strides[3] = {64 * 4, (cuuint64_t)n2 * 64 * 4, (cuuint64_t)n1 * n2 * 64 * 4};
-  cuuint32_t box[4] = {32, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tf32_box_rows(), 1};
+  cuuint32_t box[4] = {32, (cuuint32_t)di::conv_tf32_box_cols(n2), (cuuint32_t)di::conv2_tf32_box_rows(), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(h1), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -209,7 +209,7 @@ di_status encode_act_f32(CUtensorMap* map, const void* dg2, int batch, int n1, i
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[4] = {(cuuint64_t)ch, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
   cuuint64_t strides[3] = {(cuuint64_t)ch * 4, (cuuint64_t)n2 * ch * 4, (cuuint64_t)n1 * n2 * ch * 4};
-  cuuint32_t box[4] = {32, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tf32_box_rows(), 1};
+  cuuint32_t box[4] = {32, (cuuint32_t)di::conv_tf32_box_cols(n2), (cuuint32_t)di::conv2_tf32_box_rows(), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(dg2), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -224,7 +224,7 @@ di_status encode_wg2(CUtensorMap* map, const void* p, int batch, int n1, int n2,
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[4] = {(cuuint64_t)ch, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
   cuuint64_t strides[3] = {(cuuint64_t)ch * 2, (cuuint64_t)n2 * ch * 2, (cuuint64_t)n1 * n2 * ch * 2};
-  cuuint32_t box[4] = {(cuuint32_t)ch, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)box_rows, 1};
+  cuuint32_t box[4] = {(cuuint32_t)ch, (cuuint32_t)di::wgrad_box_cols(n2), (cuuint32_t)box_rows, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(p), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, ch == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,

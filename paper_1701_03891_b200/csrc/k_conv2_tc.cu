@@ -18,7 +18,8 @@
 // Work unit = (image b, R = 6 output rows from r0, <=64 output columns from c0).  The strip of the unit
 // ((R+10) rows x (W+10) columns x 64 ch, bf16) is loaded by ONE 4-D TMA box whose out-of-bounds
 // elements are zero: that is the zero padding of Eq. (1) at the image border.
-// Positions are linear in the padded strip (pitch P = W+10); tiles of 256 positions overlap by 3.
+// Positions are linear in the padded strip (pitch P = W+5, or 74 for several column segments); tiles of 256
+// positions overlap by 3.
 //
 // Roles (256 threads): warp 0 producer (strip by TMA at unit start, 16-KB weight K-blocks by bulk copies into a
 // 4-deep ring), warp 1 single-thread MMA issuer (lean loop: prebuilt descriptors), warp 2 TMEM allocator,
@@ -326,7 +327,7 @@ static Geo make_geo(int batch, int n1, int n2) {
   Geo g;
   g.n1 = n1, g.n2 = n2;
   g.wseg = n2 < WSEG ? n2 : WSEG;
-  g.P = g.wseg + 10;
+  g.P = conv2_tc_box_cols(n2);
   g.nrb = (n1 + R - 1) / R;
   g.ncs = (n2 + g.wseg - 1) / g.wseg;
   g.units = batch * g.nrb * g.ncs;
@@ -343,7 +344,13 @@ size_t conv2_tc_smem_bytes(int n2) {
 // overlaps the MMAs of the previous unit removes the strip wait but measured slower on B200 (the TMA writes
 // compete with the UMMA operand reads for shared-memory bandwidth, which this kernel saturates: DESIGN.md §11).
 int conv2_tc_box_rows() { return R + 10; }
-int conv2_tc_box_cols(int n2) { return (n2 < WSEG ? n2 : WSEG) + 10; }
+// Strip pitch P (positions per strip row).  One column segment (n2 <= 64): P = n2 + 5 -- the box starts 5 columns
+// left of the image, so its 5 out-of-bounds (zero) columns are the left padding of a row AND the right padding of the
+// row above (a tap window c + v - 5 >= n2 runs into the next strip row's zero columns).  Several segments: the
+// halos are image data on both sides, P = 64 + 10.  P = 69 instead of 74 cuts the MMA columns per 6 x 64 output
+// block from 448 to 416; measured on B200 (same box, alternating): conv2 6.62 vs 6.75 ms (+1.7 %) -- the kernel
+// is bound by the shared-memory port, not by the MMA columns.
+int conv2_tc_box_cols(int n2) { return n2 <= WSEG ? n2 + 5 : WSEG + 10; }
 
 cudaError_t setup_conv2_tc(int n2) {
   cudaError_t e = cudaFuncSetAttribute(k_conv2_tc<64, 32, C2_BIAS_RELU>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -238,7 +238,7 @@ static GeoT make_geo_t(int batch, int n1, int n2) {
   GeoT g;
   g.n1 = n1, g.n2 = n2;
   g.wseg = n2 < WSEG ? n2 : WSEG;
-  g.P = g.wseg + 10;
+  g.P = conv_tf32_box_cols(n2);
   g.nrb = (n1 + R - 1) / R;
   g.ncs = (n2 + g.wseg - 1) / g.wseg;
   g.units = batch * g.nrb * g.ncs;
@@ -252,6 +252,9 @@ size_t conv2_tf32_smem_bytes(int n2) {
 }
 
 int conv2_tf32_box_rows() { return R + 10; }
+// strip pitch: n2 + 5 for one column segment (shared zero padding between rows, as conv2_tc_box_cols), else 74
+int conv_tf32_box_cols(int n2) { return n2 <= WSEG ? n2 + 5 : WSEG + 10; }
+int wgrad_box_cols(int n2) { return (n2 < WSEG ? n2 : WSEG) + 10; }
 
 int convg_tf32_kblocks(int cin, int cout) { return (cin / 32) * 11 * ((11 + 128 / cout - 1) / (128 / cout)); }
 

@@ -70,6 +70,8 @@ cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const fl
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st);
 size_t conv2_tf32_smem_bytes(int n2);
 int conv2_tf32_box_rows();
+int conv_tf32_box_cols(int n2);   // strip pitch of k_conv_tf32 (n2 + 5, or 74 with several column segments)
+int wgrad_box_cols(int n2);       // strip pitch W + 10 of the layer-2 wgrad / wgrad1 / wgrad3 operands
 cudaError_t setup_conv2_tf32(int n2);
 // generic TF32 layer C_in -> C_out, (C_in, C_out) in {32, 64}^2, bias + ReLU (deeper / wider stacks, NEXT-3);
 // wpack: convg_tf32_kblocks(cin, cout) blocks of 16 KB (api.cu conv_tf32_pack)
