@@ -233,13 +233,13 @@ di_status encode_wg2(CUtensorMap* map, const void* p, int batch, int n1, int n2,
   return DI_OK;
 }
 
-// dG2 [batch][n1][n2][32] bf16 as the strip of the bf16 layer-2 dgrad: box 32 ch x P x (R + 10) rows, SWIZZLE_64B
+// dG2 [batch][n1][n2][32] bf16 as the strip of the bf16 layer-2 dgrad: box 32 ch x P x (11 + 10) rows, SWIZZLE_64B
 di_status encode_dg2b_strip(CUtensorMap* map, const void* p, int batch, int n1, int n2) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[4] = {32, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
   cuuint64_t strides[3] = {32 * 2, (cuuint64_t)n2 * 32 * 2, (cuuint64_t)n1 * n2 * 32 * 2};
-  cuuint32_t box[4] = {32, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tf32_box_rows(), 1};
+  cuuint32_t box[4] = {32, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::dgrad2_bf16_box_rows(), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(p), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1209,7 +1209,9 @@ static di_status train_alloc(di_ctx c) {
       return s;
     CUDA_TRY(di::setup_wgrad2_tc(c->n2));
     CUDA_TRY(di::setup_wgrad13_tc(c->n2));
-    if (bf && (s = encode_wg2(&c->tmH2w, c->h2, c->max_batch, c->n1, c->n2, 32, di::wgrad3_tc_h_box_rows())) != DI_OK)
+    // the layer-3 wgrad's bf16 h2 strip: BF16 reads h2 itself, TF32 a bf16 copy of h2 made in the (then idle) h1b
+    if ((s = encode_wg2(&c->tmH2w, bf ? c->h2 : c->h1b, c->max_batch, c->n1, c->n2, 32, di::wgrad3_tc_h_box_rows())) !=
+        DI_OK)
       return s;
     if ((s = encode_wg2(&c->tmD1w, c->dh1b, c->max_batch, c->n1, c->n2, 64, di::wgrad1_tc_d_box_rows())) != DI_OK)
       return s;
@@ -1264,10 +1266,11 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   const float* h2 = reinterpret_cast<const float*>(c->h2);
   const bool tc = c->prec != DI_PREC_FP32;   // tensor-core backward (k_conv2_tc<32, 64>, k_wgrad*_tc, dgrad3)
   const bool bf = c->prec == DI_PREC_BF16;   // BF16 contexts: x_tilde, h1, h2 are bf16
-  if (tc)
-    CUDA_TRY(di::launch_wgrad3_tc(c->h2, c->dxh, batch, c->n1, c->n2, c->part_w2, c->part_b, flip, grads + n1w + n2w,
-                                  gb + C1 + C2, c->num_sms, st, bf, bf ? &c->tmH2w : nullptr));
-  else
+  if (tc) {   // bf16 h2 operand by TMA (TF32: rounded into h1b first -- the kernel rounds to bf16 either way)
+    if (!bf) CUDA_TRY(di::launch_to_bf16(h2, c->h1b, (size_t)batch * c->N * C2, st));
+    CUDA_TRY(di::launch_wgrad3_tc(bf ? c->h2 : c->h1b, c->dxh, batch, c->n1, c->n2, c->part_w2, c->part_b, flip,
+                                  grads + n1w + n2w, gb + C1 + C2, c->num_sms, st, true, &c->tmH2w));
+  } else
     CUDA_TRY(di::launch_wgrad(3, h2, c->dxh, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w + n2w,
                               gb + C1 + C2, st));
   if (tc && c->has_tmDX)

@@ -51,6 +51,11 @@ constexpr uint32_t WBYTES = C2_KBLOCK_BYTES;  // 16 KB
 constexpr int GUARD_ROWS = 24;
 constexpr int SPS = 36;                  // epilogue transpose row stride (floats): conflict-free float4 reads
 constexpr int ECH = 16;                  // epilogue chunk: output positions per TMEM load
+constexpr int C2_WST64 = 12;             // weight stages of the 64-B-row instance (8 KB each)
+// output rows per unit of the 64-B-row instance (the layer-2 dgrad): every tile restreams the 528 KB of packed weights,
+// and that stream bounds the instance, so its units are taller -- 3 tiles of ~253 outputs per 11-row unit (18 tiles
+// per 64-row image) instead of 2 of 253 + 156 per 6-row unit (22 tiles)
+constexpr int C2_DG_ROWS = 11;
 
 struct Geo {
   int n1, n2, wseg, P, nrb, ncs, units;
@@ -87,9 +92,9 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   constexpr int QPT = COUT / 32, CPT = COUT / 8;
   // epilogue groups: C_out = 64 (twice the epilogue work per tile) runs two groups of 4 warps, one per TMEM buffer
   constexpr int EG = COUT == 64 ? 2 : 1;
-  // weight ring: the same 64 KB in blocks of WB bytes (8 stages of 8 KB for 64-B rows: the lead must cover the
-  // ~1.4k-cycle bulk-copy latency in MMA time)
-  constexpr int WST = WSTAGES * 128 / RB;
+  // weight ring: 4 stages of 16 KB for 128-B rows; 12 stages of 8 KB for 64-B rows (the layer-2 dgrad)
+  constexpr int WST = RB == 128 ? WSTAGES : C2_WST64;
+  constexpr int R = RB == 128 ? C2_ROWS : C2_DG_ROWS;   // output rows per unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int strip_bytes = (R + 10) * g.P * RB;
@@ -253,8 +258,33 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
         mbar_wait(&tfull[buf], (ti >> 1) & 1);
         tc_fence_after();
         const uint32_t tq = tmem + buf * 256 + ((uint32_t)(q * 32) << 16);
+        // this thread's output of chunk cb (reduce role): valid?, pixel index
+        auto outpos = [&](int cb, size_t& pix) {
+          const int o = n0 + cb + jj;
+          const int rr = o / g.P, cc = o - rr * g.P;
+          const int orow = r0 + rr, ocol = c0 + cc;
+          pix = ((size_t)b * g.n1 + orow) * g.n2 + ocol;
+          return jj < min(ECH, cnt - cb) && cc < g.wseg && ocol < g.n2 && rr < rows;
+        };
+        // ReLU' mask of the thread's output, loaded one chunk ahead (its global latency overlaps a whole chunk)
+        uint2 mn[CPT / 4];
+        auto mask_ld = [&](int cb) {
+          size_t px;
+          const bool v = outpos(cb, px);
+#pragma unroll
+          for (int v4 = 0; v4 < CPT / 4; ++v4)
+            mn[v4] = v ? __ldg(reinterpret_cast<const uint2*>(mask + px * COUT + c0ch + 4 * v4)) : make_uint2(0, 0);
+        };
+        if (MODE == C2_MASK) mask_ld(0);
         for (int c = 0; c < cnt; c += ECH) {
-          const int nout = min(ECH, cnt - c);
+          size_t pix;
+          const bool ok = outpos(c, pix);
+          uint2 mm[CPT / 4];
+          if (MODE == C2_MASK) {
+#pragma unroll
+            for (int v4 = 0; v4 < CPT / 4; ++v4) mm[v4] = mn[v4];
+            if (c + ECH < cnt) mask_ld(c + ECH);
+          }
           uint32_t r[ECH];
           if (c + shift + ECH <= NT)
             tmem_ld16(tq + c + shift, r);
@@ -274,12 +304,8 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
 #pragma unroll
           for (int j = 0; j < ECH; ++j) dst[j * SPS] = __uint_as_float(r[j]);
           named_bar(1 + grp, 128);
-          if (jj < nout) {
-            const int o = n0 + c + jj;
-            const int rr = o / g.P, cc = o - rr * g.P;
-            const int orow = r0 + rr, ocol = c0 + cc;
-            if (cc < g.wseg && ocol < g.n2 && rr < rows) {
-              const size_t pix = ((size_t)b * g.n1 + orow) * g.n2 + ocol;
+          {
+            if (ok) {
 #pragma unroll
               for (int v4 = 0; v4 < CPT / 4; ++v4) {
                 float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -292,11 +318,11 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
                 const size_t off = pix * COUT + c0ch + 4 * v4;
                 uint2 v;
                 if (MODE == C2_MASK) {
-                  const uint2 mm = __ldg(reinterpret_cast<const uint2*>(mask + off));
-                  v.x = pack_bf16x2(__uint_as_float(mm.x << 16) > 0.f ? sum.x : 0.f,
-                                    __uint_as_float(mm.x & 0xffff0000u) > 0.f ? sum.y : 0.f);
-                  v.y = pack_bf16x2(__uint_as_float(mm.y << 16) > 0.f ? sum.z : 0.f,
-                                    __uint_as_float(mm.y & 0xffff0000u) > 0.f ? sum.w : 0.f);
+                  const uint2 m2 = mm[v4];
+                  v.x = pack_bf16x2(__uint_as_float(m2.x << 16) > 0.f ? sum.x : 0.f,
+                                    __uint_as_float(m2.x & 0xffff0000u) > 0.f ? sum.y : 0.f);
+                  v.y = pack_bf16x2(__uint_as_float(m2.y << 16) > 0.f ? sum.z : 0.f,
+                                    __uint_as_float(m2.y & 0xffff0000u) > 0.f ? sum.w : 0.f);
                 } else {
                   if (fullmap && bias) {
                     const float4 a = *reinterpret_cast<const float4*>(bias + pix % ((size_t)g.n1 * g.n2) * COUT + c0ch + 4 * v4);
@@ -323,7 +349,7 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-static Geo make_geo(int batch, int n1, int n2) {
+static Geo make_geo(int batch, int n1, int n2, int R = C2_ROWS) {
   Geo g;
   g.n1 = n1, g.n2 = n2;
   g.wseg = n2 < WSEG ? n2 : WSEG;
@@ -335,15 +361,22 @@ static Geo make_geo(int batch, int n1, int n2) {
 }
 
 size_t conv2_tc_smem_bytes(int n2) {
-  const int wseg = n2 < WSEG ? n2 : WSEG, P = wseg + 10;
+  const int P = conv2_tc_box_cols(n2);
   const size_t strip_alloc = ((size_t)strip_rows_bytes(P) + GUARD_ROWS * 128 + 1023) & ~(size_t)1023;
   return strip_alloc + WSTAGES * WBYTES + 4 * ECH * SPS * 4 + 1024;
+}
+// <32, 64, C2_MASK>: strip of 64-B rows, C2_WST64 weight stages of 8 KB, two epilogue groups
+static size_t dgrad2_bf16_smem_bytes(int n2) {
+  const int wseg = n2 < WSEG ? n2 : WSEG, P = wseg + 10;
+  const size_t strip_alloc = ((size_t)(C2_DG_ROWS + 10) * P * 64 + GUARD_ROWS * 64 + 1023) & ~(size_t)1023;
+  return strip_alloc + (size_t)C2_WST64 * 8192 + 2 * 4 * ECH * SPS * 4 + 1024;
 }
 
 // The strip is loaded in one box per unit.  Loading it as two halves with a separate producer so that the load
 // overlaps the MMAs of the previous unit removes the strip wait but measured slower on B200 (the TMA writes
 // compete with the UMMA operand reads for shared-memory bandwidth, which this kernel saturates: DESIGN.md §11).
 int conv2_tc_box_rows() { return R + 10; }
+int dgrad2_bf16_box_rows() { return C2_DG_ROWS + 10; }
 // Strip pitch P (positions per strip row).  One column segment (n2 <= 64): P = n2 + 5 -- the box starts 5 columns
 // left of the image, so its 5 out-of-bounds (zero) columns are the left padding of a row AND the right padding of the
 // row above (a tap window c + v - 5 >= n2 runs into the next strip row's zero columns).  Several segments: the
@@ -357,7 +390,7 @@ cudaError_t setup_conv2_tc(int n2) {
                                        (int)conv2_tc_smem_bytes(n2));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_conv2_tc<32, 64, C2_MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)conv2_tc_smem_bytes(n2));
+                              (int)dgrad2_bf16_smem_bytes(n2));
 }
 
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
@@ -371,13 +404,13 @@ cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const fl
 }
 
 // training: the layer-2 data gradient on the bf16 layer-2 machinery (TMEM double buffering, weights per tile):
-// tmDGb = dG2 [B][n1][n2][32] bf16 strips (box 32 ch x P x (R + 10) rows, SWIZZLE_64B), wpack = 66 x 8-KB blocks
+// tmDGb = dG2 [B][n1][n2][32] bf16 strips (box 32 ch x P x (C2_DG_ROWS + 10) rows, SWIZZLE_64B), wpack = 66 x 8-KB blocks
 // (rows v' * 64 + ci, 32 co, SWIZZLE_64B), h1b = bf16 h1 (the ReLU' mask), dh1b = bf16 output
 cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, const void* h1b, int batch, int n1, int n2,
                                void* dh1b, int num_sms, cudaStream_t st) {
-  Geo g = make_geo(batch, n1, n2);
+  Geo g = make_geo(batch, n1, n2, C2_DG_ROWS);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  k_conv2_tc<32, 64, C2_MASK><<<grid, 384, conv2_tc_smem_bytes(n2), st>>>(
+  k_conv2_tc<32, 64, C2_MASK><<<grid, 384, dgrad2_bf16_smem_bytes(n2), st>>>(
       *tmDGb, reinterpret_cast<const __nv_bfloat16*>(wpack), nullptr, 0, g, reinterpret_cast<__nv_bfloat16*>(dh1b),
       reinterpret_cast<const __nv_bfloat16*>(h1b));
   return cudaGetLastError();

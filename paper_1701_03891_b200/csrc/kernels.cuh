@@ -66,6 +66,7 @@ cudaError_t setup_conv2_tc(int n2);
 size_t conv2_tc_smem_bytes(int n2);
 int conv2_tc_box_rows();
 int conv2_tc_box_cols(int n2);
+int dgrad2_bf16_box_rows();
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st);
 size_t conv2_tf32_smem_bytes(int n2);
