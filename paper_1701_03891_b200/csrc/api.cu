@@ -1273,14 +1273,18 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   } else
     CUDA_TRY(di::launch_wgrad(3, h2, c->dxh, batch, c->n1, c->n2, c->part_w, c->part_b, flip, grads + n1w + n2w,
                               gb + C1 + C2, st));
-  if (tc && c->has_tmDX)
-    CUDA_TRY(di::launch_dgrad3_tf32(&c->tmDX, c->wpd3, c->h2, c->dh2, batch, c->n1, c->n2, c->num_sms, st, bf));
+  const bool dg3tc = tc && c->has_tmDX;   // tensor-core dgrad3 writes bf16 dG2 and the layer-2 bias gradient itself
+  if (dg3tc)
+    CUDA_TRY(di::launch_dgrad3_tf32(&c->tmDX, c->wpd3, c->h2, c->dg2b, c->part_b, gb + C1, batch, c->n1, c->n2,
+                                    c->num_sms, st, bf));
   else
     CUDA_TRY(di::launch_dgrad3_f32(c->dxh, c->wt3, h2, c->dh2, batch, c->n1, c->n2, st));
   if (tc) {   // bf16 operands, tcgen05 MN-major contraction over pixels (k_wgrad2_tc.cu)
     const size_t npix = (size_t)batch * c->N;
-    CUDA_TRY(di::launch_dg2_bf16(c->dh2, npix, c->dg2b, c->part_b, st));
-    CUDA_TRY(di::launch_bias_reduce(c->part_b, di::WGRAD_CHUNKS, C2, gb + C1, st));
+    if (!dg3tc) {
+      CUDA_TRY(di::launch_dg2_bf16(c->dh2, npix, c->dg2b, c->part_b, st));
+      CUDA_TRY(di::launch_bias_reduce(c->part_b, di::WGRAD_CHUNKS, C2, gb + C1, st));
+    }
     if (!bf) CUDA_TRY(di::launch_to_bf16(h1, c->h1b, npix * C1, st));   // (BF16: h1 is the bf16 operand)
     CUDA_TRY(di::launch_wgrad2_tc(&c->tmH1b, &c->tmDG2b, batch, c->n1, c->n2, c->part_w2, flip, grads + n1w,
                                   c->num_sms, st));

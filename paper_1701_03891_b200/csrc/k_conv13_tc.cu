@@ -392,7 +392,7 @@ template <int COUT, bool DG3>
 __global__ void __launch_bounds__(384, 1)
     k_conv1_tf32(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ w1pack,
                  const float* __restrict__ bias, int fullmap, Geo13 g, float* __restrict__ h1,
-                 const void* __restrict__ mask, int mask_bf16) {
+                 const void* __restrict__ mask, int mask_bf16, float* __restrict__ part_b) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* wbuf = smem;                                 // 44 KB
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int n0 = 0; n0 < npos; n0 += 256, ++ti) {
           const int cnt = min(256, npos - n0);
           const int N = cnt > 128 ? 256 : (cnt > 64 ? 128 : 64);
-          const uint32_t idesc = idesc_f32acc(2, 64, N);
+          const uint32_t idesc = idesc_f32acc(2, DG3 ? 32 : 64, N);   // DG3: 32 bank rows, .ws M = 32
           const int a = ti % NACC;
           if (ti >= NACC) mbar_wait(&acc_empty[a], ((ti / NACC) - 1) & 1);
           tc_fence_after();
@@ -503,6 +503,10 @@ __global__ void __launch_bounds__(384, 1)
     const float b0 = (!fullmap && bias && ch < COUT) ? bias[ch] : 0.f;
     const float b1 = (!fullmap && bias && ch < COUT) ? bias[ch + 1] : 0.f;
     const uint32_t wmagic = (1u << 20) / (uint32_t)W + 1;
+    // DG3: .ws M = 32 puts D columns [qN/4, (q+1)N/4) in lane quadrant q, so all 8 warps hold channels
+    // 16 hh + 2 i4 (+1) of their quadrant's positions; the layer-2 bias gradient (sum of dG2) is summed per thread
+    const int ch3 = 16 * hh + 2 * i4;
+    float bs0 = 0.f, bs1 = 0.f;
     int ti = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
       const int b = u / per_img, rem = u - b * per_img;
@@ -517,13 +521,70 @@ __global__ void __launch_bounds__(384, 1)
         const int a = ti % NACC;
         mbar_wait(&acc_full[a], (ti / NACC) & 1);
         tc_fence_after();
+        if (DG3) {
+          const int quarter = N / 4;
+          const int pbq = n0 + q * quarter;
+          const uint32_t taddr3 = tmem + a * 128 + ((uint32_t)(q * 32 + 16 * hh) << 16);
+          for (int c = 0; c < quarter; c += 32) {
+            uint32_t r[16];
+            tmem_ld_16x256b_x4(taddr3 + c, r);
+            tmem_ld_wait();
+            size_t pixv[8];
+            bool ok[8];
+            float2 m[8];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {   // all 8 mask loads in flight before the stores
+              const int j = c + 8 * (kk >> 1) + cpair + (kk & 1);
+              const int p = pbq + j;
+              ok[kk] = j < quarter && p < n0 + cnt;
+              if (linear) {
+                pixv[kk] = pix0 + p;
+              } else {
+                const int rr = (int)(((uint32_t)p * wmagic) >> 20), cc = p - rr * W;
+                ok[kk] = ok[kk] && c0 + cc < g.n2;
+                pixv[kk] = pix0 + (size_t)rr * g.n2 + cc;
+              }
+            }
+            if (mask_bf16) {   // BF16 contexts: h2 is bf16 (branch hoisted so the 8 loads issue back to back)
+              uint32_t mb[8];
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                mb[kk] = ok[kk] ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const __nv_bfloat16*>(mask) +
+                                                                         pixv[kk] * 32 + ch3))
+                                : 0u;
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                m[kk] = make_float2(__uint_as_float(mb[kk] << 16), __uint_as_float(mb[kk] & 0xffff0000u));
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                m[kk] = ok[kk] ? __ldg(reinterpret_cast<const float2*>(reinterpret_cast<const float*>(mask) +
+                                                                       pixv[kk] * 32 + ch3))
+                               : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {   // dG2 = [h2 > 0] dH2 in bf16 (the dgrad2 / wgrad2 operand)
+              const float v0 = m[kk].x > 0.f ? __uint_as_float(r[4 * (kk >> 1) + (kk & 1)]) : 0.f;
+              const float v1 = m[kk].y > 0.f ? __uint_as_float(r[4 * (kk >> 1) + 2 + (kk & 1)]) : 0.f;
+              if (ok[kk]) {
+                bs0 += v0, bs1 += v1;
+                *reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(h1) + pixv[kk] * 32 + ch3) =
+                    pack_bf16x2(v0, v1);
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[a]);
+          continue;
+        }
         const int pbase = n0 + (q >> 1) * half;
         const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32 + 16 * hh) << 16);
         for (int c = 0; c < half && ch < COUT; c += 32) {   // warps of bank rows >= COUT idle
           uint32_t r[16];
           tmem_ld_16x256b_x4(taddr + c, r);
           tmem_ld_wait();
-          if (DG3) {   // all 8 mask loads in flight before the stores
+          if (DG3) {   // (not reached: DG3 runs the M = 32 epilogue above)
             size_t pixv[8];
             bool ok[8];
             float2 m[8];
@@ -593,6 +654,19 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[a]);
+      }
+    }
+    if (DG3) {   // per-CTA layer-2 bias partials: channel j = sum over its 16 threads in a fixed order
+      __shared__ float sb[256][2];
+      const int e = threadIdx.x - 128;
+      sb[e][0] = bs0, sb[e][1] = bs1;
+      named_bar(3, 256);
+      if (e < 32) {
+        const int h = e >> 4, i = (e & 15) >> 1, w01 = e & 1;
+        float t = 0.f;
+        for (int qq = 0; qq < 4; ++qq)
+          for (int l4 = 0; l4 < 4; ++l4) t += sb[(h * 4 + qq) * 32 + i * 4 + l4][w01];
+        part_b[(size_t)blockIdx.x * 32 + e] = t;
       }
     }
   }
@@ -827,7 +901,7 @@ cudaError_t launch_conv1_tf32(const CUtensorMap* tmX, const void* w1pack, const 
   Geo13 g = make_geo13(batch, n1, n2, R1T, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
   k_conv1_tf32<64, false><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack),
-                                                                      bias, fullmap, g, h1, nullptr, 0);
+                                                                      bias, fullmap, g, h1, nullptr, 0, nullptr);
   return cudaGetLastError();
 }
 
@@ -838,17 +912,22 @@ cudaError_t launch_conv1g_tf32(int cout, const CUtensorMap* tmX, const void* w1p
   Geo13 g = make_geo13(batch, n1, n2, R1T, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
   k_conv1_tf32<32, false><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmX, reinterpret_cast<const uint8_t*>(w1pack),
-                                                                      bias, 0, g, out, nullptr, 0);
+                                                                      bias, 0, g, out, nullptr, 0, nullptr);
   return cudaGetLastError();
 }
 
-cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const void* h2, float* dh2, int batch,
-                               int n1, int n2, int num_sms, cudaStream_t st, bool h2_bf16) {
+// dG2 = [h2 > 0] * dgrad3(dG3) written in bf16 (dg2b: the operand of wgrad2 and dgrad2) and the layer-2 bias
+// gradient gb2[32] = sum of dG2 (per-CTA partials in part_b, then a fixed-order fp64 reduction)
+cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const void* h2, void* dg2b, float* part_b,
+                               float* gb2, int batch, int n1, int n2, int num_sms, cudaStream_t st, bool h2_bf16) {
   Geo13 g = make_geo13(batch, n1, n2, R1T, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
   k_conv1_tf32<32, true><<<grid, 384, conv1_tf32_smem_bytes(), st>>>(*tmDX, reinterpret_cast<const uint8_t*>(wpack),
-                                                                     nullptr, 0, g, dh2, h2, h2_bf16 ? 1 : 0);
-  return cudaGetLastError();
+                                                                     nullptr, 0, g, reinterpret_cast<float*>(dg2b), h2,
+                                                                     h2_bf16 ? 1 : 0, part_b);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_bias_reduce(part_b, grid, 32, gb2, st);
 }
 
 cudaError_t setup_conv13_tc(int n2) {

@@ -146,8 +146,9 @@ cudaError_t launch_conv1g_tf32(int cout, const CUtensorMap* tmX, const void* w1p
 // custom stacks, FP32 SIMT: (cin, cout) in {(1,32), (1,64), (32,32), (32,64), (64,32), (64,64)}, bias + ReLU
 cudaError_t launch_convg_simt(int cin, int cout, const float* in, const float* wx, const float* bias, float* out,
                               int batch, int n1, int n2, cudaStream_t st);
-cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const void* h2, float* dh2, int batch,
-                               int n1, int n2, int num_sms, cudaStream_t st, bool h2_bf16 = false);
+// training: dG2 = [h2 > 0] * (layer-3 dgrad of dG3) in bf16 + the layer-2 bias gradient (k_conv1_tf32<32, true>)
+cudaError_t launch_dgrad3_tf32(const CUtensorMap* tmDX, const void* wpack, const void* h2, void* dg2b, float* part_b,
+                               float* gb2, int batch, int n1, int n2, int num_sms, cudaStream_t st, bool h2_bf16);
 // training, TF32 contexts: layer-2 weight gradient on tcgen05 from bf16 copies of h1 / dG2 (k_wgrad2_tc.cu)
 constexpr int WG2_ROWS = 6;
 size_t wgrad2_tc_smem_bytes(int n2);
