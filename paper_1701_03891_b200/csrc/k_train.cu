@@ -57,13 +57,12 @@ cudaError_t launch_dgrad_mask(float* d, const float* y, size_t n, cudaStream_t s
   return cudaGetLastError();
 }
 
-// sum of per-image losses in image order (deterministic) -> loss[0]
+// sum of per-image losses -> loss[0]: lane l sums images l, l + 32, ... then a fixed butterfly (deterministic)
 __global__ void k_sum_f64(const double* __restrict__ v, int n, double* __restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < n; ++i) t += v[i];
-    *out = t;
-  }
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) t += v[i];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (threadIdx.x == 0) *out = t;
 }
 
 cudaError_t launch_loss_grad(const float* xhat, const float* x, int N, int batch, double scale, float* dxhat,

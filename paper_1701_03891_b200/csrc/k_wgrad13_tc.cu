@@ -86,6 +86,24 @@ __global__ void __launch_bounds__(128, 1)
   const int cg = tid & 7;   // fixed 8-channel group of this thread's dG1 chunks (bias partials)
   float bs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const uint32_t id = idesc_f32acc(1, 128, 64, 1, 1);
+  // this thread's x~ halo-strip values of unit un: q = tid + 128 uu (NX <= 17 * 74 + 32 <= 128 XPT)
+  constexpr int XPT = 11;
+  uint32_t xv[XPT];   // raw bits (bf16 zero-extended, or fp32): converted only where they are stored, so the loads
+                      // stay in flight until then
+  auto load_x = [&](int un, uint32_t* v) {
+    const int bb = un / per_img, rm = un - bb * per_img;
+    const int rr0 = (rm / g.ncs) * R, cc0 = (rm % g.ncs) * g.wseg;
+#pragma unroll
+    for (int uu = 0; uu < XPT; ++uu) {
+      const int q = tid + uu * 128, row = q / P, col = q - row * P;
+      const int gr = rr0 - 5 + row, gc = cc0 - 5 + col;
+      const size_t xi = ((size_t)bb * g.n1 + gr) * g.n2 + gc;
+      v[uu] = (q < NX && gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2)
+                  ? (xbf ? (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(xt) + xi)
+                         : __ldg(reinterpret_cast<const uint32_t*>(xt) + xi))
+                  : 0u;
+    }
+  };
   int it = 0;
   uint32_t acc = 0;
   for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
@@ -126,23 +144,11 @@ __global__ void __launch_bounds__(128, 1)
         *reinterpret_cast<uint4*>(d1 + (16 + q) * 128 + ((cg ^ (q & 7)) << 4)) = w;
       }
     }
-    // x~ strip with halo: xs[q] = x~(r0 - 5 + q / P, c0 - 5 + q % P)
-    for (int q0 = tid; q0 < NX; q0 += 128 * 8) {
-      float v[8];
+    // x~ strip with halo: xs[q] = x~(r0 - 5 + q / P, c0 - 5 + q % P), loaded into registers one unit ahead
+    if (it == 0) load_x(u, xv);
 #pragma unroll
-      for (int uu = 0; uu < 8; ++uu) {
-        const int q = q0 + uu * 128, row = q / P, col = q - row * P;
-        const int gr = r0 - 5 + row, gc = c0 - 5 + col;
-        const size_t xi = ((size_t)b * g.n1 + gr) * g.n2 + gc;
-        v[uu] = (q < NX && gr >= 0 && gr < g.n1 && gc >= 0 && gc < g.n2)
-                    ? (xbf ? __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(xt) + xi))
-                           : __ldg(reinterpret_cast<const float*>(xt) + xi))
-                    : 0.f;
-      }
-#pragma unroll
-      for (int uu = 0; uu < 8; ++uu)
-        if (q0 + uu * 128 < NX) xs[q0 + uu * 128] = v[uu];
-    }
+    for (int uu = 0; uu < XPT; ++uu)
+      if (tid + uu * 128 < NX) xs[tid + uu * 128] = __uint_as_float(xbf ? xv[uu] << 16 : xv[uu]);
     if (use_tma) {
       mbar_wait(&dbar[s], (it >> 1) & 1);
       if (g.ncs > 1)   // columns wseg .. P-1 of each row belong to the next segment
@@ -183,6 +189,7 @@ __global__ void __launch_bounds__(128, 1)
       }
       umma_commit(&done[s]);
     }
+    if (u + (int)gridDim.x < g.units) load_x(u + gridDim.x, xv);   // in flight across the MMAs and the next TMA wait
     __syncthreads();   // xs is rewritten by the next unit's loaders
   }
   if (tid == 0) umma_commit(&fin);
@@ -213,21 +220,44 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 // gw1 [64][11][11] (API orientation), gb1 [64]
-__global__ void k_wgrad1_reduce(const float* __restrict__ part, const float* __restrict__ part_b, int nct, int flip,
-                                float* __restrict__ gw, float* __restrict__ gb) {
-  constexpr int NW = 64 * KS * KS;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NW + 64; i += gridDim.x * blockDim.x) {
-    double t = 0.0;
-    if (i < NW) {
-      const int bb = i % KS, a = (i / KS) % KS, co = i / (KS * KS);
-      const int m = a <= 7 ? a * 16 + bb : (a - 3) * 16 + bb, n = a <= 7 ? co : 64 + co;
-      for (int c = 0; c < nct; ++c) t += part[((size_t)c * 128 + m) * 128 + n];
-      gw[(size_t)co * KS * KS + (flip ? (KS - 1 - a) * KS + (KS - 1 - bb) : a * KS + bb)] = (float)t;
-    } else {
-      for (int c = 0; c < nct; ++c) t += part_b[(size_t)c * 64 + (i - NW)];
-      gb[i - NW] = (float)t;
-    }
+// Deterministic sums over the CTA partials: a block owns 32 consecutive partial elements (coalesced reads) x 8 slices
+// of the CTA index, combined in a fixed order in fp64.  L = 1: part [c][128][128] (m = tap slot, n = co / 64 + co),
+// L = 3: part [c][128][48]; blockIdx.y = 1 sums the bias partials (part_b [c][nb]).
+template <int L>
+__global__ void __launch_bounds__(256) k_wgrad13_reduce(const float* __restrict__ part, const float* __restrict__ part_b,
+                                                        int nct, int flip, float* __restrict__ gw,
+                                                        float* __restrict__ gb) {
+  constexpr int NCOLS = L == 1 ? 128 : 48, E = 128 * NCOLS, NB = L == 1 ? 64 : 1;
+  __shared__ double sh[8][33];
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  const bool bias = blockIdx.y == 1;
+  const int e = blockIdx.x * 32 + lx, ne = bias ? NB : E;
+  if (bias && blockIdx.x * 32 >= NB) return;
+  const float* p = (bias ? part_b : part) + e;
+  double t = 0.0;
+  if (e < ne)
+    for (int c = ly; c < nct; c += 8) t += p[(size_t)c * ne];
+  sh[ly][lx] = t;
+  __syncthreads();
+  if (ly != 0 || e >= ne) return;
+  for (int k = 1; k < 8; ++k) t += sh[k][lx];
+  if (bias) {
+    gb[e] = (float)t;
+    return;
   }
+  const int m = e / NCOLS, n = e % NCOLS;
+  int a, bb, ch;
+  if (L == 1) {   // m = a * 16 + bb (a <= 7, n = co) or (a - 3) * 16 + bb (a >= 8, n = 64 + co)
+    bb = m % 16, ch = n % 64;
+    a = n < 64 ? m / 16 : m / 16 + 3;
+    if (bb >= KS || (n >= 64 && a < 8) || a >= KS) return;
+  } else {        // m = ii * 32 + ci, n = grp * 16 + bb; a = ii (grp 0), 4 + ii (grp 1), 7 + ii (grp 2, ii >= 1)
+    const int grp = n / 16, ii = m / 32;
+    bb = n % 16, ch = m % 32;
+    a = grp == 0 ? ii : grp == 1 ? 4 + ii : 7 + ii;
+    if (bb >= KS || (grp == 2 && ii == 0)) return;
+  }
+  gw[(size_t)ch * KS * KS + (flip ? (KS - 1 - a) * KS + (KS - 1 - bb) : a * KS + bb)] = (float)t;
 }
 
 // =============================================================================================== layer 3
@@ -372,24 +402,6 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 // gw3 [32][11][11] (API orientation of W3 [1][32][11][11]), gb3 [1]
-__global__ void k_wgrad3_reduce(const float* __restrict__ part, const float* __restrict__ part_b, int nct, int flip,
-                                float* __restrict__ gw, float* __restrict__ gb) {
-  constexpr int NW = 32 * KS * KS;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NW + 1; i += gridDim.x * blockDim.x) {
-    double t = 0.0;
-    if (i < NW) {
-      const int bb = i % KS, a = (i / KS) % KS, ci = i / (KS * KS);
-      const int grp = a < 4 ? 0 : a < 8 ? 1 : 2, ii = a - (grp == 0 ? 0 : grp == 1 ? 4 : 7);
-      const int m = ii * 32 + ci, n = grp * 16 + bb;
-      for (int c = 0; c < nct; ++c) t += part[((size_t)c * 128 + m) * 48 + n];
-      gw[(size_t)ci * KS * KS + (flip ? (KS - 1 - a) * KS + (KS - 1 - bb) : a * KS + bb)] = (float)t;
-    } else {
-      for (int c = 0; c < nct; ++c) t += part_b[c];
-      gb[0] = (float)t;
-    }
-  }
-}
-
 // =============================================================================================== host
 static GeoT13 make_geo(int batch, int n1, int n2, bool l1) {
   GeoT13 g;
@@ -438,7 +450,7 @@ cudaError_t launch_wgrad1_tc(const void* xt, const void* dg1, int batch, int n1,
   k_wgrad1_tc<<<grid, 128, smem_bytes(n2, true), st>>>(xt, reinterpret_cast<const __nv_bfloat16*>(dg1), g, part,
                                                        part_b, xt_bf16 ? 1 : 0, tmD1 ? *tmD1 : dummy,
                                                        tmD1 ? 1 : 0);
-  k_wgrad1_reduce<<<(64 * KS * KS + 64 + 255) / 256, 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
+  k_wgrad13_reduce<1><<<dim3(128 * 128 / 32, 2), 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
   return cudaGetLastError();
 }
 
@@ -453,7 +465,7 @@ cudaError_t launch_wgrad3_tc(const void* h2, const float* dg3, int batch, int n1
   const int use_tma = (h2_bf16 && tmH2) ? 1 : 0;
   k_wgrad3_tc<<<grid, 128, smem_bytes(n2, false), st>>>(h2, dg3, g, part, part_b, h2_bf16 ? 1 : 0,
                                                         use_tma ? *tmH2 : dummy, use_tma);
-  k_wgrad3_reduce<<<(32 * KS * KS + 1 + 255) / 256, 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
+  k_wgrad13_reduce<3><<<dim3(128 * 48 / 32, 2), 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
   return cudaGetLastError();
 }
 

@@ -156,18 +156,27 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-// gw (API orientation, [co][ci][u][v]) = sum over the role's CTAs (fp64, fixed order)
-__global__ void k_wgrad2_reduce(const float* __restrict__ part, int nper, int flip, float* __restrict__ gw) {
-  constexpr int NW = 32 * 64 * KS * KS;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NW; i += gridDim.x * blockDim.x) {
-    const int b = i % KS, a = (i / KS) % KS, ci = (i / (KS * KS)) % 64, co = i / (KS * KS * 64);
-    const int role = a / 2, m = (a % 2) * 64 + ci;
-    const int n = b <= 7 ? (7 - b) * 32 + co : 256 + (10 - b) * 32 + co;
-    const float* p = part + ((size_t)role * nper * 128 + m) * NCOL + n;
-    double t = 0.0;
-    for (int c = 0; c < nper; ++c) t += p[(size_t)c * 128 * NCOL];
-    gw[((size_t)co * 64 + ci) * KS * KS + (flip ? (KS - 1 - a) * KS + (KS - 1 - b) : a * KS + b)] = (float)t;
-  }
+// gw (API orientation, [co][ci][u][v]) = sum over the role's CTAs (fp64, fixed order).  A block owns 32 consecutive
+// partial elements (coalesced reads) x 8 slices of the CTA index; the slices are combined in a fixed order.
+__global__ void __launch_bounds__(256) k_wgrad2_reduce(const float* __restrict__ part, int nper, int flip,
+                                                       float* __restrict__ gw) {
+  constexpr int E = 128 * NCOL;
+  __shared__ double sh[8][33];
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5, role = blockIdx.y;
+  const int e = blockIdx.x * 32 + lx;
+  const float* p = part + (size_t)role * nper * E + e;
+  double t = 0.0;
+  if (e < E)
+    for (int c = ly; c < nper; c += 8) t += p[(size_t)c * E];
+  sh[ly][lx] = t;
+  __syncthreads();
+  if (ly != 0 || e >= E) return;
+  for (int k = 1; k < 8; ++k) t += sh[k][lx];
+  const int m = e / NCOL, n = e % NCOL;
+  const int a = role * 2 + m / 64, ci = m % 64;
+  if (a >= KS) return;                                  // row tap 11 of the last role: discarded
+  const int b = n < 256 ? 7 - n / 32 : 10 - (n - 256) / 32, co = n % 32;
+  gw[((size_t)co * 64 + ci) * KS * KS + (flip ? (KS - 1 - a) * KS + (KS - 1 - b) : a * KS + b)] = (float)t;
 }
 
 // fp32 -> bf16 copy (n multiple of 8)
@@ -246,7 +255,7 @@ cudaError_t launch_wgrad2_tc(const CUtensorMap* tmH, const CUtensorMap* tmG, int
                              int flip, float* gw, int num_sms, cudaStream_t st) {
   GeoW g = make_geo_w(batch, n1, n2, num_sms);
   k_wgrad2_tc<<<NROLE * g.nper, 128, wgrad2_tc_smem_bytes(n2), st>>>(*tmH, *tmG, g, part);
-  k_wgrad2_reduce<<<(32 * 64 * KS * KS + 255) / 256, 256, 0, st>>>(part, g.nper, flip, gw);
+  k_wgrad2_reduce<<<dim3(128 * NCOL / 32, NROLE), 256, 0, st>>>(part, g.nper, flip, gw);
   return cudaGetLastError();
 }
 
