@@ -127,6 +127,21 @@ def test_invariants_bitwise(precision):
     assert np.all(zero == 0), "y = 0 -> x_hat = 0"
 
 
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+def test_shard_outputs_bitwise_identical(precision):
+    """SURVEY.md §8(e) check: the batch-sharded path (rank r recovers images [r B/G, (r+1) B/G))
+    gives bitwise the outputs of the unsharded batch for G = 1, 2, 4, 8 -- per-image arithmetic does not depend on
+    the batch size or on which persistent CTA a unit lands on."""
+    case = Case(64, 64, 410, 512, precision)
+    ctx = make_ctx(case, max_batch=512)
+    y = y_device(case, ctx)
+    whole = ctx.recover(y).cpu().numpy()
+    for g in (2, 4, 8):
+        per = 512 // g
+        parts = [ctx.recover(y[r * per:(r + 1) * per].contiguous()).cpu().numpy() for r in range(g)]
+        assert np.array_equal(np.concatenate(parts), whole), f"G = {g}"
+
+
 def test_zero_weights_give_bias_only():
     p = synth.make_params(bias="channel")
     p0 = synth.Params([np.zeros_like(w) for w in p.w], p.b)
