@@ -31,6 +31,19 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Build if stale.  Serialised across processes by an exclusive lock (torchrun ranks of bench.py, pytest
+    workers), so concurrent callers never write the same object files; a waiter finds the library fresh."""
+    import fcntl
+    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    with open(os.path.join(HERE, "build", ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            return _build_locked(force, verbose)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
+
+
+def _build_locked(force: bool, verbose: bool) -> str:
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "deepinverse.h"),
                                                                  os.path.abspath(__file__)]
     if not force and not _stale(LIB, deps):

@@ -584,49 +584,6 @@ __global__ void __launch_bounds__(384, 1)
           uint32_t r[16];
           tmem_ld_16x256b_x4(taddr + c, r);
           tmem_ld_wait();
-          if (DG3) {   // (not reached: DG3 runs the M = 32 epilogue above)
-            size_t pixv[8];
-            bool ok[8];
-            float2 m[8];
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const int p = pbase + c + 8 * (kk >> 1) + cpair + (kk & 1);
-              ok[kk] = p < n0 + cnt;
-              if (linear) {
-                pixv[kk] = pix0 + p;
-              } else {
-                const int rr = (int)(((uint32_t)p * wmagic) >> 20), cc = p - rr * W;
-                ok[kk] = ok[kk] && c0 + cc < g.n2;
-                pixv[kk] = pix0 + (size_t)rr * g.n2 + cc;
-              }
-            }
-            if (mask_bf16) {   // BF16 contexts: h2 is bf16 (branch hoisted so the 8 loads issue back to back)
-              uint32_t mb[8];
-#pragma unroll
-              for (int kk = 0; kk < 8; ++kk)
-                mb[kk] = ok[kk] ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const __nv_bfloat16*>(mask) +
-                                                                         pixv[kk] * 32 + ch))
-                                : 0u;
-#pragma unroll
-              for (int kk = 0; kk < 8; ++kk)
-                m[kk] = make_float2(__uint_as_float(mb[kk] << 16), __uint_as_float(mb[kk] & 0xffff0000u));
-            } else {
-#pragma unroll
-              for (int kk = 0; kk < 8; ++kk)
-                m[kk] = ok[kk] ? __ldg(reinterpret_cast<const float2*>(reinterpret_cast<const float*>(mask) +
-                                                                       pixv[kk] * 32 + ch))
-                               : make_float2(0.f, 0.f);
-            }
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const float v0 = __uint_as_float(r[4 * (kk >> 1) + (kk & 1)]);
-              const float v1 = __uint_as_float(r[4 * (kk >> 1) + 2 + (kk & 1)]);
-              if (ok[kk])
-                *reinterpret_cast<float2*>(h1 + pixv[kk] * 32 + ch) =
-                    make_float2(m[kk].x > 0.f ? v0 : 0.f, m[kk].y > 0.f ? v1 : 0.f);
-            }
-            continue;
-          }
 #pragma unroll
           for (int k = 0; k < 4; ++k)
 #pragma unroll
