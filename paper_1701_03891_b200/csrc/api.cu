@@ -79,7 +79,7 @@ struct di_ctx_s {
   unsigned flags = 0;
   size_t elt = 2;
   // device buffers
-  void* phi = nullptr;          // FP32: Phi [m][N] fp32 ; BF16/TF32: Phi^T [N][kpad] storage type
+  void* phi = nullptr;          // FP32: Phi [m][N] fp32 ; BF16/TF32: tile-blocked Phi^T (di::phiT_blk_index), storage type
   float* wx1 = nullptr;         // [1][11][11][64]   xcorr orientation, fp32 (bf16-rounded in BF16 mode)
   float* wx2 = nullptr;         // [64][11][11][32]
   float* wx3 = nullptr;         // [32][11][11][1]
@@ -150,6 +150,22 @@ di_status encode_2d(CUtensorMap* map, const void* base, bool bf16, int inner, in
                    const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (2d) failed: %d", (int)r);
+  return DI_OK;
+}
+
+// the tile-blocked Phi^T (di::phiT_blk_index) as [blocks][256 rows][kel]: box = one contiguous 32-KB block
+di_status encode_phiT_blk(CUtensorMap* map, const void* base, bool bf16, long long N, int kpad) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const int e = bf16 ? 2 : 4, kel = 128 / e;
+  cuuint64_t dims[3] = {(cuuint64_t)kel, 256, (cuuint64_t)((N + 255) / 256) * (cuuint64_t)(kpad / kel)};
+  cuuint64_t strides[2] = {128, 256 * 128};
+  cuuint32_t box[3] = {(cuuint32_t)kel, 256, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                   const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (Phi^T blocks) failed: %d", (int)r);
   return DI_OK;
 }
 
@@ -500,7 +516,7 @@ di_status run_proxy(di_ctx c, const void* y, long long ldy, int batch, void* xt,
     di_status s = encode_2d(&tmY, ysrc, bf16, inner, batch, ld, 128 / (int)c->elt, 128);
     if (s != DI_OK) return s;
     CUDA_TRY(di::launch_proxy_tc(&tmY, &c->tmPt, batch, c->N, c->kpad / (128 / (int)c->elt), xt, !bf16, st, out_f32,
-                                 sc));
+                                 sc, true));
     ++launches;
   }
   return DI_OK;
@@ -767,8 +783,9 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       float* tmp = nullptr;
       long long dummy = 0;
       STEP(upload(&tmp, phisrc, (size_t)a->m * N * 4, &dummy));
-      const size_t bytes = (size_t)N * c->kpad * c->elt;
+      const size_t bytes = di::phiT_blk_elems(N, c->kpad) * c->elt;   // tile-blocked, zero rows past N
       cudaError_t e = cudaMalloc(&c->phi, bytes);
+      if (e == cudaSuccess) e = cudaMemset(c->phi, 0, bytes);
       if (e != cudaSuccess) {
         cudaFree(tmp);
         free_ctx(c);
@@ -924,7 +941,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       free_ctx(c);
       return fail(DI_ERR_CUDA, "setup_proxy_tc: %s", cudaGetErrorString(e));
     }
-    STEP(encode_2d(&c->tmPt, c->phi, bf16, c->kpad, (int)N, c->kpad, 128 / (int)c->elt, 256));
+    STEP(encode_phiT_blk(&c->tmPt, c->phi, bf16, N, c->kpad));
   }
   if (bf16) {
     cudaError_t e = di::setup_conv2_tc(a->n2);
@@ -1402,13 +1419,15 @@ di_status di_debug_get_phi(di_ctx c, void* host_out, long long bytes) {
     CUDA_TRY(cudaMemcpy(host_out, c->phi, need, cudaMemcpyDeviceToHost));
     return DI_OK;
   }
-  // Phi^T [N][kpad] -> Phi [m][N]
-  std::vector<uint8_t> t((size_t)c->N * c->kpad * c->elt);
+  // tile-blocked Phi^T -> Phi [m][N]
+  std::vector<uint8_t> t(di::phiT_blk_elems(c->N, c->kpad) * c->elt);
   CUDA_TRY(cudaMemcpy(t.data(), c->phi, t.size(), cudaMemcpyDeviceToHost));
   uint8_t* o = reinterpret_cast<uint8_t*>(host_out);
+  const int kel = 128 / (int)c->elt;
   for (int i = 0; i < c->m; ++i)
     for (int j = 0; j < c->N; ++j)
-      std::memcpy(o + ((size_t)i * c->N + j) * c->elt, t.data() + ((size_t)j * c->kpad + i) * c->elt, c->elt);
+      std::memcpy(o + ((size_t)i * c->N + j) * c->elt, t.data() + di::phiT_blk_index(j, i, c->kpad, kel) * c->elt,
+                  c->elt);
   return DI_OK;
 }
 

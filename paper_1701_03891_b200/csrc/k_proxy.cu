@@ -10,6 +10,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "sm100.cuh"
 
@@ -23,33 +25,37 @@ constexpr int PX_STAGES = 4;
 
 // ELT: 2 = bf16 (kind::f16, K=16 per MMA), 4 = fp32 storage with kind::tf32 (K=8 per MMA).
 // OF32: fp32 output even for bf16 operands (row-sharded partial proxies, summed across ranks before rounding)
-template <int ELT, bool OF32 = (ELT == 4)>
+// MB: 128-image batch tiles per CTA.  MB = 2 gives each Phi^T K-block (32 KB) to two accumulators (TMEM 2 x 256
+// columns): per 1024 MMA cycles the SM ingests 64 KB instead of 2 x 48 KB -- what bounds the GEMM when Phi streams
+// from HBM (Stress: 2.15 GB of Phi, each CTA's L2 -> SM ingest at ~94 B/clk with MB = 1).  3 stages of 64 KB.
+template <int ELT, bool OF32 = (ELT == 4), int MB = 1>
 __global__ void __launch_bounds__(128, 1)
     k_proxy_tc(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmPt, int batch,
-               int N, int kblocks, void* __restrict__ xt, ProxyScatter sc) {
+               int N, int kblocks, void* __restrict__ xt, ProxyScatter sc, int bblk) {
   constexpr int KB_ELEMS = 128 / ELT;                       // K elements per 128-B swizzle row
-  constexpr uint32_t A_BYTES = PX_BM * 128, B_BYTES = PX_BN * 128;
+  constexpr uint32_t A_BYTES = MB * PX_BM * 128, B_BYTES = PX_BN * 128;
   constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  constexpr int NST = MB == 1 ? PX_STAGES : 3;
   constexpr int K_PER_MMA = 32 / ELT;                        // 16 (bf16) or 8 (tf32)
   constexpr int MMAS_PER_KB = KB_ELEMS / K_PER_MMA;          // 4
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[PX_STAGES], empty[PX_STAGES], tfull;
+  __shared__ uint64_t full[NST], empty[NST], tfull;
   __shared__ uint32_t tslot;
 
   const int warp = warp_id(), lane = lane_id();
-  const int nbt = (batch + PX_BM - 1) / PX_BM;
+  const int nbt = (batch + PX_BM * MB - 1) / (PX_BM * MB);
   const int bt = blockIdx.x % nbt, nt = blockIdx.x / nbt;   // consecutive CTAs share one Phi^T slice (L2)
-  const int b0 = bt * PX_BM, n0 = nt * PX_BN;
+  const int b0 = bt * PX_BM * MB, n0 = nt * PX_BN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmY);
     tma_prefetch_desc(&tmPt);
-    for (int s = 0; s < PX_STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     mbar_init(&tfull, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<256>(&tslot), tmem_relinquish();
+  if (warp == 2) tmem_alloc<256 * MB>(&tslot), tmem_relinquish();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -57,43 +63,51 @@ __global__ void __launch_bounds__(128, 1)
 
   if (warp == 0 && lane == 0) {  // ---------------- TMA producer
     for (int kb = 0; kb < kblocks; ++kb) {
-      const int s = kb % PX_STAGES;
-      if (kb >= PX_STAGES) mbar_wait(&empty[s], ((kb / PX_STAGES) - 1) & 1);
+      const int s = kb % NST;
+      if (kb >= NST) mbar_wait(&empty[s], ((kb / NST) - 1) & 1);
       uint8_t* sa = smem + s * STAGE;
       mbar_arrive_expect_tx(&full[s], STAGE);
-      tma_load_2d(sa, &tmY, &full[s], kb * KB_ELEMS, b0);
-      tma_load_2d(sa + A_BYTES, &tmPt, &full[s], kb * KB_ELEMS, n0);
+#pragma unroll
+      for (int h = 0; h < MB; ++h) tma_load_2d(sa + h * PX_BM * 128, &tmY, &full[s], kb * KB_ELEMS, b0 + h * PX_BM);
+      if (bblk)   // tile-blocked Phi^T: block (n-tile, kb) is one contiguous 32 KB
+        tma_load_3d(sa + A_BYTES, &tmPt, &full[s], 0, 0, nt * kblocks + kb);
+      else
+        tma_load_2d(sa + A_BYTES, &tmPt, &full[s], kb * KB_ELEMS, n0);
     }
   } else if (warp == 1 && lane == 0) {  // ---------------- MMA issuer
     constexpr uint32_t idesc = idesc_f32acc(ELT == 2 ? 1 : 2, PX_BM, PX_BN);
     for (int kb = 0; kb < kblocks; ++kb) {
-      const int s = kb % PX_STAGES;
-      mbar_wait(&full[s], (kb / PX_STAGES) & 1);
+      const int s = kb % NST;
+      mbar_wait(&full[s], (kb / NST) & 1);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
 #pragma unroll
       for (int k = 0; k < MMAS_PER_KB; ++k) {
-        const uint64_t ad = smem_desc(sa + k * 32, 16, 1024, kSwizzle128B);
         const uint64_t bd = smem_desc(sb + k * 32, 16, 1024, kSwizzle128B);
-        if (ELT == 2)
-          umma_f16_ss(tmem, ad, bd, idesc, (kb | k) != 0);
-        else
-          umma_tf32_ss(tmem, ad, bd, idesc, (kb | k) != 0);
+#pragma unroll
+        for (int h = 0; h < MB; ++h) {
+          const uint64_t ad = smem_desc(sa + h * PX_BM * 128 + k * 32, 16, 1024, kSwizzle128B);
+          if (ELT == 2)
+            umma_f16_ss(tmem + h * 256, ad, bd, idesc, (kb | k) != 0);
+          else
+            umma_tf32_ss(tmem + h * 256, ad, bd, idesc, (kb | k) != 0);
+        }
       }
       umma_commit(&empty[s]);
     }
     umma_commit(&tfull);
   }
   __syncwarp();
-  // ---------------- epilogue: all 4 warps, warp w owns TMEM lanes 32w..32w+31 (= images)
+  // ---------------- epilogue: all 4 warps, warp w owns TMEM lanes 32w..32w+31 (= images of each batch tile)
   mbar_wait(&tfull, 0);
   tc_fence_after();
-  const int b = b0 + warp * 32 + lane;
-  const bool row_ok = b < batch;
   const bool vec_ok = (N % 8) == 0;
-  for (int c = 0; c < PX_BN; c += 32) {
+  for (int hc = 0; hc < MB * PX_BN; hc += 32) {
+    const int h = hc / PX_BN, c = hc % PX_BN;
+    const int b = b0 + h * PX_BM + warp * 32 + lane;
+    const bool row_ok = b < batch;
     uint32_t r[32];
-    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
+    tmem_ld32(tmem + h * 256 + ((uint32_t)(warp * 32) << 16) + c, r);
     tmem_ld_wait();
     const int col = n0 + c;
     if (!row_ok || col >= N) continue;
@@ -136,23 +150,33 @@ __global__ void __launch_bounds__(128, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<256>(tmem);
+  if (warp == 2) tmem_dealloc<256 * MB>(tmem);
 }
 
 size_t proxy_tc_smem_bytes() { return (size_t)PX_STAGES * (PX_BM + PX_BN) * 128 + 1024; }
+static size_t proxy_tc2_smem_bytes() { return (size_t)3 * (2 * PX_BM + PX_BN) * 128 + 1024; }
 
 cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
-                            void* xt, bool tf32, cudaStream_t st, bool out_f32, const ProxyScatter* sc) {
+                            void* xt, bool tf32, cudaStream_t st, bool out_f32, const ProxyScatter* sc, bool b_blocked) {
+  const int bb = b_blocked ? 1 : 0;
   const int nbt = (batch + PX_BM - 1) / PX_BM, nnt = (N + PX_BN - 1) / PX_BN;
   const size_t smem = proxy_tc_smem_bytes();
   ProxyScatter s0{};
   if (sc) s0 = *sc;
+  if (!tf32 && nbt % 2 == 0 && getenv("DI_EXP_PROXY_MB1") == nullptr) {   // pairs of batch tiles share Phi^T K-blocks
+    const size_t smem2 = proxy_tc2_smem_bytes();
+    if (out_f32 || sc)
+      k_proxy_tc<2, true, 2><<<nbt / 2 * nnt, 128, smem2, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
+    else
+      k_proxy_tc<2, false, 2><<<nbt / 2 * nnt, 128, smem2, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
+    return cudaGetLastError();
+  }
   if (tf32) {
-    k_proxy_tc<4><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0);
+    k_proxy_tc<4><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
   } else if (out_f32 || sc) {
-    k_proxy_tc<2, true><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0);
+    k_proxy_tc<2, true><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
   } else {
-    k_proxy_tc<2><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0);
+    k_proxy_tc<2><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
   }
   return cudaGetLastError();
 }
@@ -163,6 +187,12 @@ cudaError_t setup_proxy_tc() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_proxy_tc<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)proxy_tc_smem_bytes());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_proxy_tc<2, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)proxy_tc2_smem_bytes());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_proxy_tc<2, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)proxy_tc2_smem_bytes());
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_proxy_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)proxy_tc_smem_bytes());
@@ -281,10 +311,11 @@ __global__ void k_pack_phiT(const float* __restrict__ phi, int m, int N, int kpa
     const int j = j0 + r, i = i0 + threadIdx.x;
     if (j < N && i < kpad) {
       const float v = tile[threadIdx.x][r];
+      const size_t o = phiT_blk_index(j, i, kpad, 128 / (int)sizeof(T));
       if constexpr (sizeof(T) == 2)
-        out[(size_t)j * kpad + i] = __float2bfloat16_rn(v);
+        out[o] = __float2bfloat16_rn(v);
       else
-        out[(size_t)j * kpad + i] = v;
+        out[o] = v;
     }
   }
 }

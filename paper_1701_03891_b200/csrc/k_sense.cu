@@ -48,7 +48,7 @@ __global__ void k_untranspose(const T* __restrict__ phiT, int m, int N, int kpad
   const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += 8) {
     const int j = j0 + r, i = i0 + threadIdx.x;
-    tile[r][threadIdx.x] = (j < N && i < m) ? phiT[(size_t)j * kpad + i] : T(0);
+    tile[r][threadIdx.x] = (j < N && i < m) ? phiT[phiT_blk_index(j, i, kpad, 128 / (int)sizeof(T))] : T(0);
   }
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += 8) {

@@ -31,9 +31,18 @@ struct ProxyScatter {
 };
 cudaError_t setup_proxy_tc();
 size_t proxy_tc_smem_bytes();
+// tmPt: a 2-D map over a row-major [N][K] operand (box 128 B x 256 rows), or with b_blocked a 3-D map over the
+// tile-blocked Phi^T of the lifting layer (phiT_blk_index: box = one contiguous 32-KB (N-tile, K-block) block)
 cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
                             void* xt, bool tf32, cudaStream_t st, bool out_f32 = false,
-                            const ProxyScatter* sc = nullptr);
+                            const ProxyScatter* sc = nullptr, bool b_blocked = false);
+// Tile-blocked Phi^T (BF16 / TF32 contexts): element (pixel j, measurement i) of [N-tile j / 256][K-block i / kel]
+// [j % 256][i % kel], kel = 128 B / element size; one (N-tile, K-block) block is the 32 KB the proxy GEMM stages per
+// K-block, contiguous in HBM (full DRAM pages instead of 256 strided 128-B rows).  Size: ceil(N / 256) * 256 * kpad.
+__host__ __device__ inline size_t phiT_blk_index(long long j, int i, int kpad, int kel) {
+  return ((((size_t)(j >> 8) * (size_t)(kpad / kel) + (size_t)(i / kel)) << 8) + (size_t)(j & 255)) * kel + i % kel;
+}
+__host__ __device__ inline size_t phiT_blk_elems(long long N, int kpad) { return (size_t)((N + 255) / 256) * 256 * kpad; }
 // rows of a local fp32 partial [batch][N] to the owners' slots (FP32 contexts); the owner's fixed-order slot sum
 // staging [world][nb][N] -> x_tilde [nb][N] (fp32, or RNE bf16 when bf16)
 cudaError_t launch_scatter_rows(const float* src, int batch, int N, const ProxyScatter* sc, cudaStream_t st);
