@@ -75,6 +75,7 @@ float bf2f(uint16_t b) {
 struct di_ctx_s {
   int device = 0, num_sms = 0;
   int m = 0, n1 = 0, n2 = 0, N = 0, max_batch = 0, kpad = 0;
+  int pxbn = 256;               // pixel-tile width of the lifting GEMM = row count of a Phi^T block
   di_precision prec = DI_PREC_BF16;
   unsigned flags = 0;
   size_t elt = 2;
@@ -154,13 +155,13 @@ di_status encode_2d(CUtensorMap* map, const void* base, bool bf16, int inner, in
 }
 
 // the tile-blocked Phi^T (di::phiT_blk_index) as [blocks][256 rows][kel]: box = one contiguous 32-KB block
-di_status encode_phiT_blk(CUtensorMap* map, const void* base, bool bf16, long long N, int kpad) {
+di_status encode_phiT_blk(CUtensorMap* map, const void* base, bool bf16, long long N, int kpad, int tr) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   const int e = bf16 ? 2 : 4, kel = 128 / e;
-  cuuint64_t dims[3] = {(cuuint64_t)kel, 256, (cuuint64_t)((N + 255) / 256) * (cuuint64_t)(kpad / kel)};
-  cuuint64_t strides[2] = {128, 256 * 128};
-  cuuint32_t box[3] = {(cuuint32_t)kel, 256, 1};
+  cuuint64_t dims[3] = {(cuuint64_t)kel, (cuuint64_t)tr, (cuuint64_t)((N + tr - 1) / tr) * (cuuint64_t)(kpad / kel)};
+  cuuint64_t strides[2] = {128, (cuuint64_t)tr * 128};
+  cuuint32_t box[3] = {(cuuint32_t)kel, (cuuint32_t)tr, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                    const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -516,7 +517,7 @@ di_status run_proxy(di_ctx c, const void* y, long long ldy, int batch, void* xt,
     di_status s = encode_2d(&tmY, ysrc, bf16, inner, batch, ld, 128 / (int)c->elt, 128);
     if (s != DI_OK) return s;
     CUDA_TRY(di::launch_proxy_tc(&tmY, &c->tmPt, batch, c->N, c->kpad / (128 / (int)c->elt), xt, !bf16, st, out_f32,
-                                 sc, true));
+                                 sc, true, c->pxbn));
     ++launches;
   }
   return DI_OK;
@@ -783,7 +784,8 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       float* tmp = nullptr;
       long long dummy = 0;
       STEP(upload(&tmp, phisrc, (size_t)a->m * N * 4, &dummy));
-      const size_t bytes = di::phiT_blk_elems(N, c->kpad) * c->elt;   // tile-blocked, zero rows past N
+      c->pxbn = di::proxy_tile_width(N, a->max_batch, bf16, c->num_sms);
+      const size_t bytes = di::phiT_blk_elems(N, c->kpad, c->pxbn) * c->elt;   // tile-blocked, zero rows past N
       cudaError_t e = cudaMalloc(&c->phi, bytes);
       if (e == cudaSuccess) e = cudaMemset(c->phi, 0, bytes);
       if (e != cudaSuccess) {
@@ -792,7 +794,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
         return fail(DI_ERR_OOM, "cudaMalloc(Phi^T, %zu) failed", bytes);
       }
       c->ws_bytes += bytes;
-      e = di::launch_pack_phiT(tmp, a->m, (int)N, c->kpad, c->phi, bf16, 0);
+      e = di::launch_pack_phiT(tmp, a->m, (int)N, c->kpad, c->pxbn, c->phi, bf16, 0);
       if (e == cudaSuccess) e = cudaDeviceSynchronize();
       cudaFree(tmp);
       if (e != cudaSuccess) {
@@ -941,7 +943,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       free_ctx(c);
       return fail(DI_ERR_CUDA, "setup_proxy_tc: %s", cudaGetErrorString(e));
     }
-    STEP(encode_phiT_blk(&c->tmPt, c->phi, bf16, N, c->kpad));
+    STEP(encode_phiT_blk(&c->tmPt, c->phi, bf16, N, c->kpad, c->pxbn));
   }
   if (bf16) {
     cudaError_t e = di::setup_conv2_tc(a->n2);
@@ -1134,7 +1136,7 @@ di_status di_measure(di_ctx c, const float* x, int batch, void* y, long long ldy
     CUDA_TRY(cudaMalloc(&c->phi_rm, (size_t)c->m * c->npad * c->elt));
     CUDA_TRY(cudaMalloc(&c->xs, (size_t)c->max_batch * c->npad * c->elt));
     c->ws_bytes += (long long)((size_t)c->m * c->npad + (size_t)c->max_batch * c->npad) * c->elt;
-    CUDA_TRY(di::launch_untranspose(c->phi, c->m, c->N, c->kpad, c->npad, c->phi_rm, bf16, st));
+    CUDA_TRY(di::launch_untranspose(c->phi, c->m, c->N, c->kpad, c->pxbn, c->npad, c->phi_rm, bf16, st));
   }
   CUDA_TRY(di::launch_stage_x(x, c->N, c->npad, batch, c->xs, bf16, st));
   // Y[B][m] = Xs[B][npad] . Phi_rm[m][npad]^T on the tcgen05 GEMM of the lifting layer (operand roles swapped)
@@ -1420,13 +1422,13 @@ di_status di_debug_get_phi(di_ctx c, void* host_out, long long bytes) {
     return DI_OK;
   }
   // tile-blocked Phi^T -> Phi [m][N]
-  std::vector<uint8_t> t(di::phiT_blk_elems(c->N, c->kpad) * c->elt);
+  std::vector<uint8_t> t(di::phiT_blk_elems(c->N, c->kpad, c->pxbn) * c->elt);
   CUDA_TRY(cudaMemcpy(t.data(), c->phi, t.size(), cudaMemcpyDeviceToHost));
   uint8_t* o = reinterpret_cast<uint8_t*>(host_out);
   const int kel = 128 / (int)c->elt;
   for (int i = 0; i < c->m; ++i)
     for (int j = 0; j < c->N; ++j)
-      std::memcpy(o + ((size_t)i * c->N + j) * c->elt, t.data() + di::phiT_blk_index(j, i, c->kpad, kel) * c->elt,
+      std::memcpy(o + ((size_t)i * c->N + j) * c->elt, t.data() + di::phiT_blk_index(j, i, c->kpad, kel, c->pxbn) * c->elt,
                   c->elt);
   return DI_OK;
 }

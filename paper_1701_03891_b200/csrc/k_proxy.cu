@@ -19,7 +19,7 @@ namespace di {
 
 namespace {
 constexpr int PX_BM = 128;      // images per tile (UMMA M)
-constexpr int PX_BN = 256;      // pixels per tile (UMMA N)
+constexpr int PX_BN = 256;      // pixels per tile (UMMA N); BN = 224 for the lifting layer when it fills the waves better
 constexpr int PX_STAGES = 4;
 }  // namespace
 
@@ -28,12 +28,12 @@ constexpr int PX_STAGES = 4;
 // MB: 128-image batch tiles per CTA.  MB = 2 gives each Phi^T K-block (32 KB) to two accumulators (TMEM 2 x 256
 // columns): per 1024 MMA cycles the SM ingests 64 KB instead of 2 x 48 KB -- what bounds the GEMM when Phi streams
 // from HBM (Stress: 2.15 GB of Phi, each CTA's L2 -> SM ingest at ~94 B/clk with MB = 1).  3 stages of 64 KB.
-template <int ELT, bool OF32 = (ELT == 4), int MB = 1>
+template <int ELT, bool OF32 = (ELT == 4), int MB = 1, int BN = PX_BN>
 __global__ void __launch_bounds__(128, 1)
     k_proxy_tc(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmPt, int batch,
                int N, int kblocks, void* __restrict__ xt, ProxyScatter sc, int bblk) {
   constexpr int KB_ELEMS = 128 / ELT;                       // K elements per 128-B swizzle row
-  constexpr uint32_t A_BYTES = MB * PX_BM * 128, B_BYTES = PX_BN * 128;
+  constexpr uint32_t A_BYTES = MB * PX_BM * 128, B_BYTES = BN * 128;
   constexpr uint32_t STAGE = A_BYTES + B_BYTES;
   constexpr int NST = MB == 1 ? PX_STAGES : 3;
   constexpr int K_PER_MMA = 32 / ELT;                        // 16 (bf16) or 8 (tf32)
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(128, 1)
   const int warp = warp_id(), lane = lane_id();
   const int nbt = (batch + PX_BM * MB - 1) / (PX_BM * MB);
   const int bt = blockIdx.x % nbt, nt = blockIdx.x / nbt;   // consecutive CTAs share one Phi^T slice (L2)
-  const int b0 = bt * PX_BM * MB, n0 = nt * PX_BN;
+  const int b0 = bt * PX_BM * MB, n0 = nt * BN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmY);
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(128, 1)
         tma_load_2d(sa + A_BYTES, &tmPt, &full[s], kb * KB_ELEMS, n0);
     }
   } else if (warp == 1 && lane == 0) {  // ---------------- MMA issuer
-    constexpr uint32_t idesc = idesc_f32acc(ELT == 2 ? 1 : 2, PX_BM, PX_BN);
+    constexpr uint32_t idesc = idesc_f32acc(ELT == 2 ? 1 : 2, PX_BM, BN);
     for (int kb = 0; kb < kblocks; ++kb) {
       const int s = kb % NST;
       mbar_wait(&full[s], (kb / NST) & 1);
@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(128, 1)
   mbar_wait(&tfull, 0);
   tc_fence_after();
   const bool vec_ok = (N % 8) == 0;
-  for (int hc = 0; hc < MB * PX_BN; hc += 32) {
-    const int h = hc / PX_BN, c = hc % PX_BN;
+  for (int hc = 0; hc < MB * BN; hc += 32) {
+    const int h = hc / BN, c = hc % BN;
     const int b = b0 + h * PX_BM + warp * 32 + lane;
     const bool row_ok = b < batch;
     uint32_t r[32];
@@ -154,48 +154,74 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 size_t proxy_tc_smem_bytes() { return (size_t)PX_STAGES * (PX_BM + PX_BN) * 128 + 1024; }
-static size_t proxy_tc2_smem_bytes() { return (size_t)3 * (2 * PX_BM + PX_BN) * 128 + 1024; }
+template <int MB, int BN>
+static size_t px_smem() { return (size_t)(MB == 1 ? PX_STAGES : 3) * (MB * PX_BM + BN) * 128 + 1024; }
+
+template <int ELT, bool OF32, int MB, int BN>
+static void px_launch(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks, void* xt,
+                      cudaStream_t st, const ProxyScatter& s0, int bb) {
+  const int nbt = (batch + PX_BM * MB - 1) / (PX_BM * MB), nnt = (N + BN - 1) / BN;
+  k_proxy_tc<ELT, OF32, MB, BN><<<nbt * nnt, 128, px_smem<MB, BN>(), st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
+}
+template <int ELT, bool OF32, int MB, int BN>
+static cudaError_t px_setup() {
+  return cudaFuncSetAttribute(k_proxy_tc<ELT, OF32, MB, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)px_smem<MB, BN>());
+}
+
+int proxy_tile_width(long long N, int max_batch, bool bf16, int num_sms) {
+  if (!bf16) return PX_BN;
+  const long long nbt = (max_batch + PX_BM - 1) / PX_BM, per = nbt % 2 == 0 ? nbt / 2 : nbt;
+  double best = 0.0;
+  int pick = PX_BN;
+  for (int bn : {PX_BN, 224}) {   // fraction of the issued tile slots that hold real pixels
+    const long long nnt = (N + bn - 1) / bn, ctas = per * nnt, waves = (ctas + num_sms - 1) / num_sms;
+    const double eff = (double)ctas / (double)(waves * num_sms) * (double)N / (double)(nnt * bn);
+    if (eff > best + 1e-9) best = eff, pick = bn;
+  }
+  return pick;
+}
 
 cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
-                            void* xt, bool tf32, cudaStream_t st, bool out_f32, const ProxyScatter* sc, bool b_blocked) {
+                            void* xt, bool tf32, cudaStream_t st, bool out_f32, const ProxyScatter* sc, bool b_blocked,
+                            int bn) {
   const int bb = b_blocked ? 1 : 0;
-  const int nbt = (batch + PX_BM - 1) / PX_BM, nnt = (N + PX_BN - 1) / PX_BN;
-  const size_t smem = proxy_tc_smem_bytes();
+  const int nbt = (batch + PX_BM - 1) / PX_BM;
   ProxyScatter s0{};
   if (sc) s0 = *sc;
-  if (!tf32 && nbt % 2 == 0 && getenv("DI_EXP_PROXY_MB1") == nullptr) {   // pairs of batch tiles share Phi^T K-blocks
-    const size_t smem2 = proxy_tc2_smem_bytes();
-    if (out_f32 || sc)
-      k_proxy_tc<2, true, 2><<<nbt / 2 * nnt, 128, smem2, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
-    else
-      k_proxy_tc<2, false, 2><<<nbt / 2 * nnt, 128, smem2, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
-    return cudaGetLastError();
-  }
+  const bool of = out_f32 || sc != nullptr;
   if (tf32) {
-    k_proxy_tc<4><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
-  } else if (out_f32 || sc) {
-    k_proxy_tc<2, true><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
+    if (bn != PX_BN) return cudaErrorInvalidValue;
+    px_launch<4, true, 1, PX_BN>(tmY, tmPt, batch, N, kblocks, xt, st, s0, bb);
+  } else if (nbt % 2 == 0) {   // pairs of batch tiles share each Phi^T K-block
+    if (bn == 224)
+      of ? px_launch<2, true, 2, 224>(tmY, tmPt, batch, N, kblocks, xt, st, s0, bb)
+         : px_launch<2, false, 2, 224>(tmY, tmPt, batch, N, kblocks, xt, st, s0, bb);
+    else
+      of ? px_launch<2, true, 2, PX_BN>(tmY, tmPt, batch, N, kblocks, xt, st, s0, bb)
+         : px_launch<2, false, 2, PX_BN>(tmY, tmPt, batch, N, kblocks, xt, st, s0, bb);
   } else {
-    k_proxy_tc<2><<<nbt * nnt, 128, smem, st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
+    if (bn == 224)
+      of ? px_launch<2, true, 1, 224>(tmY, tmPt, batch, N, kblocks, xt, st, s0, bb)
+         : px_launch<2, false, 1, 224>(tmY, tmPt, batch, N, kblocks, xt, st, s0, bb);
+    else
+      of ? px_launch<2, true, 1, PX_BN>(tmY, tmPt, batch, N, kblocks, xt, st, s0, bb)
+         : px_launch<2, false, 1, PX_BN>(tmY, tmPt, batch, N, kblocks, xt, st, s0, bb);
   }
   return cudaGetLastError();
 }
 
 cudaError_t setup_proxy_tc() {
-  cudaError_t e = cudaFuncSetAttribute(k_proxy_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)proxy_tc_smem_bytes());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_proxy_tc<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)proxy_tc_smem_bytes());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_proxy_tc<2, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)proxy_tc2_smem_bytes());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_proxy_tc<2, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)proxy_tc2_smem_bytes());
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_proxy_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)proxy_tc_smem_bytes());
+  cudaError_t e;
+  if ((e = px_setup<2, false, 1, PX_BN>()) != cudaSuccess) return e;
+  if ((e = px_setup<2, true, 1, PX_BN>()) != cudaSuccess) return e;
+  if ((e = px_setup<2, false, 2, PX_BN>()) != cudaSuccess) return e;
+  if ((e = px_setup<2, true, 2, PX_BN>()) != cudaSuccess) return e;
+  if ((e = px_setup<2, false, 1, 224>()) != cudaSuccess) return e;
+  if ((e = px_setup<2, true, 1, 224>()) != cudaSuccess) return e;
+  if ((e = px_setup<2, false, 2, 224>()) != cudaSuccess) return e;
+  if ((e = px_setup<2, true, 2, 224>()) != cudaSuccess) return e;
+  return px_setup<4, true, 1, PX_BN>();
 }
 
 // FP32 contexts: rows of a local partial to the owners' slots
@@ -299,7 +325,7 @@ cudaError_t launch_proxy_f32(const float* y, long long ldy, const float* phi, in
 // ----------------------------------------------------------------------------- packing helpers
 // Phi [m][N] (fp32 on device) -> Phi^T [N][kpad] in storage type (bf16 RNE or fp32), zero K tail.
 template <typename T>
-__global__ void k_pack_phiT(const float* __restrict__ phi, int m, int N, int kpad, T* __restrict__ out) {
+__global__ void k_pack_phiT(const float* __restrict__ phi, int m, int N, int kpad, int tr, T* __restrict__ out) {
   __shared__ float tile[32][33];
   const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
   for (int r = threadIdx.y; r < 32; r += 8) {
@@ -311,7 +337,7 @@ __global__ void k_pack_phiT(const float* __restrict__ phi, int m, int N, int kpa
     const int j = j0 + r, i = i0 + threadIdx.x;
     if (j < N && i < kpad) {
       const float v = tile[threadIdx.x][r];
-      const size_t o = phiT_blk_index(j, i, kpad, 128 / (int)sizeof(T));
+      const size_t o = phiT_blk_index(j, i, kpad, 128 / (int)sizeof(T), tr);
       if constexpr (sizeof(T) == 2)
         out[o] = __float2bfloat16_rn(v);
       else
@@ -320,12 +346,12 @@ __global__ void k_pack_phiT(const float* __restrict__ phi, int m, int N, int kpa
   }
 }
 
-cudaError_t launch_pack_phiT(const float* phi, int m, int N, int kpad, void* out, bool bf16, cudaStream_t st) {
+cudaError_t launch_pack_phiT(const float* phi, int m, int N, int kpad, int tr, void* out, bool bf16, cudaStream_t st) {
   dim3 grid((N + 31) / 32, (kpad + 31) / 32), block(32, 8);
   if (bf16)
-    k_pack_phiT<__nv_bfloat16><<<grid, block, 0, st>>>(phi, m, N, kpad, reinterpret_cast<__nv_bfloat16*>(out));
+    k_pack_phiT<__nv_bfloat16><<<grid, block, 0, st>>>(phi, m, N, kpad, tr, reinterpret_cast<__nv_bfloat16*>(out));
   else
-    k_pack_phiT<float><<<grid, block, 0, st>>>(phi, m, N, kpad, reinterpret_cast<float*>(out));
+    k_pack_phiT<float><<<grid, block, 0, st>>>(phi, m, N, kpad, tr, reinterpret_cast<float*>(out));
   return cudaGetLastError();
 }
 

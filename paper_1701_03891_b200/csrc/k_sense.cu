@@ -43,12 +43,12 @@ cudaError_t launch_stage_x(const float* x, int N, int ldo, int batch, void* out,
 // Phi^T [N][kpad] (storage type) -> Phi [m][ldp] (storage type, zero columns N..ldp-1): the row-major copy the
 // sensing GEMM reads K-major
 template <typename T>
-__global__ void k_untranspose(const T* __restrict__ phiT, int m, int N, int kpad, int ldp, T* __restrict__ phi) {
+__global__ void k_untranspose(const T* __restrict__ phiT, int m, int N, int kpad, int tr, int ldp, T* __restrict__ phi) {
   __shared__ T tile[32][33];
   const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += 8) {
     const int j = j0 + r, i = i0 + threadIdx.x;
-    tile[r][threadIdx.x] = (j < N && i < m) ? phiT[phiT_blk_index(j, i, kpad, 128 / (int)sizeof(T))] : T(0);
+    tile[r][threadIdx.x] = (j < N && i < m) ? phiT[phiT_blk_index(j, i, kpad, 128 / (int)sizeof(T), tr)] : T(0);
   }
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += 8) {
@@ -57,14 +57,14 @@ __global__ void k_untranspose(const T* __restrict__ phiT, int m, int N, int kpad
   }
 }
 
-cudaError_t launch_untranspose(const void* phiT, int m, int N, int kpad, int ldp, void* phi, bool bf16,
+cudaError_t launch_untranspose(const void* phiT, int m, int N, int kpad, int tr, int ldp, void* phi, bool bf16,
                                cudaStream_t st) {
   dim3 grid((ldp + 31) / 32, (m + 31) / 32), block(32, 8);
   if (bf16)
-    k_untranspose<uint16_t><<<grid, block, 0, st>>>(reinterpret_cast<const uint16_t*>(phiT), m, N, kpad, ldp,
+    k_untranspose<uint16_t><<<grid, block, 0, st>>>(reinterpret_cast<const uint16_t*>(phiT), m, N, kpad, tr, ldp,
                                                     reinterpret_cast<uint16_t*>(phi));
   else
-    k_untranspose<float><<<grid, block, 0, st>>>(reinterpret_cast<const float*>(phiT), m, N, kpad, ldp,
+    k_untranspose<float><<<grid, block, 0, st>>>(reinterpret_cast<const float*>(phiT), m, N, kpad, tr, ldp,
                                                  reinterpret_cast<float*>(phi));
   return cudaGetLastError();
 }

@@ -35,14 +35,19 @@ size_t proxy_tc_smem_bytes();
 // tile-blocked Phi^T of the lifting layer (phiT_blk_index: box = one contiguous 32-KB (N-tile, K-block) block)
 cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks,
                             void* xt, bool tf32, cudaStream_t st, bool out_f32 = false,
-                            const ProxyScatter* sc = nullptr, bool b_blocked = false);
-// Tile-blocked Phi^T (BF16 / TF32 contexts): element (pixel j, measurement i) of [N-tile j / 256][K-block i / kel]
-// [j % 256][i % kel], kel = 128 B / element size; one (N-tile, K-block) block is the 32 KB the proxy GEMM stages per
-// K-block, contiguous in HBM (full DRAM pages instead of 256 strided 128-B rows).  Size: ceil(N / 256) * 256 * kpad.
-__host__ __device__ inline size_t phiT_blk_index(long long j, int i, int kpad, int kel) {
-  return ((((size_t)(j >> 8) * (size_t)(kpad / kel) + (size_t)(i / kel)) << 8) + (size_t)(j & 255)) * kel + i % kel;
+                            const ProxyScatter* sc = nullptr, bool b_blocked = false, int bn = 256);
+// pixel-tile width of the lifting GEMM (256, or 224 when that fills the SM waves better for max_batch)
+int proxy_tile_width(long long N, int max_batch, bool bf16, int num_sms);
+// Tile-blocked Phi^T (BF16 / TF32 contexts): element (pixel j, measurement i) of [N-tile j / tr][K-block i / kel]
+// [j % tr][i % kel], kel = 128 B / element size, tr = the GEMM's pixel-tile width; one (N-tile, K-block) block is
+// the tr x 128 B the proxy GEMM stages per K-block, contiguous in HBM (full DRAM pages instead of tr strided 128-B
+// rows).  Size: ceil(N / tr) * tr * kpad.
+__host__ __device__ inline size_t phiT_blk_index(long long j, int i, int kpad, int kel, int tr) {
+  return (((size_t)(j / tr) * (size_t)(kpad / kel) + (size_t)(i / kel)) * tr + (size_t)(j % tr)) * kel + i % kel;
 }
-__host__ __device__ inline size_t phiT_blk_elems(long long N, int kpad) { return (size_t)((N + 255) / 256) * 256 * kpad; }
+__host__ __device__ inline size_t phiT_blk_elems(long long N, int kpad, int tr) {
+  return (size_t)((N + tr - 1) / tr) * tr * kpad;
+}
 // rows of a local fp32 partial [batch][N] to the owners' slots (FP32 contexts); the owner's fixed-order slot sum
 // staging [world][nb][N] -> x_tilde [nb][N] (fp32, or RNE bf16 when bf16)
 cudaError_t launch_scatter_rows(const float* src, int batch, int N, const ProxyScatter* sc, cudaStream_t st);
@@ -50,7 +55,7 @@ cudaError_t launch_reduce_slots(const float* staging, int world, int nb, int N, 
 cudaError_t launch_round_bf16(const float* src, void* dst, size_t n, cudaStream_t st);
 cudaError_t launch_proxy_f32(const float* y, long long ldy, const float* phi, int m, int N, int batch, float* xt,
                              cudaStream_t st);
-cudaError_t launch_pack_phiT(const float* phi, int m, int N, int kpad, void* out, bool bf16, cudaStream_t st);
+cudaError_t launch_pack_phiT(const float* phi, int m, int N, int kpad, int tr, void* out, bool bf16, cudaStream_t st);
 cudaError_t launch_stage_y(const void* y, long long ldy, int m, int kpad, int batch, void* out, bool bf16,
                            cudaStream_t st);
 
@@ -120,7 +125,7 @@ cudaError_t launch_conv3_tc(const CUtensorMap* tmH2, const void* w3pack, const f
 
 // sensing model and metrics (k_sense.cu)
 cudaError_t launch_stage_x(const float* x, int N, int ldo, int batch, void* out, bool bf16, cudaStream_t st);
-cudaError_t launch_untranspose(const void* phiT, int m, int N, int kpad, int ldp, void* phi, bool bf16,
+cudaError_t launch_untranspose(const void* phiT, int m, int N, int kpad, int tr, int ldp, void* phi, bool bf16,
                                cudaStream_t st);
 cudaError_t launch_measure_f32(const float* x, const float* phi, int m, int N, int batch, float* y, long long ldy,
                                cudaStream_t st);
