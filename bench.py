@@ -226,9 +226,14 @@ def oracle_sample(c, prec: str, budget_s: float, threads: int, max_images: int |
         done += y.shape[0]
         if t_total >= budget_s or (max_images is not None and done >= max_images):
             break
+    # single thread, per image: 2 images on one core
+    t0 = time.perf_counter()
+    oracle.forward(y[:2], phi, params, c.n, c.n, threads=1)
+    s1 = (time.perf_counter() - t0) / 2
     return {"value": done / t_total, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{done} images of workload {c.name} ({c.n}x{c.n}, M={c.m}) in chunks of {threads} "
-                      f"(one per OpenMP thread), fp64, {t_total:.1f} s"}
+                      f"(one per OpenMP thread), fp64, {t_total:.1f} s",
+            "single_thread_s_per_image": s1}
 
 
 def run_reference(args):
