@@ -80,7 +80,10 @@ enum { C2_BIAS_RELU = 0, C2_MASK = 1 };
 // x C_out filters in M, strip rows of C_in bf16 channels (128 B: SWIZZLE_128B; 64 B: SWIZZLE_64B), K-block = one
 // strip row (C_in / 16 MMAs of K = 16), 11 ceil(11 / TAPS) K-blocks per tile.  <32, 64, C2_MASK> is the training
 // step's layer-2 data gradient: dG2 (bf16) in, the rotated bank, out = [h1 > 0] * conv in bf16 (mask = bf16 h1).
-template <int CIN, int COUT, int MODE>
+// MC: CTA pairs (cluster of 2) share the weight stream -- each CTA copies half of every K-block to BOTH CTAs'
+// rings (multicast) and each MMA commit frees the stage in both, halving the L2 -> SM weight traffic.  Needs the two
+// CTAs of a pair to consume the same K-block sequence (equal tile counts: launch_conv2_tc checks).
+template <int CIN, int COUT, int MODE, bool MC = false>
 __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
     k_conv2_tc(const __grid_constant__ CUtensorMap tmH1, const __nv_bfloat16* __restrict__ wpack,
                const float* __restrict__ bias, int fullmap, Geo g, __nv_bfloat16* __restrict__ h2,
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmH1);
     for (int h = 0; h < 2; ++h) mbar_init(&hfull[h], 1), mbar_init(&hempty[h], 1);
-    for (int s = 0; s < WST; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], 1);
+    for (int s = 0; s < WST; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], MC ? 2 : 1);
     for (int s = 0; s < 2; ++s) mbar_init(&tfull[s], 1), mbar_init(&tempty[s], 4);
     fence_mbar_init();
   }
@@ -126,8 +129,10 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync_all();   // the peer's barriers are initialised before any multicast copy or commit
   tc_fence_after();
   const uint32_t tmem = tslot;
+  const uint32_t crank = MC ? cluster_ctarank() : 0;
 
   const int per_img = g.nrb * g.ncs;
   if (warp == 0) {
@@ -158,11 +163,16 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
             t_issue[st] = clock64();
 #endif
             mbar_arrive_expect_tx(&wfull[st], WB);
-            bulk_load(wst + st * WB, wsrc, WB, &wfull[st]);
+            if (MC)   // this CTA's half of the K-block, to both CTAs of the pair
+              bulk_load_mc(wst + st * WB + crank * (WB / 2), wsrc + crank * (WB / 2), WB / 2, &wfull[st], 0x3);
+            else
+              bulk_load(wst + st * WB, wsrc, WB, &wfull[st]);
 #endif
           }
         }
       }
+      if (MC)   // every commit (local and the peer's) into this CTA's ring has landed before the cluster exits
+        for (uint32_t k = wk > (uint32_t)WST ? wk - WST : 0; k < wk; ++k) mbar_wait(&wempty[k % WST], (k / WST) & 1);
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
@@ -218,7 +228,10 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
               umma_f16_ss(d, ad, b, idesc, (uu | j) != 0);
 #pragma unroll
               for (int kk = 1; kk < KMMA; ++kk) umma_f16_ss(d, ad + 2 * kk, b + 2 * kk, idesc, 1);
-              umma_commit(&wempty[st]);
+              if (MC)
+                umma_commit_mc(&wempty[st], 0x3);
+              else
+                umma_commit(&wempty[st]);
             }
           }
           umma_commit(&tfull[buf]);
@@ -346,6 +359,7 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync_all();
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
@@ -358,6 +372,26 @@ static Geo make_geo(int batch, int n1, int n2, int R = C2_ROWS) {
   g.ncs = (n2 + g.wseg - 1) / g.wseg;
   g.units = batch * g.nrb * g.ncs;
   return g;
+}
+
+// Weight multicast across CTA pairs (MC) needs both CTAs of every pair to run the same number of tiles: an even
+// grid, an even remainder of units over the grid, and the last row-block's units as many tiles as the full ones.
+static bool pair_balanced(const Geo& g, int grid, int R) {
+  const int Lfull = (R - 1) * g.P + g.wseg, rl = g.n1 - (g.nrb - 1) * R, Llast = (rl - 1) * g.P + g.wseg;
+  return getenv("DI_EXP_NO_MC") == nullptr && grid % 2 == 0 && (g.units % grid) % 2 == 0 &&
+         (Lfull + OUT_PER_TILE - 1) / OUT_PER_TILE == (Llast + OUT_PER_TILE - 1) / OUT_PER_TILE;
+}
+template <typename... Args>
+static cudaError_t launch_pair(void (*kern)(Args...), int grid, int threads, size_t smem, cudaStream_t st,
+                               const CUtensorMap& tm, const __nv_bfloat16* w, const float* bias, int fullmap, Geo g,
+                               __nv_bfloat16* out, const __nv_bfloat16* mask) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid), cfg.blockDim = dim3(threads), cfg.dynamicSmemBytes = smem, cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+  cfg.attrs = at, cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tm, w, bias, fullmap, g, out, mask);
 }
 
 size_t conv2_tc_smem_bytes(int n2) {
@@ -389,6 +423,12 @@ cudaError_t setup_conv2_tc(int n2) {
   cudaError_t e = cudaFuncSetAttribute(k_conv2_tc<64, 32, C2_BIAS_RELU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)conv2_tc_smem_bytes(n2));
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)conv2_tc_smem_bytes(n2));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_conv2_tc<32, 64, C2_MASK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)dgrad2_bf16_smem_bytes(n2));
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_conv2_tc<32, 64, C2_MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)dgrad2_bf16_smem_bytes(n2));
 }
@@ -397,6 +437,10 @@ cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const fl
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st) {
   Geo g = make_geo(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
+  if (pair_balanced(g, grid, R))
+    return launch_pair(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, grid, 256, conv2_tc_smem_bytes(n2), st, *tmH1,
+                       reinterpret_cast<const __nv_bfloat16*>(wpack), bias, fullmap, g,
+                       reinterpret_cast<__nv_bfloat16*>(h2), (const __nv_bfloat16*)nullptr);
   k_conv2_tc<64, 32, C2_BIAS_RELU><<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(
       *tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias, fullmap, g, reinterpret_cast<__nv_bfloat16*>(h2),
       nullptr);
@@ -410,6 +454,10 @@ cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, cons
                                void* dh1b, int num_sms, cudaStream_t st) {
   Geo g = make_geo(batch, n1, n2, C2_DG_ROWS);
   const int grid = g.units < num_sms ? g.units : num_sms;
+  if (pair_balanced(g, grid, C2_DG_ROWS))
+    return launch_pair(k_conv2_tc<32, 64, C2_MASK, true>, grid, 384, dgrad2_bf16_smem_bytes(n2), st, *tmDGb,
+                       reinterpret_cast<const __nv_bfloat16*>(wpack), nullptr, 0, g,
+                       reinterpret_cast<__nv_bfloat16*>(dh1b), reinterpret_cast<const __nv_bfloat16*>(h1b));
   k_conv2_tc<32, 64, C2_MASK><<<grid, 384, dgrad2_bf16_smem_bytes(n2), st>>>(
       *tmDGb, reinterpret_cast<const __nv_bfloat16*>(wpack), nullptr, 0, g, reinterpret_cast<__nv_bfloat16*>(dh1b),
       reinterpret_cast<const __nv_bfloat16*>(h1b));
