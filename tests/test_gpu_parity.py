@@ -142,6 +142,22 @@ def test_shard_outputs_bitwise_identical(precision):
         assert np.array_equal(np.concatenate(parts), whole), f"G = {g}"
 
 
+def test_weight_multicast_and_tile_width_are_bitwise_neutral(monkeypatch):
+    """Schedule choices that must not change a single bit: the CTA-pair weight multicast of conv2 (DESIGN.md §6;
+    DI_EXP_NO_MC switches it off per launch) and the lifting GEMM's pixel-tile width / batch tiles per CTA, which
+    di_create picks from max_batch (224-pixel tiles for max_batch 256, 256-pixel tiles for 4096 at 64x64)."""
+    case = Case(64, 64, 410, 256, "bf16")
+    ctx = make_ctx(case, max_batch=256)
+    y = y_device(case, ctx)
+    mc = ctx.recover(y).cpu().numpy()
+    monkeypatch.setenv("DI_EXP_NO_MC", "1")
+    nomc = ctx.recover(y).cpu().numpy()
+    monkeypatch.delenv("DI_EXP_NO_MC")
+    assert np.array_equal(mc, nomc), "weight multicast changed the result"
+    big = make_ctx(case, max_batch=4096)
+    assert np.array_equal(big.recover(y).cpu().numpy(), mc), "proxy tile width changed the result"
+
+
 def test_zero_weights_give_bias_only():
     p = synth.make_params(bias="channel")
     p0 = synth.Params([np.zeros_like(w) for w in p.w], p.b)
