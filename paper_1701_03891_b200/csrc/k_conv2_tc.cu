@@ -378,6 +378,7 @@ static Geo make_geo(int batch, int n1, int n2, int R = C2_ROWS) {
 // grid, an even remainder of units over the grid, and the last row-block's units as many tiles as the full ones.
 static bool pair_balanced(const Geo& g, int grid, int R) {
   const int Lfull = (R - 1) * g.P + g.wseg, rl = g.n1 - (g.nrb - 1) * R, Llast = (rl - 1) * g.P + g.wseg;
+  // DI_EXP_NO_MC (test / A-B switch, read per launch so a test can flip it): the plain one-CTA weight stream
   return getenv("DI_EXP_NO_MC") == nullptr && grid % 2 == 0 && (g.units % grid) % 2 == 0 &&
          (Lfull + OUT_PER_TILE - 1) / OUT_PER_TILE == (Llast + OUT_PER_TILE - 1) / OUT_PER_TILE;
 }
