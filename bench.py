@@ -89,88 +89,96 @@ _CLK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.ac
 _REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
 
+_NVML_LOOP = r"""
+import sys, time
+import pynvml as nv
+gpu, path = int(sys.argv[1]), sys.argv[2]
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(gpu)
+bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+        nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+with open(path, "w", buffering=1) as f:
+    while True:
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        f.write("%.6f,%d,%d,%.3f,%s\n" % (time.time(), sm, mx, pw, ",".join("1" if rs & b else "0" for b in bits)))
+        time.sleep(0.004)
+"""
+
+
 class ClockSampler:
-    """Samples SM clock, power and throttle reasons every ~5 ms while the timed region runs (NVML from a thread;
-    nvidia-smi -lms 200 as the fallback) -- the B200_PROFILING.md clocks line."""
+    """Samples SM clock, power and throttle reasons every ~5 ms while the timed region runs -- the
+    B200_PROFILING.md clocks line.  The NVML loop runs in its own PROCESS (a thread would compete with the timing
+    loop for the GIL and can miss the whole region); rows are timestamped and only those inside the region are
+    kept.  Fallback: nvidia-smi -lms 200."""
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.rows = []          # (sm_mhz, max_mhz, power_w, [hw_slowdown, hw_thermal, sw_thermal, sw_power_cap])
         self.proc = None
         self.path = None
-        self.thread = None
-        self.stop = False
-
-    def _nvml_loop(self, nv, h):
-        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        while not self.stop:
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((float(sm), float(mx), pw, [bool(rs & bt) for bt in bits]))
-            except Exception:
-                pass
-            time.sleep(0.005)
+        self.kind = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
         try:
-            import pynvml as nv
-            import threading
-            nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
-            self.thread.start()
-            time.sleep(0.05)
-            return self
+            import pynvml  # noqa: F401  (the child imports it; fail here to use the fallback)
+            self.proc = subprocess.Popen([sys.executable, "-c", _NVML_LOOP, str(self.gpu), self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            self.kind = "nvml"
         except Exception:
-            self.thread = None
-        try:
-            fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
-            os.close(fd)
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={_CLK_FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
-            time.sleep(0.3)
-        except Exception:
-            self.proc = None
+            self.kind = "nvidia-smi"
+        deadline = time.time() + 20.0      # wait for the first sample (the child's imports)
+        while time.time() < deadline and os.path.getsize(self.path) == 0 and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
-        if self.thread is not None:
-            self.stop = True
-            self.thread.join(timeout=2)
+        self.t1 = time.time()
+        time.sleep(0.02)
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.kind == "nvidia-smi":
             self.fh.close()
 
     def summary(self) -> dict:
-        rows = list(self.rows)
+        rows, inside = [], []
         if self.path and os.path.exists(self.path):
             for line in open(self.path):
                 f = [x.strip() for x in line.split(",")]
-                if len(f) < 9:
-                    continue
                 try:
-                    rows.append((float(f[1]), float(f[2]), float(f[3]) if f[3] not in ("", "[N/A]") else 0.0,
-                                 [v.lower().startswith("active") for v in f[5:9]]))
+                    if self.kind == "nvml" and len(f) >= 8:
+                        r = (float(f[1]), float(f[2]), float(f[3]), [v == "1" for v in f[4:8]])
+                        rows.append(r)
+                        if self.t0 <= float(f[0]) <= self.t1:
+                            inside.append(r)
+                    elif self.kind == "nvidia-smi" and len(f) >= 9:
+                        rows.append((float(f[1]), float(f[2]), float(f[3]) if f[3] not in ("", "[N/A]") else 0.0,
+                                     [v.lower().startswith("active") for v in f[5:9]]))
                 except ValueError:
                     continue
             os.unlink(self.path)
+        rows = inside or rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         load = [r for r in rows if r[2] > 300.0] or rows
         reasons = sorted({_REASONS[i] for r in load for i, v in enumerate(r[3]) if v})
         return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
                 "reasons": reasons, "samples": len(rows), "samples_under_load": len(load),
-                "power_w_max": max(r[2] for r in rows), "sampler": "nvml" if self.rows else "nvidia-smi"}
+                "power_w_max": max(r[2] for r in rows), "sampler": self.kind,
+                "window": "timed region only" if inside else "whole sampler run"}
 
 
 # ----------------------------------------------------------------------------- workload
