@@ -31,6 +31,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "kernels.cuh"
 #include "sm100.cuh"
@@ -382,6 +383,39 @@ static bool pair_balanced(const Geo& g, int grid, int R) {
   return getenv("DI_EXP_NO_MC") == nullptr && grid % 2 == 0 && (g.units % grid) % 2 == 0 &&
          (Lfull + OUT_PER_TILE - 1) / OUT_PER_TILE == (Llast + OUT_PER_TILE - 1) / OUT_PER_TILE;
 }
+// And every pair must be co-resident: a GPC with an odd number of usable SMs cannot host a 2-CTA cluster on all of
+// them, and a persistent grid whose last pair waits for a free GPC pair would take twice as long.  The occupancy
+// query (once per kernel and shared-memory size) gates MC on all grid / 2 clusters fitting at once.
+template <typename Kern>
+static bool pairs_fit(Kern kern, int grid, int threads, size_t smem) {
+  struct Entry {
+    const void* k;
+    size_t smem;
+    int grid, max;
+  };
+  static Entry cache[4] = {};
+  static int ncache = 0;
+  static std::mutex mu;   // contexts on several host threads
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < ncache; ++i)
+    if (cache[i].k == (const void*)kern && cache[i].smem == smem && cache[i].grid == grid) return 2 * cache[i].max >= grid;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid), cfg.blockDim = dim3(threads), cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+    cfg.attrs = at, cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
+    }
+    cache[ncache < 4 ? ncache++ : 3] = Entry{(const void*)kern, smem, grid, n};
+    if (getenv("DI_DEBUG_MC")) fprintf(stderr, "conv2 pairs: %d co-resident clusters of 2 (grid %d)\n", n, grid);
+    return 2 * n >= grid;
+  }
+}
 template <typename... Args>
 static cudaError_t launch_pair(void (*kern)(Args...), int grid, int threads, size_t smem, cudaStream_t st,
                                const CUtensorMap& tm, const __nv_bfloat16* w, const float* bias, int fullmap, Geo g,
@@ -438,7 +472,7 @@ cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const fl
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st) {
   Geo g = make_geo(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  if (pair_balanced(g, grid, R))
+  if (pair_balanced(g, grid, R) && pairs_fit(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, grid, 256, conv2_tc_smem_bytes(n2)))
     return launch_pair(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, grid, 256, conv2_tc_smem_bytes(n2), st, *tmH1,
                        reinterpret_cast<const __nv_bfloat16*>(wpack), bias, fullmap, g,
                        reinterpret_cast<__nv_bfloat16*>(h2), (const __nv_bfloat16*)nullptr);
@@ -455,7 +489,8 @@ cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, cons
                                void* dh1b, int num_sms, cudaStream_t st) {
   Geo g = make_geo(batch, n1, n2, C2_DG_ROWS);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  if (pair_balanced(g, grid, C2_DG_ROWS))
+  if (pair_balanced(g, grid, C2_DG_ROWS) &&
+      pairs_fit(k_conv2_tc<32, 64, C2_MASK, true>, grid, 384, dgrad2_bf16_smem_bytes(n2)))
     return launch_pair(k_conv2_tc<32, 64, C2_MASK, true>, grid, 384, dgrad2_bf16_smem_bytes(n2), st, *tmDGb,
                        reinterpret_cast<const __nv_bfloat16*>(wpack), nullptr, 0, g,
                        reinterpret_cast<__nv_bfloat16*>(dh1b), reinterpret_cast<const __nv_bfloat16*>(h1b));
