@@ -12,6 +12,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include "kernels.cuh"
 
 namespace di {
@@ -23,6 +25,24 @@ __device__ __forceinline__ float to_f<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
 
+// packed fp32 pairs for FFMA2 (fma.rn.f32x2, sm_100a)
+__device__ __forceinline__ uint64_t f32x2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t f32x2_bcast(float x) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void f32x2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ void ffma2(uint64_t& d, uint64_t a, uint64_t b) {   // d = a * b + d, per half, RN
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+
 // ---------------------------------------------------------------------------------------------
 // wide-output layers (C_out >= 16): block tile TH x TW pixels x all COUT channels; thread computes
 // PX pixels (strided by TW/PX along x, conflict-free smem reads) x CO_T channels.
@@ -33,12 +53,13 @@ __global__ void __launch_bounds__(256)
                 int relu, Tout* __restrict__ out, int n1, int n2) {
   constexpr int TH = 8, TW = 32, PX = 4;
   constexpr int HT = TH + 10, WT = TW + 10;
+  constexpr int WTS = 72;   // smem row stride: 72 = 8 (mod 32), so the 4 rows x 8 columns a warp reads hit 32 banks
   constexpr int PIX_THREADS = TH * TW / PX;       // 64
   constexpr int CO_GROUPS = COUT / CO_T;
   static_assert(PIX_THREADS * CO_GROUPS == 256, "256 threads");
   extern __shared__ float sm[];
-  float* sx = sm;                                  // [CI_CHUNK][HT][WT]
-  float* sw = sm + CI_CHUNK * HT * WT;             // [CI_CHUNK][121][COUT]
+  float* sx = sm;                                  // [CI_CHUNK][HT][WTS]
+  float* sw = sm + CI_CHUNK * HT * WTS;            // [CI_CHUNK][121][COUT]
 
   const int b = blockIdx.z;
   const int y0 = blockIdx.y * TH, x0 = blockIdx.x * TW;
@@ -53,43 +74,45 @@ __global__ void __launch_bounds__(256)
 
   for (int ci0 = 0; ci0 < CIN; ci0 += CI_CHUNK) {
     __syncthreads();
-    for (int e = tid; e < CI_CHUNK * HT * WT; e += 256) {
-      const int cc = e / (HT * WT), rem = e - cc * HT * WT;
-      const int yy = rem / WT, xx = rem - yy * WT;
+    for (int e = tid; e < CI_CHUNK * HT * WT; e += 256) {   // channel innermost: neighbouring threads, one pixel
+      const int cc = e % CI_CHUNK, pix = e / CI_CHUNK;
+      const int yy = pix / WT, xx = pix - yy * WT;
       const int gy = y0 + yy - 5, gx = x0 + xx - 5;
       float v = 0.f;
       if (gy >= 0 && gy < n1 && gx >= 0 && gx < n2)
         v = to_f(in[(((size_t)b * n1 + gy) * n2 + gx) * CIN + ci0 + cc]);
-      sx[e] = v;
+      sx[(cc * HT + yy) * WTS + xx] = v;
     }
     for (int e = tid; e < CI_CHUNK * 121 * COUT; e += 256) sw[e] = wx[(size_t)ci0 * 121 * COUT + e];
     __syncthreads();
 #pragma unroll 1
     for (int cc = 0; cc < CI_CHUNK; ++cc) {
-      float part[PX][CO_T];
+      // per-channel partial sums as packed fp32 pairs (channels c, c+1): one fma.rn.f32x2 (FFMA2, two IEEE fp32
+      // FMAs -- bit-identical to fmaf) per pixel and channel pair, the pixel value broadcast by ptxas into the
+      // operand: half the FMA instructions, so the loop is bound by the FMA pipe instead of instruction issue
+      uint64_t part[PX][CO_T / 2];
 #pragma unroll
       for (int p = 0; p < PX; ++p)
 #pragma unroll
-        for (int c = 0; c < CO_T; ++c) part[p][c] = 0.f;
-      const float* xr = sx + cc * HT * WT + py * WT + pxb;
+        for (int c = 0; c < CO_T / 2; ++c) part[p][c] = 0ull;
+      const float* xr = sx + cc * HT * WTS + py * WTS + pxb;
       const float* wr = sw + cc * 121 * COUT + cg * CO_T;
 #pragma unroll 1
       for (int a = 0; a < 11; ++a) {
 #pragma unroll
         for (int bb = 0; bb < 11; ++bb) {
-          float xv[PX];
+          uint64_t xv[PX];
 #pragma unroll
-          for (int p = 0; p < PX; ++p) xv[p] = xr[a * WT + bb + p * (TW / PX)];
+          for (int p = 0; p < PX; ++p) xv[p] = f32x2_bcast(xr[a * WTS + bb + p * (TW / PX)]);
           const float4* w4 = reinterpret_cast<const float4*>(wr + (a * 11 + bb) * COUT);
 #pragma unroll
           for (int c4 = 0; c4 < CO_T / 4; ++c4) {
             const float4 w = w4[c4];
+            const uint64_t w01 = f32x2_pack(w.x, w.y), w23 = f32x2_pack(w.z, w.w);
 #pragma unroll
             for (int p = 0; p < PX; ++p) {
-              part[p][4 * c4 + 0] = fmaf(xv[p], w.x, part[p][4 * c4 + 0]);
-              part[p][4 * c4 + 1] = fmaf(xv[p], w.y, part[p][4 * c4 + 1]);
-              part[p][4 * c4 + 2] = fmaf(xv[p], w.z, part[p][4 * c4 + 2]);
-              part[p][4 * c4 + 3] = fmaf(xv[p], w.w, part[p][4 * c4 + 3]);
+              ffma2(part[p][2 * c4], xv[p], w01);
+              ffma2(part[p][2 * c4 + 1], xv[p], w23);
             }
           }
         }
@@ -97,7 +120,11 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int p = 0; p < PX; ++p)
 #pragma unroll
-        for (int c = 0; c < CO_T; ++c) acc[p][c] += part[p][c];
+        for (int c = 0; c < CO_T / 2; ++c) {
+          float lo, hi;
+          f32x2_unpack(part[p][c], lo, hi);
+          acc[p][2 * c] += lo, acc[p][2 * c + 1] += hi;
+        }
     }
   }
   // epilogue: bias, ReLU, store NHWC (CO_T contiguous channels per pixel)
@@ -141,7 +168,7 @@ template <typename Tin, typename Tout, int CIN, int COUT, int CO_T, int CI_CHUNK
 static cudaError_t launch_wide(const void* in, const float* wx, const float* bias, int fullmap, int relu, void* out,
                                int batch, int n1, int n2, cudaStream_t st, const void* mask = nullptr) {
   constexpr int TH = 8, TW = 32;
-  const size_t smem = (size_t)(CI_CHUNK * (TH + 10) * (TW + 10) + CI_CHUNK * 121 * COUT) * sizeof(float);
+  const size_t smem = (size_t)(CI_CHUNK * (TH + 10) * 72 + CI_CHUNK * 121 * COUT) * sizeof(float);   // WTS = 72
   auto k = k_conv_wide<Tin, Tout, CIN, COUT, CO_T, CI_CHUNK>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -183,7 +210,7 @@ cudaError_t launch_convg_simt(int cin, int cout, const float* in, const float* w
 
 cudaError_t launch_conv2_simt_f32(const float* h1, const float* wx, const float* bias, int fullmap, float* h2,
                                   int batch, int n1, int n2, cudaStream_t st) {
-  return launch_wide<float, float, 64, 32, 8, 2>(h1, wx, bias, fullmap, 1, h2, batch, n1, n2, st);
+  return launch_wide<float, float, 64, 32, 8, 4>(h1, wx, bias, fullmap, 1, h2, batch, n1, n2, st);
 }
 
 // ---------------------------------------------------------------------------------------------
