@@ -250,6 +250,23 @@ di_status encode_wg2(CUtensorMap* map, const void* p, int batch, int n1, int n2,
   return DI_OK;
 }
 
+// bf16 NHWC activation with `pitch` channels per pixel, read `ch` channels at a time (custom BF16 stacks): box
+// ch x box_cols x box_rows, SWIZZLE_128B for 64 channels (128-B rows), SWIZZLE_64B for 32
+di_status encode_act_bf16(CUtensorMap* map, const void* p, int batch, int n1, int n2, int pitch, int ch, int box_cols,
+                          int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {(cuuint64_t)pitch, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)pitch * 2, (cuuint64_t)n2 * pitch * 2, (cuuint64_t)n1 * n2 * pitch * 2};
+  cuuint32_t box[4] = {(cuuint32_t)ch, (cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(p), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, ch == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (bf16 activation) failed: %d", (int)r);
+  return DI_OK;
+}
+
 // dG2 [batch][n1][n2][32] bf16 as the strip of the bf16 layer-2 dgrad: box 32 ch x P x (11 + 10) rows, SWIZZLE_64B
 di_status encode_dg2b_strip(CUtensorMap* map, const void* p, int batch, int n1, int n2) {
   EncodeTiledFn enc = get_encode();
@@ -454,6 +471,28 @@ std::vector<float> conv_tf32_pack(const std::vector<float>& wx, int cin, int cou
   return out;
 }
 
+// bf16 interior layer of a custom stack on k_conv2_tc<C_in, C_out>: K-block u * J + j (J = ceil(11 / TAPS), TAPS =
+// 128 / C_out column taps v0 = TAPS j ..), row v' * C_out + k, C_in channels per row (128 B: SWIZZLE_128B, 64 B:
+// SWIZZLE_64B); conv2_tc_pack is the (64, 32) case
+std::vector<uint16_t> convg_tc_pack(const std::vector<float>& wx, int cin, int cout) {
+  const int taps = 128 / cout, J = (K + taps - 1) / taps, rb = 2 * cin;
+  const size_t wb = (size_t)128 * rb;
+  std::vector<uint16_t> out((size_t)K * J * wb / 2, 0);
+  uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
+  for (int u = 0; u < K; ++u)
+    for (int j = 0; j < J; ++j)
+      for (int row = 0; row < 128; ++row) {
+        const int v = taps * j + row / cout, k = row % cout;
+        for (int ci = 0; ci < cin; ++ci) {
+          const uint16_t h = v < K ? f2bf(wx[(((size_t)k * cin + ci) * K + u) * K + v]) : 0;
+          const int sw = rb == 128 ? (row & 7) : ((row >> 1) & 3);
+          const size_t off = (size_t)(u * J + j) * wb + (size_t)row * rb + ((((size_t)ci / 8) ^ sw) << 4) + (ci % 8) * 2;
+          std::memcpy(base + off, &h, 2);
+        }
+      }
+  return out;
+}
+
 // bias: per-channel [cout] or the window of the full map [cout][n1+10][n2+10] that S keeps, as [n1][n2][cout]
 di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n1, int n2, long long* ws) {
   *dst = nullptr;
@@ -546,6 +585,27 @@ di_status run_stack(di_ctx c, int batch, void* xt, float* xhat, cudaStream_t st,
       } else {
         CUDA_TRY(di::launch_convg_tf32(l.cin, l.cout, &l.tm, l.wp, l.b, batch, c->n1, c->n2, out, c->num_sms, st));
       }
+    } else if (c->prec == DI_PREC_BF16) {   // bf16 activations (act[] holds __nv_bfloat16)
+      void* outb = c->act[i & 1];
+      if (i == 0) {
+        CUtensorMap tm;
+        const CUtensorMap* tmp = nullptr;
+        if (c->has_tmX) {
+          tmp = &c->tmX;
+          if (xt != c->xt || batch != c->max_batch) {
+            di_status s = encode_xt(&tm, xt, batch, c->n1, c->n2);
+            if (s != DI_OK) return s;
+            tmp = &tm;
+          }
+        }
+        CUDA_TRY(di::launch_conv1_tc(tmp, xt, l.wp, l.b, 0, outb, batch, c->n1, c->n2, c->num_sms, st));
+      } else if (i == L - 1) {
+        CUDA_TRY(di::launch_conv3_r4(&l.tm, l.wp, l.b, 0, relu_last, xhat, batch, c->n1, c->n2, c->num_sms, st));
+      } else {
+        CUDA_TRY(di::launch_convg_tc(l.cin, l.cout, &l.tm, l.wp, l.b, batch, c->n1, c->n2, outb, c->num_sms, st));
+      }
+      ++launches;
+      continue;
     } else {
       if (i == L - 1)
         CUDA_TRY(di::launch_conv3_simt(in, false, l.wx, l.b, 0, relu_last, xhat, batch, c->n1, c->n2, st));
@@ -706,7 +766,6 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   if (custom) {   // SURVEY.md §8(f) NEXT-3 custom stacks: shapes the kernels implement
     const int L = a->n_layers;
     if (L < 2 || !a->layers) return fail(DI_ERR_ARG, "n_layers=%d: a custom stack needs >= 2 layers", L);
-    if (a->precision == DI_PREC_BF16) return fail(DI_ERR_ARG, "custom stacks run in FP32 or TF32 contexts");
     if (a->flags & DI_FLAG_FULLMAP_BIAS) return fail(DI_ERR_ARG, "custom stacks take per-channel biases");
     if (a->precision == DI_PREC_TF32 && a->n2 % 4 != 0) return fail(DI_ERR_ARG, "TF32 custom stacks need n2 %% 4 == 0");
     for (int i = 0; i < L; ++i) {
@@ -838,6 +897,18 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       if (c->prec == DI_PREC_FP32) {
         auto sl = simt_layout(wx, al.cout, al.cin);
         STEP(upload(&l.wx, sl.data(), sl.size() * 4, &c->ws_bytes));
+      } else if (bf16) {   // k_conv1_tc (64 bank rows, rows >= cout zero) / k_conv2_tc<C_in, C_out> / k_conv3_r4
+        std::vector<uint16_t> pk;
+        if (i == 0) {
+          std::vector<float> w64((size_t)64 * K * K, 0.f);
+          std::copy(wx.begin(), wx.end(), w64.begin());
+          pk = conv1_tc_pack(w64);
+        } else if (i == L - 1) {
+          pk = conv3_r4_pack(wx);
+        } else {
+          pk = convg_tc_pack(wx, al.cin, al.cout);
+        }
+        STEP(upload(reinterpret_cast<uint16_t**>(&l.wp), pk.data(), pk.size() * 2, &c->ws_bytes));
       } else if (i == 0) {   // conv1 machinery: 64 bank rows, rows >= cout zero
         std::vector<float> w64((size_t)64 * K * K, 0.f);
         std::copy(wx.begin(), wx.end(), w64.begin());
@@ -850,7 +921,13 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
         auto pk = conv_tf32_pack(wx, al.cin, al.cout);
         STEP(upload(reinterpret_cast<float**>(&l.wp), pk.data(), pk.size() * 4, &c->ws_bytes));
       }
-      STEP(upload_bias(&l.b, al.b, al.cout, false, a->n1, a->n2, &c->ws_bytes));
+      if (bf16 && i == 0 && al.cout < 64 && al.b) {   // k_conv1_tc reads 64 biases: zero past cout
+        std::vector<float> b64(64, 0.f);
+        std::copy(al.b, al.b + al.cout, b64.begin());
+        STEP(upload_bias(&l.b, b64.data(), 64, false, a->n1, a->n2, &c->ws_bytes));
+      } else {
+        STEP(upload_bias(&l.b, al.b, al.cout, false, a->n1, a->n2, &c->ws_bytes));
+      }
     }
   } else {
     auto w1 = xcorr_taps(a->w1, C1, 1, xc, bf16);
@@ -901,7 +978,9 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     if (custom) {
       int wmax = 0;
       for (const auto& l : c->stack) wmax = std::max(wmax, l.cout);
-      for (auto& p : c->act) STEP(upload(&p, nullptr, B * N * wmax * 4, &c->ws_bytes));
+      // BF16: bf16 activations, the first layer's at pitch 64 (k_conv1_tc writes 64 channels, the rows >= cout zero)
+      if (bf16) wmax = 64;
+      for (auto& p : c->act) STEP(upload(&p, nullptr, B * N * wmax * (bf16 ? 2 : 4), &c->ws_bytes));
     } else {
       STEP(upload(&c->h1, nullptr, B * N * C1 * c->elt, &c->ws_bytes));
       STEP(upload(&c->h2, nullptr, B * N * C2 * c->elt, &c->ws_bytes));
@@ -947,17 +1026,29 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   }
   if (bf16) {
     cudaError_t e = di::setup_conv2_tc(a->n2);
+    if (e == cudaSuccess && custom) e = di::setup_convg_tc(a->n2);
     if (e != cudaSuccess) {
       free_ctx(c);
       return fail(DI_ERR_CUDA, "setup_conv2_tc: %s", cudaGetErrorString(e));
     }
-    STEP(encode_h1(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
+    if (custom) {   // layer i >= 1 reads act[(i - 1) & 1] (pitch 64 after the first layer, else the previous C_out)
+      for (int i = 1; i < (int)c->stack.size(); ++i) {
+        di_ctx_s::Layer& l = c->stack[i];
+        const int pitch = i == 1 ? 64 : c->stack[i - 1].cout;
+        const bool last = i == (int)c->stack.size() - 1;
+        STEP(encode_act_bf16(&l.tm, c->act[(i - 1) & 1], a->max_batch, a->n1, a->n2, pitch, l.cin,
+                             last ? di::conv3_tc_box_cols(a->n2) : di::conv2_tc_box_cols(a->n2),
+                             last ? di::conv3_r4_box_rows() : di::convg_tc_box_rows(l.cin)));
+      }
+    } else {
+      STEP(encode_h1(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
+    }
     e = di::setup_conv13_tc(a->n2);
     if (e != cudaSuccess) {
       free_ctx(c);
       return fail(DI_ERR_CUDA, "setup_conv13_tc: %s", cudaGetErrorString(e));
     }
-    STEP(encode_h2(&c->tmH2, c->h2, a->max_batch, a->n1, a->n2));
+    if (!custom) STEP(encode_h2(&c->tmH2, c->h2, a->max_batch, a->n1, a->n2));
     {
       cudaError_t e3 = di::setup_conv3_r4(a->n2);
       if (e3 != cudaSuccess) {

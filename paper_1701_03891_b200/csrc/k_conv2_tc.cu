@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   // epilogue groups: C_out = 64 (twice the epilogue work per tile) runs two groups of 4 warps, one per TMEM buffer
   constexpr int EG = COUT == 64 ? 2 : 1;
   // weight ring: 4 stages of 16 KB for 128-B rows; 12 stages of 8 KB for 64-B rows (the layer-2 dgrad)
-  constexpr int WST = RB == 128 ? WSTAGES : C2_WST64;
+  constexpr int WST = RB == 128 ? (COUT == 64 ? 3 : WSTAGES) : C2_WST64;   // <64, 64>: room for 2 epilogue groups
   constexpr int R = RB == 128 ? C2_ROWS : C2_DG_ROWS;   // output rows per unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -480,6 +480,50 @@ cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const fl
       *tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias, fullmap, g, reinterpret_cast<__nv_bfloat16*>(h2),
       nullptr);
   return cudaGetLastError();
+}
+
+// custom stacks, BF16 contexts: interior C_in -> C_out layers (C in {32, 64}) on the same
+// kernel, weights packed by convg_tc_pack (K-block u * J + j, rows v' * C_out + k, C_in bf16 channels per row).
+// tm: bf16 strip map over the input activation (box C_in x P x convg_tc_box_rows(C_in)); out: NHWC, C_out channels.
+int convg_tc_box_rows(int cin) { return (cin == 64 ? C2_ROWS : C2_DG_ROWS) + 10; }
+
+// <64, 64>: the 128-B-row strip, a 3-stage ring and two epilogue groups' staging
+static size_t convg64_smem_bytes(int n2) {
+  const int P = conv2_tc_box_cols(n2);
+  const size_t strip_alloc = ((size_t)strip_rows_bytes(P) + GUARD_ROWS * 128 + 1023) & ~(size_t)1023;
+  return strip_alloc + 3 * WBYTES + 2 * 4 * ECH * SPS * 4 + 1024;
+}
+
+template <int CIN, int COUT>
+static cudaError_t launch_g(const CUtensorMap* tm, const void* wpack, const float* bias, int batch, int n1, int n2,
+                            void* out, int num_sms, cudaStream_t st) {
+  Geo g = make_geo(batch, n1, n2, CIN == 64 ? C2_ROWS : C2_DG_ROWS);
+  const int grid = g.units < num_sms ? g.units : num_sms;
+  const size_t smem = CIN == 32 ? dgrad2_bf16_smem_bytes(n2) : COUT == 64 ? convg64_smem_bytes(n2) : conv2_tc_smem_bytes(n2);
+  k_conv2_tc<CIN, COUT, C2_BIAS_RELU><<<grid, COUT == 64 ? 384 : 256, smem, st>>>(
+      *tm, reinterpret_cast<const __nv_bfloat16*>(wpack), bias, 0, g, reinterpret_cast<__nv_bfloat16*>(out), nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t setup_convg_tc(int n2) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_conv2_tc<64, 64, C2_BIAS_RELU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)convg64_smem_bytes(n2))) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_conv2_tc<32, 32, C2_BIAS_RELU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)dgrad2_bf16_smem_bytes(n2))) != cudaSuccess)
+    return e;
+  return cudaFuncSetAttribute(k_conv2_tc<32, 64, C2_BIAS_RELU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)dgrad2_bf16_smem_bytes(n2));
+}
+
+cudaError_t launch_convg_tc(int cin, int cout, const CUtensorMap* tm, const void* wpack, const float* bias, int batch,
+                            int n1, int n2, void* out, int num_sms, cudaStream_t st) {
+  if (cin == 64 && cout == 32) return launch_g<64, 32>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
+  if (cin == 64 && cout == 64) return launch_g<64, 64>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
+  if (cin == 32 && cout == 32) return launch_g<32, 32>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
+  if (cin == 32 && cout == 64) return launch_g<32, 64>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
+  return cudaErrorInvalidValue;
 }
 
 // training: the layer-2 data gradient on the bf16 layer-2 machinery (TMEM double buffering, weights per tile):

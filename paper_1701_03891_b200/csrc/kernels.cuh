@@ -81,6 +81,11 @@ size_t conv2_tc_smem_bytes(int n2);
 int conv2_tc_box_rows();
 int conv2_tc_box_cols(int n2);
 int dgrad2_bf16_box_rows();
+// custom stacks, BF16: interior C_in -> C_out layers on k_conv2_tc (bias + ReLU), strip box rows per C_in
+int convg_tc_box_rows(int cin);
+cudaError_t setup_convg_tc(int n2);
+cudaError_t launch_convg_tc(int cin, int cout, const CUtensorMap* tm, const void* wpack, const float* bias, int batch,
+                            int n1, int n2, void* out, int num_sms, cudaStream_t st);
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st);
 size_t conv2_tf32_smem_bytes(int n2);

@@ -1,7 +1,9 @@
 """Custom layer stacks ("DeepInverses with larger capacities"): deeper and
 wider stacks of Eq. (1) layers through di_create_args.layers, against the fp64 oracle's forward pass over the same
 layer list (oracle.forward takes any stack).  FP32 runs the SIMT kernels, TF32 the tensor-core kernels (first layer
-on the conv1 machinery, interior layers on k_conv_tf32<C_in, C_out>, last layer on the conv3 kernel)."""
+on the conv1 machinery, interior layers on k_conv_tf32<C_in, C_out>, last layer on the conv3 kernel), BF16 the bf16
+tensor-core kernels (k_conv1_tc, k_conv2_tc<C_in, C_out>, k_conv3_r4) on bf16 activations; the oracle takes the same
+bf16-rounded weights and measurements (gpu_helpers.Case)."""
 import numpy as np
 import pytest
 
@@ -28,23 +30,31 @@ def run_stack(widths, precision, n1, n2, m, batch, flags=0, final_relu=False):
     case = Case(n1, n2, m, batch, precision, 6, 3, params=stack_params(widths))
     ctx = DeepInverse(case.phi, case.params, n1, n2, precision, flags=flags, max_batch=batch)
     assert ctx.custom
-    out = ctx.recover(torch.from_numpy(case.y).cuda()).cpu().numpy()
+    out = ctx.recover(torch.from_numpy(case.y).to(device="cuda", dtype=ctx.storage_dtype)).cpu().numpy()
     ref = oracle.forward(case.y, case.phi, case.params, n1, n2, final_relu=final_relu)
     ctx.close()
     return compare(out, ref, case.x, precision)
 
 
-@pytest.mark.parametrize("precision", ["f32", "tf32"])
-@pytest.mark.parametrize("widths", [(1, 64, 64, 32, 1), (1, 32, 32, 32, 32, 1), (1, 32, 64, 32, 1), (1, 32, 1)])
+@pytest.mark.parametrize("precision", ["f32", "tf32", "bf16"])
+@pytest.mark.parametrize("widths", [(1, 64, 64, 32, 1), (1, 32, 32, 32, 32, 1), (1, 32, 64, 32, 1), (1, 32, 1),
+                                    (1, 64, 32, 64, 64, 32, 1)])
 def test_stack_matches_oracle(precision, widths):
     rel, dps, _ = run_stack(widths, precision, 32, 32, 200, 3)
     assert rel <= TOL_REL_L2[precision], (widths, rel)
 
 
-def test_stack_column_segments_and_ragged_rows_tf32():
+@pytest.mark.parametrize("precision", ["tf32", "bf16"])
+def test_stack_column_segments_and_ragged_rows(precision):
     """72-wide, 40-row images: two column segments per row block and a partial last row block in every layer."""
-    rel, _, _ = run_stack((1, 64, 64, 32, 1), "tf32", 40, 72, 300, 2)
-    assert rel <= TOL_REL_L2["tf32"], rel
+    rel, _, _ = run_stack((1, 64, 64, 32, 32, 64, 32, 1), precision, 40, 72, 300, 2)
+    assert rel <= TOL_REL_L2[precision], rel
+
+
+def test_stack_bf16_odd_width_gather_path():
+    """n2 = 20 (not a multiple of 8): the bf16 first layer gathers its strip with plain loads instead of TMA."""
+    rel, _, _ = run_stack((1, 32, 64, 32, 1), "bf16", 24, 20, 150, 3)
+    assert rel <= TOL_REL_L2["bf16"], rel
 
 
 def test_stack_final_relu_f32():
@@ -53,13 +63,14 @@ def test_stack_final_relu_f32():
     assert rel <= TOL_REL_L2["f32"], rel
 
 
-def test_stack_batch_invariance_tf32():
+@pytest.mark.parametrize("precision", ["tf32", "bf16"])
+def test_stack_batch_invariance(precision):
     """Image i of a batch equals the same image recovered alone (every kernel is per-image independent)."""
     import torch
     from paper_1701_03891_b200 import DeepInverse
-    case = Case(32, 32, 200, 4, "tf32", 6, 3, params=stack_params((1, 64, 64, 32, 1)))
-    ctx = DeepInverse(case.phi, case.params, 32, 32, "tf32", max_batch=4)
-    y = torch.from_numpy(case.y).cuda()
+    case = Case(32, 32, 200, 4, precision, 6, 3, params=stack_params((1, 64, 64, 32, 1)))
+    ctx = DeepInverse(case.phi, case.params, 32, 32, precision, max_batch=4)
+    y = torch.from_numpy(case.y).to(device="cuda", dtype=ctx.storage_dtype)
     full = ctx.recover(y).cpu().numpy()
     one = ctx.recover(y[2:3].contiguous()).cpu().numpy()
     assert np.array_equal(full[2], one[0])
@@ -67,7 +78,7 @@ def test_stack_batch_invariance_tf32():
 
 
 @pytest.mark.parametrize("widths,precision", [((1, 16, 1), "tf32"), ((1, 64, 128, 1), "f32"), ((1, 64, 1), "tf32"),
-                                               ((1, 32, 32, 1), "bf16")])
+                                               ((1, 64, 1), "bf16"), ((1, 16, 32, 1), "bf16")])
 def test_stack_unsupported_shapes_are_rejected(widths, precision):
     from paper_1701_03891_b200 import DeepInverse, DiError
     case = Case(16, 16, 64, 1, "f32", params=stack_params(widths))
