@@ -181,6 +181,26 @@ class ClockSampler:
                 "window": "timed region only" if inside else "whole sampler run"}
 
 
+def conv2_useful_mac_ceiling(n1: int, n2: int, rows: int = 6) -> float:
+    """Fraction of the tensor-core MACs k_conv2_tc issues that are useful: 11 of 12 column-tap slots,
+    times output positions over MMA columns -- units of `rows` output rows x <= 64 columns, strip pitch n2 + 5 (one
+    column segment) or 74, tiles of <= 253 outputs issued as N = round16(count + 3) <= 256 columns."""
+    wseg = min(n2, 64)
+    ncs = -(-n2 // wseg)
+    P = n2 + 5 if ncs == 1 else wseg + 10
+    useful = cols = 0
+    for r0 in range(0, n1, rows):
+        rr = min(rows, n1 - r0)
+        L = (rr - 1) * P + wseg
+        t = 0
+        while t * 253 < L:
+            cnt = min(253, L - 253 * t)
+            cols += min(256, (cnt + 3 + 15) // 16 * 16)
+            t += 1
+        useful += rr * wseg
+    return 11.0 / 12.0 * useful / cols
+
+
 # ----------------------------------------------------------------------------- workload
 def workload(name: str):
     import synth
@@ -372,6 +392,10 @@ def run_ours(args):
             "peak_note": peak_note, "traffic": traffic_for(kname, c.name),
             "algorithmic": f"2*32*64*121 = {CONV2_FLOP_PER_PX} FLOP/pixel x {B * c.N} pixels per launch",
             "launch_ms": conv2_ms}
+    if prec == "bf16":   # the tap-stacked form's useful-MAC ceiling and the fraction of it reached
+        ceil = conv2_useful_mac_ceiling(c.n, c.n)
+        roof["design_ceiling"] = ceil
+        roof["frac_of_design_ceiling"] = roof["frac"] / ceil if roof["frac"] else None
 
     per_step = ms / args.steps
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
