@@ -288,8 +288,91 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// fp32 conv layer 3 (32 -> 1), register-blocked sliding window: block = 32 output rows x 64 columns, thread = 8
+// consecutive columns of one row.  Channels pass in chunks of 4 through a [4][42][76] halo tile; per (channel, tap
+// row) the thread's 18 inputs arrive by 4 LDS.128 + 1 LDS.64 and feed 8 x 11 FMAs (the one-pixel-per-thread
+// kernel above re-reads every input from shared memory for each tap and is bound by it).  Accumulation: per channel
+// over its 121 taps, then over the 32 channels in order.
+constexpr int C3F_TH = 32, C3F_TW = 64, C3F_CC = 4, C3F_WS = 76;
+__global__ void __launch_bounds__(256) k_conv3_f32_sw(const float* __restrict__ in, const float* __restrict__ wx,
+                                                      const float* __restrict__ bias, int fullmap, int relu,
+                                                      float* __restrict__ out, int n1, int n2) {
+  constexpr int HT = C3F_TH + 10, WT = C3F_TW + 10;
+  extern __shared__ __align__(16) float smf[];
+  float* sx = smf;                                   // [C3F_CC][HT][C3F_WS]
+  float* sw = smf + C3F_CC * HT * C3F_WS;            // [32 ci][11 a][12] (tap 11 zero)
+  const int b = blockIdx.z, y0 = blockIdx.y * C3F_TH, x0 = blockIdx.x * C3F_TW;
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  for (int e = tid; e < 32 * 11 * 12; e += 256) {
+    const int ci = e / 132, r = e - ci * 132, a = r / 12, bb = r - a * 12;
+    sw[e] = bb < 11 ? wx[(size_t)ci * 121 + a * 11 + bb] : 0.f;
+  }
+  float acc[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) acc[p] = 0.f;
+  for (int cc0 = 0; cc0 < 32; cc0 += C3F_CC) {
+    __syncthreads();
+    for (int e = tid; e < C3F_CC * HT * WT; e += 256) {   // channel innermost: one pixel's 4 channels per 4 threads
+      const int c = e % C3F_CC, pix = e / C3F_CC, yy = pix / WT, xx = pix - yy * WT;
+      const int gy = y0 + yy - 5, gx = x0 + xx - 5;
+      sx[(c * HT + yy) * C3F_WS + xx] =
+          (gy >= 0 && gy < n1 && gx >= 0 && gx < n2) ? in[(((size_t)b * n1 + gy) * n2 + gx) * 32 + cc0 + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int c = 0; c < C3F_CC; ++c) {
+      float part[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) part[p] = 0.f;
+#pragma unroll 1
+      for (int a = 0; a < 11; ++a) {
+        const float* xr = sx + (c * HT + ty + a) * C3F_WS + 8 * tx;
+        float xv[18];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 v = reinterpret_cast<const float4*>(xr)[q];
+          xv[4 * q] = v.x, xv[4 * q + 1] = v.y, xv[4 * q + 2] = v.z, xv[4 * q + 3] = v.w;
+        }
+        {
+          const float2 v = reinterpret_cast<const float2*>(xr)[8];
+          xv[16] = v.x, xv[17] = v.y;
+        }
+        const float4* w4 = reinterpret_cast<const float4*>(sw + ((cc0 + c) * 11 + a) * 12);
+        const float4 wa = w4[0], wb = w4[1], wc = w4[2];
+        const float w[11] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w, wc.x, wc.y, wc.z};
+#pragma unroll
+        for (int bb = 0; bb < 11; ++bb)
+#pragma unroll
+          for (int p = 0; p < 8; ++p) part[p] = fmaf(xv[p + bb], w[bb], part[p]);
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) acc[p] += part[p];
+    }
+  }
+  const int oy = y0 + ty;
+  if (oy >= n1) return;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int ox = x0 + 8 * tx + p;
+    if (ox >= n2) continue;
+    float bv = 0.f;
+    if (bias) bv = fullmap ? bias[(size_t)oy * n2 + ox] : bias[0];
+    float v = acc[p] + bv;
+    if (relu) v = fmaxf(v, 0.f);
+    out[((size_t)b * n1 + oy) * n2 + ox] = v;
+  }
+}
+
 cudaError_t launch_conv3_simt(const void* h2, bool bf16, const float* wx, const float* bias, int fullmap, int relu,
                               float* xhat, int batch, int n1, int n2, cudaStream_t st) {
+  if (!bf16) {
+    const size_t smem = ((size_t)C3F_CC * (C3F_TH + 10) * C3F_WS + 32 * 11 * 12) * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(k_conv3_f32_sw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((n2 + C3F_TW - 1) / C3F_TW, (n1 + C3F_TH - 1) / C3F_TH, batch);
+    k_conv3_f32_sw<<<grid, 256, smem, st>>>(reinterpret_cast<const float*>(h2), wx, bias, fullmap, relu, xhat, n1, n2);
+    return cudaGetLastError();
+  }
   constexpr int TH = 8, TW = 32;
   dim3 grid((n2 + TW - 1) / TW, (n1 + TH - 1) / TH, batch);
   if (bf16) {
