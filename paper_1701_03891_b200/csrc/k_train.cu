@@ -148,6 +148,91 @@ __global__ void __launch_bounds__(CI_T * CO_T * 4)
   if (do_bias) part_b[(size_t)chunk * COUT + co0 + co_l] = bacc;
 }
 
+// As k_wgrad for an even number of output channels per block, with packed FFMA2 (fma.rn.f32x2: two IEEE fp32 FMAs,
+// bit-identical to fmaf): a thread owns the channel PAIR (co, co + 1) of one ci, the pair's dG values sit side by
+// side in shared memory (one LDS.64), the sliding X value is broadcast into the operand -- half the FMA
+// instructions of two k_wgrad threads.
+__device__ __forceinline__ void ffma2_t(uint64_t& d, float a, uint64_t b) {   // d = (a, a) * b + d per half, RN
+  uint64_t aa;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(aa), "l"(b));
+}
+template <int CIN, int COUT, int CI_T, int CO_T>
+__global__ void __launch_bounds__(CI_T * CO_T * 2)
+    k_wgrad_pair(const float* __restrict__ X, const float* __restrict__ dG, int batch, int n1, int n2, int nchunk,
+                 float* __restrict__ part_w, float* __restrict__ part_b) {
+  constexpr int NP = CO_T / 2;                       // channel pairs per block
+  constexpr int NT = CI_T * NP * 4;
+  constexpr int HT = TH + 10, WT = TW + 10;
+  __shared__ float sx[CI_T][HT][WT];
+  __shared__ __align__(8) float sg[NP][TH][TW][2];   // (co, co + 1) interleaved
+  const int ci0 = (blockIdx.x % (CIN / CI_T)) * CI_T, co0 = (blockIdx.x / (CIN / CI_T)) * CO_T;
+  const int chunk = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int ag = tid / (CI_T * NP), rem = tid % (CI_T * NP);
+  const int cp = rem / CI_T, ci_l = rem % CI_T;
+  const bool do_bias = ci0 == 0 && ci_l == 0 && ag == 0;
+  uint64_t acc[3][KS];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < KS; ++j) acc[i][j] = 0ull;
+  float bacc0 = 0.f, bacc1 = 0.f;
+  const int tx = (n2 + TW - 1) / TW, ty = (n1 + TH - 1) / TH;
+  const long long ntiles = (long long)batch * tx * ty;
+  for (long long t = chunk; t < ntiles; t += nchunk) {
+    const int b = (int)(t / (tx * ty)), tr = (int)(t % (tx * ty));
+    const int y0 = (tr / tx) * TH, x0 = (tr % tx) * TW;
+    __syncthreads();
+    for (int e = tid; e < CI_T * HT * WT; e += NT) {
+      const int c = e / (HT * WT), r2 = e % (HT * WT), yy = r2 / WT, xx = r2 % WT;
+      const int gy = y0 + yy - 5, gx = x0 + xx - 5;
+      sx[c][yy][xx] = (gy >= 0 && gy < n1 && gx >= 0 && gx < n2)
+                          ? X[(((size_t)b * n1 + gy) * n2 + gx) * CIN + ci0 + c] : 0.f;
+    }
+    for (int e = tid; e < CO_T * TH * TW; e += NT) {
+      const int c = e % CO_T, pix = e / CO_T, yy = pix / TW, xx = pix % TW;   // channel innermost: coalesced
+      const int gy = y0 + yy, gx = x0 + xx;
+      sg[c >> 1][yy][xx][c & 1] = (gy < n1 && gx < n2) ? dG[(((size_t)b * n1 + gy) * n2 + gx) * COUT + co0 + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ai = 0; ai < 3; ++ai) {
+      const int a = ag + 4 * ai;
+      if (a >= KS) continue;
+#pragma unroll 1
+      for (int r = 0; r < TH; ++r) {
+        float xr[WT];
+#pragma unroll
+        for (int j = 0; j < WT; ++j) xr[j] = sx[ci_l][r + a][j];
+#pragma unroll
+        for (int px = 0; px < TW; ++px) {
+          const uint64_t g = *reinterpret_cast<const uint64_t*>(&sg[cp][r][px][0]);
+#pragma unroll
+          for (int bb = 0; bb < KS; ++bb) ffma2_t(acc[ai][bb], xr[px + bb], g);
+        }
+      }
+    }
+    if (do_bias)
+      for (int i = 0; i < TH * TW; ++i) bacc0 += sg[cp][i / TW][i % TW][0], bacc1 += sg[cp][i / TW][i % TW][1];
+  }
+  float* pw = part_w + (size_t)chunk * COUT * CIN * KS * KS;
+  const int co = co0 + 2 * cp;
+#pragma unroll
+  for (int ai = 0; ai < 3; ++ai) {
+    const int a = ag + 4 * ai;
+    if (a >= KS) continue;
+#pragma unroll
+    for (int bb = 0; bb < KS; ++bb) {
+      float lo, hi;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[ai][bb]));
+      pw[(((size_t)co * CIN + ci0 + ci_l) * KS + a) * KS + bb] = lo;
+      pw[(((size_t)(co + 1) * CIN + ci0 + ci_l) * KS + a) * KS + bb] = hi;
+    }
+  }
+  if (do_bias) part_b[(size_t)chunk * COUT + co] = bacc0, part_b[(size_t)chunk * COUT + co + 1] = bacc1;
+}
+
 // dW (API orientation) = sum over chunks (fp64, chunk order); xcorr-orientation tap (a, b) is the user's (u, v) =
 // (10 - a, 10 - b) unless the context was created with DI_FLAG_XCORR
 __global__ void k_wgrad_reduce(const float* __restrict__ part_w, const float* __restrict__ part_b, int nchunk,
@@ -170,7 +255,11 @@ template <int CIN, int COUT, int CI_T, int CO_T>
 static cudaError_t wgrad(const float* X, const float* dG, int batch, int n1, int n2, int nchunk, float* part_w,
                          float* part_b, int flip, float* gw, float* gb, cudaStream_t st) {
   dim3 grid((CIN / CI_T) * (COUT / CO_T), nchunk);
-  k_wgrad<CIN, COUT, CI_T, CO_T><<<grid, CI_T * CO_T * 4, 0, st>>>(X, dG, batch, n1, n2, nchunk, part_w, part_b);
+  if constexpr (CO_T % 2 == 0)
+    k_wgrad_pair<CIN, COUT, CI_T, CO_T><<<grid, CI_T * CO_T * 2, 0, st>>>(X, dG, batch, n1, n2, nchunk, part_w,
+                                                                         part_b);
+  else
+    k_wgrad<CIN, COUT, CI_T, CO_T><<<grid, CI_T * CO_T * 4, 0, st>>>(X, dG, batch, n1, n2, nchunk, part_w, part_b);
   const int nw = COUT * CIN * KS * KS;
   k_wgrad_reduce<<<(nw + COUT + 255) / 256, 256, 0, st>>>(part_w, part_b, nchunk, nw, COUT, flip, gw, gb);
   return cudaGetLastError();
