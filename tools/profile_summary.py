@@ -48,7 +48,8 @@ across boxes). CPU baseline (fp64 oracle): {b['cpu_baseline']['value']:.0f} imag
 {b['cpu_baseline']['single_thread_s_per_image']:.2f} s per image on one thread.
 """
 old = open(os.path.join(prof, "r01_summary.md")).read()
-keep = old[old.index("\nOther configs"):old.index("## Launch list")]
+start = old.index("\nRun-to-run") if "\nRun-to-run" in old else old.index("\nOther configs")
+keep = old[start:old.index("## Launch list")]   # hand-written notes between the header and the tables
 tail = old[old.index("## Where conv2's issuing thread waits"):]
 out = (head + keep + "## Launch list (cold-cache, serialised; compare shares — the e2e part of the command runs chunked "
        "batches, so\n## per-launch means mix batch sizes)\n\n" + launch + f"\n## ncu --set full (one launch each, capture {tag})\n\n"
