@@ -128,3 +128,28 @@ def test_metrics_golden():
     x = RNG.standard_normal(50)
     for c in GOLD["nmse"]["cases"]:
         assert oracle.nmse(c["scale"] * x, x) == pytest.approx(c["nmse"], abs=1e-15)
+
+
+@pytest.mark.parametrize("bias", ["zero", "channel"])
+def test_forward_xcorr_flag(bias):
+    """DI_FLAG_XCORR at the forward level: taps T given in cross-correlation
+    convention.  Pinned two ways: (1) forward(T, xcorr) == forward(flip(T)) bitwise -- the flip is an index
+    relabelling, same products in the same order; (2) torch conv2d (itself a cross-correlation) with T unflipped."""
+    torch = pytest.importorskip("torch")
+    n1, n2, m = 13, 10, 60
+    phi = synth.make_phi(m, n1 * n2).astype(np.float64)
+    p = synth.make_params(bias=bias)
+    y = RNG.standard_normal((2, m))
+    got = oracle.forward(y, phi, p, n1, n2, xcorr=True)
+    flipped = synth.Params([np.ascontiguousarray(np.asarray(w)[:, :, ::-1, ::-1]) for w in p.w], p.b)
+    assert np.array_equal(got, oracle.forward(y, phi, flipped, n1, n2))
+    a = (torch.from_numpy(y) @ torch.from_numpy(phi)).reshape(-1, 1, n1, n2)
+    for l, (w, b) in enumerate(zip(p.w, p.b)):
+        a = torch.nn.functional.conv2d(a, torch.from_numpy(np.asarray(w, np.float64)),
+                                       torch.from_numpy(np.asarray(b, np.float64)), padding=5)
+        if l < 2:
+            a = a.relu()
+    ref = a[:, 0].numpy()
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
+    # and the flag matters: the He-normal taps are not symmetric
+    assert not np.allclose(got, oracle.forward(y, phi, p, n1, n2))

@@ -82,3 +82,44 @@ def test_paper_widths_single_image_runs_and_final_relu_flag():
     assert loss > 0 and [g.shape for g in dws] == [w.shape for w in p.w]
     loss_r, dws_r, _ = oracle.train_grad(y, x, phi, p, c.n, c.n, final_relu=True)
     assert np.isfinite(loss_r) and dws_r[2].shape == p.w[2].shape
+
+
+def _loss_fr(phi, p, y, x, n1, n2):
+    xh = oracle.forward(y, phi, p, n1, n2, final_relu=True)
+    return float(np.sum((xh - x) ** 2)) / y.shape[0]
+
+
+@pytest.mark.parametrize("seed", [5, 6])
+def test_final_relu_gradient_vs_central_differences(seed):
+    """PAPER.md:118 ("each convolutional layer applies a ReLU") read literally: the layer-3 ReLU mask must reach the
+    gradient.  The case has layer-3 pre-activations on both sides of zero (checked), so a gradient that ignored the
+    mask (or masked with the wrong sign) differs from the finite differences of the masked loss."""
+    phi, p, y, x, n1, n2 = _tiny(seed)
+    xh = oracle.forward(y, phi, p, n1, n2, final_relu=True)
+    lin = oracle.forward(y, phi, p, n1, n2, final_relu=False)
+    assert np.any(lin < -1e-3) and np.any(lin > 1e-3)          # both sides of the kink
+    assert np.array_equal(xh, np.maximum(lin, 0.0))
+    loss, dws, dbs = oracle.train_grad(y, x, phi, p, n1, n2, final_relu=True)
+    assert loss == pytest.approx(_loss_fr(phi, p, y, x, n1, n2), rel=1e-12)
+    _, dws0, dbs0 = oracle.train_grad(y, x, phi, p, n1, n2, final_relu=False)
+    assert not np.allclose(dbs[2], dbs0[2])                    # the flag changes the gradient
+    r = np.random.default_rng(seed + 20)
+    eps = 1e-6
+    for l in range(3):
+        for _ in range(6):
+            idx = tuple(int(r.integers(0, s)) for s in p.w[l].shape)
+            wp = [w.copy() for w in p.w]
+            wm = [w.copy() for w in p.w]
+            wp[l][idx] += eps
+            wm[l][idx] -= eps
+            fd = (_loss_fr(phi, synth.Params(wp, p.b), y, x, n1, n2) -
+                  _loss_fr(phi, synth.Params(wm, p.b), y, x, n1, n2)) / (2 * eps)
+            assert dws[l][idx] == pytest.approx(fd, rel=1e-5, abs=1e-8), (l, idx)
+        for o in range(p.b[l].size):
+            bp = [b.copy() for b in p.b]
+            bm = [b.copy() for b in p.b]
+            bp[l][o] += eps
+            bm[l][o] -= eps
+            fd = (_loss_fr(phi, synth.Params(p.w, bp), y, x, n1, n2) -
+                  _loss_fr(phi, synth.Params(p.w, bm), y, x, n1, n2)) / (2 * eps)
+            assert dbs[l][o] == pytest.approx(fd, rel=1e-5, abs=1e-8), (l, o)
