@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdeepinverse.so")
+# DI_LIB selects another build (the experiment library libdeepinverse_exp.so, build.py); default: the product library
+LIB_PATH = os.environ.get("DI_LIB") or os.path.join(_HERE, "libdeepinverse.so")
 
 DI_OK, DI_ERR_ARG, DI_ERR_DIM, DI_ERR_DOMAIN, DI_ERR_DEVICE, DI_ERR_OOM, DI_ERR_CUDA = range(7)
 DI_PREC_FP32, DI_PREC_TF32, DI_PREC_BF16 = 0, 1, 2
@@ -122,11 +123,13 @@ def _ptr(a) -> int | None:
     return a.ctypes.data
 
 
-def _stream_handle(stream) -> int | None:
+def _stream_handle(stream, device: int | None = None) -> int | None:
+    """The raw cudaStream_t: `stream` (torch.cuda.Stream or int), else torch's current stream of `device` (the
+    context's device; torch's current device when None)."""
     if stream is None:
         try:
             import torch
-            return torch.cuda.current_stream().cuda_stream
+            return torch.cuda.current_stream(device).cuda_stream
         except Exception:  # pragma: no cover
             return None
     if hasattr(stream, "cuda_stream"):
@@ -268,15 +271,33 @@ class DeepInverse:
         import torch
         return torch.bfloat16 if self.precision == "bf16" else torch.float32
 
+    def _check_y(self, y):
+        if not hasattr(y, "is_cuda") or y.dtype != self.storage_dtype or not y.is_cuda:
+            raise TypeError(f"y must be a CUDA {self.storage_dtype} tensor")
+        if y.device.index != self.device:
+            raise TypeError(f"y is on {y.device}, the context on cuda:{self.device}")
+        if y.dim() != 2 or y.shape[1] != self.m or y.stride(1) != 1:
+            raise TypeError(f"y must be [B][{self.m}] with unit column stride (rows may be padded), got "
+                            f"{tuple(y.shape)} strides {y.stride()}")
+
+    def _check_out(self, t, shape, what):
+        import torch
+        if (t.dtype != torch.float32 or not t.is_cuda or t.device.index != self.device or not t.is_contiguous()
+                or tuple(t.shape) != tuple(shape)):
+            raise TypeError(f"{what} must be a contiguous float32 tensor {tuple(shape)} on cuda:{self.device}")
+
+    def _stream(self, stream):
+        return _stream_handle(stream, self.device)
+
     def recover(self, y, xhat=None, stream=None):
         """y: device tensor [B][ldy] of the storage dtype; returns x_hat [B][n1][n2] fp32 (device)."""
         import torch
-        if y.dtype != self.storage_dtype or not y.is_cuda:
-            raise TypeError(f"y must be a CUDA {self.storage_dtype} tensor")
+        self._check_y(y)
         b = y.shape[0]
         if xhat is None:
             xhat = torch.empty((b, self.n1, self.n2), dtype=torch.float32, device=y.device)
-        di_recover(self.ctx, y, y.stride(0), b, xhat, stream)
+        self._check_out(xhat, (b, self.n1, self.n2), "xhat")
+        di_recover(self.ctx, y, y.stride(0), b, xhat, self._stream(stream))
         return xhat
 
     def proxy_partial(self, y, out=None, stream=None):
@@ -288,7 +309,7 @@ class DeepInverse:
         b = y.shape[0]
         if out is None:
             out = torch.empty((b, self.n1 * self.n2), dtype=torch.float32, device=y.device)
-        di_proxy_partial(self.ctx, y, y.stride(0), b, out, stream)
+        di_proxy_partial(self.ctx, y, y.stride(0), b, out, self._stream(stream))
         return out
 
     def recover_from_proxy(self, xt, xhat=None, stream=None):
@@ -299,7 +320,7 @@ class DeepInverse:
         b = xt.shape[0]
         if xhat is None:
             xhat = torch.empty((b, self.n1, self.n2), dtype=torch.float32, device=xt.device)
-        di_recover_from_proxy(self.ctx, xt, b, xhat, stream)
+        di_recover_from_proxy(self.ctx, xt, b, xhat, self._stream(stream))
         return xhat
 
     def proxy_scatter(self, y, slots, world: int, rank: int, stream=None):
@@ -307,7 +328,7 @@ class DeepInverse:
         to slots[b // nb] (device pointers: the owners' [world][nb][N] fp32 staging buffers, peer-mapped)."""
         if y.dtype != self.storage_dtype or not y.is_cuda:
             raise TypeError(f"y must be a CUDA {self.storage_dtype} tensor")
-        di_proxy_scatter(self.ctx, y, y.stride(0), y.shape[0], slots, world, rank, stream)
+        di_proxy_scatter(self.ctx, y, y.stride(0), y.shape[0], slots, world, rank, self._stream(stream))
 
     def recover_from_slots(self, staging, world: int, xhat=None, stream=None):
         """Owner side: x_tilde = sum of the world slots of `staging` [world][nb][N] fp32 (rank order), then the convs."""
@@ -315,16 +336,40 @@ class DeepInverse:
         nb = staging.shape[1]
         if xhat is None:
             xhat = torch.empty((nb, self.n1, self.n2), dtype=torch.float32, device=staging.device)
-        di_recover_from_slots(self.ctx, staging, world, nb, xhat, stream)
+        di_recover_from_slots(self.ctx, staging, world, nb, xhat, self._stream(stream))
         return xhat
 
     def recover_host(self, y_host, xhat_host=None, stream=None):
-        """End-to-end: host y (numpy/pinned torch, storage dtype) -> host x_hat fp32."""
+        """End-to-end: host y (numpy or CPU torch tensor, [B][m] of the storage dtype, unit column stride; pinned
+        memory gives the fast copies) -> host x_hat fp32 [B][n1][n2] (numpy or CPU torch, contiguous)."""
+        if hasattr(y_host, "is_cuda"):            # torch
+            import torch
+            if y_host.is_cuda or y_host.dtype != self.storage_dtype:
+                raise TypeError(f"y_host must be a CPU {self.storage_dtype} tensor")
+            if y_host.dim() != 2 or y_host.shape[1] != self.m or y_host.stride(1) != 1:
+                raise TypeError(f"y_host must be [B][{self.m}] with unit column stride")
+            ldy = y_host.stride(0)
+        else:
+            if self.precision == "bf16":
+                raise TypeError("a bf16 context takes y_host as a CPU torch.bfloat16 tensor (numpy has no bf16)")
+            y_host = np.asarray(y_host)
+            if y_host.dtype != np.float32 or y_host.ndim != 2 or y_host.shape[1] != self.m or \
+                    y_host.strides[1] != 4:
+                raise TypeError(f"y_host must be float32 [B][{self.m}] with unit column stride")
+            ldy = y_host.strides[0] // 4
         b = y_host.shape[0]
         if xhat_host is None:
             xhat_host = np.empty((b, self.n1, self.n2), np.float32)
-        ldy = y_host.stride(0) if hasattr(y_host, "stride") and callable(y_host.stride) else y_host.strides[0] // y_host.itemsize
-        di_recover_host(self.ctx, y_host, ldy, b, xhat_host, stream)
+        if hasattr(xhat_host, "is_cuda"):
+            import torch
+            ok = (not xhat_host.is_cuda and xhat_host.dtype == torch.float32 and xhat_host.is_contiguous() and
+                  tuple(xhat_host.shape) == (b, self.n1, self.n2))
+        else:
+            ok = (isinstance(xhat_host, np.ndarray) and xhat_host.dtype == np.float32 and
+                  xhat_host.flags.c_contiguous and xhat_host.shape == (b, self.n1, self.n2))
+        if not ok:
+            raise TypeError(f"xhat_host must be a contiguous host float32 array {(b, self.n1, self.n2)}")
+        di_recover_host(self.ctx, y_host, ldy, b, xhat_host, self._stream(stream))
         return xhat_host
 
     def measure(self, x, y=None, stream=None):
@@ -335,12 +380,12 @@ class DeepInverse:
         b = x.shape[0]
         if y is None:
             y = torch.empty((b, self.m), dtype=self.storage_dtype, device=x.device)
-        di_measure(self.ctx, x, b, y, y.stride(0), stream)
+        di_measure(self.ctx, x, b, y, y.stride(0), self._stream(stream))
         return y
 
     def add_noise(self, y, snr_db: float, seed: int, stream=None):
         """In place: y_b += N(0, ||y_b||^2 / (m 10^(snr/10))) noise (Table 3 reading, Q14)."""
-        di_add_noise(self.ctx, y, y.stride(0), y.shape[0], snr_db, seed, stream)
+        di_add_noise(self.ctx, y, y.stride(0), y.shape[0], snr_db, seed, self._stream(stream))
         return y
 
     def metrics(self, xhat, x, stream=None):
@@ -348,7 +393,7 @@ class DeepInverse:
         import torch
         b = x.shape[0]
         out = torch.empty((3, b), dtype=torch.float64, device=x.device)
-        di_metrics(self.ctx, xhat, x, b, out, stream)
+        di_metrics(self.ctx, xhat, x, b, out, self._stream(stream))
         return out.cpu().numpy()
 
     # ------------------------------------------------------------ training (NEXT-2; paper stack, per-channel biases)
@@ -363,21 +408,21 @@ class DeepInverse:
         if grads is None:
             grads = torch.empty(di_num_params(), dtype=torch.float32, device=y.device)
         loss = torch.empty(1, dtype=torch.float64, device=y.device)
-        di_train_grad(self.ctx, y, y.stride(0), x, b, 1.0 / b if scale is None else scale, grads, loss, stream)
+        di_train_grad(self.ctx, y, y.stride(0), x, b, 1.0 / b if scale is None else scale, grads, loss, self._stream(stream))
         return loss, grads
 
     def sgd_step(self, grads, lr: float, momentum: float = 0.0, stream=None):
-        di_sgd_step(self.ctx, grads, lr, momentum, stream)
+        di_sgd_step(self.ctx, grads, lr, momentum, self._stream(stream))
 
     def params(self, stream=None):
         """Current parameters as numpy arrays ([W1, W2, W3], [b1, b2, b3]) in the orientation given at creation."""
         import torch
         p = torch.empty(di_num_params(), dtype=torch.float32, device=f"cuda:{self.device}")
-        di_get_params(self.ctx, p, stream)
+        di_get_params(self.ctx, p, self._stream(stream))
         return split_params(p.cpu().numpy())
 
     def debug_stage(self, stage: int, x_in, x_out, batch: int, stream=None):
-        di_debug_stage(self.ctx, stage, x_in, x_out, batch, stream)
+        di_debug_stage(self.ctx, stage, x_in, x_out, batch, self._stream(stream))
 
     def info(self) -> dict:
         inf = di_info()

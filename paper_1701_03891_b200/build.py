@@ -5,6 +5,7 @@ loaded with ctypes, so the same .so serves C callers, the Python binding, tests 
 """
 from __future__ import annotations
 
+import json
 import os
 import subprocess
 import sys
@@ -19,12 +20,45 @@ HEADERS = ["sm100.cuh", "kernels.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", "-diag-suppress", "177"]
-# extra flags for experiments only (e.g. DI_NVCC_EXTRA=-DDI_PROF_CONV2 for the conv2 issuer cycle breakdown)
-FLAGS += os.environ.get("DI_NVCC_EXTRA", "").split()
+# Experiment builds (e.g. DI_NVCC_EXTRA=-DDI_PROF_CONV2 for the conv2 issuer cycle breakdown) go to a SEPARATE library,
+# libdeepinverse_exp.so with its own object directory, compiled with -DDI_EXPERIMENT_BUILD (kernels.cuh refuses the
+# instrumentation macros without it).  The product library is never built with extra flags; a stamp file next to it
+# records the exact flags and nvcc version, and any difference forces a rebuild.
+EXTRA = os.environ.get("DI_NVCC_EXTRA", "").split()
+EXP_LIB = os.path.join(HERE, "libdeepinverse_exp.so")
 
 
-def _stale(target: str, deps: list[str]) -> bool:
+def _target(extra: list[str]) -> tuple[str, str, list[str]]:
+    if extra:
+        return EXP_LIB, os.path.join(HERE, "build_exp"), FLAGS + ["-DDI_EXPERIMENT_BUILD"] + extra
+    return LIB, os.path.join(HERE, "build"), list(FLAGS)
+
+
+def _nvcc_version() -> str:
+    try:
+        return subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.strip().splitlines()[-1]
+    except OSError:
+        return "?"
+
+
+def _stamp(flags: list[str]) -> str:
+    return json.dumps({"flags": flags, "nvcc": _nvcc_version()}, sort_keys=True)
+
+
+def read_stamp(lib: str = LIB) -> dict | None:
+    try:
+        return json.load(open(lib + ".stamp"))
+    except (OSError, ValueError):
+        return None
+
+
+def _stale(target: str, deps: list[str], stamp: str) -> bool:
     if not os.path.exists(target):
+        return True
+    try:
+        if open(target + ".stamp").read() != stamp:
+            return True
+    except OSError:
         return True
     t = os.path.getmtime(target)
     return any(os.path.getmtime(d) > t for d in deps)
@@ -44,18 +78,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 def _build_locked(force: bool, verbose: bool) -> str:
+    lib, objdir, flags = _target(EXTRA)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "deepinverse.h"),
                                                                  os.path.abspath(__file__)]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    objdir = os.path.join(HERE, "build")
+    stamp = _stamp(flags)
+    if not force and not _stale(lib, deps, stamp):
+        return lib
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for s in SOURCES:
         o = os.path.join(objdir, s.replace(".cu", ".o"))
         objs.append(o)
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", os.path.join(CSRC, s), "-o", o]
+        cmd = [NVCC, *flags, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -65,13 +100,15 @@ def _build_locked(force: bool, verbose: bool) -> str:
             raise RuntimeError(f"nvcc failed on {s}:\n{out}")
         if verbose and out.strip():
             print(out, file=sys.stderr)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-cudart", "static"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    with open(lib + ".stamp", "w") as f:
+        f.write(stamp)
+    return lib
 
 
 if __name__ == "__main__":

@@ -21,6 +21,21 @@ namespace {
 
 thread_local char g_err[512] = "";
 
+// Every entry point switches to the context's device and restores the caller's current device on return.
+struct DevGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DevGuard(const DevGuard&) = delete;
+  DevGuard& operator=(const DevGuard&) = delete;
+};
+
 di_status fail(di_status s, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -74,6 +89,7 @@ float bf2f(uint16_t b) {
 
 struct di_ctx_s {
   int device = 0, num_sms = 0;
+  bool conv2_mc = true;         // conv2 CTA-pair weight multicast (DI_EXP_NO_MC=1 at di_create turns it off: A/B tests)
   int m = 0, n1 = 0, n2 = 0, N = 0, max_batch = 0, kpad = 0;
   int pxbn = 256;               // pixel-tile width of the lifting GEMM = row count of a Phi^T block
   di_precision prec = DI_PREC_BF16;
@@ -693,7 +709,7 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
         if (s != DI_OK) return s;
         tmp = &tm;
       }
-      CUDA_TRY(di::launch_conv2_tc(tmp, c->wp2, c->b2, fm, batch, c->n1, c->n2, h2, c->num_sms, st));
+      CUDA_TRY(di::launch_conv2_tc(tmp, c->wp2, c->b2, fm, batch, c->n1, c->n2, h2, c->num_sms, st, c->conv2_mc));
     } else if (c->prec == DI_PREC_TF32) {
       CUtensorMap tm;
       const CUtensorMap* tmp = &c->tmH1;
@@ -737,6 +753,11 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
 }  // namespace
 
 extern "C" {
+
+#ifdef DI_EXPERIMENT_BUILD
+// present only in libdeepinverse_exp.so (tests/test_abi.py asserts the product library does not export it)
+__attribute__((visibility("default"))) const char di_experiment_build[] = "experiment build";
+#endif
 
 const char* di_status_string(di_status s) {
   switch (s) {
@@ -797,12 +818,14 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, a->device);
   if (maj != 10 || min != 0)
     return fail(DI_ERR_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a only", a->device, maj, min);
-  CUDA_TRY(cudaSetDevice(a->device));
+  DevGuard dg_(a->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", a->device);
 
   di_ctx c = new (std::nothrow) di_ctx_s();
   if (!c) return fail(DI_ERR_OOM, "host allocation failed");
   c->device = a->device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, a->device);
+  c->conv2_mc = getenv("DI_EXP_NO_MC") == nullptr;   // read once per context, never on the launch path
   c->m = a->m, c->n1 = a->n1, c->n2 = a->n2, c->N = (int)N, c->max_batch = a->max_batch;
   c->prec = a->precision, c->flags = a->flags;
   c->elt = (a->precision == DI_PREC_BF16) ? 2 : 4;
@@ -1071,7 +1094,8 @@ di_status di_recover(di_ctx c, const void* y, long long ldy, int batch, float* x
   if (!y || !xhat) return fail(DI_ERR_ARG, "y and xhat must be non-NULL device pointers");
   if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
   if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   return run_stages(c, 0, 3, y, ldy, batch, c->xt, c->h1, c->h2, xhat, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -1080,7 +1104,8 @@ di_status di_proxy_partial(di_ctx c, const void* y, long long ldy, int batch, fl
   if (!y || !xt_part) return fail(DI_ERR_ARG, "y and xt_part must be non-NULL device pointers");
   if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
   if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   int launches = 0;
   return run_proxy(c, y, ldy, batch, xt_part, true, reinterpret_cast<cudaStream_t>(stream), launches);
 }
@@ -1100,7 +1125,8 @@ di_status di_proxy_scatter(di_ctx c, const void* y, long long ldy, int batch, fl
     sc.slots[r] = slots[r];
   }
   sc.world = world, sc.rank = rank, sc.nb = batch / world;
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   int launches = 0;
   return run_proxy(c, y, ldy, batch, c->xt, true, reinterpret_cast<cudaStream_t>(stream), launches, &sc);
 }
@@ -1110,7 +1136,8 @@ di_status di_recover_from_slots(di_ctx c, const float* staging, int world, int n
   if (!staging || !xhat) return fail(DI_ERR_ARG, "staging and xhat must be non-NULL device pointers");
   if (world < 1 || world > 8) return fail(DI_ERR_ARG, "world=%d outside [1, 8]", world);
   if (nb < 1 || nb > c->max_batch) return fail(DI_ERR_ARG, "nb=%d outside [1, %d]", nb, c->max_batch);
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CUDA_TRY(di::launch_reduce_slots(staging, world, nb, c->N, c->xt, c->prec == DI_PREC_BF16, st));
   return run_stages(c, 1, 3, nullptr, 0, nb, c->xt, c->h1, c->h2, xhat, st);
@@ -1120,7 +1147,8 @@ di_status di_recover_from_proxy(di_ctx c, const float* xt, int batch, float* xha
   if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
   if (!xt || !xhat) return fail(DI_ERR_ARG, "xt and xhat must be non-NULL device pointers");
   if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   void* x1 = const_cast<float*>(xt);
   if (c->prec == DI_PREC_BF16) {   // the bf16 path's x_tilde: the summed proxy rounded once (RNE)
@@ -1135,7 +1163,8 @@ di_status di_recover_host(di_ctx c, const void* y_host, long long ldy, int batch
   if (!y_host || !xhat_host) return fail(DI_ERR_ARG, "host buffers must be non-NULL");
   if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
   if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t ybytes = (size_t)batch * ldy * c->elt;
   if (ybytes > c->yhost_bytes) {
@@ -1213,7 +1242,8 @@ di_status di_measure(di_ctx c, const float* x, int batch, void* y, long long ldy
   if (!x || !y) return fail(DI_ERR_ARG, "x and y must be non-NULL device pointers");
   if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
   if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (c->prec == DI_PREC_FP32) {
     CUDA_TRY(di::launch_measure_f32(x, c->phi_sense ? c->phi_sense : reinterpret_cast<const float*>(c->phi), c->m, c->N, batch,
@@ -1252,7 +1282,8 @@ di_status di_add_noise(di_ctx c, void* y, long long ldy, int batch, double snr_d
   if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
   if (std::isnan(snr_db)) return fail(DI_ERR_DOMAIN, "snr_db is NaN");
   if (std::isinf(snr_db) && snr_db > 0) return DI_OK;   // noiseless
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   CUDA_TRY(di::launch_add_noise(y, ldy, c->m, batch, snr_db, stream_key(5, seed), c->prec == DI_PREC_BF16,
                                 reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
@@ -1262,7 +1293,8 @@ di_status di_metrics(di_ctx c, const float* xhat, const float* x, int batch, dou
   if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
   if (!xhat || !x || !out) return fail(DI_ERR_ARG, "NULL device pointer");
   if (batch < 1) return fail(DI_ERR_ARG, "batch=%d must be >= 1", batch);
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   CUDA_TRY(di::launch_metrics(xhat, x, c->N, batch, out, reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }
@@ -1344,7 +1376,6 @@ static di_status train_check(di_ctx c) {
   if (!c->params) return fail(DI_ERR_ARG, "training needs a context with per-channel (or zero) biases");
   if (c->prec == DI_PREC_BF16 && c->n2 % 4 != 0)
     return fail(DI_ERR_ARG, "BF16 training needs n2 %% 4 == 0 (the layer-3 data gradient's strip map)");
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(DI_ERR_CUDA, "cudaSetDevice failed");
   if (!c->b1 || !c->b2 || !c->b3) {   // trainable biases need storage even when created zero
     if (!c->b1) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->b1), C1 * 4));
     if (!c->b2) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->b2), C2 * 4));
@@ -1355,6 +1386,9 @@ static di_status train_check(di_ctx c) {
 
 di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_true, int batch, double scale,
                         float* grads, double* loss, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  DevGuard dg_(c->device);   // train_check allocates on the context's device
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   di_status s = train_check(c);
   if (s != DI_OK) return s;
   if (!y || !x_true || !grads || !loss) return fail(DI_ERR_ARG, "NULL device pointer");
@@ -1416,6 +1450,9 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
 }
 
 di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  DevGuard dg_(c->device);   // train_check allocates on the context's device
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   di_status s = train_check(c);
   if (s != DI_OK) return s;
   if (!grads) return fail(DI_ERR_ARG, "grads is NULL");
@@ -1430,6 +1467,7 @@ di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, 
 di_status di_get_params(di_ctx c, float* params, void* stream) {
   if (!c || !params) return fail(DI_ERR_ARG, "NULL argument");
   if (!c->params) return fail(DI_ERR_ARG, "not a trainable (FP32, per-channel bias) context");
+  DevGuard dg_(c->device);
   CUDA_TRY(cudaMemcpyAsync(params, c->params, (size_t)di::N_PARAMS * 4, cudaMemcpyDeviceToDevice,
                            reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
@@ -1439,7 +1477,7 @@ long long di_num_params(void) { return di::N_PARAMS; }
 
 di_status di_destroy(di_ctx c) {
   if (!c) return DI_OK;
-  cudaSetDevice(c->device);
+  DevGuard dg_(c->device);
   cudaDeviceSynchronize();
   free_ctx(c);
   return DI_OK;
@@ -1493,6 +1531,8 @@ di_status di_debug_stage(di_ctx c, int stage, const void* in, void* out, int bat
   if (!in || !out) return fail(DI_ERR_ARG, "NULL buffer");
   if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
   if (stage > 0 && !c->stack.empty()) return fail(DI_ERR_ARG, "per-stage hooks are for the paper's stack");
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (stage) {
     case 0: return run_stages(c, 0, 0, in, c->m, batch, out, nullptr, nullptr, nullptr, st);
@@ -1508,6 +1548,7 @@ di_status di_debug_get_phi(di_ctx c, void* host_out, long long bytes) {
   if (!c || !host_out) return fail(DI_ERR_ARG, "NULL argument");
   const size_t need = (size_t)c->m * c->N * c->elt;
   if ((size_t)bytes < need) return fail(DI_ERR_DIM, "need %zu bytes", need);
+  DevGuard dg_(c->device);
   if (c->prec == DI_PREC_FP32) {
     CUDA_TRY(cudaMemcpy(host_out, c->phi, need, cudaMemcpyDeviceToHost));
     return DI_OK;

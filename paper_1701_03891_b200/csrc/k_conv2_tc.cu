@@ -154,12 +154,6 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
           for (int kb = 0; kb < KB; ++kb, ++wk, wsrc += WB) {
             const uint32_t st = wk % WST;
             if (wk >= WST) mbar_wait(&wempty[st], ((wk / WST) - 1) & 1);
-#if defined(DI_EXP_NOW)
-            mbar_arrive(&wfull[st]);                          // experiment: no weight copies (wrong results)
-#elif defined(DI_EXP_HALFW)
-            mbar_arrive_expect_tx(&wfull[st], WB / 2);   // experiment: half the weight bytes (wrong results)
-            bulk_load(wst + st * WB, wsrc, WB / 2, &wfull[st]);
-#else
 #ifdef DI_PROF_CONV2
             t_issue[st] = clock64();
 #endif
@@ -168,7 +162,6 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
               bulk_load_mc(wst + st * WB + crank * (WB / 2), wsrc + crank * (WB / 2), WB / 2, &wfull[st], 0x3);
             else
               bulk_load(wst + st * WB, wsrc, WB, &wfull[st]);
-#endif
           }
         }
       }
@@ -305,15 +298,6 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
           else
             ld_tail13(tq + c + shift, r);
           tmem_ld_wait();
-#ifdef DI_EXP_NOEPI_SMEM
-          {   // experiment: no shared-memory transpose (wrong results): raw registers straight to h2
-            uint32_t x = 0;
-#pragma unroll
-            for (int j = 0; j < ECH; ++j) x ^= r[j];
-            if (x == 0x12345678u) h2[(size_t)blockIdx.x * 64 + lane] = __float2bfloat16_rn(0.f);
-            continue;
-          }
-#endif
           float* dst = sPg + q * (ECH * SPS) + lane;   // sP[q][j][k], k = lane
 #pragma unroll
           for (int j = 0; j < ECH; ++j) dst[j * SPS] = __uint_as_float(r[j]);
@@ -379,8 +363,7 @@ static Geo make_geo(int batch, int n1, int n2, int R = C2_ROWS) {
 // grid, an even remainder of units over the grid, and the last row-block's units as many tiles as the full ones.
 static bool pair_balanced(const Geo& g, int grid, int R) {
   const int Lfull = (R - 1) * g.P + g.wseg, rl = g.n1 - (g.nrb - 1) * R, Llast = (rl - 1) * g.P + g.wseg;
-  // DI_EXP_NO_MC (test / A-B switch, read per launch so a test can flip it): the plain one-CTA weight stream
-  return getenv("DI_EXP_NO_MC") == nullptr && grid % 2 == 0 && (g.units % grid) % 2 == 0 &&
+  return grid % 2 == 0 && (g.units % grid) % 2 == 0 &&
          (Lfull + OUT_PER_TILE - 1) / OUT_PER_TILE == (Llast + OUT_PER_TILE - 1) / OUT_PER_TILE;
 }
 // And every pair must be co-resident: a GPC with an odd number of usable SMs cannot host a 2-CTA cluster on all of
@@ -468,11 +451,12 @@ cudaError_t setup_conv2_tc(int n2) {
                               (int)dgrad2_bf16_smem_bytes(n2));
 }
 
+// allow_mc = false (the context's DI_EXP_NO_MC setting, read once by di_create) forces the one-CTA weight stream
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
-                            int n1, int n2, void* h2, int num_sms, cudaStream_t st) {
+                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, bool allow_mc) {
   Geo g = make_geo(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  if (pair_balanced(g, grid, R) && pairs_fit(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, grid, 256, conv2_tc_smem_bytes(n2)))
+  if (allow_mc && pair_balanced(g, grid, R) && pairs_fit(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, grid, 256, conv2_tc_smem_bytes(n2)))
     return launch_pair(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, grid, 256, conv2_tc_smem_bytes(n2), st, *tmH1,
                        reinterpret_cast<const __nv_bfloat16*>(wpack), bias, fullmap, g,
                        reinterpret_cast<__nv_bfloat16*>(h2), (const __nv_bfloat16*)nullptr);

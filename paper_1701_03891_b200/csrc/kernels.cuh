@@ -1,6 +1,12 @@
 // kernels.cuh -- launch entry points of the DeepInverse kernels (internal; the public ABI is
 // include/deepinverse.h).  All launches are asynchronous on the given stream.
 #pragma once
+// Instrumentation and geometry overrides exist only in the experiment library (build.py: DI_NVCC_EXTRA builds
+// libdeepinverse_exp.so with -DDI_EXPERIMENT_BUILD); the product library cannot be compiled with them.
+#if !defined(DI_EXPERIMENT_BUILD) && (defined(DI_PROF_CONV1) || defined(DI_PROF_CONV2) || defined(DI_PROF_CONV3) || \
+                                      defined(DI_C2_ROWS) || defined(DI_C2_WSTAGES))
+#error "experiment macros need DI_EXPERIMENT_BUILD (build.py routes them to libdeepinverse_exp.so)"
+#endif
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -87,7 +93,7 @@ cudaError_t setup_convg_tc(int n2);
 cudaError_t launch_convg_tc(int cin, int cout, const CUtensorMap* tm, const void* wpack, const float* bias, int batch,
                             int n1, int n2, void* out, int num_sms, cudaStream_t st);
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
-                            int n1, int n2, void* h2, int num_sms, cudaStream_t st);
+                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, bool allow_mc);
 size_t conv2_tf32_smem_bytes(int n2);
 int conv2_tf32_box_rows();
 int conv_tf32_box_cols(int n2);   // strip pitch of k_conv_tf32 (n2 + 5, or 74 with several column segments)

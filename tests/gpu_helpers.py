@@ -51,10 +51,29 @@ def run(case: Case, ctx, rows=None) -> np.ndarray:
     return out.cpu().numpy()
 
 
+# Element-wise bound on the whole path (on top of the per-image rel-L2 of north_star): max |gpu - ref| over the pixels
+# of an image, relative to max |ref| of that image.  A single wrong output pixel (|ref_p| ~ rms ~ max/3) fails it at
+# every image size, where rel-L2 dilutes it by 1/sqrt(N).  Calibrated on the green B200 runs: the
+# observed maxima are ~5x below these values.
+TOL_PIX = {"f32": 1e-5, "tf32": 2e-2, "bf16": 2e-2}
+
+
 def compare(gpu, ref, x, precision):
-    """Per image rel-L2 and |dPSNR| (PAPER.md:165 PSNR, peak = max of ground truth)."""
+    """Per image rel-L2 and |dPSNR| (PAPER.md:165 PSNR, peak = max of ground truth); asserts the element-wise bound
+    TOL_PIX.  Returns (max rel-L2, max |dPSNR|, mean dPSNR)."""
+    import json
+    import os
     rel = [oracle.rel_l2(g, r) for g, r in zip(gpu, ref)]
+    pix = [float(np.max(np.abs(np.asarray(g, np.float64) - r)) / max(float(np.max(np.abs(r))), 1e-30))
+           for g, r in zip(gpu, ref)]
     dps = [abs(oracle.psnr(g, t) - oracle.psnr(r, t)) for g, r, t in zip(gpu, ref, x)]
+    if os.environ.get("DI_PARITY_LOG"):
+        with open(os.environ["DI_PARITY_LOG"], "a") as f:
+            f.write(json.dumps({"test": os.environ.get("PYTEST_CURRENT_TEST", "?"), "precision": precision,
+                                "rel_l2": max(rel), "pix": max(pix), "dpsnr": max(dps)}) + "\n")
+    worst = int(np.argmax(pix))
+    assert pix[worst] <= TOL_PIX[precision], (f"image {worst}: max |gpu - ref| = {pix[worst]:.3g} x max|ref| > "
+                                              f"{TOL_PIX[precision]}")
     return max(rel), max(dps), float(np.mean([oracle.psnr(g, t) for g, t in zip(gpu, x)]) -
                                      np.mean([oracle.psnr(r, t) for r, t in zip(ref, x)]))
 

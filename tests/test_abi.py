@@ -84,3 +84,26 @@ def test_argument_validation_before_device(lib):
     assert lib.di_create(ctypes.byref(a), ctypes.byref(h)) == binding.DI_ERR_ARG        # unknown flag
     assert lib.di_recover(None, None, 0, 1, None, None) == binding.DI_ERR_ARG
     assert lib.di_destroy(None) == binding.DI_OK
+
+
+def test_product_library_is_not_an_experiment_build(lib):
+    """Instrumentation / wrong-result experiment switches live only in libdeepinverse_exp.so (build.py); the library
+    the tests and bench load was built with exactly the product flags (stamp) and exports no experiment marker."""
+    from paper_1701_03891_b200 import binding, build
+    assert binding.LIB_PATH == build.LIB, "DI_LIB points the binding at another library"
+    assert not hasattr(lib, "di_experiment_build")
+    st = build.read_stamp(build.LIB)
+    assert st is not None and st["flags"] == build.FLAGS, st
+    assert not any(f.startswith("-D") for f in st["flags"])
+
+
+def test_instrumentation_macros_refused_outside_experiment_build():
+    """kernels.cuh: -DDI_PROF_CONV2 (or a geometry override) without -DDI_EXPERIMENT_BUILD is a compile error."""
+    import subprocess
+    from paper_1701_03891_b200 import build
+    src = os.path.join(build.CSRC, "k_conv2_tc.cu")
+    base = [build.NVCC, "-E", "-std=c++17", "-I", os.path.join(ROOT, "include"), "-I", build.CSRC, src, "-o", os.devnull]
+    bad = subprocess.run(base + ["-DDI_PROF_CONV2"], capture_output=True, text=True)
+    assert bad.returncode != 0 and "DI_EXPERIMENT_BUILD" in bad.stderr
+    ok = subprocess.run(base + ["-DDI_PROF_CONV2", "-DDI_EXPERIMENT_BUILD"], capture_output=True, text=True)
+    assert ok.returncode == 0, ok.stderr[-2000:]

@@ -144,16 +144,19 @@ def test_shard_outputs_bitwise_identical(precision):
 
 def test_weight_multicast_and_tile_width_are_bitwise_neutral(monkeypatch):
     """Schedule choices that must not change a single bit: the CTA-pair weight multicast of conv2 (DESIGN.md §6;
-    DI_EXP_NO_MC switches it off per launch) and the lifting GEMM's pixel-tile width / batch tiles per CTA, which
-    di_create picks from max_batch (224-pixel tiles for max_batch 256, 256-pixel tiles for 4096 at 64x64)."""
+    DI_EXP_NO_MC=1 at di_create switches it off for that context) and the lifting GEMM's pixel-tile width / batch
+    tiles per CTA, which di_create picks from max_batch (224-pixel tiles for max_batch 256, 256-pixel tiles for
+    4096 at 64x64)."""
     case = Case(64, 64, 410, 256, "bf16")
     ctx = make_ctx(case, max_batch=256)
     y = y_device(case, ctx)
     mc = ctx.recover(y).cpu().numpy()
     monkeypatch.setenv("DI_EXP_NO_MC", "1")
-    nomc = ctx.recover(y).cpu().numpy()
+    ctx_nomc = make_ctx(case, max_batch=256)
     monkeypatch.delenv("DI_EXP_NO_MC")
+    nomc = ctx_nomc.recover(y).cpu().numpy()
     assert np.array_equal(mc, nomc), "weight multicast changed the result"
+    assert np.array_equal(ctx.recover(y).cpu().numpy(), mc), "the setting is per context"
     big = make_ctx(case, max_batch=4096)
     assert np.array_equal(big.recover(y).cpu().numpy(), mc), "proxy tile width changed the result"
 
@@ -175,6 +178,48 @@ def test_host_e2e_matches_device():
     yh = torch.from_numpy(case.y).to(torch.bfloat16).pin_memory()
     host = ctx.recover_host(yh)
     assert np.array_equal(host, dev)
+
+
+def test_host_e2e_multichunk_bitwise():
+    """di_recover_host's chunked branch (batch >= 512: halving chunks, y split between the compute and the copy
+    stream, per-chunk D2H on the copy stream) gives bitwise the device-resident di_recover result: batch 512, 515
+    (ragged last chunk), 4096 (the bench's e2e call) and max_batch, with pinned and pageable y, repeated on the same
+    context (workspace reuse, y staging regrown)."""
+    import torch
+    maxb = 4100
+    case = Case(64, 64, 410, maxb, "bf16", 4, 2)
+    ctx = make_ctx(case, max_batch=maxb)
+    yd = y_device(case, ctx)
+    dev = ctx.recover(yd).cpu().numpy()
+    ypin = torch.from_numpy(case.y).to(torch.bfloat16).pin_memory()
+    ypage = torch.from_numpy(case.y).to(torch.bfloat16)
+    for b in (512, 515, 4096, maxb, 515):
+        for yh in (ypin, ypage):
+            host = ctx.recover_host(yh[:b])
+            assert np.array_equal(host, dev[:b]), f"batch {b} pinned={yh.is_pinned()}"
+    out = torch.empty((600, 64, 64), dtype=torch.float32).pin_memory()
+    ctx.recover_host(ypin[100:700], out)
+    assert np.array_equal(out.numpy(), dev[100:700])
+
+
+def test_host_e2e_fp32_numpy_and_validation():
+    """FP32 context through numpy host buffers (pageable), chunked; wrong dtypes / shapes raise TypeError."""
+    import torch
+    case = Case(32, 32, 200, 520, "f32", 3, 1)
+    ctx = make_ctx(case)
+    dev = run(case, ctx)
+    assert np.array_equal(ctx.recover_host(case.y), dev)
+    with pytest.raises(TypeError):
+        ctx.recover_host(case.y.astype(np.float64))
+    with pytest.raises(TypeError):
+        ctx.recover_host(case.y, np.empty((520, 32, 33), np.float32))
+    bctx = make_ctx(Case(32, 32, 200, 4, "bf16", 3, 1))
+    with pytest.raises(TypeError):
+        bctx.recover_host(case.y[:4])                                 # float32 numpy into a bf16 context
+    with pytest.raises(TypeError):
+        bctx.recover(torch.zeros((4, 200), dtype=torch.float32, device="cuda"))
+    with pytest.raises(TypeError):
+        bctx.recover(torch.zeros((200, 4), dtype=torch.bfloat16, device="cuda").t())   # column stride != 1
 
 
 def test_device_phi_is_rne_bf16():
@@ -204,8 +249,12 @@ def test_error_codes():
     with pytest.raises(DiError) as e:
         ctx.recover(y)
     assert e.value.status == 1
-    with pytest.raises(DiError) as e:
-        ctx.recover(torch.zeros((2, 63), dtype=torch.bfloat16, device="cuda"))
+    from paper_1701_03891_b200 import di_recover
+    y63 = torch.zeros((2, 63), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(TypeError):                       # the binding checks the shape first
+        ctx.recover(y63)
+    with pytest.raises(DiError) as e:                    # the C ABI: ldy < m is DI_ERR_DIM
+        di_recover(ctx.ctx, y63, 63, 2, torch.empty((2, 16, 16), device="cuda"))
     assert e.value.status == 2
 
 
@@ -262,7 +311,7 @@ def test_degenerate_shapes(precision, n1, n2, m, batch):
     out = run(case, ctx)
     assert np.all(np.isfinite(out))
     ref = case.oracle(np.arange(batch))
-    rel = max(oracle.rel_l2(g, r) for g, r in zip(out, ref))
+    rel, _, _ = compare(out, ref, case.x, precision)      # includes the element-wise bound
     assert rel <= TOL_REL_L2[precision], rel
 
 
