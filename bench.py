@@ -82,6 +82,39 @@ def aggregate(per_rank_units: int, world: int, max_seconds: float) -> float:
     return per_rank_units * world / max_seconds
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launcher_cmd(argv: list[str], gpus: int, port: int) -> list[str]:
+    """The command `python bench.py --gpus N` re-executes itself under: torchrun, one rank per GPU, loopback
+    rendezvous (the container hostname may not resolve)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def gather_to_all(t, world: int) -> list:
+    """all_gather of one same-shape tensor per rank (NCCL on the GPU box, gloo in the CPU tests) -- checking only,
+    outside the timed region."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return [t]
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    return parts
+
+
+def check_rows(batch: int, k: int = 32) -> list[int]:
+    """Local image indices a rank's outputs are checked on: the first and last k (all when batch <= 2k)."""
+    if batch <= 2 * k:
+        return list(range(batch))
+    return list(range(k)) + list(range(batch - k, batch))
+
+
 # ----------------------------------------------------------------------------- clocks (nvidia-smi)
 _CLK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -426,17 +459,131 @@ def run_ours(args):
                        "metrics_ms_incl_d2h": sev[2].elapsed_time(sev[3]),
                        "mean_psnr_db_random_init": float(np.mean(mt[0]))}
 
+    # ---------------- output check (outside the timed region): gather x_hat of every rank to rank 0 (NCCL
+    # all_gather -- the only use of a collective on outputs); rank 0 re-recovers the first and
+    # last 32 images of every rank's block itself (bitwise: per-image results do not depend on the rank, the batch
+    # or the CTA a unit lands on) and checks 2 + 2 of them per rank against the fp64 oracle
+    xhat_last = xhat.clone()
+    ctx.recover(y_dev, xhat)                               # the timed loop's output, once more, for the gather
+    parts = gather_to_all(xhat, world)
+    ok = True
+    if rank == 0:
+        line["gather_check"] = output_check(ctx, c, prec, B, world, parts, dev, args.no_oracle_check)
+        ok = line["gather_check"]["pass"] and bool(torch.equal(xhat_last, xhat))
+        line["gather_check"]["repeat_bitwise"] = bool(torch.equal(xhat_last, xhat))
+    del parts
+
     # ---------------- CPU baseline (oracle as it stands), rank 0 at N=1 only
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         line["cpu_baseline"] = oracle_sample(c, prec, args.cpu_budget, threads)
+        line["cpu_baseline"]["cpu_model"] = cpu_model()
+        if not args.no_cpu_configs:
+            line["cpu_baseline"]["single_thread_s_per_image"] = oracle_single_thread_per_config()
     if rank == 0:
         print(json.dumps(line), flush=True)
+        if not ok:
+            print("output check FAILED: " + json.dumps(line["gather_check"]), file=sys.stderr)
     ctx.close()
     if world > 1:
         import torch.distributed as dist
+        barrier(dev)
         dist.destroy_process_group()
-    return 0
+    return 0 if ok else 1
+
+
+def output_check(ctx, c, prec, B, world, parts, dev, no_oracle=False) -> dict:
+    """Rank 0: bitwise equality of every rank's gathered x_hat with rank 0's own recovery of the same global images
+    (first and last 32 of each block), and the oracle's rel-L2 / element-wise error on 2 + 2 of them per rank."""
+    import torch
+    rows = check_rows(B)
+    orows = [0, 1, B - 2, B - 1] if B >= 4 else list(range(B))
+    bitwise, rel_max, pix_max, n_or = True, 0.0, 0.0, 0
+    tol = {"bf16": 2e-2, "tf32": 2e-2, "f32": 1e-5}[prec]
+    for r in range(world):
+        lo = r * B
+        phi, x, y, params = make_inputs_rows(c, prec, [lo + i for i in rows])
+        yd = torch.from_numpy(y).to(device=dev, dtype=ctx.storage_dtype)
+        mine = ctx.recover(yd).cpu().numpy()
+        got = parts[r][rows].cpu().numpy()
+        bitwise &= bool(np.array_equal(mine, got))
+        if not no_oracle:
+            import oracle
+            sel = [rows.index(i) for i in orows]
+            ref = oracle.forward(y[sel], phi, params, c.n, c.n)
+            for g, rf in zip(got[sel], ref):
+                rel_max = max(rel_max, oracle.rel_l2(g, rf))
+                pix_max = max(pix_max, float(np.max(np.abs(g - rf)) / max(float(np.max(np.abs(rf))), 1e-30)))
+                n_or += 1
+    ok = bitwise and (no_oracle or (rel_max <= tol and pix_max <= tol))
+    return {"ranks": world, "bitwise_images_per_rank": len(rows), "bitwise_vs_rank0_recovery": bitwise,
+            "oracle_images": n_or, "oracle_max_rel_l2": rel_max, "oracle_max_pixel_err_over_max": pix_max,
+            "tol": tol, "pass": ok}
+
+
+def make_inputs_rows(c, prec: str, idx: list[int]):
+    """Seeded inputs for an arbitrary list of global image indices (contiguous runs generated together)."""
+    import synth
+    st = "bf16" if prec == "bf16" else "f32"
+    phi = synth.make_phi(c.m, c.N, st)
+    xs, run = [], [idx[0]]
+    for i in idx[1:] + [None]:
+        if i is not None and i == run[-1] + 1:
+            run.append(i)
+            continue
+        xs.append(synth.make_images(c.n, run[0], len(run), c.n_blobs, c.n_rects, c.texture_var))
+        if i is not None:
+            run = [i]
+    x = np.concatenate(xs)
+    y = synth.measure(phi, x, st)
+    return phi, x, y, synth.make_params().rounded(st)
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "?"
+
+
+def oracle_single_thread_per_config() -> dict:
+    """the oracle's single-thread time per image on each config (Tiny 4, Paper 16, Low-rate 16,
+    Larger 4 images; Stress 1 image, extrapolated: its lifting step is timed on the first 1024 of the 16384 rows of
+    Phi -- the proxy loop is linear in M -- and the convolutions on the whole image).  The five timings run
+    concurrently, one host thread each (ctypes releases the GIL), so the whole takes about the longest one."""
+    from concurrent.futures import ThreadPoolExecutor
+    import oracle
+    import synth
+
+    def one(name, count):
+        c = synth.CONFIGS[name]
+        st = "bf16" if c.precisions[-1] == "bf16" else "f32"
+        if name != "stress":
+            phi, x, y, params = make_inputs_rows(c, "bf16" if st == "bf16" else "f32", list(range(count)))
+            t0 = time.perf_counter()
+            oracle.forward(y, phi, params, c.n, c.n, threads=1)
+            return name, {"s_per_image": (time.perf_counter() - t0) / count, "images": count}
+        mp = 1024
+        phi = synth.make_phi(c.m, c.N, st, rows=(0, mp))
+        x = synth.make_images(c.n, 0, 1, c.n_blobs, c.n_rects, c.texture_var)
+        y = synth.measure(phi, x, st)
+        params = synth.make_params().rounded(st)
+        t0 = time.perf_counter()
+        oracle.proxy(phi, y)
+        t_rows = time.perf_counter() - t0
+        small = phi[:64]
+        t0 = time.perf_counter()
+        oracle.forward(y[:, :64], small, params, c.n, c.n, threads=1)
+        t_fwd = time.perf_counter() - t0
+        return name, {"s_per_image": t_fwd + t_rows * (c.m - 64) / mp, "images": 1,
+                      "extrapolated": f"proxy timed on {mp} of {c.m} rows (linear in M)"}
+
+    jobs = [("tiny", 4), ("paper", 16), ("lowrate", 16), ("larger", 4), ("stress", 1)]
+    with ThreadPoolExecutor(len(jobs)) as ex:
+        return dict(ex.map(lambda j: one(*j), jobs))
 
 
 def main(argv=None):
@@ -449,9 +596,21 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=0, help="override the per-GPU batch (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle time for cpu_baseline")
+    ap.add_argument("--no-cpu-configs", action="store_true", help="skip the per-config single-thread oracle times")
+    ap.add_argument("--no-oracle-check", action="store_true", help="output check: bitwise part only")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
+    if args.gpus < 1:
+        print("--gpus must be >= 1", file=sys.stderr)
+        return 2
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N`: start N ranks (one process per GPU) under torchrun; rank 0 prints the line
+        return subprocess.call(launcher_cmd(sys.argv[1:] if argv is None else list(argv), args.gpus, free_port()))
+    _, world, _ = dist_env()
+    if world != args.gpus:
+        print(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -184,3 +184,89 @@ def test_row_and_batch_ranges():
         batch_range(6, 4, 0)
     with pytest.raises(ValueError):
         row_range(2, 3, 0)
+
+
+class _OracleCtx:
+    """Stands in for DeepInverse in the CPU test of bench.output_check: recover() runs the oracle (test-only)."""
+    storage_dtype = None
+
+    def __init__(self, c, corrupt=False):
+        import torch
+        self.c, self.corrupt = c, corrupt
+        self.storage_dtype = torch.float32
+
+    def recover(self, yd):
+        import torch
+        import oracle
+        phi, _, _, params = bench.make_inputs(self.c, "f32", 0, 1)
+        out = oracle.forward(yd.numpy(), phi, params, self.c.n, self.c.n).astype(np.float32)
+        return torch.from_numpy(out)
+
+
+def _gather_worker(rank, world, port, corrupt, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c = synth.CONFIGS["tiny"]
+        B = c.batch
+        lo, hi = bench.shard(rank, B)
+        _, _, y, _ = bench.make_inputs(c, "f32", lo, B)
+        xhat = _OracleCtx(c).recover(torch.from_numpy(y))
+        if corrupt and rank == 1:
+            xhat[2, 7, 9] += 0.5                         # one wrong pixel on rank 1
+        parts = bench.gather_to_all(xhat, world)
+        if rank == 0:
+            q.put(bench.output_check(_OracleCtx(c), c, "f32", B, world, parts, "cpu"))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_gather(corrupt):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, corrupt, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    res = q.get(timeout=180)
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    return res
+
+
+def test_two_rank_output_gather_check():
+    """bench.py's output check over 2 gloo ranks: x_hat gathered to rank 0 equals rank 0's own recovery of the same
+    global images bitwise and the oracle within tolerance; one corrupted pixel on rank 1 fails both."""
+    good = _run_gather(False)
+    assert good["pass"] and good["bitwise_vs_rank0_recovery"] and good["ranks"] == 2 and good["oracle_images"] == 8
+    bad = _run_gather(True)
+    assert not bad["pass"] and not bad["bitwise_vs_rank0_recovery"]
+    assert bad["oracle_max_pixel_err_over_max"] > bad["tol"]
+
+
+def test_bench_launcher_and_world_check():
+    """`python bench.py --gpus N` without torchrun re-executes under torchrun with N ranks on a loopback rendezvous;
+    under torchrun a WORLD_SIZE different from --gpus is refused."""
+    cmd = bench.launcher_cmd(["--gpus", "4", "--steps", "3"], 4, 29555)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"] and cmd[-5].endswith("bench.py")
+    old = dict(os.environ)
+    try:
+        os.environ.update(WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+        assert bench.main(["--gpus", "4"]) == 2
+        assert bench.main(["--gpus", "0"]) == 2
+    finally:
+        os.environ.clear()
+        os.environ.update(old)
+
+
+def test_make_inputs_rows_matches_contiguous_generation():
+    c = synth.CONFIGS["tiny"]
+    _, x, y, _ = bench.make_inputs(c, "bf16", 0, 8)
+    _, x2, y2, _ = bench.make_inputs_rows(c, "bf16", [0, 1, 5, 6, 7])
+    assert np.array_equal(x2, x[[0, 1, 5, 6, 7]]) and np.array_equal(y2, y[[0, 1, 5, 6, 7]])
+    assert bench.check_rows(4096)[:2] == [0, 1] and bench.check_rows(4096)[-1] == 4095 and len(bench.check_rows(4096)) == 64
