@@ -429,6 +429,15 @@ def run_ours(args):
         ceil = conv2_useful_mac_ceiling(c.n, c.n)
         roof["design_ceiling"] = ceil
         roof["frac_of_design_ceiling"] = roof["frac"] / ceil if roof["frac"] else None
+        # like-for-like with the clock the kernel ran at: the dense bf16 rate of 148 SMs x 8192 FLOP/clk at the SM
+        # clock sampled during the timed region (MEASURED_PEAKS' burst figure was taken at a lower, power-capped
+        # clock, so `frac` alone flatters the kernel)
+        if clocks.get("sm_mhz"):
+            nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+            clk_peak = nsm * 8192 * clocks["sm_mhz"] * 1e6 / 1e12
+            roof["peak_at_sm_clock"] = clk_peak
+            roof["frac_at_sm_clock"] = achieved / clk_peak
+            roof["frac_of_design_ceiling_at_sm_clock"] = achieved / clk_peak / ceil
 
     per_step = ms / args.steps
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -25,12 +25,14 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 # instrumentation macros without it).  The product library is never built with extra flags; a stamp file next to it
 # records the exact flags and nvcc version, and any difference forces a rebuild.
 EXTRA = os.environ.get("DI_NVCC_EXTRA", "").split()
-EXP_LIB = os.path.join(HERE, "libdeepinverse_exp.so")
+_EXP_NAME = os.environ.get("DI_EXP_NAME", "")   # several experiment libraries side by side (A/B runs)
+EXP_LIB = os.path.join(HERE, f"libdeepinverse_exp{'_' + _EXP_NAME if _EXP_NAME else ''}.so")
 
 
 def _target(extra: list[str]) -> tuple[str, str, list[str]]:
     if extra:
-        return EXP_LIB, os.path.join(HERE, "build_exp"), FLAGS + ["-DDI_EXPERIMENT_BUILD"] + extra
+        return (EXP_LIB, os.path.join(HERE, "build_exp" + ("_" + _EXP_NAME if _EXP_NAME else "")),
+                FLAGS + ["-DDI_EXPERIMENT_BUILD"] + extra)
     return LIB, os.path.join(HERE, "build"), list(FLAGS)
 
 

@@ -144,6 +144,7 @@ struct di_ctx_s {
   cudaEvent_t cev[17] = {};                      // di_recover_host: chunk-done events (+ the y-copy event)
   long long ws_bytes = 0;
   CUtensorMap tmPt{}, tmH1{}, tmH2{}, tmX{};
+  CUtensorMap tmH1s{};          // BF16, n2 % 64 == 0: conv1's TMA store map over h1 (encode_h1_store)
   bool has_tmX = false;
   int last_launches = 0;
   bool profiling = false;
@@ -197,6 +198,22 @@ di_status encode_h1(CUtensorMap* map, const void* h1, int batch, int n1, int n2)
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h1) failed: %d", (int)r);
+  return DI_OK;
+}
+
+// conv1's output path (k_conv1_tc): h1 [batch][n1][n2][64] bf16, box = 16 channels (32 B) x 64 columns x 2 rows,
+// SWIZZLE_32B -- one epilogue warp's 128 positions x 16 channels, stored by one TMA tensor store
+di_status encode_h1_store(CUtensorMap* map, const void* h1, int batch, int n1, int n2) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {64, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {64 * 2, (cuuint64_t)n2 * 64 * 2, (cuuint64_t)n1 * n2 * 64 * 2};
+  cuuint32_t box[4] = {16, 64, 2, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(h1), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h1 store) failed: %d", (int)r);
   return DI_OK;
 }
 
@@ -390,16 +407,14 @@ std::vector<float> conv2_tf32_pack(const std::vector<float>& wx2) {
 }
 
 // conv1 tensor-core blocks: block u (2 KB) = 64 filter rows x 16 column taps (v >= 11 zero), bf16, SWIZZLE_32B
-// image (16-B chunk h of row m at m*32 + ((h ^ ((m >> 2) & 1)) << 4)).  Row m = 16G + j holds filter
-// 16G + 2j (j < 8) or 16G + 2(j - 8) + 1 (j >= 8): the epilogue's 16x256b TMEM load then hands each thread the two
-// adjacent channels of a bf16x2 store (k_conv13_tc.cu).
+// image (16-B chunk h of row m at m*32 + ((h ^ ((m >> 2) & 1)) << 4)).  Row m holds filter m (natural order: the
+// epilogue's stmatrix transposes 8-channel blocks, k_conv13_tc.cu).
 std::vector<uint16_t> conv1_tc_pack(const std::vector<float>& wx1) {
   std::vector<uint16_t> out(11 * 2048 / 2, 0);
   uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
   for (int u = 0; u < K; ++u)
     for (int m = 0; m < 64; ++m) {
-      const int grp = m / 16, j = m % 16;
-      const int f = 16 * grp + (j < 8 ? 2 * j : 2 * (j - 8) + 1);
+      const int f = m;
       for (int v = 0; v < 16; ++v) {
         const uint16_t h = v < K ? f2bf(wx1[((size_t)f * K + u) * K + v]) : 0;
         const size_t off = (size_t)u * 2048 + m * 32 + ((((size_t)v / 8) ^ ((m >> 2) & 1)) << 4) + (v % 8) * 2;
@@ -614,7 +629,7 @@ di_status run_stack(di_ctx c, int batch, void* xt, float* xhat, cudaStream_t st,
             tmp = &tm;
           }
         }
-        CUDA_TRY(di::launch_conv1_tc(tmp, xt, l.wp, l.b, 0, outb, batch, c->n1, c->n2, c->num_sms, st));
+        CUDA_TRY(di::launch_conv1_tc(tmp, nullptr, xt, l.wp, l.b, 0, outb, batch, c->n1, c->n2, c->num_sms, st));
       } else if (i == L - 1) {
         CUDA_TRY(di::launch_conv3_r4(&l.tm, l.wp, l.b, 0, relu_last, xhat, batch, c->n1, c->n2, c->num_sms, st));
       } else {
@@ -693,7 +708,18 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
           tmp = &tm;
         }
       }
-      CUDA_TRY(di::launch_conv1_tc(tmp, xt, c->wp1, c->b1, fm, h1, batch, c->n1, c->n2, c->num_sms, st));
+      // h1 leaves by TMA tensor stores when the image rows are whole 64-column segments (k_conv13_tc.cu)
+      CUtensorMap ts;
+      const CUtensorMap* tsp = nullptr;
+      if (c->n2 % 64 == 0) {
+        tsp = &c->tmH1s;
+        if (h1 != c->h1) {
+          di_status s = encode_h1_store(&ts, h1, batch, c->n1, c->n2);
+          if (s != DI_OK) return s;
+          tsp = &ts;
+        }
+      }
+      CUDA_TRY(di::launch_conv1_tc(tmp, tsp, xt, c->wp1, c->b1, fm, h1, batch, c->n1, c->n2, c->num_sms, st));
     }
     else
       CUDA_TRY(di::launch_conv1_simt(xt, bf16, c->wx1, c->b1, fm, h1, batch, c->n1, c->n2, st));
@@ -750,13 +776,70 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
   return DI_OK;
 }
 
+#ifdef DI_DEBUG
+}  // namespace
+namespace di {
+cudaError_t di_debug_bind_k_proxy(unsigned int*);
+cudaError_t di_debug_bind_k_conv13_tc(unsigned int*);
+cudaError_t di_debug_bind_k_conv2_tc(unsigned int*);
+cudaError_t di_debug_bind_k_conv3_r4(unsigned int*);
+cudaError_t di_debug_bind_k_conv2_tf32(unsigned int*);
+cudaError_t di_debug_bind_k_wgrad13_tc(unsigned int*);
+cudaError_t di_debug_bind_k_wgrad2_tc(unsigned int*);
+}  // namespace di
+namespace {
+// one host-mapped record per process, bound into every kernel translation unit of the current device
+volatile unsigned int* debug_record() {
+  static unsigned int* host = nullptr;
+  if (!host) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&host), 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+      return nullptr;
+    std::memset(host, 0, 64);
+  }
+  return host;
+}
+di_status debug_bind() {
+  volatile unsigned int* h = debug_record();
+  if (!h) return fail(DI_ERR_CUDA, "debug record allocation failed");
+  unsigned int* d = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), const_cast<unsigned int*>(h), 0));
+  CUDA_TRY(di::di_debug_bind_k_proxy(d));
+  CUDA_TRY(di::di_debug_bind_k_conv13_tc(d));
+  CUDA_TRY(di::di_debug_bind_k_conv2_tc(d));
+  CUDA_TRY(di::di_debug_bind_k_conv3_r4(d));
+  CUDA_TRY(di::di_debug_bind_k_conv2_tf32(d));
+  CUDA_TRY(di::di_debug_bind_k_wgrad13_tc(d));
+  CUDA_TRY(di::di_debug_bind_k_wgrad2_tc(d));
+  return DI_OK;
+}
+#endif
+
 }  // namespace
 
 extern "C" {
 
 #ifdef DI_EXPERIMENT_BUILD
 // present only in libdeepinverse_exp.so (tests/test_abi.py asserts the product library does not export it)
-__attribute__((visibility("default"))) const char di_experiment_build[] = "experiment build";
+__attribute__((visibility("default"))) extern const char di_experiment_build[] = "experiment build";
+#endif
+
+#ifdef DI_DEBUG
+// Debug library only (sm100.cuh DI_DEBUG): the host-mapped failure record of bounded mbarrier waits and device
+// asserts.  Returns the record's code (0 = no failure) and formats it into buf.
+static const char* const kTuNames[] = {"?", "k_proxy", "k_conv13_tc", "k_conv2_tc", "k_conv3_r4", "k_conv2_tf32",
+                                       "k_sense", "k_train", "k_wgrad13_tc", "k_wgrad2_tc", "k_conv_simt"};
+int di_debug_report(char* buf, int n) {
+  volatile unsigned int* r = debug_record();
+  if (!r) return -1;
+  const unsigned int code = r[0];
+  if (buf && n > 0) {
+    const unsigned int tu = code >> 8, kind = code & 0xff;
+    snprintf(buf, n, "%s: %s in %s, block %u thread %u (a=0x%x b=%u)", code ? "FAILED" : "ok",
+             kind == 1 ? "mbarrier wait timed out" : kind == 2 ? "device assert" : "-",
+             tu < sizeof(kTuNames) / sizeof(kTuNames[0]) ? kTuNames[tu] : "?", r[1], r[2], r[3], r[4]);
+  }
+  return (int)code;
+}
 #endif
 
 const char* di_status_string(di_status s) {
@@ -826,6 +909,15 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   c->device = a->device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, a->device);
   c->conv2_mc = getenv("DI_EXP_NO_MC") == nullptr;   // read once per context, never on the launch path
+#ifdef DI_DEBUG
+  {
+    di_status sd = debug_bind();
+    if (sd != DI_OK) {
+      delete c;
+      return sd;
+    }
+  }
+#endif
   c->m = a->m, c->n1 = a->n1, c->n2 = a->n2, c->N = (int)N, c->max_batch = a->max_batch;
   c->prec = a->precision, c->flags = a->flags;
   c->elt = (a->precision == DI_PREC_BF16) ? 2 : 4;
@@ -1065,6 +1157,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       }
     } else {
       STEP(encode_h1(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
+      if (a->n2 % 64 == 0) STEP(encode_h1_store(&c->tmH1s, c->h1, a->max_batch, a->n1, a->n2));
     }
     e = di::setup_conv13_tc(a->n2);
     if (e != cudaSuccess) {

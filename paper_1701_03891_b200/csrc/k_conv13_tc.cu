@@ -31,6 +31,7 @@
 #include <cstdio>
 
 #include "kernels.cuh"
+#define DI_TU_ID 2
 #include "sm100.cuh"
 
 namespace di {
@@ -54,6 +55,9 @@ constexpr int SW1_OFF = ((STRIP_WORDS + 31) & ~31) + 16;  // word offset of the 
 constexpr int FILL_PER_THREAD = ((R1 + 10) * P1MAX + 63) / 64;   // strip elements per builder thread
 constexpr int XC_STRIDE = ((R1 + 10) * (P1MAX + 8) * 2 + 64 + 127) & ~127;   // TMA strip buffer stride (bytes)
 constexpr int W1_BYTES = 11 * 64 * 32;                   // 11 tap rows x 64 filters x 16 taps bf16
+constexpr int C1_STRIPS = 2 * XC_STRIDE > 2 * SW1_OFF * 4 ? 2 * XC_STRIDE : 2 * SW1_OFF * 4;
+constexpr int C1_STAGE_OFF = (W1_BYTES + 2 * IM_BYTES + C1_STRIPS + 1023) & ~1023;
+constexpr int C1_STAGE = 4096;                           // one warp's 128 positions x 16 channels of h1, bf16
 
 // ---------------------------------------------------------------- conv3 geometry
 constexpr int R3 = C3TC_ROWS;
@@ -68,16 +72,16 @@ constexpr int SROW = 267;                                // S row stride (floats
 // zero-padded strip (pitch P); K-block u reads the window starting at row p0 + u * W.  A tile is 256 consecutive
 // output positions, so its outputs are contiguous in NHWC h1 whenever the unit spans the full image width.
 // Epilogue: tcgen05.ld.16x256b gives thread t the TMEM lanes t/4 and t/4 + 8 of a 16-lane group at columns
-// 2(t%4), 2(t%4)+1 (tools/ladder.cu t15); the filters are permuted in the packed weights so that those two lanes are
-// the adjacent channels 2i, 2i+1 -- a bf16x2 word stores straight to h1 with no shared-memory transpose.
+// 2(t%4), 2(t%4)+1 (tools/ladder.cu t15) -- the fragment layout of stmatrix, whose .trans form writes the NHWC
+// transpose into a per-warp staging buffer that one TMA tensor store per half tile moves to h1.
 // TMAX = true (n2 % 8 == 0): the strip arrives by TMA (out-of-bounds zero fill), double-buffered across units and
 // issued one unit ahead; TMAX = false: builders gather it with plain loads (any n2).  (A TMA box whose innermost
 // start coordinate is not 16-B aligned faults on B200 -- tools/scratch/tma3d.cu -- hence the 8-column left margin.)
 template <bool TMAX>
 __global__ void __launch_bounds__(384, 1)
-    k_conv1_tc(const __grid_constant__ CUtensorMap tmX, const __nv_bfloat16* __restrict__ xt,
-               const uint8_t* __restrict__ w1pack, const float* __restrict__ bias, int fullmap, Geo13 g,
-               __nv_bfloat16* __restrict__ h1) {
+    k_conv1_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmS, int tma_store,
+               const __nv_bfloat16* __restrict__ xt, const uint8_t* __restrict__ w1pack, const float* __restrict__ bias,
+               int fullmap, Geo13 g, __nv_bfloat16* __restrict__ h1) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* wbuf = smem;                                           // 22 KB
@@ -85,6 +89,7 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* const sw0 = reinterpret_cast<uint32_t*>(smem + W1_BYTES + 2 * IM_BYTES);
   uint32_t* const sw1 = sw0 + SW1_OFF;
   uint8_t* const xc0 = smem + W1_BYTES + 2 * IM_BYTES;   // TMAX: 2 buffers x 8 shifted copies (aliases sw0/sw1)
+  uint8_t* const stage0 = smem + C1_STAGE_OFF;              // epilogue: 8 warps x 2 x 4 KB h1 staging (SWIZZLE_32B)
 
   __shared__ uint64_t wbar, im_full[2], im_empty[2], acc_full[NACC], acc_empty[NACC], xfull[2];
   __shared__ uint32_t tslot;
@@ -154,6 +159,7 @@ __global__ void __launch_bounds__(384, 1)
 #endif
           tc_fence_after();
           const uint32_t d = tmem + a * 128;
+          DI_DEVICE_ASSERT(n0 + 10 * W + N <= IM_ROWS, n0, N);   // the u = 10 window stays in the im2row buffer
           uint64_t bd = bdesc_base + (uint64_t)(((s * IM_BYTES) + n0 * 32) >> 4);
 #pragma unroll
           for (int tu = 0; tu < 11; ++tu) {
@@ -294,15 +300,22 @@ __global__ void __launch_bounds__(384, 1)
 #endif
   } else {  // -------------------------------------------------------- epilogue, warps 4..11
     // .ws M=64 D layout: quadrants {0,1} = filter rows 0..63 for tile columns [0, N/2), {2,3} for [N/2, N).
-    // Warp w reads quadrant q = w % 4, 16-lane group hh = (w - 4) / 4; in group G = 2*(q&1) + hh, thread t holds
-    // channels 16G + 2i, 16G + 2i + 1 (i = t/4; permuted weight rows) at columns 2(t%4), 2(t%4)+1 of each
-    // 8-column block.
+    // Warp w reads quadrant q = w % 4, 16-lane group hh = (w - 4) / 4 = channels 16G .. 16G + 15, G = 2(q&1) + hh
+    // (packed filter rows in natural order).  tcgen05.ld.16x256b gives thread t channels ca = 16G + t/4 and
+    // cb = ca + 8 at columns 2(t%4), 2(t%4)+1 of each 8-column block k: with bias + ReLU and bf16 rounding these are
+    // the fragments of two 8 x 8 [channel][position] matrices per block, and stmatrix.trans writes their transposes
+    // -- [position][8 channels], i.e. NHWC -- into the warp's staging buffer (32-B rows = 16 channels, SWIZZLE_32B).
+    // A full 128-position half tile (two 64-column image rows) then leaves by ONE TMA tensor store per warp
+    // (box 16 ch x 64 cols x 2 rows, out-of-range rows clipped by the TMA unit): full-sector writes and no per-lane
+    // store instructions.  Other tiles (narrow images, ragged tiles, full-map biases) copy rows out with 16-B stores.
     const int q = warp & 3, hh = (warp - 4) >> 2;
     const int i4 = lane >> 2, cpair = 2 * (lane & 3);
-    const int ch = 16 * (2 * (q & 1) + hh) + 2 * i4;          // this thread's channels ch, ch + 1
-    const float b0 = (!fullmap && bias) ? bias[ch] : 0.f, b1 = (!fullmap && bias) ? bias[ch + 1] : 0.f;
+    const int G = 2 * (q & 1) + hh;
+    const int ca = 16 * G + i4, cb = ca + 8;                  // this thread's channels
+    const float ba = (!fullmap && bias) ? bias[ca] : 0.f, bb = (!fullmap && bias) ? bias[cb] : 0.f;
     const uint32_t wmagic = (1u << 20) / (uint32_t)W + 1;
-    int ti = 0;
+    uint8_t* const stg = stage0 + (warp - 4) * 2 * C1_STAGE;
+    int ti = 0, sb = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
       const int b = u / per_img, rem = u - b * per_img;
       const int r0 = (rem / g.ncs) * g.R, c0 = (rem % g.ncs) * g.wseg;
@@ -318,54 +331,74 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const int pbase = n0 + (q >> 1) * half;
         const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32 + 16 * hh) << 16);
-        // fast path: full tile, and each 32-position chunk is contiguous in h1 (full-width unit, or a full 64-wide
-        // segment: 32 | W keeps a chunk inside one image row)
-        const bool fast = cnt == N && !fullmap && (linear || (W == 64 && c0 + 64 <= g.n2));
+        const bool tma = tma_store && N == 256 && W == 64 && !fullmap;
+        uint8_t* const buf = stg + sb * C1_STAGE;
+        if (lane == 0) bulk_wait_read<1>();   // this buffer's previous store (two half tiles ago) has read it
+        __syncwarp();
+        const uint32_t sbase = smem_u32(buf);
         for (int c = 0; c < half; c += 32) {
           uint32_t r[16];
           tmem_ld_16x256b_x4(taddr + c, r);
           tmem_ld_wait();
-          if (fast) {   // no per-element checks
-            const int p0 = pbase + c;
-            const size_t cpix = linear ? pix0 + p0 : pix0 + (size_t)(p0 >> 6) * g.n2 + (p0 & 63);
-            uint32_t* dst = reinterpret_cast<uint32_t*>(h1 + (cpix + cpair) * 64 + ch);
+          uint32_t f[8];   // f[2k] = channels ca.. of block k, f[2k + 1] = channels cb.. (positions 2(t%4), +1)
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+          for (int k = 0; k < 4; ++k) {
+            float v[4] = {__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]), __uint_as_float(r[4 * k + 2]),
+                          __uint_as_float(r[4 * k + 3])};
+            if (fullmap && bias) {
 #pragma unroll
-              for (int e = 0; e < 2; ++e)
-                dst[(8 * k + e) * 32] = pack_bf16x2(fmaxf(__uint_as_float(r[4 * k + e]) + b0, 0.f),
-                                                    fmaxf(__uint_as_float(r[4 * k + 2 + e]) + b1, 0.f));
-            continue;
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int p = pbase + c + 8 * k + cpair + e;        // output position within the unit
-              if (p >= n0 + cnt) continue;
-              size_t pix;
-              if (linear) {
-                pix = pix0 + p;
-              } else {
+              for (int e = 0; e < 2; ++e) {
+                const int p = min(pbase + c + 8 * k + cpair + e, npos - 1);
                 const int rr = (int)(((uint32_t)p * wmagic) >> 20), cc = p - rr * W;
-                if (c0 + cc >= g.n2) continue;
-                pix = pix0 + (size_t)rr * g.n2 + cc;
+                const size_t pm = ((size_t)(r0 + rr) * g.n2 + min(c0 + cc, g.n2 - 1));
+                v[e] += bias[pm * 64 + ca], v[2 + e] += bias[pm * 64 + cb];
               }
-              float v0 = __uint_as_float(r[4 * k + e]), v1 = __uint_as_float(r[4 * k + 2 + e]);
-              if (fullmap && bias) {
-                const size_t pm = pix % ((size_t)g.n1 * g.n2);
-                v0 += bias[pm * 64 + ch], v1 += bias[pm * 64 + ch + 1];
-              } else {
-                v0 += b0, v1 += b1;
-              }
-              *reinterpret_cast<uint32_t*>(h1 + pix * 64 + ch) = pack_bf16x2(fmaxf(v0, 0.f), fmaxf(v1, 0.f));
+            } else {
+              v[0] += ba, v[1] += ba, v[2] += bb, v[3] += bb;
             }
+            f[2 * k] = pack_bf16x2(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f));
+            f[2 * k + 1] = pack_bf16x2(fmaxf(v[2], 0.f), fmaxf(v[3], 0.f));
+          }
+          // stored matrix j of call h: block k = 2h + j / 2, channel half j % 2; lane 8j + i -> position 8k + i
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = lane >> 3, pos = c + 8 * (2 * h + (j >> 1)) + (lane & 7), ch = j & 1;
+            stmatrix_x4_trans(sbase + pos * 32 + ((ch ^ ((pos >> 2) & 1)) << 4), f[4 * h], f[4 * h + 1],
+                              f[4 * h + 2], f[4 * h + 3]);
+          }
         }
+        if (tma) {
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&tmS, buf, 16 * G, c0, r0 + pbase / 64, b);
+            bulk_commit_group();
+          }
+        } else {
+          __syncwarp();
+          // rows of this half tile: lane -> (position, 16-B channel chunk)
+          for (int e = lane; e < 2 * half; e += 32) {
+            const int pos = e >> 1, ch = e & 1, p = pbase + pos;
+            if (p >= n0 + cnt) continue;
+            size_t pix;
+            if (linear) {
+              pix = pix0 + p;
+            } else {
+              const int rr = (int)(((uint32_t)p * wmagic) >> 20), cc = p - rr * W;
+              if (c0 + cc >= g.n2) continue;
+              pix = pix0 + (size_t)rr * g.n2 + cc;
+            }
+            const uint4 val = *reinterpret_cast<const uint4*>(buf + pos * 32 + ((ch ^ ((pos >> 2) & 1)) << 4));
+            *reinterpret_cast<uint4*>(h1 + pix * 64 + 16 * G + 8 * ch) = val;
+          }
+        }
+        sb ^= 1;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[a]);
       }
     }
+    if (lane == 0) bulk_wait<0>();   // every h1 store has completed before the CTA exits
   }
   tc_fence_before();
   __syncthreads();
@@ -828,10 +861,7 @@ static Geo13 make_geo13(int batch, int n1, int n2, int R, bool conv1) {
   return g;
 }
 
-size_t conv1_tc_smem_bytes() {
-  const size_t strips = (size_t)2 * XC_STRIDE > (size_t)2 * SW1_OFF * 4 ? (size_t)2 * XC_STRIDE : (size_t)2 * SW1_OFF * 4;
-  return (size_t)W1_BYTES + 2 * IM_BYTES + strips + 1024;
-}
+size_t conv1_tc_smem_bytes() { return (size_t)C1_STAGE_OFF + 8 * 2 * C1_STAGE + 1024; }
 
 // finite guard rows past a conv3 strip: the last tile's last K-block reads positions up to
 // (ntiles - 1) * OUT3 + 10 P + 255 of a (R + 10) P-position strip
@@ -912,13 +942,16 @@ cudaError_t setup_conv13_tc(int n2) {
 int conv1_tc_box_rows() { return R1 + 10; }
 int conv1_tc_box_cols(int n2) { return (((n2 < 64 ? n2 : 64) + 10 + 7) & ~7) + 8; }
 
-cudaError_t launch_conv1_tc(const CUtensorMap* tmX, const void* xt, const void* w1pack, const float* bias,
-                            int fullmap, void* h1, int batch, int n1, int n2, int num_sms, cudaStream_t st) {
+// tmS (may be null): the TMA store map over h1 (encode_h1_store: box 16 ch x 64 cols x 2 rows, SWIZZLE_32B)
+cudaError_t launch_conv1_tc(const CUtensorMap* tmX, const CUtensorMap* tmS, const void* xt, const void* w1pack,
+                            const float* bias, int fullmap, void* h1, int batch, int n1, int n2, int num_sms,
+                            cudaStream_t st) {
   Geo13 g = make_geo13(batch, n1, n2, R1, true);
   const int grid = g.units < num_sms ? g.units : num_sms;
   auto k = tmX ? k_conv1_tc<true> : k_conv1_tc<false>;
   CUtensorMap dummy{};
-  k<<<grid, 384, conv1_tc_smem_bytes(), st>>>(tmX ? *tmX : dummy, reinterpret_cast<const __nv_bfloat16*>(xt),
+  k<<<grid, 384, conv1_tc_smem_bytes(), st>>>(tmX ? *tmX : dummy, tmS ? *tmS : dummy, tmS ? 1 : 0,
+                                              reinterpret_cast<const __nv_bfloat16*>(xt),
                                               reinterpret_cast<const uint8_t*>(w1pack), bias, fullmap, g,
                                               reinterpret_cast<__nv_bfloat16*>(h1));
   return cudaGetLastError();
@@ -934,5 +967,7 @@ cudaError_t launch_conv3_tc(const CUtensorMap* tmH2, const void* w3pack, const f
                                                       fullmap, relu, g, xhat);
   return cudaGetLastError();
 }
+
+DI_DEBUG_BINDER(di_debug_bind_k_conv13_tc)
 
 }  // namespace di

@@ -34,6 +34,7 @@
 #include <mutex>
 
 #include "kernels.cuh"
+#define DI_TU_ID 3
 #include "sm100.cuh"
 
 namespace di {
@@ -203,6 +204,8 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
           { PT0 if (ti >= 2) mbar_wait(&tempty[buf], ((ti >> 1) - 1) & 1); PT1(c_t) }
           tc_fence_after();
           const uint32_t d = tmem + buf * 256;
+          // the last K-block's window (u = 10, v0 = TAPS (J - 1)) stays inside the strip and its guard rows
+          DI_DEVICE_ASSERT(n0 + 10 * g.P + TAPS * (J - 1) + nmma <= (R + 10) * g.P + GUARD_ROWS, n0, nmma);
           uint64_t bd = bdesc0 + (uint64_t)(n0 * (RB >> 4));
           for (int uu = 0; uu < 11; ++uu, bd += pstep) {
 #pragma unroll
@@ -527,5 +530,7 @@ cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, cons
       reinterpret_cast<const __nv_bfloat16*>(h1b));
   return cudaGetLastError();
 }
+
+DI_DEBUG_BINDER(di_debug_bind_k_conv2_tc)
 
 }  // namespace di

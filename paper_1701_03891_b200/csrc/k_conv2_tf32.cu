@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
+#define DI_TU_ID 5
 #include "sm100.cuh"
 
 namespace di {
@@ -296,5 +297,7 @@ cudaError_t launch_convg_tf32(int cin, int cout, const CUtensorMap* tmIn, const 
   if (cin == 64 && cout == 64) return launch<64, 64, EPI_BIAS_RELU>(tmIn, wpack, bias, 0, nullptr, batch, n1, n2, out, num_sms, st);
   return cudaErrorInvalidValue;
 }
+
+DI_DEBUG_BINDER(di_debug_bind_k_conv2_tf32)
 
 }  // namespace di

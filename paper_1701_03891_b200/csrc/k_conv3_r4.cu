@@ -18,73 +18,114 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
+#define DI_TU_ID 4
 #include "sm100.cuh"
 
 namespace di {
 
 namespace {
 constexpr int RP = C3R_RP, ES = C3R_ES, NWIN = C3R_NWIN, IMIN = C3R_IMIN;
-constexpr int R = 8;                   // output rows per unit
-constexpr int NPASS = R / RP;
+constexpr int R = 8;                   // output rows per unit (one pass: R == RP)
+static_assert(R == RP, "one pass per unit");
+constexpr int CH = 8;                  // strip rows per TMA chunk
+constexpr int NCH = 4;                 // chunk slots in the ring: a unit reads 3 chunks, the 4th loads ahead
+constexpr int RING_ROWS = NCH * CH;   // ring rows (power of two)
 constexpr int NACC = 4;                // TMEM accumulator slots (128 columns each)
+#ifndef DI_C3R_PF
+#define DI_C3R_PF 6
+#endif
+constexpr int C3R_PF = DI_C3R_PF;      // chunks prefetched into L2 ahead of the shared-memory loads
 constexpr int TBLK = ES * 64;          // one T entry: ES rows (v) x 32 channels bf16, SWIZZLE_64B
 constexpr int TBYTES = (C3R_NENT * TBLK + 1023) & ~1023;
-constexpr int GUARD = 16;              // zero positions past the strip (windows read up to N - P past the box)
+constexpr int GUARD = 16;              // zero positions past the ring (the last ring row's window reads N - P past it)
 constexpr int SROW = 84;               // epilogue tile row stride (floats): 16-B rows
 constexpr int RPW = 32 / ES;           // output rows per epilogue warp (its TMEM quadrant)
 constexpr int SWARP = RPW * 11 * SROW; // per epilogue warp
 
+// Work item = one column segment of one image (or a contiguous part of its row blocks when there are fewer
+// columns than SMs): its units run top to bottom, so consecutive units share 10 of their 18 strip rows.
 struct GeoR4 {
-  int n1, n2, wseg, P, N, nrb, ncs, units;
+  int n1, n2, wseg, P, N, nrb, ncs, splits, per, items;
 };
+__device__ __forceinline__ void item_of(const GeoR4& g, int it, int& b, int& c0, int& rb0, int& nu) {
+  const int col = it / g.splits, sp = it - col * g.splits;
+  b = col / g.ncs;
+  c0 = (col - b * g.ncs) * g.wseg;
+  rb0 = sp * g.per;
+  nu = min(g.per, g.nrb - rb0);
+}
 }  // namespace
 
+// Strip rows arrive in chunks of CH = 8 rows through a ring of NCH = 4 chunk slots (ROW RING): unit j of an item
+// (output rows 8 (rb0 + j) .. + 7) reads strip rows [8 (rb0 + j) - 5, + 18) = chunks j, j + 1, j + 2 of the item, and
+// releases chunk j when its MMAs complete, so chunk j + 3 loads while unit j computes.  Each strip row is fetched
+// once per item (10 chunks = 80 rows for a 64-row image) instead of 18 rows per 8-row unit: the L2 -> shared-memory
+// traffic drops from 2.25x to 1.25x the h2 rows.  Window k of a unit reads ring row (8 (chunk j) + k) mod 32 plus
+// N - P positions past it (the next row, the slot padding or the zero guard); those positions only reach D columns
+// >= P, which no output reads.
 __global__ void __launch_bounds__(256, 1)
     k_conv3_r4(const __grid_constant__ CUtensorMap tmH2, const uint8_t* __restrict__ tpack,
                const float* __restrict__ bias, int fullmap, int relu, GeoR4 g, float* __restrict__ xhat) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int P = g.P;
-  const int strip_bytes = (R + 10) * P * 64;
-  const int strip_alloc = (strip_bytes + GUARD * 64 + 1023) & ~1023;
+  const int chunk_bytes = CH * P * 64;
+  const int slot = (chunk_bytes + 1023) & ~1023;              // slot stride: 1024-aligned TMA destinations
   uint8_t* const tb = smem;                                   // T stack (1024-aligned)
-  uint8_t* const strip0 = smem + TBYTES;                      // 2 strips (TBYTES = 34 KB, 1024-aligned)
-  float* const S = reinterpret_cast<float*>(smem + TBYTES + 2 * strip_alloc);
+  uint8_t* const ring = smem + TBYTES;                        // NCH chunk slots, then the zero guard
+  const int ring_alloc = (NCH * slot + GUARD * 64 + 1023) & ~1023;
+  float* const S = reinterpret_cast<float*>(ring + ring_alloc);
 
-  __shared__ uint64_t wbar, sfull[2], sempty[2], acc_full[NACC], acc_empty[NACC];
+  __shared__ uint64_t wbar, cfull[NCH], cempty[NCH], acc_full[NACC], acc_empty[NACC];
   __shared__ uint32_t tslot;
   const int warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmH2);
     mbar_init(&wbar, 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&sfull[s], 1), mbar_init(&sempty[s], 1);
+    for (int s = 0; s < NCH; ++s) mbar_init(&cfull[s], 1), mbar_init(&cempty[s], 1);
     for (int a = 0; a < NACC; ++a) mbar_init(&acc_full[a], 1), mbar_init(&acc_empty[a], 4);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
-  for (int s = 0; s < 2; ++s)   // finite guard past each strip
-    for (int i = threadIdx.x; i < GUARD * 64 / 16; i += blockDim.x)
-      reinterpret_cast<uint4*>(strip0 + s * strip_alloc + strip_bytes)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < ring_alloc / 16; i += blockDim.x)   // finite ring (never-loaded slots) and guard
+    reinterpret_cast<uint4*>(ring)[i] = make_uint4(0, 0, 0, 0);
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
-  const int per_img = g.nrb * g.ncs;
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------ producer: T once, strips per unit
+    if (lane == 0) {  // ------------------------------------------------ producer: T once, strip chunks
       mbar_arrive_expect_tx(&wbar, TBYTES);
       bulk_load(tb, tpack, TBYTES, &wbar);
-      int it = 0;
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
-        const int b = u / per_img, rem = u - b * per_img;
-        const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
-        const int s = it & 1;
-        if (it >= 2) mbar_wait(&sempty[s], ((it >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&sfull[s], strip_bytes);
-        tma_load_4d(strip0 + s * strip_alloc, &tmH2, &sfull[s], 0, c0 - 5, r0 - 5, b);
+      // L2 prefetch cursor, PF chunks ahead of the loads: the ring holds one chunk of lead (one unit of MMAs), too
+      // few bytes in flight to cover DRAM latency; the prefetched chunks arrive from L2
+      int pit = blockIdx.x, pk = 0, pb = 0, pc0 = 0, prb0 = 0, pnu = 0;
+      if (pit < g.items) item_of(g, pit, pb, pc0, prb0, pnu);
+      auto prefetch_next = [&]() {
+        if (pit >= g.items) return;
+        tma_prefetch_l2_4d(&tmH2, 0, pc0 - 5, CH * (prb0 + pk) - 5, pb);
+        if (++pk == pnu + 2) {
+          pk = 0, pit += gridDim.x;
+          if (pit < g.items) item_of(g, pit, pb, pc0, prb0, pnu);
+        }
+      };
+      for (int i = 0; i < C3R_PF; ++i) prefetch_next();
+      uint32_t gc = 0;                 // chunks issued by this CTA
+      for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
+        int b, c0, rb0, nu;
+        item_of(g, it, b, c0, rb0, nu);
+        for (int k = 0; k < nu + 2; ++k, ++gc) {
+          const uint32_t sl = gc % NCH;
+          if (gc >= NCH) mbar_wait(&cempty[sl], ((gc / NCH) - 1) & 1);
+          mbar_arrive_expect_tx(&cfull[sl], chunk_bytes);
+          tma_load_4d(ring + sl * slot, &tmH2, &cfull[sl], 0, c0 - 5, CH * (rb0 + k) - 5, b);
+          prefetch_next();
+        }
       }
     }
   } else if (warp == 1) {
@@ -93,30 +134,43 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const uint32_t idesc = idesc_f32acc(1, 128, g.N);
       const uint64_t adesc0 = smem_desc(smem_u32(tb), 16, 512, kSwizzle64B);
-      const uint64_t bdesc0 = smem_desc(smem_u32(strip0), 16, 512, kSwizzle64B);
-      const uint64_t rstep = (uint64_t)((P * 64) >> 4);       // one strip row
-      int it = 0, pi = 0;
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
-        const int s = it & 1;
-        mbar_wait(&sfull[s], (it >> 1) & 1);
-        tc_fence_after();
-        for (int p = 0; p < NPASS; ++p, ++pi) {
+      const uint64_t bdesc0 = smem_desc(smem_u32(ring), 16, 512, kSwizzle64B);
+      uint32_t gc0 = 0;                // this item's first chunk (CTA-wide count)
+      int pi = 0;
+      for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
+        int b, c0, rb0, nu;
+        item_of(g, it, b, c0, rb0, nu);
+        for (int k = 0; k < 2; ++k) {   // the item's first two chunks
+          const uint32_t c = gc0 + k;
+          mbar_wait(&cfull[c % NCH], (c / NCH) & 1);
+        }
+        for (int j = 0; j < nu; ++j, ++pi) {
+          const uint32_t cj = gc0 + j;
+          mbar_wait(&cfull[(cj + 2) % NCH], ((cj + 2) / NCH) & 1);
+          tc_fence_after();
           const int a = pi % NACC;
           if (pi >= NACC) {
             mbar_wait(&acc_empty[a], ((pi / NACC) - 1) & 1);
             tc_fence_after();
           }
           const uint32_t d = tmem + a * 128;
-          uint64_t bd = bdesc0 + (uint64_t)((s * strip_alloc) >> 4) + (uint64_t)(RP * p) * rstep;
+          const int row0 = (int)(cj % NCH) * CH;              // ring row of the unit's strip row 0
+          // a window reads N - P positions past its row: the last slot's last row runs into the zero guard
+          DI_DEVICE_ASSERT(g.N - g.P <= GUARD, g.N, g.P);
 #pragma unroll 2
-          for (int k = 0; k < NWIN; ++k, bd += rstep) {
+          for (int k = 0; k < NWIN; ++k) {
+            const int rr = (row0 + k) & (RING_ROWS - 1);      // ring row: slot rr / CH, row rr % CH of the slot
+            const uint64_t bd = bdesc0 + (uint64_t)(((rr / CH) * slot + (rr % CH) * P * 64) >> 4);
             const uint64_t ad = adesc0 + (uint64_t)(((10 - k - IMIN) * TBLK) >> 4);   // T[10 - k] ..
             umma_f16_ss(d, ad, bd, idesc, k != 0);
             umma_f16_ss(d, ad + 2, bd + 2, idesc, 1);                       // channels 16..31: +32 B
           }
           umma_commit(&acc_full[a]);
+          umma_commit(&cempty[cj % NCH]);                     // chunk j is read by units j - 2 .. j only
         }
-        umma_commit(&sempty[s]);
+        umma_commit(&cempty[(gc0 + nu) % NCH]);               // the item's last two chunks
+        umma_commit(&cempty[(gc0 + nu + 1) % NCH]);
+        gc0 += nu + 2;
       }
     }
   } else if (warp >= 4) {  // ------------------------------- epilogue: warp q = output rows RPW q .. RPW q + RPW - 1
@@ -124,10 +178,11 @@ __global__ void __launch_bounds__(256, 1)
     float* const Sq = S + q * SWARP;
     const float bsc = (!fullmap && bias) ? bias[0] : 0.f;
     int pi = 0;
-    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-      const int b = u / per_img, rem = u - b * per_img;
-      const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
-      for (int p = 0; p < NPASS; ++p, ++pi) {
+    for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
+      int b, c0, rb0, nu;
+      item_of(g, it, b, c0, rb0, nu);
+      for (int j = 0; j < nu; ++j, ++pi) {
+        const int r0 = (rb0 + j) * R;
         const int a = pi % NACC;
         mbar_wait(&acc_full[a], (pi / NACC) & 1);
         tc_fence_after();
@@ -143,20 +198,20 @@ __global__ void __launch_bounds__(256, 1)
         if ((lane % ES) < 11) {   // S row (lane / ES) * 11 + v: tap v of output row RPW q + lane / ES
           float4* dst = reinterpret_cast<float4*>(Sq + ((lane / ES) * 11 + lane % ES) * SROW);
 #pragma unroll
-          for (int j = 0; j < 20; ++j)
-            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          for (int jj = 0; jj < 20; ++jj)
+            dst[jj] = make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
+                                  __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
         }
         __syncwarp();
 #pragma unroll
         for (int h = 0; h < 2 * RPW; ++h) {
-          const int j = lane + 32 * (h & 1), tr = h >> 1;
-          const int row = r0 + RP * p + RPW * q + tr;
+          const int jc = lane + 32 * (h & 1), tr = h >> 1;
+          const int row = r0 + RPW * q + tr;
           float acc = 0.f;
 #pragma unroll
-          for (int v = 0; v < 11; ++v) acc += Sq[(tr * 11 + v) * SROW + j + v];
-          if (j < g.wseg && c0 + j < g.n2 && row < g.n1) {
-            const size_t pix = ((size_t)b * g.n1 + row) * g.n2 + c0 + j;
+          for (int v = 0; v < 11; ++v) acc += Sq[(tr * 11 + v) * SROW + jc + v];
+          if (jc < g.wseg && c0 + jc < g.n2 && row < g.n1) {
+            const size_t pix = ((size_t)b * g.n1 + row) * g.n2 + c0 + jc;
             acc += (fullmap && bias) ? bias[pix % ((size_t)g.n1 * g.n2)] : bsc;
             if (relu) acc = fmaxf(acc, 0.f);
             xhat[pix] = acc;
@@ -171,7 +226,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-static GeoR4 make_geo_r4(int batch, int n1, int n2) {
+static GeoR4 make_geo_r4(int batch, int n1, int n2, int num_sms) {
   GeoR4 g;
   g.n1 = n1, g.n2 = n2;
   g.wseg = n2 < 64 ? n2 : 64;
@@ -179,17 +234,23 @@ static GeoR4 make_geo_r4(int batch, int n1, int n2) {
   g.N = (g.P + 15) & ~15;
   g.nrb = (n1 + R - 1) / R;
   g.ncs = (n2 + g.wseg - 1) / g.wseg;
-  g.units = batch * g.nrb * g.ncs;
+  const int cols = batch * g.ncs;
+  // fewer columns than SMs: split each column into parts of `per` row blocks
+  g.splits = cols >= num_sms ? 1 : std::min(g.nrb, (num_sms + cols - 1) / cols);
+  g.per = (g.nrb + g.splits - 1) / g.splits;
+  g.splits = (g.nrb + g.per - 1) / g.per;
+  g.items = cols * g.splits;
   return g;
 }
 
 static size_t smem_r4(int n2) {
   const int wseg = n2 < 64 ? n2 : 64, P = wseg + 10;
-  const size_t strip_alloc = ((size_t)(R + 10) * P * 64 + GUARD * 64 + 1023) & ~(size_t)1023;
-  return TBYTES + 2 * strip_alloc + 4 * SWARP * 4 + 1024;
+  const size_t slot = ((size_t)CH * P * 64 + 1023) & ~(size_t)1023;
+  const size_t ring_alloc = (NCH * slot + GUARD * 64 + 1023) & ~(size_t)1023;
+  return TBYTES + ring_alloc + 4 * SWARP * 4 + 1024;
 }
 
-int conv3_r4_box_rows() { return R + 10; }
+int conv3_r4_box_rows() { return CH; }
 int conv3_r4_tpack_bytes() { return TBYTES; }
 
 cudaError_t setup_conv3_r4(int n2) {
@@ -198,11 +259,13 @@ cudaError_t setup_conv3_r4(int n2) {
 
 cudaError_t launch_conv3_r4(const CUtensorMap* tmH2, const void* tpack, const float* bias, int fullmap, int relu,
                             float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st) {
-  GeoR4 g = make_geo_r4(batch, n1, n2);
-  const int grid = g.units < num_sms ? g.units : num_sms;
+  GeoR4 g = make_geo_r4(batch, n1, n2, num_sms);
+  const int grid = g.items < num_sms ? g.items : num_sms;
   k_conv3_r4<<<grid, 256, smem_r4(n2), st>>>(*tmH2, reinterpret_cast<const uint8_t*>(tpack), bias, fullmap, relu, g,
                                             xhat);
   return cudaGetLastError();
 }
+
+DI_DEBUG_BINDER(di_debug_bind_k_conv3_r4)
 
 }  // namespace di

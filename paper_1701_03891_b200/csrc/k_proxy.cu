@@ -13,6 +13,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#define DI_TU_ID 1
 #include "sm100.cuh"
 
 namespace di {
@@ -378,5 +379,7 @@ cudaError_t launch_stage_y(const void* y, long long ldy, int m, int kpad, int ba
                                             reinterpret_cast<float*>(out));
   return cudaGetLastError();
 }
+
+DI_DEBUG_BINDER(di_debug_bind_k_proxy)
 
 }  // namespace di

@@ -417,10 +417,10 @@ __global__ void k_repack_bf16(const float* __restrict__ params, int flip, uint16
       const int ci = (((r / 16) ^ (row & 7)) * 8) + (r % 16) / 2;
       const int u = kb / 3, b = 4 * (kb % 3) + row / 32, k = row % 32;
       wp2[e] = bfbits(b < KS ? wx_at(W2, 64, k, ci, u, b, flip) : 0.f);
-    } else if (e < E2 + E1) {         // conv1: block u, row m (permuted filter), 16 taps (32 B), SWIZZLE_32B
+    } else if (e < E2 + E1) {         // conv1: block u, row m (filter m), 16 taps (32 B), SWIZZLE_32B
       const int i = e - E2, u = i / 1024, o = (i % 1024) * 2, m = o / 32, r = o % 32;
       const int v = (((r / 16) ^ ((m >> 2) & 1)) * 8) + (r % 16) / 2;
-      const int grp = m / 16, j = m % 16, f = 16 * grp + (j < 8 ? 2 * j : 2 * (j - 8) + 1);
+      const int f = m;
       wp1[i] = bfbits(v < KS ? wx_at(W1, 1, f, 0, u, v, flip) : 0.f);
     } else {                          // conv3 (k_conv3_r4): stack row rho = entry e x ES + tap v, 32 ch, SW64
       const int i = e - E2 - E1, rho = i / 32, o = (i % 32) * 2;

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
+#define DI_TU_ID 8
 #include "sm100.cuh"
 
 namespace di {
@@ -468,5 +469,7 @@ cudaError_t launch_wgrad3_tc(const void* h2, const float* dg3, int batch, int n1
   k_wgrad13_reduce<3><<<dim3(128 * 48 / 32, 2), 256, 0, st>>>(part, part_b, grid, flip, gw, gb);
   return cudaGetLastError();
 }
+
+DI_DEBUG_BINDER(di_debug_bind_k_wgrad13_tc)
 
 }  // namespace di

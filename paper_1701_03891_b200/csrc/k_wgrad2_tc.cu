@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
+#define DI_TU_ID 9
 #include "sm100.cuh"
 
 namespace di {
@@ -268,5 +269,7 @@ cudaError_t launch_dg2_bf16(const float* dg, size_t npix, void* dst, float* part
   k_dg2_bf16<<<WGRAD_CHUNKS, 256, 0, st>>>(dg, npix, reinterpret_cast<__nv_bfloat16*>(dst), part_b);
   return cudaGetLastError();
 }
+
+DI_DEBUG_BINDER(di_debug_bind_k_wgrad2_tc)
 
 }  // namespace di

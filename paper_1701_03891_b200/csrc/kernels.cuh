@@ -4,7 +4,7 @@
 // Instrumentation and geometry overrides exist only in the experiment library (build.py: DI_NVCC_EXTRA builds
 // libdeepinverse_exp.so with -DDI_EXPERIMENT_BUILD); the product library cannot be compiled with them.
 #if !defined(DI_EXPERIMENT_BUILD) && (defined(DI_PROF_CONV1) || defined(DI_PROF_CONV2) || defined(DI_PROF_CONV3) || \
-                                      defined(DI_C2_ROWS) || defined(DI_C2_WSTAGES))
+                                      defined(DI_C2_ROWS) || defined(DI_C2_WSTAGES) || defined(DI_C3R_PF))
 #error "experiment macros need DI_EXPERIMENT_BUILD (build.py routes them to libdeepinverse_exp.so)"
 #endif
 #include <cuda.h>
@@ -73,8 +73,9 @@ cudaError_t setup_conv13_tc(int n2);
 int conv1_tc_box_rows();
 int conv1_tc_box_cols(int n2);
 // tmX: 3-D tensor map of x_tilde (n2 % 8 == 0) for the TMA strip path, or nullptr for the gather path
-cudaError_t launch_conv1_tc(const CUtensorMap* tmX, const void* xt, const void* w1pack, const float* bias,
-                            int fullmap, void* h1, int batch, int n1, int n2, int num_sms, cudaStream_t st);
+cudaError_t launch_conv1_tc(const CUtensorMap* tmX, const CUtensorMap* tmS, const void* xt, const void* w1pack,
+                            const float* bias, int fullmap, void* h1, int batch, int n1, int n2, int num_sms,
+                            cudaStream_t st);
 
 int conv1_tf32_box_rows();
 // TF32 mode: tmX = 3-D map of the fp32 x_tilde (n2 % 4 == 0), box (P + 8) x (8 + 10) x 1

@@ -12,6 +12,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
+#include <cuda_runtime.h>
 
 namespace di {
 
@@ -44,10 +45,49 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// ------------------------------------------------------------------ debug build (DI_DEBUG)
+// build.py: DI_NVCC_EXTRA=-DDI_DEBUG builds libdeepinverse_exp.so in which every mbarrier wait is bounded (~2^31
+// cycles, about a second) and a few geometry invariants are checked on the device.  A failure writes
+// {code, block, thread, a, b} to a host-mapped record (so it survives the trap that kills the context) and traps;
+// the host reads it back with di_debug_report (debug library only).  code = (translation unit << 8) | kind.
+#ifndef DI_TU_ID
+#define DI_TU_ID 0
+#endif
+enum : uint32_t { DI_DBG_MBAR = 1, DI_DBG_BOUNDS = 2 };
+#ifdef DI_DEBUG
+namespace {
+__device__ unsigned int* g_di_dbg = nullptr;
+}
+static __device__ __noinline__ void di_debug_fail(uint32_t kind, uint32_t a, uint32_t b) {
+  unsigned int* p = g_di_dbg;
+  if (p && atomicCAS(p, 0u, ((uint32_t)DI_TU_ID << 8) | kind) == 0u) {
+    p[1] = blockIdx.x, p[2] = threadIdx.x, p[3] = a, p[4] = b;
+    __threadfence_system();
+  }
+  __trap();
+}
+#define DI_DEVICE_ASSERT(cond, a, b)                                   \
+  do {                                                                 \
+    if (!(cond)) di_debug_fail(DI_DBG_BOUNDS, (uint32_t)(a), (uint32_t)(b)); \
+  } while (0)
+// each translation unit binds its own copy of g_di_dbg (no relocatable device code)
+#define DI_DEBUG_BINDER(fn) \
+  cudaError_t fn(unsigned int* p) { return cudaMemcpyToSymbol(g_di_dbg, &p, sizeof(p)); }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity))
+    if (clock64() - t0 > (1ll << 31)) di_debug_fail(DI_DBG_MBAR, smem_u32(bar), parity);
+}
+#else
+#define DI_DEVICE_ASSERT(cond, a, b) \
+  do {                               \
+  } while (0)
+#define DI_DEBUG_BINDER(fn)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+#endif
 
 // wait with back-off: for producer-side waits that are not on the critical path; keeps the spinning warp
 // from stealing issue slots from the epilogue warp that shares its SM sub-partition
@@ -83,6 +123,12 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA prefetch of a box into L2 (no shared memory, no completion)
+__device__ __forceinline__ void tma_prefetch_l2_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(c0), "r"(c1),
+               "r"(c2), "r"(c3)
+               : "memory");
+}
 // plain bulk copy global -> shared (no tensor map), completes on an mbarrier
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -108,6 +154,32 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 // all threads of all CTAs of the cluster (release / acquire)
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA tensor store shared -> global (bulk async-group of the issuing thread)
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N bulk groups of this thread still READ their shared-memory source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// four 8x8 b16 matrices from registers to shared memory, transposed: register j of thread t holds elements
+// (row t / 4, columns 2(t % 4), 2(t % 4) + 1) of matrix j (low half = the even column; the tcgen05.ld.16x256b
+// layout), and lane 8j + i gives the address of the i-th 16-B row of the STORED matrix j, which is column i of
+// matrix j (its 8 rows' elements, row 0 first)
+__device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(r0),
+               "r"(r1), "r"(r2), "r"(r3)
+               : "memory");
 }
 // generic-proxy smem writes -> visible to the async proxy (UMMA / TMA store)
 __device__ __forceinline__ void fence_async_smem() {

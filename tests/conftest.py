@@ -31,3 +31,20 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _debug_library_record(request):
+    """Under the DI_DEBUG library (DI_LIB=.../libdeepinverse_exp.so built with -DDI_DEBUG): after every GPU test, the
+    host-mapped failure record of the bounded mbarrier waits / device asserts must be clean."""
+    yield
+    if "gpu" not in request.keywords or not os.environ.get("DI_LIB"):
+        return
+    import ctypes
+    from paper_1701_03891_b200 import binding
+    lib = binding.load()
+    if not hasattr(lib, "di_debug_report"):
+        return
+    buf = ctypes.create_string_buffer(256)
+    code = lib.di_debug_report(buf, 256)
+    assert code in (0, -1), buf.value.decode()
