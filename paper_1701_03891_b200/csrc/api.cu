@@ -89,7 +89,7 @@ float bf2f(uint16_t b) {
 
 struct di_ctx_s {
   int device = 0, num_sms = 0;
-  bool conv2_mc = true;         // conv2 CTA-pair weight multicast (DI_EXP_NO_MC=1 at di_create turns it off: A/B tests)
+  int conv2_cluster = 2;        // conv2 weight-multicast cluster (DI_EXP_NO_MC=1 -> 1, DI_EXP_C2_CLUSTER=4 -> 4 at di_create)
   int m = 0, n1 = 0, n2 = 0, N = 0, max_batch = 0, kpad = 0;
   int pxbn = 256;               // pixel-tile width of the lifting GEMM = row count of a Phi^T block
   di_precision prec = DI_PREC_BF16;
@@ -735,7 +735,7 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
         if (s != DI_OK) return s;
         tmp = &tm;
       }
-      CUDA_TRY(di::launch_conv2_tc(tmp, c->wp2, c->b2, fm, batch, c->n1, c->n2, h2, c->num_sms, st, c->conv2_mc));
+      CUDA_TRY(di::launch_conv2_tc(tmp, c->wp2, c->b2, fm, batch, c->n1, c->n2, h2, c->num_sms, st, c->conv2_cluster));
     } else if (c->prec == DI_PREC_TF32) {
       CUtensorMap tm;
       const CUtensorMap* tmp = &c->tmH1;
@@ -908,7 +908,8 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   if (!c) return fail(DI_ERR_OOM, "host allocation failed");
   c->device = a->device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, a->device);
-  c->conv2_mc = getenv("DI_EXP_NO_MC") == nullptr;   // read once per context, never on the launch path
+  // read once per context, never on the launch path (A/B switches of the multicast cluster)
+  c->conv2_cluster = getenv("DI_EXP_NO_MC") ? 1 : (getenv("DI_EXP_C2_CLUSTER") ? atoi(getenv("DI_EXP_C2_CLUSTER")) : 2);
 #ifdef DI_DEBUG
   {
     di_status sd = debug_bind();

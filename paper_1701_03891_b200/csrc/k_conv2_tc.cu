@@ -85,7 +85,7 @@ enum { C2_BIAS_RELU = 0, C2_MASK = 1 };
 // MC: CTA pairs (cluster of 2) share the weight stream -- each CTA copies half of every K-block to BOTH CTAs'
 // rings (multicast) and each MMA commit frees the stage in both, halving the L2 -> SM weight traffic.  Needs the two
 // CTAs of a pair to consume the same K-block sequence (equal tile counts: launch_conv2_tc checks).
-template <int CIN, int COUT, int MODE, bool MC = false>
+template <int CIN, int COUT, int MODE, int CL = 1>
 __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
     k_conv2_tc(const __grid_constant__ CUtensorMap tmH1, const __nv_bfloat16* __restrict__ wpack,
                const float* __restrict__ bias, int fullmap, Geo g, __nv_bfloat16* __restrict__ h2,
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmH1);
     for (int h = 0; h < 2; ++h) mbar_init(&hfull[h], 1), mbar_init(&hempty[h], 1);
-    for (int s = 0; s < WST; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], MC ? 2 : 1);
+    for (int s = 0; s < WST; ++s) mbar_init(&wfull[s], 1), mbar_init(&wempty[s], CL);
     for (int s = 0; s < 2; ++s) mbar_init(&tfull[s], 1), mbar_init(&tempty[s], 4);
     fence_mbar_init();
   }
@@ -131,10 +131,11 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
-  if (MC) cluster_sync_all();   // the peer's barriers are initialised before any multicast copy or commit
+  if (CL > 1) cluster_sync_all();   // the peers' barriers are initialised before any multicast copy or commit
   tc_fence_after();
   const uint32_t tmem = tslot;
-  const uint32_t crank = MC ? cluster_ctarank() : 0;
+  const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
+  constexpr uint16_t CMASK = (uint16_t)((1u << CL) - 1);
 
   const int per_img = g.nrb * g.ncs;
   if (warp == 0) {
@@ -159,14 +160,14 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
             t_issue[st] = clock64();
 #endif
             mbar_arrive_expect_tx(&wfull[st], WB);
-            if (MC)   // this CTA's half of the K-block, to both CTAs of the pair
-              bulk_load_mc(wst + st * WB + crank * (WB / 2), wsrc + crank * (WB / 2), WB / 2, &wfull[st], 0x3);
+            if (CL > 1)   // this CTA's 1/CL of the K-block, to every CTA of the cluster
+              bulk_load_mc(wst + st * WB + crank * (WB / CL), wsrc + crank * (WB / CL), WB / CL, &wfull[st], CMASK);
             else
               bulk_load(wst + st * WB, wsrc, WB, &wfull[st]);
           }
         }
       }
-      if (MC)   // every commit (local and the peer's) into this CTA's ring has landed before the cluster exits
+      if (CL > 1)   // every commit (local and the peers') into this CTA's ring has landed before the cluster exits
         for (uint32_t k = wk > (uint32_t)WST ? wk - WST : 0; k < wk; ++k) mbar_wait(&wempty[k % WST], (k / WST) & 1);
     }
   } else if (warp == 1) {
@@ -225,8 +226,8 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
               umma_f16_ss(d, ad, b, idesc, (uu | j) != 0);
 #pragma unroll
               for (int kk = 1; kk < KMMA; ++kk) umma_f16_ss(d, ad + 2 * kk, b + 2 * kk, idesc, 1);
-              if (MC)
-                umma_commit_mc(&wempty[st], 0x3);
+              if (CL > 1)
+                umma_commit_mc(&wempty[st], CMASK);
               else
                 umma_commit(&wempty[st]);
             }
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (MC) cluster_sync_all();
+  if (CL > 1) cluster_sync_all();
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
@@ -364,16 +365,16 @@ static Geo make_geo(int batch, int n1, int n2, int R = C2_ROWS) {
 
 // Weight multicast across CTA pairs (MC) needs both CTAs of every pair to run the same number of tiles: an even
 // grid, an even remainder of units over the grid, and the last row-block's units as many tiles as the full ones.
-static bool pair_balanced(const Geo& g, int grid, int R) {
+static bool pair_balanced(const Geo& g, int grid, int R, int cl = 2) {
   const int Lfull = (R - 1) * g.P + g.wseg, rl = g.n1 - (g.nrb - 1) * R, Llast = (rl - 1) * g.P + g.wseg;
-  return grid % 2 == 0 && (g.units % grid) % 2 == 0 &&
+  return grid % cl == 0 && (g.units % grid) % cl == 0 &&
          (Lfull + OUT_PER_TILE - 1) / OUT_PER_TILE == (Llast + OUT_PER_TILE - 1) / OUT_PER_TILE;
 }
 // And every pair must be co-resident: a GPC with an odd number of usable SMs cannot host a 2-CTA cluster on all of
 // them, and a persistent grid whose last pair waits for a free GPC pair would take twice as long.  The occupancy
 // query (once per kernel and shared-memory size) gates MC on all grid / 2 clusters fitting at once.
 template <typename Kern>
-static bool pairs_fit(Kern kern, int grid, int threads, size_t smem) {
+static bool pairs_fit(Kern kern, int grid, int threads, size_t smem, int cl = 2) {
   struct Entry {
     const void* k;
     size_t smem;
@@ -384,13 +385,13 @@ static bool pairs_fit(Kern kern, int grid, int threads, size_t smem) {
   static std::mutex mu;   // contexts on several host threads
   std::lock_guard<std::mutex> lock(mu);
   for (int i = 0; i < ncache; ++i)
-    if (cache[i].k == (const void*)kern && cache[i].smem == smem && cache[i].grid == grid) return 2 * cache[i].max >= grid;
+    if (cache[i].k == (const void*)kern && cache[i].smem == smem && cache[i].grid == grid) return cl * cache[i].max >= grid;
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid), cfg.blockDim = dim3(threads), cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+    at[0].val.clusterDim.x = cl, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
     cfg.attrs = at, cfg.numAttrs = 1;
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
@@ -398,19 +399,19 @@ static bool pairs_fit(Kern kern, int grid, int threads, size_t smem) {
       n = 0;
     }
     cache[ncache < 4 ? ncache++ : 3] = Entry{(const void*)kern, smem, grid, n};
-    if (getenv("DI_DEBUG_MC")) fprintf(stderr, "conv2 pairs: %d co-resident clusters of 2 (grid %d)\n", n, grid);
-    return 2 * n >= grid;
+    if (getenv("DI_DEBUG_MC")) fprintf(stderr, "conv2: %d co-resident clusters of %d (grid %d)\n", n, cl, grid);
+    return cl * n >= grid;
   }
 }
 template <typename... Args>
 static cudaError_t launch_pair(void (*kern)(Args...), int grid, int threads, size_t smem, cudaStream_t st,
                                const CUtensorMap& tm, const __nv_bfloat16* w, const float* bias, int fullmap, Geo g,
-                               __nv_bfloat16* out, const __nv_bfloat16* mask) {
+                               __nv_bfloat16* out, const __nv_bfloat16* mask, int cl = 2) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid), cfg.blockDim = dim3(threads), cfg.dynamicSmemBytes = smem, cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+  at[0].val.clusterDim.x = cl, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
   cfg.attrs = at, cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, tm, w, bias, fullmap, g, out, mask);
 }
@@ -444,25 +445,34 @@ cudaError_t setup_conv2_tc(int n2) {
   cudaError_t e = cudaFuncSetAttribute(k_conv2_tc<64, 32, C2_BIAS_RELU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)conv2_tc_smem_bytes(n2));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(k_conv2_tc<64, 32, C2_BIAS_RELU, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)conv2_tc_smem_bytes(n2));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_conv2_tc<32, 64, C2_MASK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(k_conv2_tc<64, 32, C2_BIAS_RELU, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)conv2_tc_smem_bytes(n2));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_conv2_tc<32, 64, C2_MASK, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)dgrad2_bf16_smem_bytes(n2));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_conv2_tc<32, 64, C2_MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)dgrad2_bf16_smem_bytes(n2));
 }
 
-// allow_mc = false (the context's DI_EXP_NO_MC setting, read once by di_create) forces the one-CTA weight stream
+// cluster: weight-multicast cluster size (the context's setting, read once by di_create: 2 by default, DI_EXP_NO_MC=1
+// -> 1, DI_EXP_C2_CLUSTER=4 -> 4); falls back to smaller clusters when the balance / co-residency checks fail
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
-                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, bool allow_mc) {
+                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, int cluster) {
   Geo g = make_geo(batch, n1, n2);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  if (allow_mc && pair_balanced(g, grid, R) && pairs_fit(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, grid, 256, conv2_tc_smem_bytes(n2)))
-    return launch_pair(k_conv2_tc<64, 32, C2_BIAS_RELU, true>, grid, 256, conv2_tc_smem_bytes(n2), st, *tmH1,
-                       reinterpret_cast<const __nv_bfloat16*>(wpack), bias, fullmap, g,
-                       reinterpret_cast<__nv_bfloat16*>(h2), (const __nv_bfloat16*)nullptr);
+  const size_t sm = conv2_tc_smem_bytes(n2);
+  const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(wpack);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(h2);
+  if (cluster >= 4 && pair_balanced(g, grid, R, 4) && pairs_fit(k_conv2_tc<64, 32, C2_BIAS_RELU, 4>, grid, 256, sm, 4))
+    return launch_pair(k_conv2_tc<64, 32, C2_BIAS_RELU, 4>, grid, 256, sm, st, *tmH1, w, bias, fullmap, g, out,
+                       (const __nv_bfloat16*)nullptr, 4);
+  if (cluster >= 2 && pair_balanced(g, grid, R) && pairs_fit(k_conv2_tc<64, 32, C2_BIAS_RELU, 2>, grid, 256, sm))
+    return launch_pair(k_conv2_tc<64, 32, C2_BIAS_RELU, 2>, grid, 256, sm, st, *tmH1, w, bias, fullmap, g, out,
+                       (const __nv_bfloat16*)nullptr);
   k_conv2_tc<64, 32, C2_BIAS_RELU><<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(
       *tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias, fullmap, g, reinterpret_cast<__nv_bfloat16*>(h2),
       nullptr);
@@ -521,8 +531,8 @@ cudaError_t launch_dgrad2_bf16(const CUtensorMap* tmDGb, const void* wpack, cons
   Geo g = make_geo(batch, n1, n2, C2_DG_ROWS);
   const int grid = g.units < num_sms ? g.units : num_sms;
   if (pair_balanced(g, grid, C2_DG_ROWS) &&
-      pairs_fit(k_conv2_tc<32, 64, C2_MASK, true>, grid, 384, dgrad2_bf16_smem_bytes(n2)))
-    return launch_pair(k_conv2_tc<32, 64, C2_MASK, true>, grid, 384, dgrad2_bf16_smem_bytes(n2), st, *tmDGb,
+      pairs_fit(k_conv2_tc<32, 64, C2_MASK, 2>, grid, 384, dgrad2_bf16_smem_bytes(n2)))
+    return launch_pair(k_conv2_tc<32, 64, C2_MASK, 2>, grid, 384, dgrad2_bf16_smem_bytes(n2), st, *tmDGb,
                        reinterpret_cast<const __nv_bfloat16*>(wpack), nullptr, 0, g,
                        reinterpret_cast<__nv_bfloat16*>(dh1b), reinterpret_cast<const __nv_bfloat16*>(h1b));
   k_conv2_tc<32, 64, C2_MASK><<<grid, 384, dgrad2_bf16_smem_bytes(n2), st>>>(

@@ -135,6 +135,9 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t idesc = idesc_f32acc(1, 128, g.N);
       const uint64_t adesc0 = smem_desc(smem_u32(tb), 16, 512, kSwizzle64B);
       const uint64_t bdesc0 = smem_desc(smem_u32(ring), 16, 512, kSwizzle64B);
+      const uint64_t rstep = (uint64_t)((P * 64) >> 4);                  // one strip row
+      const uint64_t padstep = (uint64_t)((slot - chunk_bytes) >> 4);     // slot padding after a slot's last row
+      const uint64_t ringstep = (uint64_t)((NCH * slot) >> 4);           // the whole ring
       uint32_t gc0 = 0;                // this item's first chunk (CTA-wide count)
       int pi = 0;
       for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
@@ -154,16 +157,21 @@ __global__ void __launch_bounds__(256, 1)
             tc_fence_after();
           }
           const uint32_t d = tmem + a * 128;
-          const int row0 = (int)(cj % NCH) * CH;              // ring row of the unit's strip row 0
+          const int sl0 = (int)(cj % NCH);                     // slot of the unit's strip row 0
           // a window reads N - P positions past its row: the last slot's last row runs into the zero guard
           DI_DEVICE_ASSERT(g.N - g.P <= GUARD, g.N, g.P);
-#pragma unroll 2
+          // the single issuing thread is latency-bound: the B descriptor advances by adds only (one strip row per
+          // window, the slot padding every CH rows, back to slot 0 after the last slot)
+          uint64_t bd = bdesc0 + (uint64_t)((sl0 * slot) >> 4);
+          const int kwrap = (NCH - sl0) * CH - 1;               // last window before the ring wraps
+#pragma unroll
           for (int k = 0; k < NWIN; ++k) {
-            const int rr = (row0 + k) & (RING_ROWS - 1);      // ring row: slot rr / CH, row rr % CH of the slot
-            const uint64_t bd = bdesc0 + (uint64_t)(((rr / CH) * slot + (rr % CH) * P * 64) >> 4);
             const uint64_t ad = adesc0 + (uint64_t)(((10 - k - IMIN) * TBLK) >> 4);   // T[10 - k] ..
             umma_f16_ss(d, ad, bd, idesc, k != 0);
             umma_f16_ss(d, ad + 2, bd + 2, idesc, 1);                       // channels 16..31: +32 B
+            bd += rstep;
+            if ((k % CH) == CH - 1) bd += padstep;
+            if (k == kwrap) bd -= ringstep;
           }
           umma_commit(&acc_full[a]);
           umma_commit(&cempty[cj % NCH]);                     // chunk j is read by units j - 2 .. j only

@@ -157,6 +157,10 @@ def test_weight_multicast_and_tile_width_are_bitwise_neutral(monkeypatch):
     nomc = ctx_nomc.recover(y).cpu().numpy()
     assert np.array_equal(mc, nomc), "weight multicast changed the result"
     assert np.array_equal(ctx.recover(y).cpu().numpy(), mc), "the setting is per context"
+    monkeypatch.setenv("DI_EXP_C2_CLUSTER", "4")
+    ctx4 = make_ctx(case, max_batch=256)
+    monkeypatch.delenv("DI_EXP_C2_CLUSTER")
+    assert np.array_equal(ctx4.recover(y).cpu().numpy(), mc), "4-CTA weight multicast changed the result"
     big = make_ctx(case, max_batch=4096)
     assert np.array_equal(big.recover(y).cpu().numpy(), mc), "proxy tile width changed the result"
 
