@@ -145,6 +145,8 @@ struct di_ctx_s {
   long long ws_bytes = 0;
   CUtensorMap tmPt{}, tmH1{}, tmH2{}, tmX{};
   CUtensorMap tmH1s{};          // BF16, n2 % 64 == 0: conv1's TMA store map over h1 (encode_h1_store)
+  CUtensorMap tmPh{};           // BF16, proxy_pair: Phi^T blocks with half-block boxes (k_proxy_pair)
+  bool proxy_pair = false;      // the lifting GEMM on CTA pairs (cta_group::2, k_proxy_pair)
   bool has_tmX = false;
   int last_launches = 0;
   bool profiling = false;
@@ -172,13 +174,15 @@ di_status encode_2d(CUtensorMap* map, const void* base, bool bf16, int inner, in
 }
 
 // the tile-blocked Phi^T (di::phiT_blk_index) as [blocks][256 rows][kel]: box = one contiguous 32-KB block
-di_status encode_phiT_blk(CUtensorMap* map, const void* base, bool bf16, long long N, int kpad, int tr) {
+// box_rows: tr (k_proxy_tc: one whole block) or tr / 2 (k_proxy_pair: each CTA of a pair loads half of a block)
+di_status encode_phiT_blk(CUtensorMap* map, const void* base, bool bf16, long long N, int kpad, int tr,
+                          int box_rows = 0) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   const int e = bf16 ? 2 : 4, kel = 128 / e;
   cuuint64_t dims[3] = {(cuuint64_t)kel, (cuuint64_t)tr, (cuuint64_t)((N + tr - 1) / tr) * (cuuint64_t)(kpad / kel)};
   cuuint64_t strides[2] = {128, (cuuint64_t)tr * 128};
-  cuuint32_t box[3] = {(cuuint32_t)kel, (cuuint32_t)tr, 1};
+  cuuint32_t box[3] = {(cuuint32_t)kel, (cuuint32_t)(box_rows ? box_rows : tr), 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                    const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -586,8 +590,11 @@ di_status run_proxy(di_ctx c, const void* y, long long ldy, int batch, void* xt,
     CUtensorMap tmY;
     di_status s = encode_2d(&tmY, ysrc, bf16, inner, batch, ld, 128 / (int)c->elt, 128);
     if (s != DI_OK) return s;
-    CUDA_TRY(di::launch_proxy_tc(&tmY, &c->tmPt, batch, c->N, c->kpad / (128 / (int)c->elt), xt, !bf16, st, out_f32,
-                                 sc, true, c->pxbn));
+    if (c->proxy_pair && bf16 && !out_f32 && !sc)
+      CUDA_TRY(di::launch_proxy_pair(&tmY, &c->tmPh, batch, c->N, c->kpad / 64, xt, c->pxbn, st));
+    else
+      CUDA_TRY(di::launch_proxy_tc(&tmY, &c->tmPt, batch, c->N, c->kpad / (128 / (int)c->elt), xt, !bf16, st,
+                                   out_f32, sc, true, c->pxbn));
     ++launches;
   }
   return DI_OK;
@@ -960,6 +967,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       long long dummy = 0;
       STEP(upload(&tmp, phisrc, (size_t)a->m * N * 4, &dummy));
       c->pxbn = di::proxy_tile_width(N, a->max_batch, bf16, c->num_sms);
+      c->proxy_pair = bf16 && getenv("DI_EXP_PROXY_PAIR") != nullptr;   // A/B switch, read once
       const size_t bytes = di::phiT_blk_elems(N, c->kpad, c->pxbn) * c->elt;   // tile-blocked, zero rows past N
       cudaError_t e = cudaMalloc(&c->phi, bytes);
       if (e == cudaSuccess) e = cudaMemset(c->phi, 0, bytes);
@@ -1134,11 +1142,13 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   }
   if (c->prec != DI_PREC_FP32) {
     cudaError_t e = di::setup_proxy_tc();
+    if (e == cudaSuccess) e = di::setup_proxy_pair();
     if (e != cudaSuccess) {
       free_ctx(c);
       return fail(DI_ERR_CUDA, "setup_proxy_tc: %s", cudaGetErrorString(e));
     }
     STEP(encode_phiT_blk(&c->tmPt, c->phi, bf16, N, c->kpad, c->pxbn));
+    if (c->proxy_pair) STEP(encode_phiT_blk(&c->tmPh, c->phi, bf16, N, c->kpad, c->pxbn, c->pxbn / 2));
   }
   if (bf16) {
     cudaError_t e = di::setup_conv2_tc(a->n2);

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "kernels.cuh"
 #define DI_TU_ID 4
@@ -140,20 +141,28 @@ __global__ void __launch_bounds__(256, 1)
       const uint64_t ringstep = (uint64_t)((NCH * slot) >> 4);           // the whole ring
       uint32_t gc0 = 0;                // this item's first chunk (CTA-wide count)
       int pi = 0;
+#ifdef DI_PROF_CONV3
+      long long pc_chunk = 0, pc_acc = 0, pc0 = clock64(), pt;
+#define C3P0 pt = clock64();
+#define C3P1(acc) acc += clock64() - pt;
+#else
+#define C3P0
+#define C3P1(acc)
+#endif
       for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
         int b, c0, rb0, nu;
         item_of(g, it, b, c0, rb0, nu);
         for (int k = 0; k < 2; ++k) {   // the item's first two chunks
           const uint32_t c = gc0 + k;
-          mbar_wait(&cfull[c % NCH], (c / NCH) & 1);
+          C3P0 mbar_wait(&cfull[c % NCH], (c / NCH) & 1); C3P1(pc_chunk)
         }
         for (int j = 0; j < nu; ++j, ++pi) {
           const uint32_t cj = gc0 + j;
-          mbar_wait(&cfull[(cj + 2) % NCH], ((cj + 2) / NCH) & 1);
+          C3P0 mbar_wait(&cfull[(cj + 2) % NCH], ((cj + 2) / NCH) & 1); C3P1(pc_chunk)
           tc_fence_after();
           const int a = pi % NACC;
           if (pi >= NACC) {
-            mbar_wait(&acc_empty[a], ((pi / NACC) - 1) & 1);
+            C3P0 mbar_wait(&acc_empty[a], ((pi / NACC) - 1) & 1); C3P1(pc_acc)
             tc_fence_after();
           }
           const uint32_t d = tmem + a * 128;
@@ -180,6 +189,11 @@ __global__ void __launch_bounds__(256, 1)
         umma_commit(&cempty[(gc0 + nu + 1) % NCH]);
         gc0 += nu + 2;
       }
+#ifdef DI_PROF_CONV3
+      if (blockIdx.x % 37 == 0)
+        printf("conv3 cta %d issuer: cycles %lld chunk-wait %lld acc-wait %lld units %d\n", blockIdx.x,
+               clock64() - pc0, pc_chunk, pc_acc, pi);
+#endif
     }
   } else if (warp >= 4) {  // ------------------------------- epilogue: warp q = output rows RPW q .. RPW q + RPW - 1
     const int q = warp - 4;

@@ -22,6 +22,7 @@ namespace {
 constexpr int PX_BM = 128;      // images per tile (UMMA M)
 constexpr int PX_BN = 256;      // pixels per tile (UMMA N); BN = 224 for the lifting layer when it fills the waves better
 constexpr int PX_STAGES = 4;
+constexpr int PX2_STAGES = 4;   // k_proxy_pair: 4 x (16 KB + BN x 128 B)
 }  // namespace
 
 // ELT: 2 = bf16 (kind::f16, K=16 per MMA), 4 = fp32 storage with kind::tf32 (K=8 per MMA).
@@ -152,6 +153,148 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<256 * MB>(tmem);
+}
+
+// ============================================================================ lifting GEMM on CTA pairs (cta_group::2)
+// Large Phi (Stress: 2.15 GB, streamed from HBM once): a CTA pair computes a 256-image x 2 BN-pixel tile with
+// M = 256 UMMAs (cta_group::2): each CTA stages ITS 128 images of Y (16 KB per K-block) and HALF of each of the two
+// BN-row Phi^T blocks (BN / 2 rows each), the leader issues D[256][BN] += A[256][64] B[BN][64]^T for both pixel blocks
+// (two TMEM accumulators, 2 x 256 columns in each CTA: rows 0..127 in the leader, 128..255 in the peer).  Per K-block
+// an SM ingests 16 KB + BN x 128 B for 2 x 4 M=128-equivalent MMAs of N = BN, against 32 KB + BN x 128 B for the same
+// MMA time with one CTA owning both batch tiles (k_proxy_tc MB = 2): the Y traffic per SM halves.
+// Pipeline: full[s] lives in the leader (expect_tx of both CTAs' bytes, armed by the leader's producer; the peer's
+// loads complete on it through the cluster window), empty[s] / tfull in both CTAs (multicast commits).
+template <int BN>
+__global__ void __launch_bounds__(128, 1)
+    k_proxy_pair(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmPh, int batch, int N,
+                 int kblocks, __nv_bfloat16* __restrict__ xt) {
+  constexpr uint32_t A_BYTES = 128 * 128, BH_BYTES = (BN / 2) * 128;   // per CTA: 128 images; BN/2 rows per block
+  constexpr uint32_t STAGE = A_BYTES + 2 * BH_BYTES;
+  constexpr int NST = PX2_STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[NST], empty[NST], tfull;
+  __shared__ uint32_t tslot;
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int nbt = (batch + 255) / 256;
+  const int bt = pair % nbt, pt = pair / nbt;            // consecutive pairs share one Phi^T slice (L2)
+  const int b0 = bt * 256 + (int)rank * 128;             // this CTA's 128 images
+  const int blk0 = 2 * pt;                               // the pair's two BN-pixel Phi^T blocks
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmY);
+    tma_prefetch_desc(&tmPh);
+    for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    mbar_init(&tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair<512>(&tslot), tmem_relinquish_pair();
+  tc_fence_before();
+  cluster_sync_all();   // both CTAs' barriers initialised and TMEM allocated before any remote arrive / MMA
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0 && lane == 0) {  // ---------------- TMA producer (both CTAs)
+    const int nblk = (N + BN - 1) / BN;
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % NST;
+      if (kb >= NST) mbar_wait(&empty[s], ((kb / NST) - 1) & 1);
+      uint8_t* sa = smem + s * STAGE;
+      const uint32_t fbar = mapa_shared(&full[s], 0);
+      if (rank == 0) mbar_arrive_expect_tx_cluster(fbar, 2 * STAGE);
+      tma_load_2d_pair(sa, &tmY, fbar, kb * 64, b0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int blk = min(blk0 + h, nblk - 1);   // a missing second block re-reads the first (outputs discarded)
+        tma_load_3d_pair(sa + A_BYTES + h * BH_BYTES, &tmPh, fbar, 0, (int)rank * (BN / 2), blk * kblocks + kb);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader)
+    constexpr uint32_t idesc = idesc_f32acc(1, 256, BN);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % NST;
+      mbar_wait(&full[s], (kb / NST) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * STAGE);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t ad = smem_desc(sa + k * 32, 16, 1024, kSwizzle128B);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint64_t bd = smem_desc(sa + A_BYTES + h * BH_BYTES + k * 32, 16, 1024, kSwizzle128B);
+          umma_f16_ss_pair(tmem + h * 256, ad, bd, idesc, (kb | k) != 0);
+        }
+      }
+      umma_commit_pair(&empty[s], 0x3);
+    }
+    umma_commit_pair(&tfull, 0x3);
+  }
+  __syncwarp();
+  // ---------------- epilogue: each CTA's 4 warps, warp w = TMEM lanes 32w.. = images b0 + 32w + lane
+  mbar_wait(&tfull, 0);
+  tc_fence_after();
+  const int b = b0 + warp * 32 + lane;
+  const bool vec_ok = (N % 8) == 0;
+  for (int hc = 0; hc < 2 * BN; hc += 32) {
+    const int h = hc / BN, c = hc % BN;
+    uint32_t r[32];
+    tmem_ld32(tmem + h * 256 + ((uint32_t)(warp * 32) << 16) + c, r);
+    tmem_ld_wait();
+    const int col = (blk0 + h) * BN + c;
+    if (b >= batch || col >= N) continue;
+    __nv_bfloat16* dst = xt + (size_t)b * N + col;
+    if (vec_ok && col + 32 <= N) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 v;
+        v.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1]));
+        v.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3]));
+        v.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5]));
+        v.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7]));
+        reinterpret_cast<uint4*>(dst)[q] = v;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col + j < N) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();   // the peer's epilogue is done with its TMEM columns too
+  if (warp == 2) tmem_dealloc_pair<512>(tmem);
+}
+
+template <int BN>
+static size_t px2_smem() { return (size_t)PX2_STAGES * (128 * 128 + BN * 128) + 1024; }
+
+cudaError_t setup_proxy_pair() {
+  cudaError_t e = cudaFuncSetAttribute(k_proxy_pair<224>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)px2_smem<224>());
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_proxy_pair<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)px2_smem<256>());
+}
+
+// tmPh: tile-blocked Phi^T with a box of BN / 2 rows (encode_phiT_blk(..., half = true)); bn = the block width
+cudaError_t launch_proxy_pair(const CUtensorMap* tmY, const CUtensorMap* tmPh, int batch, int N, int kblocks, void* xt,
+                              int bn, cudaStream_t st) {
+  const int nbt = (batch + 255) / 256, npt = (N + 2 * bn - 1) / (2 * bn);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * nbt * npt), cfg.blockDim = dim3(128), cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+  cfg.attrs = at, cfg.numAttrs = 1;
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(xt);
+  if (bn == 224) {
+    cfg.dynamicSmemBytes = px2_smem<224>();
+    return cudaLaunchKernelEx(&cfg, k_proxy_pair<224>, *tmY, *tmPh, batch, N, kblocks, out);
+  }
+  if (bn != 256) return cudaErrorInvalidValue;
+  cfg.dynamicSmemBytes = px2_smem<256>();
+  return cudaLaunchKernelEx(&cfg, k_proxy_pair<256>, *tmY, *tmPh, batch, N, kblocks, out);
 }
 
 size_t proxy_tc_smem_bytes() { return (size_t)PX_STAGES * (PX_BM + PX_BN) * 128 + 1024; }

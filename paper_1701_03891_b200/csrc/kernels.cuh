@@ -44,6 +44,10 @@ cudaError_t launch_proxy_tc(const CUtensorMap* tmY, const CUtensorMap* tmPt, int
                             const ProxyScatter* sc = nullptr, bool b_blocked = false, int bn = 256);
 // pixel-tile width of the lifting GEMM (256, or 224 when that fills the SM waves better for max_batch)
 int proxy_tile_width(long long N, int max_batch, bool bf16, int num_sms);
+// the lifting GEMM on CTA pairs (cta_group::2, M = 256 images): bf16 x_tilde; tmPh = half-block Phi^T boxes
+cudaError_t setup_proxy_pair();
+cudaError_t launch_proxy_pair(const CUtensorMap* tmY, const CUtensorMap* tmPh, int batch, int N, int kblocks, void* xt,
+                              int bn, cudaStream_t st);
 // Tile-blocked Phi^T (BF16 / TF32 contexts): element (pixel j, measurement i) of [N-tile j / tr][K-block i / kel]
 // [j % tr][i % kel], kel = 128 B / element size, tr = the GEMM's pixel-tile width; one (N-tile, K-block) block is
 // the tr x 128 B the proxy GEMM stages per K-block, contiguous in HBM (full DRAM pages instead of tr strided 128-B

@@ -379,3 +379,30 @@ def test_inference_time_flat_across_measurement_rate():
         times[m] = float(np.median(ts))
         ctx.close()
     assert max(times.values()) <= 1.15 * min(times.values()), times
+
+
+@pytest.mark.parametrize("n,m,batch", [(128, 4096, 512), (96, 2000, 300), (64, 410, 256)])
+def test_proxy_on_cta_pairs(monkeypatch, n, m, batch):
+    """The lifting GEMM on CTA pairs (k_proxy_pair: cta_group::2, M = 256 images over two SMs, two BN-pixel
+    accumulators per CTA) against the oracle's x_tilde = Phi^T y element by element (stage 0 hook,
+    bound from the arithmetic as in test_gpu_elementwise.py) and against the one-CTA kernel.  Ragged batch (300 = one
+    full and one partial 256-image pair tile) and an N that is not a multiple of the pair's 2 x BN pixels."""
+    import torch
+    case = Case(n, n, m, batch, "bf16", 6, 3)
+    monkeypatch.setenv("DI_EXP_PROXY_PAIR", "1")
+    ctx = make_ctx(case)
+    monkeypatch.delenv("DI_EXP_PROXY_PAIR")
+    ref_ctx = make_ctx(case)
+    y = y_device(case, ctx)
+    outs = []
+    for c in (ctx, ref_ctx):
+        xt = torch.empty((batch, n, n), dtype=torch.bfloat16, device="cuda")
+        c.debug_stage(0, y, xt, batch)
+        torch.cuda.synchronize()
+        outs.append(xt.float().cpu().numpy().astype(np.float64))
+    rows = sample_rows(batch, 6)
+    ref = oracle.proxy(case.phi, case.y[rows]).reshape(len(rows), n, n)
+    S = oracle.proxy(np.abs(case.phi), np.abs(case.y[rows])).reshape(len(rows), n, n)
+    err = np.abs(outs[0][rows] - ref)
+    assert np.all(err <= 2.0 ** -8 * np.abs(ref) + 2.0 ** -14 * S), float(err.max())
+    assert np.array_equal(outs[0], outs[1]), "pair kernel differs from the one-CTA kernel"
