@@ -967,7 +967,10 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       long long dummy = 0;
       STEP(upload(&tmp, phisrc, (size_t)a->m * N * 4, &dummy));
       c->pxbn = di::proxy_tile_width(N, a->max_batch, bf16, c->num_sms);
-      c->proxy_pair = bf16 && getenv("DI_EXP_PROXY_PAIR") != nullptr;   // A/B switch, read once
+      // CTA pairs when Phi is large enough to stream from HBM (N >= 16384: Larger, Stress) and the batch fills the
+      // 256-image pair tile; DI_EXP_PROXY_PAIR=0/1 at di_create overrides (A/B runs)
+      c->proxy_pair = bf16 && N >= 16384 && a->max_batch >= 256;
+      if (const char* ev = getenv("DI_EXP_PROXY_PAIR")) c->proxy_pair = bf16 && atoi(ev) != 0;
       const size_t bytes = di::phiT_blk_elems(N, c->kpad, c->pxbn) * c->elt;   // tile-blocked, zero rows past N
       cudaError_t e = cudaMalloc(&c->phi, bytes);
       if (e == cudaSuccess) e = cudaMemset(c->phi, 0, bytes);

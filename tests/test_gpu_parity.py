@@ -391,8 +391,9 @@ def test_proxy_on_cta_pairs(monkeypatch, n, m, batch):
     case = Case(n, n, m, batch, "bf16", 6, 3)
     monkeypatch.setenv("DI_EXP_PROXY_PAIR", "1")
     ctx = make_ctx(case)
-    monkeypatch.delenv("DI_EXP_PROXY_PAIR")
+    monkeypatch.setenv("DI_EXP_PROXY_PAIR", "0")
     ref_ctx = make_ctx(case)
+    monkeypatch.delenv("DI_EXP_PROXY_PAIR")
     y = y_device(case, ctx)
     outs = []
     for c in (ctx, ref_ctx):
