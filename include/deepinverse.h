@@ -158,6 +158,14 @@ di_status di_measure(di_ctx ctx, const float* x, int batch, void* y, long long l
 di_status di_add_noise(di_ctx ctx, void* y, long long ldy, int batch, double snr_db, unsigned long long seed,
                        void* stream);
 di_status di_metrics(di_ctx ctx, const float* xhat, const float* x, int batch, double* out, void* stream);
+/* di_recover_metrics: di_recover followed by di_metrics on the same batch (the Monte-Carlo loop of PAPER.md:159-160,
+ *               Figs. 2-4), with the metrics FUSED into conv layer 3's epilogue on the BF16 path (each output is compared
+ *               with x_true as it is written; per-item fp64 partials combined in a fixed order, so the result is
+ *               deterministic) and computed by the separate di_metrics pass otherwise.  y, ldy, batch, xhat: as
+ *               di_recover; x_true: DEVICE [batch][n1][n2] fp32 ground truth; metrics: DEVICE [3][batch] double as
+ *               di_metrics.  Errors as di_recover; DI_ERR_ARG if x_true or metrics is NULL. */
+di_status di_recover_metrics(di_ctx ctx, const void* y, long long ldy, int batch, const float* x_true, float* xhat,
+                             double* metrics, void* stream);
 
 /* ---- Training step (contexts of the paper's stack with per-channel or zero biases) ----------
  * FP32 contexts: SIMT forward and backward (fp32 products).  TF32 contexts: TF32 tensor-core forward; backward on the

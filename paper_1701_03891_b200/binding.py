@@ -25,7 +25,7 @@ PRECISIONS = {"f32": DI_PREC_FP32, "tf32": DI_PREC_TF32, "bf16": DI_PREC_BF16}
 # every symbol include/deepinverse.h declares (checked by tests/test_abi.py)
 EXPORTS = ["di_create", "di_recover", "di_recover_host", "di_destroy", "di_status_string", "di_last_error",
            "di_get_info", "di_set_profiling", "di_stage_times", "di_debug_stage", "di_debug_get_phi",
-           "di_measure", "di_add_noise", "di_metrics", "di_num_params", "di_train_grad", "di_sgd_step",
+           "di_measure", "di_add_noise", "di_metrics", "di_recover_metrics", "di_num_params", "di_train_grad", "di_sgd_step",
            "di_get_params", "di_proxy_partial", "di_recover_from_proxy", "di_proxy_scatter", "di_recover_from_slots"]
 
 
@@ -90,6 +90,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.di_measure.argtypes = [V, V, I, V, LL, V]
     lib.di_add_noise.argtypes = [V, V, LL, I, ctypes.c_double, ctypes.c_ulonglong, V]
     lib.di_metrics.argtypes = [V, V, V, I, V, V]
+    lib.di_recover_metrics.argtypes = [V, V, LL, I, V, V, V, V]
     lib.di_num_params.argtypes = []
     lib.di_num_params.restype = LL
     lib.di_train_grad.argtypes = [V, V, LL, V, I, ctypes.c_double, V, V, V]
@@ -100,7 +101,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.di_proxy_scatter.argtypes = [V, V, LL, I, V, I, I, V]
     lib.di_recover_from_slots.argtypes = [V, V, I, I, V, V]
     for f in ("di_create", "di_recover", "di_recover_host", "di_destroy", "di_get_info", "di_set_profiling",
-              "di_stage_times", "di_debug_stage", "di_debug_get_phi", "di_measure", "di_add_noise", "di_metrics",
+              "di_stage_times", "di_debug_stage", "di_debug_get_phi", "di_measure", "di_add_noise", "di_metrics", "di_recover_metrics",
               "di_train_grad", "di_sgd_step", "di_get_params", "di_proxy_partial", "di_recover_from_proxy", "di_proxy_scatter",
               "di_recover_from_slots"):
         getattr(lib, f).restype = I
@@ -195,6 +196,11 @@ def di_add_noise(ctx, y, ldy: int, batch: int, snr_db: float, seed: int, stream=
 
 def di_metrics(ctx, xhat, x, batch: int, out, stream=None):
     _check(load().di_metrics(ctx, _ptr(xhat), _ptr(x), batch, _ptr(out), _stream_handle(stream)), "di_metrics")
+
+
+def di_recover_metrics(ctx, y, ldy: int, batch: int, x_true, xhat, metrics, stream=None):
+    _check(load().di_recover_metrics(ctx, _ptr(y), ldy, batch, _ptr(x_true), _ptr(xhat), _ptr(metrics),
+                                     _stream_handle(stream)), "di_recover_metrics")
 
 
 def di_num_params() -> int:
@@ -395,6 +401,20 @@ class DeepInverse:
         out = torch.empty((3, b), dtype=torch.float64, device=x.device)
         di_metrics(self.ctx, xhat, x, b, out, self._stream(stream))
         return out.cpu().numpy()
+
+    def recover_metrics(self, y, x, xhat=None, stream=None):
+        """x_hat = M(y) and, per image, PSNR / NMSE / success against the ground truth x (device fp32 [B][n1][n2]);
+        fused into conv layer 3's epilogue on the BF16 path.  Returns (x_hat device tensor, metrics numpy [3][B])."""
+        import torch
+        self._check_y(y)
+        b = y.shape[0]
+        self._check_out(x, (b, self.n1, self.n2), "x")
+        if xhat is None:
+            xhat = torch.empty((b, self.n1, self.n2), dtype=torch.float32, device=y.device)
+        self._check_out(xhat, (b, self.n1, self.n2), "xhat")
+        out = torch.empty((3, b), dtype=torch.float64, device=y.device)
+        di_recover_metrics(self.ctx, y, y.stride(0), b, x, xhat, out, self._stream(stream))
+        return xhat, out.cpu().numpy()
 
     # ------------------------------------------------------------ training (NEXT-2; paper stack, per-channel biases)
     def train_grad(self, y, x, scale=None, grads=None, stream=None):

@@ -147,6 +147,10 @@ struct di_ctx_s {
   CUtensorMap tmH1s{};          // BF16, n2 % 64 == 0: conv1's TMA store map over h1 (encode_h1_store)
   CUtensorMap tmPh{};           // BF16, proxy_pair: Phi^T blocks with half-block boxes (k_proxy_pair)
   bool proxy_pair = false;      // the lifting GEMM on CTA pairs (cta_group::2, k_proxy_pair)
+  // di_recover_metrics: set for the duration of one call (the bf16 conv3 epilogue fuses the metrics)
+  const float* m_xtrue = nullptr;
+  double* m_out = nullptr;
+  double* mpart = nullptr;      // per-item metric partials of k_conv3_r4 (allocated on first use, max_batch)
   bool has_tmX = false;
   int last_launches = 0;
   bool profiling = false;
@@ -550,7 +554,7 @@ void free_ctx(di_ctx c) {
   }
   for (auto p : c->act)
     if (p) cudaFree(p);
-  void* ps[] = {c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wpd3, c->wp2db, c->h1b, c->dg2b, c->dh1b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
+  void* ps[] = {c->mpart, c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wpd3, c->wp2db, c->h1b, c->dg2b, c->dh1b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
                 c->wt2, c->wt3, c->xh_ws, c->dxh, c->dh1, c->dh2, c->part_w, c->part_b, c->loss_img, c->phi_sense, c->b1, c->b2, c->b3, c->xt, c->h1, c->h2, c->ystage,
                 c->yhost_dev, c->xhost_dev};
   for (void* p : ps)
@@ -770,7 +774,8 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
         tmp = &tm;
       }
       if (bf16)
-        CUDA_TRY(di::launch_conv3_r4(tmp, c->wp3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, c->num_sms, st));
+        CUDA_TRY(di::launch_conv3_r4(tmp, c->wp3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, c->num_sms, st,
+                                     c->m_xtrue, c->mpart, c->m_out));
       else
         CUDA_TRY(di::launch_conv3_tc(tmp, c->wp3, c->b3, fm, relu3, xhat, batch, c->n1, c->n2, c->num_sms, true, st));
     } else {
@@ -1204,6 +1209,29 @@ di_status di_recover(di_ctx c, const void* y, long long ldy, int batch, float* x
   DevGuard dg_(c->device);
   if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   return run_stages(c, 0, 3, y, ldy, batch, c->xt, c->h1, c->h2, xhat, reinterpret_cast<cudaStream_t>(stream));
+}
+
+di_status di_recover_metrics(di_ctx c, const void* y, long long ldy, int batch, const float* x_true, float* xhat,
+                             double* metrics, void* stream) {
+  if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
+  if (!y || !xhat || !x_true || !metrics) return fail(DI_ERR_ARG, "y, x_true, xhat and metrics must be non-NULL");
+  if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
+  if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
+  DevGuard dg_(c->device);
+  if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool fused = c->prec == DI_PREC_BF16 && c->stack.empty();
+  if (fused) {
+    if (!c->mpart)
+      CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->mpart),
+                          di::conv3_r4_metrics_part_bytes(c->max_batch, c->n1, c->n2, c->num_sms)));
+    c->m_xtrue = x_true, c->m_out = metrics;
+  }
+  di_status s = run_stages(c, 0, 3, y, ldy, batch, c->xt, c->h1, c->h2, xhat, st);
+  c->m_xtrue = nullptr, c->m_out = nullptr;
+  if (s != DI_OK || fused) return s;
+  CUDA_TRY(di::launch_metrics(xhat, x_true, c->N, batch, metrics, st));   // other paths: the separate pass
+  return DI_OK;
 }
 
 di_status di_proxy_partial(di_ctx c, const void* y, long long ldy, int batch, float* xt_part, void* stream) {

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -67,9 +68,16 @@ __device__ __forceinline__ void item_of(const GeoR4& g, int it, int& b, int& c0,
 // traffic drops from 2.25x to 1.25x the h2 rows.  Window k of a unit reads ring row (8 (chunk j) + k) mod 32 plus
 // N - P positions past it (the next row, the slot padding or the zero guard); those positions only reach D columns
 // >= P, which no output reads.
+//
+// Fused metrics (di_recover_metrics): with xtrue != null each epilogue thread also reads the
+// ground truth of the outputs it writes and accumulates, in fp64 and a fixed order, sum (x_hat - x)^2, sum x^2 and
+// max x; per item the four warps' sums go to mpart[item][warp][3] (no atomics), and k_metrics_finish combines the
+// items of each image in item order: PSNR, NMSE and success without a second pass over
+// x_hat.
 __global__ void __launch_bounds__(256, 1)
     k_conv3_r4(const __grid_constant__ CUtensorMap tmH2, const uint8_t* __restrict__ tpack,
-               const float* __restrict__ bias, int fullmap, int relu, GeoR4 g, float* __restrict__ xhat) {
+               const float* __restrict__ bias, int fullmap, int relu, GeoR4 g, float* __restrict__ xhat,
+               const float* __restrict__ xtrue, double* __restrict__ mpart) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int P = g.P;
@@ -203,6 +211,8 @@ __global__ void __launch_bounds__(256, 1)
     for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
       int b, c0, rb0, nu;
       item_of(g, it, b, c0, rb0, nu);
+      double m_se = 0.0, m_sx = 0.0;
+      float m_mx = -INFINITY;
       for (int j = 0; j < nu; ++j, ++pi) {
         const int r0 = (rb0 + j) * R;
         const int a = pi % NACC;
@@ -237,9 +247,25 @@ __global__ void __launch_bounds__(256, 1)
             acc += (fullmap && bias) ? bias[pix % ((size_t)g.n1 * g.n2)] : bsc;
             if (relu) acc = fmaxf(acc, 0.f);
             xhat[pix] = acc;
+            if (xtrue) {
+              const float t = __ldg(xtrue + pix);
+              const double dd = (double)acc - (double)t;
+              m_se += dd * dd, m_sx += (double)t * (double)t, m_mx = fmaxf(m_mx, t);
+            }
           }
         }
         __syncwarp();
+      }
+      if (xtrue) {   // the warp's sums for this item, butterfly order fixed
+        for (int o = 16; o > 0; o >>= 1) {
+          m_se += __shfl_xor_sync(0xffffffffu, m_se, o);
+          m_sx += __shfl_xor_sync(0xffffffffu, m_sx, o);
+          m_mx = fmaxf(m_mx, __shfl_xor_sync(0xffffffffu, m_mx, o));
+        }
+        if (lane == 0) {
+          double* mp = mpart + ((size_t)it * 4 + q) * 3;
+          mp[0] = m_se, mp[1] = m_sx, mp[2] = (double)m_mx;
+        }
       }
     }
   }
@@ -279,12 +305,38 @@ cudaError_t setup_conv3_r4(int n2) {
   return cudaFuncSetAttribute(k_conv3_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r4(n2));
 }
 
+// per image b: the items b * per_img .. (b + 1) * per_img - 1, four warps each, summed in that order
+__global__ void k_metrics_finish(const double* __restrict__ mpart, int per_img, int N, int batch,
+                                 double* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  double se = 0.0, sx = 0.0, mx = -INFINITY;
+  const double* p = mpart + (size_t)b * per_img * 4 * 3;
+  for (int i = 0; i < per_img * 4; ++i) se += p[3 * i], sx += p[3 * i + 1], mx = fmax(mx, p[3 * i + 2]);
+  const double mse = se / N;
+  out[b] = mse == 0.0 ? INFINITY : 10.0 * log10(mx * mx / mse);
+  const double nmse = se / sx;
+  out[batch + b] = nmse;
+  out[2 * batch + b] = nmse <= 0.1 ? 1.0 : 0.0;
+}
+
+size_t conv3_r4_metrics_part_bytes(int batch, int n1, int n2, int num_sms) {
+  const GeoR4 g = make_geo_r4(batch, n1, n2, num_sms);
+  return (size_t)g.items * 4 * 3 * sizeof(double);
+}
+
 cudaError_t launch_conv3_r4(const CUtensorMap* tmH2, const void* tpack, const float* bias, int fullmap, int relu,
-                            float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st) {
+                            float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st, const float* xtrue,
+                            double* mpart, double* metrics) {
   GeoR4 g = make_geo_r4(batch, n1, n2, num_sms);
   const int grid = g.items < num_sms ? g.items : num_sms;
   k_conv3_r4<<<grid, 256, smem_r4(n2), st>>>(*tmH2, reinterpret_cast<const uint8_t*>(tpack), bias, fullmap, relu, g,
-                                            xhat);
+                                            xhat, xtrue, mpart);
+  if (xtrue) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_metrics_finish<<<(batch + 127) / 128, 128, 0, st>>>(mpart, g.ncs * g.splits, n1 * n2, batch, metrics);
+  }
   return cudaGetLastError();
 }
 

@@ -132,8 +132,12 @@ constexpr int C3R_NENT = C3R_NWIN + C3R_RP - 1;
 int conv3_r4_box_rows();
 int conv3_r4_tpack_bytes();
 cudaError_t setup_conv3_r4(int n2);
+// xtrue (optional, DEVICE [batch][n1][n2] fp32): metrics fused into the epilogue -> metrics [3][batch] (PSNR, NMSE,
+// success as di_metrics) through the per-item partial buffer mpart (conv3_r4_metrics_part_bytes)
 cudaError_t launch_conv3_r4(const CUtensorMap* tmH2, const void* tpack, const float* bias, int fullmap, int relu,
-                            float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st);
+                            float* xhat, int batch, int n1, int n2, int num_sms, cudaStream_t st,
+                            const float* xtrue = nullptr, double* mpart = nullptr, double* metrics = nullptr);
+size_t conv3_r4_metrics_part_bytes(int batch, int n1, int n2, int num_sms);
 int conv3_tc_box_cols(int n2);
 int conv3_tc_box_ch(bool tf32);
 cudaError_t launch_conv3_tc(const CUtensorMap* tmH2, const void* w3pack, const float* bias, int fullmap, int relu,

@@ -69,3 +69,25 @@ def test_metrics_match_oracle():
     # exact case: x_hat = x -> PSNR = inf, NMSE = 0, success = 1
     same = ctx.metrics(x, x)
     assert np.all(np.isinf(same[0])) and np.all(same[1] == 0) and np.all(same[2] == 1)
+
+
+@pytest.mark.parametrize("precision,n1,n2,batch", [("bf16", 64, 64, 300), ("bf16", 40, 130, 5), ("bf16", 9, 13, 3),
+                                                   ("bf16", 64, 64, 1), ("tf32", 32, 32, 6), ("f32", 16, 16, 4)])
+def test_recover_metrics_fused(precision, n1, n2, batch):
+    """di_recover_metrics: the metrics fused into conv layer 3's epilogue (BF16; items = whole image columns, several
+    column segments at n2 = 130, split columns at batch 1) equal the oracle's metrics of the GPU's own x_hat, the
+    x_hat is bitwise the di_recover result, and the result is bitwise repeatable (fixed-order reduction)."""
+    import torch
+    case = Case(n1, n2, max(1, n1 * n2 // 8), batch, precision, 6, 3)
+    ctx = make_ctx(case)
+    y = torch.from_numpy(case.y).cuda().to(ctx.storage_dtype)
+    x = torch.from_numpy(case.x).cuda()
+    xhat, got = ctx.recover_metrics(y, x)
+    xh = xhat.cpu().numpy()
+    assert np.array_equal(xh, ctx.recover(y).cpu().numpy())
+    for b in range(batch):
+        assert abs(got[0, b] - oracle.psnr(xh[b], case.x[b])) <= 1e-9
+        assert abs(got[1, b] - oracle.nmse(xh[b], case.x[b])) <= 1e-12 * max(1.0, got[1, b])
+        assert got[2, b] == oracle.success(xh[b], case.x[b])
+    _, again = ctx.recover_metrics(y, x)
+    assert np.array_equal(again, got)
