@@ -182,8 +182,16 @@ di_status di_recover_metrics(di_ctx ctx, const void* y, long long ldy, int batch
  *                Data-parallel training all-reduces `grads` across ranks (sum, with scale = 1/global batch) between
  *                di_train_grad and di_sgd_step.
  * di_sgd_step:   vel = momentum * vel + grads; params -= lr * vel; the kernels' weight layouts follow.
- * di_get_params: DEVICE copy of the current parameters. */
+ * di_get_params: DEVICE copy of the current parameters.
+ * Custom stacks (di_create_args.layers, NEXT-3; per-channel or zero biases, any precision): the same calls with the
+ *                parameter vector [W_0 | W_1 | ... | W_L-1 | b_0 | ... | b_L-1] (each W_l [cout][cin][11][11] in the
+ *                orientation given to di_create) of di_ctx_num_params(ctx) floats; forward on the context's kernels,
+ *                backward on SIMT fp32 weight / data gradient kernels per layer; in TF32 / BF16 contexts di_sgd_step
+ *                re-derives the tensor-core weight images on the host and synchronises `stream`.
+ * di_ctx_num_params: the length of the context's parameter vector (di_num_params() for the paper's stack), 0 for
+ *                contexts that cannot train (full-map biases) or ctx == NULL. */
 long long di_num_params(void);
+long long di_ctx_num_params(di_ctx ctx);
 di_status di_train_grad(di_ctx ctx, const void* y, long long ldy, const float* x_true, int batch, double scale,
                         float* grads, double* loss, void* stream);
 di_status di_sgd_step(di_ctx ctx, const float* grads, double lr, double momentum, void* stream);

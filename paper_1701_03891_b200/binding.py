@@ -25,7 +25,7 @@ PRECISIONS = {"f32": DI_PREC_FP32, "tf32": DI_PREC_TF32, "bf16": DI_PREC_BF16}
 # every symbol include/deepinverse.h declares (checked by tests/test_abi.py)
 EXPORTS = ["di_create", "di_recover", "di_recover_host", "di_destroy", "di_status_string", "di_last_error",
            "di_get_info", "di_set_profiling", "di_stage_times", "di_debug_stage", "di_debug_get_phi",
-           "di_measure", "di_add_noise", "di_metrics", "di_recover_metrics", "di_num_params", "di_train_grad", "di_sgd_step",
+           "di_measure", "di_add_noise", "di_metrics", "di_recover_metrics", "di_num_params", "di_ctx_num_params", "di_train_grad", "di_sgd_step",
            "di_get_params", "di_proxy_partial", "di_recover_from_proxy", "di_proxy_scatter", "di_recover_from_slots"]
 
 
@@ -93,6 +93,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.di_recover_metrics.argtypes = [V, V, LL, I, V, V, V, V]
     lib.di_num_params.argtypes = []
     lib.di_num_params.restype = LL
+    lib.di_ctx_num_params.argtypes = [V]
+    lib.di_ctx_num_params.restype = LL
     lib.di_train_grad.argtypes = [V, V, LL, V, I, ctypes.c_double, V, V, V]
     lib.di_sgd_step.argtypes = [V, V, ctypes.c_double, ctypes.c_double, V]
     lib.di_get_params.argtypes = [V, V, V]
@@ -253,6 +255,7 @@ class DeepInverse:
         if lift is not None and lift.shape != (phi.shape[1], phi.shape[0]):
             raise ValueError(f"lift must be [N][m] = {(phi.shape[1], phi.shape[0])}")
         widths = tuple(w.shape[0] for w in ws)
+        self.shapes = [tuple(w.shape) for w in ws]
         self.custom = len(ws) != 3 or widths != (64, 32, 1)
         if self.custom:
             if len(bs) < len(ws):
@@ -426,7 +429,7 @@ class DeepInverse:
             raise TypeError(f"y must be a CUDA {self.storage_dtype} tensor")
         b = y.shape[0]
         if grads is None:
-            grads = torch.empty(di_num_params(), dtype=torch.float32, device=y.device)
+            grads = torch.empty(self.num_params(), dtype=torch.float32, device=y.device)
         loss = torch.empty(1, dtype=torch.float64, device=y.device)
         di_train_grad(self.ctx, y, y.stride(0), x, b, 1.0 / b if scale is None else scale, grads, loss, self._stream(stream))
         return loss, grads
@@ -434,12 +437,20 @@ class DeepInverse:
     def sgd_step(self, grads, lr: float, momentum: float = 0.0, stream=None):
         di_sgd_step(self.ctx, grads, lr, momentum, self._stream(stream))
 
+    def num_params(self) -> int:
+        """Length of this context's parameter vector (include/deepinverse.h: di_ctx_num_params)."""
+        return int(load().di_ctx_num_params(self.ctx))
+
     def params(self, stream=None):
-        """Current parameters as numpy arrays ([W1, W2, W3], [b1, b2, b3]) in the orientation given at creation."""
+        """Current parameters as numpy arrays ([W_0, ...], [b_0, ...]) in the orientation given at creation."""
         import torch
-        p = torch.empty(di_num_params(), dtype=torch.float32, device=f"cuda:{self.device}")
+        p = torch.empty(self.num_params(), dtype=torch.float32, device=f"cuda:{self.device}")
         di_get_params(self.ctx, p, self._stream(stream))
-        return split_params(p.cpu().numpy())
+        return split_params(p.cpu().numpy(), self.shapes)
+
+    def split(self, flat):
+        """[W_0 | ... | W_L-1 | b_0 | ... | b_L-1] -> ([W_0, ...], [b_0, ...]) (views)."""
+        return split_params(np.asarray(flat), self.shapes)
 
     def debug_stage(self, stage: int, x_in, x_out, batch: int, stream=None):
         di_debug_stage(self.ctx, stage, x_in, x_out, batch, self._stream(stream))
@@ -482,12 +493,17 @@ class DeepInverse:
 PARAM_SHAPES = [(64, 1, 11, 11), (32, 64, 11, 11), (1, 32, 11, 11)]
 
 
-def split_params(flat):
-    """[W1 | W2 | W3 | b1 | b2 | b3] -> ([W1, W2, W3], [b1, b2, b3]) (views of `flat`)."""
+def split_params(flat, shapes=None):
+    """[W_0 | ... | W_L-1 | b_0 | ... | b_L-1] -> ([W_0, ...], [b_0, ...]) (views of `flat`); the paper's stack by
+    default."""
+    shapes = PARAM_SHAPES if shapes is None else shapes
     ws, o = [], 0
-    for sh in PARAM_SHAPES:
+    for sh in shapes:
         n = int(np.prod(sh))
         ws.append(flat[o:o + n].reshape(sh))
         o += n
-    bs = [flat[o:o + 64], flat[o + 64:o + 96], flat[o + 96:o + 97]]
+    bs = []
+    for sh in shapes:
+        bs.append(flat[o:o + sh[0]])
+        o += sh[0]
     return ws, bs

@@ -110,9 +110,15 @@ struct di_ctx_s {
     void* wp = nullptr;         // TF32: tensor-core image (conv1 / generic / conv3 layout by position)
     float* b = nullptr;
     CUtensorMap tm;             // TF32: strip map over this layer's input activation
+    size_t woff = 0, boff = 0;  // training: offsets of W_l / b_l in params ([W_0 .. W_L-1 | b_0 .. b_L-1])
+    float* wt = nullptr;        // training: backward bank [cout][a][b][cin] (rotated, transposed)
+    float* keep = nullptr;      // training: this layer's output, fp32 [max_batch][N][cout] (hidden layers)
   };
   std::vector<Layer> stack;     // empty: the paper's three layers (w1..b3)
   float* act[2] = {nullptr, nullptr};   // custom stack: ping-pong activations [max_batch][N][<= 64] fp32
+  long long nparams = 0;        // trainable contexts: parameters in `params` (di::N_PARAMS for the paper's stack)
+  float* keep_x = nullptr;      // custom-stack training, BF16: x_tilde as fp32
+  float *dA = nullptr, *dB = nullptr;   // custom-stack training: ping-pong data gradients [max_batch][N][<= 64] fp32
   float* wpd3 = nullptr;        // training, TF32 mode: layer-3 dgrad bank in the conv1 TF32 layout
   void* wp2db = nullptr;        // training, TF32 mode: layer-2 dgrad bf16 weight blocks (66 x 8 KB)
   CUtensorMap tmDG2s;           // training, TF32 mode: bf16 dG2 strips for the bf16 dgrad2 (box rows R + 10)
@@ -533,6 +539,30 @@ std::vector<uint16_t> convg_tc_pack(const std::vector<float>& wx, int cin, int c
 }
 
 // bias: per-channel [cout] or the window of the full map [cout][n1+10][n2+10] that S keeps, as [n1][n2][cout]
+// one layer of a custom stack in the layout of the kernel that runs it (di_create, and di_sgd_step's repack in TF32 /
+// BF16 contexts): FP32 SIMT [ci][a][b][co]; BF16 k_conv1_tc (64 bank rows) / k_conv2_tc<C_in, C_out> / k_conv3_r4;
+// TF32 k_conv1_tf32 / k_conv_tf32<C_in, C_out> / k_conv3_tc.  wx: cross-correlation taps [cout][cin][11][11].
+std::vector<uint8_t> pack_stack_layer(di_precision prec, int i, int L, const std::vector<float>& wx, int cin, int cout) {
+  auto bytes = [](const auto& v) {
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(v.data());
+    return std::vector<uint8_t>(p, p + v.size() * sizeof(v[0]));
+  };
+  if (prec == DI_PREC_FP32) return bytes(simt_layout(wx, cout, cin));
+  std::vector<float> w64;
+  if (i == 0) {   // the conv1 machinery: 64 bank rows, rows >= cout zero
+    w64.assign((size_t)64 * K * K, 0.f);
+    std::copy(wx.begin(), wx.end(), w64.begin());
+  }
+  if (prec == DI_PREC_BF16) {
+    if (i == 0) return bytes(conv1_tc_pack(w64));
+    if (i == L - 1) return bytes(conv3_r4_pack(wx));
+    return bytes(convg_tc_pack(wx, cin, cout));
+  }
+  if (i == 0) return bytes(conv1_tf32_pack(w64));
+  if (i == L - 1) return bytes(conv3_tf32_pack(wx));
+  return bytes(conv_tf32_pack(wx, cin, cout));
+}
+
 di_status upload_bias(float** dst, const float* b, int cout, bool fullmap, int n1, int n2, long long* ws) {
   *dst = nullptr;
   if (!b) return DI_OK;
@@ -551,7 +581,12 @@ void free_ctx(di_ctx c) {
     if (l.wx) cudaFree(l.wx);
     if (l.wp) cudaFree(l.wp);
     if (l.b) cudaFree(l.b);
+    if (l.wt) cudaFree(l.wt);
+    if (l.keep) cudaFree(l.keep);
   }
+  if (c->keep_x) cudaFree(c->keep_x);
+  if (c->dA) cudaFree(c->dA);
+  if (c->dB) cudaFree(c->dB);
   for (auto p : c->act)
     if (p) cudaFree(p);
   void* ps[] = {c->mpart, c->phi, c->wx1, c->wx2, c->wx3, c->wp2, c->wp1, c->wp3, c->wp2t, c->wpd3, c->wp2db, c->h1b, c->dg2b, c->dh1b, c->part_w2, c->phi_rm, c->xs, c->params, c->vel,
@@ -605,7 +640,8 @@ di_status run_proxy(di_ctx c, const void* y, long long ldy, int batch, void* xt,
 }
 
 // custom stack: x_tilde -> layer 0 -> ... -> x_hat, interior activations ping-pong in act[]
-di_status run_stack(di_ctx c, int batch, void* xt, float* xhat, cudaStream_t st, int& launches) {
+// keep (training): every hidden layer's output is also stored as fp32 in layer.keep for the backward
+di_status run_stack(di_ctx c, int batch, void* xt, float* xhat, cudaStream_t st, int& launches, bool keep = false) {
   const int L = (int)c->stack.size();
   const int relu_last = (c->flags & DI_FLAG_FINAL_RELU) ? 1 : 0;
   const void* in = xt;
@@ -647,6 +683,8 @@ di_status run_stack(di_ctx c, int batch, void* xt, float* xhat, cudaStream_t st,
         CUDA_TRY(di::launch_convg_tc(l.cin, l.cout, &l.tm, l.wp, l.b, batch, c->n1, c->n2, outb, c->num_sms, st));
       }
       ++launches;
+      if (keep && i < L - 1)
+        CUDA_TRY(di::launch_bf16_to_f32(outb, i == 0 ? 64 : l.cout, l.cout, (size_t)batch * c->N, l.keep, st));
       continue;
     } else {
       if (i == L - 1)
@@ -656,6 +694,8 @@ di_status run_stack(di_ctx c, int batch, void* xt, float* xhat, cudaStream_t st,
                                        c->n1, c->n2, st));
     }
     ++launches;
+    if (keep && i < L - 1)
+      CUDA_TRY(cudaMemcpyAsync(l.keep, out, (size_t)batch * c->N * l.cout * 4, cudaMemcpyDeviceToDevice, st));
     in = out;
   }
   return DI_OK;
@@ -1026,33 +1066,11 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       di_ctx_s::Layer& l = c->stack[i];
       l.cin = al.cin, l.cout = al.cout;
       auto wx = xcorr_taps(al.w, al.cout, al.cin, xc, false);
-      if (c->prec == DI_PREC_FP32) {
-        auto sl = simt_layout(wx, al.cout, al.cin);
-        STEP(upload(&l.wx, sl.data(), sl.size() * 4, &c->ws_bytes));
-      } else if (bf16) {   // k_conv1_tc (64 bank rows, rows >= cout zero) / k_conv2_tc<C_in, C_out> / k_conv3_r4
-        std::vector<uint16_t> pk;
-        if (i == 0) {
-          std::vector<float> w64((size_t)64 * K * K, 0.f);
-          std::copy(wx.begin(), wx.end(), w64.begin());
-          pk = conv1_tc_pack(w64);
-        } else if (i == L - 1) {
-          pk = conv3_r4_pack(wx);
-        } else {
-          pk = convg_tc_pack(wx, al.cin, al.cout);
-        }
-        STEP(upload(reinterpret_cast<uint16_t**>(&l.wp), pk.data(), pk.size() * 2, &c->ws_bytes));
-      } else if (i == 0) {   // conv1 machinery: 64 bank rows, rows >= cout zero
-        std::vector<float> w64((size_t)64 * K * K, 0.f);
-        std::copy(wx.begin(), wx.end(), w64.begin());
-        auto pk = conv1_tf32_pack(w64);
-        STEP(upload(reinterpret_cast<float**>(&l.wp), pk.data(), pk.size() * 4, &c->ws_bytes));
-      } else if (i == L - 1) {
-        auto pk = conv3_tf32_pack(wx);
-        STEP(upload(reinterpret_cast<float**>(&l.wp), pk.data(), pk.size() * 4, &c->ws_bytes));
-      } else {
-        auto pk = conv_tf32_pack(wx, al.cin, al.cout);
-        STEP(upload(reinterpret_cast<float**>(&l.wp), pk.data(), pk.size() * 4, &c->ws_bytes));
-      }
+      const std::vector<uint8_t> img = pack_stack_layer(c->prec, i, L, wx, al.cin, al.cout);
+      if (c->prec == DI_PREC_FP32)
+        STEP(upload(&l.wx, img.data(), img.size(), &c->ws_bytes));
+      else
+        STEP(upload(reinterpret_cast<uint8_t**>(&l.wp), img.data(), img.size(), &c->ws_bytes));
       if (bf16 && i == 0 && al.cout < 64 && al.b) {   // k_conv1_tc reads 64 biases: zero past cout
         std::vector<float> b64(64, 0.f);
         std::copy(al.b, al.b + al.cout, b64.begin());
@@ -1061,6 +1079,21 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
         STEP(upload_bias(&l.b, al.b, al.cout, false, a->n1, a->n2, &c->ws_bytes));
       }
     }
+    // trainable (NEXT-3): fp32 master parameters [W_0 .. W_L-1 | b_0 .. b_L-1] in the API orientation
+    size_t nw = 0, nb = 0;
+    for (auto& l : c->stack) l.woff = nw, nw += (size_t)l.cout * l.cin * K * K;
+    for (auto& l : c->stack) l.boff = nb, nb += (size_t)l.cout;
+    std::vector<float> prm(nw + nb, 0.f);
+    for (int i = 0; i < L; ++i) {
+      const di_layer& al = a->layers[i];
+      const di_ctx_s::Layer& l = c->stack[i];
+      std::memcpy(prm.data() + l.woff, al.w, (size_t)l.cout * l.cin * K * K * 4);
+      if (al.b) std::memcpy(prm.data() + nw + l.boff, al.b, (size_t)l.cout * 4);
+    }
+    c->nparams = (long long)prm.size();
+    STEP(upload(&c->params, prm.data(), prm.size() * 4, &c->ws_bytes));
+    STEP(upload(&c->vel, nullptr, prm.size() * 4, &c->ws_bytes));
+    CUDA_TRY(cudaMemset(c->vel, 0, prm.size() * 4));
   } else {
     auto w1 = xcorr_taps(a->w1, C1, 1, xc, bf16);
     auto w2 = xcorr_taps(a->w2, C2, C1, xc, bf16);
@@ -1089,6 +1122,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
     STEP(upload_bias(&c->b2, a->b2, C2, fm, a->n1, a->n2, &c->ws_bytes));
     STEP(upload_bias(&c->b3, a->b3, 1, fm, a->n1, a->n2, &c->ws_bytes));
     if (!fm) {   // trainable: fp32 master parameters in the API orientation
+      c->nparams = di::N_PARAMS;
       std::vector<float> prm(di::N_PARAMS, 0.f);
       const size_t n1w = (size_t)C1 * K * K, n2w = (size_t)C2 * C1 * K * K, n3w = (size_t)C2 * K * K;
       std::memcpy(prm.data(), a->w1, n1w * 4);
@@ -1505,10 +1539,50 @@ static di_status train_alloc(di_ctx c) {
   return DI_OK;
 }
 
+// custom stacks (NEXT-3): the forward keeps every hidden layer's output (fp32), the backward runs the generic SIMT
+// weight / data gradient kernels per layer
+static di_status train_alloc_stack(di_ctx c) {
+  if (c->dxh) return DI_OK;
+  const size_t B = (size_t)c->max_batch, N = (size_t)c->N;
+  auto al = [&](auto** p, size_t bytes) -> di_status {
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+    c->ws_bytes += (long long)bytes;
+    return DI_OK;
+  };
+  di_status s;
+  const int L = (int)c->stack.size();
+  int cmax = 1;
+  size_t pw = 0, pb = 0;
+  for (int i = 0; i < L; ++i) {
+    di_ctx_s::Layer& l = c->stack[i];
+    if (i < L - 1 && (s = al(&l.keep, B * N * l.cout * 4)) != DI_OK) return s;
+    if (i > 0) {
+      if ((s = al(&l.wt, (size_t)l.cout * l.cin * K * K * 4)) != DI_OK) return s;
+      cmax = std::max(cmax, l.cin);
+    }
+    if (!l.b) {   // trainable biases need storage even when created zero (k_conv1_tc reads 64)
+      const size_t nbias = (c->prec == DI_PREC_BF16 && i == 0) ? 64 : (size_t)l.cout;
+      if ((s = al(&l.b, nbias * 4)) != DI_OK) return s;
+      CUDA_TRY(cudaMemset(l.b, 0, nbias * 4));
+    }
+    pw = std::max(pw, di::wgrad_layer_part_floats(l.cin, l.cout));
+    pb = std::max(pb, di::wgrad_layer_partb_floats(l.cin, l.cout));
+  }
+  if (c->prec == DI_PREC_BF16 && (s = al(&c->keep_x, B * N * 4)) != DI_OK) return s;
+  if ((s = al(&c->xh_ws, B * N * 4)) != DI_OK) return s;
+  if ((s = al(&c->dxh, B * N * 4)) != DI_OK) return s;
+  if ((s = al(&c->dA, B * N * cmax * 4)) != DI_OK) return s;
+  if ((s = al(&c->dB, B * N * cmax * 4)) != DI_OK) return s;
+  if ((s = al(&c->part_w, pw * 4)) != DI_OK) return s;
+  if ((s = al(&c->part_b, pb * 4)) != DI_OK) return s;
+  if ((s = al(&c->loss_img, B * 8)) != DI_OK) return s;
+  return DI_OK;
+}
+
 static di_status train_check(di_ctx c) {
   if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
-  if (!c->stack.empty()) return fail(DI_ERR_ARG, "training is implemented for the paper's three-layer stack");
   if (!c->params) return fail(DI_ERR_ARG, "training needs a context with per-channel (or zero) biases");
+  if (!c->stack.empty()) return train_alloc_stack(c);
   if (c->prec == DI_PREC_BF16 && c->n2 % 4 != 0)
     return fail(DI_ERR_ARG, "BF16 training needs n2 %% 4 == 0 (the layer-3 data gradient's strip map)");
   if (!c->b1 || !c->b2 || !c->b3) {   // trainable biases need storage even when created zero
@@ -1517,6 +1591,46 @@ static di_status train_check(di_ctx c) {
     if (!c->b3) CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->b3), 4));
   }
   return train_alloc(c);
+}
+
+static di_status train_grad_stack(di_ctx c, const void* y, long long ldy, const float* x_true, int batch, double scale,
+                                  float* grads, double* loss, cudaStream_t st) {
+  const int L = (int)c->stack.size();
+  const int flip = !(c->flags & DI_FLAG_XCORR);
+  const size_t npix = (size_t)batch * c->N;
+  // backward banks from the current parameters (cheap; always consistent with params)
+  for (int i = 1; i < L; ++i) {
+    const di_ctx_s::Layer& l = c->stack[i];
+    CUDA_TRY(di::launch_repack_layer(c->params + l.woff, nullptr, l.cin, l.cout, flip, nullptr, l.wt, nullptr, st));
+  }
+  // forward through the context's own kernels, keeping x_tilde and every hidden output as fp32
+  int launches = 0;
+  di_status s = run_proxy(c, y, ldy, batch, c->xt, false, st, launches);
+  if (s != DI_OK) return s;
+  s = run_stack(c, batch, c->xt, c->xh_ws, st, launches, true);
+  if (s != DI_OK) return s;
+  const float* xt32 = reinterpret_cast<const float*>(c->xt);
+  if (c->prec == DI_PREC_BF16) {
+    CUDA_TRY(di::launch_bf16_to_f32(c->xt, 1, 1, npix, c->keep_x, st));
+    xt32 = c->keep_x;
+  }
+  // loss and dL/dx_hat, the last layer's ReLU' under DI_FLAG_FINAL_RELU
+  CUDA_TRY(di::launch_loss_grad(c->xh_ws, x_true, c->N, batch, scale, c->dxh, c->loss_img, loss, st));
+  if (c->flags & DI_FLAG_FINAL_RELU) CUDA_TRY(di::launch_dgrad_mask(c->dxh, c->xh_ws, npix, st));
+  const size_t nw = (size_t)c->nparams - (c->stack.back().boff + c->stack.back().cout);
+  float* g = c->dxh;
+  for (int i = L - 1; i >= 0; --i) {
+    const di_ctx_s::Layer& l = c->stack[i];
+    const float* X = i == 0 ? xt32 : c->stack[i - 1].keep;
+    CUDA_TRY(di::launch_wgrad_layer(l.cin, l.cout, X, g, batch, c->n1, c->n2, c->part_w, c->part_b, flip,
+                                    grads + l.woff, grads + nw + l.boff, st));
+    if (i > 0) {   // dX = [X > 0] * (dG correlated with the rotated, transposed bank)
+      float* dX = g == c->dA ? c->dB : c->dA;
+      CUDA_TRY(di::launch_dgrad_simt(l.cin, l.cout, g, l.wt, X, dX, batch, c->n1, c->n2, st));
+      g = dX;
+    }
+  }
+  return DI_OK;
 }
 
 di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_true, int batch, double scale,
@@ -1530,6 +1644,7 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   if (batch < 1 || batch > c->max_batch) return fail(DI_ERR_ARG, "batch=%d outside [1, %d]", batch, c->max_batch);
   if (ldy < c->m) return fail(DI_ERR_DIM, "ldy=%lld < m=%d", ldy, c->m);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!c->stack.empty()) return train_grad_stack(c, y, ldy, x_true, batch, scale, grads, loss, st);
   const int flip = !(c->flags & DI_FLAG_XCORR);
   const int relu3 = (c->flags & DI_FLAG_FINAL_RELU) ? 1 : 0;
   // forward, keeping x_tilde, h1, h2 (post-ReLU) in the workspace
@@ -1584,6 +1699,34 @@ di_status di_train_grad(di_ctx c, const void* y, long long ldy, const float* x_t
   return DI_OK;
 }
 
+// custom stacks: the SGD step on the device; the forward images re-derived from the parameters -- on the device for
+// FP32 contexts (SIMT layout), on the host with di_create's packers for TF32 / BF16 (the tensor-core images of every
+// layer type; one synchronisation of `st` per step)
+static di_status sgd_stack(di_ctx c, const float* grads, double lr, double momentum, cudaStream_t st) {
+  CUDA_TRY(di::launch_sgd(c->params, grads, c->vel, (int)c->nparams, (float)lr, (float)momentum, st));
+  const int L = (int)c->stack.size();
+  const bool xc = (c->flags & DI_FLAG_XCORR) != 0;
+  const size_t nw = (size_t)c->nparams - (c->stack.back().boff + c->stack.back().cout);
+  if (c->prec == DI_PREC_FP32) {
+    for (auto& l : c->stack)
+      CUDA_TRY(di::launch_repack_layer(c->params + l.woff, c->params + nw + l.boff, l.cin, l.cout, !xc, l.wx, nullptr,
+                                       l.b, st));
+    return DI_OK;
+  }
+  std::vector<float> prm((size_t)c->nparams);
+  CUDA_TRY(cudaMemcpyAsync(prm.data(), c->params, prm.size() * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < L; ++i) {
+    di_ctx_s::Layer& l = c->stack[i];
+    const auto img = pack_stack_layer(c->prec, i, L, xcorr_taps(prm.data() + l.woff, l.cout, l.cin, xc, false), l.cin,
+                                      l.cout);
+    CUDA_TRY(cudaMemcpyAsync(l.wp, img.data(), img.size(), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(l.b, prm.data() + nw + l.boff, (size_t)l.cout * 4, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));   // the host images are released on return
+  return DI_OK;
+}
+
 di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, void* stream) {
   if (!c) return fail(DI_ERR_ARG, "ctx is NULL");
   DevGuard dg_(c->device);   // train_check allocates on the context's device
@@ -1592,6 +1735,7 @@ di_status di_sgd_step(di_ctx c, const float* grads, double lr, double momentum, 
   if (s != DI_OK) return s;
   if (!grads) return fail(DI_ERR_ARG, "grads is NULL");
   if (!(lr >= 0.0) || !(momentum >= 0.0 && momentum < 1.0)) return fail(DI_ERR_DOMAIN, "lr >= 0, 0 <= momentum < 1");
+  if (!c->stack.empty()) return sgd_stack(c, grads, lr, momentum, reinterpret_cast<cudaStream_t>(stream));
   CUDA_TRY(di::launch_sgd_repack(c->params, grads, c->vel, di::N_PARAMS, (float)lr, (float)momentum,
                                  !(c->flags & DI_FLAG_XCORR), c->wx1, c->wx2, c->wx3, c->wt2, c->wt3, c->b1, c->b2,
                                  c->b3, reinterpret_cast<cudaStream_t>(stream)));
@@ -1603,12 +1747,14 @@ di_status di_get_params(di_ctx c, float* params, void* stream) {
   if (!c || !params) return fail(DI_ERR_ARG, "NULL argument");
   if (!c->params) return fail(DI_ERR_ARG, "not a trainable (FP32, per-channel bias) context");
   DevGuard dg_(c->device);
-  CUDA_TRY(cudaMemcpyAsync(params, c->params, (size_t)di::N_PARAMS * 4, cudaMemcpyDeviceToDevice,
+  CUDA_TRY(cudaMemcpyAsync(params, c->params, (size_t)c->nparams * 4, cudaMemcpyDeviceToDevice,
                            reinterpret_cast<cudaStream_t>(stream)));
   return DI_OK;
 }
 
 long long di_num_params(void) { return di::N_PARAMS; }
+
+long long di_ctx_num_params(di_ctx c) { return c ? c->nparams : 0; }
 
 di_status di_destroy(di_ctx c) {
   if (!c) return DI_OK;

@@ -74,6 +74,7 @@ __device__ __forceinline__ void item_of(const GeoR4& g, int it, int& b, int& c0,
 // max x; per item the four warps' sums go to mpart[item][warp][3] (no atomics), and k_metrics_finish combines the
 // items of each image in item order: PSNR, NMSE and success without a second pass over
 // x_hat.
+template <bool METRICS>
 __global__ void __launch_bounds__(256, 1)
     k_conv3_r4(const __grid_constant__ CUtensorMap tmH2, const uint8_t* __restrict__ tpack,
                const float* __restrict__ bias, int fullmap, int relu, GeoR4 g, float* __restrict__ xhat,
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(256, 1)
             acc += (fullmap && bias) ? bias[pix % ((size_t)g.n1 * g.n2)] : bsc;
             if (relu) acc = fmaxf(acc, 0.f);
             xhat[pix] = acc;
-            if (xtrue) {
+            if (METRICS) {
               const float t = __ldg(xtrue + pix);
               const double dd = (double)acc - (double)t;
               m_se += dd * dd, m_sx += (double)t * (double)t, m_mx = fmaxf(m_mx, t);
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         __syncwarp();
       }
-      if (xtrue) {   // the warp's sums for this item, butterfly order fixed
+      if (METRICS) {   // the warp's sums for this item, butterfly order fixed
         for (int o = 16; o > 0; o >>= 1) {
           m_se += __shfl_xor_sync(0xffffffffu, m_se, o);
           m_sx += __shfl_xor_sync(0xffffffffu, m_sx, o);
@@ -302,7 +303,10 @@ int conv3_r4_box_rows() { return CH; }
 int conv3_r4_tpack_bytes() { return TBYTES; }
 
 cudaError_t setup_conv3_r4(int n2) {
-  return cudaFuncSetAttribute(k_conv3_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r4(n2));
+  const cudaError_t e = cudaFuncSetAttribute(k_conv3_r4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem_r4(n2));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_conv3_r4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r4(n2));
 }
 
 // per image b: the items b * per_img .. (b + 1) * per_img - 1, four warps each, summed in that order
@@ -330,8 +334,12 @@ cudaError_t launch_conv3_r4(const CUtensorMap* tmH2, const void* tpack, const fl
                             double* mpart, double* metrics) {
   GeoR4 g = make_geo_r4(batch, n1, n2, num_sms);
   const int grid = g.items < num_sms ? g.items : num_sms;
-  k_conv3_r4<<<grid, 256, smem_r4(n2), st>>>(*tmH2, reinterpret_cast<const uint8_t*>(tpack), bias, fullmap, relu, g,
-                                            xhat, xtrue, mpart);
+  if (xtrue)
+    k_conv3_r4<true><<<grid, 256, smem_r4(n2), st>>>(*tmH2, reinterpret_cast<const uint8_t*>(tpack), bias, fullmap,
+                                                    relu, g, xhat, xtrue, mpart);
+  else
+    k_conv3_r4<false><<<grid, 256, smem_r4(n2), st>>>(*tmH2, reinterpret_cast<const uint8_t*>(tpack), bias, fullmap,
+                                                     relu, g, xhat, nullptr, nullptr);
   if (xtrue) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -208,6 +208,18 @@ cudaError_t launch_convg_simt(int cin, int cout, const float* in, const float* w
   return cudaErrorInvalidValue;
 }
 
+// custom stacks (NEXT-3), the data gradient of layer (cin -> cout): dX = [X > 0] * correlation of dG (cout channels)
+// with the rotated, transposed bank wt [cout][a][b][cin] -- a cout -> cin 'same' layer with a ReLU' mask, no bias
+cudaError_t launch_dgrad_simt(int cin, int cout, const float* dG, const float* wt, const float* X, float* dX, int batch,
+                              int n1, int n2, cudaStream_t st) {
+  if (cout == 32 && cin == 32) return launch_wide<float, float, 32, 32, 8, 2>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  if (cout == 32 && cin == 64) return launch_wide<float, float, 32, 64, 16, 2>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  if (cout == 64 && cin == 32) return launch_wide<float, float, 64, 32, 8, 2>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  if (cout == 64 && cin == 64) return launch_wide<float, float, 64, 64, 16, 2>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  if (cout == 1 && cin == 32) return launch_wide<float, float, 1, 32, 8, 1>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_conv2_simt_f32(const float* h1, const float* wx, const float* bias, int fullmap, float* h2,
                                   int batch, int n1, int n2, cudaStream_t st) {
   return launch_wide<float, float, 64, 32, 8, 4>(h1, wx, bias, fullmap, 1, h2, batch, n1, n2, st);

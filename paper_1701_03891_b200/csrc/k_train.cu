@@ -298,6 +298,73 @@ cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, 
   }
 }
 
+// ----------------------------------------------------------------------------- custom stacks (NEXT-3)
+// Weight gradient of one layer of a custom stack, any (C_in, C_out) a stack may hold:
+// the same register-blocked sliding-window kernels as the paper's layers, instantiated per channel pair.
+static int wgrad_layer_chunks(int cin, int cout) {   // WGRAD_CHUNKS / (blocks per chunk of the instance below)
+  if (cin == 1) return WGRAD_CHUNKS / (cout == 32 ? 2 : 4);
+  if (cout == 1) return WGRAD_CHUNKS / 4;
+  return WGRAD_CHUNKS / ((cin / 8) * (cout / 8));
+}
+cudaError_t launch_wgrad_layer(int cin, int cout, const float* X, const float* dG, int batch, int n1, int n2,
+                               float* part_w, float* part_b, int flip, float* gw, float* gb, cudaStream_t st) {
+  const int C = wgrad_layer_chunks(cin, cout);
+  if (cin == 1 && cout == 32) return wgrad<1, 32, 1, 16>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 1 && cout == 64) return wgrad<1, 64, 1, 16>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 32 && cout == 32) return wgrad<32, 32, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 32 && cout == 64) return wgrad<32, 64, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 64 && cout == 32) return wgrad<64, 32, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 64 && cout == 64) return wgrad<64, 64, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 32 && cout == 1) return wgrad<32, 1, 8, 1>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  return cudaErrorInvalidValue;
+}
+// scratch floats launch_wgrad_layer needs: part_w (chunks x weights of the layer); part_b needs chunks x cout
+size_t wgrad_layer_part_floats(int cin, int cout) {
+  return (size_t)wgrad_layer_chunks(cin, cout) * cin * cout * KS * KS;
+}
+size_t wgrad_layer_partb_floats(int cin, int cout) { return (size_t)wgrad_layer_chunks(cin, cout) * cout; }
+
+// From the API-orientation parameters of one layer (W [cout][cin][11][11], b [cout]): the forward SIMT layout
+// wx[ci][a][b][co] of the cross-correlation taps (FP32 contexts; may be null), the backward layout
+// wt[co][10-a][10-b][ci] (the data gradient is a 'same' correlation of dG with the rotated, transposed bank) and the
+// bias array (may be null)
+__global__ void k_repack_layer(const float* __restrict__ W, const float* __restrict__ bsrc, int cin, int cout, int flip,
+                               float* __restrict__ wx, float* __restrict__ wt, float* __restrict__ bdst) {
+  const int nw = cout * cin * KS * KS;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw + cout; i += gridDim.x * blockDim.x) {
+    if (i >= nw) {
+      if (bdst) bdst[i - nw] = bsrc[i - nw];
+      continue;
+    }
+    const int tap = i % (KS * KS), co = i / (KS * KS) / cin, ci = (i / (KS * KS)) % cin;
+    const int u = tap / KS, v = tap % KS;
+    const int a = flip ? KS - 1 - u : u, b = flip ? KS - 1 - v : v;
+    const float w = W[i];
+    if (wx) wx[(((size_t)ci * KS + a) * KS + b) * cout + co] = w;
+    if (wt) wt[(((size_t)co * KS + (KS - 1 - a)) * KS + (KS - 1 - b)) * cin + ci] = w;
+  }
+}
+cudaError_t launch_repack_layer(const float* W, const float* b, int cin, int cout, int flip, float* wx, float* wt,
+                                float* bdst, cudaStream_t st) {
+  const int n = cout * cin * KS * KS + cout;
+  k_repack_layer<<<(n + 255) / 256 < 592 ? (n + 255) / 256 : 592, 256, 0, st>>>(W, b, cin, cout, flip, wx, wt, bdst);
+  return cudaGetLastError();
+}
+
+// bf16 activation [npix][pitch] -> fp32 [npix][ch] (the custom stack's training forward keeps every layer's output)
+__global__ void k_bf16_to_f32(const __nv_bfloat16* __restrict__ src, int pitch, int ch, size_t npix,
+                              float* __restrict__ dst) {
+  const size_t n = npix * ch;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t p = i / ch;
+    dst[i] = __bfloat162float(src[p * pitch + (i - p * ch)]);
+  }
+}
+cudaError_t launch_bf16_to_f32(const void* src, int pitch, int ch, size_t npix, float* dst, cudaStream_t st) {
+  k_bf16_to_f32<<<1184, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(src), pitch, ch, npix, dst);
+  return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------------------- SGD and weight repacking
 // params / grads / vel: [W1 (64*121) | W2 (32*64*121) | W3 (32*121) | b1 (64) | b2 (32) | b3 (1)] in the API
 // orientation.  vel = momentum * vel + grad; param -= lr * vel.
@@ -440,6 +507,11 @@ cudaError_t launch_repack_bf16(const float* params, int flip, void* wp1, void* w
 cudaError_t launch_repack_tf32(const float* params, int flip, float* wp1, float* wp2t, float* wp3, float* wpd3,
                                void* wp2db, cudaStream_t st) {
   k_repack_tf32<<<592, 256, 0, st>>>(params, flip, wp1, wp2t, wp3, wpd3, reinterpret_cast<uint16_t*>(wp2db));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sgd(float* params, const float* grads, float* vel, int n, float lr, float momentum, cudaStream_t st) {
+  k_sgd<<<296, 256, 0, st>>>(params, grads, vel, n, lr, momentum);
   return cudaGetLastError();
 }
 

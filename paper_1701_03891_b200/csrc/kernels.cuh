@@ -209,6 +209,17 @@ cudaError_t launch_wgrad3_tc(const void* h2, const float* dg3, int batch, int n1
                              const CUtensorMap* tmH2 = nullptr);
 int wgrad3_tc_h_box_rows();   // bf16 h2 strip box of k_wgrad3_tc (32 ch x P x rows, SWIZZLE_64B)
 cudaError_t launch_bias_reduce(const float* part_b, int nchunk, int nb, float* gb, cudaStream_t st);
+// custom stacks (NEXT-3): generic SIMT weight / data gradients per layer, the per-layer repack, SGD, bf16 -> fp32
+cudaError_t launch_wgrad_layer(int cin, int cout, const float* X, const float* dG, int batch, int n1, int n2,
+                               float* part_w, float* part_b, int flip, float* gw, float* gb, cudaStream_t st);
+size_t wgrad_layer_part_floats(int cin, int cout);
+size_t wgrad_layer_partb_floats(int cin, int cout);
+cudaError_t launch_dgrad_simt(int cin, int cout, const float* dG, const float* wt, const float* X, float* dX, int batch,
+                              int n1, int n2, cudaStream_t st);
+cudaError_t launch_repack_layer(const float* W, const float* b, int cin, int cout, int flip, float* wx, float* wt,
+                                float* bdst, cudaStream_t st);
+cudaError_t launch_sgd(float* params, const float* grads, float* vel, int n, float lr, float momentum, cudaStream_t st);
+cudaError_t launch_bf16_to_f32(const void* src, int pitch, int ch, size_t npix, float* dst, cudaStream_t st);
 cudaError_t launch_sgd_repack(float* params, const float* grads, float* vel, int n, float lr, float momentum, int flip,
                               float* wx1, float* wx2, float* wx3, float* wt2, float* wt3, float* b1, float* b2,
                               float* b3, cudaStream_t st);

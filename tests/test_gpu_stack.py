@@ -86,11 +86,84 @@ def test_stack_unsupported_shapes_are_rejected(widths, precision):
         DeepInverse(case.phi, case.params, 16, 16, precision, max_batch=1)
 
 
-def test_stack_training_is_rejected():
+# ---------------------------------------------------------------------------------------------------- training
+TOL_GRAD = {"f32": 1e-4, "tf32": 2e-2, "bf16": 2e-2}
+
+
+def _stack_case(widths, precision, n1, n2, m, batch):
+    return Case(n1, n2, m, batch, precision, 6, 3, params=stack_params(widths))
+
+
+@pytest.mark.parametrize("precision", ["f32", "tf32", "bf16"])
+@pytest.mark.parametrize("widths", [(1, 32, 64, 32, 1), (1, 64, 32, 32, 32, 1), (1, 32, 1)])
+def test_stack_gradients_match_oracle(precision, widths):
+    """Training custom stacks (NEXT-3): loss and every layer's weight / bias gradient against oracle.train_grad (the
+    reverse mode of the literal forward, pinned by central finite differences for arbitrary widths --
+    tests/test_oracle_train.py) on the same (bf16-rounded) inputs; 4- and 5-layer stacks and the minimal 2-layer one,
+    a ragged 40 x 36 image (TF32 needs n2 % 4 == 0)."""
     import torch
-    from paper_1701_03891_b200 import DeepInverse, DiError
-    case = Case(16, 16, 64, 2, "f32", params=stack_params((1, 32, 32, 1)))
-    ctx = DeepInverse(case.phi, case.params, 16, 16, "f32", max_batch=2)
-    with pytest.raises(DiError):
-        ctx.train_grad(torch.from_numpy(case.y).cuda(), torch.from_numpy(case.x).cuda())
+    from paper_1701_03891_b200 import DeepInverse
+    case = _stack_case(widths, precision, 40, 36, 250, 3)
+    ctx = DeepInverse(case.phi, case.params, case.n1, case.n2, precision, max_batch=case.batch)
+    assert ctx.num_params() == sum(w.size + w.shape[0] for w in case.params.w)
+    y = torch.from_numpy(case.y).cuda().to(ctx.storage_dtype)
+    x = torch.from_numpy(case.x).cuda()
+    loss, g = ctx.train_grad(y, x)
+    torch.cuda.synchronize()
+    ws, bs = ctx.split(g.cpu().numpy().astype(np.float64))
+    rl, rw, rb = oracle.train_grad(case.y, case.x, case.phi, case.params, case.n1, case.n2)
+    tol = TOL_GRAD[precision]
+    assert abs(float(loss.item()) - rl) <= (1e-5 if precision == "f32" else 1e-2) * abs(rl)
+    for l in range(len(widths) - 1):
+        assert oracle.rel_l2(ws[l], rw[l]) <= tol, ("W", l, oracle.rel_l2(ws[l], rw[l]))
+        assert oracle.rel_l2(bs[l], rb[l]) <= tol, ("b", l, oracle.rel_l2(bs[l], rb[l]))
+    ctx.close()
+
+
+def test_stack_gradients_final_relu_and_xcorr():
+    import torch
+    from paper_1701_03891_b200 import DI_FLAG_FINAL_RELU, DI_FLAG_XCORR, DeepInverse
+    case = _stack_case((1, 32, 32, 1), "f32", 24, 24, 120, 2)
+    ctx = DeepInverse(case.phi, case.params, 24, 24, "f32", flags=DI_FLAG_FINAL_RELU | DI_FLAG_XCORR, max_batch=2)
+    loss, g = ctx.train_grad(torch.from_numpy(case.y).cuda(), torch.from_numpy(case.x).cuda())
+    ws, bs = ctx.split(g.cpu().numpy().astype(np.float64))
+    p = synth.Params([w[:, :, ::-1, ::-1].copy() for w in case.params.w], case.params.b)   # oracle: true convolution
+    rl, rw, rb = oracle.train_grad(case.y, case.x, case.phi, p, 24, 24, final_relu=True)
+    for l in range(3):
+        assert oracle.rel_l2(ws[l], rw[l][:, :, ::-1, ::-1]) <= 1e-4, l
+        assert oracle.rel_l2(bs[l], rb[l]) <= 1e-4, l
+    ctx.close()
+
+
+@pytest.mark.parametrize("precision", ["f32", "tf32", "bf16"])
+def test_stack_sgd_updates_the_forward(precision):
+    """di_sgd_step on a custom stack: the parameters move by -lr * grad (momentum 0), the forward runs on the new
+    weights (its output matches the oracle's forward over the updated parameters), and the loss decreases."""
+    import torch
+    from paper_1701_03891_b200 import DeepInverse
+    case = _stack_case((1, 32, 64, 32, 1), precision, 32, 32, 200, 4)
+    ctx = DeepInverse(case.phi, case.params, 32, 32, precision, max_batch=4)
+    y = torch.from_numpy(case.y).cuda().to(ctx.storage_dtype)
+    x = torch.from_numpy(case.x).cuda()
+    losses, lr = [], None
+    for _ in range(4):
+        loss, g = ctx.train_grad(y, x)
+        losses.append(float(loss.item()))
+        if lr is None:
+            lr = 0.05 * losses[0] / float((g.double() ** 2).sum())
+            before = ctx.params()
+            gflat = g.cpu().numpy()
+        ctx.sgd_step(g, lr, 0.0)
+        if len(losses) == 1:
+            after = ctx.params()
+            gw, gb = ctx.split(gflat)
+            for l in range(4):
+                np.testing.assert_allclose(after[0][l], before[0][l] - np.float32(lr) * gw[l], rtol=0, atol=1e-6)
+                np.testing.assert_allclose(after[1][l], before[1][l] - np.float32(lr) * gb[l], rtol=0, atol=1e-6)
+            newp = synth.Params([w.copy() for w in after[0]], [b.copy() for b in after[1]]).rounded(
+                "bf16" if precision == "bf16" else "f32")
+            out = ctx.recover(y).cpu().numpy()
+            ref = oracle.forward(case.y, case.phi, newp, 32, 32)
+            assert max(oracle.rel_l2(a, r) for a, r in zip(out, ref)) <= TOL_REL_L2[precision]
+    assert losses[-1] < losses[0], losses
     ctx.close()
