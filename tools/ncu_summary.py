@@ -57,9 +57,9 @@ def launches(path: str) -> str:
             unit = r[ui]
     scale = 1e-3 if unit == "ns" else (1.0 if unit == "us" else 1e3)
     tot = sum(sum(v) for v in d.values())
-    out = ["| kernel | launches | mean us | share of all launches |", "|---|---|---|---|"]
+    out = ["| kernel | launches | mean us | largest launch us | share of all launches |", "|---|---|---|---|---|"]
     for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
-        out.append(f"| `{k}` | {len(v)} | {sum(v) / len(v) * scale:.1f} | {sum(v) / tot:.1%} |")
+        out.append(f"| `{k}` | {len(v)} | {sum(v) / len(v) * scale:.1f} | {max(v) * scale:.1f} | {sum(v) / tot:.1%} |")
     return "\n".join(out)
 
 
