@@ -520,21 +520,26 @@ std::vector<float> conv_tf32_pack(const std::vector<float>& wx, int cin, int cou
 // 128 / C_out column taps v0 = TAPS j ..), row v' * C_out + k, C_in channels per row (128 B: SWIZZLE_128B, 64 B:
 // SWIZZLE_64B); conv2_tc_pack is the (64, 32) case
 std::vector<uint16_t> convg_tc_pack(const std::vector<float>& wx, int cin, int cout) {
-  const int taps = 128 / cout, J = (K + taps - 1) / taps, rb = 2 * cin;
+  // C_in = 128: two channel halves, K-block h * 11 J + u J + j over channels 64 h .. 64 h + 63 (k_conv2_tc NH = 2)
+  const int taps = 128 / cout, J = (K + taps - 1) / taps, nh = cin > 64 ? cin / 64 : 1, cinh = cin / nh;
+  const int rb = 2 * cinh;
   const size_t wb = (size_t)128 * rb;
-  std::vector<uint16_t> out((size_t)K * J * wb / 2, 0);
+  std::vector<uint16_t> out((size_t)nh * K * J * wb / 2, 0);
   uint8_t* base = reinterpret_cast<uint8_t*>(out.data());
-  for (int u = 0; u < K; ++u)
-    for (int j = 0; j < J; ++j)
-      for (int row = 0; row < 128; ++row) {
-        const int v = taps * j + row / cout, k = row % cout;
-        for (int ci = 0; ci < cin; ++ci) {
-          const uint16_t h = v < K ? f2bf(wx[(((size_t)k * cin + ci) * K + u) * K + v]) : 0;
-          const int sw = rb == 128 ? (row & 7) : ((row >> 1) & 3);
-          const size_t off = (size_t)(u * J + j) * wb + (size_t)row * rb + ((((size_t)ci / 8) ^ sw) << 4) + (ci % 8) * 2;
-          std::memcpy(base + off, &h, 2);
+  for (int h = 0; h < nh; ++h)
+    for (int u = 0; u < K; ++u)
+      for (int j = 0; j < J; ++j)
+        for (int row = 0; row < 128; ++row) {
+          const int v = taps * j + row / cout, k = row % cout;
+          for (int c = 0; c < cinh; ++c) {
+            const int ci = h * cinh + c;
+            const uint16_t hv = v < K ? f2bf(wx[(((size_t)k * cin + ci) * K + u) * K + v]) : 0;
+            const int sw = rb == 128 ? (row & 7) : ((row >> 1) & 3);
+            const size_t off = (size_t)((h * K + u) * J + j) * wb + (size_t)row * rb + ((((size_t)c / 8) ^ sw) << 4) +
+                               (c % 8) * 2;
+            std::memcpy(base + off, &hv, 2);
+          }
         }
-      }
   return out;
 }
 
@@ -930,11 +935,15 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       if (i > 0 && l.cin != a->layers[i - 1].cout)
         return fail(DI_ERR_DIM, "layers[%d].cin=%d != layers[%d].cout=%d", i, l.cin, i - 1, a->layers[i - 1].cout);
       const bool w32_64 = (l.cout == 32 || l.cout == 64);
+      auto wide = [](int c) { return c == 32 || c == 64 || c == 128; };
       const bool ok = i == 0 ? (l.cin == 1 && w32_64) : i == L - 1 ? (l.cin == 32 && l.cout == 1)
-                                                                   : ((l.cin == 32 || l.cin == 64) && w32_64);
+                                                                   : (wide(l.cin) && wide(l.cout));
       if (!ok)
-        return fail(DI_ERR_ARG, "layers[%d] %d -> %d unsupported (first 1 -> {32,64}, interior {32,64} -> {32,64}, "
-                    "last 32 -> 1)", i, l.cin, l.cout);
+        return fail(DI_ERR_ARG, "layers[%d] %d -> %d unsupported (first 1 -> {32,64}, interior {32,64,128} -> "
+                    "{32,64,128}, last 32 -> 1)", i, l.cin, l.cout);
+      if (a->precision == DI_PREC_TF32 && (l.cin == 128 || l.cout == 128))
+        return fail(DI_ERR_ARG, "layers[%d]: width 128 runs in FP32 and BF16 contexts (the TF32 interior kernel "
+                    "keeps C_in fp32 channels of the strip in shared memory)", i);
     }
   }
   if (a->phi_dtype != DI_DTYPE_F32 && a->phi_dtype != DI_DTYPE_BF16) return fail(DI_ERR_ARG, "bad phi_dtype");
@@ -1145,7 +1154,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
       int wmax = 0;
       for (const auto& l : c->stack) wmax = std::max(wmax, l.cout);
       // BF16: bf16 activations, the first layer's at pitch 64 (k_conv1_tc writes 64 channels, the rows >= cout zero)
-      if (bf16) wmax = 64;
+      if (bf16) wmax = std::max(wmax, 64);
       for (auto& p : c->act) STEP(upload(&p, nullptr, B * N * wmax * (bf16 ? 2 : 4), &c->ws_bytes));
     } else {
       STEP(upload(&c->h1, nullptr, B * N * C1 * c->elt, &c->ws_bytes));
@@ -1204,7 +1213,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
         di_ctx_s::Layer& l = c->stack[i];
         const int pitch = i == 1 ? 64 : c->stack[i - 1].cout;
         const bool last = i == (int)c->stack.size() - 1;
-        STEP(encode_act_bf16(&l.tm, c->act[(i - 1) & 1], a->max_batch, a->n1, a->n2, pitch, l.cin,
+        STEP(encode_act_bf16(&l.tm, c->act[(i - 1) & 1], a->max_batch, a->n1, a->n2, pitch, std::min(l.cin, 64),
                              last ? di::conv3_tc_box_cols(a->n2) : di::conv2_tc_box_cols(a->n2),
                              last ? di::conv3_r4_box_rows() : di::convg_tc_box_rows(l.cin)));
       }

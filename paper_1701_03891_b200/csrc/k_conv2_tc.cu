@@ -86,19 +86,22 @@ enum { C2_BIAS_RELU = 0, C2_MASK = 1 };
 // rings (multicast) and each MMA commit frees the stage in both, halving the L2 -> SM weight traffic.  Needs the two
 // CTAs of a pair to consume the same K-block sequence (equal tile counts: launch_conv2_tc checks).
 template <int CIN, int COUT, int MODE, int CL = 1>
-__global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
+__global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
     k_conv2_tc(const __grid_constant__ CUtensorMap tmH1, const __nv_bfloat16* __restrict__ wpack,
                const float* __restrict__ bias, int fullmap, Geo g, __nv_bfloat16* __restrict__ h2,
                const __nv_bfloat16* __restrict__ mask) {
   constexpr int TAPS = 128 / COUT, J = (11 + TAPS - 1) / TAPS, KB = 11 * J;
-  constexpr int RB = CIN * 2, KMMA = RB / 32;
+  // C_in = 128 (custom stacks, NEXT-3): two 64-channel halves, each its own strip load and 11 J K-blocks per tile,
+  // accumulated into the same TMEM tile (a 128-channel strip would need 283 KB of shared memory)
+  constexpr int NH = CIN > 64 ? CIN / 64 : 1, CINH = CIN / NH;
+  constexpr int RB = CINH * 2, KMMA = RB / 32;
   constexpr uint32_t WB = 128 * RB;
   constexpr uint32_t SWZ = RB == 128 ? kSwizzle128B : kSwizzle64B;
   constexpr int QPT = COUT / 32, CPT = COUT / 8;
   // epilogue groups: C_out = 64 (twice the epilogue work per tile) runs two groups of 4 warps, one per TMEM buffer
-  constexpr int EG = COUT == 64 ? 2 : 1;
+  constexpr int EG = COUT >= 64 ? 2 : 1;
   // weight ring: 4 stages of 16 KB for 128-B rows; 12 stages of 8 KB for 64-B rows (the layer-2 dgrad)
-  constexpr int WST = RB == 128 ? (COUT == 64 ? 3 : WSTAGES) : C2_WST64;   // <64, 64>: room for 2 epilogue groups
+  constexpr int WST = RB == 128 ? (COUT >= 64 ? 3 : WSTAGES) : C2_WST64;   // C_out >= 64: room for 2 epilogue groups
   constexpr int R = RB == 128 ? C2_ROWS : C2_DG_ROWS;   // output rows per unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -141,18 +144,22 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ strip + weight producer
       uint32_t wk = 0;                    // weight K-blocks issued (stage wk % WST)
-      int it = 0;
+      int it = 0, sl = 0;                 // units, strip loads
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
         const int b = u / per_img, rem = u - b * per_img;
         const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
         const int rows = min(R, g.n1 - r0);
         const int L = (rows - 1) * g.P + g.wseg;
         const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
-        if (it > 0) mbar_wait(&hempty[0], (it - 1) & 1);
-        mbar_arrive_expect_tx(&hfull[0], strip_bytes);
-        tma_load_4d(strip, &tmH1, &hfull[0], 0, c0 - 5, r0 - 5, b);
-        for (int t = 0; t < ntiles; ++t) {
-          const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack);
+        for (int t = 0; t < ntiles; ++t)
+         for (int h = 0; h < NH; ++h) {
+          if (NH > 1 || t == 0) {   // the unit's strip (C_in = 128: channel half h, per tile)
+            if (sl > 0) mbar_wait(&hempty[0], (sl - 1) & 1);
+            mbar_arrive_expect_tx(&hfull[0], strip_bytes);
+            tma_load_4d(strip, &tmH1, &hfull[0], CINH * h, c0 - 5, r0 - 5, b);
+            ++sl;
+          }
+          const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wpack) + (size_t)h * KB * WB;
           for (int kb = 0; kb < KB; ++kb, ++wk, wsrc += WB) {
             const uint32_t st = wk % WST;
             if (wk >= WST) mbar_wait(&wempty[st], ((wk / WST) - 1) & 1);
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
       const uint64_t adesc0 = smem_desc(smem_u32(wst), 16, 8 * RB, SWZ);
       const uint64_t pstep = (uint64_t)g.P * (RB >> 4);    // one tap row = P positions x RB bytes, >> 4
       uint32_t wk = 0;
-      int it = 0, ti = 0;
+      int it = 0, ti = 0, sl = 0;
 #ifdef DI_PROF_CONV2
       long long c_h = 0, c_t = 0, c_w = 0, c_w0 = 0, c_w1 = 0, c0_ = clock64(), c_lat = 0, c_latmax = 0;
 #define PT0 long long _t0 = clock64();
@@ -194,8 +201,6 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
         const int rows = min(R, g.n1 - r0);
         const int L = (rows - 1) * g.P + g.wseg;
         const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
-        { PT0 mbar_wait(&hfull[0], it & 1); PT1(c_h) }
-        tc_fence_after();
         for (int t = 0; t < ntiles; ++t, ++ti) {
           const int n0 = t * OUT_PER_TILE;
           const int cnt = min(OUT_PER_TILE, L - n0);
@@ -207,6 +212,11 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
           const uint32_t d = tmem + buf * 256;
           // the last K-block's window (u = 10, v0 = TAPS (J - 1)) stays inside the strip and its guard rows
           DI_DEVICE_ASSERT(n0 + 10 * g.P + TAPS * (J - 1) + nmma <= (R + 10) * g.P + GUARD_ROWS, n0, nmma);
+         for (int h = 0; h < NH; ++h) {
+          if (NH > 1 || t == 0) {
+            { PT0 mbar_wait(&hfull[0], sl & 1); PT1(c_h) }
+            tc_fence_after();
+          }
           uint64_t bd = bdesc0 + (uint64_t)(n0 * (RB >> 4));
           for (int uu = 0; uu < 11; ++uu, bd += pstep) {
 #pragma unroll
@@ -223,7 +233,7 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
               tc_fence_after();
               const uint64_t ad = adesc0 + (uint64_t)(st * (WB >> 4));
               const uint64_t b = bd + (uint64_t)(TAPS * j * (RB >> 4));   // v0 = TAPS j positions
-              umma_f16_ss(d, ad, b, idesc, (uu | j) != 0);
+              umma_f16_ss(d, ad, b, idesc, (h | uu | j) != 0);
 #pragma unroll
               for (int kk = 1; kk < KMMA; ++kk) umma_f16_ss(d, ad + 2 * kk, b + 2 * kk, idesc, 1);
               if (CL > 1)
@@ -232,9 +242,17 @@ __global__ void __launch_bounds__(COUT == 64 ? 384 : 256, 1)
                 umma_commit(&wempty[st]);
             }
           }
+          if (NH > 1) {   // this half's strip is free for the next load
+            umma_commit(&hempty[0]);
+            ++sl;
+          }
+         }
           umma_commit(&tfull[buf]);
         }
-        umma_commit(&hempty[0]);
+        if (NH == 1) {
+          umma_commit(&hempty[0]);
+          ++sl;
+        }
       }
 #ifdef DI_PROF_CONV2
       if (blockIdx.x % 37 == 0)
@@ -482,7 +500,7 @@ cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const fl
 // custom stacks, BF16 contexts: interior C_in -> C_out layers (C in {32, 64}) on the same
 // kernel, weights packed by convg_tc_pack (K-block u * J + j, rows v' * C_out + k, C_in bf16 channels per row).
 // tm: bf16 strip map over the input activation (box C_in x P x convg_tc_box_rows(C_in)); out: NHWC, C_out channels.
-int convg_tc_box_rows(int cin) { return (cin == 64 ? C2_ROWS : C2_DG_ROWS) + 10; }
+int convg_tc_box_rows(int cin) { return (cin >= 64 ? C2_ROWS : C2_DG_ROWS) + 10; }
 
 // <64, 64>: the 128-B-row strip, a 3-stage ring and two epilogue groups' staging
 static size_t convg64_smem_bytes(int n2) {
@@ -492,18 +510,31 @@ static size_t convg64_smem_bytes(int n2) {
 }
 
 template <int CIN, int COUT>
+static size_t convg_smem(int n2) {
+  return CIN == 32 ? dgrad2_bf16_smem_bytes(n2) : COUT >= 64 ? convg64_smem_bytes(n2) : conv2_tc_smem_bytes(n2);
+}
+template <int CIN, int COUT>
 static cudaError_t launch_g(const CUtensorMap* tm, const void* wpack, const float* bias, int batch, int n1, int n2,
                             void* out, int num_sms, cudaStream_t st) {
-  Geo g = make_geo(batch, n1, n2, CIN == 64 ? C2_ROWS : C2_DG_ROWS);
+  Geo g = make_geo(batch, n1, n2, CIN >= 64 ? C2_ROWS : C2_DG_ROWS);
   const int grid = g.units < num_sms ? g.units : num_sms;
-  const size_t smem = CIN == 32 ? dgrad2_bf16_smem_bytes(n2) : COUT == 64 ? convg64_smem_bytes(n2) : conv2_tc_smem_bytes(n2);
-  k_conv2_tc<CIN, COUT, C2_BIAS_RELU><<<grid, COUT == 64 ? 384 : 256, smem, st>>>(
+  k_conv2_tc<CIN, COUT, C2_BIAS_RELU><<<grid, COUT >= 64 ? 384 : 256, convg_smem<CIN, COUT>(n2), st>>>(
       *tm, reinterpret_cast<const __nv_bfloat16*>(wpack), bias, 0, g, reinterpret_cast<__nv_bfloat16*>(out), nullptr);
   return cudaGetLastError();
 }
 
+template <int CIN, int COUT>
+static cudaError_t setup_g(int n2) {
+  return cudaFuncSetAttribute(k_conv2_tc<CIN, COUT, C2_BIAS_RELU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)convg_smem<CIN, COUT>(n2));
+}
+
 cudaError_t setup_convg_tc(int n2) {
   cudaError_t e;
+  if ((e = setup_g<64, 128>(n2)) != cudaSuccess || (e = setup_g<128, 64>(n2)) != cudaSuccess ||
+      (e = setup_g<128, 32>(n2)) != cudaSuccess || (e = setup_g<128, 128>(n2)) != cudaSuccess ||
+      (e = setup_g<32, 128>(n2)) != cudaSuccess)
+    return e;
   if ((e = cudaFuncSetAttribute(k_conv2_tc<64, 64, C2_BIAS_RELU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)convg64_smem_bytes(n2))) != cudaSuccess)
     return e;
@@ -520,6 +551,11 @@ cudaError_t launch_convg_tc(int cin, int cout, const CUtensorMap* tm, const void
   if (cin == 64 && cout == 64) return launch_g<64, 64>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
   if (cin == 32 && cout == 32) return launch_g<32, 32>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
   if (cin == 32 && cout == 64) return launch_g<32, 64>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
+  if (cin == 64 && cout == 128) return launch_g<64, 128>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
+  if (cin == 128 && cout == 64) return launch_g<128, 64>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
+  if (cin == 128 && cout == 32) return launch_g<128, 32>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
+  if (cin == 128 && cout == 128) return launch_g<128, 128>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
+  if (cin == 32 && cout == 128) return launch_g<32, 128>(tm, wpack, bias, batch, n1, n2, out, num_sms, st);
   return cudaErrorInvalidValue;
 }
 

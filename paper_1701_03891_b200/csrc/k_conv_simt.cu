@@ -205,6 +205,12 @@ cudaError_t launch_convg_simt(int cin, int cout, const float* in, const float* w
   if (cin == 32 && cout == 64) return launch_wide<float, float, 32, 64, 16, 2>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
   if (cin == 64 && cout == 32) return launch_wide<float, float, 64, 32, 8, 2>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
   if (cin == 64 && cout == 64) return launch_wide<float, float, 64, 64, 16, 2>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  // width 128 (custom stacks, NEXT-3)
+  if (cin == 32 && cout == 128) return launch_wide<float, float, 32, 128, 32, 1>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  if (cin == 64 && cout == 128) return launch_wide<float, float, 64, 128, 32, 1>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  if (cin == 128 && cout == 128) return launch_wide<float, float, 128, 128, 32, 1>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  if (cin == 128 && cout == 64) return launch_wide<float, float, 128, 64, 16, 2>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
+  if (cin == 128 && cout == 32) return launch_wide<float, float, 128, 32, 8, 2>(in, wx, bias, 0, 1, out, batch, n1, n2, st);
   return cudaErrorInvalidValue;
 }
 
@@ -216,6 +222,11 @@ cudaError_t launch_dgrad_simt(int cin, int cout, const float* dG, const float* w
   if (cout == 32 && cin == 64) return launch_wide<float, float, 32, 64, 16, 2>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
   if (cout == 64 && cin == 32) return launch_wide<float, float, 64, 32, 8, 2>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
   if (cout == 64 && cin == 64) return launch_wide<float, float, 64, 64, 16, 2>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  if (cout == 128 && cin == 32) return launch_wide<float, float, 128, 32, 8, 2>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  if (cout == 128 && cin == 64) return launch_wide<float, float, 128, 64, 16, 2>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  if (cout == 128 && cin == 128) return launch_wide<float, float, 128, 128, 32, 1>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  if (cout == 64 && cin == 128) return launch_wide<float, float, 64, 128, 32, 1>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
+  if (cout == 32 && cin == 128) return launch_wide<float, float, 32, 128, 32, 1>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
   if (cout == 1 && cin == 32) return launch_wide<float, float, 1, 32, 8, 1>(dG, wt, nullptr, 0, 0, dX, batch, n1, n2, st, X);
   return cudaErrorInvalidValue;
 }

@@ -10,6 +10,8 @@
 //                        flipped weights and the previous activation as mask: k_conv_simt.cu)
 // Reductions over pixels are two-level and deterministic: fp32 per block over its pixel tiles, then fp64 over
 // blocks in a fixed order (k_wgrad_reduce).
+#include <algorithm>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -304,7 +306,7 @@ cudaError_t launch_wgrad(int layer, const float* X, const float* dG, int batch, 
 static int wgrad_layer_chunks(int cin, int cout) {   // WGRAD_CHUNKS / (blocks per chunk of the instance below)
   if (cin == 1) return WGRAD_CHUNKS / (cout == 32 ? 2 : 4);
   if (cout == 1) return WGRAD_CHUNKS / 4;
-  return WGRAD_CHUNKS / ((cin / 8) * (cout / 8));
+  return std::max(1, WGRAD_CHUNKS / ((cin / 8) * (cout / 8)));
 }
 cudaError_t launch_wgrad_layer(int cin, int cout, const float* X, const float* dG, int batch, int n1, int n2,
                                float* part_w, float* part_b, int flip, float* gw, float* gb, cudaStream_t st) {
@@ -316,6 +318,11 @@ cudaError_t launch_wgrad_layer(int cin, int cout, const float* X, const float* d
   if (cin == 64 && cout == 32) return wgrad<64, 32, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
   if (cin == 64 && cout == 64) return wgrad<64, 64, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
   if (cin == 32 && cout == 1) return wgrad<32, 1, 8, 1>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 32 && cout == 128) return wgrad<32, 128, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 64 && cout == 128) return wgrad<64, 128, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 128 && cout == 128) return wgrad<128, 128, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 128 && cout == 64) return wgrad<128, 64, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
+  if (cin == 128 && cout == 32) return wgrad<128, 32, 8, 8>(X, dG, batch, n1, n2, C, part_w, part_b, flip, gw, gb, st);
   return cudaErrorInvalidValue;
 }
 // scratch floats launch_wgrad_layer needs: part_w (chunks x weights of the layer); part_b needs chunks x cout
