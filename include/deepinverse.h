@@ -85,10 +85,12 @@ typedef struct {
   int n_layers;          /* 0: the paper's three layers w1..b3.  >= 2: the custom stack `layers` (w1..b3 unused):
                             layers[0].cin = 1, layers[n-1].cout = 1, layers[i].cin = layers[i-1].cout.  Supported
                             (FP32, TF32 and BF16 contexts, per-channel biases): first layer 1 -> {32, 64},
-                            interior layers {32, 64} -> {32, 64}, last layer 32 -> 1; TF32 also needs
+                            interior layers {32, 64} -> {32, 64} (FP32 and BF16 also
+                            128 on either side: "larger capacity"), last layer 32 -> 1; TF32 also needs
                             n2 % 4 == 0.  Other shapes or DI_FLAG_FULLMAP_BIAS: DI_ERR_ARG.  Custom stacks support
-                            di_recover / di_recover_host / di_recover_from_proxy / sensing / metrics; training and
-                            di_debug_stage stages >= 1 are for the paper's stack only (DI_ERR_ARG).            */
+                            di_recover / di_recover_host / di_recover_from_proxy / sensing / metrics and training
+                            (per-channel or zero biases); di_debug_stage stages >= 1 are for the paper's stack
+                            only (DI_ERR_ARG).                                                                   */
   const di_layer* layers;
 } di_create_args;
 
