@@ -109,3 +109,28 @@ def test_instrumentation_macros_refused_outside_experiment_build():
     assert bad.returncode != 0 and "DI_EXPERIMENT_BUILD" in bad.stderr
     ok = subprocess.run(base + ["-DDI_PROF_CONV2", "-DDI_EXPERIMENT_BUILD"], capture_output=True, text=True)
     assert ok.returncode == 0, ok.stderr[-2000:]
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+    from paper_1701_03891_b200 import build
+    build.build()
+    exe = str(tmp_path / "recover_c")
+    libdir = os.path.dirname(build.LIB)
+    r = subprocess.run(["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "recover.c"), "-L", libdir, "-ldeepinverse",
+                        f"-Wl,-rpath,{libdir}", "-lm", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_example_builds_and_refuses_without_gpu(tmp_path):
+    """examples/recover.c: the header is plain C (gcc -std=c99 -Werror) and the library links from C; without an
+    sm_100 device di_create returns DI_ERR_DEVICE (exit 2) -- there is no CPU fallback."""
+    import subprocess
+    import torch
+    exe = _build_c_example(tmp_path)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: tests/test_gpu_parity.py::test_c_example_on_gpu runs it")
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 2 and "DI_ERR_DEVICE" in r.stderr

@@ -407,3 +407,15 @@ def test_proxy_on_cta_pairs(monkeypatch, n, m, batch):
     err = np.abs(outs[0][rows] - ref)
     assert np.all(err <= 2.0 ** -8 * np.abs(ref) + 2.0 ** -14 * S), float(err.max())
     assert np.array_equal(outs[0], outs[1]), "pair kernel differs from the one-CTA kernel"
+
+
+def test_c_example_on_gpu(tmp_path):
+    """The C ABI from plain C (examples/recover.c, host buffers through di_recover_host): y = 0 -> 0 and x_hat(2y) =
+    2 x_hat(y) bitwise, synchronous argument errors."""
+    import json
+    import subprocess
+    from test_abi import _build_c_example
+    r = subprocess.run([_build_c_example(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    d = json.loads(r.stdout)
+    assert d["homogeneity_and_zero_mismatches"] == 0 and d["arg_errors_ok"] == 1 and d["norm"] > 0
