@@ -217,6 +217,17 @@ __global__ void __launch_bounds__(256, 1)
       for (int j = 0; j < nu; ++j, ++pi) {
         const int r0 = (rb0 + j) * R;
         const int a = pi % NACC;
+        // METRICS: the ground truth of this lane's outputs, loaded before the accumulator wait so the global-load
+        // latency overlaps it (a load consumed in the output loop serialises the epilogue: 0.71 vs 0.38 ms)
+        float tv[2 * RPW];
+        if (METRICS) {
+#pragma unroll
+          for (int h = 0; h < 2 * RPW; ++h) {
+            const int jc = lane + 32 * (h & 1), row = r0 + RPW * q + (h >> 1);
+            tv[h] = (jc < g.wseg && c0 + jc < g.n2 && row < g.n1)
+                        ? __ldg(xtrue + ((size_t)b * g.n1 + row) * g.n2 + c0 + jc) : 0.f;
+          }
+        }
         mbar_wait(&acc_full[a], (pi / NACC) & 1);
         tc_fence_after();
         const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32) << 16);
@@ -249,7 +260,7 @@ __global__ void __launch_bounds__(256, 1)
             if (relu) acc = fmaxf(acc, 0.f);
             xhat[pix] = acc;
             if (METRICS) {
-              const float t = __ldg(xtrue + pix);
+              const float t = tv[h];
               const double dd = (double)acc - (double)t;
               m_se += dd * dd, m_sx += (double)t * (double)t, m_mx = fmaxf(m_mx, t);
             }
