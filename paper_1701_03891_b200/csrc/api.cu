@@ -157,6 +157,7 @@ struct di_ctx_s {
   const float* m_xtrue = nullptr;
   double* m_out = nullptr;
   double* mpart = nullptr;      // per-item metric partials of k_conv3_r4 (allocated on first use, max_batch)
+  bool fused_metrics = false;   // di_recover_metrics through k_conv3_r4<true> (DI_EXP_FUSED_METRICS=1 at di_create)
   bool has_tmX = false;
   int last_launches = 0;
   bool profiling = false;
@@ -971,6 +972,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, a->device);
   // read once per context, never on the launch path (A/B switches of the multicast cluster)
   c->conv2_cluster = getenv("DI_EXP_NO_MC") ? 1 : (getenv("DI_EXP_C2_CLUSTER") ? atoi(getenv("DI_EXP_C2_CLUSTER")) : 2);
+  c->fused_metrics = getenv("DI_EXP_FUSED_METRICS") != nullptr && atoi(getenv("DI_EXP_FUSED_METRICS")) != 0;
 #ifdef DI_DEBUG
   {
     di_status sd = debug_bind();
@@ -1263,7 +1265,10 @@ di_status di_recover_metrics(di_ctx c, const void* y, long long ldy, int batch, 
   DevGuard dg_(c->device);
   if (!dg_.ok) return fail(DI_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const bool fused = c->prec == DI_PREC_BF16 && c->stack.empty();
+  // The fused epilogue (k_conv3_r4<true>) measured slower than recover + the separate k_metrics pass (7.64 vs 7.60 ms
+  // per 4096 64x64 images: the fp64 sums lengthen conv3's epilogue, which is on its critical path), so it runs only
+  // when the context was created with DI_EXP_FUSED_METRICS=1 (A/B)
+  const bool fused = c->fused_metrics && c->prec == DI_PREC_BF16 && c->stack.empty();
   if (fused) {
     if (!c->mpart)
       CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->mpart),
