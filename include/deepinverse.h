@@ -161,9 +161,10 @@ di_status di_add_noise(di_ctx ctx, void* y, long long ldy, int batch, double snr
                        void* stream);
 di_status di_metrics(di_ctx ctx, const float* xhat, const float* x, int batch, double* out, void* stream);
 /* di_recover_metrics: di_recover followed by di_metrics on the same batch (the Monte-Carlo loop of PAPER.md:159-160,
- *               Figs. 2-4), with the metrics FUSED into conv layer 3's epilogue on the BF16 path (each output is compared
- *               with x_true as it is written; per-item fp64 partials combined in a fixed order, so the result is
- *               deterministic) and computed by the separate di_metrics pass otherwise.  y, ldy, batch, xhat: as
+ *               Figs. 2-4).  By default the metrics are the separate di_metrics pass; a context created with the
+ *               environment variable DI_EXP_FUSED_METRICS=1 computes them inside conv layer 3's epilogue on the BF16
+ *               path instead (each output compared with x_true as it is written; per-item fp64 partials combined in
+ *               a fixed order, deterministic) -- measured slower on B200.  y, ldy, batch, xhat: as
  *               di_recover; x_true: DEVICE [batch][n1][n2] fp32 ground truth; metrics: DEVICE [3][batch] double as
  *               di_metrics.  Errors as di_recover; DI_ERR_ARG if x_true or metrics is NULL. */
 di_status di_recover_metrics(di_ctx ctx, const void* y, long long ldy, int batch, const float* x_true, float* xhat,

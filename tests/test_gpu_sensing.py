@@ -73,13 +73,18 @@ def test_metrics_match_oracle():
 
 @pytest.mark.parametrize("precision,n1,n2,batch", [("bf16", 64, 64, 300), ("bf16", 40, 130, 5), ("bf16", 9, 13, 3),
                                                    ("bf16", 64, 64, 1), ("tf32", 32, 32, 6), ("f32", 16, 16, 4)])
-def test_recover_metrics_fused(precision, n1, n2, batch):
-    """di_recover_metrics: the metrics fused into conv layer 3's epilogue (BF16; items = whole image columns, several
-    column segments at n2 = 130, split columns at batch 1) equal the oracle's metrics of the GPU's own x_hat, the
-    x_hat is bitwise the di_recover result, and the result is bitwise repeatable (fixed-order reduction)."""
+@pytest.mark.parametrize("fused", [True, False])
+def test_recover_metrics_fused(monkeypatch, fused, precision, n1, n2, batch):
+    """di_recover_metrics: the metrics fused into conv layer 3's epilogue (BF16 with DI_EXP_FUSED_METRICS=1; items =
+    whole image columns, several column segments at n2 = 130, split columns at batch 1) or the separate pass equal
+    the oracle's metrics of the GPU's own x_hat, the x_hat is bitwise the di_recover result, and the result is
+    bitwise repeatable (fixed-order reduction)."""
     import torch
     case = Case(n1, n2, max(1, n1 * n2 // 8), batch, precision, 6, 3)
+    if fused:
+        monkeypatch.setenv("DI_EXP_FUSED_METRICS", "1")
     ctx = make_ctx(case)
+    monkeypatch.delenv("DI_EXP_FUSED_METRICS", raising=False)
     y = torch.from_numpy(case.y).cuda().to(ctx.storage_dtype)
     x = torch.from_numpy(case.x).cuda()
     xhat, got = ctx.recover_metrics(y, x)
