@@ -1,20 +1,18 @@
 // k_conv3_r4.cu -- stage 3 of the bf16 path, conv layer 3 (1 filter 11x11x32 + bias, ReLU iff DI_FLAG_FINAL_RELU,
-// crop S) with RP = 4 or 8 OUTPUT ROWS STACKED IN M (C3R_RP in kernels.cuh; 8 by default --
-// the description below is for 4: with 8, M = 8 rows x 16 (11 column taps), 18 windows, stack entries of 16 rows).
+// crop S) with RP = 11 OUTPUT ROWS STACKED IN M.
 //
 // C_out = 1 leaves the UMMA M dimension to the taps.  The first design (k_conv3_tc) stacks the 11 column taps of one
 // tap row in M = 32 (.ws) and walks the 11 tap rows as K-blocks, so every strip position is read by 11 MMAs per
-// 246 outputs and the tensor core's shared-memory reads bound it (0.87 ms at lowrate).  Here M = 128 = RP output rows
-// t x ES rows (11 column taps v, padded): window k (k = 0 .. RP + 9) is the strip shifted by k rows, and rows (t, .)
-// of its A operand hold the taps of tap row u = k - t, so that
-//   D[(t, v)][n] = sum_k sum_c W[k - t][v][c] strip[n + k P][c]  and  x_hat[row RP p + t][j] = sum_v D[(t, v)][j + v].
+// 246 outputs and the tensor core's shared-memory reads bound it (0.87 ms at lowrate).  Here M = 128 holds RP = 11
+// output rows t x ES = 11 rows (the column taps v; 121 of the 128 rows used): window k (k = 0 .. RP + 9) is the strip
+// shifted by k rows, and rows (t, .) of its A operand hold the taps of tap row u = k - t, so that
+//   D[(t, v)][n] = sum_k sum_c W[k - t][v][c] strip[n + k P][c]  and  x_hat[row t][j] = sum_v D[(t, v)][j + v].
 // A_k = [W[k]; W[k-1]; ...; W[k-RP+1]] is a 128-row window of ONE stack T[i] = W[10 - i] (zero outside 0..10): A_k
-// starts at T[10 - k], the whole bank stays resident in shared memory, and a window is a descriptor start address.
-// N = P rounded up to 16 (<= 80) covers one strip row.  RP = 8 (ES = 16): per 8 x 64 outputs 18 windows x 2 MMAs
-// (K = 16) of 6.5 KB of operands -- 0.07 MMAs per output against 0.09 (k_conv3_tc) and 0.11 (RP = 4): 0.43 ms.
-// Each epilogue warp owns RPW = 32 / ES output rows (its TMEM quadrant) and sums their 11 diagonals through a
-// private shared-memory tile.  (Streaming the strip one row per window instead, with RP = 11, measured slower: the
-// per-window barrier handshake bounds the single issuing thread.)
+// starts at T[10 - k] (an 11-row entry: any 64-B row may start a SWIZZLE_64B window, tools/ladder.cu t3/t11), the
+// whole bank stays resident in shared memory, and a window is a descriptor start address.  N = P rounded up to 16
+// (<= 80) covers one strip row: per 11 x 64 outputs 21 windows x 2 MMAs (K = 16) -- 0.060 MMAs per output against
+// 0.070 with 8 rows x 16-row entries (r02: 0.40 ms) and 0.09 for k_conv3_tc.  The 121 tap rows do not align with
+// the TMEM lane quadrants, so the four epilogue warps share one tile (see the epilogue).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -30,11 +28,10 @@ namespace di {
 
 namespace {
 constexpr int RP = C3R_RP, ES = C3R_ES, NWIN = C3R_NWIN, IMIN = C3R_IMIN;
-constexpr int R = 8;                   // output rows per unit (one pass: R == RP)
-static_assert(R == RP, "one pass per unit");
-constexpr int CH = 8;                  // strip rows per TMA chunk
-constexpr int NCH = 4;                 // chunk slots in the ring: a unit reads 3 chunks, the 4th loads ahead
-constexpr int RING_ROWS = NCH * CH;   // ring rows (power of two)
+constexpr int R = RP;                  // output rows per unit (one pass)
+constexpr int CH = R;                  // strip rows per TMA chunk (chunk k = strip rows [R k - 5, R k + R - 5))
+constexpr int NSPAN = (R + 10 + CH - 1) / CH;   // chunks a unit reads (R + 10 strip rows): 2 for R = 11
+constexpr int NCH = NSPAN + 1;         // chunk slots in the ring: one loads while a unit computes
 constexpr int NACC = 4;                // TMEM accumulator slots (128 columns each)
 #ifndef DI_C3R_PF
 #define DI_C3R_PF 6
@@ -44,8 +41,8 @@ constexpr int TBLK = ES * 64;          // one T entry: ES rows (v) x 32 channels
 constexpr int TBYTES = (C3R_NENT * TBLK + 1023) & ~1023;
 constexpr int GUARD = 16;              // zero positions past the ring (the last ring row's window reads N - P past it)
 constexpr int SROW = 84;               // epilogue tile row stride (floats): 16-B rows
-constexpr int RPW = 32 / ES;           // output rows per epilogue warp (its TMEM quadrant)
-constexpr int SWARP = RPW * 11 * SROW; // per epilogue warp
+constexpr int SROWS = RP * ES;         // TMEM lanes holding taps (121 of 128 for RP = ES = 11)
+constexpr int OPT = (RP * 64 + 127) / 128;   // outputs per epilogue thread and unit
 
 // Work item = one column segment of one image (or a contiguous part of its row blocks when there are fewer
 // columns than SMs): its units run top to bottom, so consecutive units share 10 of their 18 strip rows.
@@ -119,7 +116,7 @@ __global__ void __launch_bounds__(256, 1)
       auto prefetch_next = [&]() {
         if (pit >= g.items) return;
         tma_prefetch_l2_4d(&tmH2, 0, pc0 - 5, CH * (prb0 + pk) - 5, pb);
-        if (++pk == pnu + 2) {
+        if (++pk == pnu + NSPAN - 1) {
           pk = 0, pit += gridDim.x;
           if (pit < g.items) item_of(g, pit, pb, pc0, prb0, pnu);
         }
@@ -129,7 +126,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
         int b, c0, rb0, nu;
         item_of(g, it, b, c0, rb0, nu);
-        for (int k = 0; k < nu + 2; ++k, ++gc) {
+        for (int k = 0; k < nu + NSPAN - 1; ++k, ++gc) {
           const uint32_t sl = gc % NCH;
           if (gc >= NCH) mbar_wait(&cempty[sl], ((gc / NCH) - 1) & 1);
           mbar_arrive_expect_tx(&cfull[sl], chunk_bytes);
@@ -161,13 +158,13 @@ __global__ void __launch_bounds__(256, 1)
       for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
         int b, c0, rb0, nu;
         item_of(g, it, b, c0, rb0, nu);
-        for (int k = 0; k < 2; ++k) {   // the item's first two chunks
+        for (int k = 0; k < NSPAN - 1; ++k) {   // the item's first chunks
           const uint32_t c = gc0 + k;
           C3P0 mbar_wait(&cfull[c % NCH], (c / NCH) & 1); C3P1(pc_chunk)
         }
         for (int j = 0; j < nu; ++j, ++pi) {
           const uint32_t cj = gc0 + j;
-          C3P0 mbar_wait(&cfull[(cj + 2) % NCH], ((cj + 2) / NCH) & 1); C3P1(pc_chunk)
+          C3P0 mbar_wait(&cfull[(cj + NSPAN - 1) % NCH], ((cj + NSPAN - 1) / NCH) & 1); C3P1(pc_chunk)
           tc_fence_after();
           const int a = pi % NACC;
           if (pi >= NACC) {
@@ -192,11 +189,10 @@ __global__ void __launch_bounds__(256, 1)
             if (k == kwrap) bd -= ringstep;
           }
           umma_commit(&acc_full[a]);
-          umma_commit(&cempty[cj % NCH]);                     // chunk j is read by units j - 2 .. j only
+          umma_commit(&cempty[cj % NCH]);                     // chunk j is read by units j - NSPAN + 1 .. j only
         }
-        umma_commit(&cempty[(gc0 + nu) % NCH]);               // the item's last two chunks
-        umma_commit(&cempty[(gc0 + nu + 1) % NCH]);
-        gc0 += nu + 2;
+        for (int k = 0; k < NSPAN - 1; ++k) umma_commit(&cempty[(gc0 + nu + k) % NCH]);   // the item's last chunks
+        gc0 += nu + NSPAN - 1;
       }
 #ifdef DI_PROF_CONV3
       if (blockIdx.x % 37 == 0)
@@ -204,9 +200,11 @@ __global__ void __launch_bounds__(256, 1)
                clock64() - pc0, pc_chunk, pc_acc, pi);
 #endif
     }
-  } else if (warp >= 4) {  // ------------------------------- epilogue: warp q = output rows RPW q .. RPW q + RPW - 1
-    const int q = warp - 4;
-    float* const Sq = S + q * SWARP;
+  } else if (warp >= 4) {  // ---------------------------------------------------------------------- epilogue
+    // The RP x ES tap rows do not align with the 32-lane TMEM quadrants (ES = 11), so the four warps write their
+    // quadrants into ONE shared tile S[lane][column] and then sum the 11 diagonals of every output from it:
+    // x_hat[row t][j] = sum_v S[t ES + v][j + v] -- 128 threads, consecutive j per warp (conflict-free).
+    const int q = warp - 4, e = threadIdx.x - 128;
     const float bsc = (!fullmap && bias) ? bias[0] : 0.f;
     int pi = 0;
     for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
@@ -217,14 +215,14 @@ __global__ void __launch_bounds__(256, 1)
       for (int j = 0; j < nu; ++j, ++pi) {
         const int r0 = (rb0 + j) * R;
         const int a = pi % NACC;
-        // METRICS: the ground truth of this lane's outputs, loaded before the accumulator wait so the global-load
-        // latency overlaps it (a load consumed in the output loop serialises the epilogue: 0.71 vs 0.38 ms)
-        float tv[2 * RPW];
+        // METRICS: the ground truth of this thread's outputs, loaded before the accumulator wait so the global-load
+        // latency overlaps it
+        float tv[OPT];
         if (METRICS) {
 #pragma unroll
-          for (int h = 0; h < 2 * RPW; ++h) {
-            const int jc = lane + 32 * (h & 1), row = r0 + RPW * q + (h >> 1);
-            tv[h] = (jc < g.wseg && c0 + jc < g.n2 && row < g.n1)
+          for (int h = 0; h < OPT; ++h) {
+            const int idx = e + 128 * h, t = idx >> 6, jc = idx & 63, row = r0 + t;
+            tv[h] = (idx < RP * 64 && jc < g.wseg && c0 + jc < g.n2 && row < g.n1)
                         ? __ldg(xtrue + ((size_t)b * g.n1 + row) * g.n2 + c0 + jc) : 0.f;
           }
         }
@@ -239,34 +237,37 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[a]);
-        if ((lane % ES) < 11) {   // S row (lane / ES) * 11 + v: tap v of output row RPW q + lane / ES
-          float4* dst = reinterpret_cast<float4*>(Sq + ((lane / ES) * 11 + lane % ES) * SROW);
+        named_bar(1, 128);          // the previous unit's sums are done with S
+        const int L = q * 32 + lane;
+        if (L < SROWS) {
+          float4* dst = reinterpret_cast<float4*>(S + L * SROW);
 #pragma unroll
           for (int jj = 0; jj < 20; ++jj)
             dst[jj] = make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
                                   __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
         }
-        __syncwarp();
+        named_bar(1, 128);          // S holds every tap row of this unit
 #pragma unroll
-        for (int h = 0; h < 2 * RPW; ++h) {
-          const int jc = lane + 32 * (h & 1), tr = h >> 1;
-          const int row = r0 + RPW * q + tr;
+        for (int h = 0; h < OPT; ++h) {
+          const int idx = e + 128 * h, t = idx >> 6, jc = idx & 63;
+          if (idx >= RP * 64) break;
+          const int row = r0 + t;
+          const float* sr = S + t * ES * SROW + jc;
           float acc = 0.f;
 #pragma unroll
-          for (int v = 0; v < 11; ++v) acc += Sq[(tr * 11 + v) * SROW + jc + v];
+          for (int v = 0; v < 11; ++v) acc += sr[v * SROW + v];
           if (jc < g.wseg && c0 + jc < g.n2 && row < g.n1) {
             const size_t pix = ((size_t)b * g.n1 + row) * g.n2 + c0 + jc;
             acc += (fullmap && bias) ? bias[pix % ((size_t)g.n1 * g.n2)] : bsc;
             if (relu) acc = fmaxf(acc, 0.f);
             xhat[pix] = acc;
             if (METRICS) {
-              const float t = tv[h];
-              const double dd = (double)acc - (double)t;
-              m_se += dd * dd, m_sx += (double)t * (double)t, m_mx = fmaxf(m_mx, t);
+              const float tt = tv[h];
+              const double dd = (double)acc - (double)tt;
+              m_se += dd * dd, m_sx += (double)tt * (double)tt, m_mx = fmaxf(m_mx, tt);
             }
           }
         }
-        __syncwarp();
       }
       if (METRICS) {   // the warp's sums for this item, butterfly order fixed
         for (int o = 16; o > 0; o >>= 1) {
@@ -307,7 +308,7 @@ static size_t smem_r4(int n2) {
   const int wseg = n2 < 64 ? n2 : 64, P = wseg + 10;
   const size_t slot = ((size_t)CH * P * 64 + 1023) & ~(size_t)1023;
   const size_t ring_alloc = (NCH * slot + GUARD * 64 + 1023) & ~(size_t)1023;
-  return TBYTES + ring_alloc + 4 * SWARP * 4 + 1024;
+  return TBYTES + ring_alloc + (size_t)SROWS * SROW * 4 + 1024;
 }
 
 int conv3_r4_box_rows() { return CH; }

@@ -121,11 +121,8 @@ cudaError_t launch_conv3_simt(const void* h2, bool bf16, const float* wx, const 
 int conv3_tc_box_rows();
 // bf16 conv layer 3 with C3R_RP output rows stacked in M (k_conv3_r4.cu); tpack: the tap-row stack T (api.cu
 // conv3_r4_pack): C3R_NENT entries T[C3R_IMIN + e] of C3R_ES rows (column taps, 11 valid) x 32 channels bf16
-#ifndef DI_C3R_RP
-#define DI_C3R_RP 8
-#endif
-constexpr int C3R_RP = DI_C3R_RP;               // output rows per pass: 4 or 8
-constexpr int C3R_ES = 128 / C3R_RP;            // M rows per output row
+constexpr int C3R_RP = 11;                      // output rows per pass (= per unit)
+constexpr int C3R_ES = 11;                      // M rows per output row: the 11 column taps (121 of 128 rows used)
 constexpr int C3R_NWIN = C3R_RP + 10;           // windows (strip rows) per pass
 constexpr int C3R_IMIN = 11 - C3R_NWIN;
 constexpr int C3R_NENT = C3R_NWIN + C3R_RP - 1;
