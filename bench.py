@@ -484,7 +484,7 @@ def run_ours(args):
         ctx.recover(y_dev, xhat)                           # the timed loop's output, once more, for the gather
         parts = gather_to_all(xhat, world)
         if rank == 0:
-            line["gather_check"] = output_check(ctx, c, prec, B, world, parts, dev, args.no_oracle_check)
+            line["gather_check"] = output_check(ctx, c, prec, B, world, parts, dev, args.no_oracle_check, phi, params)
             ok = line["gather_check"]["pass"] and bool(torch.equal(xhat_last, xhat))
             line["gather_check"]["repeat_bitwise"] = bool(torch.equal(xhat_last, xhat))
         del parts
@@ -508,7 +508,7 @@ def run_ours(args):
     return 0 if ok else 1
 
 
-def output_check(ctx, c, prec, B, world, parts, dev, no_oracle=False) -> dict:
+def output_check(ctx, c, prec, B, world, parts, dev, no_oracle=False, phi=None, params=None) -> dict:
     """Rank 0: bitwise equality of every rank's gathered x_hat with rank 0's own recovery of the same global images
     (first and last 32 of each block), and the oracle's rel-L2 / element-wise error on 2 + 2 of them per rank."""
     import torch
@@ -518,7 +518,7 @@ def output_check(ctx, c, prec, B, world, parts, dev, no_oracle=False) -> dict:
     tol = {"bf16": 2e-2, "tf32": 2e-2, "f32": 1e-5}[prec]
     for r in range(world):
         lo = r * B
-        phi, x, y, params = make_inputs_rows(c, prec, [lo + i for i in rows])
+        phi, x, y, params = make_inputs_rows(c, prec, [lo + i for i in rows], phi, params)
         yd = torch.from_numpy(y).to(device=dev, dtype=ctx.storage_dtype)
         mine = ctx.recover(yd).cpu().numpy()
         got = parts[r][rows].cpu().numpy()
@@ -537,11 +537,13 @@ def output_check(ctx, c, prec, B, world, parts, dev, no_oracle=False) -> dict:
             "tol": tol, "pass": ok}
 
 
-def make_inputs_rows(c, prec: str, idx: list[int]):
-    """Seeded inputs for an arbitrary list of global image indices (contiguous runs generated together)."""
+def make_inputs_rows(c, prec: str, idx: list[int], phi=None, params=None):
+    """Seeded inputs for an arbitrary list of global image indices (contiguous runs generated together); phi / params
+    may be passed in when the caller already generated them (they depend only on the seed)."""
     import synth
     st = "bf16" if prec == "bf16" else "f32"
-    phi = synth.make_phi(c.m, c.N, st)
+    if phi is None:
+        phi = synth.make_phi(c.m, c.N, st)
     xs, run = [], [idx[0]]
     for i in idx[1:] + [None]:
         if i is not None and i == run[-1] + 1:
@@ -552,7 +554,7 @@ def make_inputs_rows(c, prec: str, idx: list[int]):
             run = [i]
     x = np.concatenate(xs)
     y = synth.measure(phi, x, st)
-    return phi, x, y, synth.make_params().rounded(st)
+    return phi, x, y, (params if params is not None else synth.make_params().rounded(st))
 
 
 def cpu_model() -> str:
