@@ -89,6 +89,7 @@ float bf2f(uint16_t b) {
 
 struct di_ctx_s {
   int device = 0, num_sms = 0;
+  int conv2_balanced = 1;       // conv2 tiles share a unit's outputs evenly (DI_EXP_C2_SPLIT=253 at di_create: 253 + rest)
   int conv2_cluster = 2;        // conv2 weight-multicast cluster (DI_EXP_NO_MC=1 -> 1, DI_EXP_C2_CLUSTER=4 -> 4 at di_create)
   int m = 0, n1 = 0, n2 = 0, N = 0, max_batch = 0, kpad = 0;
   int pxbn = 256;               // pixel-tile width of the lifting GEMM = row count of a Phi^T block
@@ -792,7 +793,8 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
         if (s != DI_OK) return s;
         tmp = &tm;
       }
-      CUDA_TRY(di::launch_conv2_tc(tmp, c->wp2, c->b2, fm, batch, c->n1, c->n2, h2, c->num_sms, st, c->conv2_cluster));
+      CUDA_TRY(di::launch_conv2_tc(tmp, c->wp2, c->b2, fm, batch, c->n1, c->n2, h2, c->num_sms, st, c->conv2_cluster,
+                                   c->conv2_balanced));
     } else if (c->prec == DI_PREC_TF32) {
       CUtensorMap tm;
       const CUtensorMap* tmp = &c->tmH1;
@@ -973,6 +975,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   // read once per context, never on the launch path (A/B switches of the multicast cluster)
   c->conv2_cluster = getenv("DI_EXP_NO_MC") ? 1 : (getenv("DI_EXP_C2_CLUSTER") ? atoi(getenv("DI_EXP_C2_CLUSTER")) : 2);
   c->fused_metrics = getenv("DI_EXP_FUSED_METRICS") != nullptr && atoi(getenv("DI_EXP_FUSED_METRICS")) != 0;
+  c->conv2_balanced = !(getenv("DI_EXP_C2_SPLIT") && atoi(getenv("DI_EXP_C2_SPLIT")) == 253);
 #ifdef DI_DEBUG
   {
     di_status sd = debug_bind();

@@ -61,7 +61,15 @@ constexpr int C2_DG_ROWS = 11;
 
 struct Geo {
   int n1, n2, wseg, P, nrb, ncs, units;
+  int balanced;   // 1: a unit's tiles share its outputs evenly (2 x 205 at 64 x 64); 0: 253 + the rest
 };
+// Tile t of a unit with L output positions: [n0, n0 + cnt).  Balanced tiles give every tile the same MMA length,
+// so the weight stream (33 K-blocks per tile, whatever its width) is consumed at one even rate instead of a burst
+// during the short second tile.
+__device__ __forceinline__ int tile_span(const Geo& g, int L, int& ntiles) {
+  ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
+  return g.balanced ? (L + ntiles - 1) / ntiles : OUT_PER_TILE;
+}
 
 __host__ __device__ inline int strip_rows_bytes(int P) { return (R + 10) * P * 128; }   // the largest (C_in = 64)
 }  // namespace
@@ -150,7 +158,8 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
         const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
         const int rows = min(R, g.n1 - r0);
         const int L = (rows - 1) * g.P + g.wseg;
-        const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
+        int ntiles;
+        tile_span(g, L, ntiles);
         for (int t = 0; t < ntiles; ++t)
          for (int h = 0; h < NH; ++h) {
           if (NH > 1 || t == 0) {   // the unit's strip (C_in = 128: channel half h, per tile)
@@ -200,10 +209,11 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
         const int r0 = (rem / g.ncs) * R;
         const int rows = min(R, g.n1 - r0);
         const int L = (rows - 1) * g.P + g.wseg;
-        const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
+        int ntiles;
+        const int span = tile_span(g, L, ntiles);
         for (int t = 0; t < ntiles; ++t, ++ti) {
-          const int n0 = t * OUT_PER_TILE;
-          const int cnt = min(OUT_PER_TILE, L - n0);
+          const int n0 = t * span;
+          const int cnt = min(span, L - n0);
           const int nmma = min(NT, (cnt + TAPS - 1 + 15) & ~15);
           const uint32_t idesc = idesc_f32acc(1, 128, nmma);
           const int buf = ti & 1;
@@ -278,10 +288,11 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
       const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
       const int rows = min(R, g.n1 - r0);
       const int L = (rows - 1) * g.P + g.wseg;
-      const int ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
+      int ntiles;
+      const int span = tile_span(g, L, ntiles);
       for (int t = 0; t < ntiles; ++t, ++ti) {
-        const int n0 = t * OUT_PER_TILE;
-        const int cnt = min(OUT_PER_TILE, L - n0);
+        const int n0 = t * span;
+        const int cnt = min(span, L - n0);
         const int buf = ti & 1;
         if (EG == 2 && buf != grp) continue;
         mbar_wait(&tfull[buf], (ti >> 1) & 1);
@@ -378,6 +389,7 @@ static Geo make_geo(int batch, int n1, int n2, int R = C2_ROWS) {
   g.nrb = (n1 + R - 1) / R;
   g.ncs = (n2 + g.wseg - 1) / g.wseg;
   g.units = batch * g.nrb * g.ncs;
+  g.balanced = 1;
   return g;
 }
 
@@ -479,8 +491,9 @@ cudaError_t setup_conv2_tc(int n2) {
 // cluster: weight-multicast cluster size (the context's setting, read once by di_create: 2 by default, DI_EXP_NO_MC=1
 // -> 1, DI_EXP_C2_CLUSTER=4 -> 4); falls back to smaller clusters when the balance / co-residency checks fail
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
-                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, int cluster) {
+                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, int cluster, int balanced) {
   Geo g = make_geo(batch, n1, n2);
+  g.balanced = balanced;
   const int grid = g.units < num_sms ? g.units : num_sms;
   const size_t sm = conv2_tc_smem_bytes(n2);
   const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(wpack);

@@ -98,7 +98,8 @@ cudaError_t setup_convg_tc(int n2);
 cudaError_t launch_convg_tc(int cin, int cout, const CUtensorMap* tm, const void* wpack, const float* bias, int batch,
                             int n1, int n2, void* out, int num_sms, cudaStream_t st);
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
-                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, int cluster);
+                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, int cluster,
+                            int balanced = 1);
 size_t conv2_tf32_smem_bytes(int n2);
 int conv2_tf32_box_rows();
 int conv_tf32_box_cols(int n2);   // strip pitch of k_conv_tf32 (n2 + 5, or 74 with several column segments)
