@@ -217,7 +217,8 @@ class ClockSampler:
 def conv2_useful_mac_ceiling(n1: int, n2: int, rows: int = 6) -> float:
     """Fraction of the tensor-core MACs k_conv2_tc issues that are useful: 11 of 12 column-tap slots,
     times output positions over MMA columns -- units of `rows` output rows x <= 64 columns, strip pitch n2 + 5 (one
-    column segment) or 74, tiles of <= 253 outputs issued as N = round16(count + 3) <= 256 columns."""
+    column segment) or 74, ceil(L / 253) tiles sharing a unit's L outputs evenly (k_conv2_tc's balanced tiles), each
+    issued as N = round16(count + 3) <= 256 columns."""
     wseg = min(n2, 64)
     ncs = -(-n2 // wseg)
     P = n2 + 5 if ncs == 1 else wseg + 10
@@ -225,11 +226,11 @@ def conv2_useful_mac_ceiling(n1: int, n2: int, rows: int = 6) -> float:
     for r0 in range(0, n1, rows):
         rr = min(rows, n1 - r0)
         L = (rr - 1) * P + wseg
-        t = 0
-        while t * 253 < L:
-            cnt = min(253, L - 253 * t)
+        nt = -(-L // 253)
+        span = -(-L // nt)
+        for t in range(nt):
+            cnt = min(span, L - span * t)
             cols += min(256, (cnt + 3 + 15) // 16 * 16)
-            t += 1
         useful += rr * wseg
     return 11.0 / 12.0 * useful / cols
 

@@ -3,7 +3,8 @@ import bench
 
 
 def test_conv2_design_ceiling_lowrate():
-    # 64x64: ten 6-row units of 416 MMA columns (253 + 156 -> 256 + 160) and a 4-row unit (271 -> 256 + 32) for 4096
+    # 64x64: ten 6-row units of 416 MMA columns (balanced 205 + 204 -> 208 + 208) and a 4-row unit (271 -> 136 + 135 ->
+    # 144 + 144) for 4096
     # outputs; 11 of 12 column-tap slots useful
     expected = 11 / 12 * 4096 / (10 * 416 + 288)
     assert abs(bench.conv2_useful_mac_ceiling(64, 64) - expected) < 1e-12
