@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -62,7 +63,27 @@ constexpr int C2_DG_ROWS = 11;
 struct Geo {
   int n1, n2, wseg, P, nrb, ncs, units;
   int balanced;   // 1: a unit's tiles share its outputs evenly (2 x 205 at 64 x 64); 0: 253 + the rest
+  int nfull;      // row blocks whose units have the full tile count; units of the others are enumerated last
+  int batch;
 };
+// Unit u -> (image b, first output row r0, first column c0).  Units of the nfull full-height row blocks of every
+// image come first, then those of the remaining (shorter, fewer-tile) row blocks: the two CTAs of a weight-multicast
+// pair (units u and u + 1 at every step of the grid stride) then always run the same number of tiles.
+__device__ __forceinline__ void unit_of(const Geo& g, int u, int R, int& b, int& r0, int& c0) {
+  const int nf = g.nfull * g.ncs, split = g.batch * nf;
+  int rb, cs;
+  if (u < split) {
+    b = u / nf;
+    const int rem = u - b * nf;
+    rb = rem / g.ncs, cs = rem - (rem / g.ncs) * g.ncs;
+  } else {
+    const int v = u - split, ns = (g.nrb - g.nfull) * g.ncs;
+    b = v / ns;
+    const int rem = v - b * ns;
+    rb = g.nfull + rem / g.ncs, cs = rem - (rem / g.ncs) * g.ncs;
+  }
+  r0 = rb * R, c0 = cs * g.wseg;
+}
 // Tile t of a unit with L output positions: [n0, n0 + cnt).  Balanced tiles give every tile the same MMA length,
 // so the weight stream (33 K-blocks per tile, whatever its width) is consumed at one even rate instead of a burst
 // during the short second tile.
@@ -148,14 +169,13 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
   const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
   constexpr uint16_t CMASK = (uint16_t)((1u << CL) - 1);
 
-  const int per_img = g.nrb * g.ncs;
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ strip + weight producer
       uint32_t wk = 0;                    // weight K-blocks issued (stage wk % WST)
       int it = 0, sl = 0;                 // units, strip loads
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
-        const int b = u / per_img, rem = u - b * per_img;
-        const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
+        int b, r0, c0;
+        unit_of(g, u, R, b, r0, c0);
         const int rows = min(R, g.n1 - r0);
         const int L = (rows - 1) * g.P + g.wseg;
         int ntiles;
@@ -205,8 +225,8 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
 #define PT1(acc)
 #endif
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
-        const int rem = u % per_img;
-        const int r0 = (rem / g.ncs) * R;
+        int b_, r0, c0_;
+        unit_of(g, u, R, b_, r0, c0_);
         const int rows = min(R, g.n1 - r0);
         const int L = (rows - 1) * g.P + g.wseg;
         int ntiles;
@@ -284,8 +304,8 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
     for (int i = 0; i < CPT; ++i) bch[i] = (MODE == C2_BIAS_RELU && !fullmap && bias) ? bias[c0ch + i] : 0.f;
     int ti = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-      const int b = u / per_img, rem = u - b * per_img;
-      const int r0 = (rem / g.ncs) * R, c0 = (rem % g.ncs) * g.wseg;
+      int b, r0, c0;
+      unit_of(g, u, R, b, r0, c0);
       const int rows = min(R, g.n1 - r0);
       const int L = (rows - 1) * g.P + g.wseg;
       int ntiles;
@@ -390,15 +410,18 @@ static Geo make_geo(int batch, int n1, int n2, int R = C2_ROWS) {
   g.ncs = (n2 + g.wseg - 1) / g.wseg;
   g.units = batch * g.nrb * g.ncs;
   g.balanced = 1;
+  g.batch = batch;
+  // the last row block goes to the end of the enumeration when its units run fewer tiles than the full ones
+  const int Lfull = (std::min(R, n1) - 1) * g.P + g.wseg, rl = n1 - (g.nrb - 1) * R, Llast = (rl - 1) * g.P + g.wseg;
+  g.nfull = (Lfull + OUT_PER_TILE - 1) / OUT_PER_TILE == (Llast + OUT_PER_TILE - 1) / OUT_PER_TILE ? g.nrb : g.nrb - 1;
   return g;
 }
 
 // Weight multicast across CTA pairs (MC) needs both CTAs of every pair to run the same number of tiles: an even
 // grid, an even remainder of units over the grid, and the last row-block's units as many tiles as the full ones.
 static bool pair_balanced(const Geo& g, int grid, int R, int cl = 2) {
-  const int Lfull = (R - 1) * g.P + g.wseg, rl = g.n1 - (g.nrb - 1) * R, Llast = (rl - 1) * g.P + g.wseg;
-  return grid % cl == 0 && (g.units % grid) % cl == 0 &&
-         (Lfull + OUT_PER_TILE - 1) / OUT_PER_TILE == (Llast + OUT_PER_TILE - 1) / OUT_PER_TILE;
+  (void)R;   // full-tile units first (unit_of): the boundary to the shorter units must fall between clusters
+  return grid % cl == 0 && (g.units % grid) % cl == 0 && (g.batch * g.nfull * g.ncs) % cl == 0;
 }
 // And every pair must be co-resident: a GPC with an odd number of usable SMs cannot host a 2-CTA cluster on all of
 // them, and a persistent grid whose last pair waits for a free GPC pair would take twice as long.  The occupancy
