@@ -19,7 +19,7 @@ product w * 1 -- exact in every precision -- so the response must equal the flip
 exactly (bf16: bitwise; TF32: the tf32 value of the tap), and must be zero everywhere else.  The impulses sit where
 the responses land on conv2's tile tails (positions 240-255 of a 256-column TMEM tile: chunk c0 = 240 and the
 253-output overlap), the 64-column segment seams (pitch 74), the last partial row block, the image corners, and the
-8-row blocks of conv3.
+11-row units of conv3.
 """
 from __future__ import annotations
 
@@ -136,8 +136,8 @@ def _probe_positions(n1, n2):
     pos += _conv2_tile_positions(n1, n2)
     for seam in range(WSEG, n2, WSEG):                       # segment seams: the last / first column of a segment
         pos += [(n1 // 2, seam - 1), (n1 // 2, seam), (n1 - 1, seam - 1), (0, seam)]
-    for r in range(7, n1, 8):                                # conv3's 8-row blocks
-        pos.append((r, min(n2 - 1, 33)))
+    for r in range(10, n1, 11):                              # conv3's 11-row units: last row, first of the next
+        pos += [(r, min(n2 - 1, 33)), (min(n1 - 1, r + 1), min(n2 - 1, 40))]
     return sorted(set(pos))
 
 
