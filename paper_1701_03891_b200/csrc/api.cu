@@ -90,6 +90,7 @@ float bf2f(uint16_t b) {
 struct di_ctx_s {
   int device = 0, num_sms = 0;
   int conv2_balanced = 1;       // conv2 tiles share a unit's outputs evenly (DI_EXP_C2_SPLIT=253 at di_create: 253 + rest)
+  int conv2_mixed = 1;          // conv2 mixed 7- / 6-row blocks where they cut the tiles (DI_EXP_C2_MIXED=0 at di_create: off)
   int conv2_cluster = 2;        // conv2 weight-multicast cluster (DI_EXP_NO_MC=1 -> 1, DI_EXP_C2_CLUSTER=4 -> 4 at di_create)
   int m = 0, n1 = 0, n2 = 0, N = 0, max_batch = 0, kpad = 0;
   int pxbn = 256;               // pixel-tile width of the lifting GEMM = row count of a Phi^T block
@@ -203,12 +204,12 @@ di_status encode_phiT_blk(CUtensorMap* map, const void* base, bool bf16, long lo
   return DI_OK;
 }
 
-di_status encode_h1(CUtensorMap* map, const void* h1, int batch, int n1, int n2) {
+di_status encode_h1(CUtensorMap* map, const void* h1, int batch, int n1, int n2, int mixed) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[4] = {64, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
   cuuint64_t strides[3] = {64 * 2, (cuuint64_t)n2 * 64 * 2, (cuuint64_t)n1 * n2 * 64 * 2};
-  cuuint32_t box[4] = {64, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tc_box_rows(), 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)di::conv2_tc_box_cols(n2), (cuuint32_t)di::conv2_tc_box_rows(n1, n2, mixed), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(h1), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -789,12 +790,12 @@ di_status run_stages(di_ctx c, int first, int last, const void* y, long long ldy
       CUtensorMap tm;
       const CUtensorMap* tmp = &c->tmH1;
       if (h1 != c->h1 || batch != c->max_batch) {
-        di_status s = encode_h1(&tm, h1, batch, c->n1, c->n2);
+        di_status s = encode_h1(&tm, h1, batch, c->n1, c->n2, c->conv2_mixed);
         if (s != DI_OK) return s;
         tmp = &tm;
       }
       CUDA_TRY(di::launch_conv2_tc(tmp, c->wp2, c->b2, fm, batch, c->n1, c->n2, h2, c->num_sms, st, c->conv2_cluster,
-                                   c->conv2_balanced));
+                                   c->conv2_balanced, c->conv2_mixed));
     } else if (c->prec == DI_PREC_TF32) {
       CUtensorMap tm;
       const CUtensorMap* tmp = &c->tmH1;
@@ -976,6 +977,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   c->conv2_cluster = getenv("DI_EXP_NO_MC") ? 1 : (getenv("DI_EXP_C2_CLUSTER") ? atoi(getenv("DI_EXP_C2_CLUSTER")) : 2);
   c->fused_metrics = getenv("DI_EXP_FUSED_METRICS") != nullptr && atoi(getenv("DI_EXP_FUSED_METRICS")) != 0;
   c->conv2_balanced = !(getenv("DI_EXP_C2_SPLIT") && atoi(getenv("DI_EXP_C2_SPLIT")) == 253);
+  c->conv2_mixed = !(getenv("DI_EXP_C2_MIXED") && atoi(getenv("DI_EXP_C2_MIXED")) == 0);
 #ifdef DI_DEBUG
   {
     di_status sd = debug_bind();
@@ -1223,7 +1225,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
                              last ? di::conv3_r4_box_rows() : di::convg_tc_box_rows(l.cin)));
       }
     } else {
-      STEP(encode_h1(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2));
+      STEP(encode_h1(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2, c->conv2_mixed));
       if (a->n2 % 64 == 0) STEP(encode_h1_store(&c->tmH1s, c->h1, a->max_batch, a->n1, a->n2));
     }
     e = di::setup_conv13_tc(a->n2);

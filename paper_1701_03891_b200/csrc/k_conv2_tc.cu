@@ -65,11 +65,14 @@ struct Geo {
   int balanced;   // 1: a unit's tiles share its outputs evenly (2 x 205 at 64 x 64); 0: 253 + the rest
   int nfull;      // row blocks whose units have the full tile count; units of the others are enumerated last
   int batch;
+  int ntall;      // the first ntall row blocks of an image are R + 1 rows tall (mixed heights, conv2_tc_tall_blocks)
+  int srows;      // strip rows loaded per unit (the TMA box): R + 10, or R + 11 with tall blocks
 };
-// Unit u -> (image b, first output row r0, first column c0).  Units of the nfull full-height row blocks of every
-// image come first, then those of the remaining (shorter, fewer-tile) row blocks: the two CTAs of a weight-multicast
-// pair (units u and u + 1 at every step of the grid stride) then always run the same number of tiles.
-__device__ __forceinline__ void unit_of(const Geo& g, int u, int R, int& b, int& r0, int& c0) {
+// Unit u -> (image b, first output row r0, rows, first column c0).  Units of the nfull full-height row blocks of
+// every image come first, then those of the remaining (shorter, fewer-tile) row blocks: the two CTAs of a
+// weight-multicast pair (units u and u + 1 at every step of the grid stride) then always run the same number of
+// tiles.  With mixed heights the nfull = ntall tall blocks come first, then the R-row ones (both two tiles).
+__device__ __forceinline__ void unit_of(const Geo& g, int u, int R, int& b, int& r0, int& rows, int& c0) {
   const int nf = g.nfull * g.ncs, split = g.batch * nf;
   int rb, cs;
   if (u < split) {
@@ -82,17 +85,23 @@ __device__ __forceinline__ void unit_of(const Geo& g, int u, int R, int& b, int&
     const int rem = v - b * ns;
     rb = g.nfull + rem / g.ncs, cs = rem - (rem / g.ncs) * g.ncs;
   }
-  r0 = rb * R, c0 = cs * g.wseg;
+  r0 = rb * R + min(rb, g.ntall), c0 = cs * g.wseg;
+  rows = min(R + (rb < g.ntall ? 1 : 0), g.n1 - r0);
 }
 // Tile t of a unit with L output positions: [n0, n0 + cnt).  Balanced tiles give every tile the same MMA length,
 // so the weight stream (33 K-blocks per tile, whatever its width) is consumed at one even rate instead of a burst
-// during the short second tile.
-__device__ __forceinline__ int tile_span(const Geo& g, int L, int& ntiles) {
+// during the short second tile.  A tile of cnt outputs runs N = cnt + 3 rounded up to 16 MMA columns; when the even
+// share rounds up (478 = 2 x 239 -> 2 x 256 columns), the first tiles take the largest span that fits one column
+// step less (237 -> 240 columns, the last 241 -> 256) if the last tile still fits.
+__host__ __device__ inline int tile_span(const Geo& g, int L, int& ntiles) {
   ntiles = (L + OUT_PER_TILE - 1) / OUT_PER_TILE;
-  return g.balanced ? (L + ntiles - 1) / ntiles : OUT_PER_TILE;
+  if (!g.balanced) return OUT_PER_TILE;
+  const int s = (L + ntiles - 1) / ntiles, sf = ((s + 3) & ~15) - 3, lf = L - (ntiles - 1) * sf;
+  auto cols = [&](int span, int last) { return (ntiles - 1) * ((span + 3 + 15) & ~15) + ((last + 3 + 15) & ~15); };
+  return sf > 0 && lf <= OUT_PER_TILE && cols(sf, lf) < cols(s, L - (ntiles - 1) * s) ? sf : s;
 }
 
-__host__ __device__ inline int strip_rows_bytes(int P) { return (R + 10) * P * 128; }   // the largest (C_in = 64)
+__host__ __device__ inline int strip_rows_bytes(int rows, int P) { return rows * P * 128; }   // C_in = 64
 }  // namespace
 
 // last chunk of a full tile (c0 = 224, at most 29 outputs): columns c0+q .. c0+q+28 <= 255, loaded as
@@ -134,7 +143,7 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
   constexpr int R = RB == 128 ? C2_ROWS : C2_DG_ROWS;   // output rows per unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int strip_bytes = (R + 10) * g.P * RB;
+  const int strip_bytes = g.srows * g.P * RB;
   const int strip_alloc = (strip_bytes + GUARD_ROWS * RB + 1023) & ~1023;
   uint8_t* strip = smem;
   uint8_t* wst = smem + strip_alloc;
@@ -174,9 +183,8 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
       uint32_t wk = 0;                    // weight K-blocks issued (stage wk % WST)
       int it = 0, sl = 0;                 // units, strip loads
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
-        int b, r0, c0;
-        unit_of(g, u, R, b, r0, c0);
-        const int rows = min(R, g.n1 - r0);
+        int b, r0, rows, c0;
+        unit_of(g, u, R, b, r0, rows, c0);
         const int L = (rows - 1) * g.P + g.wseg;
         int ntiles;
         tile_span(g, L, ntiles);
@@ -225,9 +233,8 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
 #define PT1(acc)
 #endif
       for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
-        int b_, r0, c0_;
-        unit_of(g, u, R, b_, r0, c0_);
-        const int rows = min(R, g.n1 - r0);
+        int b_, r0, rows, c0_;
+        unit_of(g, u, R, b_, r0, rows, c0_);
         const int L = (rows - 1) * g.P + g.wseg;
         int ntiles;
         const int span = tile_span(g, L, ntiles);
@@ -241,7 +248,7 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
           tc_fence_after();
           const uint32_t d = tmem + buf * 256;
           // the last K-block's window (u = 10, v0 = TAPS (J - 1)) stays inside the strip and its guard rows
-          DI_DEVICE_ASSERT(n0 + 10 * g.P + TAPS * (J - 1) + nmma <= (R + 10) * g.P + GUARD_ROWS, n0, nmma);
+          DI_DEVICE_ASSERT(n0 + 10 * g.P + TAPS * (J - 1) + nmma <= g.srows * g.P + GUARD_ROWS, n0, nmma);
          for (int h = 0; h < NH; ++h) {
           if (NH > 1 || t == 0) {
             { PT0 mbar_wait(&hfull[0], sl & 1); PT1(c_h) }
@@ -304,9 +311,8 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
     for (int i = 0; i < CPT; ++i) bch[i] = (MODE == C2_BIAS_RELU && !fullmap && bias) ? bias[c0ch + i] : 0.f;
     int ti = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-      int b, r0, c0;
-      unit_of(g, u, R, b, r0, c0);
-      const int rows = min(R, g.n1 - r0);
+      int b, r0, rows, c0;
+      unit_of(g, u, R, b, r0, rows, c0);
       const int L = (rows - 1) * g.P + g.wseg;
       int ntiles;
       const int span = tile_span(g, L, ntiles);
@@ -411,9 +417,50 @@ static Geo make_geo(int batch, int n1, int n2, int R = C2_ROWS) {
   g.units = batch * g.nrb * g.ncs;
   g.balanced = 1;
   g.batch = batch;
+  g.ntall = 0;
+  g.srows = R + 10;
   // the last row block goes to the end of the enumeration when its units run fewer tiles than the full ones
   const int Lfull = (std::min(R, n1) - 1) * g.P + g.wseg, rl = n1 - (g.nrb - 1) * R, Llast = (rl - 1) * g.P + g.wseg;
   g.nfull = (Lfull + OUT_PER_TILE - 1) / OUT_PER_TILE == (Llast + OUT_PER_TILE - 1) / OUT_PER_TILE ? g.nrb : g.nrb - 1;
+  return g;
+}
+
+static int geo_tiles(const Geo& g) {   // MMA tiles of one image column segment
+  int n = 0;
+  for (int rb = 0; rb < g.nrb; ++rb) {
+    const int r0 = rb * C2_ROWS + std::min(rb, g.ntall), rows = std::min(C2_ROWS + (rb < g.ntall), g.n1 - r0);
+    int nt;
+    tile_span(g, (rows - 1) * g.P + g.wseg, nt);
+    n += nt;
+  }
+  return n;
+}
+
+// Mixed row-block heights (the R = 6, C_in = 64 layer-2 instance, one column segment): n1 = ntall (R + 1) +
+// (nrb - ntall) R with nrb = ceil(n1 / (R + 1)) blocks, used when every block runs the same number of tiles and the
+// image needs fewer tiles than with R-row blocks and a short last one.  Each tile restreams all 33 weight K-blocks
+// (528 KB), and that stream bounds the kernel: at 64 x 64, 4 blocks of 7 rows (478 positions, tiles
+// of 237 + 241) and 6 of 6 (2 x 205) are 20 tiles per image instead of 10 x 2 + 2 (the 4-row last block).
+int conv2_tc_tall_blocks(int n1, int n2) {
+  if (n2 > WSEG) return 0;
+  const int nrb = (n1 + C2_ROWS) / (C2_ROWS + 1), ntall = n1 - C2_ROWS * nrb;
+  if (ntall <= 0 || ntall > nrb) return 0;
+  Geo a = make_geo(1, n1, n2), m = a;
+  m.nrb = nrb, m.ntall = ntall;
+  int ttall, tshort;
+  tile_span(m, C2_ROWS * m.P + m.wseg, ttall);
+  tile_span(m, (C2_ROWS - 1) * m.P + m.wseg, tshort);
+  if (ttall != tshort) return 0;
+  return geo_tiles(m) < geo_tiles(a) ? ntall : 0;
+}
+static Geo make_geo_c2(int batch, int n1, int n2, int mixed) {
+  Geo g = make_geo(batch, n1, n2);
+  const int nt = mixed ? conv2_tc_tall_blocks(n1, n2) : 0;
+  if (nt > 0) {
+    g.nrb = (n1 + C2_ROWS) / (C2_ROWS + 1);
+    g.ntall = nt, g.nfull = nt, g.srows = C2_ROWS + 11;
+    g.units = batch * g.nrb * g.ncs;
+  }
   return g;
 }
 
@@ -469,9 +516,11 @@ static cudaError_t launch_pair(void (*kern)(Args...), int grid, int threads, siz
   return cudaLaunchKernelEx(&cfg, kern, tm, w, bias, fullmap, g, out, mask);
 }
 
+// room for the R + 11-row strip of mixed heights whenever they may apply (one column segment)
 size_t conv2_tc_smem_bytes(int n2) {
   const int P = conv2_tc_box_cols(n2);
-  const size_t strip_alloc = ((size_t)strip_rows_bytes(P) + GUARD_ROWS * 128 + 1023) & ~(size_t)1023;
+  const int rows = R + 10 + (n2 <= WSEG ? 1 : 0);
+  const size_t strip_alloc = ((size_t)strip_rows_bytes(rows, P) + GUARD_ROWS * 128 + 1023) & ~(size_t)1023;
   return strip_alloc + WSTAGES * WBYTES + 4 * ECH * SPS * 4 + 1024;
 }
 // <32, 64, C2_MASK>: strip of 64-B rows, C2_WST64 weight stages of 8 KB, two epilogue groups
@@ -484,7 +533,7 @@ static size_t dgrad2_bf16_smem_bytes(int n2) {
 // The strip is loaded in one box per unit.  Loading it as two halves with a separate producer so that the load
 // overlaps the MMAs of the previous unit removes the strip wait but measured slower on B200 (the TMA writes
 // compete with the UMMA operand reads for shared-memory bandwidth, which this kernel saturates: DESIGN.md §11).
-int conv2_tc_box_rows() { return R + 10; }
+int conv2_tc_box_rows(int n1, int n2, int mixed) { return R + 10 + (mixed && conv2_tc_tall_blocks(n1, n2) > 0); }
 int dgrad2_bf16_box_rows() { return C2_DG_ROWS + 10; }
 // Strip pitch P (positions per strip row).  One column segment (n2 <= 64): P = n2 + 5 -- the box starts 5 columns
 // left of the image, so its 5 out-of-bounds (zero) columns are the left padding of a row AND the right padding of the
@@ -514,8 +563,9 @@ cudaError_t setup_conv2_tc(int n2) {
 // cluster: weight-multicast cluster size (the context's setting, read once by di_create: 2 by default, DI_EXP_NO_MC=1
 // -> 1, DI_EXP_C2_CLUSTER=4 -> 4); falls back to smaller clusters when the balance / co-residency checks fail
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
-                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, int cluster, int balanced) {
-  Geo g = make_geo(batch, n1, n2);
+                            int n1, int n2, void* h2, int num_sms, cudaStream_t st, int cluster, int balanced,
+                            int mixed) {
+  Geo g = make_geo_c2(batch, n1, n2, mixed);
   g.balanced = balanced;
   const int grid = g.units < num_sms ? g.units : num_sms;
   const size_t sm = conv2_tc_smem_bytes(n2);
@@ -541,7 +591,7 @@ int convg_tc_box_rows(int cin) { return (cin >= 64 ? C2_ROWS : C2_DG_ROWS) + 10;
 // <64, 64>: the 128-B-row strip, a 3-stage ring and two epilogue groups' staging
 static size_t convg64_smem_bytes(int n2) {
   const int P = conv2_tc_box_cols(n2);
-  const size_t strip_alloc = ((size_t)strip_rows_bytes(P) + GUARD_ROWS * 128 + 1023) & ~(size_t)1023;
+  const size_t strip_alloc = ((size_t)strip_rows_bytes(R + 10, P) + GUARD_ROWS * 128 + 1023) & ~(size_t)1023;
   return strip_alloc + 3 * WBYTES + 2 * 4 * ECH * SPS * 4 + 1024;
 }
 

@@ -89,7 +89,9 @@ cudaError_t launch_conv1_tf32(const CUtensorMap* tmX, const void* w1pack, const 
 // stage 2: conv layer 2 (64 -> 32, ReLU)
 cudaError_t setup_conv2_tc(int n2);
 size_t conv2_tc_smem_bytes(int n2);
-int conv2_tc_box_rows();
+// mixed row-block heights (n1 = ntall 7-row + 6-row blocks) when they cut the MMA tiles per image; 0: uniform
+int conv2_tc_tall_blocks(int n1, int n2);
+int conv2_tc_box_rows(int n1, int n2, int mixed);
 int conv2_tc_box_cols(int n2);
 int dgrad2_bf16_box_rows();
 // custom stacks, BF16: interior C_in -> C_out layers on k_conv2_tc (bias + ReLU), strip box rows per C_in
@@ -99,7 +101,7 @@ cudaError_t launch_convg_tc(int cin, int cout, const CUtensorMap* tm, const void
                             int n1, int n2, void* out, int num_sms, cudaStream_t st);
 cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const float* bias, int fullmap, int batch,
                             int n1, int n2, void* h2, int num_sms, cudaStream_t st, int cluster,
-                            int balanced = 1);
+                            int balanced = 1, int mixed = 1);
 size_t conv2_tf32_smem_bytes(int n2);
 int conv2_tf32_box_rows();
 int conv_tf32_box_cols(int n2);   // strip pitch of k_conv_tf32 (n2 + 5, or 74 with several column segments)

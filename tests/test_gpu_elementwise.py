@@ -17,9 +17,9 @@ stage (di_debug_stage), so each stage is checked alone.
 Impulse probes: with one unit input at (image, row, column, channel) and zero biases, every output of a layer is ONE
 product w * 1 -- exact in every precision -- so the response must equal the flipped 11x11 tap window of that channel
 exactly (bf16: bitwise; TF32: the tf32 value of the tap), and must be zero everywhere else.  The impulses sit where
-the responses land on conv2's tile tails (positions 240-255 of a 256-column TMEM tile: chunk c0 = 240 and the
-253-output overlap), the 64-column segment seams (pitch 74), the last partial row block, the image corners, and the
-11-row units of conv3.
+the responses land on conv2's tile tails (the balanced split 205 / 237 of a unit, chunk c0 = 240 of a 256-column
+TMEM tile and the 253-output overlap), the boundary between 7- and 6-row blocks, the 64-column segment seams (pitch
+74), the last partial row block, the image corners, and the 11-row units of conv3.
 """
 from __future__ import annotations
 
@@ -67,11 +67,12 @@ def _run_stages(ctx, case):
     return [_f64(xt)[:, None], _f64(h1).transpose(0, 3, 1, 2), _f64(h2).transpose(0, 3, 1, 2), _f64(xh)[:, None]]
 
 
-SEAM_SHAPES = [(64, 64),     # the bench geometry: P = 69, tiles 0..252 / 253..408 per 6-row unit
+SEAM_SHAPES = [(64, 64),     # the bench geometry: P = 69, 4 blocks of 7 rows (tiles 237 + 241), 6 of 6 (205 + 204)
                (61, 128),    # two 64-column segments (P = 74), a 1-row last row block
                (13, 130),    # three segments, the last 2 columns wide; 2 row blocks, the last 1 row
                (61, 65),     # a 1-column last segment
                (40, 72),     # ragged second segment, 4-row last block
+               (61, 64),     # mixed row-block heights: 7 blocks of 7 rows, 2 of 6
                (9, 13)]      # one small unit: a single partial tile
 
 
@@ -108,21 +109,48 @@ def test_every_element_of_every_stage(precision, n1, n2):
 
 
 # ------------------------------------------------------------------------------------------------ impulse probes
-def _conv2_tile_positions(n1, n2):
-    """Image positions (r, c) of conv2 outputs at tile tails: tile positions 240 (chunk c0 = 240), 252 (the last of
-    the 253 complete outputs), 253 (first output of the next tile), per 6-row unit, for the first, a middle and the
-    last row block and every column segment."""
+def _ntiles(L):
+    return (L + OUT_PER_TILE - 1) // OUT_PER_TILE
+
+
+def _row_blocks(n1, n2):
+    """conv2's row blocks (r0, rows): 6-row blocks and a short last one, or -- one column segment, when it needs
+    fewer tiles and every block runs the same number -- ntall 7-row blocks then 6-row ones (mixed heights, DESIGN.md
+    §6).  An independent restatement of the kernel's rule, used only to aim the probes."""
     wseg = min(n2, WSEG)
     P = n2 + 5 if n2 <= WSEG else WSEG + 10
-    nrb = (n1 + C2_ROWS - 1) // C2_ROWS
+    uniform = [(r0, min(C2_ROWS, n1 - r0)) for r0 in range(0, n1, C2_ROWS)]
+    nrb = (n1 + C2_ROWS) // (C2_ROWS + 1)
+    ntall = n1 - C2_ROWS * nrb
+    if n2 > WSEG or not 0 < ntall <= nrb or _ntiles(C2_ROWS * P + wseg) != _ntiles((C2_ROWS - 1) * P + wseg):
+        return uniform
+    mixed, r0 = [], 0
+    for rb in range(nrb):
+        rows = C2_ROWS + (rb < ntall)
+        mixed.append((r0, rows))
+        r0 += rows
+    tiles = lambda blocks: sum(_ntiles((r - 1) * P + wseg) for _, r in blocks)
+    return mixed if tiles(mixed) < tiles(uniform) else uniform
+
+
+def _conv2_tile_positions(n1, n2):
+    """Image positions (r, c) of conv2 outputs at tile tails: positions 237 / 240 / 252 / 253 of a unit's strip
+    (the first tile of a 7-row unit ends at 237, chunk c0 = 240, the last of 253 complete outputs, the first of the
+    next tile) and the unit's last position, for the first, a middle and the last row block (and the last 7-row
+    block when heights are mixed) and every column segment."""
+    wseg = min(n2, WSEG)
+    P = n2 + 5 if n2 <= WSEG else WSEG + 10
+    blocks = _row_blocks(n1, n2)
+    pick = {0, len(blocks) // 2, len(blocks) - 1}
+    pick |= {i for i in range(1, len(blocks)) if blocks[i][1] != blocks[i - 1][1]} | \
+        {i - 1 for i in range(1, len(blocks)) if blocks[i][1] != blocks[i - 1][1]}
     out = []
-    for rb in sorted({0, nrb // 2, nrb - 1}):
-        r0 = rb * C2_ROWS
-        rows = min(C2_ROWS, n1 - r0)
+    for i in sorted(pick):
+        r0, rows = blocks[i]
         L = (rows - 1) * P + wseg
         for seg in range((n2 + wseg - 1) // wseg):
             c0 = seg * wseg
-            for o in (240, 252, 253, L - 1):
+            for o in (204, 205, 236, 237, 240, 252, 253, L - 1):
                 if o >= L:
                     continue
                 rr, cc = divmod(o, P)

@@ -165,6 +165,23 @@ def test_weight_multicast_and_tile_width_are_bitwise_neutral(monkeypatch):
     assert np.array_equal(big.recover(y).cpu().numpy(), mc), "proxy tile width changed the result"
 
 
+@pytest.mark.parametrize("n1,n2,batch", [(64, 64, 256), (64, 64, 37), (61, 64, 20), (50, 40, 24), (20, 20, 9)])
+def test_mixed_row_blocks_are_bitwise_neutral(monkeypatch, n1, n2, batch):
+    """conv2's mixed row-block heights (7- and 6-row units where they cut the MMA tiles per image, e.g. 20 instead
+    of 22 at 64 x 64) only regroup outputs into tiles: every output still accumulates the same 33
+    K-blocks in the same order, so the result equals the uniform 6-row schedule (DI_EXP_C2_MIXED=0) bit for bit."""
+    case = Case(n1, n2, max(1, n1 * n2 // 10), batch, "bf16")
+    ctx = make_ctx(case)
+    y = y_device(case, ctx)
+    mixed = ctx.recover(y).cpu().numpy()
+    monkeypatch.setenv("DI_EXP_C2_MIXED", "0")
+    uni = make_ctx(case)
+    monkeypatch.delenv("DI_EXP_C2_MIXED")
+    assert np.array_equal(uni.recover(y).cpu().numpy(), mixed)
+    idx = np.array([0, batch - 1])
+    compare(mixed[idx], case.oracle(idx), case.x[idx], "bf16")
+
+
 def test_zero_weights_give_bias_only():
     p = synth.make_params(bias="channel")
     p0 = synth.Params([np.zeros_like(w) for w in p.w], p.b)
