@@ -332,14 +332,32 @@ di_status encode_dg2b_strip(CUtensorMap* map, const void* p, int batch, int n1, 
   return DI_OK;
 }
 
+// bf16 conv3 (k_conv3_r4): [batch][n1][n2][pitch] bf16 (32 channels read) as a 4-D tensor ordered (channel, column,
+// IMAGE, row), so that one box of conv3_r4_box_cols(n2) columns x 2 images x conv3_r4_box_rows() rows lands as strip
+// rows of [image][column] -- the same image row of an image pair side by side; SWIZZLE_64B (64-B position rows)
+di_status encode_h2_pair(CUtensorMap* map, const void* h2, int batch, int n1, int n2, int pitch) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {(cuuint64_t)pitch, (cuuint64_t)n2, (cuuint64_t)batch, (cuuint64_t)n1};
+  cuuint64_t strides[3] = {(cuuint64_t)pitch * 2, (cuuint64_t)n1 * n2 * pitch * 2, (cuuint64_t)n2 * pitch * 2};
+  cuuint32_t box[4] = {32, (cuuint32_t)di::conv3_r4_box_cols(n2), 2, (cuuint32_t)di::conv3_r4_box_rows()};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(h2), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled (h2 image pairs) failed: %d", (int)r);
+  return DI_OK;
+}
+
 di_status encode_h2(CUtensorMap* map, const void* h2, int batch, int n1, int n2, bool f32 = false) {
+  if (!f32) return encode_h2_pair(map, h2, batch, n1, n2, 32);
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(DI_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   const cuuint64_t e = f32 ? 4 : 2;
   cuuint64_t dims[4] = {32, (cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)batch};
   cuuint64_t strides[3] = {32 * e, (cuuint64_t)n2 * 32 * e, (cuuint64_t)n1 * n2 * 32 * e};
   cuuint32_t box[4] = {(cuuint32_t)di::conv3_tc_box_ch(f32), (cuuint32_t)di::conv3_tc_box_cols(n2),
-                       (cuuint32_t)(f32 ? di::conv3_tc_box_rows() : di::conv3_r4_box_rows()), 1};
+                       (cuuint32_t)di::conv3_tc_box_rows(), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
                    const_cast<void*>(h2), dims, strides, box, es,
@@ -1220,9 +1238,11 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
         di_ctx_s::Layer& l = c->stack[i];
         const int pitch = i == 1 ? 64 : c->stack[i - 1].cout;
         const bool last = i == (int)c->stack.size() - 1;
-        STEP(encode_act_bf16(&l.tm, c->act[(i - 1) & 1], a->max_batch, a->n1, a->n2, pitch, std::min(l.cin, 64),
-                             last ? di::conv3_tc_box_cols(a->n2) : di::conv2_tc_box_cols(a->n2),
-                             last ? di::conv3_r4_box_rows() : di::convg_tc_box_rows(l.cin)));
+        if (last)
+          STEP(encode_h2_pair(&l.tm, c->act[(i - 1) & 1], a->max_batch, a->n1, a->n2, pitch));
+        else
+          STEP(encode_act_bf16(&l.tm, c->act[(i - 1) & 1], a->max_batch, a->n1, a->n2, pitch, std::min(l.cin, 64),
+                               di::conv2_tc_box_cols(a->n2), di::convg_tc_box_rows(l.cin)));
       }
     } else {
       STEP(encode_h1(&c->tmH1, c->h1, a->max_batch, a->n1, a->n2, c->conv2_mixed));

@@ -1,18 +1,26 @@
 // k_conv3_r4.cu -- stage 3 of the bf16 path, conv layer 3 (1 filter 11x11x32 + bias, ReLU iff DI_FLAG_FINAL_RELU,
-// crop S) with RP = 11 OUTPUT ROWS STACKED IN M.
+// crop S) with RP = 11 OUTPUT ROWS STACKED IN M, TWO IMAGES SIDE BY SIDE IN N, and the strip
+// STREAMED ROW BY ROW.
 //
 // C_out = 1 leaves the UMMA M dimension to the taps.  The first design (k_conv3_tc) stacks the 11 column taps of one
 // tap row in M = 32 (.ws) and walks the 11 tap rows as K-blocks, so every strip position is read by 11 MMAs per
 // 246 outputs and the tensor core's shared-memory reads bound it (0.87 ms at lowrate).  Here M = 128 holds RP = 11
-// output rows t x ES = 11 rows (the column taps v; 121 of the 128 rows used): window k (k = 0 .. RP + 9) is the strip
-// shifted by k rows, and rows (t, .) of its A operand hold the taps of tap row u = k - t, so that
-//   D[(t, v)][n] = sum_k sum_c W[k - t][v][c] strip[n + k P][c]  and  x_hat[row t][j] = sum_v D[(t, v)][j + v].
+// output rows t x ES = 11 rows (the column taps v; 121 of the 128 rows used): window k (k = 0 .. RP + 9) of a unit is
+// its strip row k, and rows (t, .) of its A operand hold the taps of tap row u = k - t, so that
+//   D[(t, v)][n] = sum_k sum_c W[k - t][v][c] strip[row k][n][c]  and  x_hat[row t][j] = sum_v D[(t, v)][j + v].
 // A_k = [W[k]; W[k-1]; ...; W[k-RP+1]] is a 128-row window of ONE stack T[i] = W[10 - i] (zero outside 0..10): A_k
 // starts at T[10 - k] (an 11-row entry: any 64-B row may start a SWIZZLE_64B window, tools/ladder.cu t3/t11), the
-// whole bank stays resident in shared memory, and a window is a descriptor start address.  N = P rounded up to 16
-// (<= 80) covers one strip row: per 11 x 64 outputs 21 windows x 2 MMAs (K = 16) -- 0.060 MMAs per output against
-// 0.070 with 8 rows x 16-row entries (r02: 0.40 ms) and 0.09 for k_conv3_tc.  The 121 tap rows do not align with
-// the TMEM lane quadrants, so the four epilogue warps share one tile (see the epilogue).
+// whole bank stays resident in shared memory, and a window is a descriptor start address.
+//
+// r02 (this version): a strip row holds the same image row of TWO images, PP = roundup16(W + 10) positions each
+// (one 4-D TMA box over (channel, column, image, row)), so one MMA has N = 2 PP = 160 columns at 64 x 64 -- the
+// A-operand read (4 KB per MMA, the cost that bound the one-image form at N = 80) is shared by twice the outputs.
+// Three such rows would not fit the chunk ring of whole 21-row unit strips, so the strip is streamed instead: units
+// j (output rows 11 j ..) overlap by 10 strip rows, and every strip row s feeds the (at most two) units that read
+// it -- window s - 11 j + 5 of unit j -- in the same pass.  Each row is then consumed once and released: the ring
+// only holds the lead (NSL chunks of CHR rows), two units accumulate at a time (the third TMEM slot drains in the
+// epilogue), and rows outside the image (the 5 zero rows above / below) are never loaded or multiplied.
+// Per 2 x 64 x 64 outputs: 114 windows x 2 MMAs of N = 160 against 2 x 126 x 2 of N = 80.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -28,49 +36,42 @@ namespace di {
 
 namespace {
 constexpr int RP = C3R_RP, ES = C3R_ES, NWIN = C3R_NWIN, IMIN = C3R_IMIN;
-constexpr int R = RP;                  // output rows per unit (one pass)
-constexpr int CH = R;                  // strip rows per TMA chunk (chunk k = strip rows [R k - 5, R k + R - 5))
-constexpr int NSPAN = (R + 10 + CH - 1) / CH;   // chunks a unit reads (R + 10 strip rows): 2 for R = 11
-constexpr int NCH = NSPAN + 1;         // chunk slots in the ring: one loads while a unit computes
-constexpr int NACC = 4;                // TMEM accumulator slots (128 columns each)
+constexpr int R = RP;                  // output rows per unit
+constexpr int CHR = 2;                 // strip rows per TMA chunk
+constexpr int NSL = 6;                 // chunk slots in the ring (12 rows of lead)
+constexpr int NACC = 3;                // TMEM accumulator slots: two units accumulate, one drains
+constexpr int ACOLS = 160;             // TMEM columns per slot (N <= 160)
 #ifndef DI_C3R_PF
 #define DI_C3R_PF 6
 #endif
 constexpr int C3R_PF = DI_C3R_PF;      // chunks prefetched into L2 ahead of the shared-memory loads
 constexpr int TBLK = ES * 64;          // one T entry: ES rows (v) x 32 channels bf16, SWIZZLE_64B
 constexpr int TBYTES = (C3R_NENT * TBLK + 1023) & ~1023;
-constexpr int GUARD = 16;              // zero positions past the ring (the last ring row's window reads N - P past it)
 constexpr int SROW = 84;               // epilogue tile row stride (floats): 16-B rows
 constexpr int SROWS = RP * ES;         // TMEM lanes holding taps (121 of 128 for RP = ES = 11)
-constexpr int OPT = (RP * 64 + 127) / 128;   // outputs per epilogue thread and unit
+constexpr int OPT = (RP * 64 + 127) / 128;   // outputs per epilogue thread, unit and image
 
-// Work item = one column segment of one image (or a contiguous part of its row blocks when there are fewer
-// columns than SMs): its units run top to bottom, so consecutive units share 10 of their 18 strip rows.
+// Work item = one column segment of one PAIR of images (2 p, 2 p + 1), or a contiguous part of its row blocks when
+// there are fewer pair-columns than SMs.  Its strip rows s_lo .. s_hi - 1 stream top to bottom.
 struct GeoR4 {
-  int n1, n2, wseg, P, N, nrb, ncs, splits, per, items;
+  int n1, n2, batch, wseg, PP, N, nrb, ncs, splits, per, items;
 };
-__device__ __forceinline__ void item_of(const GeoR4& g, int it, int& b, int& c0, int& rb0, int& nu) {
+__device__ __forceinline__ void item_of(const GeoR4& g, int it, int& p, int& c0, int& rb0, int& nu) {
   const int col = it / g.splits, sp = it - col * g.splits;
-  b = col / g.ncs;
-  c0 = (col - b * g.ncs) * g.wseg;
+  p = col / g.ncs;
+  c0 = (col - p * g.ncs) * g.wseg;
   rb0 = sp * g.per;
   nu = min(g.per, g.nrb - rb0);
 }
+__device__ __forceinline__ int rows_lo(int rb0) { return max(0, R * rb0 - 5); }
+__device__ __forceinline__ int rows_hi(const GeoR4& g, int rb0, int nu) { return min(g.n1, R * (rb0 + nu) + 5); }
 }  // namespace
 
-// Strip rows arrive in chunks of CH = 8 rows through a ring of NCH = 4 chunk slots (ROW RING): unit j of an item
-// (output rows 8 (rb0 + j) .. + 7) reads strip rows [8 (rb0 + j) - 5, + 18) = chunks j, j + 1, j + 2 of the item, and
-// releases chunk j when its MMAs complete, so chunk j + 3 loads while unit j computes.  Each strip row is fetched
-// once per item (10 chunks = 80 rows for a 64-row image) instead of 18 rows per 8-row unit: the L2 -> shared-memory
-// traffic drops from 2.25x to 1.25x the h2 rows.  Window k of a unit reads ring row (8 (chunk j) + k) mod 32 plus
-// N - P positions past it (the next row, the slot padding or the zero guard); those positions only reach D columns
-// >= P, which no output reads.
-//
 // Fused metrics (di_recover_metrics): with xtrue != null each epilogue thread also reads the
 // ground truth of the outputs it writes and accumulates, in fp64 and a fixed order, sum (x_hat - x)^2, sum x^2 and
-// max x; per item the four warps' sums go to mpart[item][warp][3] (no atomics), and k_metrics_finish combines the
-// items of each image in item order: PSNR, NMSE and success without a second pass over
-// x_hat.
+// max x; per item, image and warp the sums go to mpart[item][image][warp][3] (no atomics), and k_metrics_finish
+// combines the items of each image in item order: PSNR, NMSE and success without a
+// second pass over x_hat.
 template <bool METRICS>
 __global__ void __launch_bounds__(256, 1)
     k_conv3_r4(const __grid_constant__ CUtensorMap tmH2, const uint8_t* __restrict__ tpack,
@@ -78,28 +79,23 @@ __global__ void __launch_bounds__(256, 1)
                const float* __restrict__ xtrue, double* __restrict__ mpart) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int P = g.P;
-  const int chunk_bytes = CH * P * 64;
-  const int slot = (chunk_bytes + 1023) & ~1023;              // slot stride: 1024-aligned TMA destinations
+  const int rowb = g.N * 64;                                  // one strip row: 2 images x PP positions x 64 B
+  const int chunk_bytes = CHR * rowb;                         // a multiple of 1024 (PP a multiple of 16)
   uint8_t* const tb = smem;                                   // T stack (1024-aligned)
-  uint8_t* const ring = smem + TBYTES;                        // NCH chunk slots, then the zero guard
-  const int ring_alloc = (NCH * slot + GUARD * 64 + 1023) & ~1023;
-  float* const S = reinterpret_cast<float*>(ring + ring_alloc);
+  uint8_t* const ring = smem + TBYTES;                        // NSL chunk slots
+  float* const S = reinterpret_cast<float*>(ring + NSL * chunk_bytes);
 
-  __shared__ uint64_t wbar, cfull[NCH], cempty[NCH], acc_full[NACC], acc_empty[NACC];
+  __shared__ uint64_t wbar, cfull[NSL], cempty[NSL], acc_full[NACC], acc_empty[NACC];
   __shared__ uint32_t tslot;
   const int warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmH2);
     mbar_init(&wbar, 1);
-    for (int s = 0; s < NCH; ++s) mbar_init(&cfull[s], 1), mbar_init(&cempty[s], 1);
+    for (int s = 0; s < NSL; ++s) mbar_init(&cfull[s], 1), mbar_init(&cempty[s], 1);
     for (int a = 0; a < NACC; ++a) mbar_init(&acc_full[a], 1), mbar_init(&acc_empty[a], 4);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(&tslot), tmem_relinquish();
-  for (int i = threadIdx.x; i < ring_alloc / 16; i += blockDim.x)   // finite ring (never-loaded slots) and guard
-    reinterpret_cast<uint4*>(ring)[i] = make_uint4(0, 0, 0, 0);
-  fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -109,28 +105,31 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {  // ------------------------------------------------ producer: T once, strip chunks
       mbar_arrive_expect_tx(&wbar, TBYTES);
       bulk_load(tb, tpack, TBYTES, &wbar);
-      // L2 prefetch cursor, PF chunks ahead of the loads: the ring holds one chunk of lead (one unit of MMAs), too
-      // few bytes in flight to cover DRAM latency; the prefetched chunks arrive from L2
-      int pit = blockIdx.x, pk = 0, pb = 0, pc0 = 0, prb0 = 0, pnu = 0;
-      if (pit < g.items) item_of(g, pit, pb, pc0, prb0, pnu);
+      // L2 prefetch cursor, PF chunks ahead of the loads (the ring's lead is too few bytes in flight to cover DRAM
+      // latency; the prefetched chunks arrive from L2)
+      int pit = blockIdx.x, ps = 0, phi = 0, pp = 0, pc0 = 0;
+      auto start_item = [&]() {
+        if (pit >= g.items) return;
+        int rb0, nu;
+        item_of(g, pit, pp, pc0, rb0, nu);
+        ps = rows_lo(rb0), phi = rows_hi(g, rb0, nu);
+      };
+      start_item();
       auto prefetch_next = [&]() {
         if (pit >= g.items) return;
-        tma_prefetch_l2_4d(&tmH2, 0, pc0 - 5, CH * (prb0 + pk) - 5, pb);
-        if (++pk == pnu + NSPAN - 1) {
-          pk = 0, pit += gridDim.x;
-          if (pit < g.items) item_of(g, pit, pb, pc0, prb0, pnu);
-        }
+        tma_prefetch_l2_4d(&tmH2, 0, pc0 - 5, 2 * pp, ps);
+        if ((ps += CHR) >= phi) pit += gridDim.x, start_item();
       };
       for (int i = 0; i < C3R_PF; ++i) prefetch_next();
       uint32_t gc = 0;                 // chunks issued by this CTA
       for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
-        int b, c0, rb0, nu;
-        item_of(g, it, b, c0, rb0, nu);
-        for (int k = 0; k < nu + NSPAN - 1; ++k, ++gc) {
-          const uint32_t sl = gc % NCH;
-          if (gc >= NCH) mbar_wait(&cempty[sl], ((gc / NCH) - 1) & 1);
+        int p, c0, rb0, nu;
+        item_of(g, it, p, c0, rb0, nu);
+        for (int s = rows_lo(rb0), se = rows_hi(g, rb0, nu); s < se; s += CHR, ++gc) {
+          const uint32_t sl = gc % NSL;
+          if (gc >= NSL) mbar_wait(&cempty[sl], ((gc / NSL) - 1) & 1);
           mbar_arrive_expect_tx(&cfull[sl], chunk_bytes);
-          tma_load_4d(ring + sl * slot, &tmH2, &cfull[sl], 0, c0 - 5, CH * (rb0 + k) - 5, b);
+          tma_load_4d(ring + sl * chunk_bytes, &tmH2, &cfull[sl], 0, c0 - 5, 2 * p, s);
           prefetch_next();
         }
       }
@@ -142,11 +141,8 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t idesc = idesc_f32acc(1, 128, g.N);
       const uint64_t adesc0 = smem_desc(smem_u32(tb), 16, 512, kSwizzle64B);
       const uint64_t bdesc0 = smem_desc(smem_u32(ring), 16, 512, kSwizzle64B);
-      const uint64_t rstep = (uint64_t)((P * 64) >> 4);                  // one strip row
-      const uint64_t padstep = (uint64_t)((slot - chunk_bytes) >> 4);     // slot padding after a slot's last row
-      const uint64_t ringstep = (uint64_t)((NCH * slot) >> 4);           // the whole ring
-      uint32_t gc0 = 0;                // this item's first chunk (CTA-wide count)
-      int pi = 0;
+      uint32_t gc = 0;                 // chunks consumed (CTA-wide)
+      int pi = 0;                      // units started (CTA-wide): unit pi accumulates in slot pi % NACC
 #ifdef DI_PROF_CONV3
       long long pc_chunk = 0, pc_acc = 0, pc0 = clock64(), pt;
 #define C3P0 pt = clock64();
@@ -156,43 +152,42 @@ __global__ void __launch_bounds__(256, 1)
 #define C3P1(acc)
 #endif
       for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
-        int b, c0, rb0, nu;
-        item_of(g, it, b, c0, rb0, nu);
-        for (int k = 0; k < NSPAN - 1; ++k) {   // the item's first chunks
-          const uint32_t c = gc0 + k;
-          C3P0 mbar_wait(&cfull[c % NCH], (c / NCH) & 1); C3P1(pc_chunk)
-        }
-        for (int j = 0; j < nu; ++j, ++pi) {
-          const uint32_t cj = gc0 + j;
-          C3P0 mbar_wait(&cfull[(cj + NSPAN - 1) % NCH], ((cj + NSPAN - 1) / NCH) & 1); C3P1(pc_chunk)
-          tc_fence_after();
-          const int a = pi % NACC;
-          if (pi >= NACC) {
-            C3P0 mbar_wait(&acc_empty[a], ((pi / NACC) - 1) & 1); C3P1(pc_acc)
+        int p, c0, rb0, nu;
+        item_of(g, it, p, c0, rb0, nu);
+        const int slo = rows_lo(rb0), shi = rows_hi(g, rb0, nu), pi0 = pi;
+        uint64_t bd = 0;
+        for (int s = slo; s < shi; ++s) {
+          const int cr = (s - slo) % CHR;
+          if (cr == 0) {                                   // the row opens a chunk
+            C3P0 mbar_wait(&cfull[gc % NSL], (gc / NSL) & 1); C3P1(pc_chunk)
             tc_fence_after();
+            bd = bdesc0 + (uint64_t)(((gc % NSL) * chunk_bytes) >> 4);
           }
-          const uint32_t d = tmem + a * 128;
-          const int sl0 = (int)(cj % NCH);                     // slot of the unit's strip row 0
-          // a window reads N - P positions past its row: the last slot's last row runs into the zero guard
-          DI_DEVICE_ASSERT(g.N - g.P <= GUARD, g.N, g.P);
-          // the single issuing thread is latency-bound: the B descriptor advances by adds only (one strip row per
-          // window, the slot padding every CH rows, back to slot 0 after the last slot)
-          uint64_t bd = bdesc0 + (uint64_t)((sl0 * slot) >> 4);
-          const int kwrap = (NCH - sl0) * CH - 1;               // last window before the ring wraps
+          // the units reading row s: ja (window s + 5 - 11 ja in 0..10) and ja - 1 (window + 11, if <= 20); the
+          // older unit first so that it completes first
+          const int ja = (s + 5) / R, ka = s + 5 - R * ja;
 #pragma unroll
-          for (int k = 0; k < NWIN; ++k) {
+          for (int h = 0; h < 2; ++h) {
+            const int j = ja - 1 + h, k = ka + R * (1 - h);
+            if (j < rb0 || j >= rb0 + nu || k >= NWIN) continue;
+            const int pj = pi0 + (j - rb0), a = pj % NACC;
+            const bool first = s == max(0, R * j - 5);
+            if (first) {
+              if (pj >= NACC) {
+                C3P0 mbar_wait(&acc_empty[a], ((pj / NACC) - 1) & 1); C3P1(pc_acc)
+                tc_fence_after();
+              }
+              pi = pj + 1;
+            }
+            const uint32_t d = tmem + a * ACOLS;
             const uint64_t ad = adesc0 + (uint64_t)(((10 - k - IMIN) * TBLK) >> 4);   // T[10 - k] ..
-            umma_f16_ss(d, ad, bd, idesc, k != 0);
-            umma_f16_ss(d, ad + 2, bd + 2, idesc, 1);                       // channels 16..31: +32 B
-            bd += rstep;
-            if ((k % CH) == CH - 1) bd += padstep;
-            if (k == kwrap) bd -= ringstep;
+            umma_f16_ss(d, ad, bd, idesc, !first);
+            umma_f16_ss(d, ad + 2, bd + 2, idesc, 1);                                // channels 16..31: +32 B
+            if (s == min(R * j + 15, g.n1 - 1)) umma_commit(&acc_full[a]);          // the unit's last row
           }
-          umma_commit(&acc_full[a]);
-          umma_commit(&cempty[cj % NCH]);                     // chunk j is read by units j - NSPAN + 1 .. j only
+          bd += (uint64_t)(rowb >> 4);
+          if (cr == CHR - 1 || s == shi - 1) umma_commit(&cempty[gc++ % NSL]);     // the chunk is consumed
         }
-        for (int k = 0; k < NSPAN - 1; ++k) umma_commit(&cempty[(gc0 + nu + k) % NCH]);   // the item's last chunks
-        gc0 += nu + NSPAN - 1;
       }
 #ifdef DI_PROF_CONV3
       if (blockIdx.x % 37 == 0)
@@ -203,81 +198,91 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {  // ---------------------------------------------------------------------- epilogue
     // The RP x ES tap rows do not align with the 32-lane TMEM quadrants (ES = 11), so the four warps write their
     // quadrants into ONE shared tile S[lane][column] and then sum the 11 diagonals of every output from it:
-    // x_hat[row t][j] = sum_v S[t ES + v][j + v] -- 128 threads, consecutive j per warp (conflict-free).
+    // x_hat[row t][j] = sum_v S[t ES + v][j + v] -- 128 threads, consecutive j per warp (conflict-free).  Image i of
+    // the pair is TMEM columns i PP .. i PP + 79 of the unit's slot.
     const int q = warp - 4, e = threadIdx.x - 128;
     const float bsc = (!fullmap && bias) ? bias[0] : 0.f;
     int pi = 0;
     for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
-      int b, c0, rb0, nu;
-      item_of(g, it, b, c0, rb0, nu);
-      double m_se = 0.0, m_sx = 0.0;
-      float m_mx = -INFINITY;
-      for (int j = 0; j < nu; ++j, ++pi) {
-        const int r0 = (rb0 + j) * R;
+      int p, c0, rb0, nu;
+      item_of(g, it, p, c0, rb0, nu);
+      double m_se[2] = {0.0, 0.0}, m_sx[2] = {0.0, 0.0};
+      float m_mx[2] = {-INFINITY, -INFINITY};
+      for (int j = rb0; j < rb0 + nu; ++j, ++pi) {
+        const int r0 = j * R;
         const int a = pi % NACC;
-        // METRICS: the ground truth of this thread's outputs, loaded before the accumulator wait so the global-load
-        // latency overlaps it
-        float tv[OPT];
-        if (METRICS) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int b = 2 * p + i;
+          // METRICS: the ground truth of this thread's outputs, loaded before the accumulator wait / TMEM load
+          float tv[OPT];
+          if (METRICS) {
+#pragma unroll
+            for (int h = 0; h < OPT; ++h) {
+              const int idx = e + 128 * h, t = idx >> 6, jc = idx & 63, row = r0 + t;
+              tv[h] = (b < g.batch && idx < RP * 64 && jc < g.wseg && c0 + jc < g.n2 && row < g.n1)
+                          ? __ldg(xtrue + ((size_t)b * g.n1 + row) * g.n2 + c0 + jc) : 0.f;
+            }
+          }
+          if (i == 0) mbar_wait(&acc_full[a], (pi / NACC) & 1);
+          tc_fence_after();
+          const uint32_t taddr = tmem + a * ACOLS + i * g.PP + ((uint32_t)(q * 32) << 16);
+          uint32_t r[80];
+          tmem_ld32(taddr, r);
+          tmem_ld32(taddr + 32, r + 32);
+          tmem_ld16(taddr + 64, r + 64);
+          tmem_ld_wait();
+          if (i == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[a]);
+          }
+          named_bar(1, 128);          // the previous image's sums are done with S
+          const int L = q * 32 + lane;
+          if (L < SROWS) {
+            float4* dst = reinterpret_cast<float4*>(S + L * SROW);
+#pragma unroll
+            for (int jj = 0; jj < 20; ++jj)
+              dst[jj] = make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
+                                    __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
+          }
+          named_bar(1, 128);          // S holds every tap row of this image and unit
+          if (b >= g.batch) continue;
 #pragma unroll
           for (int h = 0; h < OPT; ++h) {
-            const int idx = e + 128 * h, t = idx >> 6, jc = idx & 63, row = r0 + t;
-            tv[h] = (idx < RP * 64 && jc < g.wseg && c0 + jc < g.n2 && row < g.n1)
-                        ? __ldg(xtrue + ((size_t)b * g.n1 + row) * g.n2 + c0 + jc) : 0.f;
-          }
-        }
-        mbar_wait(&acc_full[a], (pi / NACC) & 1);
-        tc_fence_after();
-        const uint32_t taddr = tmem + a * 128 + ((uint32_t)(q * 32) << 16);
-        uint32_t r[80];
-        tmem_ld32(taddr, r);
-        tmem_ld32(taddr + 32, r + 32);
-        tmem_ld16(taddr + 64, r + 64);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[a]);
-        named_bar(1, 128);          // the previous unit's sums are done with S
-        const int L = q * 32 + lane;
-        if (L < SROWS) {
-          float4* dst = reinterpret_cast<float4*>(S + L * SROW);
+            const int idx = e + 128 * h, t = idx >> 6, jc = idx & 63;
+            if (idx >= RP * 64) break;
+            const int row = r0 + t;
+            const float* sr = S + t * ES * SROW + jc;
+            float acc = 0.f;
 #pragma unroll
-          for (int jj = 0; jj < 20; ++jj)
-            dst[jj] = make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
-                                  __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
-        }
-        named_bar(1, 128);          // S holds every tap row of this unit
-#pragma unroll
-        for (int h = 0; h < OPT; ++h) {
-          const int idx = e + 128 * h, t = idx >> 6, jc = idx & 63;
-          if (idx >= RP * 64) break;
-          const int row = r0 + t;
-          const float* sr = S + t * ES * SROW + jc;
-          float acc = 0.f;
-#pragma unroll
-          for (int v = 0; v < 11; ++v) acc += sr[v * SROW + v];
-          if (jc < g.wseg && c0 + jc < g.n2 && row < g.n1) {
-            const size_t pix = ((size_t)b * g.n1 + row) * g.n2 + c0 + jc;
-            acc += (fullmap && bias) ? bias[pix % ((size_t)g.n1 * g.n2)] : bsc;
-            if (relu) acc = fmaxf(acc, 0.f);
-            xhat[pix] = acc;
-            if (METRICS) {
-              const float tt = tv[h];
-              const double dd = (double)acc - (double)tt;
-              m_se += dd * dd, m_sx += (double)tt * (double)tt, m_mx = fmaxf(m_mx, tt);
+            for (int v = 0; v < 11; ++v) acc += sr[v * SROW + v];
+            if (jc < g.wseg && c0 + jc < g.n2 && row < g.n1) {
+              const size_t pix = ((size_t)b * g.n1 + row) * g.n2 + c0 + jc;
+              acc += (fullmap && bias) ? bias[pix % ((size_t)g.n1 * g.n2)] : bsc;
+              if (relu) acc = fmaxf(acc, 0.f);
+              xhat[pix] = acc;
+              if (METRICS) {
+                const float tt = tv[h];
+                const double dd = (double)acc - (double)tt;
+                m_se[i] += dd * dd, m_sx[i] += (double)tt * (double)tt, m_mx[i] = fmaxf(m_mx[i], tt);
+              }
             }
           }
         }
       }
-      if (METRICS) {   // the warp's sums for this item, butterfly order fixed
-        for (int o = 16; o > 0; o >>= 1) {
-          m_se += __shfl_xor_sync(0xffffffffu, m_se, o);
-          m_sx += __shfl_xor_sync(0xffffffffu, m_sx, o);
-          m_mx = fmaxf(m_mx, __shfl_xor_sync(0xffffffffu, m_mx, o));
-        }
-        if (lane == 0) {
-          double* mp = mpart + ((size_t)it * 4 + q) * 3;
-          mp[0] = m_se, mp[1] = m_sx, mp[2] = (double)m_mx;
+      if (METRICS) {   // the warp's sums for this item and each image, butterfly order fixed
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          for (int o = 16; o > 0; o >>= 1) {
+            m_se[i] += __shfl_xor_sync(0xffffffffu, m_se[i], o);
+            m_sx[i] += __shfl_xor_sync(0xffffffffu, m_sx[i], o);
+            m_mx[i] = fmaxf(m_mx[i], __shfl_xor_sync(0xffffffffu, m_mx[i], o));
+          }
+          if (lane == 0) {
+            double* mp = mpart + (((size_t)it * 2 + i) * 4 + q) * 3;
+            mp[0] = m_se[i], mp[1] = m_sx[i], mp[2] = (double)m_mx[i];
+          }
         }
       }
     }
@@ -289,14 +294,14 @@ __global__ void __launch_bounds__(256, 1)
 
 static GeoR4 make_geo_r4(int batch, int n1, int n2, int num_sms) {
   GeoR4 g;
-  g.n1 = n1, g.n2 = n2;
+  g.n1 = n1, g.n2 = n2, g.batch = batch;
   g.wseg = n2 < 64 ? n2 : 64;
-  g.P = g.wseg + 10;
-  g.N = (g.P + 15) & ~15;
+  g.PP = conv3_r4_box_cols(n2);
+  g.N = 2 * g.PP;
   g.nrb = (n1 + R - 1) / R;
   g.ncs = (n2 + g.wseg - 1) / g.wseg;
-  const int cols = batch * g.ncs;
-  // fewer columns than SMs: split each column into parts of `per` row blocks
+  const int cols = (batch + 1) / 2 * g.ncs;
+  // fewer pair-columns than SMs: split each into parts of `per` row blocks
   g.splits = cols >= num_sms ? 1 : std::min(g.nrb, (num_sms + cols - 1) / cols);
   g.per = (g.nrb + g.splits - 1) / g.splits;
   g.splits = (g.nrb + g.per - 1) / g.per;
@@ -305,13 +310,13 @@ static GeoR4 make_geo_r4(int batch, int n1, int n2, int num_sms) {
 }
 
 static size_t smem_r4(int n2) {
-  const int wseg = n2 < 64 ? n2 : 64, P = wseg + 10;
-  const size_t slot = ((size_t)CH * P * 64 + 1023) & ~(size_t)1023;
-  const size_t ring_alloc = (NCH * slot + GUARD * 64 + 1023) & ~(size_t)1023;
-  return TBYTES + ring_alloc + (size_t)SROWS * SROW * 4 + 1024;
+  const size_t chunk = (size_t)CHR * 2 * conv3_r4_box_cols(n2) * 64;
+  return TBYTES + NSL * chunk + (size_t)SROWS * SROW * 4 + 1024;
 }
 
-int conv3_r4_box_rows() { return CH; }
+int conv3_r4_box_rows() { return CHR; }
+// positions per image in a strip row: the W + 10 padded columns rounded up to 16 (2 PP = the MMA N, a multiple of 16)
+int conv3_r4_box_cols(int n2) { return ((n2 < 64 ? n2 : 64) + 10 + 15) & ~15; }
 int conv3_r4_tpack_bytes() { return TBYTES; }
 
 cudaError_t setup_conv3_r4(int n2) {
@@ -321,14 +326,18 @@ cudaError_t setup_conv3_r4(int n2) {
   return cudaFuncSetAttribute(k_conv3_r4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r4(n2));
 }
 
-// per image b: the items b * per_img .. (b + 1) * per_img - 1, four warps each, summed in that order
-__global__ void k_metrics_finish(const double* __restrict__ mpart, int per_img, int N, int batch,
+// per image b (pair p = b / 2, i = b % 2): the items of pair p (per_pair consecutive items), four warps each, summed
+// in that order
+__global__ void k_metrics_finish(const double* __restrict__ mpart, int per_pair, int N, int batch,
                                  double* __restrict__ out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= batch) return;
   double se = 0.0, sx = 0.0, mx = -INFINITY;
-  const double* p = mpart + (size_t)b * per_img * 4 * 3;
-  for (int i = 0; i < per_img * 4; ++i) se += p[3 * i], sx += p[3 * i + 1], mx = fmax(mx, p[3 * i + 2]);
+  const int p = b >> 1, i = b & 1;
+  for (int t = 0; t < per_pair; ++t) {
+    const double* q = mpart + (((size_t)(p * per_pair + t) * 2 + i) * 4) * 3;
+    for (int w = 0; w < 4; ++w) se += q[3 * w], sx += q[3 * w + 1], mx = fmax(mx, q[3 * w + 2]);
+  }
   const double mse = se / N;
   out[b] = mse == 0.0 ? INFINITY : 10.0 * log10(mx * mx / mse);
   const double nmse = se / sx;
@@ -338,7 +347,7 @@ __global__ void k_metrics_finish(const double* __restrict__ mpart, int per_img, 
 
 size_t conv3_r4_metrics_part_bytes(int batch, int n1, int n2, int num_sms) {
   const GeoR4 g = make_geo_r4(batch, n1, n2, num_sms);
-  return (size_t)g.items * 4 * 3 * sizeof(double);
+  return (size_t)g.items * 2 * 4 * 3 * sizeof(double);
 }
 
 cudaError_t launch_conv3_r4(const CUtensorMap* tmH2, const void* tpack, const float* bias, int fullmap, int relu,

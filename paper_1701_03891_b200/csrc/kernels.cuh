@@ -130,6 +130,7 @@ constexpr int C3R_NWIN = C3R_RP + 10;           // windows (strip rows) per pass
 constexpr int C3R_IMIN = 11 - C3R_NWIN;
 constexpr int C3R_NENT = C3R_NWIN + C3R_RP - 1;
 int conv3_r4_box_rows();
+int conv3_r4_box_cols(int n2);   // positions per image of a strip row (W + 10 rounded up to 16)
 int conv3_r4_tpack_bytes();
 cudaError_t setup_conv3_r4(int n2);
 // xtrue (optional, DEVICE [batch][n1][n2] fp32): metrics fused into the epilogue -> metrics [3][batch] (PSNR, NMSE,
