@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Round-2 evidence summary from one gpurun capture (tools/scratch/r02j.sh):
+"""Round-2 evidence summary from one gpurun capture (tools/scratch/<tag>.sh):
    python tools/profile_summary_r02.py <tag>     (reads gpurun_out/<tag>/, writes profiles/r02_*)
 Files: r02_bench_lowrate.json (the bench line), r02_launches_lowrate.csv (+ table), r02_ncu_full.md (per-kernel
 --set full metrics; dram bytes per launch also into traffic.json), r02_ncu_pair_stress.md (the lifting GEMM on CTA
@@ -31,7 +31,7 @@ rows = "\n".join(f"| {s['cfg']} | {s['prec']} | {s['batch']} | {' / '.join(f'{x:
                  f"{s['total_ms']:.2f} | {s['images_per_s'] / 1e3:.1f} k | {s['conv2_tflops']:.0f} |" for s in stages)
 out = f"""# Round 2 — measured path (capture `{tag}`, {gpu})
 
-Commands (`tools/scratch/r02j.sh`, summarised by `tools/profile_summary_r02.py {tag}`): the `-m gpu` suite
+Commands (`tools/scratch/{tag}.sh`, summarised by `tools/profile_summary_r02.py {tag}`): the `-m gpu` suite
 ({tests}); `python bench.py` (20 timed steps, 5 warm-up, output check on); `tools/time_stages.py` per config; launch
 list `ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 --warmup 3
 --no-cpu-baseline --no-check`; full capture `ncu --set full --clock-control none --import-source on -k
