@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
         const int span = tile_span(g, L, ntiles);
         for (int t = 0; t < ntiles; ++t, ++ti) {
           const int n0 = t * span;
-          const int cnt = min(span, L - n0);
+          const int cnt = t == ntiles - 1 ? L - n0 : span;   // the last tile takes the rest (tile_span's short first tiles)
           const int nmma = min(NT, (cnt + TAPS - 1 + 15) & ~15);
           const uint32_t idesc = idesc_f32acc(1, 128, nmma);
           const int buf = ti & 1;
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
       const int span = tile_span(g, L, ntiles);
       for (int t = 0; t < ntiles; ++t, ++ti) {
         const int n0 = t * span;
-        const int cnt = min(span, L - n0);
+        const int cnt = t == ntiles - 1 ? L - n0 : span;
         const int buf = ti & 1;
         if (EG == 2 && buf != grp) continue;
         mbar_wait(&tfull[buf], (ti >> 1) & 1);

@@ -18,8 +18,12 @@
 // Three such rows would not fit the chunk ring of whole 21-row unit strips, so the strip is streamed instead: units
 // j (output rows 11 j ..) overlap by 10 strip rows, and every strip row s feeds the (at most two) units that read
 // it -- window s - 11 j + 5 of unit j -- in the same pass.  Each row is then consumed once and released: the ring
-// only holds the lead (NSL chunks of CHR rows), two units accumulate at a time (the third TMEM slot drains in the
-// epilogue), and rows outside the image (the 5 zero rows above / below) are never loaded or multiplied.
+// only holds the lead (NSL rows), two units accumulate at a time (the third TMEM slot drains in the epilogue), and rows
+// outside the image (the 5 zero rows above / below) are never loaded or multiplied.  The single issuing thread is
+// latency-bound (a general per-row loop -- unit indices, modulo slot arithmetic -- ran at ~230 cycles per MMA), so
+// rows are walked in groups of 11 aligned to the units (group jg: strip rows 11 jg - 5 + ka, ka = 0..10, feed unit
+// jg at window ka and unit jg - 1 at window ka + 11): per group the accumulators, first / last flags and clipping
+// are fixed, and the unrolled row loop is descriptor adds, one ring-slot wait and one commit per row.
 // Per 2 x 64 x 64 outputs: 114 windows x 2 MMAs of N = 160 against 2 x 126 x 2 of N = 80.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -37,14 +41,17 @@ namespace di {
 namespace {
 constexpr int RP = C3R_RP, ES = C3R_ES, NWIN = C3R_NWIN, IMIN = C3R_IMIN;
 constexpr int R = RP;                  // output rows per unit
-constexpr int CHR = 2;                 // strip rows per TMA chunk
-constexpr int NSL = 6;                 // chunk slots in the ring (12 rows of lead)
+constexpr int CHR = 1;                 // strip rows per TMA chunk (= ring slot)
+#ifndef DI_C3R_NSL
+#define DI_C3R_NSL 12
+#endif
+constexpr int NSL = DI_C3R_NSL;        // ring slots (rows of lead)
 constexpr int NACC = 3;                // TMEM accumulator slots: two units accumulate, one drains
 constexpr int ACOLS = 160;             // TMEM columns per slot (N <= 160)
 #ifndef DI_C3R_PF
-#define DI_C3R_PF 6
+#define DI_C3R_PF 16
 #endif
-constexpr int C3R_PF = DI_C3R_PF;      // chunks prefetched into L2 ahead of the shared-memory loads
+constexpr int C3R_PF = DI_C3R_PF;      // rows prefetched into L2 ahead of the shared-memory loads
 constexpr int TBLK = ES * 64;          // one T entry: ES rows (v) x 32 channels bf16, SWIZZLE_64B
 constexpr int TBYTES = (C3R_NENT * TBLK + 1023) & ~1023;
 constexpr int SROW = 84;               // epilogue tile row stride (floats): 16-B rows
@@ -141,8 +148,13 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t idesc = idesc_f32acc(1, 128, g.N);
       const uint64_t adesc0 = smem_desc(smem_u32(tb), 16, 512, kSwizzle64B);
       const uint64_t bdesc0 = smem_desc(smem_u32(ring), 16, 512, kSwizzle64B);
-      uint32_t gc = 0;                 // chunks consumed (CTA-wide)
-      int pi = 0;                      // units started (CTA-wide): unit pi accumulates in slot pi % NACC
+      const uint64_t rstep = (uint64_t)(rowb >> 4);
+      constexpr uint64_t TSTEP = TBLK >> 4;                                     // one T entry
+      const uint64_t aw0 = adesc0 + (uint64_t)(10 - IMIN) * TSTEP;              // window 0: T[10]
+      uint64_t bd = bdesc0;            // ring slot sl of the next row
+      uint32_t sl = 0, ph = 0;         // ring slot, its fill parity
+      uint32_t an = 0, aph = 0;        // TMEM slot of the next unit to start, and its reuse parity
+      int pi = 0;                      // units started (CTA-wide)
 #ifdef DI_PROF_CONV3
       long long pc_chunk = 0, pc_acc = 0, pc0 = clock64(), pt;
 #define C3P0 pt = clock64();
@@ -154,39 +166,45 @@ __global__ void __launch_bounds__(256, 1)
       for (int it = blockIdx.x; it < g.items; it += gridDim.x) {
         int p, c0, rb0, nu;
         item_of(g, it, p, c0, rb0, nu);
-        const int slo = rows_lo(rb0), shi = rows_hi(g, rb0, nu), pi0 = pi;
-        uint64_t bd = 0;
-        for (int s = slo; s < shi; ++s) {
-          const int cr = (s - slo) % CHR;
-          if (cr == 0) {                                   // the row opens a chunk
-            C3P0 mbar_wait(&cfull[gc % NSL], (gc / NSL) & 1); C3P1(pc_chunk)
-            tc_fence_after();
-            bd = bdesc0 + (uint64_t)(((gc % NSL) * chunk_bytes) >> 4);
-          }
-          // the units reading row s: ja (window s + 5 - 11 ja in 0..10) and ja - 1 (window + 11, if <= 20); the
-          // older unit first so that it completes first
-          const int ja = (s + 5) / R, ka = s + 5 - R * ja;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j = ja - 1 + h, k = ka + R * (1 - h);
-            if (j < rb0 || j >= rb0 + nu || k >= NWIN) continue;
-            const int pj = pi0 + (j - rb0), a = pj % NACC;
-            const bool first = s == max(0, R * j - 5);
-            if (first) {
-              if (pj >= NACC) {
-                C3P0 mbar_wait(&acc_empty[a], ((pj / NACC) - 1) & 1); C3P1(pc_acc)
-                tc_fence_after();
-              }
-              pi = pj + 1;
+        const int slo = rows_lo(rb0), shi = rows_hi(g, rb0, nu);
+        uint32_t dold = 0, aold = 0;
+        for (int jg = rb0; jg <= rb0 + nu; ++jg) {
+          const bool hasN = jg < rb0 + nu, hasO = jg > rb0;
+          const int sb = R * jg - 5;                                    // strip row of ka = 0
+          const int klo = max(0, slo - sb), khi = min(R, shi - sb);
+          uint32_t dnew = 0;
+          if (hasN) {                                                   // unit jg starts in this group
+            if (pi >= NACC) {
+              C3P0 mbar_wait(&acc_empty[an], aph ^ 1); C3P1(pc_acc)
+              tc_fence_after();
             }
-            const uint32_t d = tmem + a * ACOLS;
-            const uint64_t ad = adesc0 + (uint64_t)(((10 - k - IMIN) * TBLK) >> 4);   // T[10 - k] ..
-            umma_f16_ss(d, ad, bd, idesc, !first);
-            umma_f16_ss(d, ad + 2, bd + 2, idesc, 1);                                // channels 16..31: +32 B
-            if (s == min(R * j + 15, g.n1 - 1)) umma_commit(&acc_full[a]);          // the unit's last row
+            dnew = tmem + an * ACOLS;
           }
-          bd += (uint64_t)(rowb >> 4);
-          if (cr == CHR - 1 || s == shi - 1) umma_commit(&cempty[gc++ % NSL]);     // the chunk is consumed
+#pragma unroll
+          for (int ka = 0; ka < R; ++ka) {
+            if (ka < klo || ka >= khi) continue;
+            C3P0 mbar_wait(&cfull[sl], ph); C3P1(pc_chunk)
+            tc_fence_after();
+            if (hasO && ka < NWIN - R) {                                // unit jg - 1, window ka + 11
+              const uint64_t ad = aw0 - (uint64_t)(ka + R) * TSTEP;
+              umma_f16_ss(dold, ad, bd, idesc, 1);
+              umma_f16_ss(dold, ad + 2, bd + 2, idesc, 1);              // channels 16..31: +32 B
+            }
+            if (hasN) {                                                 // unit jg, window ka
+              const uint64_t ad = aw0 - (uint64_t)ka * TSTEP;
+              umma_f16_ss(dnew, ad, bd, idesc, ka != klo);
+              umma_f16_ss(dnew, ad + 2, bd + 2, idesc, 1);
+            }
+            umma_commit(&cempty[sl]);                                   // the row is consumed
+            bd += rstep;
+            if (++sl == NSL) sl = 0, ph ^= 1, bd = bdesc0;
+          }
+          if (hasO) umma_commit(&acc_full[aold]);                       // unit jg - 1 is complete
+          if (hasN) {
+            dold = dnew, aold = an;
+            ++pi;
+            if (++an == NACC) an = 0, aph ^= 1;
+          }
         }
       }
 #ifdef DI_PROF_CONV3
