@@ -214,22 +214,51 @@ class ClockSampler:
                 "window": "timed region only" if inside else "whole sampler run"}
 
 
+def _conv2_tiles(L: int):
+    """Output counts of k_conv2_tc's tiles for a unit of L strip positions: ceil(L / 253) tiles sharing the outputs
+    evenly, or -- when that saves MMA columns -- first tiles one 16-column step shorter and the rest in the last."""
+    r16 = lambda x: (x + 15) // 16 * 16
+    nt = -(-L // 253)
+    s = -(-L // nt)
+    sf = (s + 3) // 16 * 16 - 3
+    lf = L - (nt - 1) * sf
+    cols = lambda sp, last: (nt - 1) * r16(sp + 3) + r16(last + 3)
+    if sf > 0 and lf <= 253 and cols(sf, lf) < cols(s, L - (nt - 1) * s):
+        s = sf
+    return [s] * (nt - 1) + [L - (nt - 1) * s]
+
+
+def conv2_row_blocks(n1: int, n2: int, rows: int = 6):
+    """k_conv2_tc's row blocks (r0, height): `rows`-row blocks and a short last one, or (one column segment) ntall
+    blocks of rows + 1 then rows-row ones when every block runs the same number of tiles and the image needs fewer
+    tiles (mixed row-block heights)."""
+    wseg = min(n2, 64)
+    P = n2 + 5 if n2 <= 64 else wseg + 10
+    uni = [(r0, min(rows, n1 - r0)) for r0 in range(0, n1, rows)]
+    nrb = (n1 + rows) // (rows + 1)
+    ntall = n1 - rows * nrb
+    ntl = lambda h: len(_conv2_tiles((h - 1) * P + wseg))
+    if n2 > 64 or not 0 < ntall <= nrb or ntl(rows + 1) != ntl(rows):
+        return uni
+    mixed, r0 = [], 0
+    for rb in range(nrb):
+        h = rows + (rb < ntall)
+        mixed.append((r0, h))
+        r0 += h
+    return mixed if sum(ntl(h) for _, h in mixed) < sum(ntl(h) for _, h in uni) else uni
+
+
 def conv2_useful_mac_ceiling(n1: int, n2: int, rows: int = 6) -> float:
     """Fraction of the tensor-core MACs k_conv2_tc issues that are useful: 11 of 12 column-tap slots,
-    times output positions over MMA columns -- units of `rows` output rows x <= 64 columns, strip pitch n2 + 5 (one
-    column segment) or 74, ceil(L / 253) tiles sharing a unit's L outputs evenly (k_conv2_tc's balanced tiles), each
-    issued as N = round16(count + 3) <= 256 columns."""
+    times output positions over MMA columns -- row blocks of conv2_row_blocks x <= 64 columns, strip pitch n2 + 5 (one
+    column segment) or 74, tiles of _conv2_tiles, each issued as N = round16(count + 3) <= 256 columns."""
     wseg = min(n2, 64)
     ncs = -(-n2 // wseg)
     P = n2 + 5 if ncs == 1 else wseg + 10
     useful = cols = 0
-    for r0 in range(0, n1, rows):
-        rr = min(rows, n1 - r0)
+    for _, rr in conv2_row_blocks(n1, n2, rows):
         L = (rr - 1) * P + wseg
-        nt = -(-L // 253)
-        span = -(-L // nt)
-        for t in range(nt):
-            cnt = min(span, L - span * t)
+        for cnt in _conv2_tiles(L):
             cols += min(256, (cnt + 3 + 15) // 16 * 16)
         useful += rr * wseg
     return 11.0 / 12.0 * useful / cols

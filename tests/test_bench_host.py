@@ -3,11 +3,24 @@ import bench
 
 
 def test_conv2_design_ceiling_lowrate():
-    # 64x64: ten 6-row units of 416 MMA columns (balanced 205 + 204 -> 208 + 208) and a 4-row unit (271 -> 136 + 135 ->
-    # 144 + 144) for 4096
-    # outputs; 11 of 12 column-tap slots useful
-    expected = 11 / 12 * 4096 / (10 * 416 + 288)
+    # 64x64 (mixed row-block heights): four 7-row units of 478 positions (237 + 241 outputs -> 240 + 256
+    # MMA columns) and six 6-row units (205 + 204 -> 208 + 208) for 4096 outputs; 11 of 12 column-tap slots useful
+    expected = 11 / 12 * 4096 / (4 * 496 + 6 * 416)
     assert abs(bench.conv2_useful_mac_ceiling(64, 64) - expected) < 1e-12
+    assert bench.conv2_row_blocks(64, 64) == [(0, 7), (7, 7), (14, 7), (21, 7)] + [(28 + 6 * i, 6) for i in range(6)]
+
+
+def test_conv2_row_blocks_rule():
+    # uniform where mixing saves no tile: two column segments (a 7-row unit of pitch 74 needs 3 tiles), n1 = 9 / 33
+    assert bench.conv2_row_blocks(128, 128) == [(r, min(6, 128 - r)) for r in range(0, 128, 6)]
+    assert bench.conv2_row_blocks(9, 13) == [(0, 6), (6, 3)]
+    assert bench.conv2_row_blocks(33, 33) == [(r, min(6, 33 - r)) for r in range(0, 33, 6)]
+    # the blocks tile the image exactly, heights R or R + 1, tall ones first
+    for n1, n2 in [(64, 64), (61, 64), (50, 40), (20, 20), (64, 16)]:
+        blocks = bench.conv2_row_blocks(n1, n2)
+        assert blocks[0][0] == 0 and sum(h for _, h in blocks) == n1
+        assert all(b[0] + b[1] == c[0] for b, c in zip(blocks, blocks[1:]))
+    assert bench._conv2_tiles(478) == [237, 241] and bench._conv2_tiles(409) == [205, 204]
 
 
 def test_conv2_design_ceiling_pitch74_and_bounds():
