@@ -458,8 +458,13 @@ static Geo make_geo_c2(int batch, int n1, int n2, int mixed) {
   const int nt = mixed ? conv2_tc_tall_blocks(n1, n2) : 0;
   if (nt > 0) {
     g.nrb = (n1 + C2_ROWS) / (C2_ROWS + 1);
-    g.ntall = nt, g.nfull = nt, g.srows = C2_ROWS + 11;
+    g.ntall = nt, g.srows = C2_ROWS + 11;
     g.units = batch * g.nrb * g.ncs;
+    // every unit runs two tiles, so multicast pairs always consume the same K-blocks; they also keep the same pace
+    // when a pair never straddles a tall and a short unit: with an even count of each per image the natural order
+    // (image by image, row blocks top to bottom -- neighbouring CTAs share strip rows in L2) does that, otherwise the
+    // tall units of all images go first
+    g.nfull = (nt * g.ncs) % 2 == 0 && ((g.nrb - nt) * g.ncs) % 2 == 0 ? g.nrb : nt;
   }
   return g;
 }
@@ -468,6 +473,8 @@ static Geo make_geo_c2(int batch, int n1, int n2, int mixed) {
 // grid, an even remainder of units over the grid, and the last row-block's units as many tiles as the full ones.
 static bool pair_balanced(const Geo& g, int grid, int R, int cl = 2) {
   (void)R;   // full-tile units first (unit_of): the boundary to the shorter units must fall between clusters
+  if (g.ntall > 0 && g.nfull == g.nrb && ((g.ntall * g.ncs) % cl != 0 || (g.nrb * g.ncs) % cl != 0))
+    return false;   // mixed heights in natural order: clusters of cl units must not straddle a tall and a short unit
   return grid % cl == 0 && (g.units % grid) % cl == 0 && (g.batch * g.nfull * g.ncs) % cl == 0;
 }
 // And every pair must be co-resident: a GPC with an odd number of usable SMs cannot host a 2-CTA cluster on all of
