@@ -113,6 +113,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
+  griddep_wait();                 // the preceding grid's outputs (PDL: only the prologue above overlapped it)
+  griddep_launch_dependents();
   const int per_img = g.nrb * g.ncs;
   const int P = g.P, W = g.wseg;
 
@@ -950,11 +952,9 @@ cudaError_t launch_conv1_tc(const CUtensorMap* tmX, const CUtensorMap* tmS, cons
   const int grid = g.units < num_sms ? g.units : num_sms;
   auto k = tmX ? k_conv1_tc<true> : k_conv1_tc<false>;
   CUtensorMap dummy{};
-  k<<<grid, 384, conv1_tc_smem_bytes(), st>>>(tmX ? *tmX : dummy, tmS ? *tmS : dummy, tmS ? 1 : 0,
-                                              reinterpret_cast<const __nv_bfloat16*>(xt),
-                                              reinterpret_cast<const uint8_t*>(w1pack), bias, fullmap, g,
-                                              reinterpret_cast<__nv_bfloat16*>(h1));
-  return cudaGetLastError();
+  return launch_ex(k, dim3(grid), dim3(384), conv1_tc_smem_bytes(), st, 1, true, tmX ? *tmX : dummy,
+                   tmS ? *tmS : dummy, tmS ? 1 : 0, reinterpret_cast<const __nv_bfloat16*>(xt),
+                   reinterpret_cast<const uint8_t*>(w1pack), bias, fullmap, g, reinterpret_cast<__nv_bfloat16*>(h1));
 }
 
 cudaError_t launch_conv3_tc(const CUtensorMap* tmH2, const void* w3pack, const float* bias, int fullmap, int relu,

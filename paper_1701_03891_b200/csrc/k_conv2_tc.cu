@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
   if (CL > 1) cluster_sync_all();   // the peers' barriers are initialised before any multicast copy or commit
   tc_fence_after();
   const uint32_t tmem = tslot;
+  griddep_wait();                 // the preceding grid's outputs (PDL: only the prologue above overlapped it)
+  griddep_launch_dependents();
   const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
   constexpr uint16_t CMASK = (uint16_t)((1u << CL) - 1);
 
@@ -510,17 +512,12 @@ static bool pairs_fit(Kern kern, int grid, int threads, size_t smem, int cl = 2)
     return cl * n >= grid;
   }
 }
+// cluster launch, programmatic dependent launch (the kernel waits for its predecessor in griddep_wait)
 template <typename... Args>
 static cudaError_t launch_pair(void (*kern)(Args...), int grid, int threads, size_t smem, cudaStream_t st,
                                const CUtensorMap& tm, const __nv_bfloat16* w, const float* bias, int fullmap, Geo g,
                                __nv_bfloat16* out, const __nv_bfloat16* mask, int cl = 2) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid), cfg.blockDim = dim3(threads), cfg.dynamicSmemBytes = smem, cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cl, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
-  cfg.attrs = at, cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tm, w, bias, fullmap, g, out, mask);
+  return launch_ex(kern, dim3(grid), dim3(threads), smem, st, cl, true, tm, w, bias, fullmap, g, out, mask);
 }
 
 // room for the R + 11-row strip of mixed heights whenever they may apply (one column segment)
@@ -584,10 +581,8 @@ cudaError_t launch_conv2_tc(const CUtensorMap* tmH1, const void* wpack, const fl
   if (cluster >= 2 && pair_balanced(g, grid, R) && pairs_fit(k_conv2_tc<64, 32, C2_BIAS_RELU, 2>, grid, 256, sm))
     return launch_pair(k_conv2_tc<64, 32, C2_BIAS_RELU, 2>, grid, 256, sm, st, *tmH1, w, bias, fullmap, g, out,
                        (const __nv_bfloat16*)nullptr);
-  k_conv2_tc<64, 32, C2_BIAS_RELU><<<grid, 256, conv2_tc_smem_bytes(n2), st>>>(
-      *tmH1, reinterpret_cast<const __nv_bfloat16*>(wpack), bias, fullmap, g, reinterpret_cast<__nv_bfloat16*>(h2),
-      nullptr);
-  return cudaGetLastError();
+  return launch_pair(k_conv2_tc<64, 32, C2_BIAS_RELU>, grid, 256, sm, st, *tmH1, w, bias, fullmap, g, out,
+                     (const __nv_bfloat16*)nullptr, 1);
 }
 
 // custom stacks, BF16 contexts: interior C_in -> C_out layers (C in {32, 64}) on the same

@@ -107,6 +107,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
+  griddep_wait();                 // the preceding grid's outputs (PDL: only the prologue above overlapped it)
+  griddep_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ producer: T once, strip chunks
@@ -172,6 +174,9 @@ __global__ void __launch_bounds__(256, 1)
           const bool hasN = jg < rb0 + nu, hasO = jg > rb0;
           const int sb = R * jg - 5;                                    // strip row of ka = 0
           const int klo = max(0, slo - sb), khi = min(R, shi - sb);
+          // a starting unit has rows in its first group (its accumulate-0 MMA), and N fits one TMEM slot
+          DI_DEVICE_ASSERT(!hasN || (klo < khi && klo <= 5), klo, khi);
+          DI_DEVICE_ASSERT(g.N <= ACOLS, g.N, ACOLS);
           uint32_t dnew = 0;
           if (hasN) {                                                   // unit jg starts in this group
             if (pi >= NACC) {
@@ -374,11 +379,12 @@ cudaError_t launch_conv3_r4(const CUtensorMap* tmH2, const void* tpack, const fl
   GeoR4 g = make_geo_r4(batch, n1, n2, num_sms);
   const int grid = g.items < num_sms ? g.items : num_sms;
   if (xtrue)
-    k_conv3_r4<true><<<grid, 256, smem_r4(n2), st>>>(*tmH2, reinterpret_cast<const uint8_t*>(tpack), bias, fullmap,
-                                                    relu, g, xhat, xtrue, mpart);
+    launch_ex(k_conv3_r4<true>, dim3(grid), dim3(256), smem_r4(n2), st, 1, true, *tmH2,
+              reinterpret_cast<const uint8_t*>(tpack), bias, fullmap, relu, g, xhat, xtrue, mpart);
   else
-    k_conv3_r4<false><<<grid, 256, smem_r4(n2), st>>>(*tmH2, reinterpret_cast<const uint8_t*>(tpack), bias, fullmap,
-                                                     relu, g, xhat, nullptr, nullptr);
+    launch_ex(k_conv3_r4<false>, dim3(grid), dim3(256), smem_r4(n2), st, 1, true, *tmH2,
+              reinterpret_cast<const uint8_t*>(tpack), bias, fullmap, relu, g, xhat, (const float*)nullptr,
+              (double*)nullptr);
   if (xtrue) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

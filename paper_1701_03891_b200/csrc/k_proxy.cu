@@ -62,6 +62,8 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
+  griddep_wait();                 // the preceding grid's outputs (PDL: only the prologue above overlapped it)
+  griddep_launch_dependents();
 
   if (warp == 0 && lane == 0) {  // ---------------- TMA producer
     for (int kb = 0; kb < kblocks; ++kb) {
@@ -195,6 +197,8 @@ __global__ void __launch_bounds__(128, 1)
   cluster_sync_all();   // both CTAs' barriers initialised and TMEM allocated before any remote arrive / MMA
   tc_fence_after();
   const uint32_t tmem = tslot;
+  griddep_wait();                 // the preceding grid's outputs (PDL: only the prologue above overlapped it)
+  griddep_launch_dependents();
 
   if (warp == 0 && lane == 0) {  // ---------------- TMA producer (both CTAs)
     const int nblk = (N + BN - 1) / BN;
@@ -283,10 +287,12 @@ cudaError_t launch_proxy_pair(const CUtensorMap* tmY, const CUtensorMap* tmPh, i
   const int nbt = (batch + 255) / 256, npt = (N + 2 * bn - 1) / (2 * bn);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * nbt * npt), cfg.blockDim = dim3(128), cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
-  cfg.attrs = at, cfg.numAttrs = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL: the kernel waits in griddep_wait
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at, cfg.numAttrs = 2;
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(xt);
   if (bn == 224) {
     cfg.dynamicSmemBytes = px2_smem<224>();
@@ -305,7 +311,8 @@ template <int ELT, bool OF32, int MB, int BN>
 static void px_launch(const CUtensorMap* tmY, const CUtensorMap* tmPt, int batch, int N, int kblocks, void* xt,
                       cudaStream_t st, const ProxyScatter& s0, int bb) {
   const int nbt = (batch + PX_BM * MB - 1) / (PX_BM * MB), nnt = (N + BN - 1) / BN;
-  k_proxy_tc<ELT, OF32, MB, BN><<<nbt * nnt, 128, px_smem<MB, BN>(), st>>>(*tmY, *tmPt, batch, N, kblocks, xt, s0, bb);
+  launch_ex(k_proxy_tc<ELT, OF32, MB, BN>, dim3(nbt * nnt), dim3(128), px_smem<MB, BN>(), st, 1, true, *tmY, *tmPt, batch,
+            N, kblocks, xt, s0, bb);
 }
 template <int ELT, bool OF32, int MB, int BN>
 static cudaError_t px_setup() {

@@ -223,6 +223,14 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
       : "memory");
 }
 __device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Programmatic dependent launch (PDL).  griddep_wait: block until the preceding grid in the stream has completed and
+// its memory is visible (a no-op when this grid was launched without programmatic serialization); every kernel
+// calls it before its first global access to data another kernel produces or reads (activations AND weights: a
+// training step may have just rewritten them), so only the prologue (barrier init, TMEM allocation, descriptor
+// prefetch) overlaps the predecessor's tail.  griddep_launch_dependents: let the next grid launch now (its CTAs take
+// the SMs this grid's CTAs free).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // wait until at most N bulk groups of this thread still READ their shared-memory source
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -437,6 +445,29 @@ __device__ __forceinline__ bool elect_one() {
       : "=r"(pred)
       : "r"(0xffffffffu));
   return pred != 0;
+}
+
+// host: launch with an optional cluster dimension and programmatic dependent launch (the kernel calls griddep_wait
+// before touching data of the preceding grid)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                             bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid, cfg.blockDim = block, cfg.dynamicSmemBytes = smem, cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  unsigned n = 0;
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster, at[n].val.clusterDim.y = 1, at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = at, cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 }  // namespace di
