@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256, 1)
     // The RP x ES tap rows do not align with the 32-lane TMEM quadrants (ES = 11), so the four warps write their
     // quadrants into ONE shared tile S[lane][column] and then sum the 11 diagonals of every output from it:
     // x_hat[row t][j] = sum_v S[t ES + v][j + v] -- 128 threads, consecutive j per warp (conflict-free).  Image i of
-    // the pair is TMEM columns i PP .. i PP + 79 of the unit's slot.
+    // the pair is TMEM columns i PP .. i PP + 75 of the unit's slot.
     const int q = warp - 4, e = threadIdx.x - 128;
     const float bsc = (!fullmap && bias) ? bias[0] : 0.f;
     int pi = 0;
@@ -250,10 +250,11 @@ __global__ void __launch_bounds__(256, 1)
           if (i == 0) mbar_wait(&acc_full[a], (pi / NACC) & 1);
           tc_fence_after();
           const uint32_t taddr = tmem + a * ACOLS + i * g.PP + ((uint32_t)(q * 32) << 16);
-          uint32_t r[80];
+          uint32_t r[76];             // outputs j < 64 read columns j + v <= 73
           tmem_ld32(taddr, r);
           tmem_ld32(taddr + 32, r + 32);
-          tmem_ld16(taddr + 64, r + 64);
+          tmem_ld8(taddr + 64, r + 64);
+          tmem_ld4(taddr + 72, r + 72);
           tmem_ld_wait();
           if (i == 1) {
             tc_fence_before();
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(256, 1)
           if (L < SROWS) {
             float4* dst = reinterpret_cast<float4*>(S + L * SROW);
 #pragma unroll
-            for (int jj = 0; jj < 20; ++jj)
+            for (int jj = 0; jj < 19; ++jj)
               dst[jj] = make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
                                     __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
           }
