@@ -136,8 +136,8 @@ di_status di_recover_from_slots(di_ctx ctx, const float* staging, int world, int
 
 /* End-to-end variant with HOST buffers: copies y (host, pinned or pageable) to the device, recovers, copies
  * x_hat back to `xhat_host` (pinned host memory makes the copies asynchronous).  Kernels run on `stream`; batches
- * >= 512 are split into chunks of halving size (B/2, B/4, ..., >= 128) whose x_hat copies run on an internal
- * stream, overlapping the next chunk's kernels.  Returns after all work and copies have completed.  Results equal di_recover's bit for bit (every
+ * >= 512 are split into chunks shrinking 4x (3B/4, 3B/16, ..., the last >= 128 images) whose x_hat copies run on an
+ * internal stream, overlapping the next chunk's kernels.  Returns after all work and copies have completed.  Results equal di_recover's bit for bit (every
  * image is computed independently of the batch composition). */
 di_status di_recover_host(di_ctx ctx, const void* y_host, long long ldy, int batch, float* xhat_host,
                           void* stream);

@@ -150,6 +150,7 @@ struct di_ctx_s {
   float* xhost_dev = nullptr;
   cudaStream_t cstream = nullptr;               // di_recover_host: device->host copy stream
   cudaEvent_t cev[17] = {};                      // di_recover_host: chunk-done events (+ the y-copy event)
+  int host_chunk_ratio = 4;                      // di_recover_host: chunk k+1 = chunk k / ratio (DI_EXP_E2E_RATIO)
   long long ws_bytes = 0;
   CUtensorMap tmPt{}, tmH1{}, tmH2{}, tmX{};
   CUtensorMap tmH1s{};          // BF16, n2 % 64 == 0: conv1's TMA store map over h1 (encode_h1_store)
@@ -996,6 +997,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   c->fused_metrics = getenv("DI_EXP_FUSED_METRICS") != nullptr && atoi(getenv("DI_EXP_FUSED_METRICS")) != 0;
   c->conv2_balanced = !(getenv("DI_EXP_C2_SPLIT") && atoi(getenv("DI_EXP_C2_SPLIT")) == 253);
   c->conv2_mixed = !(getenv("DI_EXP_C2_MIXED") && atoi(getenv("DI_EXP_C2_MIXED")) == 0);
+  c->host_chunk_ratio = getenv("DI_EXP_E2E_RATIO") ? std::max(2, atoi(getenv("DI_EXP_E2E_RATIO"))) : 4;
 #ifdef DI_DEBUG
   {
     di_status sd = debug_bind();
@@ -1386,22 +1388,25 @@ di_status di_recover_host(di_ctx c, const void* y_host, long long ldy, int batch
   if (!c->cstream) CUDA_TRY(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
   for (auto& e : c->cev)
     if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  // Chunks of halving size (batch/2, batch/4, ..., >= 128 images): the device->host copy of x_hat for chunk k (copy
-  // stream) overlaps the kernels of chunk k+1 (caller's stream), and the last, smallest chunk leaves only a short
-  // copy exposed (x_hat leaves ~6x faster over PCIe than the path computes it).  Chunks share the workspace:
-  // chunk k+1 only overwrites x_tilde/h1/h2, never the x_hat rows chunk k is still copying out.
+  // Chunks shrinking geometrically by host_chunk_ratio r (4: 3B/4, 3B/16, ... while >= 128 images are left): the
+  // device->host copy of x_hat for chunk k (copy stream) overlaps the kernels of chunk k+1 (caller's stream).  x_hat
+  // leaves over PCIe ~4.7x faster than the path computes it (r02 e2e probe: 1.45 ms for 67 MB vs 6.9 ms), so a
+  // chunk r = 4 times smaller still covers its predecessor's copy, and only the last, small chunk's copy is exposed.
+  // Few chunks matter as much: every chunk pays the four kernels' ramp-up and drain (r = 2, the r01 plan, ran 6
+  // chunks).  Chunks share the workspace: chunk k+1 only overwrites x_tilde/h1/h2, never the x_hat rows chunk k is
+  // still copying out.
   int cuts[17] = {0};
   int nchunk = 0;
   if (batch >= 512) {
-    int left = batch, sz = (batch / 2) & ~3;
+    const int r = c->host_chunk_ratio;
+    int left = batch;
     while (left > 0 && nchunk < 15) {
-      const int take = (left - sz < 128) ? left : sz;
+      int take = (left - left / r) & ~3;
+      if (left - take < 128 || nchunk == 14) take = left;
       cuts[nchunk + 1] = cuts[nchunk] + take;
       ++nchunk;
       left -= take;
-      sz = std::max(128, (sz / 2) & ~3);
     }
-    if (left > 0) cuts[nchunk] += left;
   } else {
     cuts[1] = batch, nchunk = 1;
   }

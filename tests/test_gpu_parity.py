@@ -202,7 +202,7 @@ def test_host_e2e_matches_device():
 
 
 def test_host_e2e_multichunk_bitwise():
-    """di_recover_host's chunked branch (batch >= 512: halving chunks, y split between the compute and the copy
+    """di_recover_host's chunked branch (batch >= 512: chunks shrinking 4x: 3072 + 768 + 260 at 4100, y split between the compute and the copy
     stream, per-chunk D2H on the copy stream) gives bitwise the device-resident di_recover result: batch 512, 515
     (ragged last chunk), 4096 (the bench's e2e call) and max_batch, with pinned and pageable y, repeated on the same
     context (workspace reuse, y staging regrown)."""
