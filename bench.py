@@ -479,6 +479,17 @@ def run_ours(args):
                           "conv2": stage_ms[2] / max(calls, 1), "conv3": stage_ms[3] / max(calls, 1)},
             "path_tflops": (PATH_FLOP_PER_PX + 2 * c.m) * c.N * B / (per_step / 1e3) / 1e12,
             "per_gpu_images_s": B / (per_step / 1e3)}
+    if prec == "bf16":
+        # the thin layers against HBM: algorithmic bytes = bf16 h1 written by conv1 (128 B/px) and bf16
+        # h2 read + fp32 x_hat written by conv3 (64 + 4 B/px), over each kernel's mean launch time; both kernels are
+        # bound by the shared-memory port, not by HBM (ncu tc + lsu shared wavefronts, profiles/r04_*)
+        thin = {}
+        for name, idx, bpp in (("conv1", 1, 128), ("conv3", 3, 68)):
+            t = stage_ms[idx] / max(calls, 1) / 1e3
+            gbs = bpp * B * c.N / t / 1e9
+            thin[name] = {"achieved_GBs": gbs, "peak_GBs": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"],
+                          "bytes_per_px": bpp, "launch_ms": t * 1e3}
+        line["thin_layers"] = thin
 
     # ---------------- sensing model and metrics around the path, device-timed
     xt_dev = torch.from_numpy(x).to(dev)
@@ -503,6 +514,10 @@ def run_ours(args):
                        "recover_metrics_ms_incl_d2h": sev[4].elapsed_time(sev[5]),
                        "recover_metrics_equals_separate_psnr": bool(np.allclose(mf[0], mt[0], rtol=0, atol=1e-9)),
                        "mean_psnr_db_random_init": float(np.mean(mt[0]))}
+
+    # ---------------- training step, device-timed on its own context
+    if not args.no_train:
+        line["training"] = train_probe(c, prec, phi, x, y, B, world, local, dev)
 
     # ---------------- output check (outside the timed region): gather x_hat of every rank to rank 0 (NCCL
     # all_gather -- the only use of a collective on outputs); rank 0 re-recovers the first and
@@ -536,6 +551,54 @@ def run_ours(args):
         barrier(dev)
         dist.destroy_process_group()
     return 0 if ok else 1
+
+
+def train_probe(c, prec, phi, x, y, B, world, local, dev, batch=1024, steps=10, warmup=3) -> dict:
+    """One data-parallel SGD step per iteration: di_train_grad of this
+    rank's first `batch` images with scale 1/global batch, the NCCL all-reduce of the gradient (the method's only
+    hot collective; absent at N = 1), di_sgd_step.  Own context (the weights change), per-channel biases; CUDA events
+    on the launching stream, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import synth
+    from paper_1701_03891_b200 import DeepInverse
+    bt = min(batch, B)
+    st = "bf16" if prec == "bf16" else "f32"
+    tctx = DeepInverse(phi, synth.make_params(bias="channel").rounded(st), c.n, c.n, prec, device=local, max_batch=bt)
+    yd = torch.from_numpy(y[:bt]).to(device=dev, dtype=tctx.storage_dtype)
+    xd = torch.from_numpy(x[:bt]).to(dev)
+    scale = 1.0 / (bt * world)
+    grads = torch.empty(tctx.num_params(), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(lr):
+        loss, _ = tctx.train_grad(yd, xd, scale, grads)
+        if world > 1:
+            dist.all_reduce(grads)
+            dist.all_reduce(loss)
+        tctx.sgd_step(grads, lr, 0.9)
+        return loss
+
+    loss0 = step(0.0)
+    lr = 0.05 * float(loss0.item()) / max(float((grads.double() ** 2).sum()), 1e-30)
+    for _ in range(warmup):
+        step(lr)
+    torch.cuda.synchronize(dev)
+    barrier(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        loss = step(lr)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = max_over_ranks(e0.elapsed_time(e1) / 1e3, dev)
+    out = {"images_s": aggregate(bt * steps, world, t), "ms_per_step": t / steps * 1e3, "batch_per_gpu": bt,
+           "precision": prec, "steps": steps, "warmup": warmup, "allreduce": "nccl" if world > 1 else "none (N = 1)",
+           "loss_first_last": [float(loss0.item()), float(loss.item())],
+           "what": "di_train_grad (forward keeping activations, MSE loss, backprop through the 3 convs and Phi^T) "
+                   "+ gradient all-reduce + di_sgd_step (momentum 0.9), per-channel biases"}
+    tctx.close()
+    return out
 
 
 def output_check(ctx, c, prec, B, world, parts, dev, no_oracle=False, phi=None, params=None) -> dict:
@@ -647,6 +710,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-configs", action="store_true", help="skip the per-config single-thread oracle times")
     ap.add_argument("--no-oracle-check", action="store_true", help="output check: bitwise part only")
     ap.add_argument("--no-check", action="store_true", help="skip the output check (profiling runs: launch lists)")
+    ap.add_argument("--no-train", action="store_true", help="skip the training-step probe")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)

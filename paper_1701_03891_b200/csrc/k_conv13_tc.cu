@@ -205,6 +205,9 @@ __global__ void __launch_bounds__(384, 1)
 #endif
       uint8_t* dst = im0 + s * IM_BYTES;
       const int nrows = (g.R + 10) * W;
+#ifdef DI_PROF_CONV1
+      long long bt2 = 0;
+#endif
       if (TMAX) {
         if (bt == 0) {
           // the strip of unit `un` into buffer `buf` (unit it+1 is issued one unit ahead).  TMA needs a 16-B
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         mbar_wait(&xfull[s], (it >> 1) & 1);
 #ifdef DI_PROF_CONV1
-        long long bt2 = clock64();
+        bt2 = clock64();
         b_load += bt2 - bt1;
 #endif
         // row p -> copy position m = r*Q + c + 3; its 16-element window = 8 words funnel-shifted by (m & 1) * 16
@@ -244,13 +247,7 @@ __global__ void __launch_bounds__(384, 1)
           *reinterpret_cast<uint4*>(dst + p * 32 + (sw << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
           *reinterpret_cast<uint4*>(dst + p * 32 + ((1 ^ sw) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
         }
-#ifdef DI_PROF_CONV1
-        b_build += clock64() - bt2;
-#endif
       } else {
-#ifdef DI_PROF_CONV1
-        long long bt2 = clock64();
-#endif
         const uint16_t* src = reinterpret_cast<const uint16_t*>(xt) + (size_t)b * g.n1 * g.n2;
         // all loads of this thread first (memory-level parallelism), then the shared-memory stores
         const int strip_real = (g.R + 10) * P;
@@ -274,7 +271,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         named_bar(2, 64);
   #ifdef DI_PROF_CONV1
-        long long bt2 = clock64();
+        bt2 = clock64();
         b_load += bt2 - bt1;
   #endif
         // im2row row p (output position r*W + c) = strip_lin[r*P + c .. +15], SWIZZLE_32B
