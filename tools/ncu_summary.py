@@ -30,6 +30,9 @@ KEYS = [
     "smsp__inst_executed.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
     "lts__t_bytes.sum",
     "launch__registers_per_thread",
     "launch__grid_size",
@@ -86,7 +89,13 @@ def full(rep: str, config: str) -> tuple[str, dict]:
             return x * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}.get(u, 1.0)
         b = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
         traffic[f"{kname.split('<')[0]}@{config}"] = {"bytes_per_launch": b, "source": os.path.basename(rep)}
-        out.append(f"\ndram read+write per launch: {b / 1e9:.3f} GB\n")
+        out.append(f"\ndram read+write per launch: {b / 1e9:.3f} GB")
+        tc = num("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")
+        ls = num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")
+        if tc or ls:
+            out.append(f"shared-memory data pipe (one 128-B wavefront per clock per SM): tensor-core operand reads "
+                       f"{tc:.1f} % + LSU {ls:.1f} % = {tc + ls:.1f} % of the elapsed cycles")
+        out.append("")
     return "\n".join(out), traffic
 
 
