@@ -35,7 +35,7 @@ out = f"""# Round 2 (final) — measured path (capture `{tag}`, {gpu})
 Commands (`tools/scratch/{tag}.sh`, summarised by `tools/profile_summary_r04.py {tag}`): the `-m gpu` suite
 ({tests}); `python bench.py` (20 timed steps, 5 warm-up, output check on); `tools/time_stages.py` per config; launch
 list `ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 --warmup 3
---no-cpu-baseline --no-check`; full capture `ncu --set full --clock-control none --import-source on -k
+--no-cpu-baseline --no-check --no-train`; full capture `ncu --set full --clock-control none --import-source on -k
 regex:"k_conv1_tc|k_conv2_tc|k_conv3_r4|k_proxy" -s 12 -c 4` of the same command (the fourth recovery, full batch);
 `ncu --set full -k regex:k_proxy_pair -s 3 -c 1 python tools/time_stages.py stress 3`.
 
