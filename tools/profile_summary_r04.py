@@ -35,7 +35,7 @@ out = f"""# Round 2 (final) — measured path (capture `{tag}`, {gpu})
 Commands (`tools/scratch/{tag}.sh`, summarised by `tools/profile_summary_r04.py {tag}`): the `-m gpu` suite
 ({tests}); `python bench.py` (20 timed steps, 5 warm-up, output check on); `tools/time_stages.py` per config; launch
 list `ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 --warmup 3
---no-cpu-baseline --no-check --no-train`; full capture `ncu --set full --clock-control none --import-source on -k
+--no-cpu-baseline --no-check --no-train --no-sustained`; full capture `ncu --set full --clock-control none --import-source on -k
 regex:"k_conv1_tc|k_conv2_tc|k_conv3_r4|k_proxy" -s 12 -c 4` of the same command (the fourth recovery, full batch);
 `ncu --set full -k regex:k_proxy_pair -s 3 -c 1 python tools/time_stages.py stress 3`.
 
@@ -46,6 +46,7 @@ regex:"k_conv1_tc|k_conv2_tc|k_conv3_r4|k_proxy" -s 12 -c 4` of the same command
 | step (device, CUDA events) | **{b['ms_per_step']:.2f} ms** |
 | images/s device-resident | **{b['value'] / 1e3:.0f} k** |
 | images/s end to end (pinned host y in, host x̂ out) | **{b['e2e']['value'] / 1e3:.0f} k** |
+| images/s sustained (≈ 2 s back to back after the timed region) | **{b.get('sustained', {}).get('images_s', 0) / 1e3:.0f} k** at {b.get('sustained', {}).get('sm_mhz')} MHz, {b.get('sustained', {}).get('power_w_max')} W max, {', '.join(b.get('sustained', {}).get('reasons') or [])} |
 | stages (ms) | lifting {st['proxy']:.3f}, conv1 {st['conv1']:.3f}, conv2 {st['conv2']:.3f}, conv3 {st['conv3']:.3f} |
 | conv2 | {rf['achieved']:.0f} TFLOP/s = {rf['frac']:.3f} of the measured burst {rf['peak']:.0f}; {rf.get('frac_at_sm_clock', 0):.3f} of {rf.get('peak_at_sm_clock', 0):.0f} TFLOP/s at the sampled SM clock; design ceiling {rf.get('design_ceiling', 0):.3f} |
 | clocks (timed region) | median {cl['sm_mhz']:.0f} MHz (max {cl['sm_max_mhz']:.0f}), reasons: {', '.join(cl['reasons']) or 'none'} |
