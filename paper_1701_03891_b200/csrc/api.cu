@@ -151,6 +151,7 @@ struct di_ctx_s {
   cudaStream_t cstream = nullptr;               // di_recover_host: device->host copy stream
   cudaEvent_t cev[17] = {};                      // di_recover_host: chunk-done events (+ the y-copy event)
   int host_chunk_ratio = 4;                      // di_recover_host: chunk k+1 = chunk k / ratio (DI_EXP_E2E_RATIO)
+  int host_waves = 1;                            // di_recover_host: chunks in whole conv3 waves (DI_EXP_E2E_WAVES=0: off)
   long long ws_bytes = 0;
   CUtensorMap tmPt{}, tmH1{}, tmH2{}, tmX{};
   CUtensorMap tmH1s{};          // BF16, n2 % 64 == 0: conv1's TMA store map over h1 (encode_h1_store)
@@ -998,6 +999,7 @@ di_status di_create(const di_create_args* a, di_ctx* out) {
   c->conv2_balanced = !(getenv("DI_EXP_C2_SPLIT") && atoi(getenv("DI_EXP_C2_SPLIT")) == 253);
   c->conv2_mixed = !(getenv("DI_EXP_C2_MIXED") && atoi(getenv("DI_EXP_C2_MIXED")) == 0);
   c->host_chunk_ratio = getenv("DI_EXP_E2E_RATIO") ? std::max(2, atoi(getenv("DI_EXP_E2E_RATIO"))) : 4;
+  c->host_waves = !(getenv("DI_EXP_E2E_WAVES") && atoi(getenv("DI_EXP_E2E_WAVES")) == 0);
 #ifdef DI_DEBUG
   {
     di_status sd = debug_bind();
@@ -1399,9 +1401,15 @@ di_status di_recover_host(di_ctx c, const void* y_host, long long ldy, int batch
   int nchunk = 0;
   if (batch >= 512) {
     const int r = c->host_chunk_ratio;
+    // wave quantum (BF16 path): chunks of whole conv3 waves -- 2 images per item, one item per SM and 64-column
+    // segment (k_conv3_r4) -- so the small chunks do not pay a partial last wave (lowrate: 2960 + 888 + 248 instead of
+    // 3072 + 768 + 256, 14 instead of 16 conv3 waves per call)
+    const int ncs = (c->n2 + 63) / 64;
+    const int wq = (c->prec == DI_PREC_BF16 && c->host_waves) ? std::max(4, (2 * c->num_sms / ncs) & ~3) : 4;
     int left = batch;
     while (left > 0 && nchunk < 15) {
       int take = (left - left / r) & ~3;
+      if (wq > 4) take = std::max(wq, (take + wq / 2) / wq * wq);
       if (left - take < 128 || nchunk == 14) take = left;
       cuts[nchunk + 1] = cuts[nchunk] + take;
       ++nchunk;
