@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(384, 1)
                const __nv_bfloat16* __restrict__ xt, const uint8_t* __restrict__ w1pack, const float* __restrict__ bias,
                int fullmap, Geo13 g, __nv_bfloat16* __restrict__ h1) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* wbuf = smem;                                           // 22 KB
   uint8_t* const im0 = smem + W1_BYTES;   // 2 im2row buffers (1024-aligned: W1_BYTES = 22528)
   uint32_t* const sw0 = reinterpret_cast<uint32_t*>(smem + W1_BYTES + 2 * IM_BYTES);
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(384, 1)
                  const float* __restrict__ bias, int fullmap, Geo13 g, float* __restrict__ h1,
                  const void* __restrict__ mask, int mask_bf16, float* __restrict__ part_b) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* wbuf = smem;                                 // 44 KB
   uint8_t* const im0 = smem + W1T_BYTES;                // 2 im2row buffers
   uint8_t* const xc0 = smem + W1T_BYTES + 2 * IM_BYTES_T;   // 2 strip buffers
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(256, 1)
   constexpr int NH = TF32 ? 2 : 1;
   constexpr int WB = NH * W3_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const int P = g.P;
   const int strip_bytes = (g.R + 10) * P * 64;
   const int strip_alloc = (strip_bytes + g.guard * 64 + 1023) & ~1023;

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(COUT >= 64 ? 384 : 256, 1)
   constexpr int WST = RB == 128 ? (COUT >= 64 ? 3 : WSTAGES) : C2_WST64;   // C_out >= 64: room for 2 epilogue groups
   constexpr int R = RB == 128 ? C2_ROWS : C2_DG_ROWS;   // output rows per unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const int strip_bytes = g.srows * g.P * RB;
   const int strip_alloc = (strip_bytes + GUARD_ROWS * RB + 1023) & ~1023;
   uint8_t* strip = smem;

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(384, 1)
   constexpr int QPT = COUT / 32;              // TMEM lane quadrants per tap
   constexpr int CPT = COUT / 8;               // channels per epilogue thread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const int strip_bytes = (R + 10) * g.P * RB;
   const int strip_alloc = (strip_bytes + GUARD_ROWS * RB + 1023) & ~1023;
   uint8_t* strip = smem;

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256, 1)
                const float* __restrict__ bias, int fullmap, int relu, GeoR4 g, float* __restrict__ xhat,
                const float* __restrict__ xtrue, double* __restrict__ mpart) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const int rowb = g.N * 64;                                  // one strip row: 2 images x PP positions x 64 B
   const int chunk_bytes = CHR * rowb;                         // a multiple of 1024 (PP a multiple of 16)
   uint8_t* const tb = smem;                                   // T stack (1024-aligned)

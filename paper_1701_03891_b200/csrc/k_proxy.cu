@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(128, 1)
   constexpr int K_PER_MMA = 32 / ELT;                        // 16 (bf16) or 8 (tf32)
   constexpr int MMAS_PER_KB = KB_ELEMS / K_PER_MMA;          // 4
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   __shared__ uint64_t full[NST], empty[NST], tfull;
   __shared__ uint32_t tslot;
 
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(128, 1)
   constexpr uint32_t STAGE = A_BYTES + 2 * BH_BYTES;
   constexpr int NST = PX2_STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   __shared__ uint64_t full[NST], empty[NST], tfull;
   __shared__ uint32_t tslot;
   const int warp = warp_id(), lane = lane_id();

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(128, 1)
                 float* __restrict__ part, float* __restrict__ part_b, int xbf, const __grid_constant__ CUtensorMap tmD1,
                 int use_tma) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   float* xs = reinterpret_cast<float*>(smem + 2 * g.stage);
   __shared__ uint64_t done[2], fin, dbar[2];
   __shared__ uint32_t tslot;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(128, 1)
     k_wgrad3_tc(const void* __restrict__ h2, const float* __restrict__ dg3, GeoT13 g, float* __restrict__ part,
                 float* __restrict__ part_b, int hbf, const __grid_constant__ CUtensorMap tmH2, int use_tma) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   float* ds = reinterpret_cast<float*>(smem + 2 * g.stage) + 16;   // ds[-16 .. NB + 16)
   __shared__ uint64_t done[2], fin, hbar[2];
   __shared__ uint32_t tslot;

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(128, 1)
     k_wgrad2_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmG, GeoW g,
                 float* __restrict__ part) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   __shared__ uint64_t full[2], ready[2], empty[2], done;
   __shared__ uint32_t tslot;
   const int warp = warp_id(), lane = lane_id();

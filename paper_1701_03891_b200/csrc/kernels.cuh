@@ -5,7 +5,7 @@
 // libdeepinverse_exp.so with -DDI_EXPERIMENT_BUILD); the product library cannot be compiled with them.
 #if !defined(DI_EXPERIMENT_BUILD) && (defined(DI_PROF_CONV1) || defined(DI_PROF_CONV2) || defined(DI_PROF_CONV3) || \
                                       defined(DI_C2_ROWS) || defined(DI_C2_WSTAGES) || defined(DI_C3R_PF) || \
-                                      defined(DI_C3R_NSL))
+                                      defined(DI_C3R_NSL) || defined(DI_EXP_GENERIC_SMEM))
 #error "experiment macros need DI_EXPERIMENT_BUILD (build.py routes them to libdeepinverse_exp.so)"
 #endif
 #include <cuda.h>

@@ -34,6 +34,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// The dynamic shared-memory base rounded up to 1024 B (the SWIZZLE_128B atom) by pointer arithmetic on the shared
+// array itself, so the compiler keeps the pointer in the shared state space and emits LDS / STS for accesses through
+// it (a round trip through an integer makes them generic LD / ST).  DI_EXP_GENERIC_SMEM (experiment builds): the
+// integer round trip, for A/B.
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* p) {
+#ifdef DI_EXP_GENERIC_SMEM
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+#else
+  return p + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(p)) & 1023u)) & 1023u);
+#endif
+}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
