@@ -73,6 +73,7 @@ SEAM_SHAPES = [(64, 64),     # the bench geometry: P = 69, 4 blocks of 7 rows (t
                (61, 65),     # a 1-column last segment
                (40, 72),     # ragged second segment, 4-row last block
                (61, 64),     # mixed row-block heights: 7 blocks of 7 rows, 2 of 6
+               (20, 48),     # one segment narrower than 64 columns with n2 % 8 == 0 (conv1's TMA strip, P = 53)
                (9, 13)]      # one small unit: a single partial tile
 
 
