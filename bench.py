@@ -120,6 +120,9 @@ _CLK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.ac
                "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 _REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+# the remaining nvmlClocksEventReason bits (nvml.h), reported as `other_clock_events`
+_OTHER_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x10: "sync_boost",
+                  0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
 
 _NVML_LOOP = r"""
@@ -136,7 +139,13 @@ with open(path, "w", buffering=1) as f:
         sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
         pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
         rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-        f.write("%.6f,%d,%d,%.3f,%s\n" % (time.time(), sm, mx, pw, ",".join("1" if rs & b else "0" for b in bits)))
+        try:     # instantaneous draw: nvmlDeviceGetPowerUsage is an average that lags a 0.14-s timed region
+            pi = nv.nvmlDeviceGetFieldValues(h, [nv.NVML_FI_DEV_POWER_INSTANT])[0]
+            pin = pi.value.uiVal / 1000.0 if pi.nvmlReturn == 0 else -1.0
+        except Exception:
+            pin = -1.0
+        f.write("%.6f,%d,%d,%.3f,%s,%.3f,%d\n" % (time.time(), sm, mx, pw,
+                                                  ",".join("1" if rs & b else "0" for b in bits), pin, rs))
         time.sleep(0.004)
 """
 
@@ -193,13 +202,18 @@ class ClockSampler:
                 f = [x.strip() for x in line.split(",")]
                 try:
                     if self.kind == "nvml" and len(f) >= 8:
-                        r = (float(f[1]), float(f[2]), float(f[3]), [v == "1" for v in f[4:8]])
+                        pin = float(f[8]) if len(f) >= 10 else -1.0
+                        mask = int(f[9]) if len(f) >= 10 else 0
+                        # r[2]: the draw that decides "under load" -- instantaneous when NVML reports it
+                        r = (float(f[1]), float(f[2]), pin if pin >= 0 else float(f[3]), [v == "1" for v in f[4:8]],
+                             float(f[3]), mask)
                         rows.append(r)
                         if self.t0 <= float(f[0]) <= self.t1:
                             inside.append(r)
                     elif self.kind == "nvidia-smi" and len(f) >= 9:
-                        rows.append((float(f[1]), float(f[2]), float(f[3]) if f[3] not in ("", "[N/A]") else 0.0,
-                                     [v.lower().startswith("active") for v in f[5:9]]))
+                        pw = float(f[3]) if f[3] not in ("", "[N/A]") else 0.0
+                        rows.append((float(f[1]), float(f[2]), pw, [v.lower().startswith("active") for v in f[5:9]],
+                                     pw, 0))
                 except ValueError:
                     continue
             os.unlink(self.path)
@@ -208,9 +222,16 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         load = [r for r in rows if r[2] > 300.0] or rows
         reasons = sorted({_REASONS[i] for r in load for i, v in enumerate(r[3]) if v})
+        # every other NVML clocks-event bit seen under load, by name, so that a clock below max never reads as
+        # "no reason" only because the reason is not one of the four above
+        mask = 0
+        for r in load:
+            mask |= r[5]
+        other = sorted(n for b, n in _OTHER_REASONS.items() if mask & b)
         return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load),
-                "power_w_max": max(r[2] for r in rows), "sampler": self.kind,
+                "reasons": reasons, "other_clock_events": other, "samples": len(rows),
+                "samples_under_load": len(load), "power_w_max": max(r[2] for r in rows),
+                "power_avg_w_max": max(r[4] for r in rows), "sampler": self.kind,
                 "window": "timed region only" if inside else "whole sampler run"}
 
 
