@@ -9,6 +9,7 @@
 //   t6  UMMA throughput (SS / TS, N sweep, with and without TMA ingest)
 //   t7  .ws MMA exploration (M=32/64/128): D layout, collector reuse, B shift
 //   t8  collector::a reuse throughput
+//   t16 disable-output-lane masks of tcgen05.mma (per-lane keep / overwrite / accumulate)
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -1160,6 +1161,110 @@ static void t15() {
   cudaFree(d);
 }
 
+// ------------------------------------------------------------------------ t16: disable-output-lane
+// tcgen05.mma's optional disable-output-lane operand (4 x 32-bit masks for cta_group::1, one bit per TMEM lane):
+// which lanes of D does an MMA leave untouched, with and without enable-input-d?  TMEM is pre-filled with -1,
+// A = ones in K column 1, B[n] = n + 1 in K column 1, so an enabled lane reads n + 1 (overwrite) or n (accumulate).
+__device__ __forceinline__ void umma_f16_ss_dol(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                                uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(m0), "r"(m1), "r"(m2), "r"(m3)
+      : "memory");
+}
+__global__ void k_dol(const __nv_bfloat16* A, const __nv_bfloat16* B, int N, uint32_t acc, uint32_t m0, uint32_t m1,
+                      uint32_t m2, uint32_t m3, float* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + 32768;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  int w = threadIdx.x >> 5;
+  st_sw128(sA, A, 128);
+  st_sw128(sB, B, 320);
+  fence_async_smem();
+  if (w == 0) tmem_alloc<512>(&tslot), tmem_relinquish();
+  if (threadIdx.x == 32) mbar_init(&bar, 1), fence_mbar_init();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tb = tslot;
+  if (w < 4) {
+    uint32_t r[16];
+    for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(-1.0f);
+    for (int c = 0; c < 512; c += 16) tmem_st16(tb + ((uint32_t)(w * 32) << 16) + c, r);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    uint32_t idesc = idesc_f32acc(1, 128, N);
+    uint64_t ad = smem_desc(smem_u32(sA), 16, 1024, kSwizzle128B);
+    uint64_t bd = smem_desc(smem_u32(sB), 16, 1024, kSwizzle128B);
+    umma_f16_ss_dol(tb, ad, bd, idesc, acc, m0, m1, m2, m3);
+    umma_commit(&bar);
+    wait_bounded(&bar, 0);
+  }
+  __syncthreads();
+  tc_fence_after();
+  dump_tmem(tb, out, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (w == 0) tmem_dealloc<512>(tb);
+}
+
+static void t16() {
+  std::vector<__nv_bfloat16> A(128 * 64), B(320 * 64);
+  for (auto& v : A) v = __float2bfloat16(0.f);
+  for (auto& v : B) v = __float2bfloat16(0.f);
+  for (int m = 0; m < 128; ++m) A[m * 64 + 1] = __float2bfloat16(1.f);
+  for (int n = 0; n < 320; ++n) B[n * 64 + 1] = __float2bfloat16((float)(n + 1));
+  __nv_bfloat16 *dA = dup(A), *dB = dup(B);
+  float* dD;
+  CK(cudaMalloc(&dD, 128 * 512 * 4));
+  CK(cudaFuncSetAttribute(k_dol, cudaFuncAttributeMaxDynamicSharedMemorySize, 98304));
+  std::vector<float> D(128 * 512);
+  struct S { uint32_t acc, m[4]; const char* name; };
+  std::vector<S> ss = {
+      {0, {0, 0, 0, 0}, "overwrite_mask0"},
+      {0, {0x0000F800u, 0, 0, 0}, "overwrite_disable_lanes11to15"},
+      {1, {0x0000F800u, 0, 0, 0}, "accumulate_disable_lanes11to15"},
+      {0, {0xFFFF07FFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}, "overwrite_only_lanes11to15"},
+      {1, {0, 0x00000001u, 0, 0x80000000u}, "accumulate_disable_lane32_and_127"},
+  };
+  const int N = 64;
+  for (auto s : ss) {
+    k_dol<<<1, 128, 98304>>>(dA, dB, N, s.acc, s.m[0], s.m[1], s.m[2], s.m[3], dD);
+    if (check_err("t16")) return;
+    CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+    // classify every lane by its columns 0..N-1: 'k' kept (-1), 'w' written (n + 1), 'a' accumulated (n), '?' other
+    std::string cls(128, '?');
+    int exact = 1;
+    for (int l = 0; l < 128; ++l) {
+      int k = 1, w = 1, a = 1;
+      for (int c = 0; c < N; ++c) {
+        const float v = D[l * 512 + c];
+        k &= v == -1.f, w &= v == (float)(c + 1), a &= v == (float)c;
+      }
+      cls[l] = k ? 'k' : (w ? 'w' : (a ? 'a' : '?'));
+      const bool dis = (s.m[l >> 5] >> (l & 31)) & 1u;
+      const char want = dis ? 'k' : (s.acc ? 'a' : 'w');
+      exact &= cls[l] == want;
+    }
+    int beyond = 1;   // columns >= N untouched
+    for (int l = 0; l < 128; ++l)
+      for (int c = N; c < 512; ++c) beyond &= D[l * 512 + c] == -1.f;
+    printf("{\"test\":\"t16_%s\",\"acc\":%u,\"masks\":[%u,%u,%u,%u],\"lanes\":\"%s\",\"as_expected\":%d,"
+           "\"cols_beyond_N_untouched\":%d}\n", s.name, s.acc, s.m[0], s.m[1], s.m[2], s.m[3], cls.c_str(), exact, beyond);
+  }
+  cudaFree(dA), cudaFree(dB), cudaFree(dD);
+}
+
+
 int main(int argc, char** argv) {
   int dev = 0, nsm = 0;
   CK(cudaSetDevice(dev));
@@ -1181,5 +1286,6 @@ int main(int argc, char** argv) {
   if (on("t13")) t13(nsm);
   if (on("t14")) t14(nsm);
   if (on("t15")) t15();
+  if (on("t16")) t16();
   return 0;
 }
