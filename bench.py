@@ -220,7 +220,11 @@ class ClockSampler:
         rows = inside or rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        load = [r for r in rows if r[2] > 300.0] or rows
+        # rows inside the timed region are under load by construction (the steps are queued back to back between two
+        # synchronisations); NVML's power readings -- averaged AND "instantaneous" -- lag a 0.14-s region by up to
+        # ~0.1 s, so filtering on them kept only the late, already power-capped samples.  Without timestamps (the
+        # nvidia-smi fallback, or no row inside) fall back to the draw.
+        load = rows if inside else ([r for r in rows if r[2] > 300.0] or rows)
         reasons = sorted({_REASONS[i] for r in load for i, v in enumerate(r[3]) if v})
         # every other NVML clocks-event bit seen under load, by name, so that a clock below max never reads as
         # "no reason" only because the reason is not one of the four above

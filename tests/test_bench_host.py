@@ -40,33 +40,33 @@ def test_clock_sampler_keeps_only_rows_inside_the_timed_region(tmp_path):
     rows = [(50.0, 1000, 1965, 500.0, "0,0,0,1"),      # before the region: ignored
             (120.0, 1800, 1965, 400.0, "0,0,0,1"),
             (150.0, 1900, 1965, 420.0, "0,0,0,0"),
-            (180.0, 1700, 1965, 250.0, "0,0,0,0"),      # inside but idle (power <= 300 W): not under load
+            (180.0, 1700, 1965, 250.0, "0,0,0,0"),      # inside: under load whatever the (lagging) power reading
             (250.0, 900, 1965, 450.0, "1,0,0,0")]       # after the region: ignored
     with open(s.path, "w") as f:
         for t, sm, mx, pw, rs in rows:
             f.write(f"{t},{sm},{mx},{pw},{rs}\n")
     d = s.summary()
-    assert d["samples"] == 3 and d["samples_under_load"] == 2
-    assert d["sm_mhz"] == 1850.0 and d["sm_max_mhz"] == 1965.0
+    assert d["samples"] == 3 and d["samples_under_load"] == 3
+    assert d["sm_mhz"] == 1800.0 and d["sm_max_mhz"] == 1965.0
     assert d["reasons"] == ["sw_power_cap"] and d["window"] == "timed region only"
 
 
 def test_clock_sampler_uses_instant_power_and_names_other_events(tmp_path):
-    """Rows of the current NVML child carry the instantaneous draw and the raw clocks-event mask: "under load" is
-    decided by the instantaneous draw (the averaged one lags a short timed region), and event bits other than the four
-    throttle reasons are reported by name, so a clock below max is never reported without its reason."""
+    """Rows of the current NVML child carry the instantaneous draw and the raw clocks-event mask: every row inside the
+    timed region counts as under load (both power readings lag a short region), both draws are reported, and event
+    bits other than the four throttle reasons are named, so a clock below max is never reported without its reason."""
     s = bench.ClockSampler(0)
     s.kind, s.t0, s.t1 = "nvml", 100.0, 200.0
     s.path = str(tmp_path / "clk.csv")
     rows = [(110.0, 1950, 1965, 250.0, "0,0,0,0", 980.0, 0x0),      # averaged power still low, instant draw high
             (120.0, 1900, 1965, 260.0, "0,0,0,1", 1010.0, 0x4),
             (130.0, 1500, 1965, 270.0, "0,0,0,0", 990.0, 0x80),     # hw power brake: not one of the four columns
-            (140.0, 1965, 1965, 280.0, "0,0,0,0", 120.0, 0x1)]      # instant draw low: idle sample, not under load
+            (140.0, 1965, 1965, 280.0, "0,0,0,0", 120.0, 0x0)]      # a lagging low reading: still inside, still counted
     with open(s.path, "w") as f:
         for t, sm, mx, pw, rs, pin, mask in rows:
             f.write(f"{t},{sm},{mx},{pw},{rs},{pin},{mask}\n")
     d = s.summary()
-    assert d["samples"] == 4 and d["samples_under_load"] == 3
-    assert d["sm_mhz"] == 1900.0
+    assert d["samples"] == 4 and d["samples_under_load"] == 4
+    assert d["sm_mhz"] == 1925.0
     assert d["reasons"] == ["sw_power_cap"] and d["other_clock_events"] == ["hw_power_brake_slowdown"]
     assert d["power_w_max"] == 1010.0 and d["power_avg_w_max"] == 280.0
