@@ -476,7 +476,8 @@ def run_ours(args):
     kname = ctx.info()["stage_kernels"][2]
     roof = {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": (achieved / peak) if peak else None,
-            "frac_of_sustained": (achieved / pk["bf16_tflops_sustained"]) if (peak and prec == "bf16") else None,
+            "frac_of_sustained": (achieved / pk["bf16_tflops_sustained"])
+            if (peak and prec == "bf16" and pk.get("bf16_tflops_sustained")) else None,
             "peak_note": peak_note, "traffic": traffic_for(kname, c.name),
             "algorithmic": f"2*32*64*121 = {CONV2_FLOP_PER_PX} FLOP/pixel x {B * c.N} pixels per launch",
             "launch_ms": conv2_ms}
